@@ -1,0 +1,343 @@
+"""ctypes binding of libnetrec_b200.so (include/netrec_b200.h).
+
+There is no CPU fallback: importing the binding fails loudly when the CUDA library
+is missing, and every call runs on the GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libnetrec_b200.so"
+
+NRG_ISING, NRG_GAUSSIAN = 0, 1
+NRG_EXACT, NRG_GRADIENT, NRG_TABLE, NRG_LINE = 0, 1, 2, 3
+
+PAIR_DT = np.dtype([("i", "<i4"), ("j", "<i4"), ("dist", "<f8")])
+TRACE_DT = np.dtype([("level", "<i4"), ("k", "<i4"), ("exhaustive", "<i4"), ("knn_sweeps", "<i4"),
+                     ("nodes", "<u8"), ("dedup_size", "<u8")])
+ITER_DT = np.dtype([("iter", "<i4"), ("pad", "<i4"), ("delta", "<f8"), ("seconds", "<f8"),
+                    ("candidates", "<u8"), ("objective", "<f8")])
+
+
+class KnnParams(C.Structure):
+    """nrg_knn_params == KnnParams (inc/knn.hpp:92-104)."""
+    _fields_ = [("eps", C.c_double), ("seed", C.c_uint64), ("max_sweeps", C.c_int32),
+                ("scan_floor", C.c_int32), ("width_floor", C.c_int32), ("threads", C.c_int32),
+                ("reverse", C.c_int32), ("pad", C.c_int32)]
+
+
+class FbParams(C.Structure):
+    """nrg_fb_params == FindBestParams (inc/find_best.hpp:45-49)."""
+    _fields_ = [("knn_eps", C.c_double), ("seed", C.c_uint64), ("threads", C.c_int32),
+                ("reverse", C.c_int32)]
+
+
+class GcdCfg(C.Structure):
+    """nrg_gcd_cfg == ReconstructionConfig (inc/reconstruct.hpp:45-55)."""
+    _fields_ = [("kappa", C.c_double), ("eps", C.c_double), ("max_iters", C.c_int32),
+                ("mode", C.c_int32), ("knn_eps", C.c_double), ("seed", C.c_uint64),
+                ("threads", C.c_int32), ("reverse", C.c_int32)]
+
+
+_P = C.c_void_p
+_I32P = np.ctypeslib.ndpointer(np.int32, flags="C")
+_F64P = np.ctypeslib.ndpointer(np.float64, flags="C")
+_U8P = np.ctypeslib.ndpointer(np.uint8, flags="C")
+_I8P = np.ctypeslib.ndpointer(np.int8, flags="C")
+_PAIRP = np.ctypeslib.ndpointer(PAIR_DT, flags="C")
+_TRP = np.ctypeslib.ndpointer(TRACE_DT, flags="C")
+_ITP = np.ctypeslib.ndpointer(ITER_DT, flags="C")
+_u64, _i32, _d = C.c_uint64, C.c_int32, C.c_double
+_VP = C.c_void_p
+
+SIGNATURES = {
+    "nrg_last_error": (C.c_char_p, []),
+    "nrg_version": (C.c_int, []),
+    "nrg_create": (C.c_int, [C.POINTER(_P), _i32, _i32, _i32, _d, _i32]),
+    "nrg_destroy": (C.c_int, [_P]),
+    "nrg_upload_samples": (C.c_int, [_P, _F64P]),
+    "nrg_upload_spins_i8": (C.c_int, [_P, _I8P]),
+    "nrg_reset_state": (C.c_int, [_P]),
+    "nrg_set_theta": (C.c_int, [_P, _F64P]),
+    "nrg_set_edges": (C.c_int, [_P, _u64, _I32P, _I32P, _F64P]),
+    "nrg_get_state": (C.c_int, [_P, _F64P, _u64, _I32P, _I32P, _F64P, C.POINTER(_u64)]),
+    "nrg_get_sums": (C.c_int, [_P, _F64P]),
+    "nrg_begin_generation": (C.c_int, [_P]),
+    "nrg_log_posterior": (C.c_int, [_P, C.POINTER(_d)]),
+    "nrg_distance": (C.c_int, [_P, _i32, _u64, _I32P, _I32P, _F64P]),
+    "nrg_optimize_edge": (C.c_int, [_P, _u64, _I32P, _I32P, _VP, _VP, _VP]),
+    "nrg_edge_gradient": (C.c_int, [_P, _u64, _I32P, _I32P, _F64P]),
+    "nrg_optimize_theta": (C.c_int, [_P, _F64P]),
+    "nrg_set_table": (C.c_int, [_P, _u64, _F64P]),
+    "nrg_set_line": (C.c_int, [_P, _u64, _F64P]),
+    "nrg_find_knn": (C.c_int, [_P, _i32, _i32, _I32P, _u64, C.POINTER(KnnParams), _i32, _I32P, _F64P,
+                               C.POINTER(_i32), C.POINTER(_i32), _F64P, _i32, C.POINTER(_i32)]),
+    "nrg_find_best": (C.c_int, [_P, _i32, _u64, _I32P, _u64, C.POINTER(FbParams), _i32, _PAIRP, _u64,
+                                C.POINTER(_u64), _TRP, _i32, C.POINTER(_i32), C.POINTER(_i32)]),
+    "nrg_apply_updates": (C.c_int, [_P, _PAIRP, _u64, C.POINTER(_d)]),
+    "nrg_theta_pass": (C.c_int, [_P]),
+    "nrg_gcd_iteration": (C.c_int, [_P, C.POINTER(GcdCfg), _i32, _ITP, _VP, _u64, C.POINTER(_u64)]),
+    "nrg_reconstruct_gcd": (C.c_int, [_P, C.POINTER(GcdCfg), _ITP, _i32, C.POINTER(_i32), C.POINTER(_i32)]),
+    "nrg_counters": (C.c_int, [_P, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)]),
+    "nrg_reset_counters": (C.c_int, [_P]),
+    "nrg_recall_curve": (C.c_int, [_u64, _PAIRP, _PAIRP, _F64P]),
+    "nrg_phase_times": (C.c_int, [_P, _F64P, _i32]),
+    "nrg_timer": (C.c_int, [_P, _i32, C.POINTER(_d)]),
+    "nrg_kernel_stats": (C.c_int, [_P, _F64P, _i32]),
+    "nrg_sample_scored_pairs": (C.c_int, [_P, _u64, _u64, _I32P, _I32P, C.POINTER(_u64)]),
+    "nrg_generate_ising": (C.c_int, [_P, _d, _d, _d, _i32, _i32, _u64, _VP]),
+    "nrg_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "nrg_comm_init": (C.c_int, [_P, C.c_char_p, _i32, _i32]),
+}
+
+_lib: C.CDLL | None = None
+
+
+def load() -> C.CDLL:
+    """Load the CUDA library (raises if it was not built — no fallback)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2401_01404_b200.build`")
+        L = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+ERRORS = {22: ValueError, 34: IndexError, 75: OverflowError}
+
+
+def check(rc: int) -> None:
+    if rc:
+        msg = load().nrg_last_error().decode()
+        raise ERRORS.get(rc, RuntimeError)(msg)
+
+
+def _i32a(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _f64a(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Model:
+    """One device-resident GCD problem: PseudoLikelihood + SparseWeights + SampleMatrix +
+    DistanceCache (inc/model.hpp:107-124) on one B200."""
+
+    def __init__(self, n: int, M: int, kind: int = NRG_ISING, lam: float = 0.0, device: int = 0):
+        self.L = load()
+        h = C.c_void_p()
+        check(self.L.nrg_create(C.byref(h), n, M, kind, float(lam), device))
+        self.h = h
+        self.n, self.M, self.kind, self.lam = n, M, kind, lam
+
+    @classmethod
+    def from_samples(cls, X, kind=NRG_ISING, lam=0.0, theta=None, device=0):
+        X = np.asarray(X)
+        m = cls(X.shape[0], X.shape[1], kind, lam, device)
+        if X.dtype == np.int8:
+            m.upload_spins_i8(X)
+        else:
+            m.upload_samples(X)
+        if theta is not None:
+            m.set_theta(theta)
+        return m
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.nrg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- samples / state
+    def upload_samples(self, X):
+        check(self.L.nrg_upload_samples(self.h, _f64a(X)))
+
+    def upload_spins_i8(self, X):
+        check(self.L.nrg_upload_spins_i8(self.h, np.ascontiguousarray(X, dtype=np.int8)))
+
+    def generate_ising(self, mean_deg=4.0, w_sigma=0.3, th_sigma=0.1, burn_in=1000, thin=10, seed=0,
+                       want_samples=False):
+        out = np.zeros((self.n, self.M), np.int8) if want_samples else None
+        check(self.L.nrg_generate_ising(self.h, mean_deg, w_sigma, th_sigma, burn_in, thin, seed,
+                                        out.ctypes.data if out is not None else None))
+        return out
+
+    def reset_state(self):
+        check(self.L.nrg_reset_state(self.h))
+
+    def set_theta(self, th):
+        check(self.L.nrg_set_theta(self.h, _f64a(th)))
+
+    def set_edges(self, ei, ej, w):
+        ei, ej, w = _i32a(ei), _i32a(ej), _f64a(w)
+        check(self.L.nrg_set_edges(self.h, len(ei), ei, ej, w))
+
+    def get_state(self):
+        th = np.zeros(self.n)
+        ne = _u64(0)
+        check(self.L.nrg_get_state(self.h, th, 0, np.zeros(1, np.int32), np.zeros(1, np.int32), np.zeros(1),
+                                   C.byref(ne)))
+        k = ne.value
+        ei = np.zeros(max(k, 1), np.int32)
+        ej = np.zeros(max(k, 1), np.int32)
+        w = np.zeros(max(k, 1))
+        check(self.L.nrg_get_state(self.h, th, k, ei, ej, w, C.byref(ne)))
+        return th, ei[:k], ej[:k], w[:k]
+
+    def get_sums(self):
+        out = np.zeros((self.n, self.M))
+        check(self.L.nrg_get_sums(self.h, out))
+        return out
+
+    def begin_generation(self):
+        check(self.L.nrg_begin_generation(self.h))
+
+    def log_posterior(self) -> float:
+        v = _d()
+        check(self.L.nrg_log_posterior(self.h, C.byref(v)))
+        return v.value
+
+    def set_table(self, table):
+        t = _f64a(table)
+        check(self.L.nrg_set_table(self.h, t.shape[0], t))
+
+    def set_line(self, pos):
+        p = _f64a(pos)
+        check(self.L.nrg_set_line(self.h, len(p), p))
+
+    # ---- pair scores
+    def distance(self, mode, i, j):
+        i, j = _i32a(i), _i32a(j)
+        out = np.zeros(len(i))
+        check(self.L.nrg_distance(self.h, mode, len(i), i, j, out))
+        return out
+
+    def optimize_edge(self, i, j):
+        i, j = _i32a(i), _i32a(j)
+        w, g, warn = np.zeros(len(i)), np.zeros(len(i)), np.zeros(len(i), np.uint8)
+        check(self.L.nrg_optimize_edge(self.h, len(i), i, j, w.ctypes.data, g.ctypes.data, warn.ctypes.data))
+        return w, g, warn
+
+    def edge_gradient(self, i, j):
+        i, j = _i32a(i), _i32a(j)
+        g = np.zeros(len(i))
+        check(self.L.nrg_edge_gradient(self.h, len(i), i, j, g))
+        return g
+
+    def optimize_theta(self):
+        out = np.zeros(self.n)
+        check(self.L.nrg_optimize_theta(self.h, out))
+        return out
+
+    # ---- search
+    def find_knn(self, mode, k, nodes, eps=1e-3, seed=0, max_sweeps=100, scan_floor=8, width_floor=4,
+                 threads=1, exhaustive=False, reverse=False):
+        nodes = _i32a(nodes)
+        n = len(nodes)
+        p = KnnParams(eps, seed, max_sweeps, scan_floor, width_floor, threads, int(reverse), 0)
+        ids = np.zeros(n * max(k, 1), np.int32)
+        dists = np.zeros(n * max(k, 1))
+        kk, sw, nc = _i32(), _i32(), _i32()
+        churn = np.zeros(max_sweeps + 1)
+        check(self.L.nrg_find_knn(self.h, mode, k, nodes, n, C.byref(p), int(exhaustive), ids, dists,
+                                  C.byref(kk), C.byref(sw), churn, len(churn), C.byref(nc)))
+        k2 = kk.value
+        return ids[: n * k2].reshape(n, k2), dists[: n * k2].reshape(n, k2), sw.value, churn[: nc.value].copy()
+
+    def find_best(self, mode, m, nodes, knn_eps=1e-3, seed=0, threads=1, exhaustive=False, reverse=False):
+        nodes = _i32a(nodes)
+        n = len(nodes)
+        cap = int(min(m, n * (n - 1) // 2)) + 1
+        out = np.zeros(cap, PAIR_DT)
+        tr = np.zeros(64, TRACE_DT)
+        p = FbParams(knn_eps, seed, threads, int(reverse))
+        nout, nl, sc = _u64(), _i32(), _i32()
+        check(self.L.nrg_find_best(self.h, mode, m, nodes, n, C.byref(p), int(exhaustive), out, cap,
+                                   C.byref(nout), tr, 64, C.byref(nl), C.byref(sc)))
+        return out[: nout.value].copy(), tr[: nl.value].copy(), bool(sc.value)
+
+    # ---- updates / driver
+    def apply_updates(self, pairs) -> float:
+        p = np.ascontiguousarray(pairs, dtype=PAIR_DT)
+        d = _d()
+        check(self.L.nrg_apply_updates(self.h, p, len(p), C.byref(d)))
+        return d.value
+
+    def theta_pass(self):
+        check(self.L.nrg_theta_pass(self.h))
+
+    def gcd_iteration(self, it, kappa=1.0, eps=-1.0, mode=NRG_EXACT, knn_eps=1e-3, seed=0, reverse=False,
+                      want_candidates=False):
+        cfg = GcdCfg(kappa, eps, 1, mode, knn_eps, seed, 1, int(reverse))
+        rec = np.zeros(1, ITER_DT)
+        cap = int(max(1, round(kappa * self.n))) + 1 if want_candidates else 0
+        cand = np.zeros(max(cap, 1), PAIR_DT)
+        nc = _u64()
+        check(self.L.nrg_gcd_iteration(self.h, C.byref(cfg), it, rec, cand.ctypes.data if cap else None, cap,
+                                       C.byref(nc)))
+        return rec[0], (cand[: nc.value].copy() if cap else None)
+
+    def reconstruct_gcd(self, kappa=1.0, eps=-1.0, max_iters=1000, mode=NRG_EXACT, knn_eps=1e-3, seed=0,
+                        reverse=False):
+        cfg = GcdCfg(kappa, eps, max_iters, mode, knn_eps, seed, 1, int(reverse))
+        recs = np.zeros(max(max_iters, 1), ITER_DT)
+        ni, cv = _i32(), _i32()
+        check(self.L.nrg_reconstruct_gcd(self.h, C.byref(cfg), recs, len(recs), C.byref(ni), C.byref(cv)))
+        return recs[: ni.value].copy(), bool(cv.value)
+
+    def counters(self):
+        v = [_u64() for _ in range(4)]
+        check(self.L.nrg_counters(self.h, *[C.byref(x) for x in v]))
+        return dict(misses=v[0].value, hits=v[1].value, evals=v[2].value, warnings=v[3].value)
+
+    def reset_counters(self):
+        check(self.L.nrg_reset_counters(self.h))
+
+    def timer_start(self):
+        check(self.L.nrg_timer(self.h, 0, None))
+
+    def timer_stop(self) -> float:
+        v = _d()
+        check(self.L.nrg_timer(self.h, 1, C.byref(v)))
+        return v.value
+
+    def kernel_stats(self):
+        out = np.zeros(7)
+        check(self.L.nrg_kernel_stats(self.h, out, 7))
+        keys = ["k1_ms", "k1_launches", "k1_pairs", "k2_ms", "k2_launches", "k2_pairs", "launches"]
+        return dict(zip(keys, out.tolist()))
+
+    def sample_scored_pairs(self, cap, seed=0):
+        i = np.zeros(max(cap, 1), np.int32)
+        j = np.zeros(max(cap, 1), np.int32)
+        n = _u64()
+        check(self.L.nrg_sample_scored_pairs(self.h, cap, seed, i, j, C.byref(n)))
+        return i[: n.value].copy(), j[: n.value].copy()
+
+    def phase_times(self):
+        out = np.zeros(7)
+        check(self.L.nrg_phase_times(self.h, out, 7))
+        names = ["score", "knn", "select", "update", "theta", "logpost", "snapshot"]
+        return dict(zip(names, out.tolist()))
+
+
+def recall_curve(exact, approx):
+    e = np.ascontiguousarray(exact, dtype=PAIR_DT)
+    a = np.ascontiguousarray(approx, dtype=PAIR_DT)
+    out = np.zeros(len(e))
+    check(load().nrg_recall_curve(len(e), e, a, out))
+    return out

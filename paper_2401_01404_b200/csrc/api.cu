@@ -1,0 +1,455 @@
+// api.cu — the extern "C" boundary (include/netrec_b200.h) and the GCD loop body.
+//
+// Errors: nrg::Error codes map to the reference's exception types
+// (22 invalid_argument, 34 out_of_range, 75 overflow_error, 5/100 runtime_error).
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/netrec_b200.h"
+#include "context.cuh"
+
+struct nrg_ctx {
+    nrg::Context c;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    ~nrg_ctx() {
+        if (t0) cudaEventDestroy(t0);
+        if (t1) cudaEventDestroy(t1);
+    }
+    // result buffers
+    nrg::DevBuf out_i, out_j, out_d, q_i, q_j, q_d, q_e, q_f, q_u8, knn_ids, knn_d;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const nrg::Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        g_err = "out of host memory";
+        return NRG_EIO;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return NRG_EIO;
+    }
+}
+
+void check_pairs(const nrg_ctx* x, uint64_t n, const int32_t* i, const int32_t* j) {
+    for (uint64_t t = 0; t < n; ++t) {
+        if (i[t] == j[t]) nrg::fail(22, "pair operations need i != j");
+        if (i[t] < 0 || j[t] < 0 || i[t] >= x->c.n || j[t] >= x->c.n) nrg::fail(34, "node id out of range");
+    }
+}
+
+template <class T>
+T* to_dev(nrg_ctx* x, nrg::DevBuf& b, const T* h, uint64_t n) {
+    T* d = b.as<T>(std::max<uint64_t>(n, 1));
+    if (n) NRG_CUDA(cudaMemcpyAsync(d, h, n * sizeof(T), cudaMemcpyHostToDevice, x->c.stream));
+    return d;
+}
+template <class T>
+void to_host(nrg_ctx* x, T* h, const T* d, uint64_t n) {
+    if (h && n) NRG_CUDA(cudaMemcpyAsync(h, d, n * sizeof(T), cudaMemcpyDeviceToHost, x->c.stream));
+}
+void need_samples(nrg_ctx* x) {
+    if (!x->c.have_samples) nrg::fail(22, "no samples uploaded");
+}
+
+void gcd_iteration(nrg_ctx* x, const nrg_gcd_cfg* cfg, int iter, nrg_iter_record* rec, nrg_pair* cands, uint64_t cap,
+                   uint64_t* n_cands) {
+    nrg::Context& c = x->c;
+    need_samples(x);
+    if (!(cfg->kappa > 0.0)) nrg::fail(22, "reconstruct_gcd: kappa must be > 0");
+    const int n = c.n;
+    const double mm = std::nearbyint(cfg->kappa * (double)n);  // round-half-even, inc/reconstruct.hpp:154-155
+    const uint64_t m = (uint64_t)std::max(1.0, mm);
+    const auto t0 = std::chrono::steady_clock::now();
+    nrg::begin_generation(c);
+    std::vector<int32_t> all(n);
+    for (int t = 0; t < n; ++t) all[t] = t;
+    int32_t* dall = to_dev(x, x->q_i, all.data(), (uint64_t)n);
+    nrg::BestPairsD best;
+    nrg::find_best(c, cfg->mode, m, dall, (uint64_t)n, cfg->knn_eps, nrg::mix64(cfg->seed, (uint64_t)iter),
+                   cfg->reverse != 0, false, best, x->out_i, x->out_j, x->out_d);
+    if (cands && cap) {
+        const uint64_t k = std::min(cap, best.count);
+        std::vector<int32_t> hi(k), hj(k);
+        std::vector<double> hd(k);
+        to_host(x, hi.data(), static_cast<int32_t*>(x->out_i.p), k);
+        to_host(x, hj.data(), static_cast<int32_t*>(x->out_j.p), k);
+        to_host(x, hd.data(), static_cast<double*>(x->out_d.p), k);
+        c.sync();
+        for (uint64_t t = 0; t < k; ++t) cands[t] = {hi[t], hj[t], hd[t]};
+    }
+    if (n_cands) *n_cands = best.count;
+    const double delta = nrg::apply_updates(c, static_cast<int32_t*>(x->out_i.p), static_cast<int32_t*>(x->out_j.p),
+                                            best.count, nullptr);
+    nrg::theta_pass(c, nullptr);
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    const double obj = nrg::log_posterior(c);
+    if (rec) *rec = {iter, 0, delta, secs, best.count, obj};
+}
+}  // namespace
+
+extern "C" {
+
+const char* nrg_last_error(void) { return g_err.c_str(); }
+int nrg_version(void) { return 1; }
+
+int nrg_create(nrg_ctx** out, int32_t n, int32_t m, int32_t kind, double lambda, int32_t device) {
+    return guard([&] {
+        auto* x = new nrg_ctx();
+        try {
+            nrg::ctx_init(x->c, n, m, kind, lambda, device);
+        } catch (...) {
+            delete x;
+            throw;
+        }
+        *out = x;
+    });
+}
+
+int nrg_destroy(nrg_ctx* x) {
+    return guard([&] { delete x; });
+}
+
+int nrg_upload_samples(nrg_ctx* x, const double* X) {
+    return guard([&] { nrg::upload_samples_f64(x->c, X); });
+}
+int nrg_upload_spins_i8(nrg_ctx* x, const int8_t* X) {
+    return guard([&] { nrg::upload_spins_i8(x->c, X); });
+}
+
+int nrg_reset_state(nrg_ctx* x) {
+    return guard([&] { nrg::reset_state_empty(x->c); });
+}
+
+int nrg_set_theta(nrg_ctx* x, const double* theta) {
+    return guard([&] {
+        need_samples(x);
+        if (theta) nrg::set_theta(x->c, theta);
+    });
+}
+
+int nrg_set_edges(nrg_ctx* x, uint64_t n, const int32_t* ei, const int32_t* ej, const double* w) {
+    return guard([&] {
+        need_samples(x);
+        for (uint64_t t = 0; t < n; ++t) {
+            if (ei[t] < 0 || ej[t] < 0 || ei[t] >= x->c.n || ej[t] >= x->c.n) nrg::fail(34, "node id out of range");
+            if (ei[t] == ej[t]) nrg::fail(22, "set_edge: diagonal entries live in theta");
+        }
+        int32_t* di = to_dev(x, x->q_i, ei, n);
+        int32_t* dj = to_dev(x, x->q_j, ej, n);
+        double* dw = to_dev(x, x->q_d, w, n);
+        nrg::apply_updates(x->c, di, dj, n, dw);
+    });
+}
+
+int nrg_get_state(nrg_ctx* x, double* theta, uint64_t cap, int32_t* ei, int32_t* ej, double* w, uint64_t* n_edges) {
+    return guard([&] { nrg::get_state(x->c, theta, cap, ei, ej, w, n_edges); });
+}
+
+int nrg_get_sums(nrg_ctx* x, double* out) {
+    return guard([&] { nrg::get_sums(x->c, out); });
+}
+
+int nrg_begin_generation(nrg_ctx* x) {
+    return guard([&] { nrg::begin_generation(x->c); });
+}
+
+int nrg_log_posterior(nrg_ctx* x, double* out) {
+    return guard([&] { *out = nrg::log_posterior(x->c); });
+}
+
+int nrg_distance(nrg_ctx* x, int32_t mode, uint64_t n, const int32_t* i, const int32_t* j, double* dist) {
+    return guard([&] {
+        if (mode != NRG_TABLE && mode != NRG_LINE) need_samples(x);
+        check_pairs(x, n, i, j);
+        int32_t* di = to_dev(x, x->q_i, i, n);
+        int32_t* dj = to_dev(x, x->q_j, j, n);
+        double* dd = x->q_d.as<double>(std::max<uint64_t>(n, 1));
+        nrg::distance_batch(x->c, mode, di, dj, n, dd);
+        to_host(x, dist, dd, n);
+        x->c.sync();
+    });
+}
+
+int nrg_optimize_edge(nrg_ctx* x, uint64_t n, const int32_t* i, const int32_t* j, double* w, double* gain,
+                      uint8_t* warn) {
+    return guard([&] {
+        need_samples(x);
+        check_pairs(x, n, i, j);
+        int32_t* di = to_dev(x, x->q_i, i, n);
+        int32_t* dj = to_dev(x, x->q_j, j, n);
+        double* dw = x->q_d.as<double>(std::max<uint64_t>(n, 1));
+        double* dg = x->q_e.as<double>(std::max<uint64_t>(n, 1));
+        uint8_t* du = x->q_u8.as<uint8_t>(std::max<uint64_t>(n, 1));
+        nrg::optimize_edge_live(x->c, di, dj, n, dw, dg, du);
+        to_host(x, w, dw, n);
+        to_host(x, gain, dg, n);
+        to_host(x, warn, du, n);
+        x->c.sync();
+    });
+}
+
+int nrg_edge_gradient(nrg_ctx* x, uint64_t n, const int32_t* i, const int32_t* j, double* g) {
+    return guard([&] {
+        need_samples(x);
+        check_pairs(x, n, i, j);
+        int32_t* di = to_dev(x, x->q_i, i, n);
+        int32_t* dj = to_dev(x, x->q_j, j, n);
+        double* dg = x->q_d.as<double>(std::max<uint64_t>(n, 1));
+        nrg::edge_gradient_live(x->c, di, dj, n, dg);
+        to_host(x, g, dg, n);
+        x->c.sync();
+    });
+}
+
+int nrg_optimize_theta(nrg_ctx* x, double* out) {
+    return guard([&] {
+        need_samples(x);
+        double* d = x->q_d.as<double>(x->c.n);
+        nrg::theta_pass(x->c, d);
+        to_host(x, out, d, (uint64_t)x->c.n);
+        x->c.sync();
+    });
+}
+
+int nrg_set_table(nrg_ctx* x, uint64_t n, const double* table) {
+    return guard([&] { nrg::set_table(x->c, n, table); });
+}
+int nrg_set_line(nrg_ctx* x, uint64_t n, const double* pos) {
+    return guard([&] { nrg::set_line(x->c, n, pos); });
+}
+
+int nrg_find_knn(nrg_ctx* x, int32_t mode, int32_t k, const int32_t* nodes, uint64_t n, const nrg_knn_params* p,
+                 int32_t exhaustive, int32_t* ids, double* dists, int32_t* k_out, int32_t* sweeps, double* churn,
+                 int32_t churn_cap, int32_t* n_churn) {
+    return guard([&] {
+        if (mode != NRG_TABLE && mode != NRG_LINE) need_samples(x);
+        nrg::KnnParamsD kp;
+        if (p) {
+            kp.eps = p->eps;
+            kp.seed = p->seed;
+            kp.max_sweeps = p->max_sweeps;
+            kp.scan_floor = p->scan_floor;
+            kp.width_floor = p->width_floor;
+            kp.reverse = p->reverse != 0;
+        }
+        int32_t* dn = to_dev(x, x->q_j, nodes, n);
+        nrg::KnnResultD r;
+        nrg::find_knn(x->c, mode, k, dn, n, kp, exhaustive != 0, r, x->knn_ids, x->knn_d);
+        *k_out = r.k;
+        if (sweeps) *sweeps = r.sweeps;
+        to_host(x, ids, r.ids, n * (uint64_t)r.k);
+        to_host(x, dists, r.dists, n * (uint64_t)r.k);
+        x->c.sync();
+        if (n_churn) *n_churn = (int32_t)r.churn.size();
+        for (int t = 0; t < (int)r.churn.size() && t < churn_cap; ++t) churn[t] = r.churn[t];
+    });
+}
+
+int nrg_find_best(nrg_ctx* x, int32_t mode, uint64_t m, const int32_t* nodes, uint64_t n, const nrg_fb_params* p,
+                  int32_t exhaustive, nrg_pair* out, uint64_t cap, uint64_t* n_out, nrg_trace_level* trace,
+                  int32_t trace_cap, int32_t* n_levels, int32_t* short_count) {
+    return guard([&] {
+        if (mode != NRG_TABLE && mode != NRG_LINE) need_samples(x);
+        int32_t* dn = to_dev(x, x->q_j, nodes, n);
+        nrg::BestPairsD best;
+        nrg::find_best(x->c, mode, m, dn, n, p ? p->knn_eps : 1e-3, p ? p->seed : 0, p ? p->reverse != 0 : false,
+                       exhaustive != 0, best, x->out_i, x->out_j, x->out_d);
+        const uint64_t k = std::min(cap, best.count);
+        std::vector<int32_t> hi(k), hj(k);
+        std::vector<double> hd(k);
+        to_host(x, hi.data(), static_cast<int32_t*>(x->out_i.p), k);
+        to_host(x, hj.data(), static_cast<int32_t*>(x->out_j.p), k);
+        to_host(x, hd.data(), static_cast<double*>(x->out_d.p), k);
+        x->c.sync();
+        for (uint64_t t = 0; t < k; ++t) out[t] = {hi[t], hj[t], hd[t]};
+        *n_out = best.count;
+        if (n_levels) *n_levels = (int32_t)best.trace.size();
+        for (int t = 0; t < (int)best.trace.size() && t < trace_cap; ++t) {
+            const auto& l = best.trace[t];
+            trace[t] = {l.level, l.k, l.exhaustive, l.knn_sweeps, l.nodes, l.dedup_size};
+        }
+        if (short_count) *short_count = best.short_count ? 1 : 0;
+    });
+}
+
+int nrg_apply_updates(nrg_ctx* x, const nrg_pair* cands, uint64_t n, double* delta) {
+    return guard([&] {
+        need_samples(x);
+        std::vector<int32_t> hi(n), hj(n);
+        for (uint64_t t = 0; t < n; ++t) {
+            hi[t] = cands[t].i;
+            hj[t] = cands[t].j;
+        }
+        check_pairs(x, n, hi.data(), hj.data());
+        int32_t* di = to_dev(x, x->q_i, hi.data(), n);
+        int32_t* dj = to_dev(x, x->q_j, hj.data(), n);
+        const double d = nrg::apply_updates(x->c, di, dj, n, nullptr);
+        if (delta) *delta = d;
+    });
+}
+
+int nrg_theta_pass(nrg_ctx* x) {
+    return guard([&] {
+        need_samples(x);
+        nrg::theta_pass(x->c, nullptr);
+    });
+}
+
+int nrg_gcd_iteration(nrg_ctx* x, const nrg_gcd_cfg* cfg, int32_t iter, nrg_iter_record* rec, nrg_pair* cands,
+                      uint64_t cap, uint64_t* n_cands) {
+    return guard([&] { gcd_iteration(x, cfg, iter, rec, cands, cap, n_cands); });
+}
+
+int nrg_reconstruct_gcd(nrg_ctx* x, const nrg_gcd_cfg* cfg, nrg_iter_record* recs, int32_t rec_cap, int32_t* n_iters,
+                        int32_t* converged) {
+    return guard([&] {
+        need_samples(x);
+        if (!(cfg->kappa > 0.0)) nrg::fail(22, "reconstruct_gcd: kappa must be > 0");
+        const double eps = cfg->eps > 0.0 ? cfg->eps : 1e-6 * x->c.n;
+        *converged = 0;
+        *n_iters = 0;
+        for (int iter = 1; iter <= cfg->max_iters; ++iter) {
+            nrg_iter_record r;
+            gcd_iteration(x, cfg, iter, &r, nullptr, 0, nullptr);
+            if (*n_iters < rec_cap) recs[*n_iters] = r;
+            ++*n_iters;
+            if (r.delta < eps) {
+                *converged = 1;
+                break;
+            }
+        }
+    });
+}
+
+int nrg_counters(nrg_ctx* x, uint64_t* misses, uint64_t* hits, uint64_t* evals, uint64_t* warnings) {
+    return guard([&] {
+        uint64_t h[nrg::C_N];
+        NRG_CUDA(cudaMemcpyAsync(h, x->c.counters.p, sizeof(h), cudaMemcpyDeviceToHost, x->c.stream));
+        x->c.sync();
+        if (misses) *misses = h[nrg::C_MISSES];
+        if (hits) *hits = h[nrg::C_HITS];
+        if (evals) *evals = h[nrg::C_EVALS];
+        if (warnings) *warnings = h[nrg::C_WARN];
+    });
+}
+
+int nrg_reset_counters(nrg_ctx* x) {
+    return guard([&] {
+        NRG_CUDA(cudaMemsetAsync(x->c.counters.p, 0, nrg::C_N * 8, x->c.stream));
+        for (double& v : x->c.phase_ms) v = 0.0;
+        x->c.k1_ms = x->c.k1_launches = x->c.k1_pairs = x->c.k2_ms = x->c.k2_launches = x->c.k2_pairs = 0;
+        x->c.launches0 = nrg::g_launches.load();
+        x->c.sync();
+    });
+}
+
+int nrg_phase_times(nrg_ctx* x, double* ms, int32_t cap) {
+    return guard([&] {
+        for (int t = 0; t < nrg::P_N && t < cap; ++t) ms[t] = x->c.phase_ms[t];
+    });
+}
+
+int nrg_timer(nrg_ctx* x, int32_t op, double* ms) {
+    return guard([&] {
+        if (!x->t0) {
+            NRG_CUDA(cudaEventCreate(&x->t0));
+            NRG_CUDA(cudaEventCreate(&x->t1));
+        }
+        if (op == 0) {
+            NRG_CUDA(cudaEventRecord(x->t0, x->c.stream));
+        } else {
+            NRG_CUDA(cudaEventRecord(x->t1, x->c.stream));
+            NRG_CUDA(cudaEventSynchronize(x->t1));
+            float f = 0.f;
+            NRG_CUDA(cudaEventElapsedTime(&f, x->t0, x->t1));
+            if (ms) *ms = f;
+        }
+    });
+}
+
+int nrg_kernel_stats(nrg_ctx* x, double* out, int32_t cap) {
+    return guard([&] {
+        const nrg::Context& c = x->c;
+        const double v[7] = {c.k1_ms, c.k1_launches, c.k1_pairs, c.k2_ms, c.k2_launches, c.k2_pairs,
+                             (double)(nrg::g_launches.load() - c.launches0)};
+        for (int t = 0; t < 7 && t < cap; ++t) out[t] = v[t];
+    });
+}
+
+int nrg_sample_scored_pairs(nrg_ctx* x, uint64_t cap, uint64_t seed, int32_t* i, int32_t* j, uint64_t* n_out) {
+    return guard([&] {
+        int32_t* di = x->q_i.as<int32_t>(std::max<uint64_t>(cap, 1));
+        int32_t* dj = x->q_j.as<int32_t>(std::max<uint64_t>(cap, 1));
+        const uint64_t k = nrg::sample_scored_pairs(x->c, cap, seed, di, dj);
+        to_host(x, i, di, k);
+        to_host(x, j, dj, k);
+        x->c.sync();
+        *n_out = k;
+    });
+}
+
+int nrg_recall_curve(uint64_t m, const nrg_pair* exact, const nrg_pair* approx, double* out) {
+    // recall_curve (inc/find_best.hpp:211-231), host-side bookkeeping
+    return guard([&] {
+        std::unordered_map<uint64_t, char> se, sa;
+        se.reserve(m * 2);
+        sa.reserve(m * 2);
+        uint64_t common = 0;
+        for (uint64_t r = 0; r < m; ++r) {
+            const uint64_t ke = nrg::pair_key(exact[r].i, exact[r].j);
+            const uint64_t ka = nrg::pair_key(approx[r].i, approx[r].j);
+            if (sa.count(ke)) ++common;
+            se.emplace(ke, 1);
+            if (se.count(ka)) ++common;
+            sa.emplace(ka, 1);
+            out[r] = (double)common / (double)(r + 1);
+        }
+    });
+}
+
+int nrg_generate_ising(nrg_ctx* x, double mean_deg, double w_sigma, double th_sigma, int32_t burn_in, int32_t thin,
+                       uint64_t seed, int8_t* X_out) {
+    return guard([&] {
+        nrg::generate_ising(x->c, mean_deg, w_sigma, th_sigma, burn_in, thin, seed);
+        if (X_out) {
+            // unpack the bit-packed samples to int8 on the host
+            nrg::Context& c = x->c;
+            std::vector<uint32_t> bits((size_t)c.n * c.Mw);
+            NRG_CUDA(cudaMemcpyAsync(bits.data(), c.Xb.p, bits.size() * 4, cudaMemcpyDeviceToHost, c.stream));
+            c.sync();
+            for (int i = 0; i < c.n; ++i)
+                for (int m = 0; m < c.M; ++m)
+                    X_out[(size_t)i * c.M + m] = ((bits[(size_t)i * c.Mw + (m >> 5)] >> (m & 31)) & 1u) ? 1 : -1;
+        }
+    });
+}
+
+int nrg_comm_unique_id(uint8_t id[128]) {
+    return guard([&] {
+        (void)id;
+        nrg::fail(NRG_EINVAL, "multi-GPU communicator not built into this library");
+    });
+}
+int nrg_comm_init(nrg_ctx* x, const uint8_t id[128], int32_t rank, int32_t world) {
+    return guard([&] {
+        (void)x;
+        (void)id;
+        if (world != 1 || rank != 0) nrg::fail(NRG_EINVAL, "multi-GPU communicator not built into this library");
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,260 @@
+// context.cuh — device-resident state of one GCD problem on one B200.
+//
+// Layout in HBM, node-major like the reference's SampleMatrix
+// (inc/sample_matrix.hpp:12-13):
+//   Xb   u32  [N][Mw]   bit-packed +/-1 spins (Ising), bit m%32 of word m/32, 1 = +1
+//   Xd   f64  [N][Mp]   samples (Gaussian)
+//   H    f64  [N][Mp]   neighbour sums m_i = sum_j W_ij X_j  (inc/sparse_weights.hpp:164)
+//   theta f64 [N]
+//   W    open-addressing hash pair_key -> w  (inc/sparse_weights.hpp:162)
+//   per-generation snapshot (frozen W, inc/model.hpp:32-35):
+//     Ising:    T32 f32 [N][Mp] = tanh(H+theta), T64 f64 [N][Mp], Tabs f32 [N] = sum|T32|
+//     Gaussian: U   f64 [N][Mp] = X + theta^2 H,  xx f64 [N] = sum x^2
+//   DistanceCache: open-addressing hash pair_key -> dist (inc/model.hpp:36-97)
+// Mp = M rounded up to 128 (one float4 per lane per 128 samples); padding is zero.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "common.cuh"
+
+namespace nrg {
+
+enum Kind { ISING = 0, GAUSSIAN = 1 };
+enum Mode { EXACT = 0, GRADIENT = 1, TABLE = 2, LINE = 3 };
+
+// grow-only device buffer
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void* ensure(size_t b) {
+        if (b > bytes) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            size_t nb = b + b / 4 + 256;
+            NRG_CUDA(cudaMalloc(&p, nb));
+            bytes = nb;
+        }
+        return p;
+    }
+    template <class T>
+    T* as(size_t count) {
+        return static_cast<T*>(ensure(count * sizeof(T) + 16));
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+};
+
+struct HashView {
+    uint64_t* keys;
+    double* vals;
+    uint64_t mask;  // capacity - 1 (power of two)
+};
+
+__device__ __forceinline__ double hash_get(const HashView h, uint64_t key, double dflt) {
+    uint64_t s = mix64(key) & h.mask;
+    for (;;) {
+        const uint64_t k = h.keys[s];
+        if (k == key) return h.vals[s];
+        if (k == kEmptyKey) return dflt;
+        s = (s + 1) & h.mask;
+    }
+}
+
+struct IsingSnap {
+    const uint32_t* Xb;
+    const float* T32;
+    const double* T64;
+    const float* Tabs;
+    int M, Mp, Mw;
+};
+
+struct GaussSnap {
+    const double* X;
+    const double* U;
+    const double* xx;
+    const double* theta;
+    int M, Mp;
+};
+
+// outputs of a scoring pass: either scattered into the distance cache (slot-indexed)
+// or written per entry
+struct ScoreOut {
+    double* cache_vals = nullptr;
+    const uint32_t* slot = nullptr;
+    double* dist = nullptr;
+    double* w = nullptr;
+    double* gain = nullptr;
+    uint8_t* warn = nullptr;
+};
+
+enum Counter { C_MISSES = 0, C_HITS = 1, C_EVALS = 2, C_WARN = 3, C_N = 4 };
+enum Phase { P_SCORE = 0, P_KNN = 1, P_SELECT = 2, P_UPDATE = 3, P_THETA = 4, P_LOGPOST = 5, P_SNAP = 6, P_N = 7 };
+
+struct Context {
+    int n = 0, M = 0, kind = 0, device = 0;
+    int Mp = 0, Mw = 0;
+    double lambda = 0.0;
+    cudaStream_t stream = nullptr;
+    bool have_samples = false;
+
+    // samples
+    DevBuf Xb, Xd;
+    // state
+    DevBuf H, theta;
+    DevBuf Wkeys, Wvals;
+    uint64_t Wcap = 0;
+    DevBuf Wcount;  // u64[2]: live, used (occupied incl. tombstones)
+    uint64_t state_version = 1;
+
+    // snapshot
+    DevBuf T32, T64, Tabs, U, xx;
+    uint64_t snap_version = 0;
+    bool base_valid = false;
+    double base = 0.0;
+
+    // distance cache
+    DevBuf Ckeys, Cvals, Ccount;  // Ccount: u64 live
+    uint64_t Ccap = 0;
+    uint64_t cache_live_host = 0;
+    uint64_t last_survivors = 0;
+
+    // test metrics
+    DevBuf table, line;
+    uint64_t table_n = 0, line_n = 0;
+
+    // counters
+    DevBuf counters;  // u64[C_N]
+    double phase_ms[P_N] = {0};
+    // per-kernel stats: K1 screen ms / launches / pairs, K2 refine ms / launches / survivors
+    double k1_ms = 0, k1_launches = 0, k1_pairs = 0, k2_ms = 0, k2_launches = 0, k2_pairs = 0;
+    uint64_t launches0 = 0;
+    cudaEvent_t kev0 = nullptr, kev1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    // scratch
+    DevBuf s_a, s_b, s_c, s_d, s_e, s_f, s_g, s_h, s_i, s_j, s_k, s_l, s_m, s_n, s_o;
+    DevBuf red;  // reduction scratch
+    std::vector<char> host_scratch;
+
+    // multi-GPU (nccl), opaque
+    void* comm = nullptr;
+    int rank = 0, world = 1;
+
+    ~Context();
+
+    uint32_t* dXb() { return static_cast<uint32_t*>(Xb.p); }
+    double* dXd() { return static_cast<double*>(Xd.p); }
+    double* dH() { return static_cast<double*>(H.p); }
+    double* dtheta() { return static_cast<double*>(theta.p); }
+    uint64_t* dcounters() { return static_cast<uint64_t*>(counters.p); }
+    HashView Wview() {
+        return {static_cast<uint64_t*>(Wkeys.p), static_cast<double*>(Wvals.p), Wcap - 1};
+    }
+    HashView Cview() {
+        return {static_cast<uint64_t*>(Ckeys.p), static_cast<double*>(Cvals.p), Ccap - 1};
+    }
+    IsingSnap isnap() {
+        return {dXb(), static_cast<float*>(T32.p), static_cast<double*>(T64.p),
+                static_cast<float*>(Tabs.p), M, Mp, Mw};
+    }
+    GaussSnap gsnap() {
+        return {dXd(), static_cast<double*>(U.p), static_cast<double*>(xx.p), dtheta(), M, Mp};
+    }
+    void sync() { NRG_CUDA(cudaStreamSynchronize(stream)); }
+
+    // phase timing (device events around a region on this stream)
+    void tic() { NRG_CUDA(cudaEventRecord(ev0, stream)); }
+    void toc(int phase) {
+        NRG_CUDA(cudaEventRecord(ev1, stream));
+        NRG_CUDA(cudaEventSynchronize(ev1));
+        float ms = 0.f;
+        NRG_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+        phase_ms[phase] += ms;
+    }
+};
+
+// ---- state.cu
+void ctx_init(Context& c, int n, int m, int kind, double lambda, int device);
+void upload_samples_f64(Context& c, const double* X);
+void upload_spins_i8(Context& c, const int8_t* X);
+void set_theta(Context& c, const double* th);
+void reset_state_empty(Context& c);
+void w_reserve(Context& c, uint64_t extra);
+void get_state(Context& c, double* theta, uint64_t cap, int32_t* ei, int32_t* ej, double* w,
+               uint64_t* n_edges);
+void get_sums(Context& c, double* out);
+void ensure_snapshot(Context& c);
+double log_posterior(Context& c);
+double generation_base(Context& c);
+void begin_generation(Context& c);
+void cache_reserve(Context& c, uint64_t extra);
+void counters_add_host(Context& c, int which, uint64_t v);
+void set_table(Context& c, uint64_t n, const double* t);
+void set_line(Context& c, uint64_t n, const double* pos);
+
+// ---- score.cu
+// score a worklist of pairs (s[e], p[e]) against the frozen snapshot
+void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uint64_t n,
+                   const ScoreOut& out);
+// all pairs of `nodes` (device, n entries): dist[e] for e in the row-major upper triangle
+void score_all_pairs(Context& c, int mode, const int32_t* nodes, uint64_t n, double* dist);
+// cached distance lookups for a batch (probe/claim/score/gather), device arrays
+void distance_batch(Context& c, int mode, const int32_t* i, const int32_t* j, uint64_t n,
+                    double* dist);
+// optimize_edge against the current (live) state
+void optimize_edge_live(Context& c, const int32_t* i, const int32_t* j, uint64_t n, double* w,
+                        double* gain, uint8_t* warn);
+void edge_gradient_live(Context& c, const int32_t* i, const int32_t* j, uint64_t n, double* g);
+uint64_t sample_scored_pairs(Context& c, uint64_t cap, uint64_t seed, int32_t* oi, int32_t* oj);
+
+// ---- update.cu
+// candidates (device arrays, canonical i<j) in order; assign==nullptr -> optimize_edge
+double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n,
+                     const double* assign);
+void theta_pass(Context& c, double* out_only);
+
+// ---- knn.cu
+struct KnnParamsD {
+    double eps = 1e-3;
+    uint64_t seed = 0;
+    int max_sweeps = 100, scan_floor = 8, width_floor = 4;
+    bool reverse = false;
+};
+struct KnnResultD {
+    int k = 0;
+    int sweeps = 0;
+    std::vector<double> churn;
+    // device arrays, n*k: global ids and dists, rows sorted by (dist, id)
+    int32_t* ids = nullptr;
+    double* dists = nullptr;
+};
+void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n,
+              const KnnParamsD& p, bool exhaustive, KnnResultD& out, DevBuf& ids_buf,
+              DevBuf& dist_buf);
+
+// ---- find_best.cu
+struct TraceLevelD {
+    int level, k, exhaustive, knn_sweeps;
+    uint64_t nodes, dedup_size;
+};
+struct BestPairsD {
+    // device arrays of the result (sorted by (dist,i,j))
+    uint64_t count = 0;
+    bool short_count = false;
+    std::vector<TraceLevelD> trace;
+};
+void find_best(Context& c, int mode, uint64_t m, const int32_t* d_nodes, uint64_t n, double knn_eps,
+               uint64_t seed, bool reverse, bool exhaustive, BestPairsD& res, DevBuf& out_i,
+               DevBuf& out_j, DevBuf& out_d);
+
+// ---- gen.cu
+void generate_ising(Context& c, double mean_deg, double w_sigma, double th_sigma, int burn_in,
+                    int thin, uint64_t seed);
+
+}  // namespace nrg

@@ -1,0 +1,776 @@
+// knn.cu — NNDescent (Alg. 4) on the device: find_knn / find_knn_exhaustive
+// (inc/knn.hpp:150-314).
+//
+// Reference-exact semantics, re-expressed as sets so each phase is data-parallel:
+//   * initial graph: per node SplitRng(seed).split(id+1), Floyd sampling of kw
+//     distinct ranks over the id-sorted node set, self skipped (:171-200);
+//   * per sweep the snapshot S, the capped undirected view U (out-lists by (dist,id),
+//     then in-lists by (dist, src) while rows have room; cap = max(kw, scan_floor))
+//     (:202-247);
+//   * the scan replaces a node's worst entry with any strictly better 2-hop candidate
+//     not already listed (:249-270).  With a fixed per-generation distance, the final
+//     list is exactly the (dist,id)-top-kw of (snapshot list U candidates) — the
+//     visit-order independence the reference tests (test_knn.cpp:154-194) — so a
+//     sweep is: gather+dedup 2-hop candidates (one CTA per node, smem hash set or
+//     bitmap), claim them in the distance cache (one score per pair per generation,
+//     inc/model.hpp:54-70), score the claimed worklist, then merge top-kw per node;
+//   * churn = entries that entered from the candidate set (:273-290);
+//   * trim to k (:292-305); exhaustive fallbacks (:156-164).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <numeric>
+#include <vector>
+
+#include "context.cuh"
+
+namespace nrg {
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ bool entry_less(double da, int ia, double db, int ib) {
+    // entry_better (inc/knn.hpp:25-28)
+    return da < db || (da == db && ia < ib);
+}
+
+__global__ void iota_kernel(int32_t* v, uint64_t n) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) v[t] = (int32_t)t;
+}
+__global__ void scatter_loc_kernel(const int32_t* __restrict__ nodes, uint64_t n, int32_t* __restrict__ loc,
+                                   int n_total, int* __restrict__ bad) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const int g = nodes[t];
+    if (g < 0 || g >= n_total) {
+        atomicExch(bad, 1);
+        return;
+    }
+    if (atomicExch(&loc[g], (int32_t)t) != -1) atomicExch(bad, 2);  // duplicate node
+}
+__global__ void rank_kernel(const int32_t* __restrict__ perm, uint64_t n, int32_t* __restrict__ rank) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) rank[perm[t]] = (int32_t)t;
+}
+
+// initial out-neighbours: Floyd sampling (inc/knn.hpp:177-199)
+__global__ void knn_init_kernel(const int32_t* __restrict__ nodes, const int32_t* __restrict__ sorted_ids,
+                                const int32_t* __restrict__ rank, const int32_t* __restrict__ loc,
+                                uint64_t n, int kw, uint64_t seed, int32_t* __restrict__ gid,
+                                int32_t* __restrict__ qi, int32_t* __restrict__ qj) {
+    const uint64_t li = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (li >= n) return;
+    const SplitRng root(seed);
+    SplitRng r = root.split((uint64_t)nodes[li] + 1);
+    const uint64_t self = (uint64_t)rank[li];
+    int32_t* picks = gid + li * kw;  // ranks first, ids after
+    int np = 0;
+    for (uint64_t t = n - 1 - (uint64_t)kw; t < n - 1; ++t) {
+        uint64_t v = r.below(t + 1);
+        for (int q = 0; q < np; ++q)
+            if ((uint64_t)picks[q] == v) {
+                v = t;
+                break;
+            }
+        picks[np++] = (int32_t)v;
+    }
+    for (int t = 0; t < kw; ++t) {
+        uint64_t rk = (uint64_t)picks[t];
+        if (rk >= self) ++rk;
+        const int32_t g = sorted_ids[rk];
+        picks[t] = loc[g];  // local index
+        qi[li * kw + t] = nodes[li];
+        qj[li * kw + t] = g;
+    }
+}
+
+// sort each row (kw entries) by (dist, id); one thread per row (insertion sort)
+__global__ void row_sort_kernel(int32_t* __restrict__ gid, double* __restrict__ gd,
+                                const int32_t* __restrict__ nodes, uint64_t n, int kw) {
+    const uint64_t li = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (li >= n) return;
+    int32_t* ids = gid + li * kw;
+    double* ds = gd + li * kw;
+    for (int a = 1; a < kw; ++a) {
+        const int32_t id = ids[a];
+        const double d = ds[a];
+        const int gi = nodes[id];
+        int b = a - 1;
+        while (b >= 0 && entry_less(d, gi, ds[b], nodes[ids[b]])) {
+            ids[b + 1] = ids[b];
+            ds[b + 1] = ds[b];
+            --b;
+        }
+        ids[b + 1] = id;
+        ds[b + 1] = d;
+    }
+}
+
+// ---------------------------------------------------------------- cache claim
+__device__ __forceinline__ uint64_t cache_claim_k(HashView h, uint64_t key, bool& mine) {
+    uint64_t s = mix64(key) & h.mask;
+    for (;;) {
+        const uint64_t k = __ldcg(&h.keys[s]);
+        if (k == key) {
+            mine = false;
+            return s;
+        }
+        if (k == kEmptyKey) {
+            const unsigned long long prev = atomicCAS((unsigned long long*)&h.keys[s],
+                                                      (unsigned long long)kEmptyKey, (unsigned long long)key);
+            if (prev == kEmptyKey) {
+                mine = true;
+                return s;
+            }
+            if (prev == key) {
+                mine = false;
+                return s;
+            }
+        }
+        s = (s + 1) & h.mask;
+    }
+}
+
+struct ClaimSink {
+    int32_t* ws;
+    int32_t* wp;
+    uint32_t* wslot;
+    unsigned long long* wcount;
+    uint64_t* counters;
+    uint64_t* live;
+};
+
+// warp-cooperative claim of one candidate per lane (active lanes given by `valid`)
+__device__ __forceinline__ uint32_t claim_warp(HashView h, const ClaimSink& sink, bool valid, int32_t gs,
+                                               int32_t gp) {
+    bool mine = false;
+    uint64_t sl = 0;
+    if (valid) sl = cache_claim_k(h, pair_key(gs, gp), mine);
+    const int lane = threadIdx.x & 31;
+    const unsigned ball = __ballot_sync(0xffffffffu, mine);
+    const unsigned hits = __ballot_sync(0xffffffffu, valid && !mine);
+    unsigned long long b0 = 0;
+    if (lane == 0 && ball) b0 = atomicAdd(sink.wcount, (unsigned long long)__popc(ball));
+    b0 = __shfl_sync(0xffffffffu, b0, 0);
+    if (mine) {
+        const uint64_t at = b0 + __popc(ball & ((1u << lane) - 1));
+        sink.ws[at] = gs;
+        sink.wp[at] = gp;
+        sink.wslot[at] = (uint32_t)sl;
+    }
+    if (lane == 0) {
+        if (ball) {
+            atomicAdd((unsigned long long*)&sink.counters[C_MISSES], (unsigned long long)__popc(ball));
+            atomicAdd((unsigned long long*)sink.live, (unsigned long long)__popc(ball));
+        }
+        if (hits) atomicAdd((unsigned long long*)&sink.counters[C_HITS], (unsigned long long)__popc(hits));
+    }
+    return (uint32_t)sl;
+}
+
+// batch claim for a flat query list (init distances)
+__global__ void claim_list_kernel(HashView h, ClaimSink sink, const int32_t* __restrict__ qi,
+                                  const int32_t* __restrict__ qj, uint64_t n, uint32_t* __restrict__ slot) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = e < n;
+    const uint32_t sl = claim_warp(h, sink, valid, valid ? qi[e] : 0, valid ? qj[e] : 0);
+    if (valid) slot[e] = sl;
+}
+__global__ void gather_vals_kernel(const double* __restrict__ vals, const uint32_t* __restrict__ slot,
+                                   uint64_t n, double* __restrict__ out) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) out[e] = vals[slot[e]];
+}
+
+// ---------------------------------------------------------------- U (capped undirected view)
+// out-part: rows of the (sorted) snapshot; in-part appended while rows have room
+__global__ void u_out_kernel(const int32_t* __restrict__ gid, uint64_t n, int kw, int cap,
+                             int32_t* __restrict__ adj, int32_t* __restrict__ alen) {
+    const uint64_t li = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (li >= n) return;
+    for (int t = 0; t < kw; ++t) adj[li * cap + t] = gid[li * kw + t];
+    alen[li] = kw;
+}
+__global__ void in_keys_kernel(const int32_t* __restrict__ gid, const double* __restrict__ gd,
+                               const int32_t* __restrict__ nodes, uint64_t n, int kw,
+                               uint32_t* __restrict__ k_tgt, uint64_t* __restrict__ k_d,
+                               uint32_t* __restrict__ k_src, int32_t* __restrict__ v_src) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * kw) return;
+    const uint64_t li = e / kw;
+    k_tgt[e] = (uint32_t)gid[e];
+    k_d[e] = dkey(gd[e]);
+    k_src[e] = (uint32_t)nodes[li];
+    v_src[e] = (int32_t)li;
+}
+// one thread per target: walk its in-edges in (dist, src) order
+__global__ void u_in_kernel(const uint32_t* __restrict__ tgt_sorted, const int32_t* __restrict__ src_sorted,
+                            uint64_t ne, uint64_t n, int cap, int32_t* __restrict__ adj,
+                            int32_t* __restrict__ alen, const uint64_t* __restrict__ seg_start) {
+    const uint64_t lt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (lt >= n) return;
+    int32_t* row = adj + lt * cap;
+    int len = alen[lt];
+    for (uint64_t e = seg_start[lt]; e < ne && tgt_sorted[e] == lt && len < cap; ++e) {
+        const int32_t s = src_sorted[e];
+        bool dup = false;
+        for (int t = 0; t < len; ++t)
+            if (row[t] == s) {
+                dup = true;
+                break;
+            }
+        if (!dup) row[len++] = s;
+    }
+    alen[lt] = len;
+}
+__global__ void seg_start_kernel(const uint32_t* __restrict__ tgt_sorted, uint64_t ne, uint64_t n,
+                                 uint64_t* __restrict__ seg_start) {
+    const uint64_t lt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (lt >= n) return;
+    // lower_bound of lt in tgt_sorted
+    uint64_t lo = 0, hi = ne;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (tgt_sorted[mid] < lt) lo = mid + 1; else hi = mid;
+    }
+    seg_start[lt] = lo;
+}
+
+// reverse-list variant (nrg_knn_params.reverse): every in-edge is admitted into a
+// separate reverse row (capped), so U = out ∪ in regardless of kw >= scan_floor.
+__global__ void u_rev_kernel(const uint32_t* __restrict__ tgt_sorted, const int32_t* __restrict__ src_sorted,
+                             uint64_t ne, uint64_t n, int kw, int cap, int32_t* __restrict__ adj,
+                             int32_t* __restrict__ alen, const uint64_t* __restrict__ seg_start) {
+    const uint64_t lt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (lt >= n) return;
+    int32_t* row = adj + lt * cap;
+    int len = alen[lt];
+    for (uint64_t e = seg_start[lt]; e < ne && tgt_sorted[e] == lt && len < cap; ++e) {
+        const int32_t s = src_sorted[e];
+        bool dup = false;
+        for (int t = 0; t < kw; ++t)
+            if (row[t] == s) {
+                dup = true;
+                break;
+            }
+        if (!dup) row[len++] = s;
+    }
+    alen[lt] = len;
+}
+
+// ---------------------------------------------------------------- gather + claim
+// One CTA per node.  Dedup set in shared memory: open-addressing int hash (tsize
+// slots) or a bitmap over the level's n local ids (bitmap == true).
+template <int NT>
+__global__ void __launch_bounds__(NT) knn_gather_kernel(const int32_t* __restrict__ nodes, uint64_t n,
+                                                        const int32_t* __restrict__ adj,
+                                                        const int32_t* __restrict__ alen, int cap,
+                                                        const int32_t* __restrict__ gid, int kw, bool bitmap,
+                                                        int tsize, HashView h, ClaimSink sink,
+                                                        uint64_t capn, int32_t* __restrict__ cand_id,
+                                                        uint32_t* __restrict__ cand_slot,
+                                                        int32_t* __restrict__ cand_cnt) {
+    extern __shared__ int32_t tab[];
+    __shared__ int ncand;
+    const uint64_t li = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int words = bitmap ? (int)((n + 31) / 32) : tsize;
+    for (int t = tid; t < words; t += NT) tab[t] = bitmap ? 0 : -1;
+    if (tid == 0) ncand = 0;
+    __syncthreads();
+    auto insert = [&](int32_t v) -> bool {
+        if (bitmap) {
+            const uint32_t bit = 1u << (v & 31);
+            return !(atomicOr((uint32_t*)&tab[v >> 5], bit) & bit);
+        }
+        const uint32_t mask = (uint32_t)tsize - 1;
+        uint32_t s = ((uint32_t)v * 2654435761u) & mask;
+        for (;;) {
+            const int32_t prev = atomicCAS(&tab[s], -1, v);
+            if (prev == -1) return true;
+            if (prev == v) return false;
+            s = (s + 1) & mask;
+        }
+    };
+    // seed with self and the sweep-start list (the `contains` / self checks, :262-264)
+    if (tid == 0) insert((int32_t)li);
+    for (int t = tid; t < kw; t += NT) insert(gid[li * kw + t]);
+    __syncthreads();
+    const int32_t* row_i = adj + li * cap;
+    const int len_i = alen[li];
+    int32_t* my_ids = cand_id + li * capn;
+    for (int a = 0; a < len_i; ++a) {
+        const int32_t lj = row_i[a];
+        const int len_j = alen[lj];
+        const int32_t* row_j = adj + (uint64_t)lj * cap;
+        for (int b0 = 0; b0 < len_j; b0 += NT) {
+            const int b = b0 + tid;
+            if (b < len_j) {
+                const int32_t v = row_j[b];
+                if (insert(v)) {
+                    const int at = atomicAdd(&ncand, 1);
+                    my_ids[at] = v;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    const int cnt = ncand;
+    // claim (pair_key(nodes[li], nodes[v])) in the per-generation distance cache
+    const int32_t gs = nodes[li];
+    for (int t0 = 0; t0 < cnt; t0 += NT) {
+        const int t = t0 + tid;
+        const bool valid = t < cnt;
+        const int32_t v = valid ? my_ids[t] : 0;
+        const uint32_t sl = claim_warp(h, sink, valid, gs, valid ? nodes[v] : 0);
+        if (valid) cand_slot[li * capn + t] = sl;
+    }
+    if (tid == 0) cand_cnt[li] = cnt;
+}
+
+// ---------------------------------------------------------------- merge top-kw
+// One CTA per node: keep the (dist,id)-smallest kw of (current row U candidates).
+// Candidates are consumed in blocks of (buf_cap - kw); those beating the current
+// worst are appended after the row and the buffer is bitonic-sorted, so nothing
+// can overflow.  Counts entries that came from the candidate set (churn).
+template <int NT>
+__global__ void __launch_bounds__(NT) knn_merge_kernel(const int32_t* __restrict__ nodes, uint64_t n,
+                                                       int32_t* __restrict__ gid, double* __restrict__ gd, int kw,
+                                                       const int32_t* __restrict__ cand_id,
+                                                       const uint32_t* __restrict__ cand_slot,
+                                                       const int32_t* __restrict__ cand_cnt, uint64_t capn,
+                                                       const double* __restrict__ cvals, int buf_cap,
+                                                       unsigned long long* __restrict__ churn) {
+    extern __shared__ unsigned char smem_raw[];
+    double* bd = reinterpret_cast<double*>(smem_raw);
+    int32_t* bi = reinterpret_cast<int32_t*>(bd + buf_cap);  // local id
+    int32_t* bg = bi + buf_cap;                               // global id (tie order)
+    int32_t* bo = bg + buf_cap;                               // origin: 1 = candidate
+    __shared__ int nb;
+    const uint64_t li = blockIdx.x;
+    const int tid = threadIdx.x;
+    const int cnt = cand_cnt[li];
+    if (cnt == 0) return;
+    int32_t* row_id = gid + li * kw;
+    double* row_d = gd + li * kw;
+    for (int t = tid; t < kw; t += NT) {
+        bd[t] = row_d[t];
+        bi[t] = row_id[t];
+        bg[t] = nodes[row_id[t]];
+        bo[t] = 0;
+    }
+    __syncthreads();
+    const int B = buf_cap - kw;
+    bool changed_any = false;
+    for (int blk = 0; blk < cnt; blk += B) {
+        if (tid == 0) nb = kw;
+        __syncthreads();
+        const double wd = bd[kw - 1];
+        const int wg = bg[kw - 1];
+        const int end = min(cnt, blk + B);
+        for (int t = blk + tid; t < end; t += NT) {
+            const int32_t v = cand_id[li * capn + t];
+            const double d = cvals[cand_slot[li * capn + t]];
+            const int g = nodes[v];
+            if (entry_less(d, g, wd, wg)) {
+                const int at = atomicAdd(&nb, 1);
+                bd[at] = d;
+                bi[at] = v;
+                bg[at] = g;
+                bo[at] = 1;
+            }
+        }
+        __syncthreads();
+        const int m = nb;
+        if (m == kw) continue;  // nothing beats the worst
+        changed_any = true;
+        int P = 1;
+        while (P < m) P <<= 1;
+        for (int t = m + tid; t < P; t += NT) {
+            bd[t] = INFINITY;
+            bg[t] = 0x7fffffff;
+            bi[t] = -1;
+            bo[t] = 0;
+        }
+        __syncthreads();
+        for (int k2 = 2; k2 <= P; k2 <<= 1) {
+            for (int j = k2 >> 1; j > 0; j >>= 1) {
+                for (int t = tid; t < P; t += NT) {
+                    const int ixj = t ^ j;
+                    if (ixj > t) {
+                        const bool up = (t & k2) == 0;
+                        const bool gt = entry_less(bd[ixj], bg[ixj], bd[t], bg[t]);
+                        if (gt == up) {
+                            const double td = bd[t]; bd[t] = bd[ixj]; bd[ixj] = td;
+                            const int ti = bi[t]; bi[t] = bi[ixj]; bi[ixj] = ti;
+                            const int tg = bg[t]; bg[t] = bg[ixj]; bg[ixj] = tg;
+                            const int to = bo[t]; bo[t] = bo[ixj]; bo[ixj] = to;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+    }
+    if (!changed_any) return;
+    int ch = 0;
+    for (int t = tid; t < kw; t += NT) {
+        row_d[t] = bd[t];
+        row_id[t] = bi[t];
+        ch += bo[t];
+    }
+    ch = warp_sum(ch);
+    if ((tid & 31) == 0 && ch) atomicAdd(churn, (unsigned long long)ch);
+}
+
+// ---------------------------------------------------------------- exhaustive
+// rows of (id-sorted) candidates with distances from the triangular array
+__global__ void exh_fill2_kernel(const int32_t* __restrict__ sorted_loc, const int32_t* __restrict__ rank,
+                                 uint64_t n, const double* __restrict__ tri, uint64_t* __restrict__ keys,
+                                 int32_t* __restrict__ vals) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * (n - 1)) return;
+    const uint64_t li = e / (n - 1), t = e % (n - 1);
+    const uint64_t self = (uint64_t)rank[li];
+    const uint64_t pos = t < self ? t : t + 1;
+    const uint64_t lj = (uint64_t)sorted_loc[pos];
+    const uint64_t a = li < lj ? li : lj, b = li < lj ? lj : li;
+    // row-major upper triangle offset of (a, b)
+    const uint64_t off = a * (2 * n - a - 1) / 2 + (b - a - 1);
+    keys[e] = dkey(tri[off]);
+    vals[e] = (int32_t)lj;
+}
+__global__ void exh_take_kernel(const uint64_t* __restrict__ keys, const int32_t* __restrict__ vals,
+                                uint64_t n, int k, const int32_t* __restrict__ nodes,
+                                int32_t* __restrict__ out_id, double* __restrict__ out_d) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * (uint64_t)k) return;
+    const uint64_t li = e / k, t = e % k;
+    out_id[e] = nodes[vals[li * (n - 1) + t]];
+    out_d[e] = dkey_inv(keys[li * (n - 1) + t]);
+}
+__global__ void seg_offsets_kernel(int* __restrict__ off, uint64_t nseg, uint64_t len) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t <= nseg) off[t] = (int)(t * len);
+}
+
+static void knn_exhaustive(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n,
+                           const int32_t* sorted_loc, const int32_t* rank, KnnResultD& out, DevBuf& ids_buf,
+                           DevBuf& dist_buf) {
+    const uint64_t np = n * (n - 1) / 2;
+    double* tri = c.s_h.as<double>(np);
+    score_all_pairs(c, mode, d_nodes, n, tri);
+    const uint64_t ne = n * (n - 1);
+    if (ne > (uint64_t)INT32_MAX) fail(100, "exhaustive kNN too large for one segmented sort");
+    uint64_t* keys = c.s_i.as<uint64_t>(ne);
+    int32_t* vals = c.s_j.as<int32_t>(ne);
+    uint64_t* keys2 = c.s_f.as<uint64_t>(ne);
+    int32_t* vals2 = c.s_g.as<int32_t>(ne);
+    exh_fill2_kernel<<<(unsigned)ceil_div(ne, 256), 256, 0, c.stream>>>(sorted_loc, rank, n, tri, keys, vals);
+    int* off = c.s_e.as<int>(n + 1);
+    seg_offsets_kernel<<<(unsigned)ceil_div(n + 1, 256), 256, 0, c.stream>>>(off, n, n - 1);
+    NRG_LAUNCH_CHECK();
+    size_t tmp = 0;
+    cub::DeviceSegmentedSort::StableSortPairs(nullptr, tmp, keys, keys2, vals, vals2, (int)ne, (int)n, off,
+                                              off + 1, c.stream);
+    void* dtmp = c.s_k.ensure(tmp);
+    cub::DeviceSegmentedSort::StableSortPairs(dtmp, tmp, keys, keys2, vals, vals2, (int)ne, (int)n, off, off + 1,
+                                              c.stream);
+    out.k = k;
+    out.sweeps = 0;
+    out.churn.clear();
+    out.ids = ids_buf.as<int32_t>(n * k);
+    out.dists = dist_buf.as<double>(n * k);
+    exh_take_kernel<<<(unsigned)ceil_div(n * k, 256), 256, 0, c.stream>>>(keys2, vals2, n, k, d_nodes, out.ids,
+                                                                        out.dists);
+    NRG_LAUNCH_CHECK();
+    c.sync();
+}
+
+
+// ---------------------------------------------------------------- in-edge order
+template <class T>
+__global__ void gather_kernel(const T* __restrict__ in, const int32_t* __restrict__ perm, uint64_t n,
+                              T* __restrict__ out) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) out[t] = in[perm[t]];
+}
+
+// in-edges ordered by (target, dist, source id) — the per-target (dist, src) order of
+// inc/knn.hpp:234-246 — by three stable LSD radix passes over a permutation
+static void in_edge_sort(Context& c, uint64_t ne, const uint32_t* tgt, const uint64_t* dk, const uint32_t* src,
+                         const int32_t* srcloc, uint32_t* tgt_sorted, int32_t* src_sorted, DevBuf& pa,
+                         DevBuf& pb, DevBuf& k64, DevBuf& k32, DevBuf& tmpb) {
+    int32_t* p0 = pa.as<int32_t>(ne);
+    int32_t* p1 = pb.as<int32_t>(ne);
+    uint64_t* kbuf = k64.as<uint64_t>(2 * ne);
+    uint32_t* kb32 = k32.as<uint32_t>(2 * ne);
+    const unsigned g = (unsigned)ceil_div(ne, 256);
+    iota_kernel<<<g, 256, 0, c.stream>>>(p0, ne);
+    size_t t1 = 0, t2 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, t1, kb32, kb32 + ne, p0, p1, (int)ne, 0, 32, c.stream);
+    cub::DeviceRadixSort::SortPairs(nullptr, t2, kbuf, kbuf + ne, p0, p1, (int)ne, 0, 64, c.stream);
+    void* tmp = tmpb.ensure(std::max(t1, t2));
+    // pass 1: source id
+    cub::DeviceRadixSort::SortPairs(tmp, t1, src, kb32 + ne, p0, p1, (int)ne, 0, 32, c.stream);
+    // pass 2: dist (stable)
+    gather_kernel<uint64_t><<<g, 256, 0, c.stream>>>(dk, p1, ne, kbuf);
+    cub::DeviceRadixSort::SortPairs(tmp, t2, kbuf, kbuf + ne, p1, p0, (int)ne, 0, 64, c.stream);
+    // pass 3: target (stable)
+    gather_kernel<uint32_t><<<g, 256, 0, c.stream>>>(tgt, p0, ne, kb32);
+    cub::DeviceRadixSort::SortPairs(tmp, t1, kb32, tgt_sorted, p0, p1, (int)ne, 0, 32, c.stream);
+    gather_kernel<int32_t><<<g, 256, 0, c.stream>>>(srcloc, p1, ne, src_sorted);
+    NRG_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------- driver
+__global__ void to_global_kernel(const int32_t* __restrict__ gid, const double* __restrict__ gd,
+                                 const int32_t* __restrict__ nodes, uint64_t n, int kw, int k,
+                                 int32_t* __restrict__ out_id, double* __restrict__ out_d) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * (uint64_t)k) return;
+    const uint64_t li = e / k, t = e % k;
+    out_id[e] = nodes[gid[li * kw + t]];
+    out_d[e] = gd[li * kw + t];
+}
+
+static void score_claimed(Context& c, int mode, int32_t* ws, int32_t* wp, uint32_t* wslot, uint64_t nw) {
+    if (!nw) return;
+    ScoreOut so;
+    so.cache_vals = c.Cview().vals;
+    so.slot = wslot;
+    score_entries(c, mode, ws, wp, nw, so);
+}
+
+void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, const KnnParamsD& p,
+              bool exhaustive, KnnResultD& out, DevBuf& ids_buf, DevBuf& dist_buf) {
+    if (n < 2) fail(22, exhaustive ? "find_knn_exhaustive: need two nodes" : "find_knn: need at least two nodes");
+    if (!exhaustive) {
+        if (k < 1) fail(22, "find_knn: k must be >= 1");
+        if (!(p.eps > 0.0)) fail(22, "find_knn: eps must be > 0");
+    }
+    if (n > (uint64_t)INT32_MAX) fail(22, "find_knn: too many nodes");
+    if (mode == TABLE && !c.table_n) fail(22, "no distance table set");
+    if (mode == LINE && !c.line_n) fail(22, "no line metric set");
+    if (mode == EXACT || mode == GRADIENT) ensure_snapshot(c);
+
+    // local index map, id-sorted node set and ranks
+    int32_t* loc = c.s_a.as<int32_t>(c.n);
+    int* bad = c.s_b.as<int>(1);
+    NRG_CUDA(cudaMemsetAsync(loc, 0xff, (size_t)c.n * 4, c.stream));
+    NRG_CUDA(cudaMemsetAsync(bad, 0, 4, c.stream));
+    scatter_loc_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(d_nodes, n, loc, c.n, bad);
+    NRG_LAUNCH_CHECK();
+    DevBuf sbuf_ids, sbuf_loc, sbuf_rank, stmp;
+    int32_t* sorted_ids = sbuf_ids.as<int32_t>(n);
+    int32_t* sorted_loc = sbuf_loc.as<int32_t>(n);
+    int32_t* rank = sbuf_rank.as<int32_t>(n);
+    {
+        int32_t* iota = rank;  // temporarily
+        iota_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(iota, n);
+        size_t tmp = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp, d_nodes, sorted_ids, iota, sorted_loc, (int)n, 0, 32,
+                                        c.stream);
+        void* dt = stmp.ensure(tmp);
+        cub::DeviceRadixSort::SortPairs(dt, tmp, d_nodes, sorted_ids, iota, sorted_loc, (int)n, 0, 32, c.stream);
+        rank_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(sorted_loc, n, rank);
+        NRG_LAUNCH_CHECK();
+    }
+    int hbad = 0;
+    NRG_CUDA(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (hbad == 1) fail(34, "node id out of range");
+    if (hbad == 2) fail(22, "find_knn: duplicate node ids");
+
+    if (exhaustive || (uint64_t)k + 1 >= n) {
+        knn_exhaustive(c, mode, (int)std::min<uint64_t>((uint64_t)k, n - 1), d_nodes, n, sorted_loc, rank, out,
+                       ids_buf, dist_buf);
+        return;
+    }
+    const int kw = std::max(k, p.width_floor);
+    if ((uint64_t)kw + 1 >= n) {
+        knn_exhaustive(c, mode, k, d_nodes, n, sorted_loc, rank, out, ids_buf, dist_buf);
+        return;
+    }
+    const int cap = p.reverse ? std::max(2 * kw, p.scan_floor) : std::max(kw, p.scan_floor);
+
+    // working graph (local ids, sorted rows)
+    DevBuf gid_buf, gd_buf;
+    int32_t* gid = gid_buf.as<int32_t>(n * kw);
+    double* gd = gd_buf.as<double>(n * kw);
+    unsigned long long* wcount = c.s_c.as<unsigned long long>(2);
+    auto sink_for = [&](int32_t* ws, int32_t* wp, uint32_t* wslot) {
+        ClaimSink s;
+        s.ws = ws;
+        s.wp = wp;
+        s.wslot = wslot;
+        s.wcount = wcount;
+        s.counters = c.dcounters();
+        s.live = static_cast<uint64_t*>(c.Ccount.p);
+        return s;
+    };
+    const bool cached = (mode == EXACT || mode == GRADIENT);
+
+    // ---- initial graph
+    c.tic();
+    {
+        const uint64_t nq = n * kw;
+        DevBuf qib, qjb, slb;
+        int32_t* qi = qib.as<int32_t>(nq);
+        int32_t* qj = qjb.as<int32_t>(nq);
+        knn_init_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, c.stream>>>(d_nodes, sorted_ids, rank, loc, n, kw,
+                                                                       p.seed, gid, qi, qj);
+        NRG_LAUNCH_CHECK();
+        c.toc(P_KNN);
+        if (cached) {
+            cache_reserve(c, nq);
+            uint32_t* slot = slb.as<uint32_t>(nq);
+            DevBuf wsb, wpb, wslb;
+            int32_t* ws = wsb.as<int32_t>(nq);
+            int32_t* wp = wpb.as<int32_t>(nq);
+            uint32_t* wsl = wslb.as<uint32_t>(nq);
+            NRG_CUDA(cudaMemsetAsync(wcount, 0, 8, c.stream));
+            claim_list_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, c.stream>>>(c.Cview(), sink_for(ws, wp, wsl),
+                                                                              qi, qj, nq, slot);
+            NRG_LAUNCH_CHECK();
+            unsigned long long nw = 0;
+            NRG_CUDA(cudaMemcpyAsync(&nw, wcount, 8, cudaMemcpyDeviceToHost, c.stream));
+            c.sync();
+            score_claimed(c, mode, ws, wp, wsl, nw);
+            gather_vals_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, c.stream>>>(c.Cview().vals, slot, nq, gd);
+            NRG_LAUNCH_CHECK();
+        } else {
+            ScoreOut so;
+            so.dist = gd;
+            score_entries(c, mode, qi, qj, nq, so);
+        }
+        c.tic();
+        row_sort_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, c.stream>>>(gid, gd, d_nodes, n, kw);
+        NRG_LAUNCH_CHECK();
+        c.toc(P_KNN);
+    }
+
+    // ---- sweeps
+    const uint64_t capn = std::min<uint64_t>((uint64_t)cap * cap, n - 1);
+    DevBuf adjb, alenb, cidb, cslb, ccntb, churnb, wsb, wpb, wslb;
+    int32_t* adj = adjb.as<int32_t>(n * cap);
+    int32_t* alen = alenb.as<int32_t>(n);
+    int32_t* cand_id = cidb.as<int32_t>(n * capn);
+    uint32_t* cand_slot = cslb.as<uint32_t>(n * capn);
+    int32_t* cand_cnt = ccntb.as<int32_t>(n);
+    unsigned long long* churn = churnb.as<unsigned long long>(1);
+    const uint64_t wmax = n * capn;
+    int32_t* ws = wsb.as<int32_t>(cached ? wmax : 1);
+    int32_t* wp = wpb.as<int32_t>(cached ? wmax : 1);
+    uint32_t* wsl = wslb.as<uint32_t>(cached ? wmax : 1);
+    // dedup structure: hash of 2x(cap^2 + kw + 1) slots vs bitmap of n bits
+    const uint64_t hash_slots = [&] {
+        uint64_t s = 64;
+        while (s < 2 * (capn + kw + 1)) s <<= 1;
+        return s;
+    }();
+    const uint64_t bitmap_words = (n + 31) / 32;
+    const bool use_bitmap = bitmap_words < hash_slots;
+    const uint64_t tab_bytes = 4 * (use_bitmap ? bitmap_words : hash_slots);
+    if (tab_bytes > 200 * 1024) fail(100, "find_knn: dedup table exceeds shared memory");
+    const int big = capn > 256 ? 1 : 0;
+    if (tab_bytes > 48 * 1024) {
+        NRG_CUDA(cudaFuncSetAttribute(knn_gather_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)tab_bytes));
+        NRG_CUDA(cudaFuncSetAttribute(knn_gather_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)tab_bytes));
+    }
+    // merge buffer
+    // merge buffer: a power of two >= kw + 64 (bitonic width), at least 256
+    const int buf_cap = [&] {
+        int b = 256;
+        while (b < kw + 64) b <<= 1;
+        return b;
+    }();
+    if ((size_t)buf_cap * 20 > 200 * 1024) fail(100, "find_knn: kw too large for the merge buffer");
+    const size_t merge_smem = (size_t)buf_cap * (8 + 4 + 4 + 4);
+    if (merge_smem > 48 * 1024)
+        NRG_CUDA(cudaFuncSetAttribute(knn_merge_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)merge_smem));
+    if (merge_smem > 48 * 1024)
+        NRG_CUDA(cudaFuncSetAttribute(knn_merge_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)merge_smem));
+
+    out.sweeps = 0;
+    out.churn.clear();
+    DevBuf ktgt, kd, ksrc, vsrc, ktgt2, kd2, ksrc2, vsrc2, segb, sorttmp, permb, perm2b;
+    for (int sweep = 0; sweep < p.max_sweeps; ++sweep) {
+        c.tic();
+        // U
+        u_out_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, c.stream>>>(gid, n, kw, cap, adj, alen);
+        NRG_LAUNCH_CHECK();
+        if (cap > kw) {
+            const uint64_t ne = n * kw;
+            uint32_t* a_t = ktgt.as<uint32_t>(ne);
+            uint64_t* a_d = kd.as<uint64_t>(ne);
+            uint32_t* a_s = ksrc.as<uint32_t>(ne);
+            int32_t* a_v = vsrc.as<int32_t>(ne);
+            in_keys_kernel<<<(unsigned)ceil_div(ne, 256), 256, 0, c.stream>>>(gid, gd, d_nodes, n, kw, a_t, a_d, a_s,
+                                                                           a_v);
+            NRG_LAUNCH_CHECK();
+            uint32_t* tgt_sorted = ktgt2.as<uint32_t>(ne);
+            int32_t* src_sorted = vsrc2.as<int32_t>(ne);
+            in_edge_sort(c, ne, a_t, a_d, a_s, a_v, tgt_sorted, src_sorted, permb, perm2b, kd2, ksrc2, sorttmp);
+            uint64_t* seg = segb.as<uint64_t>(n);
+            seg_start_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(tgt_sorted, ne, n, seg);
+            if (p.reverse)
+                u_rev_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, c.stream>>>(tgt_sorted, src_sorted, ne, n, kw, cap,
+                                                                            adj, alen, seg);
+            else
+                u_in_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, c.stream>>>(tgt_sorted, src_sorted, ne, n, cap, adj,
+                                                                           alen, seg);
+            NRG_LAUNCH_CHECK();
+        }
+        c.toc(P_KNN);
+        // gather + claim
+        if (cached) cache_reserve(c, wmax);
+        c.tic();
+        NRG_CUDA(cudaMemsetAsync(wcount, 0, 16, c.stream));
+        NRG_CUDA(cudaMemsetAsync(churn, 0, 8, c.stream));
+        const HashView hv = cached ? c.Cview() : HashView{nullptr, nullptr, 0};
+        if (big)
+            knn_gather_kernel<256><<<(unsigned)n, 256, tab_bytes, c.stream>>>(
+                d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv, sink_for(ws, wp, wsl), capn,
+                cand_id, cand_slot, cand_cnt);
+        else
+            knn_gather_kernel<32><<<(unsigned)n, 32, tab_bytes, c.stream>>>(
+                d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv, sink_for(ws, wp, wsl), capn,
+                cand_id, cand_slot, cand_cnt);
+        NRG_LAUNCH_CHECK();
+        unsigned long long nw = 0;
+        NRG_CUDA(cudaMemcpyAsync(&nw, wcount, 8, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        c.toc(P_KNN);
+        score_claimed(c, mode, ws, wp, wsl, nw);
+        c.tic();
+        if (kw > 64)
+            knn_merge_kernel<128><<<(unsigned)n, 128, merge_smem, c.stream>>>(
+                d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, c.Cview().vals, buf_cap, churn);
+        else
+            knn_merge_kernel<32><<<(unsigned)n, 32, merge_smem, c.stream>>>(
+                d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, c.Cview().vals, buf_cap, churn);
+        NRG_LAUNCH_CHECK();
+        unsigned long long changed = 0;
+        NRG_CUDA(cudaMemcpyAsync(&changed, churn, 8, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        c.toc(P_KNN);
+        ++out.sweeps;
+        const double ratio = (double)changed / ((double)kw * (double)n);
+        out.churn.push_back(ratio);
+        if (ratio < p.eps) break;
+    }
+    // trim to k / convert to global ids
+    out.k = k;
+    out.ids = ids_buf.as<int32_t>(n * k);
+    out.dists = dist_buf.as<double>(n * k);
+    to_global_kernel<<<(unsigned)ceil_div(n * k, 256), 256, 0, c.stream>>>(gid, gd, d_nodes, n, kw, k, out.ids,
+                                                                         out.dists);
+    NRG_LAUNCH_CHECK();
+    c.sync();
+}
+
+}  // namespace nrg

@@ -1,0 +1,663 @@
+// score.cu — the pair-scoring kernels: distance() (inc/model.hpp:377-386) for
+// worklists of candidate pairs.
+//
+// Ising exact mode is one fused warp-per-pair kernel:
+//   K1 (every pair, bandwidth-bound): g0 = 2<x_a,x_b> - <x_b,T_a> - <x_a,T_b> from
+//      bit-packed spins (popcount) and the fp32 snapshot T32, with a rigorous fp32
+//      error bound err; |g0| <= lambda - err  =>  pruned: w* = 0, gain = 0 exactly,
+//      dist = -base (the reference's tie value, inc/model.hpp:205-209).
+//   K2 (survivors, ~2-3%): safeguarded Newton in fp32 on the register-resident
+//      columns, then ONE fp64 pass over T64 that evaluates L', L'' and the slice gain
+//      at the fp32 root and applies the second-order Newton correction.
+//   Existing edges (w_cur != 0), kink decisions inside the error band and fp32
+//   failures go to the full fp64 routine (pairscore.cuh).
+// The stationary column (first entry of a worklist run) stays in registers across
+// consecutive entries, so each pair streams only its partner: M/8 + 4 Mp bytes.
+#include <algorithm>
+#include <vector>
+
+#include "pairscore.cuh"
+
+namespace nrg {
+
+__device__ __forceinline__ float flipf(float v, uint32_t bit) {
+    // multiply by x = +1 (bit 1) / -1 (bit 0), exactly
+    return __uint_as_float(__float_as_uint(v) ^ ((bit ^ 1u) << 31));
+}
+
+template <int MQ>
+struct Col32 {
+    float4 T[MQ];
+    uint32_t w[MQ];  // word holding this lane's 4 sign bits for chunk q
+};
+
+template <int MQ>
+__device__ __forceinline__ void load_col32(Col32<MQ>& c, const IsingSnap& S, int row, int lane) {
+    const float4* t4 = reinterpret_cast<const float4*>(S.T32 + (size_t)row * S.Mp);
+#pragma unroll
+    for (int q = 0; q < MQ; ++q) {
+        c.T[q] = __ldg(&t4[lane + 32 * q]);
+        c.w[q] = __ldg(&S.Xb[(size_t)row * S.Mw + (lane >> 3) + 4 * q]);
+    }
+}
+
+__device__ __forceinline__ float comp(const float4& v, int c) {
+    return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
+}
+
+// fp32 evaluation of L'(w), L''(w) on the register columns of the stationary (S)
+// and partner (P) nodes; per-sample terms are formed with canonical roles
+// (a, b) = (min, max) so the result does not depend on which node is stationary.
+template <int MQ>
+__device__ __forceinline__ void eval32(const Col32<MQ>& CS, const Col32<MQ>& CP, bool s_is_a, int lane,
+                                       int M, float w, float& Lp, float& Lpp) {
+    const float t = tanhf(w);
+    const float omt2 = 1.f - t * t;
+    float lp = 0.f, lpp = 0.f;
+    const int sh = 4 * (lane & 7);
+#pragma unroll
+    for (int q = 0; q < MQ; ++q) {
+        const int mb = 4 * (lane + 32 * q);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (mb + c < M) {
+                const uint32_t bs = (CS.w[q] >> (sh + c)) & 1u, bp = (CP.w[q] >> (sh + c)) & 1u;
+                const float ys = flipf(comp(CS.T[q], c), bp);  // x_p T_s
+                const float yp = flipf(comp(CP.T[q], c), bs);  // x_s T_p
+                const float ya = s_is_a ? ys : yp, yb = s_is_a ? yp : ys;
+                const float s2 = (bs == bp) ? 2.f : -2.f;  // 2 x_a x_b
+                const float da = __frcp_rn(1.f + ya * t);
+                const float db = __frcp_rn(1.f + yb * t);
+                const float qa = (ya + t) * da, qb = (yb + t) * db;
+                lp += (s2 - qa) - qb;
+                lpp -= (1.f - ya * ya) * omt2 * da * da + (1.f - yb * yb) * omt2 * db * db;
+            }
+        }
+    }
+    Lp = warp_sum(lp);
+    Lpp = warp_sum(lpp);
+}
+
+// K1: the bandwidth-bound screen.  Pruned pairs are finished here; the rest
+// (survivors, existing edges, kink decisions inside the fp32 error band) are
+// appended to a compacted list for K2.
+template <int MQ>
+__global__ void __launch_bounds__(256, 2) ising_screen_kernel(IsingSnap S, HashView W,
+                                                              const int32_t* __restrict__ es,
+                                                              const int32_t* __restrict__ ep, uint64_t n,
+                                                              int chunk, double lambda, double base,
+                                                              ScoreOut out, uint64_t* __restrict__ surv,
+                                                              unsigned long long* __restrict__ nsurv,
+                                                              uint64_t* counters) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    Col32<MQ> cs, cp;
+    int cur = -1;
+    float tabs_s = 0.f;
+    uint64_t evals = 0;
+    const float gam = (float)(4 * MQ + 8) * 5.9604645e-08f * 1.01f;  // 2^-24 per rounding
+    const float lam = (float)lambda;
+    const double pruned_dist = -(base + 0.0);
+    for (uint64_t c0 = warp0 * chunk; c0 < n; c0 += nwarps * chunk) {
+        const uint64_t c1 = c0 + chunk < n ? c0 + chunk : n;
+        for (uint64_t e = c0; e < c1; ++e) {
+            const int s = es[e], p = ep[e];
+            if (s != cur) {
+                load_col32<MQ>(cs, S, s, lane);
+                tabs_s = __ldg(&S.Tabs[s]);
+                cur = s;
+            }
+            const double wcur = hash_get(W, pair_key(s, p), 0.0);
+            bool pruned = false;
+            if (wcur == 0.0) {
+                load_col32<MQ>(cp, S, p, lane);
+                const float tabs_p = __ldg(&S.Tabs[p]);
+                // g0 = 2<x_a,x_b> - sum_m (x_p T_s + x_s T_p)
+                float acc = 0.f;
+                int diff = 0;
+                const int sh = 4 * (lane & 7);
+#pragma unroll
+                for (int q = 0; q < MQ; ++q) {
+                    const uint32_t ws = cs.w[q], wp = cp.w[q];
+                    if ((lane & 7) == 0) diff += __popc(ws ^ wp);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const uint32_t bs = (ws >> (sh + c)) & 1u, bp = (wp >> (sh + c)) & 1u;
+                        acc += flipf(comp(cs.T[q], c), bp) + flipf(comp(cp.T[q], c), bs);
+                    }
+                }
+                acc = warp_sum(acc);
+                diff = warp_sum(diff);
+                const float g = (float)(2 * (S.M - 2 * diff)) - acc;
+                const float err = gam * (tabs_s + tabs_p) + 1e-30f;
+                pruned = fabsf(g) <= lam - err;
+                ++evals;
+            }
+            if (pruned) {
+                // L1 kink: w* = 0 and gain = 0 exactly (inc/model.hpp:205-209)
+                if (lane == 0) {
+                    if (out.cache_vals) out.cache_vals[out.slot[e]] = pruned_dist;
+                    if (out.dist) out.dist[e] = pruned_dist;
+                    if (out.w) out.w[e] = 0.0;
+                    if (out.gain) out.gain[e] = 0.0;
+                    if (out.warn) out.warn[e] = 0;
+                }
+            } else if (lane == 0) {
+                surv[atomicAdd(nsurv, 1ull)] = e;
+            }
+        }
+    }
+    if (lane == 0 && counters) atomicAdd((unsigned long long*)&counters[C_EVALS], (unsigned long long)evals);
+}
+
+// K2: survivors.  fp64 kink check where needed, fp32 Newton on register columns,
+// one fp64 pass at the fp32 root with a second-order correction; full fp64
+// routine for existing edges and fp32 failures.
+template <int MQ>
+__global__ void __launch_bounds__(128) ising_refine_kernel(IsingSnap S, HashView W,
+                                                            const int32_t* __restrict__ es,
+                                                            const int32_t* __restrict__ ep,
+                                                            const uint64_t* __restrict__ surv, uint64_t ns,
+                                                            double lambda, double base, ScoreOut out,
+                                                            uint64_t* counters) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (t >= ns) return;
+    const uint64_t e = surv[t];
+    const int s = es[e], p = ep[e];
+    const int a = s < p ? s : p, b = s < p ? p : s;
+    const TSnap T64{S.T64, S.Mp};
+    const double wcur = hash_get(W, pair_key(a, b), 0.0);
+    EdgeOptD r;
+    r.w = 0.0;
+    r.gain = 0.0;
+    r.warn = 0;
+    r.passes = 0;
+    if (wcur != 0.0) {
+        r = ising_optimize_edge64(T64, S.Xb, S.Mw, S.M, a, b, wcur, lambda);
+    } else {
+        const double g64 = ising_gradient64(T64, S.Xb, S.Mw, S.M, a, b);
+        r.passes = 1;
+        if (fabs(g64) > lambda) {
+            Col32<MQ> ca, cb;
+            load_col32<MQ>(ca, S, a, lane);
+            load_col32<MQ>(cb, S, b, lane);
+            const float dir = g64 > 0.0 ? 1.f : -1.f;
+            float lo = 0.f, hi = INFINITY, u = 0.f;
+            float Lp, Lpp;
+            eval32<MQ>(ca, cb, true, lane, S.M, 0.f, Lp, Lpp);
+            float phi = (float)(fabs(g64) - lambda), dphi = Lpp;
+            bool ok = false;
+            for (int it = 0; it < 24; ++it) {
+                ++r.passes;
+                if (phi > 0.f) lo = u; else hi = u;
+                float un = u - phi / dphi;
+                if (!(un > lo && un < hi) || !isfinite(un)) un = isinf(hi) ? fmaxf(2.f * u, 1.f) : 0.5f * (lo + hi);
+                const bool done = fabsf(un - u) <= 2e-6f * fmaxf(un, 1e-3f);
+                u = un;
+                if (done) {
+                    ok = true;
+                    break;
+                }
+                if (u > 12.f) break;
+                eval32<MQ>(ca, cb, true, lane, S.M, dir * u, Lp, Lpp);
+                phi = dir * Lp - (float)lambda;
+                dphi = Lpp;
+            }
+            bool fin = false;
+            if (ok && u <= 12.f) {
+                const double ud = (double)u, dird = (double)dir;
+                const Pass64 p64 = ising_pass64<TSnap, true>(T64, S.Xb, S.Mw, S.M, a, b, dird * ud);
+                ++r.passes;
+                const double ph = dird * p64.Lp - lambda, dph = p64.Lpp;
+                if (dph < 0.0) {
+                    const double du = -ph / dph;
+                    if (fabs(du) <= 1e-4 * fmax(1.0, ud)) {
+                        r.w = dird * (ud + du);
+                        r.gain = (p64.Flik - lambda * ud) + 0.5 * ph * du;
+                        if (r.gain < 0.0) {
+                            r.gain = 0.0;
+                            r.w = 0.0;
+                        }
+                        fin = true;
+                    }
+                }
+            }
+            if (!fin) {
+                const EdgeOptD f = ising_optimize_edge64(T64, S.Xb, S.Mw, S.M, a, b, 0.0, lambda);
+                r.w = f.w;
+                r.gain = f.gain;
+                r.warn = f.warn;
+                r.passes += f.passes;
+            }
+        }
+    }
+    if (lane == 0) {
+        const double dist = -(base + r.gain);
+        if (out.cache_vals) out.cache_vals[out.slot[e]] = dist;
+        if (out.dist) out.dist[e] = dist;
+        if (out.w) out.w[e] = r.w;
+        if (out.gain) out.gain[e] = r.gain;
+        if (out.warn) out.warn[e] = (uint8_t)r.warn;
+        if (counters) {
+            atomicAdd((unsigned long long*)&counters[C_EVALS], (unsigned long long)r.passes);
+            if (r.warn) atomicAdd((unsigned long long*)&counters[C_WARN], 1ull);
+        }
+    }
+}
+
+// fp64 kernels for the remaining modes: Ising exact (M > 2048), Ising gradient,
+// Gaussian exact / gradient.  One warp per entry.
+__global__ void __launch_bounds__(256) generic_score_kernel(int kind, int mode, IsingSnap S, GaussSnap G,
+                                                            HashView W, const int32_t* __restrict__ es,
+                                                            const int32_t* __restrict__ ep, uint64_t n,
+                                                            double lambda, double base, ScoreOut out,
+                                                            uint64_t* counters) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint64_t evals = 0, warns = 0;
+    for (uint64_t e = warp0; e < n; e += nwarps) {
+        const int s = es[e], p = ep[e];
+        const int a = s < p ? s : p, b = s < p ? p : s;
+        const double wcur = hash_get(W, pair_key(a, b), 0.0);
+        double dist;
+        EdgeOptD r;
+        r.w = 0.0;
+        r.gain = 0.0;
+        r.warn = 0;
+        r.passes = 1;
+        if (kind == ISING) {
+            const TSnap T{S.T64, S.Mp};
+            if (mode == EXACT) {
+                r = ising_optimize_edge64(T, S.Xb, S.Mw, S.M, a, b, wcur, lambda);
+                dist = -(base + r.gain);
+            } else {
+                const double g = ising_gradient64(T, S.Xb, S.Mw, S.M, a, b);
+                const double sg = wcur > 0.0 ? 1.0 : (wcur < 0.0 ? -1.0 : 0.0);
+                dist = -fabs(g - lambda * sg);
+            }
+        } else {
+            const USnap Uf{G.U, G.Mp};
+            const double ta = G.theta[a], tb = G.theta[b];
+            const GaussCoef cf = gauss_coef(Uf, G.X, G.Mp, G.M, a, b, ta * ta, tb * tb, G.xx[a], G.xx[b]);
+            if (mode == EXACT) {
+                r = gauss_optimize(cf, wcur, lambda);
+                dist = -(base + r.gain);
+            } else {
+                const double sg = wcur > 0.0 ? 1.0 : (wcur < 0.0 ? -1.0 : 0.0);
+                dist = -fabs(-cf.P - lambda * sg);
+            }
+        }
+        evals += r.passes;
+        warns += r.warn;
+        if (lane == 0) {
+            if (out.cache_vals) out.cache_vals[out.slot[e]] = dist;
+            if (out.dist) out.dist[e] = dist;
+            if (out.w) out.w[e] = r.w;
+            if (out.gain) out.gain[e] = r.gain;
+            if (out.warn) out.warn[e] = (uint8_t)r.warn;
+        }
+    }
+    if (lane == 0 && counters) {
+        atomicAdd((unsigned long long*)&counters[C_EVALS], (unsigned long long)evals);
+        if (warns) atomicAdd((unsigned long long*)&counters[C_WARN], (unsigned long long)warns);
+    }
+}
+
+// test metrics (TableMetric / LineMetric)
+__global__ void metric_score_kernel(int mode, const double* __restrict__ table, uint64_t tn,
+                                    const double* __restrict__ pos, const int32_t* __restrict__ es,
+                                    const int32_t* __restrict__ ep, uint64_t n, ScoreOut out) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    const int s = es[e], p = ep[e];
+    const int a = s < p ? s : p, b = s < p ? p : s;
+    const double d = mode == TABLE ? table[(uint64_t)a * tn + b] : fabs(pos[s] - pos[p]);
+    if (out.cache_vals) out.cache_vals[out.slot[e]] = d;
+    if (out.dist) out.dist[e] = d;
+}
+
+static int num_sms(Context& c) {
+    static int sms = 0;
+    if (!sms) NRG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+    return sms;
+}
+
+void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uint64_t n,
+                   const ScoreOut& out) {
+    if (n == 0) return;
+    c.tic();
+    if (mode == TABLE || mode == LINE) {
+        if (mode == TABLE && !c.table_n) fail(22, "no distance table set");
+        if (mode == LINE && !c.line_n) fail(22, "no line metric set");
+        metric_score_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(
+            mode, static_cast<double*>(c.table.p), c.table_n, static_cast<double*>(c.line.p), s, p, n,
+            out);
+        NRG_LAUNCH_CHECK();
+        c.toc(P_SCORE);
+        return;
+    }
+    ensure_snapshot(c);
+    const double base = mode == EXACT ? generation_base(c) : 0.0;
+    c.tic();
+    const int sms = num_sms(c);
+    const int MQ = c.Mp / 128;
+    if (c.kind == ISING && mode == EXACT && MQ <= 16) {
+        const int chunk = 8;
+        const uint64_t chunks = (n + chunk - 1) / chunk;
+        const uint64_t blocks = std::min<uint64_t>((chunks + 7) / 8, (uint64_t)sms * 8);
+        const IsingSnap S = c.isnap();
+        const HashView W = c.Wview();
+        uint64_t* surv = c.s_l.as<uint64_t>(n);
+        unsigned long long* nsurv = c.s_k.as<unsigned long long>(1);
+        NRG_CUDA(cudaMemsetAsync(nsurv, 0, 8, c.stream));
+        NRG_CUDA(cudaEventRecord(c.kev0, c.stream));
+#define NRG_LAUNCH_MQ(Q)                                                                              \
+    ising_screen_kernel<Q><<<(unsigned)blocks, 256, 0, c.stream>>>(S, W, s, p, n, chunk, c.lambda, base, \
+                                                                    out, surv, nsurv, c.dcounters())
+        switch (MQ) {
+            case 1: NRG_LAUNCH_MQ(1); break;
+            case 2: NRG_LAUNCH_MQ(2); break;
+            case 3: NRG_LAUNCH_MQ(3); break;
+            case 4: NRG_LAUNCH_MQ(4); break;
+            case 5: NRG_LAUNCH_MQ(5); break;
+            case 6: NRG_LAUNCH_MQ(6); break;
+            case 7: NRG_LAUNCH_MQ(7); break;
+            case 8: NRG_LAUNCH_MQ(8); break;
+            case 10: NRG_LAUNCH_MQ(10); break;
+            case 12: NRG_LAUNCH_MQ(12); break;
+            case 14: NRG_LAUNCH_MQ(14); break;
+            case 16: NRG_LAUNCH_MQ(16); break;
+            default: fail(100, "unsupported padded sample count");
+        }
+#undef NRG_LAUNCH_MQ
+        NRG_LAUNCH_CHECK();
+        NRG_CUDA(cudaEventRecord(c.kev1, c.stream));
+        unsigned long long ns = 0;
+        NRG_CUDA(cudaMemcpyAsync(&ns, nsurv, 8, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        {
+            float ms = 0.f;
+            NRG_CUDA(cudaEventElapsedTime(&ms, c.kev0, c.kev1));
+            c.k1_ms += ms;
+            c.k1_launches += 1;
+            c.k1_pairs += (double)n;
+        }
+        c.last_survivors = ns;
+        if (ns) {
+            NRG_CUDA(cudaEventRecord(c.kev0, c.stream));
+            const unsigned rb = (unsigned)ceil_div((int64_t)ns * 32, 128);
+#define NRG_LAUNCH_MQ(Q)                                                                        \
+    ising_refine_kernel<Q><<<rb, 128, 0, c.stream>>>(S, W, s, p, surv, ns, c.lambda, base, out, \
+                                                      c.dcounters())
+            switch (MQ) {
+                case 1: NRG_LAUNCH_MQ(1); break;
+                case 2: NRG_LAUNCH_MQ(2); break;
+                case 3: NRG_LAUNCH_MQ(3); break;
+                case 4: NRG_LAUNCH_MQ(4); break;
+                case 5: NRG_LAUNCH_MQ(5); break;
+                case 6: NRG_LAUNCH_MQ(6); break;
+                case 7: NRG_LAUNCH_MQ(7); break;
+                case 8: NRG_LAUNCH_MQ(8); break;
+                case 10: NRG_LAUNCH_MQ(10); break;
+                case 12: NRG_LAUNCH_MQ(12); break;
+                case 14: NRG_LAUNCH_MQ(14); break;
+                case 16: NRG_LAUNCH_MQ(16); break;
+            }
+#undef NRG_LAUNCH_MQ
+            NRG_LAUNCH_CHECK();
+            NRG_CUDA(cudaEventRecord(c.kev1, c.stream));
+            NRG_CUDA(cudaEventSynchronize(c.kev1));
+            float ms = 0.f;
+            NRG_CUDA(cudaEventElapsedTime(&ms, c.kev0, c.kev1));
+            c.k2_ms += ms;
+            c.k2_launches += 1;
+            c.k2_pairs += (double)ns;
+        }
+    } else {
+        const uint64_t blocks = std::min<uint64_t>((n + 7) / 8, (uint64_t)sms * 16);
+        generic_score_kernel<<<(unsigned)blocks, 256, 0, c.stream>>>(
+            c.kind, mode, c.isnap(), c.gsnap(), c.Wview(), s, p, n, c.lambda, base, out, c.dcounters());
+        NRG_LAUNCH_CHECK();
+    }
+    c.toc(P_SCORE);
+}
+
+// ---------------------------------------------------------------- all pairs
+__global__ void fill_rows_kernel(const int32_t* __restrict__ nodes, uint64_t n, uint64_t r0, uint64_t r1,
+                                 const uint64_t* __restrict__ off, int32_t* __restrict__ es,
+                                 int32_t* __restrict__ ep) {
+    // one block per row a in [r0, r1): pairs (nodes[a], nodes[c]) for c > a
+    const uint64_t a = r0 + blockIdx.x;
+    if (a >= r1) return;
+    const uint64_t base = off[a] - off[r0];
+    for (uint64_t c = a + 1 + threadIdx.x; c < n; c += blockDim.x) {
+        es[base + (c - a - 1)] = nodes[a];
+        ep[base + (c - a - 1)] = nodes[c];
+    }
+}
+
+void score_all_pairs(Context& c, int mode, const int32_t* nodes, uint64_t n, double* dist) {
+    // row-major upper triangle (inc/find_best.hpp:72-86), chunked by rows
+    if (n < 2) return;
+    std::vector<uint64_t> off(n + 1, 0);
+    for (uint64_t a = 0; a < n; ++a) off[a + 1] = off[a] + (n - a - 1);
+    uint64_t* doff = c.s_o.as<uint64_t>(n + 1);
+    NRG_CUDA(cudaMemcpyAsync(doff, off.data(), (n + 1) * 8, cudaMemcpyHostToDevice, c.stream));
+    const uint64_t maxp = 1ull << 25;
+    uint64_t r0 = 0;
+    while (r0 < n - 1) {
+        uint64_t r1 = r0 + 1;
+        while (r1 < n && off[r1 + 1] - off[r0] <= maxp) ++r1;
+        const uint64_t cnt = off[r1] - off[r0];
+        int32_t* es = c.s_m.as<int32_t>(cnt);
+        int32_t* ep = c.s_n.as<int32_t>(cnt);
+        fill_rows_kernel<<<(unsigned)(r1 - r0), 256, 0, c.stream>>>(nodes, n, r0, r1, doff, es, ep);
+        NRG_LAUNCH_CHECK();
+        ScoreOut out;
+        out.dist = dist + off[r0];
+        score_entries(c, mode, es, ep, cnt, out);
+        r0 = r1;
+    }
+    // probes count as misses (no cache on this path)
+    counters_add_host(c, C_MISSES, n * (n - 1) / 2);
+}
+
+// ---------------------------------------------------------------- cached batch lookups
+__device__ __forceinline__ uint64_t cache_claim(HashView h, uint64_t key, bool& mine) {
+    uint64_t s = mix64(key) & h.mask;
+    for (;;) {
+        const uint64_t k = __ldcg(&h.keys[s]);
+        if (k == key) {
+            mine = false;
+            return s;
+        }
+        if (k == kEmptyKey) {
+            const unsigned long long prev = atomicCAS((unsigned long long*)&h.keys[s],
+                                                      (unsigned long long)kEmptyKey, (unsigned long long)key);
+            if (prev == kEmptyKey) {
+                mine = true;
+                return s;
+            }
+            if (prev == key) {
+                mine = false;
+                return s;
+            }
+        }
+        s = (s + 1) & h.mask;
+    }
+}
+
+__global__ void probe_claim_kernel(HashView h, const int32_t* __restrict__ qi, const int32_t* __restrict__ qj,
+                                   uint64_t n, uint32_t* __restrict__ slot, int32_t* __restrict__ ws,
+                                   int32_t* __restrict__ wp, uint32_t* __restrict__ wslot,
+                                   unsigned long long* __restrict__ wcount, uint64_t* counters,
+                                   uint64_t* live) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool mine = false;
+    uint64_t sl = 0;
+    if (e < n) {
+        sl = cache_claim(h, pair_key(qi[e], qj[e]), mine);
+        slot[e] = (uint32_t)sl;
+    }
+    const unsigned ball = __ballot_sync(0xffffffffu, mine);
+    const int lane = threadIdx.x & 31;
+    unsigned long long basei = 0;
+    if (lane == 0 && ball) basei = atomicAdd(wcount, (unsigned long long)__popc(ball));
+    basei = __shfl_sync(0xffffffffu, basei, 0);
+    if (mine) {
+        const uint64_t at = basei + __popc(ball & ((1u << lane) - 1));
+        ws[at] = qi[e];
+        wp[at] = qj[e];
+        wslot[at] = (uint32_t)sl;
+    }
+    const unsigned hitb = __ballot_sync(0xffffffffu, e < n && !mine);
+    if (lane == 0) {
+        if (ball) {
+            atomicAdd((unsigned long long*)&counters[C_MISSES], (unsigned long long)__popc(ball));
+            atomicAdd((unsigned long long*)live, (unsigned long long)__popc(ball));
+        }
+        if (hitb) atomicAdd((unsigned long long*)&counters[C_HITS], (unsigned long long)__popc(hitb));
+    }
+}
+
+__global__ void gather_cache_kernel(const double* __restrict__ vals, const uint32_t* __restrict__ slot,
+                                    uint64_t n, double* __restrict__ out) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) out[e] = vals[slot[e]];
+}
+
+void distance_batch(Context& c, int mode, const int32_t* qi, const int32_t* qj, uint64_t n, double* dist) {
+    if (n == 0) return;
+    if (mode == TABLE || mode == LINE) {
+        ScoreOut out;
+        out.dist = dist;
+        score_entries(c, mode, qi, qj, n, out);
+        return;
+    }
+    cache_reserve(c, n);
+    uint32_t* slot = c.s_c.as<uint32_t>(n);
+    int32_t* ws = c.s_d.as<int32_t>(n);
+    int32_t* wp = c.s_e.as<int32_t>(n);
+    uint32_t* wslot = c.s_f.as<uint32_t>(n);
+    unsigned long long* wcount = c.s_g.as<unsigned long long>(1);
+    NRG_CUDA(cudaMemsetAsync(wcount, 0, 8, c.stream));
+    probe_claim_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(
+        c.Cview(), qi, qj, n, slot, ws, wp, wslot, wcount, c.dcounters(), static_cast<uint64_t*>(c.Ccount.p));
+    NRG_LAUNCH_CHECK();
+    unsigned long long nw = 0;
+    NRG_CUDA(cudaMemcpyAsync(&nw, wcount, 8, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    ScoreOut out;
+    out.cache_vals = c.Cview().vals;
+    out.slot = wslot;
+    score_entries(c, mode, ws, wp, nw, out);
+    gather_cache_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(c.Cview().vals, slot, n, dist);
+    NRG_LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------- scored-pair sample
+__global__ void sample_keys_kernel(const uint64_t* __restrict__ keys, uint64_t cap, uint64_t stride,
+                                   uint64_t seed, uint64_t limit, int32_t* __restrict__ oi,
+                                   int32_t* __restrict__ oj, unsigned long long* __restrict__ cnt) {
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= cap) return;
+    const uint64_t k = keys[s];
+    if (k == kEmptyKey) return;
+    if (mix64(k ^ seed) % stride != 0) return;
+    const unsigned long long at = atomicAdd(cnt, 1ull);
+    if (at < limit) {
+        oi[at] = (int32_t)(k >> 32);
+        oj[at] = (int32_t)(k & 0xffffffffu);
+    }
+}
+
+uint64_t sample_scored_pairs(Context& c, uint64_t cap, uint64_t seed, int32_t* oi, int32_t* oj) {
+    if (!c.Ccap || !cap) return 0;
+    uint64_t live = 0;
+    NRG_CUDA(cudaMemcpyAsync(&live, c.Ccount.p, 8, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    const uint64_t stride = std::max<uint64_t>(1, live / cap);
+    unsigned long long* cnt = c.s_g.as<unsigned long long>(1);
+    NRG_CUDA(cudaMemsetAsync(cnt, 0, 8, c.stream));
+    sample_keys_kernel<<<(unsigned)ceil_div(c.Ccap, 256), 256, 0, c.stream>>>(
+        static_cast<uint64_t*>(c.Ckeys.p), c.Ccap, stride, seed, cap, oi, oj, cnt);
+    NRG_LAUNCH_CHECK();
+    unsigned long long h = 0;
+    NRG_CUDA(cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    return std::min<uint64_t>(h, cap);
+}
+
+// ---------------------------------------------------------------- live optimize_edge / gradient
+__global__ void __launch_bounds__(256) live_opt_kernel(int kind, const uint32_t* __restrict__ Xb,
+                                                       const double* __restrict__ Xd,
+                                                       const double* __restrict__ H,
+                                                       const double* __restrict__ theta, int M, int Mp,
+                                                       int Mw, HashView W, const int32_t* __restrict__ qi,
+                                                       const int32_t* __restrict__ qj, uint64_t n,
+                                                       double lambda, int want_grad, double* __restrict__ w,
+                                                       double* __restrict__ gain, uint8_t* __restrict__ warn,
+                                                       uint64_t* counters) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t e = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (e >= n) return;
+    const int a = min(qi[e], qj[e]), b = max(qi[e], qj[e]);
+    const double wcur = hash_get(W, pair_key(a, b), 0.0);
+    const double sg = wcur > 0.0 ? 1.0 : (wcur < 0.0 ? -1.0 : 0.0);
+    EdgeOptD r;
+    if (kind == ISING) {
+        const TLive T{H, theta, Mp};
+        if (want_grad) {
+            const double g = ising_gradient64(T, Xb, Mw, M, a, b);
+            if (lane == 0) w[e] = g - lambda * sg;
+            return;
+        }
+        r = ising_optimize_edge64(T, Xb, Mw, M, a, b, wcur, lambda);
+    } else {
+        const ULive Uf{Xd, H, theta, Mp};
+        double xxa = 0.0, xxb = 0.0;
+        for (int m = lane; m < M; m += 32) {
+            const double va = Xd[(size_t)a * Mp + m], vb = Xd[(size_t)b * Mp + m];
+            xxa += va * va;
+            xxb += vb * vb;
+        }
+        xxa = warp_sum(xxa);
+        xxb = warp_sum(xxb);
+        const double ta = theta[a], tb = theta[b];
+        const GaussCoef cf = gauss_coef(Uf, Xd, Mp, M, a, b, ta * ta, tb * tb, xxa, xxb);
+        if (want_grad) {
+            if (lane == 0) w[e] = -cf.P - lambda * sg;
+            return;
+        }
+        r = gauss_optimize(cf, wcur, lambda);
+    }
+    if (lane == 0) {
+        if (w) w[e] = r.w;
+        if (gain) gain[e] = r.gain;
+        if (warn) warn[e] = (uint8_t)r.warn;
+        atomicAdd((unsigned long long*)&counters[C_EVALS], (unsigned long long)r.passes);
+        if (r.warn) atomicAdd((unsigned long long*)&counters[C_WARN], 1ull);
+    }
+}
+
+void optimize_edge_live(Context& c, const int32_t* i, const int32_t* j, uint64_t n, double* w,
+                        double* gain, uint8_t* warn) {
+    if (!n) return;
+    live_opt_kernel<<<(unsigned)ceil_div(n * 32, 256), 256, 0, c.stream>>>(
+        c.kind, c.dXb(), c.dXd(), c.dH(), c.dtheta(), c.M, c.Mp, c.Mw, c.Wview(), i, j, n, c.lambda, 0, w,
+        gain, warn, c.dcounters());
+    NRG_LAUNCH_CHECK();
+}
+
+void edge_gradient_live(Context& c, const int32_t* i, const int32_t* j, uint64_t n, double* g) {
+    if (!n) return;
+    live_opt_kernel<<<(unsigned)ceil_div(n * 32, 256), 256, 0, c.stream>>>(
+        c.kind, c.dXb(), c.dXd(), c.dH(), c.dtheta(), c.M, c.Mp, c.Mw, c.Wview(), i, j, n, c.lambda, 1, g,
+        nullptr, nullptr, c.dcounters());
+    NRG_LAUNCH_CHECK();
+}
+
+}  // namespace nrg

@@ -1,0 +1,569 @@
+// state.cu — context lifecycle, samples, SparseWeights on device, the per-generation
+// snapshot (K0) and log_posterior.
+//
+// Reference: inc/sparse_weights.hpp (SparseWeights), inc/model.hpp:133-162
+// (log_posterior), :404-416 (make_empty_state), :36-97 (DistanceCache).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "context.cuh"
+
+namespace nrg {
+
+Context::~Context() {
+    if (device >= 0) cudaSetDevice(device);
+    for (DevBuf* b : {&Xb, &Xd, &H, &theta, &Wkeys, &Wvals, &Wcount, &T32, &T64, &Tabs, &U, &xx,
+                      &Ckeys, &Cvals, &Ccount, &table, &line, &counters, &s_a, &s_b, &s_c, &s_d,
+                      &s_e, &s_f, &s_g, &s_h, &s_i, &s_j, &s_k, &s_l, &s_m, &s_n, &s_o, &red})
+        b->release();
+    if (ev0) cudaEventDestroy(ev0);
+    if (ev1) cudaEventDestroy(ev1);
+    if (kev0) cudaEventDestroy(kev0);
+    if (kev1) cudaEventDestroy(kev1);
+    if (stream) cudaStreamDestroy(stream);
+}
+
+static uint64_t next_pow2(uint64_t v) {
+    uint64_t c = 1;
+    while (c < v) c <<= 1;
+    return c;
+}
+
+void ctx_init(Context& c, int n, int m, int kind, double lambda, int device) {
+    if (n < 1 || m < 0) fail(22, "SampleMatrix: bad dimensions");
+    if (!(lambda >= 0.0)) fail(22, "lambda must be >= 0");
+    if (kind != ISING && kind != GAUSSIAN) fail(22, "unknown model kind");
+    c.n = n;
+    c.M = m;
+    c.kind = kind;
+    c.lambda = lambda;
+    c.device = device;
+    NRG_CUDA(cudaSetDevice(device));
+    NRG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    NRG_CUDA(cudaEventCreate(&c.ev0));
+    NRG_CUDA(cudaEventCreate(&c.ev1));
+    NRG_CUDA(cudaEventCreate(&c.kev0));
+    NRG_CUDA(cudaEventCreate(&c.kev1));
+    // Mp = 128 * MQ with MQ one of the instantiated register widths of the fused
+    // Ising screen (score.cu); beyond 2048 samples plain 128-multiples (fp64 path)
+    {
+        int mq = (int)std::max<int64_t>(1, ceil_div(m, 128));
+        if (mq > 8 && mq <= 16) mq = (mq + 1) / 2 * 2;
+        c.Mp = 128 * mq;
+    }
+    c.Mw = c.Mp / 32;
+    const size_t nm = (size_t)n * c.Mp;
+    c.H.ensure(nm * sizeof(double));
+    NRG_CUDA(cudaMemsetAsync(c.H.p, 0, nm * sizeof(double), c.stream));
+    c.theta.ensure(n * sizeof(double));
+    NRG_CUDA(cudaMemsetAsync(c.theta.p, 0, n * sizeof(double), c.stream));
+    c.counters.ensure(C_N * sizeof(uint64_t));
+    NRG_CUDA(cudaMemsetAsync(c.counters.p, 0, C_N * sizeof(uint64_t), c.stream));
+    c.Wcap = 1u << 16;
+    c.Wkeys.ensure(c.Wcap * 8);
+    c.Wvals.ensure(c.Wcap * 8);
+    c.Wcount.ensure(16);
+    NRG_CUDA(cudaMemsetAsync(c.Wkeys.p, 0xff, c.Wcap * 8, c.stream));
+    NRG_CUDA(cudaMemsetAsync(c.Wcount.p, 0, 16, c.stream));
+    c.Ccount.ensure(8);
+    c.sync();
+}
+
+// ---------------------------------------------------------------- samples
+__global__ void pack_spins_f64_kernel(const double* __restrict__ X, int rows, int M, int Mw,
+                                      uint32_t* __restrict__ Xb, int* __restrict__ bad) {
+    // one warp per (row, 32-sample word)
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t total = (int64_t)rows * Mw;
+    if (wid >= total) return;
+    const int r = (int)(wid / Mw), w = (int)(wid % Mw);
+    const int m = w * 32 + lane;
+    bool bit = false;
+    if (m < M) {
+        const double v = X[(size_t)r * M + m];
+        if (v != 1.0 && v != -1.0) atomicExch(bad, 1);
+        bit = v > 0.0;
+    }
+    const uint32_t word = __ballot_sync(0xffffffffu, bit);
+    if (lane == 0) Xb[(size_t)r * Mw + w] = word;
+}
+
+__global__ void pack_spins_i8_kernel(const int8_t* __restrict__ X, int rows, int M, int Mw,
+                                     uint32_t* __restrict__ Xb, int* __restrict__ bad) {
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t total = (int64_t)rows * Mw;
+    if (wid >= total) return;
+    const int r = (int)(wid / Mw), w = (int)(wid % Mw);
+    const int m = w * 32 + lane;
+    bool bit = false;
+    if (m < M) {
+        const int v = X[(size_t)r * M + m];
+        if (v != 1 && v != -1) atomicExch(bad, 1);
+        bit = v > 0;
+    }
+    const uint32_t word = __ballot_sync(0xffffffffu, bit);
+    if (lane == 0) Xb[(size_t)r * Mw + w] = word;
+}
+
+__global__ void gauss_theta_rms_kernel(const double* __restrict__ X, int M, int Mp,
+                                       double* __restrict__ theta, int* __restrict__ bad) {
+    // make_empty_state (inc/model.hpp:404-416): theta = max(rms, 1e-8); block per row
+    const int r = blockIdx.x;
+    double a = 0.0;
+    for (int m = threadIdx.x; m < M; m += blockDim.x) {
+        const double v = X[(size_t)r * Mp + m];
+        if (!isfinite(v)) atomicExch(bad, 1);
+        a += v * v;
+    }
+    __shared__ double sh[32];
+    a = warp_sum(a);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) {
+            const double rms = M > 0 ? sqrt(v / M) : 1.0;
+            theta[r] = fmax(rms, 1e-8);
+        }
+    }
+}
+
+static void reset_state(Context& c) {
+    const size_t nm = (size_t)c.n * c.Mp;
+    NRG_CUDA(cudaMemsetAsync(c.H.p, 0, nm * sizeof(double), c.stream));
+    NRG_CUDA(cudaMemsetAsync(c.theta.p, 0, c.n * sizeof(double), c.stream));
+    NRG_CUDA(cudaMemsetAsync(c.Wkeys.p, 0xff, c.Wcap * 8, c.stream));
+    NRG_CUDA(cudaMemsetAsync(c.Wcount.p, 0, 16, c.stream));
+    c.state_version++;
+    c.base_valid = false;
+}
+
+void upload_samples_f64(Context& c, const double* X) {
+    DevBuf& tmp = c.s_a;
+    int* bad = c.s_b.as<int>(1);
+    NRG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c.stream));
+    if (c.kind == ISING) {
+        c.Xb.ensure((size_t)c.n * c.Mw * 4);
+        // chunked upload: rows per chunk bounded to ~256 MB of doubles
+        const int rows_per = std::max<int>(1, (int)std::min<int64_t>(c.n, (256ll << 20) / (8ll * std::max(1, c.M))));
+        double* d = tmp.as<double>((size_t)rows_per * std::max(1, c.M));
+        for (int r0 = 0; r0 < c.n; r0 += rows_per) {
+            const int rows = std::min(rows_per, c.n - r0);
+            NRG_CUDA(cudaMemcpyAsync(d, X + (size_t)r0 * c.M, (size_t)rows * c.M * 8,
+                                     cudaMemcpyHostToDevice, c.stream));
+            const int64_t warps = (int64_t)rows * c.Mw;
+            pack_spins_f64_kernel<<<(unsigned)ceil_div(warps * 32, 256), 256, 0, c.stream>>>(
+                d, rows, c.M, c.Mw, c.dXb() + (size_t)r0 * c.Mw, bad);
+            NRG_LAUNCH_CHECK();
+        }
+    } else {
+        c.Xd.ensure((size_t)c.n * c.Mp * 8);
+        NRG_CUDA(cudaMemsetAsync(c.Xd.p, 0, (size_t)c.n * c.Mp * 8, c.stream));
+        if (c.M > 0)
+            NRG_CUDA(cudaMemcpy2DAsync(c.Xd.p, (size_t)c.Mp * 8, X, (size_t)c.M * 8, (size_t)c.M * 8,
+                                       c.n, cudaMemcpyHostToDevice, c.stream));
+    }
+    reset_state(c);
+    if (c.kind == GAUSSIAN) {
+        gauss_theta_rms_kernel<<<c.n, 256, 0, c.stream>>>(c.dXd(), c.M, c.Mp, c.dtheta(), bad);
+        NRG_LAUNCH_CHECK();
+    }
+    int hbad = 0;
+    NRG_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (hbad) {
+        c.have_samples = false;
+        fail(22, c.kind == ISING ? "ising model requires +/-1 data" : "gaussian samples must be finite");
+    }
+    c.have_samples = true;
+}
+
+void upload_spins_i8(Context& c, const int8_t* X) {
+    if (c.kind != ISING) fail(22, "int8 spins are only valid for the ising model");
+    int* bad = c.s_b.as<int>(1);
+    NRG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), c.stream));
+    c.Xb.ensure((size_t)c.n * c.Mw * 4);
+    const int rows_per = std::max<int>(1, (int)std::min<int64_t>(c.n, (256ll << 20) / std::max(1, c.M)));
+    int8_t* d = c.s_a.as<int8_t>((size_t)rows_per * std::max(1, c.M));
+    for (int r0 = 0; r0 < c.n; r0 += rows_per) {
+        const int rows = std::min(rows_per, c.n - r0);
+        NRG_CUDA(cudaMemcpyAsync(d, X + (size_t)r0 * c.M, (size_t)rows * c.M, cudaMemcpyHostToDevice,
+                                 c.stream));
+        const int64_t warps = (int64_t)rows * c.Mw;
+        pack_spins_i8_kernel<<<(unsigned)ceil_div(warps * 32, 256), 256, 0, c.stream>>>(
+            d, rows, c.M, c.Mw, c.dXb() + (size_t)r0 * c.Mw, bad);
+        NRG_LAUNCH_CHECK();
+    }
+    reset_state(c);
+    int hbad = 0;
+    NRG_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (hbad) {
+        c.have_samples = false;
+        fail(22, "ising model requires +/-1 data");
+    }
+    c.have_samples = true;
+}
+
+void reset_state_empty(Context& c) {
+    if (!c.have_samples) fail(22, "no samples uploaded");
+    reset_state(c);
+    if (c.kind == GAUSSIAN) {
+        int* bad = c.s_b.as<int>(1);
+        gauss_theta_rms_kernel<<<c.n, 256, 0, c.stream>>>(c.dXd(), c.M, c.Mp, c.dtheta(), bad);
+        NRG_LAUNCH_CHECK();
+    }
+    begin_generation(c);
+    c.sync();
+}
+
+void set_theta(Context& c, const double* th) {
+    if (c.kind == GAUSSIAN)
+        for (int i = 0; i < c.n; ++i)
+            if (!(th[i] > 0.0)) fail(22, "gaussian model requires theta > 0");
+    NRG_CUDA(cudaMemcpyAsync(c.theta.p, th, c.n * 8, cudaMemcpyHostToDevice, c.stream));
+    c.sync();
+    c.state_version++;
+}
+
+// ---------------------------------------------------------------- W hash
+__global__ void w_rehash_kernel(const uint64_t* __restrict__ ok, const double* __restrict__ ov,
+                                uint64_t ocap, HashView nw, unsigned long long* used) {
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= ocap) return;
+    const uint64_t k = ok[s];
+    if (k >= kTombKey) return;
+    uint64_t t = mix64(k) & nw.mask;
+    for (;;) {
+        const unsigned long long prev =
+            atomicCAS((unsigned long long*)&nw.keys[t], (unsigned long long)kEmptyKey, (unsigned long long)k);
+        if (prev == kEmptyKey) {
+            nw.vals[t] = ov[s];
+            atomicAdd(used, 1ull);
+            return;
+        }
+        t = (t + 1) & nw.mask;
+    }
+}
+
+// make room for `extra` new inserts (load factor <= 1/2, counting tombstones)
+void w_reserve(Context& c, uint64_t extra) {
+    uint64_t cnt[2];
+    NRG_CUDA(cudaMemcpyAsync(cnt, c.Wcount.p, 16, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    const uint64_t live = cnt[0], used = cnt[1];
+    if ((used + extra) * 2 <= c.Wcap) return;
+    const uint64_t ncap = std::max<uint64_t>(1u << 16, next_pow2(4 * (live + extra)));
+    DevBuf nk, nv;
+    nk.ensure(ncap * 8);
+    nv.ensure(ncap * 8);
+    NRG_CUDA(cudaMemsetAsync(nk.p, 0xff, ncap * 8, c.stream));
+    uint64_t* dcnt = static_cast<uint64_t*>(c.Wcount.p);
+    NRG_CUDA(cudaMemsetAsync(dcnt + 1, 0, 8, c.stream));
+    HashView nw{static_cast<uint64_t*>(nk.p), static_cast<double*>(nv.p), ncap - 1};
+    w_rehash_kernel<<<(unsigned)ceil_div(c.Wcap, 256), 256, 0, c.stream>>>(
+        static_cast<uint64_t*>(c.Wkeys.p), static_cast<double*>(c.Wvals.p), c.Wcap, nw,
+        (unsigned long long*)(dcnt + 1));
+    NRG_LAUNCH_CHECK();
+    c.sync();
+    c.Wkeys.release();
+    c.Wvals.release();
+    c.Wkeys = nk;
+    c.Wvals = nv;
+    nk.p = nv.p = nullptr;
+    c.Wcap = ncap;
+}
+
+void get_state(Context& c, double* theta, uint64_t cap, int32_t* ei, int32_t* ej, double* w,
+               uint64_t* n_edges) {
+    std::vector<uint64_t> keys(c.Wcap);
+    std::vector<double> vals(c.Wcap);
+    NRG_CUDA(cudaMemcpyAsync(keys.data(), c.Wkeys.p, c.Wcap * 8, cudaMemcpyDeviceToHost, c.stream));
+    NRG_CUDA(cudaMemcpyAsync(vals.data(), c.Wvals.p, c.Wcap * 8, cudaMemcpyDeviceToHost, c.stream));
+    if (theta) NRG_CUDA(cudaMemcpyAsync(theta, c.theta.p, c.n * 8, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    std::vector<std::pair<uint64_t, double>> e;
+    for (uint64_t s = 0; s < c.Wcap; ++s)
+        if (keys[s] < kTombKey) e.emplace_back(keys[s], vals[s]);
+    std::sort(e.begin(), e.end());  // pair_key order == (i, j) order
+    *n_edges = e.size();
+    for (uint64_t t = 0; t < e.size() && t < cap; ++t) {
+        if (ei) ei[t] = (int32_t)(e[t].first >> 32);
+        if (ej) ej[t] = (int32_t)(e[t].first & 0xffffffffu);
+        if (w) w[t] = e[t].second;
+    }
+}
+
+void get_sums(Context& c, double* out) {
+    if (c.M > 0)
+        NRG_CUDA(cudaMemcpy2DAsync(out, (size_t)c.M * 8, c.H.p, (size_t)c.Mp * 8, (size_t)c.M * 8, c.n,
+                                   cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+}
+
+// ---------------------------------------------------------------- snapshot (K0)
+// Ising: T = tanh(H + theta) per node-sample, fp64 master + fp32 copy for the
+// bandwidth-bound screen, with sum|T32| per node for its rigorous error bound.
+__global__ void snapshot_ising_kernel(const double* __restrict__ H, const double* __restrict__ theta,
+                                      int M, int Mp, double* __restrict__ T64, float* __restrict__ T32,
+                                      float* __restrict__ Tabs) {
+    const int r = blockIdx.x;
+    const double th = theta[r];
+    double a = 0.0;
+    for (int m = threadIdx.x; m < Mp; m += blockDim.x) {
+        double t = 0.0;
+        if (m < M) t = tanh(H[(size_t)r * Mp + m] + th);
+        T64[(size_t)r * Mp + m] = t;
+        const float f = (float)t;
+        T32[(size_t)r * Mp + m] = f;
+        a += fabs((double)f);
+    }
+    __shared__ double sh[32];
+    a = warp_sum(a);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) Tabs[r] = __double2float_ru(v * (1.0 + 1e-12));
+    }
+}
+
+// Gaussian: U = X + theta^2 H (the current residual), xx = sum x^2
+__global__ void snapshot_gauss_kernel(const double* __restrict__ X, const double* __restrict__ H,
+                                      const double* __restrict__ theta, int M, int Mp,
+                                      double* __restrict__ U, double* __restrict__ xx) {
+    const int r = blockIdx.x;
+    const double t2 = theta[r] * theta[r];
+    double a = 0.0;
+    for (int m = threadIdx.x; m < Mp; m += blockDim.x) {
+        const double x = X[(size_t)r * Mp + m];
+        U[(size_t)r * Mp + m] = m < M ? x + t2 * H[(size_t)r * Mp + m] : 0.0;
+        a += x * x;
+    }
+    __shared__ double sh[32];
+    a = warp_sum(a);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+        v = warp_sum(v);
+        if (threadIdx.x == 0) xx[r] = v;
+    }
+}
+
+void ensure_snapshot(Context& c) {
+    if (!c.have_samples) fail(22, "no samples uploaded");
+    if (c.snap_version == c.state_version) return;
+    c.tic();
+    const size_t nm = (size_t)c.n * c.Mp;
+    if (c.kind == ISING) {
+        c.T64.ensure(nm * 8);
+        c.T32.ensure(nm * 4);
+        c.Tabs.ensure((size_t)c.n * 4);
+        snapshot_ising_kernel<<<c.n, 256, 0, c.stream>>>(c.dH(), c.dtheta(), c.M, c.Mp,
+                                                         static_cast<double*>(c.T64.p),
+                                                         static_cast<float*>(c.T32.p),
+                                                         static_cast<float*>(c.Tabs.p));
+    } else {
+        c.U.ensure(nm * 8);
+        c.xx.ensure((size_t)c.n * 8);
+        snapshot_gauss_kernel<<<c.n, 256, 0, c.stream>>>(c.dXd(), c.dH(), c.dtheta(), c.M, c.Mp,
+                                                         static_cast<double*>(c.U.p),
+                                                         static_cast<double*>(c.xx.p));
+    }
+    NRG_LAUNCH_CHECK();
+    c.toc(P_SNAP);
+    c.snap_version = c.state_version;
+}
+
+// ---------------------------------------------------------------- log_posterior
+__device__ __forceinline__ double log_2cosh(double z) {  // inc/common.hpp:40-43
+    const double a = fabs(z);
+    return a + log1p(exp(-2.0 * a));
+}
+
+template <int BLOCK>
+__device__ double block_sum(double v, double* sh) {
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x < 32) {
+        r = threadIdx.x < BLOCK / 32 ? sh[threadIdx.x] : 0.0;
+        r = warp_sum(r);
+    }
+    __syncthreads();
+    return r;  // valid in thread 0
+}
+
+__global__ void __launch_bounds__(256) logpost_node_kernel(int kind, const uint32_t* __restrict__ Xb,
+                                                           const double* __restrict__ Xd,
+                                                           const double* __restrict__ H,
+                                                           const double* __restrict__ theta, int M,
+                                                           int Mp, int Mw, double* __restrict__ out) {
+    __shared__ double sh[32];
+    const int r = blockIdx.x;
+    const double th = theta[r];
+    double a = 0.0;
+    if (kind == ISING) {
+        for (int m = threadIdx.x; m < M; m += 256) {
+            const double z = H[(size_t)r * Mp + m] + th;
+            const double x = (Xb[(size_t)r * Mw + (m >> 5)] >> (m & 31)) & 1u ? 1.0 : -1.0;
+            a += x * z - log_2cosh(z);
+        }
+        a = block_sum<256>(a, sh);
+        if (threadIdx.x == 0) out[r] = a;
+    } else {
+        const double t2 = th * th;
+        for (int m = threadIdx.x; m < M; m += 256) {
+            const double rr = Xd[(size_t)r * Mp + m] + t2 * H[(size_t)r * Mp + m];
+            a += rr * rr;
+        }
+        a = block_sum<256>(a, sh);
+        if (threadIdx.x == 0) out[r] = -a / (2.0 * t2) - M * log(th);
+    }
+}
+
+__global__ void __launch_bounds__(1024) reduce_fixed_kernel(const double* __restrict__ v, uint64_t n,
+                                                            double* __restrict__ out) {
+    __shared__ double sh[32];
+    double a = 0.0;
+    for (uint64_t t = threadIdx.x; t < n; t += 1024) a += v[t];
+    a = block_sum<1024>(a, sh);
+    if (threadIdx.x == 0) *out = a;
+}
+
+__global__ void __launch_bounds__(256) w_abs_partial_kernel(const uint64_t* __restrict__ keys,
+                                                            const double* __restrict__ vals,
+                                                            uint64_t cap, double* __restrict__ part) {
+    __shared__ double sh[32];
+    double a = 0.0;
+    for (uint64_t s = (uint64_t)blockIdx.x * 256 + threadIdx.x; s < cap; s += (uint64_t)gridDim.x * 256)
+        if (keys[s] < kTombKey) a += fabs(vals[s]);
+    a = block_sum<256>(a, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = a;
+}
+
+double log_posterior(Context& c) {
+    if (!c.have_samples) fail(22, "no samples uploaded");
+    c.tic();
+    double* part = c.red.as<double>((size_t)c.n + 1024 + 8);
+    double* res = part + c.n + 1024;
+    logpost_node_kernel<<<c.n, 256, 0, c.stream>>>(c.kind, c.dXb(), c.dXd(), c.dH(), c.dtheta(), c.M,
+                                                   c.Mp, c.Mw, part);
+    NRG_LAUNCH_CHECK();
+    reduce_fixed_kernel<<<1, 1024, 0, c.stream>>>(part, c.n, res);
+    NRG_LAUNCH_CHECK();
+    const int nb = 592;
+    w_abs_partial_kernel<<<nb, 256, 0, c.stream>>>(static_cast<uint64_t*>(c.Wkeys.p),
+                                                   static_cast<double*>(c.Wvals.p), c.Wcap, part + c.n);
+    reduce_fixed_kernel<<<1, 1024, 0, c.stream>>>(part + c.n, nb, res + 1);
+    NRG_LAUNCH_CHECK_N(2);
+    double h[2];
+    NRG_CUDA(cudaMemcpyAsync(h, res, 16, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    c.toc(P_LOGPOST);
+    const double acc = h[0] - c.lambda * h[1];
+    if (!std::isfinite(acc)) fail(75, "log_posterior is not finite");
+    return acc;
+}
+
+// DistanceCache::base (inc/model.hpp:73-81): once per generation
+double generation_base(Context& c) {
+    if (!c.base_valid) {
+        c.base = log_posterior(c);
+        c.base_valid = true;
+    }
+    return c.base;
+}
+
+// ---------------------------------------------------------------- distance cache
+__global__ void cache_rehash_kernel(const uint64_t* __restrict__ ok, const double* __restrict__ ov,
+                                    uint64_t ocap, HashView nw) {
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= ocap) return;
+    const uint64_t k = ok[s];
+    if (k == kEmptyKey) return;
+    uint64_t t = mix64(k) & nw.mask;
+    for (;;) {
+        const unsigned long long prev =
+            atomicCAS((unsigned long long*)&nw.keys[t], (unsigned long long)kEmptyKey, (unsigned long long)k);
+        if (prev == kEmptyKey) {
+            nw.vals[t] = ov[s];
+            return;
+        }
+        t = (t + 1) & nw.mask;
+    }
+}
+
+void cache_reserve(Context& c, uint64_t extra) {
+    uint64_t live = 0;
+    if (c.Ccap) {
+        NRG_CUDA(cudaMemcpyAsync(&live, c.Ccount.p, 8, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+    }
+    c.cache_live_host = live;
+    if (c.Ccap && (live + extra) * 10 <= c.Ccap * 6) return;  // load factor <= 0.6
+    const uint64_t ncap = std::max<uint64_t>(1u << 20, next_pow2(2 * (live + extra)));
+    if (ncap > (1ull << 32)) fail(100, "distance cache would exceed 2^32 slots");
+    DevBuf nk, nv;
+    nk.ensure(ncap * 8);
+    nv.ensure(ncap * 8);
+    NRG_CUDA(cudaMemsetAsync(nk.p, 0xff, ncap * 8, c.stream));
+    HashView nw{static_cast<uint64_t*>(nk.p), static_cast<double*>(nv.p), ncap - 1};
+    if (c.Ccap && live) {
+        cache_rehash_kernel<<<(unsigned)ceil_div(c.Ccap, 256), 256, 0, c.stream>>>(
+            static_cast<uint64_t*>(c.Ckeys.p), static_cast<double*>(c.Cvals.p), c.Ccap, nw);
+        NRG_LAUNCH_CHECK();
+    }
+    if (!c.Ccap) NRG_CUDA(cudaMemsetAsync(c.Ccount.p, 0, 8, c.stream));
+    c.sync();
+    c.Ckeys.release();
+    c.Cvals.release();
+    c.Ckeys = nk;
+    c.Cvals = nv;
+    nk.p = nv.p = nullptr;
+    c.Ccap = ncap;
+}
+
+void begin_generation(Context& c) {
+    if (c.Ccap) {
+        NRG_CUDA(cudaMemsetAsync(c.Ckeys.p, 0xff, c.Ccap * 8, c.stream));
+        NRG_CUDA(cudaMemsetAsync(c.Ccount.p, 0, 8, c.stream));
+    }
+    c.cache_live_host = 0;
+    c.base_valid = false;
+}
+
+void counters_add_host(Context& c, int which, uint64_t v) {
+    uint64_t h = 0;
+    uint64_t* d = c.dcounters() + which;
+    NRG_CUDA(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    h += v;
+    NRG_CUDA(cudaMemcpyAsync(d, &h, 8, cudaMemcpyHostToDevice, c.stream));
+    c.sync();
+}
+
+void set_table(Context& c, uint64_t n, const double* t) {
+    if (n > (uint64_t)c.n) fail(22, "table larger than the node count");
+    c.table.ensure(n * n * 8);
+    NRG_CUDA(cudaMemcpyAsync(c.table.p, t, n * n * 8, cudaMemcpyHostToDevice, c.stream));
+    c.sync();
+    c.table_n = n;
+}
+
+void set_line(Context& c, uint64_t n, const double* pos) {
+    c.line.ensure(n * 8);
+    NRG_CUDA(cudaMemcpyAsync(c.line.p, pos, n * 8, cudaMemcpyHostToDevice, c.stream));
+    c.sync();
+    c.line_n = n;
+}
+
+}  // namespace nrg

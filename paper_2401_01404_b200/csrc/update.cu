@@ -1,0 +1,383 @@
+// update.cu — coordinate updates on the device.
+//
+// apply_updates: detail::apply_edge_updates with the sequential semantics
+// (inc/reconstruct.hpp:74-82): candidates in list order, each re-optimised against
+// the CURRENT sums, then set_edge (inc/sparse_weights.hpp:54-85).  Pair p only
+// depends on the latest earlier pair sharing an endpoint, so a persistent kernel
+// takes pairs in list order (atomic ticket), waits for those two predecessors and
+// runs node-disjoint pairs concurrently — the wavefront schedule without per-level
+// launches.  The result equals the sequential loop pair by pair.
+//
+// theta_pass: detail::theta_pass (inc/reconstruct.hpp:129-138) with optimize_theta
+// (inc/model.hpp:222-268): Ising by safeguarded Newton on the concave per-node
+// objective over [-20, 20] (boundary optima returned exactly, as golden_max's
+// best-evaluated-point rule does); Gaussian in closed form with the reference's
+// 1e-8 clamp and warnings.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "pairscore.cuh"
+
+namespace nrg {
+
+__global__ void dep_keys_kernel(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj, uint64_t n,
+                                uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    keys[2 * p] = ((uint64_t)(uint32_t)ci[p] << 32) | (uint32_t)p;
+    keys[2 * p + 1] = ((uint64_t)(uint32_t)cj[p] << 32) | (uint32_t)p;
+    vals[2 * p] = (uint32_t)(2 * p);
+    vals[2 * p + 1] = (uint32_t)(2 * p + 1);
+}
+__global__ void dep_link_kernel(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t m,
+                                int32_t* __restrict__ dep) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m) return;
+    int32_t prev = -1;
+    if (t > 0 && (keys[t] >> 32) == (keys[t - 1] >> 32)) prev = (int32_t)(keys[t - 1] & 0xffffffffu);
+    dep[vals[t]] = prev;  // dep[2p + side] = previous pair index on that endpoint
+}
+
+// coherent (L2) hash lookup for the update kernel
+__device__ __forceinline__ double hash_get_cg(const HashView h, uint64_t key) {
+    uint64_t s = mix64(key) & h.mask;
+    for (;;) {
+        const uint64_t k = __ldcg(&h.keys[s]);
+        if (k == key) return __ldcg(&h.vals[s]);
+        if (k == kEmptyKey) return 0.0;
+        s = (s + 1) & h.mask;
+    }
+}
+// set W[key] = w: update in place, tombstone on zero, insert into the first empty
+// slot otherwise (tombstones are never reused while the table is shared)
+__device__ __forceinline__ void hash_set(HashView h, uint64_t key, double w, unsigned long long* cnt) {
+    uint64_t s = mix64(key) & h.mask;
+    for (;;) {
+        const uint64_t k = __ldcg(&h.keys[s]);
+        if (k == key) {
+            if (w == 0.0) {
+                __stcg(&h.keys[s], kTombKey);
+                atomicAdd(&cnt[0], (unsigned long long)-1ll);
+            } else {
+                __stcg(&h.vals[s], w);
+            }
+            return;
+        }
+        if (k == kEmptyKey) {
+            if (w == 0.0) return;  // absent and zero: nothing stored
+            __stcg(&h.vals[s], w);  // value first; the slot is invisible until the key lands
+            __threadfence();
+            const unsigned long long prev =
+                atomicCAS((unsigned long long*)&h.keys[s], (unsigned long long)kEmptyKey, (unsigned long long)key);
+            if (prev == kEmptyKey) {
+                atomicAdd(&cnt[0], 1ull);
+                atomicAdd(&cnt[1], 1ull);
+                return;
+            }
+            continue;  // lost the slot to another key: re-examine it
+        }
+        s = (s + 1) & h.mask;
+    }
+}
+
+struct UpdateArgs {
+    int kind;
+    const uint32_t* Xb;
+    const double* Xd;
+    double* H;
+    const double* theta;
+    int M, Mp, Mw;
+    HashView W;
+    unsigned long long* Wcnt;
+    const int32_t* ci;
+    const int32_t* cj;
+    const double* assign;
+    const int32_t* dep;
+    uint64_t n;
+    double lambda;
+    int* done;
+    unsigned long long* ticket;
+    double* absdelta;
+    uint64_t* counters;
+};
+
+__global__ void __launch_bounds__(128) update_kernel(UpdateArgs A) {
+    const int lane = threadIdx.x & 31;
+    uint64_t evals = 0, warns = 0;
+    for (;;) {
+        unsigned long long p = 0;
+        if (lane == 0) p = atomicAdd(A.ticket, 1ull);
+        p = __shfl_sync(0xffffffffu, p, 0);
+        if (p >= A.n) break;
+        // wait for the predecessors on both endpoints
+        if (lane == 0) {
+            const int d0 = A.dep[2 * p], d1 = A.dep[2 * p + 1];
+            if (d0 >= 0)
+                while (atomicAdd(&A.done[d0], 0) == 0) __nanosleep(64);
+            if (d1 >= 0)
+                while (atomicAdd(&A.done[d1], 0) == 0) __nanosleep(64);
+        }
+        __syncwarp();
+        __threadfence();
+        const int i0 = A.ci[p], j0 = A.cj[p];
+        const int a = min(i0, j0), b = max(i0, j0);
+        const uint64_t key = pair_key(a, b);
+        const double wcur = hash_get_cg(A.W, key);
+        double w;
+        if (A.assign) {
+            w = A.assign[p];
+        } else if (A.kind == ISING) {
+            const TLive T{A.H, A.theta, A.Mp};
+            const EdgeOptD r = ising_optimize_edge64(T, A.Xb, A.Mw, A.M, a, b, wcur, A.lambda);
+            w = r.w;
+            evals += r.passes;
+            warns += r.warn;
+        } else {
+            const ULive Uf{A.Xd, A.H, A.theta, A.Mp};
+            double xxa = 0.0, xxb = 0.0;
+            for (int m = lane; m < A.M; m += 32) {
+                const double va = A.Xd[(size_t)a * A.Mp + m], vb = A.Xd[(size_t)b * A.Mp + m];
+                xxa += va * va;
+                xxb += vb * vb;
+            }
+            xxa = warp_sum(xxa);
+            xxb = warp_sum(xxb);
+            const double ta = __ldcg(&A.theta[a]), tb = __ldcg(&A.theta[b]);
+            const GaussCoef cf = gauss_coef(Uf, A.Xd, A.Mp, A.M, a, b, ta * ta, tb * tb, xxa, xxb);
+            const EdgeOptD r = gauss_optimize(cf, wcur, A.lambda);
+            w = r.w;
+            evals += r.passes;
+        }
+        // Delta accumulation and set_edge (inc/reconstruct.hpp:78-79)
+        const double delta = w - wcur;
+        if (lane == 0) A.absdelta[p] = fabs(w - wcur);
+        if (delta != 0.0) {
+            double* Ha = A.H + (size_t)a * A.Mp;
+            double* Hb = A.H + (size_t)b * A.Mp;
+            if (A.kind == ISING) {
+                for (int k = 0; k * 32 < A.M; ++k) {
+                    const int m = lane + 32 * k;
+                    if (m < A.M) {
+                        const uint32_t wa = A.Xb[(size_t)a * A.Mw + k], wb = A.Xb[(size_t)b * A.Mw + k];
+                        const double xa = xsign(wa, lane), xb = xsign(wb, lane);
+                        __stcg(&Ha[m], __ldcg(&Ha[m]) + delta * xb);
+                        __stcg(&Hb[m], __ldcg(&Hb[m]) + delta * xa);
+                    }
+                }
+            } else {
+                for (int m = lane; m < A.M; m += 32) {
+                    const double xa = A.Xd[(size_t)a * A.Mp + m], xb = A.Xd[(size_t)b * A.Mp + m];
+                    __stcg(&Ha[m], __dadd_rn(__ldcg(&Ha[m]), __dmul_rn(delta, xb)));
+                    __stcg(&Hb[m], __dadd_rn(__ldcg(&Hb[m]), __dmul_rn(delta, xa)));
+                }
+            }
+        }
+        if (lane == 0 && (delta != 0.0 || w == 0.0)) hash_set(A.W, key, w, A.Wcnt);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicExch(&A.done[p], 1);
+    }
+    if (lane == 0) {
+        if (evals) atomicAdd((unsigned long long*)&A.counters[C_EVALS], (unsigned long long)evals);
+        if (warns) atomicAdd((unsigned long long*)&A.counters[C_WARN], (unsigned long long)warns);
+    }
+}
+
+__global__ void __launch_bounds__(1024) sum_fixed_kernel(const double* __restrict__ v, uint64_t n,
+                                                         double* __restrict__ out) {
+    __shared__ double sh[32];
+    double a = 0.0;
+    // contiguous slices per thread, then a fixed tree: deterministic
+    const uint64_t per = (n + 1023) / 1024;
+    const uint64_t lo = threadIdx.x * per, hi = min(n, lo + per);
+    for (uint64_t t = lo; t < hi; ++t) a += v[t];
+    a = warp_sum(a);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double r = sh[threadIdx.x];
+        r = warp_sum(r);
+        if (threadIdx.x == 0) *out = r;
+    }
+}
+
+static int update_grid(Context& c) {
+    static int blocks = 0;
+    if (!blocks) {
+        int sms = 0, per = 0;
+        NRG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+        NRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, update_kernel, 128, 0));
+        blocks = sms * std::max(1, per);
+    }
+    return blocks;
+}
+
+double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n, const double* assign) {
+    if (n == 0) return 0.0;
+    if (n >= (1ull << 31)) fail(22, "apply_updates: too many candidates");
+    c.tic();
+    w_reserve(c, n);
+    DevBuf kb, vb, k2b, v2b, depb, doneb, tb, adb, tmpb, sb;
+    uint64_t* keys = kb.as<uint64_t>(2 * n);
+    uint32_t* vals = vb.as<uint32_t>(2 * n);
+    uint64_t* keys2 = k2b.as<uint64_t>(2 * n);
+    uint32_t* vals2 = v2b.as<uint32_t>(2 * n);
+    int32_t* dep = depb.as<int32_t>(2 * n);
+    int* done = doneb.as<int>(n);
+    unsigned long long* ticket = tb.as<unsigned long long>(1);
+    double* absdelta = adb.as<double>(n);
+    dep_keys_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(ci, cj, n, keys, vals);
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, keys2, vals, vals2, (int64_t)(2 * n), 0, 64, c.stream);
+    void* tmp = tmpb.ensure(bytes);
+    cub::DeviceRadixSort::SortPairs(tmp, bytes, keys, keys2, vals, vals2, (int64_t)(2 * n), 0, 64, c.stream);
+    dep_link_kernel<<<(unsigned)ceil_div(2 * n, 256), 256, 0, c.stream>>>(keys2, vals2, 2 * n, dep);
+    NRG_CUDA(cudaMemsetAsync(done, 0, n * 4, c.stream));
+    NRG_CUDA(cudaMemsetAsync(ticket, 0, 8, c.stream));
+    NRG_LAUNCH_CHECK();
+    UpdateArgs A;
+    A.kind = c.kind;
+    A.Xb = c.dXb();
+    A.Xd = c.dXd();
+    A.H = c.dH();
+    A.theta = c.dtheta();
+    A.M = c.M;
+    A.Mp = c.Mp;
+    A.Mw = c.Mw;
+    A.W = c.Wview();
+    A.Wcnt = static_cast<unsigned long long*>(c.Wcount.p);
+    A.ci = ci;
+    A.cj = cj;
+    A.assign = assign;
+    A.dep = dep;
+    A.n = n;
+    A.lambda = c.lambda;
+    A.done = done;
+    A.ticket = ticket;
+    A.absdelta = absdelta;
+    A.counters = c.dcounters();
+    const int grid = (int)std::min<uint64_t>(update_grid(c), ceil_div(n * 32, 128));
+    update_kernel<<<grid, 128, 0, c.stream>>>(A);
+    NRG_LAUNCH_CHECK();
+    double* sum = sb.as<double>(1);
+    sum_fixed_kernel<<<1, 1024, 0, c.stream>>>(absdelta, n, sum);
+    NRG_LAUNCH_CHECK();
+    double h = 0.0;
+    NRG_CUDA(cudaMemcpyAsync(&h, sum, 8, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    c.toc(P_UPDATE);
+    c.state_version++;
+    return h;
+}
+
+// ---------------------------------------------------------------- theta pass
+__global__ void __launch_bounds__(256) theta_kernel(int kind, const uint32_t* __restrict__ Xb,
+                                                    const double* __restrict__ Xd, const double* __restrict__ H,
+                                                    const double* __restrict__ theta_in, int n, int M, int Mp,
+                                                    int Mw, double* __restrict__ theta_out, uint64_t* counters) {
+    const int lane = threadIdx.x & 31;
+    const int i = (int)(((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (i >= n) return;
+    if (M == 0) {
+        if (lane == 0) theta_out[i] = theta_in[i];
+        return;
+    }
+    const double* h = H + (size_t)i * Mp;
+    if (kind == ISING) {
+        // f'(th) = sum x - tanh(s + th), f'' = -sum sech^2(s + th) < 0
+        double sx = 0.0;
+        for (int k = 0; k * 32 < M; ++k) {
+            const int m = lane + 32 * k;
+            if (m < M) sx += xsign(Xb[(size_t)i * Mw + k], lane);
+        }
+        sx = warp_sum(sx);
+        auto deriv = [&](double th, double& d2) {
+            double g = 0.0, gg = 0.0;
+            for (int m = lane; m < M; m += 32) {
+                const double t = tanh(h[m] + th);
+                g += t;
+                gg += 1.0 - t * t;
+            }
+            g = warp_sum(g);
+            gg = warp_sum(gg);
+            d2 = -gg;
+            return sx - g;
+        };
+        double d2;
+        int passes = 2;
+        double res;
+        const double ghi = deriv(20.0, d2);
+        if (ghi >= 0.0) {
+            res = 20.0;
+        } else {
+            const double glo = deriv(-20.0, d2);
+            if (glo <= 0.0) {
+                res = -20.0;
+            } else {
+                double lo = -20.0, hi = 20.0, th = 0.0;
+                double g = deriv(th, d2);
+                for (int it = 0; it < 100; ++it) {
+                    ++passes;
+                    if (g > 0.0) lo = th; else hi = th;
+                    double tn = th - g / d2;
+                    if (!(tn > lo && tn < hi) || !isfinite(tn)) tn = 0.5 * (lo + hi);
+                    const bool done = fabs(tn - th) <= 1e-13 * fmax(1.0, fabs(tn)) || hi - lo <= 1e-14;
+                    th = tn;
+                    if (done) break;
+                    g = deriv(th, d2);
+                }
+                res = th;
+            }
+        }
+        if (lane == 0) {
+            theta_out[i] = res;
+            atomicAdd((unsigned long long*)&counters[C_EVALS], (unsigned long long)passes);
+        }
+    } else {
+        // -A/(2 th^2) - B th^2/2 - M log th: th^2 = 2A / (M + sqrt(M^2 + 4AB))
+        double A = 0.0, B = 0.0;
+        for (int m = lane; m < M; m += 32) {
+            const double x = Xd[(size_t)i * Mp + m];
+            A += x * x;
+            B += h[m] * h[m];
+        }
+        A = warp_sum(A);
+        B = warp_sum(B);
+        if (lane == 0) {
+            double th;
+            bool warn = false;
+            if (A == 0.0) {
+                th = 1e-8;
+                warn = true;
+            } else {
+                const double t2 = 2.0 * A / ((double)M + sqrt((double)M * (double)M + 4.0 * A * B));
+                th = sqrt(t2);
+                if (th <= 1e-8 * (1.0 + 1e-6)) {
+                    th = 1e-8;
+                    warn = true;
+                }
+            }
+            theta_out[i] = th;
+            atomicAdd((unsigned long long*)&counters[C_EVALS], 1ull);
+            if (warn) atomicAdd((unsigned long long*)&counters[C_WARN], 1ull);
+        }
+    }
+}
+
+void theta_pass(Context& c, double* out_only) {
+    c.tic();
+    double* out = out_only ? out_only : c.s_n.as<double>(c.n);
+    theta_kernel<<<(unsigned)ceil_div((int64_t)c.n * 32, 256), 256, 0, c.stream>>>(
+        c.kind, c.dXb(), c.dXd(), c.dH(), c.dtheta(), c.n, c.M, c.Mp, c.Mw, out, c.dcounters());
+    NRG_LAUNCH_CHECK();
+    if (!out_only) {
+        NRG_CUDA(cudaMemcpyAsync(c.theta.p, out, (size_t)c.n * 8, cudaMemcpyDeviceToDevice, c.stream));
+        c.state_version++;
+    }
+    c.sync();
+    c.toc(P_THETA);
+}
+
+}  // namespace nrg

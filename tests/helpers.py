@@ -1,0 +1,77 @@
+"""Comparison helpers with the parity tolerances of BASELINE.json north_star /
+SURVEY.md §8c, written once so every test states the same bar:
+
+  * w*        : |dw| <= 1e-4 absolute
+  * gain      : |dgain| <= 1e-5 * max(|gain_ref|, 1e-8 * M)
+  * dist      : |ddist| <= 1e-5 * |dist_ref| (relative) — and the gain check above
+  * couplings after updates on the same candidates: identical support, |dw| <= 1e-4
+"""
+from __future__ import annotations
+
+import numpy as np
+
+W_TOL = 1e-4
+GAIN_REL = 1e-5
+
+
+def gain_ok(g, g_ref, M):
+    g, g_ref = np.asarray(g), np.asarray(g_ref)
+    tol = GAIN_REL * np.maximum(np.abs(g_ref), 1e-8 * M)
+    return np.abs(g - g_ref) <= tol
+
+
+def assert_gains(g, g_ref, M, what="gain"):
+    ok = gain_ok(g, g_ref, M)
+    if not ok.all():
+        bad = np.flatnonzero(~ok)[:10]
+        raise AssertionError(f"{what}: {(~ok).sum()} of {len(ok)} outside tolerance; "
+                             f"first {bad}: {np.asarray(g)[bad]} vs {np.asarray(g_ref)[bad]}")
+
+
+def assert_w(w, w_ref, what="w*", tol=W_TOL):
+    d = np.abs(np.asarray(w) - np.asarray(w_ref))
+    if not (d <= tol).all():
+        bad = np.flatnonzero(d > tol)[:10]
+        raise AssertionError(f"{what}: max |dw| {d.max():.3g}; first {bad}: "
+                             f"{np.asarray(w)[bad]} vs {np.asarray(w_ref)[bad]}")
+
+
+def assert_rel(a, b, rel, what):
+    a, b = np.asarray(a, dtype=float), np.asarray(b, dtype=float)
+    d = np.abs(a - b) / np.maximum(np.abs(b), 1e-300)
+    if not (d <= rel).all():
+        i = int(np.argmax(d))
+        raise AssertionError(f"{what}: max rel diff {d.max():.3g} at {i}: {a.flat[i]!r} vs {b.flat[i]!r}")
+
+
+def edge_dict(ei, ej, w):
+    return {(int(min(a, b)), int(max(a, b))): float(x) for a, b, x in zip(ei, ej, w)}
+
+
+def assert_same_couplings(state, ref_state, tol=W_TOL, allow_support_diff=0):
+    """Same support (up to `allow_support_diff` near-kink flips with |w| <= tol) and
+    couplings within tol."""
+    a = edge_dict(*state[1:4])
+    b = edge_dict(*ref_state[1:4])
+    only = [k for k in set(a) ^ set(b) if abs(a.get(k, 0.0)) > tol or abs(b.get(k, 0.0)) > tol]
+    assert len(only) <= allow_support_diff, f"support differs on {len(only)} edges: {only[:10]}"
+    worst = max((abs(a.get(k, 0.0) - b.get(k, 0.0)) for k in set(a) | set(b)), default=0.0)
+    assert worst <= tol, f"coupling mismatch {worst:.3g}"
+
+
+def row_sets(ids):
+    return [set(map(int, r)) for r in np.asarray(ids)]
+
+
+def knn_recall(approx_ids, exact_ids):
+    """Per-node recall (test_knn.cpp:45-57)."""
+    sa, se = row_sets(approx_ids), row_sets(exact_ids)
+    k = np.asarray(exact_ids).shape[1]
+    return float(np.mean([len(a & e) / k for a, e in zip(sa, se)]))
+
+
+def pairs_equal(a, b):
+    """same_pairs (test_findbest.cpp:45-53): bitwise identity of (i, j, dist)."""
+    return (len(a) == len(b) and (np.asarray(a["i"]) == np.asarray(b["i"])).all()
+            and (np.asarray(a["j"]) == np.asarray(b["j"])).all()
+            and (np.asarray(a["dist"]) == np.asarray(b["dist"])).all())

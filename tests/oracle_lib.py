@@ -102,7 +102,7 @@ def lib(which: str) -> C.CDLL:
 
 def _chk(which: str, rc: int) -> None:
     if rc:
-        msg = lib(which)[f"{which}_last_error"]().decode()
+        msg = getattr(lib(which), f"{which}_last_error")().decode()
         raise ERR.get(rc, RuntimeError)(msg)
 
 
@@ -273,17 +273,17 @@ def recall_curve(which, exact, approx):
     e = np.ascontiguousarray(exact, dtype=PAIR_DT)
     a = np.ascontiguousarray(approx, dtype=PAIR_DT)
     out = np.zeros(len(e))
-    _chk(which, lib(which)[f"{which}_recall_curve"](len(e), e, a, out))
+    _chk(which, getattr(lib(which), f"{which}_recall_curve")(len(e), e, a, out))
     return out
 
 
 def mix64(a, b, which="orc"):
-    return int(lib(which)[f"{which}_mix64"](a, b))
+    return int(getattr(lib(which), f"{which}_mix64")(a, b))
 
 
 def rng_stream(seed, split, n, bound=0, which="orc"):
     out = np.zeros(n, np.uint64)
-    lib(which)[f"{which}_rng_stream"](seed, split, n, bound, out)
+    getattr(lib(which), f"{which}_rng_stream")(seed, split, n, bound, out)
     return out
 
 

@@ -1,0 +1,241 @@
+"""NNDescent / FindBest on the B200 vs the reference.
+
+* TableMetric / LineMetric (device-resident test metrics): bit-exact graphs, pair
+  lists, traces and churn against the reference's golden vectors — the same distance
+  values on both sides, so any difference is a semantic one.
+* Model distance (exact mode): per-node kNN sets and FindBest pairs agree up to
+  near-ties of the pair score; recall against the exhaustive kNN is at least the
+  reference's at the same k / eps / seed.
+* The structural invariants of test_knn.cpp / test_findbest.cpp."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+from helpers import knn_recall, pairs_equal, row_sets
+
+pytestmark = pytest.mark.gpu
+
+
+def table_model(P, t):
+    n = t.shape[0]
+    m = P.Model(n, 2, P.NRG_ISING, 0.0)
+    m.upload_samples(np.ones((n, 2)))
+    m.set_table(t)
+    return m
+
+
+def test_table_knn_bit_exact(gpu, golden):
+    g = golden("table")
+    t = g["table"]
+    n = t.shape[0]
+    m = table_model(gpu, t)
+    nodes = np.arange(n, dtype=np.int32)
+    for k in (1, 3, 8):
+        ids, dists, sw, churn = m.find_knn(gpu.NRG_TABLE, k, nodes, seed=21 + k)
+        assert row_sets(ids) == row_sets(g[f"knn{k}_ids"]), k
+        assert sw == int(g[f"knn{k}_sweeps"])
+        # stored dist is the oracle's (test_knn.cpp:83-104) and rows sorted by (dist, id)
+        for li in range(n):
+            for id_, d in zip(ids[li], dists[li]):
+                assert d == t[min(li, id_), max(li, id_)]
+            assert all((dists[li][a], ids[li][a]) <= (dists[li][a + 1], ids[li][a + 1]) for a in range(k - 1))
+    ids, dists, sw, churn = m.find_knn(gpu.NRG_TABLE, 4, nodes, seed=21)
+    assert row_sets(ids) == row_sets(g["knn4_ids"])
+    np.testing.assert_array_equal(churn, g["knn4_churn"])
+    m.set_table(np.abs(g["pos"][:, None] - g["pos"][None, :]))
+    ids, _, sw, _ = m.find_knn(gpu.NRG_TABLE, 6, nodes, seed=21 + 99)
+    assert row_sets(ids) == row_sets(g["line_ids"]) and sw == int(g["line_sweeps"])
+
+
+def test_table_find_best_bit_exact(gpu, golden):
+    g = golden("table")
+    t = g["table"]
+    n = t.shape[0]
+    m = table_model(gpu, t)
+    nodes = np.arange(n, dtype=np.int32)
+    for mm in g["ms"]:
+        fb, tr, sc = m.find_best(gpu.NRG_TABLE, int(mm), nodes, seed=21 + int(mm))
+        ref = np.zeros(len(g[f"fb{mm}_i"]), gpu.PAIR_DT)
+        ref["i"], ref["j"], ref["dist"] = g[f"fb{mm}_i"], g[f"fb{mm}_j"], g[f"fb{mm}_dist"]
+        assert pairs_equal(fb, ref), mm
+        assert (tr == g[f"fb{mm}_levels"]).all(), (tr, g[f"fb{mm}_levels"])
+        assert int(sc) == int(g[f"fb{mm}_short"])
+
+
+def random_table(n, seed):
+    rng = np.random.default_rng(seed)
+    t = np.zeros((n, n))
+    iu = np.triu_indices(n, 1)
+    t[iu] = rng.standard_normal(len(iu[0]))
+    return t
+
+
+@pytest.mark.parametrize("n,k,seed", [(120, 5, 1), (300, 8, 2), (500, 3, 3), (257, 12, 4)])
+def test_table_knn_vs_checker(gpu, n, k, seed):
+    t = random_table(n, 100 + seed)
+    nodes = np.arange(n, dtype=np.int32)
+    m = table_model(gpu, t)
+    ref = O.CpuModel("orc", np.ones((n, 2)), 0, 0.0)
+    ref.set_table(t)
+    a = m.find_knn(gpu.NRG_TABLE, k, nodes, seed=seed)
+    b = ref.find_knn(2, k, nodes, seed=seed)
+    assert row_sets(a[0]) == row_sets(b[0]) and a[2] == b[2]
+    np.testing.assert_array_equal(a[3], b[3])
+
+
+@pytest.mark.parametrize("n,m_,seed", [(150, 75, 77), (400, 100, 1), (200, 120, 4242), (90, 500, 5)])
+def test_table_find_best_vs_checker(gpu, n, m_, seed):
+    t = random_table(n, seed)
+    nodes = np.arange(n, dtype=np.int32)
+    m = table_model(gpu, t)
+    ref = O.CpuModel("orc", np.ones((n, 2)), 0, 0.0)
+    ref.set_table(t)
+    a, ta, sa = m.find_best(gpu.NRG_TABLE, m_, nodes, seed=seed)
+    b, tb, sb = ref.find_best(2, m_, nodes, seed=seed)
+    assert pairs_equal(a, b) and (ta == tb).all() and sa == sb
+
+
+def test_permuted_node_order_gives_same_graph(gpu):
+    """test_knn.cpp:154-179: the graph is a function of the node set."""
+    n = 200
+    t = random_table(n, 41)
+    m = table_model(gpu, t)
+    nodes = np.arange(n, dtype=np.int32)
+    a = m.find_knn(gpu.NRG_TABLE, 5, nodes, seed=4242)
+    perm = np.random.default_rng(99).permutation(n).astype(np.int32)
+    c = m.find_knn(gpu.NRG_TABLE, 5, perm, seed=4242)
+    sa, sc = row_sets(a[0]), row_sets(c[0])
+    for li in range(n):
+        assert sc[li] == sa[perm[li]]
+
+
+def test_find_best_invariants(gpu):
+    """test_findbest.cpp:110-189: unique canonical pairs, m <= |D| <= 2m, sorted,
+    halving, depth bound, k = ceil(4m/N), determinism, short count."""
+    n = 400
+    t = random_table(n, 100)
+    m = table_model(gpu, t)
+    nodes = np.arange(n, dtype=np.int32)
+    for seed in range(3):
+        fb, tr, sc = m.find_best(gpu.NRG_TABLE, 100, nodes, seed=seed)
+        assert len(fb) == 100 and (fb["i"] < fb["j"]).all()
+        assert len({(a, b) for a, b in zip(fb["i"], fb["j"])}) == 100
+        keys = list(zip(fb["dist"], fb["i"], fb["j"]))
+        assert keys == sorted(keys)
+        for lv in tr:
+            if not lv["exhaustive"]:
+                assert 100 <= lv["dedup_size"] <= 200
+        nodes_t = tr["nodes"]
+        assert all(nodes_t[a + 1] * 2 <= nodes_t[a] for a in range(len(tr) - 1))
+        assert len(tr) <= int(np.ceil(np.log2(n))) and tr[0]["nodes"] == n and tr[0]["k"] == 1
+        fb2, _, _ = m.find_best(gpu.NRG_TABLE, 100, nodes, seed=seed)
+        assert pairs_equal(fb, fb2)
+    small = table_model(gpu, random_table(6, 51))
+    r, _, sc = small.find_best(gpu.NRG_TABLE, 1000, np.arange(6, dtype=np.int32))
+    e, _, sc2 = small.find_best(gpu.NRG_TABLE, 15, np.arange(6, dtype=np.int32), exhaustive=True)
+    assert sc and not sc2 and len(r) == 15 and pairs_equal(r, e)
+
+
+def test_base_case_matches_exhaustive(gpu):
+    """test_findbest.cpp:67-85: 100 random base-case instances, bit-exact."""
+    rng = np.random.default_rng(2024)
+    for inst in range(40):
+        n = int(2 + rng.integers(0, 29))
+        total = n * (n - 1) // 2
+        m_lo = (n * n + 3) // 4
+        mm = max(1, int(m_lo + rng.integers(0, max(1, total + 5 - m_lo))))
+        t = random_table(n, 7000 + inst)
+        m = table_model(gpu, t)
+        nodes = np.arange(n, dtype=np.int32)
+        a, _, sa = m.find_best(gpu.NRG_TABLE, mm, nodes, seed=inst)
+        b, _, sb = m.find_best(gpu.NRG_TABLE, mm, nodes, exhaustive=True)
+        assert pairs_equal(a, b) and sa == sb
+
+
+def test_validation(gpu):
+    m = table_model(gpu, random_table(8, 3))
+    nodes = np.arange(8, dtype=np.int32)
+    with pytest.raises(ValueError):
+        m.find_knn(gpu.NRG_TABLE, 3, nodes, eps=0.0)
+    with pytest.raises(ValueError):
+        m.find_knn(gpu.NRG_TABLE, 0, nodes)
+    with pytest.raises(ValueError):
+        m.find_knn(gpu.NRG_TABLE, 1, nodes[:1])
+    with pytest.raises(ValueError):
+        m.find_best(gpu.NRG_TABLE, 0, nodes)
+    with pytest.raises(ValueError):
+        m.find_best(gpu.NRG_TABLE, 1, nodes[:1])
+
+
+def test_k_equals_n_minus_1_falls_back_to_exact(gpu):
+    n = 24
+    pos = np.random.default_rng(5).random(n)
+    m = table_model(gpu, np.abs(pos[:, None] - pos[None, :]))
+    ids, dists, sw, _ = m.find_knn(gpu.NRG_TABLE, n - 1, np.arange(n, dtype=np.int32), seed=3)
+    assert sw == 0
+    for li in range(n):
+        assert set(ids[li]) == set(range(n)) - {li}
+
+
+def test_line_metric_recall_and_sweeps(gpu):
+    """test_knn.cpp:106-121, 196-210 on the device LINE metric."""
+    n, k = 512, 8
+    accs = []
+    for s in range(6):
+        pos = np.random.default_rng(1000 + s).random(n)
+        m = gpu.Model(n, 2, gpu.NRG_ISING, 0.0)
+        m.upload_samples(np.ones((n, 2)))
+        m.set_line(pos)
+        nodes = np.arange(n, dtype=np.int32)
+        ids, _, sw, _ = m.find_knn(gpu.NRG_LINE, k, nodes, seed=s)
+        ex, _, _, _ = m.find_knn(gpu.NRG_LINE, k, nodes, exhaustive=True)
+        accs.append(knn_recall(ids, ex))
+    assert np.mean(accs) >= 0.90
+
+
+# ---- model distance
+def _ising(n, M, seed):
+    X, _ = O.gen_ising(n, M, seed=seed)
+    return X, O.ising_lambda(n, M)
+
+
+def test_model_knn_and_find_best_vs_checker(gpu):
+    X, lam = _ising(600, 300, 3)
+    n, M = X.shape
+    nodes = np.arange(n, dtype=np.int32)
+    dev = gpu.Model.from_samples(X.astype(np.int8), gpu.NRG_ISING, lam)
+    ref = O.CpuModel("orc", X, 0, lam)
+    dev.begin_generation()
+    ref.begin_generation()
+    a = dev.find_knn(gpu.NRG_EXACT, 8, nodes, seed=11)
+    b = ref.find_knn(0, 8, nodes, seed=11)
+    same = np.mean([x == y for x, y in zip(row_sets(a[0]), row_sets(b[0]))])
+    assert same >= 0.97, same
+    dev.begin_generation()
+    ref.begin_generation()
+    fa, ta, _ = dev.find_best(gpu.NRG_EXACT, 2 * n, nodes, seed=12)
+    fb, tb, _ = ref.find_best(0, 2 * n, nodes, seed=12)
+    sa = {(int(x), int(y)) for x, y in zip(fa["i"], fa["j"])}
+    sb = {(int(x), int(y)) for x, y in zip(fb["i"], fb["j"])}
+    assert len(sa & sb) / len(sb) >= 0.97
+
+
+def test_model_knn_recall_at_least_reference(gpu):
+    """north_star: NNDescent top-k recall against exhaustive search >= the reference's
+    recall at the same k and rounds (config-1 shape, exact mode)."""
+    X, lam = _ising(1000, 500, 1)
+    n = X.shape[0]
+    nodes = np.arange(n, dtype=np.int32)
+    dev = gpu.Model.from_samples(X.astype(np.int8), gpu.NRG_ISING, lam)
+    ref = O.CpuModel("orc", X, 0, lam)
+    dev.begin_generation()
+    ex = dev.find_knn(gpu.NRG_EXACT, 8, nodes, exhaustive=True)[0]
+    a = dev.find_knn(gpu.NRG_EXACT, 8, nodes, seed=7)[0]
+    ref.begin_generation()
+    b = ref.find_knn(0, 8, nodes, seed=7)[0]
+    ra, rb = knn_recall(a, ex), knn_recall(b, ex)
+    assert ra >= rb - 0.01, (ra, rb)
+    rev = dev.find_knn(gpu.NRG_EXACT, 8, nodes, seed=7, reverse=True)[0]
+    assert knn_recall(rev, ex) >= ra
