@@ -139,12 +139,20 @@ struct ClaimSink {
     uint64_t* live;
 };
 
-// warp-cooperative claim of one candidate per lane (active lanes given by `valid`)
+// warp-cooperative claim of one candidate per lane (active lanes given by `valid`).
+// Uncached metrics (h.keys == nullptr) claim every candidate into its flat slot.
 __device__ __forceinline__ uint32_t claim_warp(HashView h, const ClaimSink& sink, bool valid, int32_t gs,
-                                               int32_t gp) {
+                                               int32_t gp, uint64_t flat = 0) {
     bool mine = false;
     uint64_t sl = 0;
-    if (valid) sl = cache_claim_k(h, pair_key(gs, gp), mine);
+    if (valid) {
+        if (h.keys) {
+            sl = cache_claim_k(h, pair_key(gs, gp), mine);
+        } else {
+            sl = flat;
+            mine = true;
+        }
+    }
     const int lane = threadIdx.x & 31;
     const unsigned ball = __ballot_sync(0xffffffffu, mine);
     const unsigned hits = __ballot_sync(0xffffffffu, valid && !mine);
@@ -157,7 +165,7 @@ __device__ __forceinline__ uint32_t claim_warp(HashView h, const ClaimSink& sink
         sink.wp[at] = gp;
         sink.wslot[at] = (uint32_t)sl;
     }
-    if (lane == 0) {
+    if (lane == 0 && h.keys) {
         if (ball) {
             atomicAdd((unsigned long long*)&sink.counters[C_MISSES], (unsigned long long)__popc(ball));
             atomicAdd((unsigned long long*)sink.live, (unsigned long long)__popc(ball));
@@ -321,7 +329,7 @@ __global__ void __launch_bounds__(NT) knn_gather_kernel(const int32_t* __restric
         const int t = t0 + tid;
         const bool valid = t < cnt;
         const int32_t v = valid ? my_ids[t] : 0;
-        const uint32_t sl = claim_warp(h, sink, valid, gs, valid ? nodes[v] : 0);
+        const uint32_t sl = claim_warp(h, sink, valid, gs, valid ? nodes[v] : 0, li * capn + t);
         if (valid) cand_slot[li * capn + t] = sl;
     }
     if (tid == 0) cand_cnt[li] = cnt;
@@ -659,9 +667,13 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
     int32_t* cand_cnt = ccntb.as<int32_t>(n);
     unsigned long long* churn = churnb.as<unsigned long long>(1);
     const uint64_t wmax = n * capn;
-    int32_t* ws = wsb.as<int32_t>(cached ? wmax : 1);
-    int32_t* wp = wpb.as<int32_t>(cached ? wmax : 1);
-    uint32_t* wsl = wslb.as<uint32_t>(cached ? wmax : 1);
+    int32_t* ws = wsb.as<int32_t>(wmax);
+    int32_t* wp = wpb.as<int32_t>(wmax);
+    uint32_t* wsl = wslb.as<uint32_t>(wmax);
+    // uncached metrics (TABLE / LINE): per-candidate distances in a flat array
+    DevBuf flatb;
+    double* flat_d = cached ? nullptr : flatb.as<double>(wmax);
+    if (!cached && wmax >= (1ull << 32)) fail(100, "find_knn: candidate buffer exceeds 2^32");
     // dedup structure: hash of 2x(cap^2 + kw + 1) slots vs bitmap of n bits
     const uint64_t hash_slots = [&] {
         uint64_t s = 64;
@@ -745,14 +757,22 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         NRG_CUDA(cudaMemcpyAsync(&nw, wcount, 8, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
         c.toc(P_KNN);
-        score_claimed(c, mode, ws, wp, wsl, nw);
+        if (cached) {
+            score_claimed(c, mode, ws, wp, wsl, nw);
+        } else if (nw) {
+            ScoreOut so;
+            so.cache_vals = flat_d;
+            so.slot = wsl;
+            score_entries(c, mode, ws, wp, nw, so);
+        }
+        const double* dvals = cached ? c.Cview().vals : flat_d;
         c.tic();
         if (kw > 64)
             knn_merge_kernel<128><<<(unsigned)n, 128, merge_smem, c.stream>>>(
-                d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, c.Cview().vals, buf_cap, churn);
+                d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dvals, buf_cap, churn);
         else
             knn_merge_kernel<32><<<(unsigned)n, 32, merge_smem, c.stream>>>(
-                d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, c.Cview().vals, buf_cap, churn);
+                d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dvals, buf_cap, churn);
         NRG_LAUNCH_CHECK();
         unsigned long long changed = 0;
         NRG_CUDA(cudaMemcpyAsync(&changed, churn, 8, cudaMemcpyDeviceToHost, c.stream));

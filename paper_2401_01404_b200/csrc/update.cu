@@ -16,6 +16,8 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "pairscore.cuh"
@@ -124,7 +126,11 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs A) {
         const int i0 = A.ci[p], j0 = A.cj[p];
         const int a = min(i0, j0), b = max(i0, j0);
         const uint64_t key = pair_key(a, b);
-        const double wcur = hash_get_cg(A.W, key);
+        // one lane reads W and broadcasts: lanes are not in lockstep (independent
+        // thread scheduling), so a per-lane read could observe this pair's own write
+        double wcur = 0.0;
+        if (lane == 0) wcur = hash_get_cg(A.W, key);
+        wcur = __shfl_sync(0xffffffffu, wcur, 0);
         double w;
         if (A.assign) {
             w = A.assign[p];
@@ -174,6 +180,7 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs A) {
                 }
             }
         }
+        __syncwarp();  // every lane has read W and H before lane 0 publishes the new W
         if (lane == 0 && (delta != 0.0 || w == 0.0)) hash_set(A.W, key, w, A.Wcnt);
         __threadfence();
         __syncwarp();
@@ -258,9 +265,35 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
     A.ticket = ticket;
     A.absdelta = absdelta;
     A.counters = c.dcounters();
-    const int grid = (int)std::min<uint64_t>(update_grid(c), ceil_div(n * 32, 128));
-    update_kernel<<<grid, 128, 0, c.stream>>>(A);
+    int grid = (int)std::min<uint64_t>(update_grid(c), ceil_div(n * 32, 128));
+    const bool dbg = getenv("NRG_DEBUG_UPDATES") != nullptr;
+    if (dbg && getenv("NRG_DEBUG_SERIAL")) grid = 1;
+    update_kernel<<<grid, dbg && getenv("NRG_DEBUG_SERIAL") ? 32 : 128, 0, c.stream>>>(A);
     NRG_LAUNCH_CHECK();
+    if (dbg) {
+        std::vector<int32_t> hd(2 * n), hi(n), hj(n);
+        std::vector<int> hdone(n);
+        NRG_CUDA(cudaMemcpyAsync(hd.data(), dep, 8 * n, cudaMemcpyDeviceToHost, c.stream));
+        NRG_CUDA(cudaMemcpyAsync(hi.data(), ci, 4 * n, cudaMemcpyDeviceToHost, c.stream));
+        NRG_CUDA(cudaMemcpyAsync(hj.data(), cj, 4 * n, cudaMemcpyDeviceToHost, c.stream));
+        NRG_CUDA(cudaMemcpyAsync(hdone.data(), done, 4 * n, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        std::vector<int32_t> last(c.n, -1);
+        int bad = 0, ndone = 0;
+        for (uint64_t p = 0; p < n; ++p) {
+            const int e0 = last[hi[p]], e1 = last[hj[p]];
+            if (hd[2 * p] != e0 || hd[2 * p + 1] != e1) {
+                if (bad < 10)
+                    fprintf(stderr, "dep mismatch p=%llu (%d,%d): got %d %d want %d %d\n", (unsigned long long)p, hi[p],
+                            hj[p], hd[2 * p], hd[2 * p + 1], e0, e1);
+                ++bad;
+            }
+            last[hi[p]] = last[hj[p]] = (int32_t)p;
+            ndone += hdone[p];
+        }
+        fprintf(stderr, "apply_updates debug: n=%llu grid=%d dep mismatches=%d done=%d\n", (unsigned long long)n, grid,
+                bad, ndone);
+    }
     double* sum = sb.as<double>(1);
     sum_fixed_kernel<<<1, 1024, 0, c.stream>>>(absdelta, n, sum);
     NRG_LAUNCH_CHECK();
