@@ -44,6 +44,19 @@ int guard(F&& f) {
     }
 }
 
+template <class F>
+int guardx(nrg_ctx* x, F&& f) {
+    if (!x) {
+        g_err = "null context";
+        return NRG_EINVAL;
+    }
+    return guard([&] {
+        NRG_CUDA(cudaSetDevice(x->c.device));
+        nrg::StreamScope ss(x->c.stream);
+        f();
+    });
+}
+
 void check_pairs(const nrg_ctx* x, uint64_t n, const int32_t* i, const int32_t* j) {
     for (uint64_t t = 0; t < n; ++t) {
         if (i[t] == j[t]) nrg::fail(22, "pair operations need i != j");
@@ -108,6 +121,7 @@ int nrg_version(void) { return 1; }
 
 int nrg_create(nrg_ctx** out, int32_t n, int32_t m, int32_t kind, double lambda, int32_t device) {
     return guard([&] {
+        nrg::StreamScope ss(nullptr);
         auto* x = new nrg_ctx();
         try {
             nrg::ctx_init(x->c, n, m, kind, lambda, device);
@@ -120,29 +134,29 @@ int nrg_create(nrg_ctx** out, int32_t n, int32_t m, int32_t kind, double lambda,
 }
 
 int nrg_destroy(nrg_ctx* x) {
-    return guard([&] { delete x; });
+    return guardx(x, [&] { delete x; });
 }
 
 int nrg_upload_samples(nrg_ctx* x, const double* X) {
-    return guard([&] { nrg::upload_samples_f64(x->c, X); });
+    return guardx(x, [&] { nrg::upload_samples_f64(x->c, X); });
 }
 int nrg_upload_spins_i8(nrg_ctx* x, const int8_t* X) {
-    return guard([&] { nrg::upload_spins_i8(x->c, X); });
+    return guardx(x, [&] { nrg::upload_spins_i8(x->c, X); });
 }
 
 int nrg_reset_state(nrg_ctx* x) {
-    return guard([&] { nrg::reset_state_empty(x->c); });
+    return guardx(x, [&] { nrg::reset_state_empty(x->c); });
 }
 
 int nrg_set_theta(nrg_ctx* x, const double* theta) {
-    return guard([&] {
+    return guardx(x, [&] {
         need_samples(x);
         if (theta) nrg::set_theta(x->c, theta);
     });
 }
 
 int nrg_set_edges(nrg_ctx* x, uint64_t n, const int32_t* ei, const int32_t* ej, const double* w) {
-    return guard([&] {
+    return guardx(x, [&] {
         need_samples(x);
         for (uint64_t t = 0; t < n; ++t) {
             if (ei[t] < 0 || ej[t] < 0 || ei[t] >= x->c.n || ej[t] >= x->c.n) nrg::fail(34, "node id out of range");
@@ -156,23 +170,23 @@ int nrg_set_edges(nrg_ctx* x, uint64_t n, const int32_t* ei, const int32_t* ej, 
 }
 
 int nrg_get_state(nrg_ctx* x, double* theta, uint64_t cap, int32_t* ei, int32_t* ej, double* w, uint64_t* n_edges) {
-    return guard([&] { nrg::get_state(x->c, theta, cap, ei, ej, w, n_edges); });
+    return guardx(x, [&] { nrg::get_state(x->c, theta, cap, ei, ej, w, n_edges); });
 }
 
 int nrg_get_sums(nrg_ctx* x, double* out) {
-    return guard([&] { nrg::get_sums(x->c, out); });
+    return guardx(x, [&] { nrg::get_sums(x->c, out); });
 }
 
 int nrg_begin_generation(nrg_ctx* x) {
-    return guard([&] { nrg::begin_generation(x->c); });
+    return guardx(x, [&] { nrg::begin_generation(x->c); });
 }
 
 int nrg_log_posterior(nrg_ctx* x, double* out) {
-    return guard([&] { *out = nrg::log_posterior(x->c); });
+    return guardx(x, [&] { *out = nrg::log_posterior(x->c); });
 }
 
 int nrg_distance(nrg_ctx* x, int32_t mode, uint64_t n, const int32_t* i, const int32_t* j, double* dist) {
-    return guard([&] {
+    return guardx(x, [&] {
         if (mode != NRG_TABLE && mode != NRG_LINE) need_samples(x);
         check_pairs(x, n, i, j);
         int32_t* di = to_dev(x, x->q_i, i, n);
@@ -186,7 +200,7 @@ int nrg_distance(nrg_ctx* x, int32_t mode, uint64_t n, const int32_t* i, const i
 
 int nrg_optimize_edge(nrg_ctx* x, uint64_t n, const int32_t* i, const int32_t* j, double* w, double* gain,
                       uint8_t* warn) {
-    return guard([&] {
+    return guardx(x, [&] {
         need_samples(x);
         check_pairs(x, n, i, j);
         int32_t* di = to_dev(x, x->q_i, i, n);
@@ -203,7 +217,7 @@ int nrg_optimize_edge(nrg_ctx* x, uint64_t n, const int32_t* i, const int32_t* j
 }
 
 int nrg_edge_gradient(nrg_ctx* x, uint64_t n, const int32_t* i, const int32_t* j, double* g) {
-    return guard([&] {
+    return guardx(x, [&] {
         need_samples(x);
         check_pairs(x, n, i, j);
         int32_t* di = to_dev(x, x->q_i, i, n);
@@ -216,7 +230,7 @@ int nrg_edge_gradient(nrg_ctx* x, uint64_t n, const int32_t* i, const int32_t* j
 }
 
 int nrg_optimize_theta(nrg_ctx* x, double* out) {
-    return guard([&] {
+    return guardx(x, [&] {
         need_samples(x);
         double* d = x->q_d.as<double>(x->c.n);
         nrg::theta_pass(x->c, d);
@@ -226,16 +240,16 @@ int nrg_optimize_theta(nrg_ctx* x, double* out) {
 }
 
 int nrg_set_table(nrg_ctx* x, uint64_t n, const double* table) {
-    return guard([&] { nrg::set_table(x->c, n, table); });
+    return guardx(x, [&] { nrg::set_table(x->c, n, table); });
 }
 int nrg_set_line(nrg_ctx* x, uint64_t n, const double* pos) {
-    return guard([&] { nrg::set_line(x->c, n, pos); });
+    return guardx(x, [&] { nrg::set_line(x->c, n, pos); });
 }
 
 int nrg_find_knn(nrg_ctx* x, int32_t mode, int32_t k, const int32_t* nodes, uint64_t n, const nrg_knn_params* p,
                  int32_t exhaustive, int32_t* ids, double* dists, int32_t* k_out, int32_t* sweeps, double* churn,
                  int32_t churn_cap, int32_t* n_churn) {
-    return guard([&] {
+    return guardx(x, [&] {
         if (mode != NRG_TABLE && mode != NRG_LINE) need_samples(x);
         nrg::KnnParamsD kp;
         if (p) {
@@ -262,7 +276,7 @@ int nrg_find_knn(nrg_ctx* x, int32_t mode, int32_t k, const int32_t* nodes, uint
 int nrg_find_best(nrg_ctx* x, int32_t mode, uint64_t m, const int32_t* nodes, uint64_t n, const nrg_fb_params* p,
                   int32_t exhaustive, nrg_pair* out, uint64_t cap, uint64_t* n_out, nrg_trace_level* trace,
                   int32_t trace_cap, int32_t* n_levels, int32_t* short_count) {
-    return guard([&] {
+    return guardx(x, [&] {
         if (mode != NRG_TABLE && mode != NRG_LINE) need_samples(x);
         int32_t* dn = to_dev(x, x->q_j, nodes, n);
         nrg::BestPairsD best;
@@ -287,7 +301,7 @@ int nrg_find_best(nrg_ctx* x, int32_t mode, uint64_t m, const int32_t* nodes, ui
 }
 
 int nrg_apply_updates(nrg_ctx* x, const nrg_pair* cands, uint64_t n, double* delta) {
-    return guard([&] {
+    return guardx(x, [&] {
         need_samples(x);
         std::vector<int32_t> hi(n), hj(n);
         for (uint64_t t = 0; t < n; ++t) {
@@ -303,7 +317,7 @@ int nrg_apply_updates(nrg_ctx* x, const nrg_pair* cands, uint64_t n, double* del
 }
 
 int nrg_theta_pass(nrg_ctx* x) {
-    return guard([&] {
+    return guardx(x, [&] {
         need_samples(x);
         nrg::theta_pass(x->c, nullptr);
     });
@@ -311,12 +325,12 @@ int nrg_theta_pass(nrg_ctx* x) {
 
 int nrg_gcd_iteration(nrg_ctx* x, const nrg_gcd_cfg* cfg, int32_t iter, nrg_iter_record* rec, nrg_pair* cands,
                       uint64_t cap, uint64_t* n_cands) {
-    return guard([&] { gcd_iteration(x, cfg, iter, rec, cands, cap, n_cands); });
+    return guardx(x, [&] { gcd_iteration(x, cfg, iter, rec, cands, cap, n_cands); });
 }
 
 int nrg_reconstruct_gcd(nrg_ctx* x, const nrg_gcd_cfg* cfg, nrg_iter_record* recs, int32_t rec_cap, int32_t* n_iters,
                         int32_t* converged) {
-    return guard([&] {
+    return guardx(x, [&] {
         need_samples(x);
         if (!(cfg->kappa > 0.0)) nrg::fail(22, "reconstruct_gcd: kappa must be > 0");
         const double eps = cfg->eps > 0.0 ? cfg->eps : 1e-6 * x->c.n;
@@ -336,7 +350,7 @@ int nrg_reconstruct_gcd(nrg_ctx* x, const nrg_gcd_cfg* cfg, nrg_iter_record* rec
 }
 
 int nrg_counters(nrg_ctx* x, uint64_t* misses, uint64_t* hits, uint64_t* evals, uint64_t* warnings) {
-    return guard([&] {
+    return guardx(x, [&] {
         uint64_t h[nrg::C_N];
         NRG_CUDA(cudaMemcpyAsync(h, x->c.counters.p, sizeof(h), cudaMemcpyDeviceToHost, x->c.stream));
         x->c.sync();
@@ -348,7 +362,7 @@ int nrg_counters(nrg_ctx* x, uint64_t* misses, uint64_t* hits, uint64_t* evals, 
 }
 
 int nrg_reset_counters(nrg_ctx* x) {
-    return guard([&] {
+    return guardx(x, [&] {
         NRG_CUDA(cudaMemsetAsync(x->c.counters.p, 0, nrg::C_N * 8, x->c.stream));
         for (double& v : x->c.phase_ms) v = 0.0;
         x->c.k1_ms = x->c.k1_launches = x->c.k1_pairs = x->c.k2_ms = x->c.k2_launches = x->c.k2_pairs = 0;
@@ -358,13 +372,13 @@ int nrg_reset_counters(nrg_ctx* x) {
 }
 
 int nrg_phase_times(nrg_ctx* x, double* ms, int32_t cap) {
-    return guard([&] {
+    return guardx(x, [&] {
         for (int t = 0; t < nrg::P_N && t < cap; ++t) ms[t] = x->c.phase_ms[t];
     });
 }
 
 int nrg_timer(nrg_ctx* x, int32_t op, double* ms) {
-    return guard([&] {
+    return guardx(x, [&] {
         if (!x->t0) {
             NRG_CUDA(cudaEventCreate(&x->t0));
             NRG_CUDA(cudaEventCreate(&x->t1));
@@ -382,7 +396,7 @@ int nrg_timer(nrg_ctx* x, int32_t op, double* ms) {
 }
 
 int nrg_kernel_stats(nrg_ctx* x, double* out, int32_t cap) {
-    return guard([&] {
+    return guardx(x, [&] {
         const nrg::Context& c = x->c;
         const double v[7] = {c.k1_ms, c.k1_launches, c.k1_pairs, c.k2_ms, c.k2_launches, c.k2_pairs,
                              (double)(nrg::g_launches.load() - c.launches0)};
@@ -391,7 +405,7 @@ int nrg_kernel_stats(nrg_ctx* x, double* out, int32_t cap) {
 }
 
 int nrg_sample_scored_pairs(nrg_ctx* x, uint64_t cap, uint64_t seed, int32_t* i, int32_t* j, uint64_t* n_out) {
-    return guard([&] {
+    return guardx(x, [&] {
         int32_t* di = x->q_i.as<int32_t>(std::max<uint64_t>(cap, 1));
         int32_t* dj = x->q_j.as<int32_t>(std::max<uint64_t>(cap, 1));
         const uint64_t k = nrg::sample_scored_pairs(x->c, cap, seed, di, dj);
@@ -423,7 +437,7 @@ int nrg_recall_curve(uint64_t m, const nrg_pair* exact, const nrg_pair* approx, 
 
 int nrg_generate_ising(nrg_ctx* x, double mean_deg, double w_sigma, double th_sigma, int32_t burn_in, int32_t thin,
                        uint64_t seed, int8_t* X_out) {
-    return guard([&] {
+    return guardx(x, [&] {
         nrg::generate_ising(x->c, mean_deg, w_sigma, th_sigma, burn_in, thin, seed);
         if (X_out) {
             // unpack the bit-packed samples to int8 on the host
@@ -445,7 +459,7 @@ int nrg_comm_unique_id(uint8_t id[128]) {
     });
 }
 int nrg_comm_init(nrg_ctx* x, const uint8_t id[128], int32_t rank, int32_t world) {
-    return guard([&] {
+    return guardx(x, [&] {
         (void)x;
         (void)id;
         if (world != 1 || rank != 0) nrg::fail(NRG_EINVAL, "multi-GPU communicator not built into this library");

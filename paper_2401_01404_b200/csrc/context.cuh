@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -25,16 +26,53 @@ namespace nrg {
 enum Kind { ISING = 0, GAUSSIAN = 1 };
 enum Mode { EXACT = 0, GRADIENT = 1, TABLE = 2, LINE = 3 };
 
-// grow-only device buffer
+// Stream the calling API entry works on; device buffers are allocated and freed in
+// that stream's order from the device's memory pool (release threshold pinned, so
+// scratch buffers are recycled without cudaMalloc/cudaFree synchronisation).
+inline thread_local cudaStream_t tl_stream = nullptr;
+inline bool sync_alloc() {  // NRG_SYNC_ALLOC=1: plain cudaMalloc/cudaFree (A/B testing)
+    static const bool v = getenv("NRG_SYNC_ALLOC") != nullptr;
+    return v;
+}
+struct StreamScope {
+    cudaStream_t prev;
+    explicit StreamScope(cudaStream_t s) : prev(tl_stream) { tl_stream = s; }
+    ~StreamScope() { tl_stream = prev; }
+};
+
+// grow-only device buffer (RAII, move-only, stream-ordered)
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), s(o.s) {
+        o.p = nullptr;
+        o.bytes = 0;
+    }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p;
+            bytes = o.bytes;
+            s = o.s;
+            o.p = nullptr;
+            o.bytes = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }
     void* ensure(size_t b) {
         if (b > bytes) {
-            if (p) cudaFree(p);
-            p = nullptr;
-            size_t nb = b + b / 4 + 256;
-            NRG_CUDA(cudaMalloc(&p, nb));
+            release();
+            const size_t nb = b + b / 4 + 256;
+            s = tl_stream;
+            if (sync_alloc())
+                NRG_CUDA(cudaMalloc(&p, nb));
+            else
+                NRG_CUDA(cudaMallocAsync(&p, nb, s));
             bytes = nb;
         }
         return p;
@@ -44,7 +82,12 @@ struct DevBuf {
         return static_cast<T*>(ensure(count * sizeof(T) + 16));
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            if (sync_alloc())
+                cudaFree(p);
+            else
+                cudaFreeAsync(p, s);
+        }
         p = nullptr;
         bytes = 0;
     }
@@ -70,7 +113,8 @@ struct IsingSnap {
     const uint32_t* Xb;
     const float* T32;
     const double* T64;
-    const float* Tabs;
+    const float* Tabs;   // sum |T32| per node (rigorous screen error bound)
+    const double* Tsq;   // sum T64^2 per node (L''(0) = -(2M - Tsq_a - Tsq_b) for w_cur = 0)
     int M, Mp, Mw;
 };
 
@@ -96,7 +140,18 @@ struct ScoreOut {
 enum Counter { C_MISSES = 0, C_HITS = 1, C_EVALS = 2, C_WARN = 3, C_N = 4 };
 enum Phase { P_SCORE = 0, P_KNN = 1, P_SELECT = 2, P_UPDATE = 3, P_THETA = 4, P_LOGPOST = 5, P_SNAP = 6, P_N = 7 };
 
+struct StreamOwner {  // declared first in Context: destroyed after every DevBuf member
+    cudaStream_t s = nullptr;
+    ~StreamOwner() {
+        if (s) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
+        }
+    }
+};
+
 struct Context {
+    StreamOwner stream_owner;
     int n = 0, M = 0, kind = 0, device = 0;
     int Mp = 0, Mw = 0;
     double lambda = 0.0;
@@ -113,7 +168,7 @@ struct Context {
     uint64_t state_version = 1;
 
     // snapshot
-    DevBuf T32, T64, Tabs, U, xx;
+    DevBuf T32, T64, Tabs, Tsq, U, xx;
     uint64_t snap_version = 0;
     bool base_valid = false;
     double base = 0.0;
@@ -140,6 +195,8 @@ struct Context {
     // scratch
     DevBuf s_a, s_b, s_c, s_d, s_e, s_f, s_g, s_h, s_i, s_j, s_k, s_l, s_m, s_n, s_o;
     DevBuf red;  // reduction scratch
+    // scorer-private scratch (score_entries only)
+    DevBuf sc_surv, sc_g, sc_flag, sc_w32, sc_n;
     std::vector<char> host_scratch;
 
     // multi-GPU (nccl), opaque
@@ -161,7 +218,7 @@ struct Context {
     }
     IsingSnap isnap() {
         return {dXb(), static_cast<float*>(T32.p), static_cast<double*>(T64.p),
-                static_cast<float*>(Tabs.p), M, Mp, Mw};
+                static_cast<float*>(Tabs.p), static_cast<double*>(Tsq.p), M, Mp, Mw};
     }
     GaussSnap gsnap() {
         return {dXd(), static_cast<double*>(U.p), static_cast<double*>(xx.p), dtheta(), M, Mp};

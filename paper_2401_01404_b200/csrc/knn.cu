@@ -52,28 +52,32 @@ __global__ void rank_kernel(const int32_t* __restrict__ perm, uint64_t n, int32_
     if (t < n) rank[perm[t]] = (int32_t)t;
 }
 
-// initial out-neighbours: Floyd sampling (inc/knn.hpp:177-199)
+// initial out-neighbours: Floyd sampling (inc/knn.hpp:177-199).  One warp per node:
+// lane 0 draws the sequence, the warp tests membership in parallel.
 __global__ void knn_init_kernel(const int32_t* __restrict__ nodes, const int32_t* __restrict__ sorted_ids,
                                 const int32_t* __restrict__ rank, const int32_t* __restrict__ loc,
                                 uint64_t n, int kw, uint64_t seed, int32_t* __restrict__ gid,
                                 int32_t* __restrict__ qi, int32_t* __restrict__ qj) {
-    const uint64_t li = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t li = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (li >= n) return;
     const SplitRng root(seed);
     SplitRng r = root.split((uint64_t)nodes[li] + 1);
     const uint64_t self = (uint64_t)rank[li];
-    int32_t* picks = gid + li * kw;  // ranks first, ids after
+    int32_t* picks = gid + li * kw;  // ranks first, local ids after
     int np = 0;
     for (uint64_t t = n - 1 - (uint64_t)kw; t < n - 1; ++t) {
-        uint64_t v = r.below(t + 1);
-        for (int q = 0; q < np; ++q)
-            if ((uint64_t)picks[q] == v) {
-                v = t;
-                break;
-            }
-        picks[np++] = (int32_t)v;
+        uint64_t v = 0;
+        if (lane == 0) v = r.below(t + 1);
+        v = __shfl_sync(0xffffffffu, v, 0);
+        bool hit = false;
+        for (int q = lane; q < np; q += 32) hit |= ((uint64_t)picks[q] == v);
+        if (__any_sync(0xffffffffu, hit)) v = t;
+        if (lane == 0) picks[np] = (int32_t)v;
+        __syncwarp();
+        ++np;
     }
-    for (int t = 0; t < kw; ++t) {
+    for (int t = lane; t < kw; t += 32) {
         uint64_t rk = (uint64_t)picks[t];
         if (rk >= self) ++rk;
         const int32_t g = sorted_ids[rk];
@@ -83,25 +87,48 @@ __global__ void knn_init_kernel(const int32_t* __restrict__ nodes, const int32_t
     }
 }
 
-// sort each row (kw entries) by (dist, id); one thread per row (insertion sort)
-__global__ void row_sort_kernel(int32_t* __restrict__ gid, double* __restrict__ gd,
-                                const int32_t* __restrict__ nodes, uint64_t n, int kw) {
-    const uint64_t li = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (li >= n) return;
-    int32_t* ids = gid + li * kw;
-    double* ds = gd + li * kw;
-    for (int a = 1; a < kw; ++a) {
-        const int32_t id = ids[a];
-        const double d = ds[a];
-        const int gi = nodes[id];
-        int b = a - 1;
-        while (b >= 0 && entry_less(d, gi, ds[b], nodes[ids[b]])) {
-            ids[b + 1] = ids[b];
-            ds[b + 1] = ds[b];
-            --b;
+// sort each row (kw entries) by (dist, id): one CTA per row, bitonic in shared memory
+template <int NT>
+__global__ void __launch_bounds__(NT) row_sort_kernel(int32_t* __restrict__ gid, double* __restrict__ gd,
+                                                      const int32_t* __restrict__ nodes, uint64_t n, int kw, int P) {
+    extern __shared__ unsigned char rs_smem[];
+    double* bd = reinterpret_cast<double*>(rs_smem);
+    int32_t* bi = reinterpret_cast<int32_t*>(bd + P);
+    int32_t* bg = bi + P;
+    const uint64_t li = blockIdx.x;
+    const int tid = threadIdx.x;
+    for (int t = tid; t < P; t += NT) {
+        if (t < kw) {
+            bd[t] = gd[li * kw + t];
+            bi[t] = gid[li * kw + t];
+            bg[t] = nodes[bi[t]];
+        } else {
+            bd[t] = INFINITY;
+            bi[t] = -1;
+            bg[t] = 0x7fffffff;
         }
-        ids[b + 1] = id;
-        ds[b + 1] = d;
+    }
+    __syncthreads();
+    for (int k2 = 2; k2 <= P; k2 <<= 1) {
+        for (int j = k2 >> 1; j > 0; j >>= 1) {
+            for (int t = tid; t < P; t += NT) {
+                const int ixj = t ^ j;
+                if (ixj > t) {
+                    const bool up = (t & k2) == 0;
+                    const bool gt = bd[ixj] < bd[t] || (bd[ixj] == bd[t] && bg[ixj] < bg[t]);
+                    if (gt == up) {
+                        const double td = bd[t]; bd[t] = bd[ixj]; bd[ixj] = td;
+                        const int ti = bi[t]; bi[t] = bi[ixj]; bi[ixj] = ti;
+                        const int tg = bg[t]; bg[t] = bg[ixj]; bg[ixj] = tg;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int t = tid; t < kw; t += NT) {
+        gd[li * kw + t] = bd[t];
+        gid[li * kw + t] = bi[t];
     }
 }
 
@@ -625,8 +652,8 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         DevBuf qib, qjb, slb;
         int32_t* qi = qib.as<int32_t>(nq);
         int32_t* qj = qjb.as<int32_t>(nq);
-        knn_init_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, c.stream>>>(d_nodes, sorted_ids, rank, loc, n, kw,
-                                                                       p.seed, gid, qi, qj);
+        knn_init_kernel<<<(unsigned)ceil_div(n * 32, 128), 128, 0, c.stream>>>(d_nodes, sorted_ids, rank, loc, n,
+                                                                            kw, p.seed, gid, qi, qj);
         NRG_LAUNCH_CHECK();
         c.toc(P_KNN);
         if (cached) {
@@ -652,7 +679,14 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             score_entries(c, mode, qi, qj, nq, so);
         }
         c.tic();
-        row_sort_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, c.stream>>>(gid, gd, d_nodes, n, kw);
+        int P = 1;
+        while (P < kw) P <<= 1;
+        const size_t rs_smem = (size_t)P * 16;
+        if (rs_smem > 48 * 1024) fail(100, "find_knn: kw too large for the row sort");
+        if (P <= 64)
+            row_sort_kernel<32><<<(unsigned)n, 32, rs_smem, c.stream>>>(gid, gd, d_nodes, n, kw, P);
+        else
+            row_sort_kernel<128><<<(unsigned)n, 128, rs_smem, c.stream>>>(gid, gd, d_nodes, n, kw, P);
         NRG_LAUNCH_CHECK();
         c.toc(P_KNN);
     }

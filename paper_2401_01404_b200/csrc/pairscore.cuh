@@ -27,6 +27,7 @@ __device__ __forceinline__ double xsign(uint32_t word, int bit) {
 struct Pass64 {
     double Lp;    // L'(w)
     double Lpp;   // L''(w)
+    double Lppp;  // L'''(w)
     double Flik;  // likelihood part of F(w) - F(w_cur)
 };
 
@@ -57,7 +58,7 @@ __device__ __forceinline__ Pass64 ising_pass64(const TP& T, const uint32_t* __re
     const double A = fabs(D);
     const double sg = D > 0.0 ? 1.0 : (D < 0.0 ? -1.0 : 0.0);
     const double E = -expm1(-2.0 * A);  // 1 - e^{-2|D|}
-    double Lp = 0.0, Lpp = 0.0, F = 0.0;
+    double Lp = 0.0, Lpp = 0.0, L3 = 0.0, F = 0.0;
     for (int k = 0; k * 32 < M; ++k) {
         const int m = lane + 32 * k;
         const uint32_t wa = __ldg(&Xb[(size_t)a * Mw + k]);
@@ -71,7 +72,9 @@ __device__ __forceinline__ Pass64 ising_pass64(const TP& T, const uint32_t* __re
             const double db = 1.0 / (1.0 + yb * t);
             const double qa = (ya + t) * da, qb = (yb + t) * db;
             Lp += (2.0 * s - qa) - qb;
-            Lpp -= (1.0 - ya * ya) * omt2 * da * da + (1.0 - yb * yb) * omt2 * db * db;
+            const double d1a = (1.0 - ya * ya) * omt2 * da * da, d1b = (1.0 - yb * yb) * omt2 * db * db;
+            Lpp -= d1a + d1b;
+            L3 += 2.0 * (qa * d1a + qb * d1b);
             if (kNeedF) {
                 const double la = A + log1p(-0.5 * (1.0 - sg * ya) * E);
                 const double lb = A + log1p(-0.5 * (1.0 - sg * yb) * E);
@@ -82,6 +85,7 @@ __device__ __forceinline__ Pass64 ising_pass64(const TP& T, const uint32_t* __re
     Pass64 r;
     r.Lp = warp_sum(Lp);
     r.Lpp = warp_sum(Lpp);
+    r.Lppp = warp_sum(L3);
     r.Flik = kNeedF ? warp_sum(F) : 0.0;
     return r;
 }
@@ -92,18 +96,91 @@ struct EdgeOptD {
     int passes;
 };
 
-// Full fp64 optimize_edge for the Ising slice (a < b canonical).  Used for existing
-// edges, uncertain kink decisions, fp32 fallbacks and the update kernel.
+// Safeguarded Newton for phi(u) = dir L'(dir u) - lambda = 0 on u > 0 (D = dir u - w_cur),
+// started from the root of the quadratic model phi0 + phi1 u + phi2 u^2/2 (phi1 < 0).
+// Passes without the log1p objective until the step predicts convergence; the last
+// pass evaluates the slice gain and applies the second-order Newton correction.
+template <class TP>
+__device__ EdgeOptD ising_newton64(const TP& T, const uint32_t* __restrict__ Xb, int Mw, int M, int a, int b,
+                                   double w_cur, double lambda, double dir, double phi0, double phi1,
+                                   double phi2, int passes) {
+    EdgeOptD r;
+    r.warn = 0;
+    r.passes = passes;
+    double u;
+    {
+        const double disc = phi1 * phi1 - 2.0 * phi2 * phi0;
+        u = (disc >= 0.0 && phi1 < 0.0) ? 2.0 * phi0 / (-phi1 + sqrt(disc)) : phi0 / fmax(-phi1, 1e-300);
+        if (!(u > 0.0) || !isfinite(u)) u = 1.0;
+    }
+    double lo = 0.0, hi = INFINITY, du_last = u, prevF = -INFINITY;
+    for (int it = 0; it < 100; ++it) {
+        const double scale = fmax(u, 1e-3);
+        const bool final_try = fabs(du_last) <= 0.03 * scale;
+        const double D = dir * u - w_cur;
+        const Pass64 p = final_try ? ising_pass64<TP, true>(T, Xb, Mw, M, a, b, D)
+                                   : ising_pass64<TP, false>(T, Xb, Mw, M, a, b, D);
+        ++r.passes;
+        const double phi = dir * p.Lp - lambda, dphi = p.Lpp;
+        const double du = (dphi < 0.0) ? -phi / dphi : NAN;
+        if (final_try && isfinite(du) && fabs(du) <= 1e-3 * scale) {
+            const double gain = (p.Flik - lambda * u) + lambda * fabs(w_cur) + 0.5 * phi * du;
+            if (gain < 0.0) {  // inc/model.hpp:215
+                r.w = w_cur;
+                r.gain = 0.0;
+            } else {
+                r.w = dir * (u + du);
+                r.gain = gain;
+            }
+            return r;
+        }
+        if (phi > 0.0) lo = u; else hi = u;
+        double un = u + du;
+        if (!(un > lo && un < hi) || !isfinite(un)) un = isinf(hi) ? fmax(2.0 * u, 1.0) : 0.5 * (lo + hi);
+        if (un > 0x1.0p64) {  // bracket failure (inc/line_search.hpp:64-84 cap)
+            r.warn = 1;
+            break;
+        }
+        if (isinf(hi) && un > 64.0) {
+            // separable columns: the slice saturates numerically; stop once the
+            // objective no longer increases (the reference's doubling stops there too)
+            const Pass64 pf = ising_pass64<TP, true>(T, Xb, Mw, M, a, b, dir * un - w_cur);
+            ++r.passes;
+            const double F = pf.Flik - lambda * un;
+            if (!(F > prevF)) break;
+            prevF = F;
+        }
+        du_last = un - u;
+        u = un;
+        if (hi - lo <= 1e-15 * fmax(1.0, u)) du_last = 0.0;
+    }
+    // plateau / bracket failure: objective at the last iterate
+    const Pass64 pf = ising_pass64<TP, true>(T, Xb, Mw, M, a, b, dir * u - w_cur);
+    ++r.passes;
+    const double gain = (pf.Flik - lambda * u) + lambda * fabs(w_cur);
+    if (gain < 0.0) {
+        r.w = w_cur;
+        r.gain = 0.0;
+    } else {
+        r.w = dir * u;
+        r.gain = gain;
+    }
+    return r;
+}
+
+// Full fp64 optimize_edge for the Ising slice (a < b canonical): the kink pass at
+// w = 0 (inc/model.hpp:204-209), then ising_newton64.  Used for existing edges,
+// uncertain kink decisions and the update kernel.
 template <class TP>
 __device__ EdgeOptD ising_optimize_edge64(const TP& T, const uint32_t* __restrict__ Xb, int Mw, int M,
                                           int a, int b, double w_cur, double lambda) {
-    EdgeOptD r;
-    r.warn = 0;
-    r.passes = 1;
-    // kink test at w = 0 (inc/model.hpp:204-209)
-    const Pass64 p0 = ising_pass64<TP, true>(T, Xb, Mw, M, a, b, -w_cur);
+    const Pass64 p0 = w_cur != 0.0 ? ising_pass64<TP, true>(T, Xb, Mw, M, a, b, -w_cur)
+                                   : ising_pass64<TP, false>(T, Xb, Mw, M, a, b, 0.0);
     const double g0 = p0.Lp;
     if (fabs(g0) <= lambda) {
+        EdgeOptD r;
+        r.warn = 0;
+        r.passes = 1;
         double gain = p0.Flik + lambda * fabs(w_cur);  // F(0) - F(w_cur)
         if (w_cur == 0.0) gain = 0.0;
         r.w = 0.0;
@@ -111,57 +188,16 @@ __device__ EdgeOptD ising_optimize_edge64(const TP& T, const uint32_t* __restric
         return r;
     }
     const double dir = g0 > 0.0 ? 1.0 : -1.0;
-    // phi(u) = dir L'(dir u) - lambda, decreasing in u >= 0; phi(0) > 0
-    double lo = 0.0, hi = INFINITY, u = 0.0;
-    double phi = fabs(g0) - lambda, dphi = p0.Lpp;
-    double Fpen = p0.Flik;  // F_lik(0) - F_lik(w_cur) - lambda*0
-    double best_u = 0.0, best_F = Fpen, best_phi = phi, best_dphi = dphi;
-    for (int it = 0; it < 80; ++it) {
-        if (phi > 0.0) lo = u; else hi = u;
-        double un = u - phi / dphi;
-        if (!(un > lo && un < hi) || !isfinite(un)) un = isinf(hi) ? fmax(2.0 * u, 1.0) : 0.5 * (lo + hi);
-        if (un > 0x1.0p64) {  // bracket failure (inc/line_search.hpp:64-84 cap)
-            r.warn = 1;
-            break;
-        }
-        const bool done = fabs(un - u) <= 1e-13 * fmax(1.0, un);
-        u = un;
-        const Pass64 p = ising_pass64<TP, true>(T, Xb, Mw, M, a, b, dir * u - w_cur);
-        ++r.passes;
-        phi = dir * p.Lp - lambda;
-        dphi = p.Lpp;
-        const double F = p.Flik - lambda * u;
-        if (F >= best_F || done) {
-            // plateau guard: the slice saturates numerically for separable columns
-            if (!(F > best_F) && isinf(hi) && u > 64.0) {
-                break;
-            }
-            best_u = u;
-            best_F = F;
-            best_phi = phi;
-            best_dphi = dphi;
-        }
-        if (done) break;
-    }
-    // second-order correction to the last Newton iterate
-    double gain = best_F + lambda * fabs(w_cur);
-    double wstar = dir * best_u;
-    if (best_dphi < 0.0 && isfinite(best_phi)) {
-        const double du = -best_phi / best_dphi;
-        if (fabs(du) <= 1e-6 * fmax(1.0, best_u)) {
-            gain += 0.5 * best_phi * du;
-            wstar = dir * (best_u + du);
-        }
-    }
-    if (gain < 0.0) {  // inc/model.hpp:215
-        r.w = w_cur;
-        r.gain = 0.0;
-    } else {
-        r.w = wstar;
-        r.gain = gain;
-    }
-    return r;
+    return ising_newton64(T, Xb, Mw, M, a, b, w_cur, lambda, dir, fabs(g0) - lambda, p0.Lpp, dir * p0.Lppp, 1);
 }
+
+// T rows staged in shared memory (update kernel: tanh computed once per pair)
+struct TStaged {
+    const double* ta;
+    const double* tb;
+    int a;
+    __device__ __forceinline__ double operator()(int row, int m) const { return row == a ? ta[m] : tb[m]; }
+};
 
 // fp64 likelihood derivative at the current coupling with the L1 subgradient:
 // edge_gradient (inc/model.hpp:175-195).  g = sum 2 x_a x_b - x_b T_a - x_a T_b.

@@ -45,39 +45,6 @@ __device__ __forceinline__ float comp(const float4& v, int c) {
     return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
 }
 
-// fp32 evaluation of L'(w), L''(w) on the register columns of the stationary (S)
-// and partner (P) nodes; per-sample terms are formed with canonical roles
-// (a, b) = (min, max) so the result does not depend on which node is stationary.
-template <int MQ>
-__device__ __forceinline__ void eval32(const Col32<MQ>& CS, const Col32<MQ>& CP, bool s_is_a, int lane,
-                                       int M, float w, float& Lp, float& Lpp) {
-    const float t = tanhf(w);
-    const float omt2 = 1.f - t * t;
-    float lp = 0.f, lpp = 0.f;
-    const int sh = 4 * (lane & 7);
-#pragma unroll
-    for (int q = 0; q < MQ; ++q) {
-        const int mb = 4 * (lane + 32 * q);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            if (mb + c < M) {
-                const uint32_t bs = (CS.w[q] >> (sh + c)) & 1u, bp = (CP.w[q] >> (sh + c)) & 1u;
-                const float ys = flipf(comp(CS.T[q], c), bp);  // x_p T_s
-                const float yp = flipf(comp(CP.T[q], c), bs);  // x_s T_p
-                const float ya = s_is_a ? ys : yp, yb = s_is_a ? yp : ys;
-                const float s2 = (bs == bp) ? 2.f : -2.f;  // 2 x_a x_b
-                const float da = __frcp_rn(1.f + ya * t);
-                const float db = __frcp_rn(1.f + yb * t);
-                const float qa = (ya + t) * da, qb = (yb + t) * db;
-                lp += (s2 - qa) - qb;
-                lpp -= (1.f - ya * ya) * omt2 * da * da + (1.f - yb * yb) * omt2 * db * db;
-            }
-        }
-    }
-    Lp = warp_sum(lp);
-    Lpp = warp_sum(lpp);
-}
-
 // K1: the bandwidth-bound screen.  Pruned pairs are finished here; the rest
 // (survivors, existing edges, kink decisions inside the fp32 error band) are
 // appended to a compacted list for K2.
@@ -87,6 +54,8 @@ __global__ void __launch_bounds__(256, 2) ising_screen_kernel(IsingSnap S, HashV
                                                               const int32_t* __restrict__ ep, uint64_t n,
                                                               int chunk, double lambda, double base,
                                                               ScoreOut out, uint64_t* __restrict__ surv,
+                                                              float* __restrict__ surv_g,
+                                                              uint8_t* __restrict__ surv_flag,
                                                               unsigned long long* __restrict__ nsurv,
                                                               uint64_t* counters) {
     const int lane = threadIdx.x & 31;
@@ -108,11 +77,16 @@ __global__ void __launch_bounds__(256, 2) ising_screen_kernel(IsingSnap S, HashV
                 tabs_s = __ldg(&S.Tabs[s]);
                 cur = s;
             }
+            // issue the partner column and its error-bound sum first (the volatile load
+            // pins Tabs[p] next to the column loads); the W lookup overlaps them
+            float tabs_p;
+            asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(tabs_p) : "l"(S.Tabs + p));
+            load_col32<MQ>(cp, S, p, lane);
             const double wcur = hash_get(W, pair_key(s, p), 0.0);
             bool pruned = false;
+            float gk = 0.f;
+            uint8_t flag = 2;  // 2: existing edge (full fp64), 1: kink inside the error band, 0: survivor
             if (wcur == 0.0) {
-                load_col32<MQ>(cp, S, p, lane);
-                const float tabs_p = __ldg(&S.Tabs[p]);
                 // g0 = 2<x_a,x_b> - sum_m (x_p T_s + x_s T_p)
                 float acc = 0.f;
                 int diff = 0;
@@ -132,6 +106,8 @@ __global__ void __launch_bounds__(256, 2) ising_screen_kernel(IsingSnap S, HashV
                 const float g = (float)(2 * (S.M - 2 * diff)) - acc;
                 const float err = gam * (tabs_s + tabs_p) + 1e-30f;
                 pruned = fabsf(g) <= lam - err;
+                flag = fabsf(g) < lam + err ? 1 : 0;
+                gk = g;
                 ++evals;
             }
             if (pruned) {
@@ -144,21 +120,27 @@ __global__ void __launch_bounds__(256, 2) ising_screen_kernel(IsingSnap S, HashV
                     if (out.warn) out.warn[e] = 0;
                 }
             } else if (lane == 0) {
-                surv[atomicAdd(nsurv, 1ull)] = e;
+                const unsigned long long at = atomicAdd(nsurv, 1ull);
+                surv[at] = e;
+                surv_g[at] = gk;
+                surv_flag[at] = flag;
             }
         }
     }
     if (lane == 0 && counters) atomicAdd((unsigned long long*)&counters[C_EVALS], (unsigned long long)evals);
 }
 
-// K2: survivors.  fp64 kink check where needed, fp32 Newton on register columns,
-// one fp64 pass at the fp32 root with a second-order correction; full fp64
-// routine for existing edges and fp32 failures.
-template <int MQ>
-__global__ void __launch_bounds__(128) ising_refine_kernel(IsingSnap S, HashView W,
-                                                            const int32_t* __restrict__ es,
+// K2: survivors.  Certain survivors (w_cur = 0, |g0| > lambda + err) start Newton
+// from K1's fp32 g0 and the per-node sums Tsq = sum T^2 (second derivative at 0 is
+// -(2M - Tsq_a - Tsq_b)), so no fp64 pass is spent at w = 0: typically one or two
+// fp64 passes without and one with the log1p objective.  Existing edges and kink
+// decisions inside the error band take the full fp64 routine.  (A third-derivative
+// start computed in K1 was tried: it cost K1 35% for no K2 gain.)
+__global__ void __launch_bounds__(128) ising_refine_kernel(IsingSnap S, HashView W, const int32_t* __restrict__ es,
                                                             const int32_t* __restrict__ ep,
-                                                            const uint64_t* __restrict__ surv, uint64_t ns,
+                                                            const uint64_t* __restrict__ surv,
+                                                            const float* __restrict__ surv_g,
+                                                            const uint8_t* __restrict__ surv_flag, uint64_t ns,
                                                             double lambda, double base, ScoreOut out,
                                                             uint64_t* counters) {
     const int lane = threadIdx.x & 31;
@@ -168,70 +150,16 @@ __global__ void __launch_bounds__(128) ising_refine_kernel(IsingSnap S, HashView
     const int s = es[e], p = ep[e];
     const int a = s < p ? s : p, b = s < p ? p : s;
     const TSnap T64{S.T64, S.Mp};
-    const double wcur = hash_get(W, pair_key(a, b), 0.0);
     EdgeOptD r;
-    r.w = 0.0;
-    r.gain = 0.0;
-    r.warn = 0;
-    r.passes = 0;
-    if (wcur != 0.0) {
-        r = ising_optimize_edge64(T64, S.Xb, S.Mw, S.M, a, b, wcur, lambda);
+    if (surv_flag[t] == 0) {
+        const float g = surv_g[t];
+        const double dir = g > 0.f ? 1.0 : -1.0;
+        const double phi0 = fabs((double)g) - lambda;
+        const double phi1 = -(2.0 * S.M - S.Tsq[a] - S.Tsq[b]);
+        r = ising_newton64(T64, S.Xb, S.Mw, S.M, a, b, 0.0, lambda, dir, phi0, phi1, 0.0, 0);
     } else {
-        const double g64 = ising_gradient64(T64, S.Xb, S.Mw, S.M, a, b);
-        r.passes = 1;
-        if (fabs(g64) > lambda) {
-            Col32<MQ> ca, cb;
-            load_col32<MQ>(ca, S, a, lane);
-            load_col32<MQ>(cb, S, b, lane);
-            const float dir = g64 > 0.0 ? 1.f : -1.f;
-            float lo = 0.f, hi = INFINITY, u = 0.f;
-            float Lp, Lpp;
-            eval32<MQ>(ca, cb, true, lane, S.M, 0.f, Lp, Lpp);
-            float phi = (float)(fabs(g64) - lambda), dphi = Lpp;
-            bool ok = false;
-            for (int it = 0; it < 24; ++it) {
-                ++r.passes;
-                if (phi > 0.f) lo = u; else hi = u;
-                float un = u - phi / dphi;
-                if (!(un > lo && un < hi) || !isfinite(un)) un = isinf(hi) ? fmaxf(2.f * u, 1.f) : 0.5f * (lo + hi);
-                const bool done = fabsf(un - u) <= 2e-6f * fmaxf(un, 1e-3f);
-                u = un;
-                if (done) {
-                    ok = true;
-                    break;
-                }
-                if (u > 12.f) break;
-                eval32<MQ>(ca, cb, true, lane, S.M, dir * u, Lp, Lpp);
-                phi = dir * Lp - (float)lambda;
-                dphi = Lpp;
-            }
-            bool fin = false;
-            if (ok && u <= 12.f) {
-                const double ud = (double)u, dird = (double)dir;
-                const Pass64 p64 = ising_pass64<TSnap, true>(T64, S.Xb, S.Mw, S.M, a, b, dird * ud);
-                ++r.passes;
-                const double ph = dird * p64.Lp - lambda, dph = p64.Lpp;
-                if (dph < 0.0) {
-                    const double du = -ph / dph;
-                    if (fabs(du) <= 1e-4 * fmax(1.0, ud)) {
-                        r.w = dird * (ud + du);
-                        r.gain = (p64.Flik - lambda * ud) + 0.5 * ph * du;
-                        if (r.gain < 0.0) {
-                            r.gain = 0.0;
-                            r.w = 0.0;
-                        }
-                        fin = true;
-                    }
-                }
-            }
-            if (!fin) {
-                const EdgeOptD f = ising_optimize_edge64(T64, S.Xb, S.Mw, S.M, a, b, 0.0, lambda);
-                r.w = f.w;
-                r.gain = f.gain;
-                r.warn = f.warn;
-                r.passes += f.passes;
-            }
-        }
+        const double wcur = hash_get(W, pair_key(a, b), 0.0);
+        r = ising_optimize_edge64(T64, S.Xb, S.Mw, S.M, a, b, wcur, lambda);
     }
     if (lane == 0) {
         const double dist = -(base + r.gain);
@@ -350,13 +278,16 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
         const uint64_t blocks = std::min<uint64_t>((chunks + 7) / 8, (uint64_t)sms * 8);
         const IsingSnap S = c.isnap();
         const HashView W = c.Wview();
-        uint64_t* surv = c.s_l.as<uint64_t>(n);
-        unsigned long long* nsurv = c.s_k.as<unsigned long long>(1);
+        uint64_t* surv = c.sc_surv.as<uint64_t>(n);
+        float* surv_g = c.sc_g.as<float>(n);
+        uint8_t* surv_flag = c.sc_flag.as<uint8_t>(n);
+        unsigned long long* nsurv = c.sc_n.as<unsigned long long>(1);
         NRG_CUDA(cudaMemsetAsync(nsurv, 0, 8, c.stream));
         NRG_CUDA(cudaEventRecord(c.kev0, c.stream));
 #define NRG_LAUNCH_MQ(Q)                                                                              \
     ising_screen_kernel<Q><<<(unsigned)blocks, 256, 0, c.stream>>>(S, W, s, p, n, chunk, c.lambda, base, \
-                                                                    out, surv, nsurv, c.dcounters())
+                                                                    out, surv, surv_g, surv_flag, nsurv,   \
+                                                                    c.dcounters())
         switch (MQ) {
             case 1: NRG_LAUNCH_MQ(1); break;
             case 2: NRG_LAUNCH_MQ(2); break;
@@ -389,24 +320,8 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
         if (ns) {
             NRG_CUDA(cudaEventRecord(c.kev0, c.stream));
             const unsigned rb = (unsigned)ceil_div((int64_t)ns * 32, 128);
-#define NRG_LAUNCH_MQ(Q)                                                                        \
-    ising_refine_kernel<Q><<<rb, 128, 0, c.stream>>>(S, W, s, p, surv, ns, c.lambda, base, out, \
-                                                      c.dcounters())
-            switch (MQ) {
-                case 1: NRG_LAUNCH_MQ(1); break;
-                case 2: NRG_LAUNCH_MQ(2); break;
-                case 3: NRG_LAUNCH_MQ(3); break;
-                case 4: NRG_LAUNCH_MQ(4); break;
-                case 5: NRG_LAUNCH_MQ(5); break;
-                case 6: NRG_LAUNCH_MQ(6); break;
-                case 7: NRG_LAUNCH_MQ(7); break;
-                case 8: NRG_LAUNCH_MQ(8); break;
-                case 10: NRG_LAUNCH_MQ(10); break;
-                case 12: NRG_LAUNCH_MQ(12); break;
-                case 14: NRG_LAUNCH_MQ(14); break;
-                case 16: NRG_LAUNCH_MQ(16); break;
-            }
-#undef NRG_LAUNCH_MQ
+            ising_refine_kernel<<<rb, 128, 0, c.stream>>>(S, W, s, p, surv, surv_g, surv_flag, ns, c.lambda, base, out,
+                                                          c.dcounters());
             NRG_LAUNCH_CHECK();
             NRG_CUDA(cudaEventRecord(c.kev1, c.stream));
             NRG_CUDA(cudaEventSynchronize(c.kev1));

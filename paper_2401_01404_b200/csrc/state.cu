@@ -14,15 +14,12 @@ namespace nrg {
 
 Context::~Context() {
     if (device >= 0) cudaSetDevice(device);
-    for (DevBuf* b : {&Xb, &Xd, &H, &theta, &Wkeys, &Wvals, &Wcount, &T32, &T64, &Tabs, &U, &xx,
-                      &Ckeys, &Cvals, &Ccount, &table, &line, &counters, &s_a, &s_b, &s_c, &s_d,
-                      &s_e, &s_f, &s_g, &s_h, &s_i, &s_j, &s_k, &s_l, &s_m, &s_n, &s_o, &red})
-        b->release();
+    // DevBuf members release themselves; the device must be current for cudaFree
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
     if (kev0) cudaEventDestroy(kev0);
     if (kev1) cudaEventDestroy(kev1);
-    if (stream) cudaStreamDestroy(stream);
+    tl_stream = stream;  // members free in stream order; StreamOwner destroys the stream last
 }
 
 static uint64_t next_pow2(uint64_t v) {
@@ -42,6 +39,14 @@ void ctx_init(Context& c, int n, int m, int kind, double lambda, int device) {
     c.device = device;
     NRG_CUDA(cudaSetDevice(device));
     NRG_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    c.stream_owner.s = c.stream;
+    tl_stream = c.stream;
+    {
+        cudaMemPool_t pool;
+        NRG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = UINT64_MAX;
+        NRG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    }
     NRG_CUDA(cudaEventCreate(&c.ev0));
     NRG_CUDA(cudaEventCreate(&c.ev1));
     NRG_CUDA(cudaEventCreate(&c.kev0));
@@ -271,11 +276,8 @@ void w_reserve(Context& c, uint64_t extra) {
         (unsigned long long*)(dcnt + 1));
     NRG_LAUNCH_CHECK();
     c.sync();
-    c.Wkeys.release();
-    c.Wvals.release();
-    c.Wkeys = nk;
-    c.Wvals = nv;
-    nk.p = nv.p = nullptr;
+    c.Wkeys = std::move(nk);
+    c.Wvals = std::move(nv);
     c.Wcap = ncap;
 }
 
@@ -311,10 +313,10 @@ void get_sums(Context& c, double* out) {
 // bandwidth-bound screen, with sum|T32| per node for its rigorous error bound.
 __global__ void snapshot_ising_kernel(const double* __restrict__ H, const double* __restrict__ theta,
                                       int M, int Mp, double* __restrict__ T64, float* __restrict__ T32,
-                                      float* __restrict__ Tabs) {
+                                      float* __restrict__ Tabs, double* __restrict__ Tsq) {
     const int r = blockIdx.x;
     const double th = theta[r];
-    double a = 0.0;
+    double a = 0.0, q = 0.0;
     for (int m = threadIdx.x; m < Mp; m += blockDim.x) {
         double t = 0.0;
         if (m < M) t = tanh(H[(size_t)r * Mp + m] + th);
@@ -322,15 +324,25 @@ __global__ void snapshot_ising_kernel(const double* __restrict__ H, const double
         const float f = (float)t;
         T32[(size_t)r * Mp + m] = f;
         a += fabs((double)f);
+        q += t * t;
     }
-    __shared__ double sh[32];
+    __shared__ double sh[32], sq[32];
     a = warp_sum(a);
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = a;
+    q = warp_sum(q);
+    if ((threadIdx.x & 31) == 0) {
+        sh[threadIdx.x >> 5] = a;
+        sq[threadIdx.x >> 5] = q;
+    }
     __syncthreads();
     if (threadIdx.x < 32) {
         double v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+        double w = threadIdx.x < (blockDim.x >> 5) ? sq[threadIdx.x] : 0.0;
         v = warp_sum(v);
-        if (threadIdx.x == 0) Tabs[r] = __double2float_ru(v * (1.0 + 1e-12));
+        w = warp_sum(w);
+        if (threadIdx.x == 0) {
+            Tabs[r] = __double2float_ru(v * (1.0 + 1e-12));
+            Tsq[r] = w;
+        }
     }
 }
 
@@ -366,10 +378,12 @@ void ensure_snapshot(Context& c) {
         c.T64.ensure(nm * 8);
         c.T32.ensure(nm * 4);
         c.Tabs.ensure((size_t)c.n * 4);
+        c.Tsq.ensure((size_t)c.n * 8);
         snapshot_ising_kernel<<<c.n, 256, 0, c.stream>>>(c.dH(), c.dtheta(), c.M, c.Mp,
                                                          static_cast<double*>(c.T64.p),
                                                          static_cast<float*>(c.T32.p),
-                                                         static_cast<float*>(c.Tabs.p));
+                                                         static_cast<float*>(c.Tabs.p),
+                                                         static_cast<double*>(c.Tsq.p));
     } else {
         c.U.ensure(nm * 8);
         c.xx.ensure((size_t)c.n * 8);
@@ -524,11 +538,8 @@ void cache_reserve(Context& c, uint64_t extra) {
     }
     if (!c.Ccap) NRG_CUDA(cudaMemsetAsync(c.Ccount.p, 0, 8, c.stream));
     c.sync();
-    c.Ckeys.release();
-    c.Cvals.release();
-    c.Ckeys = nk;
-    c.Cvals = nv;
-    nk.p = nv.p = nullptr;
+    c.Ckeys = std::move(nk);
+    c.Cvals = std::move(nv);
     c.Ccap = ncap;
 }
 

@@ -103,10 +103,14 @@ struct UpdateArgs {
     unsigned long long* ticket;
     double* absdelta;
     uint64_t* counters;
+    int stage;  // stage tanh(H + theta) of both rows in shared memory once per pair
 };
 
 __global__ void __launch_bounds__(128) update_kernel(UpdateArgs A) {
+    extern __shared__ double stage_smem[];
     const int lane = threadIdx.x & 31;
+    double* ta = stage_smem + (size_t)(threadIdx.x >> 5) * 2 * A.Mp;
+    double* tb = ta + A.Mp;
     uint64_t evals = 0, warns = 0;
     for (;;) {
         unsigned long long p = 0;
@@ -135,8 +139,18 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs A) {
         if (A.assign) {
             w = A.assign[p];
         } else if (A.kind == ISING) {
-            const TLive T{A.H, A.theta, A.Mp};
-            const EdgeOptD r = ising_optimize_edge64(T, A.Xb, A.Mw, A.M, a, b, wcur, A.lambda);
+            EdgeOptD r;
+            if (A.stage) {
+                const double tha = __ldcg(&A.theta[a]), thb = __ldcg(&A.theta[b]);
+                for (int m = lane; m < A.M; m += 32) {
+                    ta[m] = tanh(__ldcg(&A.H[(size_t)a * A.Mp + m]) + tha);
+                    tb[m] = tanh(__ldcg(&A.H[(size_t)b * A.Mp + m]) + thb);
+                }
+                __syncwarp();
+                r = ising_optimize_edge64(TStaged{ta, tb, a}, A.Xb, A.Mw, A.M, a, b, wcur, A.lambda);
+            } else {
+                r = ising_optimize_edge64(TLive{A.H, A.theta, A.Mp}, A.Xb, A.Mw, A.M, a, b, wcur, A.lambda);
+            }
             w = r.w;
             evals += r.passes;
             warns += r.warn;
@@ -210,15 +224,13 @@ __global__ void __launch_bounds__(1024) sum_fixed_kernel(const double* __restric
     }
 }
 
-static int update_grid(Context& c) {
-    static int blocks = 0;
-    if (!blocks) {
-        int sms = 0, per = 0;
-        NRG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
-        NRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, update_kernel, 128, 0));
-        blocks = sms * std::max(1, per);
-    }
-    return blocks;
+static int update_grid(Context& c, size_t smem) {
+    int sms = 0, per = 0;
+    NRG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+    if (smem > 48 * 1024)
+        NRG_CUDA(cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    NRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, update_kernel, 128, smem));
+    return sms * std::max(1, per);
 }
 
 double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n, const double* assign) {
@@ -265,10 +277,13 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
     A.ticket = ticket;
     A.absdelta = absdelta;
     A.counters = c.dcounters();
-    int grid = (int)std::min<uint64_t>(update_grid(c), ceil_div(n * 32, 128));
+    const size_t smem = (size_t)4 * 2 * c.Mp * sizeof(double);
+    A.stage = (c.kind == ISING && smem <= 160 * 1024) ? 1 : 0;
+    const size_t smem_use = A.stage ? smem : 0;
+    int grid = (int)std::min<uint64_t>(update_grid(c, smem_use), ceil_div(n * 32, 128));
     const bool dbg = getenv("NRG_DEBUG_UPDATES") != nullptr;
     if (dbg && getenv("NRG_DEBUG_SERIAL")) grid = 1;
-    update_kernel<<<grid, dbg && getenv("NRG_DEBUG_SERIAL") ? 32 : 128, 0, c.stream>>>(A);
+    update_kernel<<<grid, dbg && getenv("NRG_DEBUG_SERIAL") ? 32 : 128, smem_use, c.stream>>>(A);
     NRG_LAUNCH_CHECK();
     if (dbg) {
         std::vector<int32_t> hd(2 * n), hi(n), hj(n);
