@@ -23,6 +23,67 @@ __device__ __forceinline__ double xsign(uint32_t word, int bit) {
     return ((word >> bit) & 1u) ? 1.0 : -1.0;
 }
 
+// Reduction scope of the per-sample loops: one warp (scoring kernels) or one CTA
+// (update kernel, where a dependency chain of updates makes per-update latency the
+// bound).  Element m of a row is owned by thread m % NT of the scope.
+struct WarpScope {
+    static constexpr int NT = 32;
+    __device__ __forceinline__ int tid() const { return threadIdx.x & 31; }
+    __device__ __forceinline__ void sum4(double& a, double& b, double& c, double& d) const {
+        a = warp_sum(a);
+        b = warp_sum(b);
+        c = warp_sum(c);
+        d = warp_sum(d);
+    }
+    __device__ __forceinline__ double sum(double a) const { return warp_sum(a); }
+};
+template <int NT_>
+struct BlockScope {
+    static constexpr int NT = NT_;
+    double* red;  // shared scratch: 4 * (NT/32) + 4 doubles
+    __device__ __forceinline__ int tid() const { return threadIdx.x; }
+    __device__ __forceinline__ void sum4(double& a, double& b, double& c, double& d) const {
+        constexpr int W = NT / 32;
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        a = warp_sum(a);
+        b = warp_sum(b);
+        c = warp_sum(c);
+        d = warp_sum(d);
+        if (lane == 0) {
+            red[4 * w + 0] = a;
+            red[4 * w + 1] = b;
+            red[4 * w + 2] = c;
+            red[4 * w + 3] = d;
+        }
+        __syncthreads();
+        if (w == 0) {
+            double x0 = lane < W ? red[4 * lane + 0] : 0.0, x1 = lane < W ? red[4 * lane + 1] : 0.0;
+            double x2 = lane < W ? red[4 * lane + 2] : 0.0, x3 = lane < W ? red[4 * lane + 3] : 0.0;
+            x0 = warp_sum(x0);
+            x1 = warp_sum(x1);
+            x2 = warp_sum(x2);
+            x3 = warp_sum(x3);
+            if (lane == 0) {
+                red[4 * W + 0] = x0;
+                red[4 * W + 1] = x1;
+                red[4 * W + 2] = x2;
+                red[4 * W + 3] = x3;
+            }
+        }
+        __syncthreads();
+        a = red[4 * W + 0];
+        b = red[4 * W + 1];
+        c = red[4 * W + 2];
+        d = red[4 * W + 3];
+        __syncthreads();  // scratch reusable
+    }
+    __device__ __forceinline__ double sum(double a) const {
+        double b = 0.0, c = 0.0, d = 0.0;
+        sum4(a, b, c, d);
+        return a;
+    }
+};
+
 // Result of one fp64 pass over the samples at coupling w (D = w - w_cur).
 struct Pass64 {
     double Lp;    // L'(w)
@@ -48,23 +109,22 @@ struct TLive {
     }
 };
 
-// One warp-wide fp64 pass (all lanes participate; result valid in all lanes).
-template <class TP, bool kNeedF>
+// One fp64 pass over the samples by the whole scope (result valid in every thread).
+template <class TP, bool kNeedF, class SC = WarpScope>
 __device__ __forceinline__ Pass64 ising_pass64(const TP& T, const uint32_t* __restrict__ Xb, int Mw,
-                                               int M, int a, int b, double D) {
-    const int lane = threadIdx.x & 31;
+                                               int M, int a, int b, double D, const SC& sc = SC()) {
+    const int tid = sc.tid();
     const double t = tanh(D);
     const double omt2 = 1.0 - t * t;
     const double A = fabs(D);
     const double sg = D > 0.0 ? 1.0 : (D < 0.0 ? -1.0 : 0.0);
     const double E = -expm1(-2.0 * A);  // 1 - e^{-2|D|}
     double Lp = 0.0, Lpp = 0.0, L3 = 0.0, F = 0.0;
-    for (int k = 0; k * 32 < M; ++k) {
-        const int m = lane + 32 * k;
-        const uint32_t wa = __ldg(&Xb[(size_t)a * Mw + k]);
-        const uint32_t wb = __ldg(&Xb[(size_t)b * Mw + k]);
-        if (m < M) {
-            const double xa = xsign(wa, lane), xb = xsign(wb, lane);
+    for (int m = tid; m < M; m += SC::NT) {
+        const uint32_t wa = __ldg(&Xb[(size_t)a * Mw + (m >> 5)]);
+        const uint32_t wb = __ldg(&Xb[(size_t)b * Mw + (m >> 5)]);
+        {
+            const double xa = xsign(wa, m & 31), xb = xsign(wb, m & 31);
             const double ya = xb * T(a, m);
             const double yb = xa * T(b, m);
             const double s = xa * xb;
@@ -82,11 +142,12 @@ __device__ __forceinline__ Pass64 ising_pass64(const TP& T, const uint32_t* __re
             }
         }
     }
+    sc.sum4(Lp, Lpp, L3, F);
     Pass64 r;
-    r.Lp = warp_sum(Lp);
-    r.Lpp = warp_sum(Lpp);
-    r.Lppp = warp_sum(L3);
-    r.Flik = kNeedF ? warp_sum(F) : 0.0;
+    r.Lp = Lp;
+    r.Lpp = Lpp;
+    r.Lppp = L3;
+    r.Flik = kNeedF ? F : 0.0;
     return r;
 }
 
@@ -100,10 +161,10 @@ struct EdgeOptD {
 // started from the root of the quadratic model phi0 + phi1 u + phi2 u^2/2 (phi1 < 0).
 // Passes without the log1p objective until the step predicts convergence; the last
 // pass evaluates the slice gain and applies the second-order Newton correction.
-template <class TP>
+template <class TP, class SC = WarpScope>
 __device__ EdgeOptD ising_newton64(const TP& T, const uint32_t* __restrict__ Xb, int Mw, int M, int a, int b,
                                    double w_cur, double lambda, double dir, double phi0, double phi1,
-                                   double phi2, int passes) {
+                                   double phi2, int passes, const SC& sc = SC()) {
     EdgeOptD r;
     r.warn = 0;
     r.passes = passes;
@@ -118,8 +179,8 @@ __device__ EdgeOptD ising_newton64(const TP& T, const uint32_t* __restrict__ Xb,
         const double scale = fmax(u, 1e-3);
         const bool final_try = fabs(du_last) <= 0.03 * scale;
         const double D = dir * u - w_cur;
-        const Pass64 p = final_try ? ising_pass64<TP, true>(T, Xb, Mw, M, a, b, D)
-                                   : ising_pass64<TP, false>(T, Xb, Mw, M, a, b, D);
+        const Pass64 p = final_try ? ising_pass64<TP, true, SC>(T, Xb, Mw, M, a, b, D, sc)
+                                   : ising_pass64<TP, false, SC>(T, Xb, Mw, M, a, b, D, sc);
         ++r.passes;
         const double phi = dir * p.Lp - lambda, dphi = p.Lpp;
         const double du = (dphi < 0.0) ? -phi / dphi : NAN;
@@ -144,7 +205,7 @@ __device__ EdgeOptD ising_newton64(const TP& T, const uint32_t* __restrict__ Xb,
         if (isinf(hi) && un > 64.0) {
             // separable columns: the slice saturates numerically; stop once the
             // objective no longer increases (the reference's doubling stops there too)
-            const Pass64 pf = ising_pass64<TP, true>(T, Xb, Mw, M, a, b, dir * un - w_cur);
+            const Pass64 pf = ising_pass64<TP, true, SC>(T, Xb, Mw, M, a, b, dir * un - w_cur, sc);
             ++r.passes;
             const double F = pf.Flik - lambda * un;
             if (!(F > prevF)) break;
@@ -155,7 +216,7 @@ __device__ EdgeOptD ising_newton64(const TP& T, const uint32_t* __restrict__ Xb,
         if (hi - lo <= 1e-15 * fmax(1.0, u)) du_last = 0.0;
     }
     // plateau / bracket failure: objective at the last iterate
-    const Pass64 pf = ising_pass64<TP, true>(T, Xb, Mw, M, a, b, dir * u - w_cur);
+    const Pass64 pf = ising_pass64<TP, true, SC>(T, Xb, Mw, M, a, b, dir * u - w_cur, sc);
     ++r.passes;
     const double gain = (pf.Flik - lambda * u) + lambda * fabs(w_cur);
     if (gain < 0.0) {
@@ -171,11 +232,11 @@ __device__ EdgeOptD ising_newton64(const TP& T, const uint32_t* __restrict__ Xb,
 // Full fp64 optimize_edge for the Ising slice (a < b canonical): the kink pass at
 // w = 0 (inc/model.hpp:204-209), then ising_newton64.  Used for existing edges,
 // uncertain kink decisions and the update kernel.
-template <class TP>
+template <class TP, class SC = WarpScope>
 __device__ EdgeOptD ising_optimize_edge64(const TP& T, const uint32_t* __restrict__ Xb, int Mw, int M,
-                                          int a, int b, double w_cur, double lambda) {
-    const Pass64 p0 = w_cur != 0.0 ? ising_pass64<TP, true>(T, Xb, Mw, M, a, b, -w_cur)
-                                   : ising_pass64<TP, false>(T, Xb, Mw, M, a, b, 0.0);
+                                          int a, int b, double w_cur, double lambda, const SC& sc = SC()) {
+    const Pass64 p0 = w_cur != 0.0 ? ising_pass64<TP, true, SC>(T, Xb, Mw, M, a, b, -w_cur, sc)
+                                   : ising_pass64<TP, false, SC>(T, Xb, Mw, M, a, b, 0.0, sc);
     const double g0 = p0.Lp;
     if (fabs(g0) <= lambda) {
         EdgeOptD r;
@@ -188,7 +249,8 @@ __device__ EdgeOptD ising_optimize_edge64(const TP& T, const uint32_t* __restric
         return r;
     }
     const double dir = g0 > 0.0 ? 1.0 : -1.0;
-    return ising_newton64(T, Xb, Mw, M, a, b, w_cur, lambda, dir, fabs(g0) - lambda, p0.Lpp, dir * p0.Lppp, 1);
+    return ising_newton64<TP, SC>(T, Xb, Mw, M, a, b, w_cur, lambda, dir, fabs(g0) - lambda, p0.Lpp,
+                                  dir * p0.Lppp, 1, sc);
 }
 
 // T rows staged in shared memory (update kernel: tanh computed once per pair)
@@ -225,18 +287,17 @@ __device__ __forceinline__ double ising_gradient64(const TP& T, const uint32_t* 
 struct GaussCoef {
     double P, Hc;
 };
-template <class UP>
+template <class UP, class SC = WarpScope>
 __device__ __forceinline__ GaussCoef gauss_coef(const UP& Uf, const double* __restrict__ X, int Mp, int M,
                                                 int a, int b, double ta2, double tb2, double xxa,
-                                                double xxb) {
-    const int lane = threadIdx.x & 31;
+                                                double xxb, const SC& sc = SC()) {
     double P = 0.0;
-    for (int m = lane; m < M; m += 32) {
+    for (int m = sc.tid(); m < M; m += SC::NT) {
         const double xa = X[(size_t)a * Mp + m], xb = X[(size_t)b * Mp + m];
         P += Uf(a, m) * xb + Uf(b, m) * xa;
     }
     GaussCoef c;
-    c.P = warp_sum(P);
+    c.P = sc.sum(P);
     c.Hc = ta2 * xxb + tb2 * xxa;
     return c;
 }

@@ -106,35 +106,45 @@ struct UpdateArgs {
     int stage;  // stage tanh(H + theta) of both rows in shared memory once per pair
 };
 
-__global__ void __launch_bounds__(128) update_kernel(UpdateArgs A) {
+// One CTA per update: the chain of dependent updates is the critical path (thousands
+// of levels at config 4), so per-update latency, not throughput, bounds the phase;
+// NT threads share each pass over the samples with block reductions.
+template <int NT>
+__global__ void __launch_bounds__(NT) update_kernel(UpdateArgs A) {
     extern __shared__ double stage_smem[];
-    const int lane = threadIdx.x & 31;
-    double* ta = stage_smem + (size_t)(threadIdx.x >> 5) * 2 * A.Mp;
+    __shared__ double red[4 * (NT / 32) + 4];
+    __shared__ unsigned long long s_p;
+    __shared__ double s_w;
+    const int tid = threadIdx.x;
+    const BlockScope<NT> sc{red};
+    double* ta = stage_smem;
     double* tb = ta + A.Mp;
     uint64_t evals = 0, warns = 0;
     for (;;) {
-        unsigned long long p = 0;
-        if (lane == 0) p = atomicAdd(A.ticket, 1ull);
-        p = __shfl_sync(0xffffffffu, p, 0);
-        if (p >= A.n) break;
-        // wait for the predecessors on both endpoints
-        if (lane == 0) {
-            const int d0 = A.dep[2 * p], d1 = A.dep[2 * p + 1];
-            if (d0 >= 0)
-                while (atomicAdd(&A.done[d0], 0) == 0) __nanosleep(64);
-            if (d1 >= 0)
-                while (atomicAdd(&A.done[d1], 0) == 0) __nanosleep(64);
+        if (tid == 0) {
+            unsigned long long p = atomicAdd(A.ticket, 1ull);
+            if (p < A.n) {
+                // wait for the predecessors on both endpoints
+                const int d0 = A.dep[2 * p], d1 = A.dep[2 * p + 1];
+                if (d0 >= 0)
+                    while (atomicAdd(&A.done[d0], 0) == 0) __nanosleep(32);
+                if (d1 >= 0)
+                    while (atomicAdd(&A.done[d1], 0) == 0) __nanosleep(32);
+                __threadfence();
+            }
+            s_p = p;
         }
-        __syncwarp();
+        __syncthreads();
+        const unsigned long long p = s_p;
+        if (p >= A.n) break;
         __threadfence();
         const int i0 = A.ci[p], j0 = A.cj[p];
         const int a = min(i0, j0), b = max(i0, j0);
         const uint64_t key = pair_key(a, b);
-        // one lane reads W and broadcasts: lanes are not in lockstep (independent
-        // thread scheduling), so a per-lane read could observe this pair's own write
-        double wcur = 0.0;
-        if (lane == 0) wcur = hash_get_cg(A.W, key);
-        wcur = __shfl_sync(0xffffffffu, wcur, 0);
+        // one thread reads W and broadcasts (threads are not in lockstep)
+        if (tid == 0) s_w = hash_get_cg(A.W, key);
+        __syncthreads();
+        const double wcur = s_w;
         double w;
         if (A.assign) {
             w = A.assign[p];
@@ -142,65 +152,66 @@ __global__ void __launch_bounds__(128) update_kernel(UpdateArgs A) {
             EdgeOptD r;
             if (A.stage) {
                 const double tha = __ldcg(&A.theta[a]), thb = __ldcg(&A.theta[b]);
-                for (int m = lane; m < A.M; m += 32) {
+                for (int m = tid; m < A.M; m += NT) {
                     ta[m] = tanh(__ldcg(&A.H[(size_t)a * A.Mp + m]) + tha);
                     tb[m] = tanh(__ldcg(&A.H[(size_t)b * A.Mp + m]) + thb);
                 }
-                __syncwarp();
-                r = ising_optimize_edge64(TStaged{ta, tb, a}, A.Xb, A.Mw, A.M, a, b, wcur, A.lambda);
+                __syncthreads();
+                r = ising_optimize_edge64<TStaged, BlockScope<NT>>(TStaged{ta, tb, a}, A.Xb, A.Mw, A.M, a, b, wcur,
+                                                                   A.lambda, sc);
             } else {
-                r = ising_optimize_edge64(TLive{A.H, A.theta, A.Mp}, A.Xb, A.Mw, A.M, a, b, wcur, A.lambda);
+                r = ising_optimize_edge64<TLive, BlockScope<NT>>(TLive{A.H, A.theta, A.Mp}, A.Xb, A.Mw, A.M, a, b,
+                                                                 wcur, A.lambda, sc);
             }
             w = r.w;
             evals += r.passes;
             warns += r.warn;
         } else {
             const ULive Uf{A.Xd, A.H, A.theta, A.Mp};
-            double xxa = 0.0, xxb = 0.0;
-            for (int m = lane; m < A.M; m += 32) {
+            double xxa = 0.0, xxb = 0.0, z0 = 0.0, z1 = 0.0;
+            for (int m = tid; m < A.M; m += NT) {
                 const double va = A.Xd[(size_t)a * A.Mp + m], vb = A.Xd[(size_t)b * A.Mp + m];
                 xxa += va * va;
                 xxb += vb * vb;
             }
-            xxa = warp_sum(xxa);
-            xxb = warp_sum(xxb);
-            const double ta = __ldcg(&A.theta[a]), tb = __ldcg(&A.theta[b]);
-            const GaussCoef cf = gauss_coef(Uf, A.Xd, A.Mp, A.M, a, b, ta * ta, tb * tb, xxa, xxb);
+            sc.sum4(xxa, xxb, z0, z1);
+            const double tha = __ldcg(&A.theta[a]), thb = __ldcg(&A.theta[b]);
+            const GaussCoef cf = gauss_coef<ULive, BlockScope<NT>>(Uf, A.Xd, A.Mp, A.M, a, b, tha * tha, thb * thb,
+                                                                  xxa, xxb, sc);
             const EdgeOptD r = gauss_optimize(cf, wcur, A.lambda);
             w = r.w;
             evals += r.passes;
         }
         // Delta accumulation and set_edge (inc/reconstruct.hpp:78-79)
         const double delta = w - wcur;
-        if (lane == 0) A.absdelta[p] = fabs(w - wcur);
         if (delta != 0.0) {
             double* Ha = A.H + (size_t)a * A.Mp;
             double* Hb = A.H + (size_t)b * A.Mp;
             if (A.kind == ISING) {
-                for (int k = 0; k * 32 < A.M; ++k) {
-                    const int m = lane + 32 * k;
-                    if (m < A.M) {
-                        const uint32_t wa = A.Xb[(size_t)a * A.Mw + k], wb = A.Xb[(size_t)b * A.Mw + k];
-                        const double xa = xsign(wa, lane), xb = xsign(wb, lane);
-                        __stcg(&Ha[m], __ldcg(&Ha[m]) + delta * xb);
-                        __stcg(&Hb[m], __ldcg(&Hb[m]) + delta * xa);
-                    }
+                for (int m = tid; m < A.M; m += NT) {
+                    const uint32_t wa = A.Xb[(size_t)a * A.Mw + (m >> 5)], wb = A.Xb[(size_t)b * A.Mw + (m >> 5)];
+                    const double xa = xsign(wa, m & 31), xb = xsign(wb, m & 31);
+                    __stcg(&Ha[m], __ldcg(&Ha[m]) + delta * xb);
+                    __stcg(&Hb[m], __ldcg(&Hb[m]) + delta * xa);
                 }
             } else {
-                for (int m = lane; m < A.M; m += 32) {
+                for (int m = tid; m < A.M; m += NT) {
                     const double xa = A.Xd[(size_t)a * A.Mp + m], xb = A.Xd[(size_t)b * A.Mp + m];
                     __stcg(&Ha[m], __dadd_rn(__ldcg(&Ha[m]), __dmul_rn(delta, xb)));
                     __stcg(&Hb[m], __dadd_rn(__ldcg(&Hb[m]), __dmul_rn(delta, xa)));
                 }
             }
         }
-        __syncwarp();  // every lane has read W and H before lane 0 publishes the new W
-        if (lane == 0 && (delta != 0.0 || w == 0.0)) hash_set(A.W, key, w, A.Wcnt);
         __threadfence();
-        __syncwarp();
-        if (lane == 0) atomicExch(&A.done[p], 1);
+        __syncthreads();  // every thread has read W / H and written H before W and the flag publish
+        if (tid == 0) {
+            A.absdelta[p] = fabs(w - wcur);
+            if (delta != 0.0 || w == 0.0) hash_set(A.W, key, w, A.Wcnt);
+            __threadfence();
+            atomicExch(&A.done[p], 1);
+        }
     }
-    if (lane == 0) {
+    if (tid == 0) {
         if (evals) atomicAdd((unsigned long long*)&A.counters[C_EVALS], (unsigned long long)evals);
         if (warns) atomicAdd((unsigned long long*)&A.counters[C_WARN], (unsigned long long)warns);
     }
@@ -224,13 +235,16 @@ __global__ void __launch_bounds__(1024) sum_fixed_kernel(const double* __restric
     }
 }
 
+constexpr int kUpdNT = 256;
+
 static int update_grid(Context& c, size_t smem) {
     int sms = 0, per = 0;
     NRG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
     if (smem > 48 * 1024)
-        NRG_CUDA(cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    NRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, update_kernel, 128, smem));
-    return sms * std::max(1, per);
+        NRG_CUDA(cudaFuncSetAttribute(update_kernel<kUpdNT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    NRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, update_kernel<kUpdNT>, kUpdNT, smem));
+    if (per < 1) fail(100, "update kernel does not fit on an SM");
+    return sms * per;  // persistent grid: every CTA resident (the dependency waits need it)
 }
 
 double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n, const double* assign) {
@@ -277,13 +291,13 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
     A.ticket = ticket;
     A.absdelta = absdelta;
     A.counters = c.dcounters();
-    const size_t smem = (size_t)4 * 2 * c.Mp * sizeof(double);
+    const size_t smem = (size_t)2 * c.Mp * sizeof(double);
     A.stage = (c.kind == ISING && smem <= 160 * 1024) ? 1 : 0;
     const size_t smem_use = A.stage ? smem : 0;
-    int grid = (int)std::min<uint64_t>(update_grid(c, smem_use), ceil_div(n * 32, 128));
+    int grid = (int)std::min<uint64_t>(update_grid(c, smem_use), n);
     const bool dbg = getenv("NRG_DEBUG_UPDATES") != nullptr;
     if (dbg && getenv("NRG_DEBUG_SERIAL")) grid = 1;
-    update_kernel<<<grid, dbg && getenv("NRG_DEBUG_SERIAL") ? 32 : 128, smem_use, c.stream>>>(A);
+    update_kernel<kUpdNT><<<grid, kUpdNT, smem_use, c.stream>>>(A);
     NRG_LAUNCH_CHECK();
     if (dbg) {
         std::vector<int32_t> hd(2 * n), hi(n), hj(n);
