@@ -216,11 +216,21 @@ int nrg_sample_scored_pairs(nrg_ctx* ctx, uint64_t cap, uint64_t seed, int32_t* 
 int nrg_generate_ising(nrg_ctx* ctx, double mean_deg, double w_sigma, double th_sigma,
                        int32_t burn_in, int32_t thin, uint64_t seed, int8_t* X_out);
 
-/* Multi-GPU: node-sharded NNDescent over NCCL.  rank 0 calls
- * nrg_comm_unique_id and broadcasts the 128-byte id; every rank then calls
- * nrg_comm_init.  world == 1 or no call = single GPU. */
+/* Multi-GPU: samples, sums, W and theta replicated (updates and theta
+ * passes run identically on every rank); NNDescent nodes sharded by contiguous ranges;
+ * the per-generation distance cache sharded by pair key, so each unique pair is scored
+ * once job-wide (two all-to-alls per sweep route requests and answers); kNN rows
+ * all-gathered once per sweep; churn all-reduced; base broadcast from rank 0.  Every
+ * rank issues the same calls with the same inputs.
+ * NCCL: rank 0 calls nrg_comm_unique_id and shares the 128-byte id; every rank then
+ * calls nrg_comm_init.  world == 1 or no call = single GPU. */
 int nrg_comm_unique_id(uint8_t id[128]);
 int nrg_comm_init(nrg_ctx* ctx, const uint8_t id[128], int32_t rank, int32_t world);
+/* In-process loopback group (one host thread per virtual rank, contexts on one or more
+ * devices of this process): the same sharded path without NCCL, for verification. */
+int nrg_loopback_create(int32_t world, void** group);
+int nrg_loopback_destroy(void* group);
+int nrg_comm_init_loopback(nrg_ctx* ctx, void* group, int32_t rank);
 
 #ifdef __cplusplus
 }

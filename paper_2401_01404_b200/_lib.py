@@ -91,6 +91,9 @@ SIGNATURES = {
     "nrg_generate_ising": (C.c_int, [_P, _d, _d, _d, _i32, _i32, _u64, _VP]),
     "nrg_comm_unique_id": (C.c_int, [C.c_char_p]),
     "nrg_comm_init": (C.c_int, [_P, C.c_char_p, _i32, _i32]),
+    "nrg_loopback_create": (C.c_int, [_i32, C.POINTER(_VP)]),
+    "nrg_loopback_destroy": (C.c_int, [_VP]),
+    "nrg_comm_init_loopback": (C.c_int, [_P, _VP, _i32]),
 }
 
 _lib: C.CDLL | None = None
@@ -328,11 +331,40 @@ class Model:
         check(self.L.nrg_sample_scored_pairs(self.h, cap, seed, i, j, C.byref(n)))
         return i[: n.value].copy(), j[: n.value].copy()
 
+    def comm_init(self, uid: bytes, rank: int, world: int):
+        """Join an NCCL job (uid from comm_unique_id() on rank 0)."""
+        check(self.L.nrg_comm_init(self.h, uid, rank, world))
+
+    def comm_init_loopback(self, group, rank: int):
+        check(self.L.nrg_comm_init_loopback(self.h, group, rank))
+
     def phase_times(self):
         out = np.zeros(7)
         check(self.L.nrg_phase_times(self.h, out, 7))
         names = ["score", "knn", "select", "update", "theta", "logpost", "snapshot"]
         return dict(zip(names, out.tolist()))
+
+
+def comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(load().nrg_comm_unique_id(buf))
+    return buf.raw
+
+
+class LoopbackGroup:
+    """In-process group of virtual ranks (one host thread per rank)."""
+
+    def __init__(self, world: int):
+        self.L = load()
+        h = C.c_void_p()
+        check(self.L.nrg_loopback_create(world, C.byref(h)))
+        self.h = h
+        self.world = world
+
+    def close(self):
+        if self.h:
+            self.L.nrg_loopback_destroy(self.h)
+            self.h = None
 
 
 def recall_curve(exact, approx):

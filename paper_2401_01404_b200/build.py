@@ -74,6 +74,23 @@ def build_lib(verbose: bool = False, jobs: int | None = None) -> Path:
     return LIB
 
 
+def build_cpp_tests(verbose: bool = False) -> Path:
+    """tests/cpp/test_dropin.cpp against include/netrec_b200/netrec.hpp + the library."""
+    src = ROOT / "tests" / "cpp" / "test_dropin.cpp"
+    out = PKG / "test_dropin"
+    deps = [src, LIB, ROOT / "include" / "netrec_b200" / "netrec.hpp", ROOT / "include" / "netrec_b200.h"]
+    if _stale(out, deps):
+        cmd = ["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", str(src), f"-L{PKG}", "-lnetrec_b200",
+               "-Wl,-rpath,$ORIGIN", "-o", str(out)]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("C++ drop-in test build failed")
+    return out
+
+
 def build_oracle(verbose: bool = False) -> None:
     """oracle/_build/libnrg_oracle.so always; oracle/_ref/libnetrec_ref.so when the
     reference headers are present (this container, not the GPU box)."""
@@ -92,6 +109,7 @@ def main() -> None:
     ap.add_argument("-v", "--verbose", action="store_true")
     a = ap.parse_args()
     print(build_lib(a.verbose))
+    print(build_cpp_tests(a.verbose))
     if a.oracle:
         build_oracle(a.verbose)
 

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../include/netrec_b200.h"
+#include "comm.cuh"
 #include "context.cuh"
 
 struct nrg_ctx {
@@ -453,16 +454,42 @@ int nrg_generate_ising(nrg_ctx* x, double mean_deg, double w_sigma, double th_si
 }
 
 int nrg_comm_unique_id(uint8_t id[128]) {
-    return guard([&] {
-        (void)id;
-        nrg::fail(NRG_EINVAL, "multi-GPU communicator not built into this library");
-    });
+    return guard([&] { nrg::nccl_unique_id(id); });
 }
+
 int nrg_comm_init(nrg_ctx* x, const uint8_t id[128], int32_t rank, int32_t world) {
     return guardx(x, [&] {
-        (void)x;
-        (void)id;
-        if (world != 1 || rank != 0) nrg::fail(NRG_EINVAL, "multi-GPU communicator not built into this library");
+        if (world < 1 || rank < 0 || rank >= world) nrg::fail(NRG_EINVAL, "bad rank/world");
+        delete static_cast<nrg::Comm*>(x->c.comm);
+        x->c.comm = nullptr;
+        x->c.rank = 0;
+        x->c.world = 1;
+        if (world == 1) return;
+        x->c.comm = nrg::make_nccl_comm(id, rank, world, x->c.device);
+        x->c.rank = rank;
+        x->c.world = world;
+    });
+}
+
+int nrg_loopback_create(int32_t world, void** group) {
+    return guard([&] {
+        if (world < 1) nrg::fail(NRG_EINVAL, "bad world");
+        *group = nrg::loopback_group_create(world);
+    });
+}
+
+int nrg_loopback_destroy(void* group) {
+    return guard([&] { nrg::loopback_group_destroy(static_cast<nrg::LoopbackGroup*>(group)); });
+}
+
+int nrg_comm_init_loopback(nrg_ctx* x, void* group, int32_t rank) {
+    return guardx(x, [&] {
+        auto* g = static_cast<nrg::LoopbackGroup*>(group);
+        delete static_cast<nrg::Comm*>(x->c.comm);
+        nrg::Comm* cm = nrg::make_loopback_comm(g, rank);
+        x->c.comm = cm;
+        x->c.rank = rank;
+        x->c.world = cm->world;
     });
 }
 

@@ -199,8 +199,8 @@ struct Context {
     DevBuf sc_surv, sc_g, sc_flag, sc_w32, sc_n;
     std::vector<char> host_scratch;
 
-    // multi-GPU (nccl), opaque
-    void* comm = nullptr;
+    // multi-GPU: node-sharded NNDescent + key-sharded distance cache (comm.cuh)
+    void* comm = nullptr;  // nrg::Comm*
     int rank = 0, world = 1;
 
     ~Context();

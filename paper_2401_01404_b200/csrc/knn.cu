@@ -22,6 +22,7 @@
 #include <numeric>
 #include <vector>
 
+#include "comm.cuh"
 #include "context.cuh"
 
 namespace nrg {
@@ -54,13 +55,14 @@ __global__ void rank_kernel(const int32_t* __restrict__ perm, uint64_t n, int32_
 
 // initial out-neighbours: Floyd sampling (inc/knn.hpp:177-199).  One warp per node:
 // lane 0 draws the sequence, the warp tests membership in parallel.
+// (nodes, rank, gid, qi, qj point at this rank's first own row; `own` rows, n = level size)
 __global__ void knn_init_kernel(const int32_t* __restrict__ nodes, const int32_t* __restrict__ sorted_ids,
-                                const int32_t* __restrict__ rank, const int32_t* __restrict__ loc,
+                                const int32_t* __restrict__ rank, const int32_t* __restrict__ loc, uint64_t own,
                                 uint64_t n, int kw, uint64_t seed, int32_t* __restrict__ gid,
                                 int32_t* __restrict__ qi, int32_t* __restrict__ qj) {
     const uint64_t li = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (li >= n) return;
+    if (li >= own) return;
     const SplitRng root(seed);
     SplitRng r = root.split((uint64_t)nodes[li] + 1);
     const uint64_t self = (uint64_t)rank[li];
@@ -157,6 +159,14 @@ __device__ __forceinline__ uint64_t cache_claim_k(HashView h, uint64_t key, bool
     }
 }
 
+constexpr uint32_t kRemote = 0x80000000u;  // cand slot flag: value comes from a remote owner
+
+// owner rank of a pair key in the key-sharded distance cache (independent of the
+// cache's slot hash so every rank's table stays uniformly loaded)
+__host__ __device__ __forceinline__ int key_owner(uint64_t key, int world) {
+    return (int)((mix64(key ^ 0x5bd1e9955bd1e995ULL) >> 33) % (uint64_t)world);
+}
+
 struct ClaimSink {
     int32_t* ws;
     int32_t* wp;
@@ -164,25 +174,46 @@ struct ClaimSink {
     unsigned long long* wcount;
     uint64_t* counters;
     uint64_t* live;
+    // remote routing (world > 1): keys owned by other ranks
+    int rank = 0, world = 1;
+    uint64_t* rkeys = nullptr;
+    int32_t* rdest = nullptr;
+    unsigned long long* rcount = nullptr;
 };
 
 // warp-cooperative claim of one candidate per lane (active lanes given by `valid`).
 // Uncached metrics (h.keys == nullptr) claim every candidate into its flat slot.
 __device__ __forceinline__ uint32_t claim_warp(HashView h, const ClaimSink& sink, bool valid, int32_t gs,
                                                int32_t gp, uint64_t flat = 0) {
-    bool mine = false;
+    bool mine = false, remote = false;
     uint64_t sl = 0;
+    int dest = 0;
+    const uint64_t key = pair_key(gs, gp);
     if (valid) {
-        if (h.keys) {
-            sl = cache_claim_k(h, pair_key(gs, gp), mine);
-        } else {
+        if (!h.keys) {
             sl = flat;
             mine = true;
+        } else if (sink.world > 1 && (dest = key_owner(key, sink.world)) != sink.rank) {
+            remote = true;
+        } else {
+            sl = cache_claim_k(h, key, mine);
         }
     }
     const int lane = threadIdx.x & 31;
+    {
+        const unsigned rb = __ballot_sync(0xffffffffu, remote);
+        unsigned long long r0 = 0;
+        if (lane == 0 && rb) r0 = atomicAdd(sink.rcount, (unsigned long long)__popc(rb));
+        r0 = __shfl_sync(0xffffffffu, r0, 0);
+        if (remote) {
+            const uint64_t at = r0 + __popc(rb & ((1u << lane) - 1));
+            sink.rkeys[at] = key;
+            sink.rdest[at] = dest;
+            sl = kRemote | (uint32_t)at;
+        }
+    }
     const unsigned ball = __ballot_sync(0xffffffffu, mine);
-    const unsigned hits = __ballot_sync(0xffffffffu, valid && !mine);
+    const unsigned hits = __ballot_sync(0xffffffffu, valid && !mine && !remote);
     unsigned long long b0 = 0;
     if (lane == 0 && ball) b0 = atomicAdd(sink.wcount, (unsigned long long)__popc(ball));
     b0 = __shfl_sync(0xffffffffu, b0, 0);
@@ -210,10 +241,45 @@ __global__ void claim_list_kernel(HashView h, ClaimSink sink, const int32_t* __r
     const uint32_t sl = claim_warp(h, sink, valid, valid ? qi[e] : 0, valid ? qj[e] : 0);
     if (valid) slot[e] = sl;
 }
-__global__ void gather_vals_kernel(const double* __restrict__ vals, const uint32_t* __restrict__ slot,
-                                   uint64_t n, double* __restrict__ out) {
+__global__ void gather_vals_kernel(const double* __restrict__ vals, const double* __restrict__ rvals,
+                                   const uint32_t* __restrict__ slot, uint64_t n, double* __restrict__ out) {
     const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < n) out[e] = vals[slot[e]];
+    if (e < n) {
+        const uint32_t sl = slot[e];
+        out[e] = (sl & kRemote) ? rvals[sl & ~kRemote] : vals[sl];
+    }
+}
+
+// ---------------------------------------------------------------- key-sharded cache exchange
+__global__ void dest_hist_kernel(const int32_t* __restrict__ dest, uint64_t n, unsigned long long* __restrict__ cnt) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) atomicAdd(&cnt[dest[t]], 1ull);
+}
+__global__ void gather_u64_kernel(const uint64_t* __restrict__ in, const int32_t* __restrict__ perm, uint64_t n,
+                                  uint64_t* __restrict__ out) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) out[t] = in[perm[t]];
+}
+__global__ void scatter_f64_kernel(const double* __restrict__ in, const int32_t* __restrict__ perm, uint64_t n,
+                                   double* __restrict__ out) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) out[perm[t]] = in[t];
+}
+// owner side: claim incoming keys (sorted, so worklist runs share their first node)
+__global__ void claim_keys_kernel(HashView h, ClaimSink sink, const uint64_t* __restrict__ keys,
+                                  const int32_t* __restrict__ idx, uint64_t n, uint32_t* __restrict__ slot_of) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = e < n;
+    const uint64_t k = valid ? keys[e] : 0;
+    ClaimSink local = sink;
+    local.world = 1;  // owner: claim here
+    const uint32_t sl = claim_warp(h, local, valid, (int32_t)(k >> 32), (int32_t)(k & 0xffffffffu));
+    if (valid) slot_of[idx[e]] = sl;
+}
+__global__ void answer_kernel(const double* __restrict__ vals, const uint32_t* __restrict__ slot_of, uint64_t n,
+                              double* __restrict__ out) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) out[t] = vals[slot_of[t]];
 }
 
 // ---------------------------------------------------------------- U (capped undirected view)
@@ -303,10 +369,10 @@ __global__ void __launch_bounds__(NT) knn_gather_kernel(const int32_t* __restric
                                                         int tsize, HashView h, ClaimSink sink,
                                                         uint64_t capn, int32_t* __restrict__ cand_id,
                                                         uint32_t* __restrict__ cand_slot,
-                                                        int32_t* __restrict__ cand_cnt) {
+                                                        int32_t* __restrict__ cand_cnt, uint64_t lo) {
     extern __shared__ int32_t tab[];
     __shared__ int ncand;
-    const uint64_t li = blockIdx.x;
+    const uint64_t li = lo + blockIdx.x;
     const int tid = threadIdx.x;
     const int words = bitmap ? (int)((n + 31) / 32) : tsize;
     for (int t = tid; t < words; t += NT) tab[t] = bitmap ? 0 : -1;
@@ -373,15 +439,16 @@ __global__ void __launch_bounds__(NT) knn_merge_kernel(const int32_t* __restrict
                                                        const int32_t* __restrict__ cand_id,
                                                        const uint32_t* __restrict__ cand_slot,
                                                        const int32_t* __restrict__ cand_cnt, uint64_t capn,
-                                                       const double* __restrict__ cvals, int buf_cap,
-                                                       unsigned long long* __restrict__ churn) {
+                                                       const double* __restrict__ cvals,
+                                                       const double* __restrict__ rvals, int buf_cap,
+                                                       unsigned long long* __restrict__ churn, uint64_t lo) {
     extern __shared__ unsigned char smem_raw[];
     double* bd = reinterpret_cast<double*>(smem_raw);
     int32_t* bi = reinterpret_cast<int32_t*>(bd + buf_cap);  // local id
     int32_t* bg = bi + buf_cap;                               // global id (tie order)
     int32_t* bo = bg + buf_cap;                               // origin: 1 = candidate
     __shared__ int nb;
-    const uint64_t li = blockIdx.x;
+    const uint64_t li = lo + blockIdx.x;
     const int tid = threadIdx.x;
     const int cnt = cand_cnt[li];
     if (cnt == 0) return;
@@ -404,7 +471,8 @@ __global__ void __launch_bounds__(NT) knn_merge_kernel(const int32_t* __restrict
         const int end = min(cnt, blk + B);
         for (int t = blk + tid; t < end; t += NT) {
             const int32_t v = cand_id[li * capn + t];
-            const double d = cvals[cand_slot[li * capn + t]];
+            const uint32_t sl = cand_slot[li * capn + t];
+            const double d = (sl & kRemote) ? rvals[sl & ~kRemote] : cvals[sl];
             const int g = nodes[v];
             if (entry_less(d, g, wd, wg)) {
                 const int at = atomicAdd(&nb, 1);
@@ -557,6 +625,110 @@ static void in_edge_sort(Context& c, uint64_t ne, const uint32_t* tgt, const uin
     NRG_LAUNCH_CHECK();
 }
 
+
+// ---------------------------------------------------------------- key-sharded exchange (host)
+struct ExchangeBufs {
+    DevBuf rkeys, rdest, rcount, perm, perm2, dsorted, skeys, hist, recv_keys, ridx, sorted_keys, sorted_idx, slot_of,
+        ans, resp, rvals, ws2, wp2, wsl2, tmp;
+};
+
+static void score_claimed(Context& c, int mode, int32_t* ws, int32_t* wp, uint32_t* wslot, uint64_t nw);
+
+// Route the remote requests of the last claim phase to their owner ranks, claim them
+// there, score every pair this rank claimed (local + remote), answer the requests.
+// On return X.rvals holds the distance of request r (slot kRemote | r) of this rank.
+static void exchange_and_score(Context& c, int mode, const ClaimSink& sink, uint64_t nw_local, ExchangeBufs& X,
+                               uint64_t reserve_hint) {
+    Comm* comm = static_cast<Comm*>(c.comm);
+    const int W = c.world, me = c.rank;
+    unsigned long long R = 0;
+    if (W > 1) {
+        NRG_CUDA(cudaMemcpyAsync(&R, sink.rcount, 8, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+    }
+    (void)reserve_hint;
+    if (W == 1) {
+        score_claimed(c, mode, sink.ws, sink.wp, sink.wslot, nw_local);
+        return;
+    }
+    // 1. requests grouped by owner rank
+    int32_t* perm = X.perm.as<int32_t>(R + 1);
+    int32_t* perm2 = X.perm2.as<int32_t>(R + 1);
+    int32_t* dsorted = X.dsorted.as<int32_t>(R + 1);
+    uint64_t* skeys = X.skeys.as<uint64_t>(R + 1);
+    unsigned long long* hist = X.hist.as<unsigned long long>(W);
+    NRG_CUDA(cudaMemsetAsync(hist, 0, 8 * W, c.stream));
+    if (R) {
+        iota_kernel<<<(unsigned)ceil_div(R, 256), 256, 0, c.stream>>>(perm, R);
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, sink.rdest, dsorted, perm, perm2, (int64_t)R, 0, 16, c.stream);
+        void* tmp = X.tmp.ensure(tb);
+        cub::DeviceRadixSort::SortPairs(tmp, tb, sink.rdest, dsorted, perm, perm2, (int64_t)R, 0, 16, c.stream);
+        dest_hist_kernel<<<(unsigned)ceil_div(R, 256), 256, 0, c.stream>>>(sink.rdest, R, hist);
+        gather_u64_kernel<<<(unsigned)ceil_div(R, 256), 256, 0, c.stream>>>(sink.rkeys, perm2, R, skeys);
+        NRG_LAUNCH_CHECK_N(3);
+    }
+    std::vector<uint64_t> cnt(W), mat((size_t)W * W, 0);
+    NRG_CUDA(cudaMemcpyAsync(cnt.data(), hist, 8 * W, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    for (int d = 0; d < W; ++d) mat[(size_t)me * W + d] = cnt[d];
+    comm->allreduce_u64(mat.data(), W * W, false, c.stream);
+    std::vector<size_t> sb(W), so(W), rb(W), ro(W);
+    uint64_t Q = 0;
+    for (int r = 0, off = 0, roff = 0; r < W; ++r) {
+        sb[r] = cnt[r] * 8;
+        so[r] = (size_t)off;
+        off += (int)sb[r];
+        rb[r] = mat[(size_t)r * W + me] * 8;
+        ro[r] = (size_t)roff;
+        roff += (int)rb[r];
+        Q += mat[(size_t)r * W + me];
+    }
+    uint64_t* recv_keys = X.recv_keys.as<uint64_t>(Q + 1);
+    comm->alltoallv(skeys, sb, so, recv_keys, rb, ro, c.stream);
+    // 2. owner side: claim (key-sorted for K1 locality), score local + remote claims
+    uint32_t* slot_of = X.slot_of.as<uint32_t>(Q + 1);
+    int32_t* ws2 = X.ws2.as<int32_t>(Q + 1);
+    int32_t* wp2 = X.wp2.as<int32_t>(Q + 1);
+    uint32_t* wsl2 = X.wsl2.as<uint32_t>(Q + 1);
+    unsigned long long nw2 = 0;
+    if (Q) {
+        int32_t* ridx = X.ridx.as<int32_t>(Q);
+        uint64_t* sk = X.sorted_keys.as<uint64_t>(Q);
+        int32_t* si = X.sorted_idx.as<int32_t>(Q);
+        iota_kernel<<<(unsigned)ceil_div(Q, 256), 256, 0, c.stream>>>(ridx, Q);
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, recv_keys, sk, ridx, si, (int64_t)Q, 0, 64, c.stream);
+        void* tmp = X.tmp.ensure(tb);
+        cub::DeviceRadixSort::SortPairs(tmp, tb, recv_keys, sk, ridx, si, (int64_t)Q, 0, 64, c.stream);
+        ClaimSink s2 = sink;
+        s2.ws = ws2;
+        s2.wp = wp2;
+        s2.wslot = wsl2;
+        s2.wcount = sink.wcount + 1;
+        NRG_CUDA(cudaMemsetAsync(s2.wcount, 0, 8, c.stream));
+        claim_keys_kernel<<<(unsigned)ceil_div(Q, 256), 256, 0, c.stream>>>(c.Cview(), s2, sk, si, Q, slot_of);
+        NRG_LAUNCH_CHECK_N(2);
+        NRG_CUDA(cudaMemcpyAsync(&nw2, s2.wcount, 8, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+    }
+    score_claimed(c, mode, sink.ws, sink.wp, sink.wslot, nw_local);
+    score_claimed(c, mode, ws2, wp2, wsl2, nw2);
+    // 3. answers back to the requesters, scattered into request order
+    double* ans = X.ans.as<double>(Q + 1);
+    double* resp = X.resp.as<double>(R + 1);
+    double* rvals = X.rvals.as<double>(R + 1);
+    if (Q) {
+        answer_kernel<<<(unsigned)ceil_div(Q, 256), 256, 0, c.stream>>>(c.Cview().vals, slot_of, Q, ans);
+        NRG_LAUNCH_CHECK();
+    }
+    comm->alltoallv(ans, rb, ro, resp, sb, so, c.stream);
+    if (R) {
+        scatter_f64_kernel<<<(unsigned)ceil_div(R, 256), 256, 0, c.stream>>>(resp, perm2, R, rvals);
+        NRG_LAUNCH_CHECK();
+    }
+}
+
 // ---------------------------------------------------------------- driver
 __global__ void to_global_kernel(const int32_t* __restrict__ gid, const double* __restrict__ gd,
                                  const int32_t* __restrict__ nodes, uint64_t n, int kw, int k,
@@ -587,6 +759,8 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
     if (mode == TABLE && !c.table_n) fail(22, "no distance table set");
     if (mode == LINE && !c.line_n) fail(22, "no line metric set");
     if (mode == EXACT || mode == GRADIENT) ensure_snapshot(c);
+    // collective in multi-rank jobs: every rank resolves the generation's base here
+    if (mode == EXACT) generation_base(c);
 
     // local index map, id-sorted node set and ranks
     int32_t* loc = c.s_a.as<int32_t>(c.n);
@@ -633,7 +807,14 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
     int32_t* gid = gid_buf.as<int32_t>(n * kw);
     double* gd = gd_buf.as<double>(n * kw);
     unsigned long long* wcount = c.s_c.as<unsigned long long>(2);
-    auto sink_for = [&](int32_t* ws, int32_t* wp, uint32_t* wslot) {
+    const bool cached = (mode == EXACT || mode == GRADIENT);
+    // node shard of this rank; the distance cache is sharded by key
+    const int W = cached ? c.world : 1;
+    uint64_t lo = 0, hi = n;
+    if (c.world > 1) shard_range(n, c.rank, c.world, lo, hi);
+    const uint64_t own = hi - lo;
+    ExchangeBufs X;
+    auto sink_for = [&](int32_t* ws, int32_t* wp, uint32_t* wslot, uint64_t rcap) {
         ClaimSink s;
         s.ws = ws;
         s.wp = wp;
@@ -641,41 +822,67 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         s.wcount = wcount;
         s.counters = c.dcounters();
         s.live = static_cast<uint64_t*>(c.Ccount.p);
+        s.rank = c.rank;
+        s.world = W;
+        if (W > 1) {
+            s.rkeys = X.rkeys.as<uint64_t>(rcap);
+            s.rdest = X.rdest.as<int32_t>(rcap);
+            s.rcount = X.rcount.as<unsigned long long>(1);
+            NRG_CUDA(cudaMemsetAsync(s.rcount, 0, 8, c.stream));
+        }
         return s;
     };
-    const bool cached = (mode == EXACT || mode == GRADIENT);
+    // rows [lo, hi) of the graph are this rank's; make every rank's copy whole
+    auto allgather_rows = [&](int32_t* gid_, double* gd_, int kwid) {
+        if (c.world == 1) return;
+        Comm* comm = static_cast<Comm*>(c.comm);
+        std::vector<size_t> bi(c.world), bd(c.world);
+        for (int r = 0; r < c.world; ++r) {
+            uint64_t l, h;
+            shard_range(n, r, c.world, l, h);
+            bi[r] = (h - l) * kwid * 4;
+            bd[r] = (h - l) * kwid * 8;
+        }
+        comm->allgatherv(gid_ + lo * kwid, gid_, bi, c.stream);
+        comm->allgatherv(gd_ + lo * kwid, gd_, bd, c.stream);
+    };
 
     // ---- initial graph
     c.tic();
     {
-        const uint64_t nq = n * kw;
+        const uint64_t nq = own * kw;
         DevBuf qib, qjb, slb;
-        int32_t* qi = qib.as<int32_t>(nq);
-        int32_t* qj = qjb.as<int32_t>(nq);
-        knn_init_kernel<<<(unsigned)ceil_div(n * 32, 128), 128, 0, c.stream>>>(d_nodes, sorted_ids, rank, loc, n,
-                                                                            kw, p.seed, gid, qi, qj);
+        int32_t* qi = qib.as<int32_t>(nq + 1);
+        int32_t* qj = qjb.as<int32_t>(nq + 1);
+        knn_init_kernel<<<(unsigned)ceil_div(own * 32, 128), 128, 0, c.stream>>>(
+            d_nodes + lo, sorted_ids, rank + lo, loc, own, n, kw, p.seed, gid + lo * kw, qi, qj);
         NRG_LAUNCH_CHECK();
         c.toc(P_KNN);
         if (cached) {
-            cache_reserve(c, nq);
-            uint32_t* slot = slb.as<uint32_t>(nq);
+            cache_reserve(c, n * (uint64_t)kw);
+            uint32_t* slot = slb.as<uint32_t>(nq + 1);
             DevBuf wsb, wpb, wslb;
-            int32_t* ws = wsb.as<int32_t>(nq);
-            int32_t* wp = wpb.as<int32_t>(nq);
-            uint32_t* wsl = wslb.as<uint32_t>(nq);
-            NRG_CUDA(cudaMemsetAsync(wcount, 0, 8, c.stream));
-            claim_list_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, c.stream>>>(c.Cview(), sink_for(ws, wp, wsl),
-                                                                              qi, qj, nq, slot);
-            NRG_LAUNCH_CHECK();
+            int32_t* ws = wsb.as<int32_t>(nq + 1);
+            int32_t* wp = wpb.as<int32_t>(nq + 1);
+            uint32_t* wsl = wslb.as<uint32_t>(nq + 1);
+            NRG_CUDA(cudaMemsetAsync(wcount, 0, 16, c.stream));
+            const ClaimSink sk = sink_for(ws, wp, wsl, nq + 1);
+            if (nq) {
+                claim_list_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, c.stream>>>(c.Cview(), sk, qi, qj, nq, slot);
+                NRG_LAUNCH_CHECK();
+            }
             unsigned long long nw = 0;
             NRG_CUDA(cudaMemcpyAsync(&nw, wcount, 8, cudaMemcpyDeviceToHost, c.stream));
             c.sync();
-            score_claimed(c, mode, ws, wp, wsl, nw);
-            gather_vals_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, c.stream>>>(c.Cview().vals, slot, nq, gd);
-            NRG_LAUNCH_CHECK();
+            exchange_and_score(c, mode, sk, nw, X, 0);
+            if (nq) {
+                gather_vals_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, c.stream>>>(
+                    c.Cview().vals, static_cast<double*>(X.rvals.p), slot, nq, gd + lo * kw);
+                NRG_LAUNCH_CHECK();
+            }
         } else {
             ScoreOut so;
-            so.dist = gd;
+            so.dist = gd + lo * kw;
             score_entries(c, mode, qi, qj, nq, so);
         }
         c.tic();
@@ -683,11 +890,16 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         while (P < kw) P <<= 1;
         const size_t rs_smem = (size_t)P * 16;
         if (rs_smem > 48 * 1024) fail(100, "find_knn: kw too large for the row sort");
-        if (P <= 64)
-            row_sort_kernel<32><<<(unsigned)n, 32, rs_smem, c.stream>>>(gid, gd, d_nodes, n, kw, P);
-        else
-            row_sort_kernel<128><<<(unsigned)n, 128, rs_smem, c.stream>>>(gid, gd, d_nodes, n, kw, P);
-        NRG_LAUNCH_CHECK();
+        if (own) {
+            if (P <= 64)
+                row_sort_kernel<32><<<(unsigned)own, 32, rs_smem, c.stream>>>(gid + lo * kw, gd + lo * kw, d_nodes, own,
+                                                                             kw, P);
+            else
+                row_sort_kernel<128><<<(unsigned)own, 128, rs_smem, c.stream>>>(gid + lo * kw, gd + lo * kw, d_nodes,
+                                                                               own, kw, P);
+            NRG_LAUNCH_CHECK();
+        }
+        allgather_rows(gid, gd, kw);
         c.toc(P_KNN);
     }
 
@@ -772,27 +984,30 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             NRG_LAUNCH_CHECK();
         }
         c.toc(P_KNN);
-        // gather + claim
+        // gather + claim (own nodes; remote keys routed to their owner ranks)
         if (cached) cache_reserve(c, wmax);
         c.tic();
         NRG_CUDA(cudaMemsetAsync(wcount, 0, 16, c.stream));
         NRG_CUDA(cudaMemsetAsync(churn, 0, 8, c.stream));
         const HashView hv = cached ? c.Cview() : HashView{nullptr, nullptr, 0};
-        if (big)
-            knn_gather_kernel<256><<<(unsigned)n, 256, tab_bytes, c.stream>>>(
-                d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv, sink_for(ws, wp, wsl), capn,
-                cand_id, cand_slot, cand_cnt);
-        else
-            knn_gather_kernel<32><<<(unsigned)n, 32, tab_bytes, c.stream>>>(
-                d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv, sink_for(ws, wp, wsl), capn,
-                cand_id, cand_slot, cand_cnt);
-        NRG_LAUNCH_CHECK();
+        const ClaimSink sk = sink_for(ws, wp, wsl, own * capn + 1);
+        if (own) {
+            if (big)
+                knn_gather_kernel<256><<<(unsigned)own, 256, tab_bytes, c.stream>>>(
+                    d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv, sk, capn, cand_id, cand_slot,
+                    cand_cnt, lo);
+            else
+                knn_gather_kernel<32><<<(unsigned)own, 32, tab_bytes, c.stream>>>(
+                    d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv, sk, capn, cand_id, cand_slot,
+                    cand_cnt, lo);
+            NRG_LAUNCH_CHECK();
+        }
         unsigned long long nw = 0;
         NRG_CUDA(cudaMemcpyAsync(&nw, wcount, 8, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
         c.toc(P_KNN);
         if (cached) {
-            score_claimed(c, mode, ws, wp, wsl, nw);
+            exchange_and_score(c, mode, sk, nw, X, 0);
         } else if (nw) {
             ScoreOut so;
             so.cache_vals = flat_d;
@@ -800,17 +1015,26 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             score_entries(c, mode, ws, wp, nw, so);
         }
         const double* dvals = cached ? c.Cview().vals : flat_d;
+        const double* rvals = static_cast<double*>(X.rvals.p);
         c.tic();
-        if (kw > 64)
-            knn_merge_kernel<128><<<(unsigned)n, 128, merge_smem, c.stream>>>(
-                d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dvals, buf_cap, churn);
-        else
-            knn_merge_kernel<32><<<(unsigned)n, 32, merge_smem, c.stream>>>(
-                d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dvals, buf_cap, churn);
-        NRG_LAUNCH_CHECK();
+        if (own) {
+            if (kw > 64)
+                knn_merge_kernel<128><<<(unsigned)own, 128, merge_smem, c.stream>>>(
+                    d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dvals, rvals, buf_cap, churn, lo);
+            else
+                knn_merge_kernel<32><<<(unsigned)own, 32, merge_smem, c.stream>>>(
+                    d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dvals, rvals, buf_cap, churn, lo);
+            NRG_LAUNCH_CHECK();
+        }
         unsigned long long changed = 0;
         NRG_CUDA(cudaMemcpyAsync(&changed, churn, 8, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
+        allgather_rows(gid, gd, kw);
+        if (c.world > 1) {
+            uint64_t ch = changed;
+            static_cast<Comm*>(c.comm)->allreduce_u64(&ch, 1, false, c.stream);
+            changed = ch;
+        }
         c.toc(P_KNN);
         ++out.sweeps;
         const double ratio = (double)changed / ((double)kw * (double)n);

@@ -376,8 +376,8 @@ void score_all_pairs(Context& c, int mode, const int32_t* nodes, uint64_t n, dou
         score_entries(c, mode, es, ep, cnt, out);
         r0 = r1;
     }
-    // probes count as misses (no cache on this path)
-    counters_add_host(c, C_MISSES, n * (n - 1) / 2);
+    // probes count as misses (no cache on this path); replicated on every rank, counted once
+    if (c.rank == 0) counters_add_host(c, C_MISSES, n * (n - 1) / 2);
 }
 
 // ---------------------------------------------------------------- cached batch lookups

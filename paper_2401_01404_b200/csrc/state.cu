@@ -8,6 +8,7 @@
 #include <cstring>
 #include <vector>
 
+#include "comm.cuh"
 #include "context.cuh"
 
 namespace nrg {
@@ -20,6 +21,7 @@ Context::~Context() {
     if (kev0) cudaEventDestroy(kev0);
     if (kev1) cudaEventDestroy(kev1);
     tl_stream = stream;  // members free in stream order; StreamOwner destroys the stream last
+    delete static_cast<Comm*>(comm);
 }
 
 static uint64_t next_pow2(uint64_t v) {
@@ -492,6 +494,8 @@ double log_posterior(Context& c) {
 double generation_base(Context& c) {
     if (!c.base_valid) {
         c.base = log_posterior(c);
+        // one base for the whole job: pruned pairs tie at exactly -base on every rank
+        if (c.world > 1) static_cast<Comm*>(c.comm)->bcast_f64(&c.base, 1, c.stream);
         c.base_valid = true;
     }
     return c.base;
@@ -525,7 +529,7 @@ void cache_reserve(Context& c, uint64_t extra) {
     c.cache_live_host = live;
     if (c.Ccap && (live + extra) * 10 <= c.Ccap * 6) return;  // load factor <= 0.6
     const uint64_t ncap = std::max<uint64_t>(1u << 20, next_pow2(2 * (live + extra)));
-    if (ncap > (1ull << 32)) fail(100, "distance cache would exceed 2^32 slots");
+    if (ncap > (1ull << 31)) fail(100, "distance cache would exceed 2^31 slots");
     DevBuf nk, nv;
     nk.ensure(ncap * 8);
     nv.ensure(ncap * 8);

@@ -1,0 +1,28 @@
+"""The drop-in C++ API (include/netrec_b200/netrec.hpp) exercised by a C++ program
+written like the reference's own tests (tests/cpp/test_dropin.cpp)."""
+from __future__ import annotations
+
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+BIN = ROOT / "paper_2401_01404_b200" / "test_dropin"
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_program():
+    if not BIN.exists():
+        from paper_2401_01404_b200 import build
+        build.build_cpp_tests()
+    r = subprocess.run([str(BIN)], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "PASSED" in r.stdout
+
+
+def test_cpp_dropin_compiles():
+    """CPU: the header compiles against the C-ABI and links against the library."""
+    from paper_2401_01404_b200 import build
+    assert build.build_cpp_tests().exists()
