@@ -231,6 +231,11 @@ int nrg_comm_init(nrg_ctx* ctx, const uint8_t id[128], int32_t rank, int32_t wor
 int nrg_loopback_create(int32_t world, void** group);
 int nrg_loopback_destroy(void* group);
 int nrg_comm_init_loopback(nrg_ctx* ctx, void* group, int32_t rank);
+/* The partition functions of the sharded path (host-only, no GPU needed): the node
+ * range [lo, hi) of `rank` in a level of n nodes, and the owner rank of a pair key in
+ * the key-sharded distance cache. */
+int nrg_shard_range(uint64_t n, int32_t rank, int32_t world, uint64_t* lo, uint64_t* hi);
+int32_t nrg_key_owner(uint64_t key, int32_t world);
 
 #ifdef __cplusplus
 }

@@ -94,6 +94,8 @@ SIGNATURES = {
     "nrg_loopback_create": (C.c_int, [_i32, C.POINTER(_VP)]),
     "nrg_loopback_destroy": (C.c_int, [_VP]),
     "nrg_comm_init_loopback": (C.c_int, [_P, _VP, _i32]),
+    "nrg_shard_range": (C.c_int, [_u64, _i32, _i32, C.POINTER(_u64), C.POINTER(_u64)]),
+    "nrg_key_owner": (_i32, [_u64, _i32]),
 }
 
 _lib: C.CDLL | None = None
@@ -343,6 +345,16 @@ class Model:
         check(self.L.nrg_phase_times(self.h, out, 7))
         names = ["score", "knn", "select", "update", "theta", "logpost", "snapshot"]
         return dict(zip(names, out.tolist()))
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    lo, hi = _u64(), _u64()
+    check(load().nrg_shard_range(n, rank, world, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
+def key_owner(key: int, world: int) -> int:
+    return int(load().nrg_key_owner(key, world))
 
 
 def comm_unique_id() -> bytes:

@@ -493,4 +493,13 @@ int nrg_comm_init_loopback(nrg_ctx* x, void* group, int32_t rank) {
     });
 }
 
+int nrg_shard_range(uint64_t n, int32_t rank, int32_t world, uint64_t* lo, uint64_t* hi) {
+    return guard([&] {
+        if (world < 1 || rank < 0 || rank >= world) nrg::fail(NRG_EINVAL, "bad rank/world");
+        nrg::shard_range(n, rank, world, *lo, *hi);
+    });
+}
+
+int32_t nrg_key_owner(uint64_t key, int32_t world) { return world > 1 ? nrg::key_owner(key, world) : 0; }
+
 }  // extern "C"

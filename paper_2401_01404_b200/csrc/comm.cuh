@@ -14,6 +14,8 @@
 #include <cstdint>
 #include <vector>
 
+#include "common.cuh"
+
 namespace nrg {
 
 struct Comm {
@@ -39,6 +41,12 @@ struct LoopbackGroup;
 LoopbackGroup* loopback_group_create(int world);
 void loopback_group_destroy(LoopbackGroup* g);
 Comm* make_loopback_comm(LoopbackGroup* g, int rank);
+
+// owner rank of a pair key in the key-sharded distance cache (independent of the
+// cache's slot hash so every rank's table stays uniformly loaded)
+__host__ __device__ __forceinline__ int key_owner(uint64_t key, int world) {
+    return (int)((mix64(key ^ 0x5bd1e9955bd1e995ULL) >> 33) % (uint64_t)world);
+}
 
 // contiguous node-range shard of a level's n nodes (local indices)
 inline void shard_range(uint64_t n, int rank, int world, uint64_t& lo, uint64_t& hi) {

@@ -161,11 +161,6 @@ __device__ __forceinline__ uint64_t cache_claim_k(HashView h, uint64_t key, bool
 
 constexpr uint32_t kRemote = 0x80000000u;  // cand slot flag: value comes from a remote owner
 
-// owner rank of a pair key in the key-sharded distance cache (independent of the
-// cache's slot hash so every rank's table stays uniformly loaded)
-__host__ __device__ __forceinline__ int key_owner(uint64_t key, int world) {
-    return (int)((mix64(key ^ 0x5bd1e9955bd1e995ULL) >> 33) % (uint64_t)world);
-}
 
 struct ClaimSink {
     int32_t* ws;
