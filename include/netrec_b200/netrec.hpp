@@ -36,6 +36,13 @@
 
 #include "../netrec_b200.h"
 
+// This header defines the reference's core types itself; mark the reference headers
+// that define them as already included, so reference headers that only *use* them
+// (e.g. inc/io.hpp, the CLI's text formats) compile against these definitions.
+#define NETREC_COMMON_HPP
+#define NETREC_SAMPLE_MATRIX_HPP
+#define NETREC_SPARSE_WEIGHTS_HPP
+
 namespace netrec {
 
 using NodeId = std::int32_t;

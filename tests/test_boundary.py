@@ -65,3 +65,29 @@ def test_fails_loudly_without_gpu(lib):
 def test_error_codes_map_to_reference_exceptions():
     from paper_2401_01404_b200._lib import ERRORS
     assert ERRORS[22] is ValueError and ERRORS[34] is IndexError and ERRORS[75] is OverflowError
+
+
+@pytest.mark.skipif(not Path("/root/reference/proj/include/netrec/io.hpp").exists(),
+                    reason="reference headers not present")
+def test_reference_io_compiles_on_dropin_types(tmp_path):
+    """the reference's own text I/O header compiles unchanged on the
+    drop-in types (and round-trips a state through them)."""
+    src = tmp_path / "io_dropin.cpp"
+    src.write_text("""
+#include "netrec_b200/netrec.hpp"
+#include "netrec/io.hpp"
+int main() {
+    netrec::SampleMatrix x(3, 2);
+    for (int i = 0; i < 3; ++i) for (int m = 0; m < 2; ++m) x.set(i, m, (i + m) % 2 ? 1.0 : -1.0);
+    netrec::SparseWeights w(3, 2);
+    w.set_edge(0, 2, 0.25, x);
+    w.set_theta(1, -0.5);
+    const std::string t = netrec::weights_to_text(w);
+    return t.find("0.25") == std::string::npos;
+}
+""")
+    out = tmp_path / "io_dropin"
+    r = subprocess.run(["g++", "-std=c++20", f"-I{ROOT / 'include'}", "-I/root/reference/proj/include", str(src),
+                        "-o", str(out)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert subprocess.run([str(out)]).returncode == 0
