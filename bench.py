@@ -177,7 +177,6 @@ def reference_pairs_per_sec(X_f64, lam, pairs_i, pairs_j, target_s, threads):
 
         def run(i, j):
             out = np.zeros(len(i))
-            m.begin_generation()
             rc = f(m.h, 0, len(i), np.ascontiguousarray(i, np.int32), np.ascontiguousarray(j, np.int32), out,
                    threads)
             assert rc == 0
@@ -186,17 +185,21 @@ def reference_pairs_per_sec(X_f64, lam, pairs_i, pairs_j, target_s, threads):
         threads = 1
 
         def run(i, j):
-            m.begin_generation()
             return m.distance(0, i, j)
-    # warm up (base = log_posterior once per generation) and calibrate the sample size
-    n0 = min(len(pairs_i), max(2000, 500 * threads))
+    # one generation: the first call computes the per-generation base (log_posterior,
+    # amortised over ~1e8 pairs in a real sweep); calibration and the timed run then
+    # use disjoint slices so no pair is a cache hit
+    m.begin_generation()
+    run(pairs_i[:1], pairs_j[:1])
+    n0 = min(len(pairs_i) // 4, max(2000, 500 * threads))
     t = time.perf_counter()
-    run(pairs_i[:n0], pairs_j[:n0])
+    run(pairs_i[1:1 + n0], pairs_j[1:1 + n0])
     dt = time.perf_counter() - t
     rate = n0 / max(dt, 1e-6)
-    n = int(min(len(pairs_i), max(n0, rate * target_s)))
+    rest_i, rest_j = pairs_i[1 + n0:], pairs_j[1 + n0:]
+    n = int(min(len(rest_i), max(n0, rate * target_s)))
     t = time.perf_counter()
-    run(pairs_i[:n], pairs_j[:n])
+    run(rest_i[:n], rest_j[:n])
     dt = time.perf_counter() - t
     m.close()
     return n / dt, n, dt, which, threads
@@ -305,9 +308,10 @@ def run_ours(args, rank, world, local, dist):
     e2e_ms, = allreduce(dist, [e2e_ms], "max")
 
     # roofline of the dominant kernel (K1 screen): algorithmic bytes = the partner column
-    # per screened pair (fp32 tanh field 4M + packed spins M/8)
+    # per screened pair (fp16 tanh field 2M + packed spins M/8; the stationary column is
+    # held in registers across a worklist run)
     peak, peak_kind = measured_peaks()
-    bytes_per_pair = 4 * M + M / 8
+    bytes_per_pair = 2 * M + M / 8
     k1_ms_avg = kst["k1_ms"] / max(1.0, kst["k1_launches"])
     k1_pairs_avg = kst["k1_pairs"] / max(1.0, kst["k1_launches"])
     achieved = (k1_pairs_avg * bytes_per_pair) / (k1_ms_avg / 1e3) / 1e9 if k1_ms_avg > 0 else 0.0

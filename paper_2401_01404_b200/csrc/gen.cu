@@ -22,28 +22,59 @@ static double h_normal(SplitRng& r) {  // inc/random.hpp:55-60
     return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586477 * u2);
 }
 
-__global__ void gibbs_color_kernel(const int32_t* __restrict__ members, int cnt, const int64_t* __restrict__ off,
-                                   const int32_t* __restrict__ nbr, const double* __restrict__ nw,
-                                   const double* __restrict__ theta, int8_t* __restrict__ spin, uint64_t key,
-                                   uint64_t sweep) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= cnt) return;
-    const int i = members[t];
-    double field = theta[i];
-    for (int64_t q = off[i]; q < off[i + 1]; ++q) field += nw[q] * (double)spin[nbr[q]];
-    const uint64_t r = mix64(key ^ mix64(sweep * 0x9e3779b97f4a7c15ULL + (uint64_t)i));
-    const double u = (double)(r >> 11) * 0x1.0p-53;
-    const double z = 2.0 * field;
-    const double p = z >= 0.0 ? 1.0 / (1.0 + exp(-z)) : exp(z) / (1.0 + exp(z));
-    spin[i] = u < p ? 1 : -1;
+// software grid barrier for the cooperative (co-resident) launch below
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
 }
 
-__global__ void record_kernel(const int8_t* __restrict__ spin, int n, int m, int Mw, uint32_t* __restrict__ Xb) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    uint32_t* w = &Xb[(size_t)i * Mw + (m >> 5)];
-    const uint32_t bit = 1u << (m & 31);
-    *w = spin[i] > 0 ? (*w | bit) : (*w & ~bit);
+// The whole chain in one launch: colour classes updated in order with a grid barrier
+// between them; samples recorded after burn-in every `thin` sweeps.
+__global__ void gibbs_persistent_kernel(const int32_t* __restrict__ members, const int* __restrict__ cstart, int ncol,
+                                        const int64_t* __restrict__ off, const int32_t* __restrict__ nbr,
+                                        const double* __restrict__ nw, const double* __restrict__ theta,
+                                        int8_t* spin, uint64_t key, int64_t sweeps, int burn_in, int thin, int M,
+                                        int Mw, int n, uint32_t* __restrict__ Xb, unsigned* bar) {
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nth = gridDim.x * blockDim.x;
+    int rec = 0;
+    for (int64_t s = 0; s < sweeps; ++s) {
+        for (int k = 0; k < ncol; ++k) {
+            for (int t = cstart[k] + tid; t < cstart[k + 1]; t += nth) {
+                const int i = members[t];
+                double field = theta[i];
+                for (int64_t q = off[i]; q < off[i + 1]; ++q) field += nw[q] * (double)__ldcg(&spin[nbr[q]]);
+                const uint64_t r = mix64(key ^ mix64((uint64_t)s * 0x9e3779b97f4a7c15ULL + (uint64_t)i));
+                const double u = (double)(r >> 11) * 0x1.0p-53;
+                const double z = 2.0 * field;
+                const double p = z >= 0.0 ? 1.0 / (1.0 + exp(-z)) : exp(z) / (1.0 + exp(z));
+                __stcg(&spin[i], (int8_t)(u < p ? 1 : -1));
+            }
+            grid_sync(bar, gridDim.x);
+        }
+        if (s >= burn_in && (s - burn_in + 1) % thin == 0 && rec < M) {
+            for (int i = tid; i < n; i += nth) {
+                uint32_t* w = &Xb[(size_t)i * Mw + (rec >> 5)];
+                const uint32_t bit = 1u << (rec & 31);
+                *w = __ldcg(&spin[i]) > 0 ? (*w | bit) : (*w & ~bit);
+            }
+            ++rec;
+            grid_sync(bar, gridDim.x);
+        }
+    }
 }
 
 void generate_ising(Context& c, double mean_deg, double w_sigma, double th_sigma, int burn_in, int thin,
@@ -145,20 +176,25 @@ void generate_ising(Context& c, double mean_deg, double w_sigma, double th_sigma
     NRG_CUDA(cudaMemsetAsync(c.Xb.p, 0, (size_t)n * c.Mw * 4, c.stream));
     const uint64_t key = mix64(seed, 2);
     const int64_t sweeps = (int64_t)burn_in + (int64_t)c.M * thin;
-    int rec = 0;
-    for (int64_t s = 0; s < sweeps; ++s) {
-        for (int k = 0; k < ncol; ++k) {
-            const int cnt = cstart[k + 1] - cstart[k];
-            gibbs_color_kernel<<<(cnt + 255) / 256, 256, 0, c.stream>>>(d_mem + cstart[k], cnt, d_off, d_nbr, d_nw,
-                                                                        d_th, d_spin, key, (uint64_t)s);
-        }
-        if (s >= burn_in && (s - burn_in + 1) % thin == 0 && rec < c.M) {
-            record_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(d_spin, n, rec, c.Mw, c.dXb());
-            ++rec;
-        }
+    {
+        DevBuf dcs, dbar;
+        int* d_cstart = dcs.as<int>(ncol + 1);
+        unsigned* bar = dbar.as<unsigned>(2);
+        NRG_CUDA(cudaMemcpyAsync(d_cstart, cstart.data(), (ncol + 1) * 4, cudaMemcpyHostToDevice, c.stream));
+        NRG_CUDA(cudaMemsetAsync(bar, 0, 8, c.stream));
+        int per = 0, sms = 0;
+        NRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gibbs_persistent_kernel, 256, 0));
+        NRG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+        int grid = std::max(1, std::min(per * sms, (n + 255) / 256));
+        uint32_t* xb = c.dXb();
+        int M = c.M, Mw = c.Mw;
+        int64_t sw = sweeps;
+        void* args[] = {&d_mem, &d_cstart, &ncol, &d_off, &d_nbr, &d_nw, &d_th, &d_spin, (void*)&key, &sw,
+                        &burn_in, &thin, &M, &Mw, (void*)&n, &xb, &bar};
+        NRG_CUDA(cudaLaunchCooperativeKernel((void*)gibbs_persistent_kernel, grid, 256, args, 0, c.stream));
+        NRG_LAUNCH_CHECK();
+        c.sync();
     }
-    NRG_LAUNCH_CHECK();
-    c.sync();
     // fresh state: make_empty_state for Ising (theta = 0, W empty, sums 0)
     const size_t nm = (size_t)n * c.Mp;
     NRG_CUDA(cudaMemsetAsync(c.H.p, 0, nm * 8, c.stream));

@@ -109,45 +109,67 @@ struct TLive {
     }
 };
 
+// 1/x for x = (1 + y_a tanh D)(1 + y_b tanh D) in (0, 4): fp32 reciprocal refined by two fp64 Newton
+// steps (relative error ~2^-96 before rounding), a third of the cost of an IEEE divide
+__device__ __forceinline__ double rcp64(double x) {
+    double r = (double)__frcp_rn((float)x);
+    r = r * fma(-x, r, 2.0);
+    r = r * fma(-x, r, 2.0);
+    return r;
+}
+
+// <x_a, x_b> = M - 2 popc(x_a ^ x_b) (padding bits are zero in both rows)
+template <class SC = WarpScope>
+__device__ __forceinline__ int spin_dot(const uint32_t* __restrict__ Xb, int Mw, int M, int a, int b,
+                                        const SC& sc = SC()) {
+    double d = 0.0;
+    for (int k = sc.tid(); k < Mw; k += SC::NT) d += (double)__popc(__ldg(&Xb[(size_t)a * Mw + k]) ^ __ldg(&Xb[(size_t)b * Mw + k]));
+    return M - 2 * (int)sc.sum(d);
+}
+
 // One fp64 pass over the samples by the whole scope (result valid in every thread).
-template <class TP, bool kNeedF, class SC = WarpScope>
+// With t = tanh D, A = 1 + y_a t, B = 1 + y_b t:
+//   q_a = (y_a + t) B / (A B),  q_b = (y_b + t) A / (A B)        (one reciprocal)
+//   L'  = 2 <x_a,x_b> - sum (q_a + q_b),   L'' = -sum (1-q_a^2) + (1-q_b^2)
+//   F   = 2 D <x_a,x_b> - 2 M ln cosh D - sum log1p((y_a + y_b) t + y_a y_b t^2)
+// (ln(cosh D + y sinh D) = ln cosh D + ln(1 + y t); one log1p per sample for both
+// sides).  kNeedF adds the objective, kL3 the third derivative (kink pass only).
+template <class TP, bool kNeedF, class SC = WarpScope, bool kL3 = false>
 __device__ __forceinline__ Pass64 ising_pass64(const TP& T, const uint32_t* __restrict__ Xb, int Mw,
-                                               int M, int a, int b, double D, const SC& sc = SC()) {
+                                               int M, int a, int b, double D, int dot, const SC& sc = SC()) {
     const int tid = sc.tid();
     const double t = tanh(D);
     const double omt2 = 1.0 - t * t;
-    const double A = fabs(D);
-    const double sg = D > 0.0 ? 1.0 : (D < 0.0 ? -1.0 : 0.0);
-    const double E = -expm1(-2.0 * A);  // 1 - e^{-2|D|}
-    double Lp = 0.0, Lpp = 0.0, L3 = 0.0, F = 0.0;
+    const double t2 = t * t;
+    double Sq = 0.0, Lpp = 0.0, L3 = 0.0, Sl = 0.0;
     for (int m = tid; m < M; m += SC::NT) {
         const uint32_t wa = __ldg(&Xb[(size_t)a * Mw + (m >> 5)]);
         const uint32_t wb = __ldg(&Xb[(size_t)b * Mw + (m >> 5)]);
-        {
-            const double xa = xsign(wa, m & 31), xb = xsign(wb, m & 31);
-            const double ya = xb * T(a, m);
-            const double yb = xa * T(b, m);
-            const double s = xa * xb;
-            const double da = 1.0 / (1.0 + ya * t);
-            const double db = 1.0 / (1.0 + yb * t);
-            const double qa = (ya + t) * da, qb = (yb + t) * db;
-            Lp += (2.0 * s - qa) - qb;
-            const double d1a = (1.0 - ya * ya) * omt2 * da * da, d1b = (1.0 - yb * yb) * omt2 * db * db;
-            Lpp -= d1a + d1b;
-            L3 += 2.0 * (qa * d1a + qb * d1b);
-            if (kNeedF) {
-                const double la = A + log1p(-0.5 * (1.0 - sg * ya) * E);
-                const double lb = A + log1p(-0.5 * (1.0 - sg * yb) * E);
-                F += (2.0 * s * D - la) - lb;
-            }
-        }
+        const double xa = xsign(wa, m & 31), xb = xsign(wb, m & 31);
+        const double ya = xb * T(a, m);
+        const double yb = xa * T(b, m);
+        const double A = fma(ya, t, 1.0), B = fma(yb, t, 1.0);
+        const double r = rcp64(A * B);
+        const double da = B * r, db = A * r;
+        const double qa = (ya + t) * da, qb = (yb + t) * db;
+        Sq += qa + qb;
+        const double d1a = (1.0 - ya * ya) * omt2 * da * da, d1b = (1.0 - yb * yb) * omt2 * db * db;
+        Lpp -= d1a + d1b;
+        if (kL3) L3 += 2.0 * (qa * d1a + qb * d1b);
+        if (kNeedF) Sl += log1p(fma((ya + yb), t, ya * yb * t2));
     }
-    sc.sum4(Lp, Lpp, L3, F);
+    sc.sum4(Sq, Lpp, L3, Sl);
     Pass64 r;
-    r.Lp = Lp;
+    r.Lp = 2.0 * dot - Sq;
     r.Lpp = Lpp;
     r.Lppp = L3;
-    r.Flik = kNeedF ? F : 0.0;
+    if (kNeedF) {
+        const double ad = fabs(D);
+        const double lncosh = ad + log1p(exp(-2.0 * ad)) - 0.69314718055994530942;
+        r.Flik = (2.0 * D * dot - 2.0 * M * lncosh) - Sl;
+    } else {
+        r.Flik = 0.0;
+    }
     return r;
 }
 
@@ -164,7 +186,7 @@ struct EdgeOptD {
 template <class TP, class SC = WarpScope>
 __device__ EdgeOptD ising_newton64(const TP& T, const uint32_t* __restrict__ Xb, int Mw, int M, int a, int b,
                                    double w_cur, double lambda, double dir, double phi0, double phi1,
-                                   double phi2, int passes, const SC& sc = SC()) {
+                                   double phi2, int passes, int dot, const SC& sc = SC()) {
     EdgeOptD r;
     r.warn = 0;
     r.passes = passes;
@@ -179,8 +201,8 @@ __device__ EdgeOptD ising_newton64(const TP& T, const uint32_t* __restrict__ Xb,
         const double scale = fmax(u, 1e-3);
         const bool final_try = fabs(du_last) <= 0.03 * scale;
         const double D = dir * u - w_cur;
-        const Pass64 p = final_try ? ising_pass64<TP, true, SC>(T, Xb, Mw, M, a, b, D, sc)
-                                   : ising_pass64<TP, false, SC>(T, Xb, Mw, M, a, b, D, sc);
+        const Pass64 p = final_try ? ising_pass64<TP, true, SC>(T, Xb, Mw, M, a, b, D, dot, sc)
+                                   : ising_pass64<TP, false, SC>(T, Xb, Mw, M, a, b, D, dot, sc);
         ++r.passes;
         const double phi = dir * p.Lp - lambda, dphi = p.Lpp;
         const double du = (dphi < 0.0) ? -phi / dphi : NAN;
@@ -205,7 +227,7 @@ __device__ EdgeOptD ising_newton64(const TP& T, const uint32_t* __restrict__ Xb,
         if (isinf(hi) && un > 64.0) {
             // separable columns: the slice saturates numerically; stop once the
             // objective no longer increases (the reference's doubling stops there too)
-            const Pass64 pf = ising_pass64<TP, true, SC>(T, Xb, Mw, M, a, b, dir * un - w_cur, sc);
+            const Pass64 pf = ising_pass64<TP, true, SC>(T, Xb, Mw, M, a, b, dir * un - w_cur, dot, sc);
             ++r.passes;
             const double F = pf.Flik - lambda * un;
             if (!(F > prevF)) break;
@@ -216,7 +238,7 @@ __device__ EdgeOptD ising_newton64(const TP& T, const uint32_t* __restrict__ Xb,
         if (hi - lo <= 1e-15 * fmax(1.0, u)) du_last = 0.0;
     }
     // plateau / bracket failure: objective at the last iterate
-    const Pass64 pf = ising_pass64<TP, true, SC>(T, Xb, Mw, M, a, b, dir * u - w_cur, sc);
+    const Pass64 pf = ising_pass64<TP, true, SC>(T, Xb, Mw, M, a, b, dir * u - w_cur, dot, sc);
     ++r.passes;
     const double gain = (pf.Flik - lambda * u) + lambda * fabs(w_cur);
     if (gain < 0.0) {
@@ -235,8 +257,9 @@ __device__ EdgeOptD ising_newton64(const TP& T, const uint32_t* __restrict__ Xb,
 template <class TP, class SC = WarpScope>
 __device__ EdgeOptD ising_optimize_edge64(const TP& T, const uint32_t* __restrict__ Xb, int Mw, int M,
                                           int a, int b, double w_cur, double lambda, const SC& sc = SC()) {
-    const Pass64 p0 = w_cur != 0.0 ? ising_pass64<TP, true, SC>(T, Xb, Mw, M, a, b, -w_cur, sc)
-                                   : ising_pass64<TP, false, SC>(T, Xb, Mw, M, a, b, 0.0, sc);
+    const int dot = spin_dot<SC>(Xb, Mw, M, a, b, sc);
+    const Pass64 p0 = w_cur != 0.0 ? ising_pass64<TP, true, SC, true>(T, Xb, Mw, M, a, b, -w_cur, dot, sc)
+                                   : ising_pass64<TP, false, SC, true>(T, Xb, Mw, M, a, b, 0.0, dot, sc);
     const double g0 = p0.Lp;
     if (fabs(g0) <= lambda) {
         EdgeOptD r;
@@ -250,7 +273,7 @@ __device__ EdgeOptD ising_optimize_edge64(const TP& T, const uint32_t* __restric
     }
     const double dir = g0 > 0.0 ? 1.0 : -1.0;
     return ising_newton64<TP, SC>(T, Xb, Mw, M, a, b, w_cur, lambda, dir, fabs(g0) - lambda, p0.Lpp,
-                                  dir * p0.Lppp, 1, sc);
+                                  dir * p0.Lppp, 1, dot, sc);
 }
 
 // T rows staged in shared memory (update kernel: tanh computed once per pair)

@@ -25,31 +25,36 @@ __device__ __forceinline__ float flipf(float v, uint32_t bit) {
     return __uint_as_float(__float_as_uint(v) ^ ((bit ^ 1u) << 31));
 }
 
-template <int MQ>
-struct Col32 {
-    float4 T[MQ];
-    uint32_t w[MQ];  // word holding this lane's 4 sign bits for chunk q
+// Register column of one node for the screen: lane l holds samples
+// m = 8 (l + 32 q) + c, c < 8, of chunk q < HQ as one 16-byte fp16 load, plus the packed
+// spin word holding their 8 sign bits (word l/4 + 8q, bits 8 (l%4) + c).
+template <int HQ>
+struct Col16 {
+    uint4 T[HQ];
+    uint32_t w[HQ];
 };
 
-template <int MQ>
-__device__ __forceinline__ void load_col32(Col32<MQ>& c, const IsingSnap& S, int row, int lane) {
-    const float4* t4 = reinterpret_cast<const float4*>(S.T32 + (size_t)row * S.Mp);
+template <int HQ>
+__device__ __forceinline__ void load_col16(Col16<HQ>& c, const IsingSnap& S, int row, int lane) {
+    const uint4* t = reinterpret_cast<const uint4*>(S.T16 + (size_t)row * S.Mp);
 #pragma unroll
-    for (int q = 0; q < MQ; ++q) {
-        c.T[q] = __ldg(&t4[lane + 32 * q]);
-        c.w[q] = __ldg(&S.Xb[(size_t)row * S.Mw + (lane >> 3) + 4 * q]);
+    for (int q = 0; q < HQ; ++q) {
+        c.T[q] = __ldg(&t[lane + 32 * q]);
+        c.w[q] = __ldg(&S.Xb[(size_t)row * S.Mw + (lane >> 2) + 8 * q]);
     }
 }
 
-__device__ __forceinline__ float comp(const float4& v, int c) {
-    return c == 0 ? v.x : (c == 1 ? v.y : (c == 2 ? v.z : v.w));
+__device__ __forceinline__ float2 h2f(uint32_t v) {
+    __half2 h;
+    memcpy(&h, &v, 4);
+    return __half22float2(h);
 }
 
 // K1: the bandwidth-bound screen.  Pruned pairs are finished here; the rest
 // (survivors, existing edges, kink decisions inside the fp32 error band) are
 // appended to a compacted list for K2.
-template <int MQ>
-__global__ void __launch_bounds__(256, 2) ising_screen_kernel(IsingSnap S, HashView W,
+template <int HQ>
+__global__ void __launch_bounds__(256, HQ <= 4 ? 3 : 2) ising_screen_kernel(IsingSnap S, HashView W,
                                                               const int32_t* __restrict__ es,
                                                               const int32_t* __restrict__ ep, uint64_t n,
                                                               int chunk, double lambda, double base,
@@ -61,11 +66,13 @@ __global__ void __launch_bounds__(256, 2) ising_screen_kernel(IsingSnap S, HashV
     const int lane = threadIdx.x & 31;
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    Col32<MQ> cs, cp;
+    Col16<HQ> cs, cp;
     int cur = -1;
     float tabs_s = 0.f;
     uint64_t evals = 0;
-    const float gam = (float)(4 * MQ + 8) * 5.9604645e-08f * 1.01f;  // 2^-24 per rounding
+    // |g32 - g64| <= (2^-11 (fp16 field) + (8 HQ + 8) 2^-24 (fp32 sums)) sum|T| + 2M 2^-24
+    const float gam = (4.8828125e-04f + (float)(8 * HQ + 8) * 5.9604645e-08f) * 1.01f;
+    const float err0 = 2.f * (float)S.M * 5.9604645e-08f;
     const float lam = (float)lambda;
     const double pruned_dist = -(base + 0.0);
     for (uint64_t c0 = warp0 * chunk; c0 < n; c0 += nwarps * chunk) {
@@ -73,7 +80,7 @@ __global__ void __launch_bounds__(256, 2) ising_screen_kernel(IsingSnap S, HashV
         for (uint64_t e = c0; e < c1; ++e) {
             const int s = es[e], p = ep[e];
             if (s != cur) {
-                load_col32<MQ>(cs, S, s, lane);
+                load_col16<HQ>(cs, S, s, lane);
                 tabs_s = __ldg(&S.Tabs[s]);
                 cur = s;
             }
@@ -81,7 +88,7 @@ __global__ void __launch_bounds__(256, 2) ising_screen_kernel(IsingSnap S, HashV
             // pins Tabs[p] next to the column loads); the W lookup overlaps them
             float tabs_p;
             asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(tabs_p) : "l"(S.Tabs + p));
-            load_col32<MQ>(cp, S, p, lane);
+            load_col16<HQ>(cp, S, p, lane);
             const double wcur = hash_get(W, pair_key(s, p), 0.0);
             bool pruned = false;
             float gk = 0.f;
@@ -90,21 +97,25 @@ __global__ void __launch_bounds__(256, 2) ising_screen_kernel(IsingSnap S, HashV
                 // g0 = 2<x_a,x_b> - sum_m (x_p T_s + x_s T_p)
                 float acc = 0.f;
                 int diff = 0;
-                const int sh = 4 * (lane & 7);
+                const int sh = 8 * (lane & 3);
 #pragma unroll
-                for (int q = 0; q < MQ; ++q) {
-                    const uint32_t ws = cs.w[q], wp = cp.w[q];
-                    if ((lane & 7) == 0) diff += __popc(ws ^ wp);
+                for (int q = 0; q < HQ; ++q) {
+                    const uint32_t ws = cs.w[q] >> sh, wp = cp.w[q] >> sh;
+                    if ((lane & 3) == 0) diff += __popc(cs.w[q] ^ cp.w[q]);
+                    const uint32_t ts[4] = {cs.T[q].x, cs.T[q].y, cs.T[q].z, cs.T[q].w};
+                    const uint32_t tp[4] = {cp.T[q].x, cp.T[q].y, cp.T[q].z, cp.T[q].w};
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
-                        const uint32_t bs = (ws >> (sh + c)) & 1u, bp = (wp >> (sh + c)) & 1u;
-                        acc += flipf(comp(cs.T[q], c), bp) + flipf(comp(cp.T[q], c), bs);
+                        const float2 fs = h2f(ts[c]), fp = h2f(tp[c]);
+                        const uint32_t b0 = 2 * c, b1 = 2 * c + 1;
+                        acc += flipf(fs.x, (wp >> b0) & 1u) + flipf(fp.x, (ws >> b0) & 1u);
+                        acc += flipf(fs.y, (wp >> b1) & 1u) + flipf(fp.y, (ws >> b1) & 1u);
                     }
                 }
                 acc = warp_sum(acc);
                 diff = warp_sum(diff);
                 const float g = (float)(2 * (S.M - 2 * diff)) - acc;
-                const float err = gam * (tabs_s + tabs_p) + 1e-30f;
+                const float err = gam * (tabs_s + tabs_p) + err0;
                 pruned = fabsf(g) <= lam - err;
                 flag = fabsf(g) < lam + err ? 1 : 0;
                 gk = g;
@@ -156,7 +167,8 @@ __global__ void __launch_bounds__(128) ising_refine_kernel(IsingSnap S, HashView
         const double dir = g > 0.f ? 1.0 : -1.0;
         const double phi0 = fabs((double)g) - lambda;
         const double phi1 = -(2.0 * S.M - S.Tsq[a] - S.Tsq[b]);
-        r = ising_newton64(T64, S.Xb, S.Mw, S.M, a, b, 0.0, lambda, dir, phi0, phi1, 0.0, 0);
+        const int dot = spin_dot(S.Xb, S.Mw, S.M, a, b);
+        r = ising_newton64(T64, S.Xb, S.Mw, S.M, a, b, 0.0, lambda, dir, phi0, phi1, 0.0, 0, dot);
     } else {
         const double wcur = hash_get(W, pair_key(a, b), 0.0);
         r = ising_optimize_edge64(T64, S.Xb, S.Mw, S.M, a, b, wcur, lambda);
@@ -271,11 +283,11 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
     const double base = mode == EXACT ? generation_base(c) : 0.0;
     c.tic();
     const int sms = num_sms(c);
-    const int MQ = c.Mp / 128;
-    if (c.kind == ISING && mode == EXACT && MQ <= 16) {
+    const int HQ = c.Mp / 256;
+    if (c.kind == ISING && mode == EXACT && HQ <= 8) {
         const int chunk = 8;
         const uint64_t chunks = (n + chunk - 1) / chunk;
-        const uint64_t blocks = std::min<uint64_t>((chunks + 7) / 8, (uint64_t)sms * 8);
+        const uint64_t blocks = std::min<uint64_t>((chunks + 7) / 8, (uint64_t)sms * 12);
         const IsingSnap S = c.isnap();
         const HashView W = c.Wview();
         uint64_t* surv = c.sc_surv.as<uint64_t>(n);
@@ -288,7 +300,7 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
     ising_screen_kernel<Q><<<(unsigned)blocks, 256, 0, c.stream>>>(S, W, s, p, n, chunk, c.lambda, base, \
                                                                     out, surv, surv_g, surv_flag, nsurv,   \
                                                                     c.dcounters())
-        switch (MQ) {
+        switch (HQ) {
             case 1: NRG_LAUNCH_MQ(1); break;
             case 2: NRG_LAUNCH_MQ(2); break;
             case 3: NRG_LAUNCH_MQ(3); break;
@@ -297,10 +309,6 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
             case 6: NRG_LAUNCH_MQ(6); break;
             case 7: NRG_LAUNCH_MQ(7); break;
             case 8: NRG_LAUNCH_MQ(8); break;
-            case 10: NRG_LAUNCH_MQ(10); break;
-            case 12: NRG_LAUNCH_MQ(12); break;
-            case 14: NRG_LAUNCH_MQ(14); break;
-            case 16: NRG_LAUNCH_MQ(16); break;
             default: fail(100, "unsupported padded sample count");
         }
 #undef NRG_LAUNCH_MQ

@@ -53,13 +53,9 @@ void ctx_init(Context& c, int n, int m, int kind, double lambda, int device) {
     NRG_CUDA(cudaEventCreate(&c.ev1));
     NRG_CUDA(cudaEventCreate(&c.kev0));
     NRG_CUDA(cudaEventCreate(&c.kev1));
-    // Mp = 128 * MQ with MQ one of the instantiated register widths of the fused
-    // Ising screen (score.cu); beyond 2048 samples plain 128-multiples (fp64 path)
-    {
-        int mq = (int)std::max<int64_t>(1, ceil_div(m, 128));
-        if (mq > 8 && mq <= 16) mq = (mq + 1) / 2 * 2;
-        c.Mp = 128 * mq;
-    }
+    // Mp = 256 * HQ: one 16-byte fp16 load per lane per 256 samples in the Ising screen
+    // (score.cu instantiates HQ = 1..8, i.e. M <= 2048; larger M uses the fp64 path)
+    c.Mp = 256 * (int)std::max<int64_t>(1, ceil_div(m, 256));
     c.Mw = c.Mp / 32;
     const size_t nm = (size_t)n * c.Mp;
     c.H.ensure(nm * sizeof(double));
@@ -314,7 +310,7 @@ void get_sums(Context& c, double* out) {
 // Ising: T = tanh(H + theta) per node-sample, fp64 master + fp32 copy for the
 // bandwidth-bound screen, with sum|T32| per node for its rigorous error bound.
 __global__ void snapshot_ising_kernel(const double* __restrict__ H, const double* __restrict__ theta,
-                                      int M, int Mp, double* __restrict__ T64, float* __restrict__ T32,
+                                      int M, int Mp, double* __restrict__ T64, __half* __restrict__ T16,
                                       float* __restrict__ Tabs, double* __restrict__ Tsq) {
     const int r = blockIdx.x;
     const double th = theta[r];
@@ -323,9 +319,9 @@ __global__ void snapshot_ising_kernel(const double* __restrict__ H, const double
         double t = 0.0;
         if (m < M) t = tanh(H[(size_t)r * Mp + m] + th);
         T64[(size_t)r * Mp + m] = t;
-        const float f = (float)t;
-        T32[(size_t)r * Mp + m] = f;
-        a += fabs((double)f);
+        const __half h = __double2half(t);
+        T16[(size_t)r * Mp + m] = h;
+        a += fabs((double)__half2float(h));
         q += t * t;
     }
     __shared__ double sh[32], sq[32];
@@ -378,12 +374,12 @@ void ensure_snapshot(Context& c) {
     const size_t nm = (size_t)c.n * c.Mp;
     if (c.kind == ISING) {
         c.T64.ensure(nm * 8);
-        c.T32.ensure(nm * 4);
+        c.T16.ensure(nm * 2);
         c.Tabs.ensure((size_t)c.n * 4);
         c.Tsq.ensure((size_t)c.n * 8);
         snapshot_ising_kernel<<<c.n, 256, 0, c.stream>>>(c.dH(), c.dtheta(), c.M, c.Mp,
                                                          static_cast<double*>(c.T64.p),
-                                                         static_cast<float*>(c.T32.p),
+                                                         static_cast<__half*>(c.T16.p),
                                                          static_cast<float*>(c.Tabs.p),
                                                          static_cast<double*>(c.Tsq.p));
     } else {

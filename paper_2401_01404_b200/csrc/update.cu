@@ -69,11 +69,14 @@ __device__ __forceinline__ void hash_set(HashView h, uint64_t key, double w, uns
         }
         if (k == kEmptyKey) {
             if (w == 0.0) return;  // absent and zero: nothing stored
-            __stcg(&h.vals[s], w);  // value first; the slot is invisible until the key lands
-            __threadfence();
+            // claim the slot first, then store the value: writing the value before the CAS
+            // lets a losing inserter of another key overwrite the winner's value.  Only
+            // this pair's successors read vals[s], and they are ordered after us by the
+            // done flags; concurrent probes for other keys compare keys only.
             const unsigned long long prev =
                 atomicCAS((unsigned long long*)&h.keys[s], (unsigned long long)kEmptyKey, (unsigned long long)key);
             if (prev == kEmptyKey) {
+                __stcg(&h.vals[s], w);
                 atomicAdd(&cnt[0], 1ull);
                 atomicAdd(&cnt[1], 1ull);
                 return;

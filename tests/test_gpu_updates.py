@@ -99,3 +99,26 @@ def test_device_generator_and_full_iteration(gpu):
     assert objs[1] > objs[0] and objs[2] >= objs[1] - 1e-6 * abs(objs[1])
     ne = len(m.get_state()[1])
     assert 500 < ne < 20000
+
+
+def test_concurrent_inserts_keep_their_values(gpu):
+    """set_edges on many node-disjoint pairs: the update kernel inserts them into the
+    coupling hash concurrently (probe chains collide); every value must read back as
+    written (regression: value stored before the slot claim could be overwritten by a
+    losing inserter of another key)."""
+    n, M = 20000, 64
+    rng = np.random.default_rng(11)
+    X = np.where(rng.random((n, M)) < 0.5, 1, -1).astype(np.int8)
+    m = gpu.Model.from_samples(X, gpu.NRG_ISING, 1.0)
+    for rep in range(4):
+        perm = rng.permutation(n)
+        ei, ej = perm[0::2].astype(np.int32), perm[1::2].astype(np.int32)
+        w = rng.uniform(0.01, 0.5, len(ei)) * rng.choice([-1.0, 1.0], len(ei))
+        m.reset_state()
+        m.set_edges(ei, ej, w)
+        _, gi, gj, gw = m.get_state()
+        lo, hi = np.minimum(ei, ej), np.maximum(ei, ej)
+        order = np.lexsort((hi, lo))
+        np.testing.assert_array_equal(gi, lo[order])
+        np.testing.assert_array_equal(gj, hi[order])
+        np.testing.assert_array_equal(gw, w[order])
