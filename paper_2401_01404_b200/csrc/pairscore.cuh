@@ -109,10 +109,12 @@ struct TLive {
     }
 };
 
-// 1/x for x = (1 + y_a tanh D)(1 + y_b tanh D) in (0, 4): fp32 reciprocal refined by two fp64 Newton
-// steps (relative error ~2^-96 before rounding), a third of the cost of an IEEE divide
+// 1/x for x = (1 + y_a tanh D)(1 + y_b tanh D) in (0, 4): the MUFU.RCP64H seed
+// (rcp.approx.ftz.f64, ~2^-22) refined by two fp64 Newton steps (~2^-88 before
+// rounding); a third of the cost of an IEEE divide and no fp32 round trip.
 __device__ __forceinline__ double rcp64(double x) {
-    double r = (double)__frcp_rn((float)x);
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
     r = r * fma(-x, r, 2.0);
     r = r * fma(-x, r, 2.0);
     return r;
@@ -132,35 +134,71 @@ __device__ __forceinline__ int spin_dot(const uint32_t* __restrict__ Xb, int Mw,
 //   q_a = (y_a + t) B / (A B),  q_b = (y_b + t) A / (A B)        (one reciprocal)
 //   L'  = 2 <x_a,x_b> - sum (q_a + q_b),   L'' = -sum (1-q_a^2) + (1-q_b^2)
 //   F   = 2 D <x_a,x_b> - 2 M ln cosh D - sum log1p((y_a + y_b) t + y_a y_b t^2)
-// (ln(cosh D + y sinh D) = ln cosh D + ln(1 + y t); one log1p per sample for both
-// sides).  kNeedF adds the objective, kL3 the third derivative (kink pass only).
+// (ln(cosh D + y sinh D) = ln cosh D + ln(1 + y t), and 1 + (y_a + y_b) t + y_a y_b t^2
+// = A B).  kNeedF adds the objective, kL3 the third derivative (kink pass only).
 template <class TP, bool kNeedF, class SC = WarpScope, bool kL3 = false>
 __device__ __forceinline__ Pass64 ising_pass64(const TP& T, const uint32_t* __restrict__ Xb, int Mw,
                                                int M, int a, int b, double D, int dot, const SC& sc = SC()) {
+    // kU independent accumulator sets per thread for a warp scope: the fp64 add chains,
+    // not the math, bound a single-set loop at the occupancy the scoring kernels run at
+    // (a CTA scope has enough warps and only a few samples per thread)
+    constexpr int kU = SC::NT >= 128 ? 1 : 4;
     const int tid = sc.tid();
     const double t = tanh(D);
     const double omt2 = 1.0 - t * t;
     const double t2 = t * t;
-    double Sq = 0.0, Lpp = 0.0, L3 = 0.0, Sl = 0.0;
-    for (int m = tid; m < M; m += SC::NT) {
-        const uint32_t wa = __ldg(&Xb[(size_t)a * Mw + (m >> 5)]);
-        const uint32_t wb = __ldg(&Xb[(size_t)b * Mw + (m >> 5)]);
-        const double xa = xsign(wa, m & 31), xb = xsign(wb, m & 31);
-        const double ya = xb * T(a, m);
-        const double yb = xa * T(b, m);
-        const double A = fma(ya, t, 1.0), B = fma(yb, t, 1.0);
-        const double r = rcp64(A * B);
-        const double da = B * r, db = A * r;
-        const double qa = (ya + t) * da, qb = (yb + t) * db;
-        Sq += qa + qb;
-        const double d1a = (1.0 - ya * ya) * omt2 * da * da, d1b = (1.0 - yb * yb) * omt2 * db * db;
-        Lpp -= d1a + d1b;
-        if (kL3) L3 += 2.0 * (qa * d1a + qb * d1b);
-        if (kNeedF) Sl += log1p(fma((ya + yb), t, ya * yb * t2));
+    // objective: sum ln(A B) as one log per kU samples of the product (A B >= 1/4 for
+    // |t| <= 1/2, so a product of kU factors stays far from under/overflow); per-sample
+    // log1p beyond that
+    const bool prodlog = fabs(t) <= 0.5;
+    double Sq[kU], Lq[kU], L3q[kU], Slq[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) Sq[u] = Lq[u] = L3q[u] = Slq[u] = 0.0;
+    double P = 1.0;
+    int nP = 0;
+    for (int m0 = tid; m0 < M; m0 += SC::NT * kU) {
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int m = m0 + u * SC::NT;
+            if (m < M) {
+                const uint32_t wa = __ldg(&Xb[(size_t)a * Mw + (m >> 5)]);
+                const uint32_t wb = __ldg(&Xb[(size_t)b * Mw + (m >> 5)]);
+                const double xa = xsign(wa, m & 31), xb = xsign(wb, m & 31);
+                const double ya = xb * T(a, m);
+                const double yb = xa * T(b, m);
+                const double A = fma(ya, t, 1.0), B = fma(yb, t, 1.0);
+                const double AB = A * B;
+                const double r = rcp64(AB);
+                const double da = B * r, db = A * r;
+                const double qa = (ya + t) * da, qb = (yb + t) * db;
+                Sq[u] += qa + qb;
+                const double d1a = (1.0 - ya * ya) * omt2 * da * da, d1b = (1.0 - yb * yb) * omt2 * db * db;
+                Lq[u] -= d1a + d1b;
+                if (kL3) L3q[u] += 2.0 * (qa * d1a + qb * d1b);
+                if (kNeedF) {
+                    if (prodlog) P *= AB;
+                    else Slq[u] += log1p(fma((ya + yb), t, ya * yb * t2));
+                }
+            }
+        }
+        if (kNeedF && prodlog && (nP += kU) >= 4) {
+            Slq[0] += log(P);
+            P = 1.0;
+            nP = 0;
+        }
     }
-    sc.sum4(Sq, Lpp, L3, Sl);
+    if (kNeedF && prodlog && nP) Slq[0] += log(P);
+    double Sqs = Sq[0], Lpp = Lq[0], L3 = L3q[0], Sl = Slq[0];
+#pragma unroll
+    for (int u = 1; u < kU; ++u) {
+        Sqs += Sq[u];
+        Lpp += Lq[u];
+        L3 += L3q[u];
+        Sl += Slq[u];
+    }
+    sc.sum4(Sqs, Lpp, L3, Sl);
     Pass64 r;
-    r.Lp = 2.0 * dot - Sq;
+    r.Lp = 2.0 * dot - Sqs;
     r.Lpp = Lpp;
     r.Lppp = L3;
     if (kNeedF) {
@@ -173,30 +211,71 @@ __device__ __forceinline__ Pass64 ising_pass64(const TP& T, const uint32_t* __re
     return r;
 }
 
+// fp32 pass over the fp32 field copy (warp scope): L'(w) and L''(w) at w = dir u for
+// w_cur = 0, for the Newton iterations ahead of the final fp64 pass.  Lane l owns
+// samples 4 l + 128 j .. +3 (one 16-byte load per row and step).
+struct Pass32 {
+    float Lp, Lpp;
+};
+__device__ __forceinline__ float rcp32(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ Pass32 ising_pass32(const float* __restrict__ T32, int Mp, const uint32_t* __restrict__ Xb,
+                                               int Mw, int M, int a, int b, float t, int dot) {
+    const int lane = threadIdx.x & 31;
+    const float4* Ta = reinterpret_cast<const float4*>(T32 + (size_t)a * Mp);
+    const float4* Tb = reinterpret_cast<const float4*>(T32 + (size_t)b * Mp);
+    float Sq = 0.f, Lq = 0.f;
+    for (int m0 = 4 * lane; m0 < M; m0 += 128) {
+        const float4 va = __ldg(&Ta[m0 >> 2]), vb = __ldg(&Tb[m0 >> 2]);
+        const uint32_t wa = __ldg(&Xb[(size_t)a * Mw + (m0 >> 5)]) >> (m0 & 31);
+        const uint32_t wb = __ldg(&Xb[(size_t)b * Mw + (m0 >> 5)]) >> (m0 & 31);
+        const float ta[4] = {va.x, va.y, va.z, va.w}, tb[4] = {vb.x, vb.y, vb.z, vb.w};
+        float s = 0.f, l = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (m0 + c < M) {
+                const float ya = ((wb >> c) & 1u) ? ta[c] : -ta[c];
+                const float yb = ((wa >> c) & 1u) ? tb[c] : -tb[c];
+                const float A = fmaf(ya, t, 1.f), B = fmaf(yb, t, 1.f);
+                const float r = rcp32(A * B);
+                const float da = B * r, db = A * r;
+                s += (ya + t) * da + (yb + t) * db;
+                l += fmaf(-ya, ya, 1.f) * da * da + fmaf(-yb, yb, 1.f) * db * db;
+            }
+        }
+        Sq += s;
+        Lq += l;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        Sq += __shfl_xor_sync(0xffffffffu, Sq, o);
+        Lq += __shfl_xor_sync(0xffffffffu, Lq, o);
+    }
+    return {(float)(2 * dot) - Sq, -(1.f - t * t) * Lq};
+}
+
 struct EdgeOptD {
     double w, gain;
     int warn;
     int passes;
 };
 
-// Safeguarded Newton for phi(u) = dir L'(dir u) - lambda = 0 on u > 0 (D = dir u - w_cur),
-// started from the root of the quadratic model phi0 + phi1 u + phi2 u^2/2 (phi1 < 0).
-// Passes without the log1p objective until the step predicts convergence; the last
-// pass evaluates the slice gain and applies the second-order Newton correction.
+// Safeguarded Newton for phi(u) = dir L'(w) - lambda = 0 on u > 0 (w = dir u,
+// D = w - w_cur), from the iterate u.  Passes without the objective until the last
+// step predicts convergence (|du_last| small: the first pass when the caller already
+// converged u, e.g. in fp32); that pass evaluates the slice gain and applies the
+// second-order Newton correction, so the gain is exact to O(du^3).
 template <class TP, class SC = WarpScope>
-__device__ EdgeOptD ising_newton64(const TP& T, const uint32_t* __restrict__ Xb, int Mw, int M, int a, int b,
-                                   double w_cur, double lambda, double dir, double phi0, double phi1,
-                                   double phi2, int passes, int dot, const SC& sc = SC()) {
+__device__ EdgeOptD ising_newton64_at(const TP& T, const uint32_t* __restrict__ Xb, int Mw, int M, int a, int b,
+                                      double w_cur, double lambda, double dir, double u, double du_last,
+                                      int passes, int dot, const SC& sc = SC()) {
     EdgeOptD r;
     r.warn = 0;
     r.passes = passes;
-    double u;
-    {
-        const double disc = phi1 * phi1 - 2.0 * phi2 * phi0;
-        u = (disc >= 0.0 && phi1 < 0.0) ? 2.0 * phi0 / (-phi1 + sqrt(disc)) : phi0 / fmax(-phi1, 1e-300);
-        if (!(u > 0.0) || !isfinite(u)) u = 1.0;
-    }
-    double lo = 0.0, hi = INFINITY, du_last = u, prevF = -INFINITY;
+    double lo = 0.0, hi = INFINITY, prevF = -INFINITY;
     for (int it = 0; it < 100; ++it) {
         const double scale = fmax(u, 1e-3);
         const bool final_try = fabs(du_last) <= 0.03 * scale;
@@ -249,6 +328,44 @@ __device__ EdgeOptD ising_newton64(const TP& T, const uint32_t* __restrict__ Xb,
         r.gain = gain;
     }
     return r;
+}
+
+// Newton from the quadratic model phi0 + phi1 u + phi2 u^2 / 2 of phi at u = 0.
+template <class TP, class SC = WarpScope>
+__device__ EdgeOptD ising_newton64(const TP& T, const uint32_t* __restrict__ Xb, int Mw, int M, int a, int b,
+                                   double w_cur, double lambda, double dir, double phi0, double phi1,
+                                   double phi2, int passes, int dot, const SC& sc = SC()) {
+    const double disc = phi1 * phi1 - 2.0 * phi2 * phi0;
+    double u = (disc >= 0.0 && phi1 < 0.0) ? 2.0 * phi0 / (-phi1 + sqrt(disc)) : phi0 / fmax(-phi1, 1e-300);
+    if (!(u > 0.0) || !isfinite(u)) u = 1.0;
+    return ising_newton64_at<TP, SC>(T, Xb, Mw, M, a, b, w_cur, lambda, dir, u, u, passes, dot, sc);
+}
+
+// Newton iterations in fp32 for a certain survivor (w_cur = 0, |g0| > lambda) from the
+// quadratic-model start u; returns the fp32-converged iterate (|error| ~ 1e-7 / M) for
+// the single fp64 objective pass, or the start when fp32 cannot be trusted (|u| large,
+// no descent).  Adds the passes spent to *passes.
+__device__ __forceinline__ double ising_newton32(const IsingSnap& S, int a, int b, double lambda, double dir,
+                                                 double u0, int dot, int* passes, bool* conv) {
+    *conv = false;
+    float u = (float)u0;
+    const float lam = (float)lambda, fd = (float)dir;
+    for (int it = 0; it < 12; ++it) {
+        if (!(u > 0.f && u < 2.f)) return u0;
+        const Pass32 p = ising_pass32(S.T32, S.Mp, S.Xb, S.Mw, S.M, a, b, tanhf(fd * u), dot);
+        ++*passes;
+        const float phi = fd * p.Lp - lam;
+        if (!(p.Lpp < 0.f)) return u0;
+        const float du = -phi / p.Lpp;
+        float un = u + du;
+        if (!(un > 0.f)) un = 0.5f * u;
+        u = un;
+        if (fabsf(du) <= 1e-4f * fmaxf(u, 1e-3f)) {
+            *conv = true;
+            return (double)u;
+        }
+    }
+    return (double)u;
 }
 
 // Full fp64 optimize_edge for the Ising slice (a < b canonical): the kink pass at

@@ -143,8 +143,10 @@ __global__ void __launch_bounds__(256, HQ <= 4 ? 3 : 2) ising_screen_kernel(Isin
 
 // K2: survivors.  Certain survivors (w_cur = 0, |g0| > lambda + err) start Newton
 // from K1's fp32 g0 and the per-node sums Tsq = sum T^2 (second derivative at 0 is
-// -(2M - Tsq_a - Tsq_b)), so no fp64 pass is spent at w = 0: typically one or two
-// fp64 passes without and one with the log1p objective.  Existing edges and kink
+// -(2M - Tsq_a - Tsq_b)), so no pass is spent at w = 0; Newton then runs in fp32 on
+// the fp32 field copy (8 bytes per sample pair per pass) to fp32 convergence, and one
+// fp64 pass on T64 evaluates the objective, the exact derivative and the second-order
+// correction (the gain is exact to O(du^3), du ~ 1e-7 / M).  Existing edges and kink
 // decisions inside the error band take the full fp64 routine.  (A third-derivative
 // start computed in K1 was tried: it cost K1 35% for no K2 gain.)
 __global__ void __launch_bounds__(128) ising_refine_kernel(IsingSnap S, HashView W, const int32_t* __restrict__ es,
@@ -168,7 +170,11 @@ __global__ void __launch_bounds__(128) ising_refine_kernel(IsingSnap S, HashView
         const double phi0 = fabs((double)g) - lambda;
         const double phi1 = -(2.0 * S.M - S.Tsq[a] - S.Tsq[b]);
         const int dot = spin_dot(S.Xb, S.Mw, S.M, a, b);
-        r = ising_newton64(T64, S.Xb, S.Mw, S.M, a, b, 0.0, lambda, dir, phi0, phi1, 0.0, 0, dot);
+        const double u0 = phi0 / fmax(-phi1, 1e-300);
+        int passes = 0;
+        bool conv = false;
+        const double u = ising_newton32(S, a, b, lambda, dir, u0, dot, &passes, &conv);
+        r = ising_newton64_at(T64, S.Xb, S.Mw, S.M, a, b, 0.0, lambda, dir, u, conv ? 0.0 : u, passes, dot);
     } else {
         const double wcur = hash_get(W, pair_key(a, b), 0.0);
         r = ising_optimize_edge64(T64, S.Xb, S.Mw, S.M, a, b, wcur, lambda);

@@ -307,11 +307,13 @@ void get_sums(Context& c, double* out) {
 }
 
 // ---------------------------------------------------------------- snapshot (K0)
-// Ising: T = tanh(H + theta) per node-sample, fp64 master + fp32 copy for the
-// bandwidth-bound screen, with sum|T32| per node for its rigorous error bound.
+// Ising: T = tanh(H + theta) per node-sample: fp64 master, fp32 copy for the Newton
+// iterations, fp16 copy for the bandwidth-bound screen with sum|T16| per node for its
+// rigorous error bound, and sum T^2 per node.
 __global__ void snapshot_ising_kernel(const double* __restrict__ H, const double* __restrict__ theta,
-                                      int M, int Mp, double* __restrict__ T64, __half* __restrict__ T16,
-                                      float* __restrict__ Tabs, double* __restrict__ Tsq) {
+                                      int M, int Mp, double* __restrict__ T64, float* __restrict__ T32,
+                                      __half* __restrict__ T16, float* __restrict__ Tabs,
+                                      double* __restrict__ Tsq) {
     const int r = blockIdx.x;
     const double th = theta[r];
     double a = 0.0, q = 0.0;
@@ -319,6 +321,7 @@ __global__ void snapshot_ising_kernel(const double* __restrict__ H, const double
         double t = 0.0;
         if (m < M) t = tanh(H[(size_t)r * Mp + m] + th);
         T64[(size_t)r * Mp + m] = t;
+        T32[(size_t)r * Mp + m] = (float)t;
         const __half h = __double2half(t);
         T16[(size_t)r * Mp + m] = h;
         a += fabs((double)__half2float(h));
@@ -375,10 +378,12 @@ void ensure_snapshot(Context& c) {
     if (c.kind == ISING) {
         c.T64.ensure(nm * 8);
         c.T16.ensure(nm * 2);
+        c.T32.ensure(nm * 4);
         c.Tabs.ensure((size_t)c.n * 4);
         c.Tsq.ensure((size_t)c.n * 8);
         snapshot_ising_kernel<<<c.n, 256, 0, c.stream>>>(c.dH(), c.dtheta(), c.M, c.Mp,
                                                          static_cast<double*>(c.T64.p),
+                                                         static_cast<float*>(c.T32.p),
                                                          static_cast<__half*>(c.T16.p),
                                                          static_cast<float*>(c.Tabs.p),
                                                          static_cast<double*>(c.Tsq.p));

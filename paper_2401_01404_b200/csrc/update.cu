@@ -113,7 +113,7 @@ struct UpdateArgs {
 // of levels at config 4), so per-update latency, not throughput, bounds the phase;
 // NT threads share each pass over the samples with block reductions.
 template <int NT>
-__global__ void __launch_bounds__(NT) update_kernel(UpdateArgs A) {
+__global__ void __launch_bounds__(NT, 3) update_kernel(UpdateArgs A) {
     extern __shared__ double stage_smem[];
     __shared__ double red[4 * (NT / 32) + 4];
     __shared__ unsigned long long s_p;
