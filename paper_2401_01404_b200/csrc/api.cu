@@ -107,7 +107,7 @@ void gcd_iteration(nrg_ctx* x, const nrg_gcd_cfg* cfg, int iter, nrg_iter_record
     }
     if (n_cands) *n_cands = best.count;
     const double delta = nrg::apply_updates(c, static_cast<int32_t*>(x->out_i.p), static_cast<int32_t*>(x->out_j.p),
-                                            best.count, nullptr);
+                                            best.count, nullptr, static_cast<double*>(x->out_d.p));
     nrg::theta_pass(c, nullptr);
     const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     const double obj = nrg::log_posterior(c);
@@ -305,14 +305,17 @@ int nrg_apply_updates(nrg_ctx* x, const nrg_pair* cands, uint64_t n, double* del
     return guardx(x, [&] {
         need_samples(x);
         std::vector<int32_t> hi(n), hj(n);
+        std::vector<double> hd(n);
         for (uint64_t t = 0; t < n; ++t) {
             hi[t] = cands[t].i;
             hj[t] = cands[t].j;
+            hd[t] = cands[t].dist;
         }
         check_pairs(x, n, hi.data(), hj.data());
         int32_t* di = to_dev(x, x->q_i, hi.data(), n);
         int32_t* dj = to_dev(x, x->q_j, hj.data(), n);
-        const double d = nrg::apply_updates(x->c, di, dj, n, nullptr);
+        double* dd = to_dev(x, x->q_d, hd.data(), n);
+        const double d = nrg::apply_updates(x->c, di, dj, n, nullptr, dd);
         if (delta) *delta = d;
     });
 }
@@ -367,6 +370,7 @@ int nrg_reset_counters(nrg_ctx* x) {
         NRG_CUDA(cudaMemsetAsync(x->c.counters.p, 0, nrg::C_N * 8, x->c.stream));
         for (double& v : x->c.phase_ms) v = 0.0;
         x->c.k1_ms = x->c.k1_launches = x->c.k1_pairs = x->c.k2_ms = x->c.k2_launches = x->c.k2_pairs = 0;
+        x->c.tail_rounds = 0;
         x->c.launches0 = nrg::g_launches.load();
         x->c.sync();
     });
@@ -399,9 +403,9 @@ int nrg_timer(nrg_ctx* x, int32_t op, double* ms) {
 int nrg_kernel_stats(nrg_ctx* x, double* out, int32_t cap) {
     return guardx(x, [&] {
         const nrg::Context& c = x->c;
-        const double v[7] = {c.k1_ms, c.k1_launches, c.k1_pairs, c.k2_ms, c.k2_launches, c.k2_pairs,
-                             (double)(nrg::g_launches.load() - c.launches0)};
-        for (int t = 0; t < 7 && t < cap; ++t) out[t] = v[t];
+        const double v[8] = {c.k1_ms, c.k1_launches, c.k1_pairs, c.k2_ms, c.k2_launches, c.k2_pairs,
+                             (double)(nrg::g_launches.load() - c.launches0), c.tail_rounds};
+        for (int t = 0; t < 8 && t < cap; ++t) out[t] = v[t];
     });
 }
 

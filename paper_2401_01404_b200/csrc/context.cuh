@@ -191,6 +191,7 @@ struct Context {
     double phase_ms[P_N] = {0};
     // per-kernel stats: K1 screen ms / launches / pairs, K2 refine ms / launches / survivors
     double k1_ms = 0, k1_launches = 0, k1_pairs = 0, k2_ms = 0, k2_launches = 0, k2_pairs = 0;
+    double tail_rounds = 0;  // apply_updates: parallel rounds spent on tie tails
     uint64_t launches0 = 0;
     cudaEvent_t kev0 = nullptr, kev1 = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -274,9 +275,10 @@ void edge_gradient_live(Context& c, const int32_t* i, const int32_t* j, uint64_t
 uint64_t sample_scored_pairs(Context& c, uint64_t cap, uint64_t seed, int32_t* oi, int32_t* oj);
 
 // ---- update.cu
-// candidates (device arrays, canonical i<j) in order; assign==nullptr -> optimize_edge
+// candidates (device arrays, canonical i<j) in order; assign==nullptr -> optimize_edge;
+// dist (optional, device): the candidates' distances, used only to find a tie tail
 double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n,
-                     const double* assign);
+                     const double* assign, const double* dist = nullptr);
 void theta_pass(Context& c, double* out_only);
 
 // ---- knn.cu

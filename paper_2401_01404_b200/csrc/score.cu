@@ -286,7 +286,8 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
         return;
     }
     ensure_snapshot(c);
-    const double base = mode == EXACT ? generation_base(c) : 0.0;
+    // the generation base only enters distances (update rounds ask for w alone)
+    const double base = (mode == EXACT && (out.dist || out.cache_vals)) ? generation_base(c) : 0.0;
     c.tic();
     const int sms = num_sms(c);
     const int HQ = c.Mp / 256;

@@ -250,12 +250,12 @@ static int update_grid(Context& c, size_t smem) {
     return sms * per;  // persistent grid: every CTA resident (the dependency waits need it)
 }
 
-double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n, const double* assign) {
-    if (n == 0) return 0.0;
-    if (n >= (1ull << 31)) fail(22, "apply_updates: too many candidates");
-    c.tic();
-    w_reserve(c, n);
-    DevBuf kb, vb, k2b, v2b, depb, doneb, tb, adb, tmpb, sb;
+// The dependency-ordered kernel over candidates [0, n) of (ci, cj): |w - w_cur| per
+// pair into absdelta.
+static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n, const double* assign,
+                        double* absdelta) {
+    if (n == 0) return;
+    DevBuf kb, vb, k2b, v2b, depb, doneb, tb, tmpb;
     uint64_t* keys = kb.as<uint64_t>(2 * n);
     uint32_t* vals = vb.as<uint32_t>(2 * n);
     uint64_t* keys2 = k2b.as<uint64_t>(2 * n);
@@ -263,7 +263,6 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
     int32_t* dep = depb.as<int32_t>(2 * n);
     int* done = doneb.as<int>(n);
     unsigned long long* ticket = tb.as<unsigned long long>(1);
-    double* absdelta = adb.as<double>(n);
     dep_keys_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(ci, cj, n, keys, vals);
     size_t bytes = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, keys2, vals, vals2, (int64_t)(2 * n), 0, 64, c.stream);
@@ -325,6 +324,85 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
         }
         fprintf(stderr, "apply_updates debug: n=%llu grid=%d dep mismatches=%d done=%d\n", (unsigned long long)n, grid,
                 bad, ndone);
+    }
+}
+
+__global__ void tail_start_kernel(const double* __restrict__ dist, uint64_t n, unsigned long long* k) {
+    const uint64_t p = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p + 1 < n && dist[p] != dist[n - 1]) atomicMax(k, (unsigned long long)(p + 1));
+}
+
+// first p in [lo, n) whose re-evaluated coupling w[p - lo] differs from the current one
+__global__ void first_change_kernel(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj, uint64_t lo,
+                                    uint64_t n, const double* __restrict__ w, HashView W,
+                                    unsigned long long* first) {
+    const uint64_t p = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= n) return;
+    const int i = ci[p], j = cj[p];
+    const double wcur = hash_get(W, pair_key(min(i, j), max(i, j)), 0.0);
+    if (w[p - lo] != wcur) atomicMin(first, (unsigned long long)p);
+}
+
+constexpr uint64_t kTailMin = 256;  // shorter tie tails go through the ordered kernel
+constexpr int kTailRounds = 32;     // flips in a tail before the rest is ordered instead
+
+// detail::apply_edge_updates, sequential semantics.  A FindBest list sorted by
+// distance ends in a block of exact ties -- at a converging state mostly the
+// zero-gain (kink) pairs, listed by (i, j), so a few low-id nodes sit in tens of
+// thousands of them and the dependency chain through those nodes is as long as the
+// block.  Such a tail is resolved in rounds instead: every remaining pair is
+// re-evaluated in parallel against the current state; all pairs before the first one
+// whose coupling would change are no-ops in the sequential loop too (nothing before
+// them changed), the first changing pair is applied at that same state, and the next
+// round starts after it.  The prefix before the tail and any tail with too many
+// changes go through the dependency-ordered kernel.  `dist` (device, optional) only
+// locates the tail; results never depend on it.
+double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n, const double* assign,
+                     const double* dist) {
+    if (n == 0) return 0.0;
+    if (n >= (1ull << 31)) fail(22, "apply_updates: too many candidates");
+    c.tic();
+    w_reserve(c, n);
+    DevBuf adb, sb, kb, wb;
+    double* absdelta = adb.as<double>(n);
+    NRG_CUDA(cudaMemsetAsync(absdelta, 0, n * 8, c.stream));
+    uint64_t k = n;
+    if (!assign && dist && n >= kTailMin && !getenv("NRG_ORDERED_ONLY")) {
+        unsigned long long* dk = kb.as<unsigned long long>(1);
+        NRG_CUDA(cudaMemsetAsync(dk, 0, 8, c.stream));
+        tail_start_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(dist, n, dk);
+        NRG_LAUNCH_CHECK();
+        unsigned long long hk = 0;
+        NRG_CUDA(cudaMemcpyAsync(&hk, dk, 8, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        if (n - hk >= kTailMin) k = hk;
+    }
+    ordered_run(c, ci, cj, k, assign, absdelta);
+    uint64_t start = k;
+    for (int round = 0; start < n; ++round) {
+        if (round == kTailRounds) {
+            ordered_run(c, ci + start, cj + start, n - start, nullptr, absdelta + start);
+            break;
+        }
+        c.state_version++;  // the evaluation snapshot must include every update so far
+        double* w = wb.as<double>(n - start);
+        ScoreOut out;
+        out.w = w;
+        c.toc(P_UPDATE);
+        score_entries(c, EXACT, ci + start, cj + start, n - start, out);  // times itself as P_SCORE
+        c.tic();
+        unsigned long long* first = kb.as<unsigned long long>(1);
+        NRG_CUDA(cudaMemcpyAsync(first, &n, 8, cudaMemcpyHostToDevice, c.stream));
+        first_change_kernel<<<(unsigned)ceil_div(n - start, 256), 256, 0, c.stream>>>(ci, cj, start, n, w, c.Wview(),
+                                                                                      first);
+        NRG_LAUNCH_CHECK();
+        unsigned long long f = n;
+        NRG_CUDA(cudaMemcpyAsync(&f, first, 8, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        c.tail_rounds++;
+        if (f >= n) break;
+        ordered_run(c, ci + f, cj + f, 1, nullptr, absdelta + f);
+        start = f + 1;
     }
     double* sum = sb.as<double>(1);
     sum_fixed_kernel<<<1, 1024, 0, c.stream>>>(absdelta, n, sum);
