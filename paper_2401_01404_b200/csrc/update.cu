@@ -332,38 +332,55 @@ __global__ void tail_start_kernel(const double* __restrict__ dist, uint64_t n, u
     if (p + 1 < n && dist[p] != dist[n - 1]) atomicMax(k, (unsigned long long)(p + 1));
 }
 
-// first p in [lo, n) whose re-evaluated coupling w[p - lo] differs from the current one
-__global__ void first_change_kernel(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj, uint64_t lo,
+// changed[p - lo] = 1 when the re-evaluated coupling of pair p differs from the current one
+__global__ void change_flags_kernel(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj, uint64_t lo,
                                     uint64_t n, const double* __restrict__ w, HashView W,
-                                    unsigned long long* first) {
+                                    uint8_t* __restrict__ changed) {
     const uint64_t p = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p >= n) return;
     const int i = ci[p], j = cj[p];
     const double wcur = hash_get(W, pair_key(min(i, j), max(i, j)), 0.0);
-    if (w[p - lo] != wcur) atomicMin(first, (unsigned long long)p);
+    changed[p - lo] = w[p - lo] != wcur ? 1 : 0;
+}
+
+__global__ void gather_pairs_kernel(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj,
+                                    const uint32_t* __restrict__ idx, uint32_t m, int32_t* __restrict__ oi,
+                                    int32_t* __restrict__ oj) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m) return;
+    oi[t] = ci[idx[t]];
+    oj[t] = cj[idx[t]];
+}
+
+__global__ void scatter_delta_kernel(const double* __restrict__ d, const uint32_t* __restrict__ idx, uint32_t m,
+                                     double* __restrict__ absdelta) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < m) absdelta[idx[t]] = d[t];
 }
 
 constexpr uint64_t kTailMin = 256;  // shorter tie tails go through the ordered kernel
-constexpr int kTailRounds = 32;     // flips in a tail before the rest is ordered instead
+constexpr int kTailRounds = 64;     // rounds before the rest of a tail is ordered instead
 
 // detail::apply_edge_updates, sequential semantics.  A FindBest list sorted by
 // distance ends in a block of exact ties -- at a converging state mostly the
 // zero-gain (kink) pairs, listed by (i, j), so a few low-id nodes sit in tens of
 // thousands of them and the dependency chain through those nodes is as long as the
 // block.  Such a tail is resolved in rounds instead: every remaining pair is
-// re-evaluated in parallel against the current state; all pairs before the first one
-// whose coupling would change are no-ops in the sequential loop too (nothing before
-// them changed), the first changing pair is applied at that same state, and the next
-// round starts after it.  The prefix before the tail and any tail with too many
-// changes go through the dependency-ordered kernel.  `dist` (device, optional) only
-// locates the tail; results never depend on it.
+// re-evaluated in parallel against the current state, then walked in list order
+// keeping the set of nodes the round modifies.  A pair touching none of them sees
+// exactly the state the sequential loop would give it, so its evaluation stands:
+// no-ops are done, changing pairs are applied (node-disjoint, so one ordered launch
+// applies them all exactly).  The first pair touching a modified node ends the round
+// and starts the next.  The prefix before the tail, and a tail with more changes
+// than rounds left, go through the dependency-ordered kernel.  `dist` (device,
+// optional) only locates the tail; results never depend on it.
 double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n, const double* assign,
                      const double* dist) {
     if (n == 0) return 0.0;
     if (n >= (1ull << 31)) fail(22, "apply_updates: too many candidates");
     c.tic();
     w_reserve(c, n);
-    DevBuf adb, sb, kb, wb;
+    DevBuf adb, sb, kb, wb, fb, ib, pib, pjb, ddb;
     double* absdelta = adb.as<double>(n);
     NRG_CUDA(cudaMemsetAsync(absdelta, 0, n * 8, c.stream));
     uint64_t k = n;
@@ -379,30 +396,78 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
     }
     ordered_run(c, ci, cj, k, assign, absdelta);
     uint64_t start = k;
-    for (int round = 0; start < n; ++round) {
-        if (round == kTailRounds) {
-            ordered_run(c, ci + start, cj + start, n - start, nullptr, absdelta + start);
-            break;
+    if (start < n) {
+        const uint64_t nt = n - start;
+        std::vector<int32_t> hi(nt), hj(nt);
+        std::vector<uint8_t> hch(nt);
+        NRG_CUDA(cudaMemcpyAsync(hi.data(), ci + start, nt * 4, cudaMemcpyDeviceToHost, c.stream));
+        NRG_CUDA(cudaMemcpyAsync(hj.data(), cj + start, nt * 4, cudaMemcpyDeviceToHost, c.stream));
+        std::vector<uint8_t> mod(c.n, 0);
+        std::vector<int32_t> touched;
+        std::vector<uint32_t> apply;
+        for (int round = 0; start < n; ++round) {
+            if (round == kTailRounds) {
+                ordered_run(c, ci + start, cj + start, n - start, nullptr, absdelta + start);
+                break;
+            }
+            c.state_version++;  // the evaluation snapshot must include every update so far
+            const uint64_t m = n - start;
+            double* w = wb.as<double>(m);
+            ScoreOut out;
+            out.w = w;
+            c.toc(P_UPDATE);
+            score_entries(c, EXACT, ci + start, cj + start, m, out);  // times itself as P_SCORE
+            c.tic();
+            uint8_t* ch = fb.as<uint8_t>(m);
+            change_flags_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, c.stream>>>(ci, cj, start, n, w, c.Wview(), ch);
+            NRG_LAUNCH_CHECK();
+            NRG_CUDA(cudaMemcpyAsync(hch.data(), ch, m, cudaMemcpyDeviceToHost, c.stream));
+            c.sync();
+            c.tail_rounds++;
+            uint64_t nch = 0;
+            for (uint64_t q = 0; q < m; ++q) nch += hch[q];
+            if (nch > (uint64_t)(kTailRounds - round)) {
+                // more changes than rounds left (a tail still far from converged, e.g. the
+                // first sweep): the ordered kernel is the faster exact path
+                ordered_run(c, ci + start, cj + start, m, nullptr, absdelta + start);
+                break;
+            }
+            apply.clear();
+            uint64_t p = start;
+            for (; p < n; ++p) {
+                const uint64_t q = p - k;
+                const int a = hi[q], b = hj[q];
+                if (mod[a] || mod[b]) break;
+                if (hch[p - start]) {
+                    apply.push_back((uint32_t)p);
+                    mod[a] = mod[b] = 1;
+                    touched.push_back(a);
+                    touched.push_back(b);
+                }
+            }
+            if (getenv("NRG_DEBUG_TAIL")) {
+                fprintf(stderr, "tail round %d: start=%llu m=%llu changed=%llu applied=%zu stop=%llu\n", round,
+                        (unsigned long long)start, (unsigned long long)m, (unsigned long long)nch, apply.size(),
+                        (unsigned long long)p);
+            }
+            for (int32_t v : touched) mod[v] = 0;
+            touched.clear();
+            if (!apply.empty()) {
+                const uint32_t na = (uint32_t)apply.size();
+                uint32_t* di = ib.as<uint32_t>(na);
+                int32_t* pi = pib.as<int32_t>(na);
+                int32_t* pj = pjb.as<int32_t>(na);
+                double* dd = ddb.as<double>(na);
+                NRG_CUDA(cudaMemcpyAsync(di, apply.data(), na * 4, cudaMemcpyHostToDevice, c.stream));
+                gather_pairs_kernel<<<ceil_div(na, 256), 256, 0, c.stream>>>(ci, cj, di, na, pi, pj);
+                NRG_LAUNCH_CHECK();
+                ordered_run(c, pi, pj, na, nullptr, dd);
+                scatter_delta_kernel<<<ceil_div(na, 256), 256, 0, c.stream>>>(dd, di, na, absdelta);
+                NRG_LAUNCH_CHECK();
+                c.sync();  // `apply` is reused next round
+            }
+            start = p;
         }
-        c.state_version++;  // the evaluation snapshot must include every update so far
-        double* w = wb.as<double>(n - start);
-        ScoreOut out;
-        out.w = w;
-        c.toc(P_UPDATE);
-        score_entries(c, EXACT, ci + start, cj + start, n - start, out);  // times itself as P_SCORE
-        c.tic();
-        unsigned long long* first = kb.as<unsigned long long>(1);
-        NRG_CUDA(cudaMemcpyAsync(first, &n, 8, cudaMemcpyHostToDevice, c.stream));
-        first_change_kernel<<<(unsigned)ceil_div(n - start, 256), 256, 0, c.stream>>>(ci, cj, start, n, w, c.Wview(),
-                                                                                      first);
-        NRG_LAUNCH_CHECK();
-        unsigned long long f = n;
-        NRG_CUDA(cudaMemcpyAsync(&f, first, 8, cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
-        c.tail_rounds++;
-        if (f >= n) break;
-        ordered_run(c, ci + f, cj + f, 1, nullptr, absdelta + f);
-        start = f + 1;
     }
     double* sum = sb.as<double>(1);
     sum_fixed_kernel<<<1, 1024, 0, c.stream>>>(absdelta, n, sum);
