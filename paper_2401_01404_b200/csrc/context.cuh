@@ -8,7 +8,8 @@
 //   theta f64 [N]
 //   W    open-addressing hash pair_key -> w  (inc/sparse_weights.hpp:162)
 //   per-generation snapshot (frozen W, inc/model.hpp:32-35):
-//     Ising:    T64 f64 [N][Mp] = tanh(H+theta), T32 / T16 copies, Tabs = sum|T16|, Tsq = sum T64^2
+//     Ising:    T64 f64 [N][Mp] = tanh(H+theta), T32 copy, int8 T8 + bit planes P8 + per-node
+//               {step, error, sum} Q8 for the screen, Tsq = sum T64^2
 //     Gaussian: U   f64 [N][Mp] = X + theta^2 H,  xx f64 [N] = sum x^2
 //   DistanceCache: open-addressing hash pair_key -> dist (inc/model.hpp:36-97)
 // Mp = M rounded up to 256 (one 16-byte fp16 load per lane per 256 samples); padding is zero.
@@ -113,10 +114,11 @@ __device__ __forceinline__ double hash_get(const HashView h, uint64_t key, doubl
 
 struct IsingSnap {
     const uint32_t* Xb;
-    const __half* T16;   // fp16 copy of the field for the bandwidth-bound screen
     const float* T32;    // fp32 copy for the Newton iterations ahead of the final fp64 pass
     const double* T64;
-    const float* Tabs;   // sum |T16| per node, rounded up (rigorous screen error bound)
+    const int8_t* T8;    // int8 field T8 = round(T / d) for the screen (partner side)
+    const uint32_t* P8;  // T8's 8 bit planes per 32-sample word (screen, register side)
+    const float4* Q8;    // per node {d, E = sum |T - d T8| rounded up, sum T8 (int bits), 0}
     const double* Tsq;   // sum T64^2 per node (L''(0) = -(2M - Tsq_a - Tsq_b) for w_cur = 0)
     int M, Mp, Mw;
 };
@@ -171,7 +173,7 @@ struct Context {
     uint64_t state_version = 1;
 
     // snapshot
-    DevBuf T16, T32, T64, Tabs, Tsq, U, xx;
+    DevBuf T32, T64, T8, P8, Q8, Tsq, U, xx;
     uint64_t snap_version = 0;
     bool base_valid = false;
     double base = 0.0;
@@ -221,8 +223,8 @@ struct Context {
         return {static_cast<uint64_t*>(Ckeys.p), static_cast<double*>(Cvals.p), Ccap - 1};
     }
     IsingSnap isnap() {
-        return {dXb(), static_cast<__half*>(T16.p), static_cast<float*>(T32.p), static_cast<double*>(T64.p),
-                static_cast<float*>(Tabs.p), static_cast<double*>(Tsq.p), M, Mp, Mw};
+        return {dXb(), static_cast<float*>(T32.p), static_cast<double*>(T64.p), static_cast<int8_t*>(T8.p),
+                static_cast<uint32_t*>(P8.p), static_cast<float4*>(Q8.p), static_cast<double*>(Tsq.p), M, Mp, Mw};
     }
     GaussSnap gsnap() {
         return {dXd(), static_cast<double*>(U.p), static_cast<double*>(xx.p), dtheta(), M, Mp};

@@ -1,18 +1,19 @@
 // score.cu — the pair-scoring kernels: distance() (inc/model.hpp:377-386) for
 // worklists of candidate pairs.
 //
-// Ising exact mode is one fused warp-per-pair kernel:
-//   K1 (every pair, bandwidth-bound): g0 = 2<x_a,x_b> - <x_b,T_a> - <x_a,T_b> from
-//      bit-packed spins (popcount) and the fp32 snapshot T32, with a rigorous fp32
-//      error bound err; |g0| <= lambda - err  =>  pruned: w* = 0, gain = 0 exactly,
-//      dist = -base (the reference's tie value, inc/model.hpp:205-209).
-//   K2 (survivors, ~2-3%): safeguarded Newton in fp32 on the register-resident
-//      columns, then ONE fp64 pass over T64 that evaluates L', L'' and the slice gain
-//      at the fp32 root and applies the second-order Newton correction.
-//   Existing edges (w_cur != 0), kink decisions inside the error band and fp32
-//   failures go to the full fp64 routine (pairscore.cuh).
-// The stationary column (first entry of a worklist run) stays in registers across
-// consecutive entries, so each pair streams only its partner: M/8 + 4 Mp bytes.
+// Ising exact mode (M <= 2048) runs two kernels:
+//   K1 (every pair, bandwidth-bound): g0 = 2<x_a,x_b> - <x_b,T_a> - <x_a,T_b> in exact
+//      integer arithmetic on the snapshot's int8 field (per-node step d, rigorous
+//      quantisation error E per node): popcount over bit planes and dp4a.
+//      |g0| <= lambda - err  =>  pruned: w* = 0, gain = 0 exactly, dist = -base (the
+//      reference's tie value, inc/model.hpp:205-209).  Streams M + M/8 bytes per pair.
+//   K2 (survivors, a few per mille at a converging state): Newton in fp32 on the fp32
+//      field, then ONE fp64 pass over T64 that evaluates L', L'' and the slice gain at
+//      the fp32 root and applies the second-order Newton correction.  Existing edges
+//      (w_cur != 0) and kink decisions inside the error band take the full fp64 routine
+//      (pairscore.cuh).
+// The stationary node's operands (first entry of a worklist run) stay in registers
+// across consecutive entries, so each pair streams only its partner.
 #include <algorithm>
 #include <vector>
 
@@ -20,41 +21,53 @@
 
 namespace nrg {
 
-__device__ __forceinline__ float flipf(float v, uint32_t bit) {
-    // multiply by x = +1 (bit 1) / -1 (bit 0), exactly
-    return __uint_as_float(__float_as_uint(v) ^ ((bit ^ 1u) << 31));
-}
-
-// Register column of one node for the screen: lane l holds samples
-// m = 8 (l + 32 q) + c, c < 8, of chunk q < HQ as one 16-byte fp16 load, plus the packed
-// spin word holding their 8 sign bits (word l/4 + 8q, bits 8 (l%4) + c).
-template <int HQ>
-struct Col16 {
-    uint4 T[HQ];
-    uint32_t w[HQ];
+// Register side of the screen for one node: for each 32-sample word w = lane + 32 q
+// (q < HW) the 8 bit planes of T8 (sum_{m: b_m = 1} T8_m = sum_k 2^k popc(P_k & b) with
+// the sign plane weighted -2^7), the spins as +-1 bytes for dp4a, and the spin word.
+template <int HW>
+struct Src8 {
+    uint32_t P[HW][8];
+    uint32_t X[HW][8];
+    uint32_t b[HW];
 };
 
-template <int HQ>
-__device__ __forceinline__ void load_col16(Col16<HQ>& c, const IsingSnap& S, int row, int lane) {
-    const uint4* t = reinterpret_cast<const uint4*>(S.T16 + (size_t)row * S.Mp);
+// 4 spin bits -> 4 bytes of +1 (bit 1) / -1 (bit 0)
+__device__ __forceinline__ uint32_t pm1_bytes(uint32_t nib) {
+    const uint32_t m = ((nib & 0xfu) * 0x00204081u) & 0x01010101u;  // bit i -> byte i bit 0
+    return ((m * 0xffu) ^ 0xfefefefeu) | 0x01010101u;               // 1 -> 0x01, 0 -> 0xff
+}
+
+template <int HW>
+__device__ __forceinline__ void load_src8(Src8<HW>& c, const IsingSnap& S, int row, int lane) {
 #pragma unroll
-    for (int q = 0; q < HQ; ++q) {
-        c.T[q] = __ldg(&t[lane + 32 * q]);
-        c.w[q] = __ldg(&S.Xb[(size_t)row * S.Mw + (lane >> 2) + 8 * q]);
+    for (int q = 0; q < HW; ++q) {
+        const int w = lane + 32 * q;
+        if (w < S.Mw) {
+            const uint4* pp = reinterpret_cast<const uint4*>(S.P8 + ((size_t)row * S.Mw + w) * 8);
+            const uint4 p0 = __ldg(pp), p1 = __ldg(pp + 1);
+            c.P[q][0] = p0.x, c.P[q][1] = p0.y, c.P[q][2] = p0.z, c.P[q][3] = p0.w;
+            c.P[q][4] = p1.x, c.P[q][5] = p1.y, c.P[q][6] = p1.z, c.P[q][7] = p1.w;
+            c.b[q] = __ldg(&S.Xb[(size_t)row * S.Mw + w]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) c.P[q][k] = 0u;
+            c.b[q] = 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) c.X[q][j] = pm1_bytes(c.b[q] >> (4 * j));
     }
 }
 
-__device__ __forceinline__ float2 h2f(uint32_t v) {
-    __half2 h;
-    memcpy(&h, &v, 4);
-    return __half22float2(h);
-}
-
-// K1: the bandwidth-bound screen.  Pruned pairs are finished here; the rest
-// (survivors, existing edges, kink decisions inside the fp32 error band) are
-// appended to a compacted list for K2.
-template <int HQ>
-__global__ void __launch_bounds__(256, HQ <= 4 ? 3 : 2) ising_screen_kernel(IsingSnap S, HashView W,
+// K1: the bandwidth-bound screen on the int8 field.  Per pair (s stationary, p streamed)
+//   g0 = 2<x_s,x_p> - sum_m x_p T_s - sum_m x_s T_p
+//      ~ 2 (M - 2 popc(b_s ^ b_p)) - d_s (2 sum_{b_p=1} T8_s - sum T8_s) - d_p sum x_s T8_p
+// in exact integer arithmetic (popc over the source's bit planes, dp4a of the partner's
+// int8 field against the source's +-1 bytes), |g0 - g| <= E_s + E_p (+ fp32 rounding).
+// Pruned pairs are finished here; the rest (survivors, existing edges, kink decisions
+// inside the error band) are appended to a compacted list for K2.  Streams M + M/8 bytes
+// per pair.
+template <int HW>
+__global__ void __launch_bounds__(256, HW == 1 ? 4 : 3) ising_screen_kernel(IsingSnap S, HashView W,
                                                               const int32_t* __restrict__ es,
                                                               const int32_t* __restrict__ ep, uint64_t n,
                                                               int chunk, double lambda, double base,
@@ -66,56 +79,70 @@ __global__ void __launch_bounds__(256, HQ <= 4 ? 3 : 2) ising_screen_kernel(Isin
     const int lane = threadIdx.x & 31;
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    Col16<HQ> cs, cp;
+    Src8<HW> cs;
     int cur = -1;
-    float tabs_s = 0.f;
+    float4 qs = make_float4(0.f, 0.f, 0.f, 0.f);
     uint64_t evals = 0;
-    // |g32 - g64| <= (2^-11 (fp16 field) + (8 HQ + 8) 2^-24 (fp32 sums)) sum|T| + 2M 2^-24
-    const float gam = (4.8828125e-04f + (float)(8 * HQ + 8) * 5.9604645e-08f) * 1.01f;
-    const float err0 = 2.f * (float)S.M * 5.9604645e-08f;
+    const float err0 = 4.f * (float)S.M * 5.9604645e-08f;  // fp32 rounding of the combination
     const float lam = (float)lambda;
     const double pruned_dist = -(base + 0.0);
     for (uint64_t c0 = warp0 * chunk; c0 < n; c0 += nwarps * chunk) {
-        const uint64_t c1 = c0 + chunk < n ? c0 + chunk : n;
+        const uint64_t c1 = min(c0 + (uint64_t)chunk, n);
         for (uint64_t e = c0; e < c1; ++e) {
             const int s = es[e], p = ep[e];
             if (s != cur) {
-                load_col16<HQ>(cs, S, s, lane);
-                tabs_s = __ldg(&S.Tabs[s]);
+                load_src8<HW>(cs, S, s, lane);
+                qs = __ldg(&S.Q8[s]);
                 cur = s;
             }
-            // issue the partner column and its error-bound sum first (the volatile load
-            // pins Tabs[p] next to the column loads); the W lookup overlaps them
-            float tabs_p;
-            asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(tabs_p) : "l"(S.Tabs + p));
-            load_col16<HQ>(cp, S, p, lane);
+            // partner loads first (the W lookup and the per-node constants overlap them)
+            uint4 t0[HW], t1[HW];
+            uint32_t bp[HW];
+#pragma unroll
+            for (int q = 0; q < HW; ++q) {
+                const int w = lane + 32 * q;
+                if (w < S.Mw) {
+                    const uint4* tp = reinterpret_cast<const uint4*>(S.T8 + (size_t)p * S.Mp + 32 * w);
+                    t0[q] = __ldg(tp);
+                    t1[q] = __ldg(tp + 1);
+                    bp[q] = __ldg(&S.Xb[(size_t)p * S.Mw + w]);
+                } else {
+                    t0[q] = t1[q] = make_uint4(0u, 0u, 0u, 0u);
+                    bp[q] = 0u;
+                }
+            }
+            const float4 qp = __ldg(&S.Q8[p]);
             const double wcur = hash_get(W, pair_key(s, p), 0.0);
             bool pruned = false;
             float gk = 0.f;
             uint8_t flag = 2;  // 2: existing edge (full fp64), 1: kink inside the error band, 0: survivor
             if (wcur == 0.0) {
-                // g0 = 2<x_a,x_b> - sum_m (x_p T_s + x_s T_p)
-                float acc = 0.f;
-                int diff = 0;
-                const int sh = 8 * (lane & 3);
+                int a1 = 0, a2 = 0, diff = 0;
 #pragma unroll
-                for (int q = 0; q < HQ; ++q) {
-                    const uint32_t ws = cs.w[q] >> sh, wp = cp.w[q] >> sh;
-                    if ((lane & 3) == 0) diff += __popc(cs.w[q] ^ cp.w[q]);
-                    const uint32_t ts[4] = {cs.T[q].x, cs.T[q].y, cs.T[q].z, cs.T[q].w};
-                    const uint32_t tp[4] = {cp.T[q].x, cp.T[q].y, cp.T[q].z, cp.T[q].w};
+                for (int q = 0; q < HW; ++q) {
+                    const uint32_t b = bp[q];
+                    int lo = 0;
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        const float2 fs = h2f(ts[c]), fp = h2f(tp[c]);
-                        const uint32_t b0 = 2 * c, b1 = 2 * c + 1;
-                        acc += flipf(fs.x, (wp >> b0) & 1u) + flipf(fp.x, (ws >> b0) & 1u);
-                        acc += flipf(fs.y, (wp >> b1) & 1u) + flipf(fp.y, (ws >> b1) & 1u);
-                    }
+                    for (int k = 0; k < 7; ++k) lo += __popc(cs.P[q][k] & b) << k;
+                    a1 += lo - (__popc(cs.P[q][7] & b) << 7);
+                    const uint32_t tw[8] = {t0[q].x, t0[q].y, t0[q].z, t0[q].w, t1[q].x, t1[q].y, t1[q].z, t1[q].w};
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) a2 = __dp4a((int)tw[j], (int)cs.X[q][j], a2);
+                    diff += __popc(cs.b[q] ^ b);
                 }
-                acc = warp_sum(acc);
-                diff = warp_sum(diff);
-                const float g = (float)(2 * (S.M - 2 * diff)) - acc;
-                const float err = gam * (tabs_s + tabs_p) + err0;
+                // one packed reduction for (a1, diff): |a1| <= 127 M < 2^19, diff <= M < 2^12
+                int v = (a1 << 12) + diff;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    v += __shfl_xor_sync(0xffffffffu, v, o);
+                    a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+                }
+                const int dsum = v & 4095;
+                const int asum = (v - dsum) >> 12;
+                const float A = qs.x * (float)(2 * asum - __float_as_int(qs.z));
+                const float B = qp.x * (float)a2;
+                const float g = (float)(2 * (S.M - 2 * dsum)) - (A + B);
+                const float err = (qs.y + qp.y) * 1.0001f + err0;
                 pruned = fabsf(g) <= lam - err;
                 flag = fabsf(g) < lam + err ? 1 : 0;
                 gk = g;
@@ -290,8 +317,8 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
     const double base = (mode == EXACT && (out.dist || out.cache_vals)) ? generation_base(c) : 0.0;
     c.tic();
     const int sms = num_sms(c);
-    const int HQ = c.Mp / 256;
-    if (c.kind == ISING && mode == EXACT && HQ <= 8) {
+    const int HW = (c.Mp + 1023) / 1024;  // 32-sample words per lane
+    if (c.kind == ISING && mode == EXACT && HW <= 2) {
         const int chunk = 8;
         const uint64_t chunks = (n + chunk - 1) / chunk;
         const uint64_t blocks = std::min<uint64_t>((chunks + 7) / 8, (uint64_t)sms * 12);
@@ -307,15 +334,9 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
     ising_screen_kernel<Q><<<(unsigned)blocks, 256, 0, c.stream>>>(S, W, s, p, n, chunk, c.lambda, base, \
                                                                     out, surv, surv_g, surv_flag, nsurv,   \
                                                                     c.dcounters())
-        switch (HQ) {
+        switch (HW) {
             case 1: NRG_LAUNCH_MQ(1); break;
             case 2: NRG_LAUNCH_MQ(2); break;
-            case 3: NRG_LAUNCH_MQ(3); break;
-            case 4: NRG_LAUNCH_MQ(4); break;
-            case 5: NRG_LAUNCH_MQ(5); break;
-            case 6: NRG_LAUNCH_MQ(6); break;
-            case 7: NRG_LAUNCH_MQ(7); break;
-            case 8: NRG_LAUNCH_MQ(8); break;
             default: fail(100, "unsupported padded sample count");
         }
 #undef NRG_LAUNCH_MQ

@@ -308,42 +308,83 @@ void get_sums(Context& c, double* out) {
 
 // ---------------------------------------------------------------- snapshot (K0)
 // Ising: T = tanh(H + theta) per node-sample: fp64 master, fp32 copy for the Newton
-// iterations, fp16 copy for the bandwidth-bound screen with sum|T16| per node for its
-// rigorous error bound, and sum T^2 per node.
-__global__ void snapshot_ising_kernel(const double* __restrict__ H, const double* __restrict__ theta,
-                                      int M, int Mp, double* __restrict__ T64, float* __restrict__ T32,
-                                      __half* __restrict__ T16, float* __restrict__ Tabs,
-                                      double* __restrict__ Tsq) {
+// iterations, sum T^2 per node, and the int8 copy for the screen: T8 = round(T / d)
+// with the per-node step d = max|T| / 127 (rounded up), its 8 two's-complement bit
+// planes per 32-sample word (the screen's register-side operand), and per node
+// {d, E = sum |T - d T8| (rounded up: the screen's rigorous error), sum T8}.
+__global__ void __launch_bounds__(256) snapshot_ising_kernel(const double* __restrict__ H,
+                                                             const double* __restrict__ theta, int M, int Mp,
+                                                             double* __restrict__ T64, float* __restrict__ T32,
+                                                             int8_t* __restrict__ T8, uint32_t* __restrict__ P8,
+                                                             float4* __restrict__ Q, double* __restrict__ Tsq) {
     const int r = blockIdx.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const double th = theta[r];
-    double a = 0.0, q = 0.0;
+    __shared__ double sh[8], sq[8];
+    __shared__ int si[8];
+    __shared__ float s_d;
+    double mx = 0.0, q = 0.0;
     for (int m = threadIdx.x; m < Mp; m += blockDim.x) {
         double t = 0.0;
         if (m < M) t = tanh(H[(size_t)r * Mp + m] + th);
         T64[(size_t)r * Mp + m] = t;
         T32[(size_t)r * Mp + m] = (float)t;
-        const __half h = __double2half(t);
-        T16[(size_t)r * Mp + m] = h;
-        a += fabs((double)__half2float(h));
+        mx = fmax(mx, fabs(t));
         q += t * t;
     }
-    __shared__ double sh[32], sq[32];
-    a = warp_sum(a);
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     q = warp_sum(q);
-    if ((threadIdx.x & 31) == 0) {
-        sh[threadIdx.x >> 5] = a;
-        sq[threadIdx.x >> 5] = q;
+    if (lane == 0) {
+        sh[wid] = mx;
+        sq[wid] = q;
     }
     __syncthreads();
-    if (threadIdx.x < 32) {
-        double v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
-        double w = threadIdx.x < (blockDim.x >> 5) ? sq[threadIdx.x] : 0.0;
-        v = warp_sum(v);
-        w = warp_sum(w);
-        if (threadIdx.x == 0) {
-            Tabs[r] = __double2float_ru(v * (1.0 + 1e-12));
-            Tsq[r] = w;
+    if (threadIdx.x == 0) {
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < 8; ++w) {
+            a = fmax(a, sh[w]);
+            b += sq[w];
         }
+        Tsq[r] = b;
+        s_d = a > 0.0 ? __double2float_ru(a / 127.0) : 1.0f;
+    }
+    __syncthreads();
+    const double d = (double)s_d;
+    const int Mw = Mp >> 5;
+    double e = 0.0;
+    int sum = 0;
+    for (int w = wid; w < Mw; w += 8) {
+        const int m = 32 * w + lane;
+        const double t = T64[(size_t)r * Mp + m];  // 0 on padding
+        int v = (int)rint(t / d);
+        v = max(-127, min(127, v));
+        e += fabs(t - d * (double)v);
+        sum += v;
+        T8[(size_t)r * Mp + m] = (int8_t)v;
+        uint32_t mine = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t pl = __ballot_sync(0xffffffffu, ((uint32_t)v >> k) & 1u);
+            if (lane == k) mine = pl;
+        }
+        if (lane < 8) P8[((size_t)r * Mw + w) * 8 + lane] = mine;
+    }
+    e = warp_sum(e);
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    __syncthreads();
+    if (lane == 0) {
+        sh[wid] = e;
+        si[wid] = sum;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+        int b = 0;
+        for (int w = 0; w < 8; ++w) {
+            a += sh[w];
+            b += si[w];
+        }
+        Q[r] = make_float4(s_d, __double2float_ru(a * (1.0 + 1e-12)), __int_as_float(b), 0.f);
     }
 }
 
@@ -377,15 +418,17 @@ void ensure_snapshot(Context& c) {
     const size_t nm = (size_t)c.n * c.Mp;
     if (c.kind == ISING) {
         c.T64.ensure(nm * 8);
-        c.T16.ensure(nm * 2);
         c.T32.ensure(nm * 4);
-        c.Tabs.ensure((size_t)c.n * 4);
+        c.T8.ensure(nm);
+        c.P8.ensure(nm);
+        c.Q8.ensure((size_t)c.n * 16);
         c.Tsq.ensure((size_t)c.n * 8);
         snapshot_ising_kernel<<<c.n, 256, 0, c.stream>>>(c.dH(), c.dtheta(), c.M, c.Mp,
                                                          static_cast<double*>(c.T64.p),
                                                          static_cast<float*>(c.T32.p),
-                                                         static_cast<__half*>(c.T16.p),
-                                                         static_cast<float*>(c.Tabs.p),
+                                                         static_cast<int8_t*>(c.T8.p),
+                                                         static_cast<uint32_t*>(c.P8.p),
+                                                         static_cast<float4*>(c.Q8.p),
                                                          static_cast<double*>(c.Tsq.p));
     } else {
         c.U.ensure(nm * 8);
