@@ -115,8 +115,11 @@ __device__ __forceinline__ int warp_sum(int v) {
 constexpr uint64_t kEmptyKey = 0xffffffffffffffffULL;
 constexpr uint64_t kTombKey = 0xfffffffffffffffeULL;
 
-__host__ __device__ __forceinline__ uint32_t hash_slot(uint64_t key, uint64_t mask) {
-    return (uint32_t)(mix64(key) & mask);
+// home slot of a pair key in the open-addressing tables (couplings W, distance cache):
+// Fibonacci hashing, bits 32..63 of key * 2^64/phi (one 64-bit multiply; both node
+// ids reach those bits), masked to a power-of-two capacity <= 2^32
+__host__ __device__ __forceinline__ uint64_t slot_of(uint64_t key, uint64_t mask) {
+    return ((key * 0x9e3779b97f4a7c15ULL) >> 32) & mask;
 }
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -103,7 +103,7 @@ struct HashView {
 };
 
 __device__ __forceinline__ double hash_get(const HashView h, uint64_t key, double dflt) {
-    uint64_t s = mix64(key) & h.mask;
+    uint64_t s = slot_of(key, h.mask);
     for (;;) {
         const uint64_t k = h.keys[s];
         if (k == key) return h.vals[s];

@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(NT) row_sort_kernel(int32_t* __restrict__ gid,
 
 // ---------------------------------------------------------------- cache claim
 __device__ __forceinline__ uint64_t cache_claim_k(HashView h, uint64_t key, bool& mine) {
-    uint64_t s = mix64(key) & h.mask;
+    uint64_t s = slot_of(key, h.mask);
     for (;;) {
         const uint64_t k = __ldcg(&h.keys[s]);
         if (k == key) {

@@ -131,12 +131,9 @@ __global__ void __launch_bounds__(256, HW == 1 ? 4 : 3) ising_screen_kernel(Isin
                     diff += __popc(cs.b[q] ^ b);
                 }
                 // one packed reduction for (a1, diff): |a1| <= 127 M < 2^19, diff <= M < 2^12
-                int v = (a1 << 12) + diff;
-#pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                    v += __shfl_xor_sync(0xffffffffu, v, o);
-                    a2 += __shfl_xor_sync(0xffffffffu, a2, o);
-                }
+                // (REDUX: one instruction per warp sum)
+                const int v = __reduce_add_sync(0xffffffffu, (a1 << 12) + diff);
+                a2 = __reduce_add_sync(0xffffffffu, a2);
                 const int dsum = v & 4095;
                 const int asum = (v - dsum) >> 12;
                 const float A = qs.x * (float)(2 * asum - __float_as_int(qs.z));
@@ -418,7 +415,7 @@ void score_all_pairs(Context& c, int mode, const int32_t* nodes, uint64_t n, dou
 
 // ---------------------------------------------------------------- cached batch lookups
 __device__ __forceinline__ uint64_t cache_claim(HashView h, uint64_t key, bool& mine) {
-    uint64_t s = mix64(key) & h.mask;
+    uint64_t s = slot_of(key, h.mask);
     for (;;) {
         const uint64_t k = __ldcg(&h.keys[s]);
         if (k == key) {

@@ -241,7 +241,7 @@ __global__ void w_rehash_kernel(const uint64_t* __restrict__ ok, const double* _
     if (s >= ocap) return;
     const uint64_t k = ok[s];
     if (k >= kTombKey) return;
-    uint64_t t = mix64(k) & nw.mask;
+    uint64_t t = slot_of(k, nw.mask);
     for (;;) {
         const unsigned long long prev =
             atomicCAS((unsigned long long*)&nw.keys[t], (unsigned long long)kEmptyKey, (unsigned long long)k);
@@ -552,7 +552,7 @@ __global__ void cache_rehash_kernel(const uint64_t* __restrict__ ok, const doubl
     if (s >= ocap) return;
     const uint64_t k = ok[s];
     if (k == kEmptyKey) return;
-    uint64_t t = mix64(k) & nw.mask;
+    uint64_t t = slot_of(k, nw.mask);
     for (;;) {
         const unsigned long long prev =
             atomicCAS((unsigned long long*)&nw.keys[t], (unsigned long long)kEmptyKey, (unsigned long long)k);

@@ -44,7 +44,7 @@ __global__ void dep_link_kernel(const uint64_t* __restrict__ keys, const uint32_
 
 // coherent (L2) hash lookup for the update kernel
 __device__ __forceinline__ double hash_get_cg(const HashView h, uint64_t key) {
-    uint64_t s = mix64(key) & h.mask;
+    uint64_t s = slot_of(key, h.mask);
     for (;;) {
         const uint64_t k = __ldcg(&h.keys[s]);
         if (k == key) return __ldcg(&h.vals[s]);
@@ -55,7 +55,7 @@ __device__ __forceinline__ double hash_get_cg(const HashView h, uint64_t key) {
 // set W[key] = w: update in place, tombstone on zero, insert into the first empty
 // slot otherwise (tombstones are never reused while the table is shared)
 __device__ __forceinline__ void hash_set(HashView h, uint64_t key, double w, unsigned long long* cnt) {
-    uint64_t s = mix64(key) & h.mask;
+    uint64_t s = slot_of(key, h.mask);
     for (;;) {
         const uint64_t k = __ldcg(&h.keys[s]);
         if (k == key) {
