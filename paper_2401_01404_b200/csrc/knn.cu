@@ -12,8 +12,10 @@
 //     list is exactly the (dist,id)-top-kw of (snapshot list U candidates) — the
 //     visit-order independence the reference tests (test_knn.cpp:154-194) — so a
 //     sweep is: gather+dedup 2-hop candidates (one CTA per node, smem hash set or
-//     bitmap), claim them in the distance cache (one score per pair per generation,
-//     inc/model.hpp:54-70), score the claimed worklist, then merge top-kw per node;
+//     bitmap; paths whose two hops were both already in U last sweep are skipped, see
+//     u_new_kernel), claim them in the distance cache (one score per pair per
+//     generation, inc/model.hpp:54-70), score the claimed worklist, then merge top-kw
+//     per node;
 //   * churn = entries that entered from the candidate set (:273-290);
 //   * trim to k (:292-305); exhaustive fallbacks (:156-164).
 #include <cub/cub.cuh>
@@ -353,6 +355,28 @@ __global__ void u_rev_kernel(const uint32_t* __restrict__ tgt_sorted, const int3
     alen[lt] = len;
 }
 
+// Incremental local join (exact under the set semantics): newf[i][a] = 1 when entry a
+// of U(i) was not in U(i) in the previous sweep.  A 2-hop path i -> u -> v with both
+// hops old was already a candidate of i in the previous sweep of this generation,
+// where it lost to i's row; rows only improve and distances are fixed within a
+// generation, so it cannot enter now and the gather skips it.  One warp per node.
+__global__ void u_new_kernel(const int32_t* __restrict__ adj, const int32_t* __restrict__ alen,
+                             const int32_t* __restrict__ adjp, const int32_t* __restrict__ alenp, uint64_t n,
+                             int cap, int first, uint8_t* __restrict__ newf) {
+    const uint64_t li = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (li >= n) return;
+    const int len = alen[li], lenp = first ? 0 : alenp[li];
+    const int32_t* row = adj + li * cap;
+    const int32_t* prow = adjp + li * cap;
+    for (int a = lane; a < len; a += 32) {
+        const int32_t v = row[a];
+        bool seen = false;
+        for (int t = 0; t < lenp && !seen; ++t) seen = prow[t] == v;
+        newf[li * cap + a] = seen ? 0 : 1;
+    }
+}
+
 // ---------------------------------------------------------------- gather + claim
 // One CTA per node.  Dedup set in shared memory: open-addressing int hash (tsize
 // slots) or a bitmap over the level's n local ids (bitmap == true).
@@ -364,7 +388,8 @@ __global__ void __launch_bounds__(NT) knn_gather_kernel(const int32_t* __restric
                                                         int tsize, HashView h, ClaimSink sink,
                                                         uint64_t capn, int32_t* __restrict__ cand_id,
                                                         uint32_t* __restrict__ cand_slot,
-                                                        int32_t* __restrict__ cand_cnt, uint64_t lo) {
+                                                        int32_t* __restrict__ cand_cnt, uint64_t lo, int lw,
+                                                        const uint8_t* __restrict__ newf) {
     extern __shared__ int32_t tab[];
     __shared__ int ncand;
     const uint64_t li = lo + blockIdx.x;
@@ -394,13 +419,20 @@ __global__ void __launch_bounds__(NT) knn_gather_kernel(const int32_t* __restric
     const int32_t* row_i = adj + li * cap;
     const int len_i = alen[li];
     int32_t* my_ids = cand_id + li * capn;
-    for (int a = 0; a < len_i; ++a) {
-        const int32_t lj = row_i[a];
-        const int len_j = alen[lj];
-        const int32_t* row_j = adj + (uint64_t)lj * cap;
-        for (int b0 = 0; b0 < len_j; b0 += NT) {
-            const int b = b0 + tid;
-            if (b < len_j) {
+    // 2-hop rows side by side: a group of 2^lw >= cap threads per row (or the whole CTA
+    // stepping through a row when cap > NT)
+    const int gw = 1 << lw;
+    const int rows = gw >= NT ? 1 : NT / gw;
+    const int r = gw >= NT ? 0 : tid >> lw, b0 = gw >= NT ? tid : tid & (gw - 1);
+    for (int a0 = 0; a0 < len_i; a0 += rows) {
+        const int a = a0 + r;
+        if (a < len_i) {
+            const int32_t lj = row_i[a];
+            const int len_j = alen[lj];
+            const int32_t* row_j = adj + (uint64_t)lj * cap;
+            const bool old_a = !newf[li * cap + a];
+            for (int b = b0; b < len_j; b += (gw >= NT ? NT : gw)) {
+                if (old_a && !newf[(uint64_t)lj * cap + b]) continue;  // old-old: lost last sweep
                 const int32_t v = row_j[b];
                 if (insert(v)) {
                     const int at = atomicAdd(&ncand, 1);
@@ -426,8 +458,11 @@ __global__ void __launch_bounds__(NT) knn_gather_kernel(const int32_t* __restric
 // ---------------------------------------------------------------- merge top-kw
 // One CTA per node: keep the (dist,id)-smallest kw of (current row U candidates).
 // Candidates are consumed in blocks of (buf_cap - kw); those beating the current
-// worst are appended after the row and the buffer is bitonic-sorted, so nothing
-// can overflow.  Counts entries that came from the candidate set (churn).
+// worst are appended after the row, and the new row is selected by rank: entries are
+// distinct in (dist, global id), so an entry's rank is the number of entries ahead of
+// it and the ranks < kw are the new row, in order (one barrier; blocks of more than 96
+// entries are bitonic-sorted instead).
+// Counts entries that came from the candidate set (churn).
 template <int NT>
 __global__ void __launch_bounds__(NT) knn_merge_kernel(const int32_t* __restrict__ nodes, uint64_t n,
                                                        int32_t* __restrict__ gid, double* __restrict__ gd, int kw,
@@ -439,9 +474,13 @@ __global__ void __launch_bounds__(NT) knn_merge_kernel(const int32_t* __restrict
                                                        unsigned long long* __restrict__ churn, uint64_t lo) {
     extern __shared__ unsigned char smem_raw[];
     double* bd = reinterpret_cast<double*>(smem_raw);
-    int32_t* bi = reinterpret_cast<int32_t*>(bd + buf_cap);  // local id
+    double* od = bd + buf_cap;                               // selected row (kw)
+    int32_t* bi = reinterpret_cast<int32_t*>(od + kw);       // local id
     int32_t* bg = bi + buf_cap;                               // global id (tie order)
     int32_t* bo = bg + buf_cap;                               // origin: 1 = candidate
+    int32_t* oi = bo + buf_cap;
+    int32_t* og = oi + kw;
+    int32_t* oo = og + kw;
     __shared__ int nb;
     const uint64_t li = lo + blockIdx.x;
     const int tid = threadIdx.x;
@@ -481,33 +520,56 @@ __global__ void __launch_bounds__(NT) knn_merge_kernel(const int32_t* __restrict
         const int m = nb;
         if (m == kw) continue;  // nothing beats the worst
         changed_any = true;
-        int P = 1;
-        while (P < m) P <<= 1;
-        for (int t = m + tid; t < P; t += NT) {
-            bd[t] = INFINITY;
-            bg[t] = 0x7fffffff;
-            bi[t] = -1;
-            bo[t] = 0;
-        }
-        __syncthreads();
-        for (int k2 = 2; k2 <= P; k2 <<= 1) {
-            for (int j = k2 >> 1; j > 0; j >>= 1) {
-                for (int t = tid; t < P; t += NT) {
-                    const int ixj = t ^ j;
-                    if (ixj > t) {
-                        const bool up = (t & k2) == 0;
-                        const bool gt = entry_less(bd[ixj], bg[ixj], bd[t], bg[t]);
-                        if (gt == up) {
-                            const double td = bd[t]; bd[t] = bd[ixj]; bd[ixj] = td;
-                            const int ti = bi[t]; bi[t] = bi[ixj]; bi[ixj] = ti;
-                            const int tg = bg[t]; bg[t] = bg[ixj]; bg[ixj] = tg;
-                            const int to = bo[t]; bo[t] = bo[ixj]; bo[ixj] = to;
+        if (m > 96) {  // large blocks (first sweeps, wide rows): bitonic sort of the buffer
+            int P = 1;
+            while (P < m) P <<= 1;
+            for (int t = m + tid; t < P; t += NT) {
+                bd[t] = INFINITY;
+                bg[t] = 0x7fffffff;
+                bi[t] = -1;
+                bo[t] = 0;
+            }
+            __syncthreads();
+            for (int k2 = 2; k2 <= P; k2 <<= 1) {
+                for (int j = k2 >> 1; j > 0; j >>= 1) {
+                    for (int t = tid; t < P; t += NT) {
+                        const int ixj = t ^ j;
+                        if (ixj > t) {
+                            const bool up = (t & k2) == 0;
+                            const bool gt = entry_less(bd[ixj], bg[ixj], bd[t], bg[t]);
+                            if (gt == up) {
+                                const double td = bd[t]; bd[t] = bd[ixj]; bd[ixj] = td;
+                                const int ti = bi[t]; bi[t] = bi[ixj]; bi[ixj] = ti;
+                                const int tg = bg[t]; bg[t] = bg[ixj]; bg[ixj] = tg;
+                                const int to = bo[t]; bo[t] = bo[ixj]; bo[ixj] = to;
+                            }
                         }
                     }
+                    __syncthreads();
                 }
-                __syncthreads();
+            }
+            continue;
+        }
+        for (int t = tid; t < m; t += NT) {
+            const double d = bd[t];
+            const int g = bg[t];
+            int r = 0;
+            for (int j = 0; j < m; ++j) r += entry_less(bd[j], bg[j], d, g) ? 1 : 0;
+            if (r < kw) {
+                od[r] = d;
+                oi[r] = bi[t];
+                og[r] = g;
+                oo[r] = bo[t];
             }
         }
+        __syncthreads();
+        for (int t = tid; t < kw; t += NT) {
+            bd[t] = od[t];
+            bi[t] = oi[t];
+            bg[t] = og[t];
+            bo[t] = oo[t];
+        }
+        __syncthreads();
     }
     if (!changed_any) return;
     int ch = 0;
@@ -900,9 +962,13 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
 
     // ---- sweeps
     const uint64_t capn = std::min<uint64_t>((uint64_t)cap * cap, n - 1);
-    DevBuf adjb, alenb, cidb, cslb, ccntb, churnb, wsb, wpb, wslb;
+    DevBuf adjb, alenb, adjpb, alenpb, newfb, cidb, cslb, ccntb, churnb, wsb, wpb, wslb;
     int32_t* adj = adjb.as<int32_t>(n * cap);
     int32_t* alen = alenb.as<int32_t>(n);
+    int32_t* adjp = adjpb.as<int32_t>(n * cap);  // U of the previous sweep
+    int32_t* alenp = alenpb.as<int32_t>(n);
+    uint8_t* newf = newfb.as<uint8_t>(n * cap);
+    const bool incremental = !getenv("NRG_KNN_FULL_JOIN");
     int32_t* cand_id = cidb.as<int32_t>(n * capn);
     uint32_t* cand_slot = cslb.as<uint32_t>(n * capn);
     int32_t* cand_cnt = ccntb.as<int32_t>(n);
@@ -940,7 +1006,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         return b;
     }();
     if ((size_t)buf_cap * 20 > 200 * 1024) fail(100, "find_knn: kw too large for the merge buffer");
-    const size_t merge_smem = (size_t)buf_cap * (8 + 4 + 4 + 4);
+    const size_t merge_smem = (size_t)(buf_cap + kw) * (8 + 4 + 4 + 4);
     if (merge_smem > 48 * 1024)
         NRG_CUDA(cudaFuncSetAttribute(knn_merge_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)merge_smem));
@@ -978,6 +1044,9 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                                                                            alen, seg);
             NRG_LAUNCH_CHECK();
         }
+        u_new_kernel<<<(unsigned)ceil_div(n * 32, 256), 256, 0, c.stream>>>(adj, alen, adjp, alenp, n, cap,
+                                                                         (sweep == 0 || !incremental) ? 1 : 0, newf);
+        NRG_LAUNCH_CHECK();
         c.toc(P_KNN);
         // gather + claim (own nodes; remote keys routed to their owner ranks)
         if (cached) cache_reserve(c, wmax);
@@ -987,14 +1056,16 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         const HashView hv = cached ? c.Cview() : HashView{nullptr, nullptr, 0};
         const ClaimSink sk = sink_for(ws, wp, wsl, own * capn + 1);
         if (own) {
+            int lw = 0;
+            while ((1 << lw) < cap) ++lw;
             if (big)
                 knn_gather_kernel<256><<<(unsigned)own, 256, tab_bytes, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv, sk, capn, cand_id, cand_slot,
-                    cand_cnt, lo);
+                    cand_cnt, lo, lw, newf);
             else
                 knn_gather_kernel<32><<<(unsigned)own, 32, tab_bytes, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv, sk, capn, cand_id, cand_slot,
-                    cand_cnt, lo);
+                    cand_cnt, lo, lw, newf);
             NRG_LAUNCH_CHECK();
         }
         unsigned long long nw = 0;
@@ -1031,6 +1102,8 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             changed = ch;
         }
         c.toc(P_KNN);
+        std::swap(adj, adjp);  // this sweep's U is the next sweep's "previous"
+        std::swap(alen, alenp);
         ++out.sweeps;
         const double ratio = (double)changed / ((double)kw * (double)n);
         out.churn.push_back(ratio);

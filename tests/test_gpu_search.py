@@ -239,3 +239,29 @@ def test_model_knn_recall_at_least_reference(gpu):
     assert ra >= rb - 0.01, (ra, rb)
     rev = dev.find_knn(gpu.NRG_EXACT, 8, nodes, seed=7, reverse=True)[0]
     assert knn_recall(rev, ex) >= ra
+
+
+def test_incremental_join_equals_full_join(gpu, monkeypatch):
+    """Skipping 2-hop paths whose hops were both in U last sweep (incremental local
+    join) gives the identical graph, churn trace and FindBest list as the full join."""
+    X, lam = _ising(800, 300, 5)
+    n = X.shape[0]
+    nodes = np.arange(n, dtype=np.int32)
+
+    def run(full):
+        if full:
+            monkeypatch.setenv("NRG_KNN_FULL_JOIN", "1")
+        else:
+            monkeypatch.delenv("NRG_KNN_FULL_JOIN", raising=False)
+        m = gpu.Model.from_samples(X.astype(np.int8), gpu.NRG_ISING, lam)
+        m.begin_generation()
+        ids, d, sw, churn = m.find_knn(gpu.NRG_EXACT, 8, nodes, seed=3)
+        m.begin_generation()
+        fb, _, _ = m.find_best(gpu.NRG_EXACT, 2 * n, nodes, seed=4)
+        return ids, d, sw, churn, fb
+    a, b = run(False), run(True)
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+    assert a[2] == b[2]
+    np.testing.assert_array_equal(a[3], b[3])
+    np.testing.assert_array_equal(a[4], b[4])
