@@ -253,6 +253,7 @@ void get_state(Context& c, double* theta, uint64_t cap, int32_t* ei, int32_t* ej
                uint64_t* n_edges);
 void get_sums(Context& c, double* out);
 void ensure_snapshot(Context& c);
+void snapshot_rows(Context& c, const int32_t* rows, uint64_t nr);  // refresh only these rows
 double log_posterior(Context& c);
 double generation_base(Context& c);
 void begin_generation(Context& c);

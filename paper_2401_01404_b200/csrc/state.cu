@@ -316,8 +316,9 @@ __global__ void __launch_bounds__(256) snapshot_ising_kernel(const double* __res
                                                              const double* __restrict__ theta, int M, int Mp,
                                                              double* __restrict__ T64, float* __restrict__ T32,
                                                              int8_t* __restrict__ T8, uint32_t* __restrict__ P8,
-                                                             float4* __restrict__ Q, double* __restrict__ Tsq) {
-    const int r = blockIdx.x;
+                                                             float4* __restrict__ Q, double* __restrict__ Tsq,
+                                                             const int32_t* __restrict__ rows) {
+    const int r = rows ? rows[blockIdx.x] : (int)blockIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const double th = theta[r];
     __shared__ double sh[8], sq[8];
@@ -391,8 +392,9 @@ __global__ void __launch_bounds__(256) snapshot_ising_kernel(const double* __res
 // Gaussian: U = X + theta^2 H (the current residual), xx = sum x^2
 __global__ void snapshot_gauss_kernel(const double* __restrict__ X, const double* __restrict__ H,
                                       const double* __restrict__ theta, int M, int Mp,
-                                      double* __restrict__ U, double* __restrict__ xx) {
-    const int r = blockIdx.x;
+                                      double* __restrict__ U, double* __restrict__ xx,
+                                      const int32_t* __restrict__ rows) {
+    const int r = rows ? rows[blockIdx.x] : (int)blockIdx.x;
     const double t2 = theta[r] * theta[r];
     double a = 0.0;
     for (int m = threadIdx.x; m < Mp; m += blockDim.x) {
@@ -429,14 +431,36 @@ void ensure_snapshot(Context& c) {
                                                          static_cast<int8_t*>(c.T8.p),
                                                          static_cast<uint32_t*>(c.P8.p),
                                                          static_cast<float4*>(c.Q8.p),
-                                                         static_cast<double*>(c.Tsq.p));
+                                                         static_cast<double*>(c.Tsq.p), nullptr);
     } else {
         c.U.ensure(nm * 8);
         c.xx.ensure((size_t)c.n * 8);
         snapshot_gauss_kernel<<<c.n, 256, 0, c.stream>>>(c.dXd(), c.dH(), c.dtheta(), c.M, c.Mp,
                                                          static_cast<double*>(c.U.p),
-                                                         static_cast<double*>(c.xx.p));
+                                                         static_cast<double*>(c.xx.p), nullptr);
     }
+    NRG_LAUNCH_CHECK();
+    c.toc(P_SNAP);
+    c.snap_version = c.state_version;
+}
+
+// Refresh the snapshot rows of `rows` (device list, nr entries) after updates that
+// changed only those nodes' sums; the rest of the snapshot must be current otherwise.
+void snapshot_rows(Context& c, const int32_t* rows, uint64_t nr) {
+    if (nr == 0) {
+        c.snap_version = c.state_version;
+        return;
+    }
+    c.tic();
+    if (c.kind == ISING)
+        snapshot_ising_kernel<<<(unsigned)nr, 256, 0, c.stream>>>(
+            c.dH(), c.dtheta(), c.M, c.Mp, static_cast<double*>(c.T64.p), static_cast<float*>(c.T32.p),
+            static_cast<int8_t*>(c.T8.p), static_cast<uint32_t*>(c.P8.p), static_cast<float4*>(c.Q8.p),
+            static_cast<double*>(c.Tsq.p), rows);
+    else
+        snapshot_gauss_kernel<<<(unsigned)nr, 256, 0, c.stream>>>(c.dXd(), c.dH(), c.dtheta(), c.M, c.Mp,
+                                                                   static_cast<double*>(c.U.p),
+                                                                   static_cast<double*>(c.xx.p), rows);
     NRG_LAUNCH_CHECK();
     c.toc(P_SNAP);
     c.snap_version = c.state_version;

@@ -405,12 +405,16 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
         std::vector<uint8_t> mod(c.n, 0);
         std::vector<int32_t> touched;
         std::vector<uint32_t> apply;
+        DevBuf rowsb;
+        int32_t* rows_dev = nullptr;
+        uint64_t n_rows = 0;
         for (int round = 0; start < n; ++round) {
             if (round == kTailRounds) {
                 ordered_run(c, ci + start, cj + start, n - start, nullptr, absdelta + start);
                 break;
             }
             c.state_version++;  // the evaluation snapshot must include every update so far
+            if (round > 0) snapshot_rows(c, rows_dev, n_rows);  // only the last round's endpoints changed
             const uint64_t m = n - start;
             double* w = wb.as<double>(m);
             ScoreOut out;
@@ -464,7 +468,14 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
                 ordered_run(c, pi, pj, na, nullptr, dd);
                 scatter_delta_kernel<<<ceil_div(na, 256), 256, 0, c.stream>>>(dd, di, na, absdelta);
                 NRG_LAUNCH_CHECK();
+                // endpoints of the applied pairs: the rows the next round must re-snapshot
+                rows_dev = rowsb.as<int32_t>(2 * (size_t)na);
+                NRG_CUDA(cudaMemcpyAsync(rows_dev, pi, na * 4, cudaMemcpyDeviceToDevice, c.stream));
+                NRG_CUDA(cudaMemcpyAsync(rows_dev + na, pj, na * 4, cudaMemcpyDeviceToDevice, c.stream));
+                n_rows = 2 * (uint64_t)na;
                 c.sync();  // `apply` is reused next round
+            } else {
+                n_rows = 0;
             }
             start = p;
         }
