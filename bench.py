@@ -333,6 +333,16 @@ def run_ours(args, rank, world, local, dist):
     k1_pairs_avg = kst["k1_pairs"] / max(1.0, kst["k1_launches"])
     achieved = (k1_pairs_avg * bytes_per_pair) / (k1_ms_avg / 1e3) / 1e9 if k1_ms_avg > 0 else 0.0
 
+    # DRAM traffic per K1 launch: the per-pair bytes of the committed ncu --set full
+    # capture (dram__bytes_read.sum + dram__bytes_write.sum of one launch / its pairs)
+    # times this run's pairs per launch
+    traffic = None
+    tf = ROOT / "profiles" / "r01_k1_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text())["dram_bytes_per_pair"] * k1_pairs_avg
+        except Exception:
+            traffic = None
     line = {
         "metric": "scored candidate pairs/sec and wall-time per GCD sweep (N=1e5, M=1e3)",
         "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -356,7 +366,8 @@ def run_ours(args, rank, world, local, dist):
                   "edges_at_start": int(len(ei_w)), "objective": [float(r["objective"]) for r in recs],
                   "tail_rounds": kst.get("tail_rounds")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "kernel": "ising_screen_kernel (K1)",
+                     "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per launch",
+                     "traffic_source": "profiles/r01_k1_traffic.json", "kernel": "ising_screen_kernel (K1)",
                      "bytes_per_unit": bytes_per_pair, "units_per_launch": k1_pairs_avg,
                      "ms_per_launch": k1_ms_avg, "peak_kind": peak_kind},
         "e2e": {"value": e2e_pairs / (e2e_ms / 1e3), "unit": "pairs/s", "h2d_bytes_per_step": h2d // args.steps,

@@ -15,6 +15,8 @@
 // The stationary node's operands (first entry of a worklist run) stay in registers
 // across consecutive entries, so each pair streams only its partner.
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "pairscore.cuh"
@@ -348,6 +350,9 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
             c.k1_ms += ms;
             c.k1_launches += 1;
             c.k1_pairs += (double)n;
+            if (getenv("NRG_DEBUG_K1"))
+                fprintf(stderr, "K1 launch %d: %llu pairs, %llu survivors, %.3f ms\n", (int)c.k1_launches - 1,
+                        (unsigned long long)n, (unsigned long long)ns, ms);
         }
         c.last_survivors = ns;
         if (ns) {
