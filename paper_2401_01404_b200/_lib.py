@@ -321,9 +321,10 @@ class Model:
         return v.value
 
     def kernel_stats(self):
-        out = np.zeros(8)
-        check(self.L.nrg_kernel_stats(self.h, out, 8))
-        keys = ["k1_ms", "k1_launches", "k1_pairs", "k2_ms", "k2_launches", "k2_pairs", "launches", "tail_rounds"]
+        out = np.zeros(10)
+        check(self.L.nrg_kernel_stats(self.h, out, 10))
+        keys = ["k1_ms", "k1_launches", "k1_pairs", "k2_ms", "k2_launches", "k2_pairs", "launches", "tail_rounds",
+                "tc_launches", "tc_pairs"]
         return dict(zip(keys, out.tolist()))
 
     def sample_scored_pairs(self, cap, seed=0):

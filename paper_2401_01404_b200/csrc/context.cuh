@@ -194,6 +194,7 @@ struct Context {
     // per-kernel stats: K1 screen ms / launches / pairs, K2 refine ms / launches / survivors
     double k1_ms = 0, k1_launches = 0, k1_pairs = 0, k2_ms = 0, k2_launches = 0, k2_pairs = 0;
     double tail_rounds = 0;  // apply_updates: parallel rounds spent on tie tails
+    double tc_launches = 0, tc_pairs = 0;  // tensor-core exhaustive screen
     uint64_t launches0 = 0;
     cudaEvent_t kev0 = nullptr, kev1 = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -268,6 +269,10 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
                    const ScoreOut& out);
 // all pairs of `nodes` (device, n entries): dist[e] for e in the row-major upper triangle
 void score_all_pairs(Context& c, int mode, const int32_t* nodes, uint64_t n, double* dist);
+// tensor-core all-pairs screen (exhaustive_tc.cu); false = not applicable, nothing written
+bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* dist);
+void refine_survivors(Context& c, const int32_t* s, const int32_t* p, const uint64_t* surv, const float* surv_g,
+                      const uint8_t* surv_flag, uint64_t ns, double base, const ScoreOut& out);
 // cached distance lookups for a batch (probe/claim/score/gather), device arrays
 void distance_batch(Context& c, int mode, const int32_t* i, const int32_t* j, uint64_t n,
                     double* dist);

@@ -1,0 +1,423 @@
+// exhaustive_tc.cu — the O(n^2) all-pairs screen (SURVEY §8a row A5:
+// all_pairs_scan inc/find_best.hpp:72-86, knn_exhaustive inc/knn.hpp:117-135) on the
+// 5th-generation tensor cores.
+//
+// Over all pairs the Ising screen is a dense contraction:
+//   g0(i,j) = 2<x_i,x_j> - <x_j,T_i> - <x_i,T_j>
+//           ~ 2 (X X^T)_ij - d_j (X T8^T)_ij - d_i (T8 X^T)_ij
+// with X the +-1 spins as int8 and T8 the snapshot's per-node int8 field (step d_i,
+// rigorous error sum E_i).  Three int8 GEMM accumulators per 128x128 tile live in TMEM
+// (3 x 128 of 512 columns); the integer products are exact, so |g0 - g| <= E_i + E_j
+// exactly as in K1 and kink decisions stay exact.  Per tile (upper triangle of tiles
+// only): TMA loads 128-byte-swizzled K-major tiles of X and T8 for both row blocks into a
+// 3-stage smem ring, one elected thread issues tcgen05.mma.kind::i8 (M=128, N=128, K=32)
+// and commits to mbarriers, and all four warps drain TMEM with tcgen05.ld: pruned pairs
+// get dist = -base exactly, the rest are compacted for K2 (ising_refine_kernel), which
+// also re-decides existing edges.  The result is bitwise the CUDA-core path's.
+#include <cuda.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "context.cuh"
+
+namespace nrg {
+
+namespace tc {
+
+constexpr int kBM = 128;      // tile rows (TMEM lanes)
+constexpr int kBN = 128;      // tile columns (per accumulator)
+constexpr int kBK = 128;      // K bytes per stage = one 128B swizzle atom
+constexpr int kStages = 3;
+constexpr int kTileBytes = kBM * kBK;  // 16 KB
+constexpr int kStageBytes = 4 * kTileBytes;
+constexpr int kTmemCols = 512;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+// K-major operand tile of 128 rows x 128 bytes, SWIZZLE_128B: 8-row atoms 1024 B apart
+__device__ __forceinline__ uint64_t smem_desc(const void* tile, int k_bytes) {
+    const uint64_t addr = smem_u32(tile) + (uint32_t)k_bytes;
+    uint64_t d = 0;
+    d |= (addr >> 4) & 0x3fffull;          // start address
+    d |= (uint64_t)1 << 16;                // leading byte offset (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;      // stride byte offset: next 8-row group
+    d |= (uint64_t)1 << 46;                // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;                // SWIZZLE_128B
+    return d;
+}
+// instruction descriptor: s8 x s8 -> s32, K-major A and B, M = 128, N = 128
+__host__ __device__ constexpr uint32_t idesc_i8() {
+    return (2u << 4)             // c_format: S32
+           | (1u << 7)           // a_format: signed 8 bit
+           | (1u << 10)          // b_format: signed 8 bit
+           | ((kBN >> 3) << 17)  // n_dim
+           | ((kBM >> 4) << 24); // m_dim
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem_c, uint64_t da, uint64_t db, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_c),
+        "l"(da), "l"(db), "r"(idesc_i8()), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+
+struct TcOut {
+    double* dist;  // upper-triangle distances, row-major over the node list
+    int32_t* si;   // survivors: list positions (i < j), float g0, flag (0 certain, 1 band)
+    int32_t* sj;
+    float* sg;
+    uint8_t* sf;
+    unsigned long long* ns;
+    uint64_t cap;
+};
+
+// one 128x128 tile (row block I <= column block J) per CTA, 4 warps
+__global__ void __launch_bounds__(128, 1)
+    tc_screen_kernel(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mt,
+                     const float4* __restrict__ q, int n, int M, int Mp, double lambda, double base, TcOut out) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* ring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                                           ~(uintptr_t)1023);
+    __shared__ __align__(8) uint64_t full[kStages], empty[kStages], done;
+    __shared__ uint32_t tmem_base;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // linear tile index -> (I, J), I <= J
+    const int T = (n + kBM - 1) / kBM;
+    int I = 0, rem = (int)blockIdx.x;
+    while (rem >= T - I) {
+        rem -= T - I;
+        ++I;
+    }
+    const int J = I + rem;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_base;
+    const int nkb = Mp / kBK;
+    if (warp == 0 && lane == 0) {
+        // TMA producer
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int s = kb % kStages;
+            const uint32_t ph = (uint32_t)(kb / kStages) & 1u;
+            mbar_wait(&empty[s], ph ^ 1u);
+            unsigned char* st = ring + s * kStageBytes;
+            mbar_expect_tx(&full[s], kStageBytes);
+            tma_load_2d(st + 0 * kTileBytes, &mx, kb * kBK, I * kBM, &full[s]);
+            tma_load_2d(st + 1 * kTileBytes, &mt, kb * kBK, I * kBM, &full[s]);
+            tma_load_2d(st + 2 * kTileBytes, &mx, kb * kBK, J * kBN, &full[s]);
+            tma_load_2d(st + 3 * kTileBytes, &mt, kb * kBK, J * kBN, &full[s]);
+        }
+    } else if (warp == 1 && lane == 0) {
+        // MMA issuer: acc1 = X_I X_J^T, acc2 = X_I T8_J^T, acc3 = T8_I X_J^T
+        for (int kb = 0; kb < nkb; ++kb) {
+            const int s = kb % kStages;
+            const uint32_t ph = (uint32_t)(kb / kStages) & 1u;
+            mbar_wait(&full[s], ph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const unsigned char* st = ring + s * kStageBytes;
+#pragma unroll
+            for (int kk = 0; kk < kBK / 32; ++kk) {
+                const uint32_t acc = (kb | kk) ? 1u : 0u;
+                const uint64_t xi = smem_desc(st + 0 * kTileBytes, 32 * kk);
+                const uint64_t ti = smem_desc(st + 1 * kTileBytes, 32 * kk);
+                const uint64_t xj = smem_desc(st + 2 * kTileBytes, 32 * kk);
+                const uint64_t tj = smem_desc(st + 3 * kTileBytes, 32 * kk);
+                mma_i8(tmem + 0, xi, xj, acc);
+                mma_i8(tmem + kBN, xi, tj, acc);
+                mma_i8(tmem + 2 * kBN, ti, xj, acc);
+            }
+            mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+        }
+        mma_commit(&done);
+    }
+    __syncwarp();
+    mbar_wait(&done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // epilogue: thread = one row of the tile
+    const int r = warp * 32 + lane;
+    const int i = I * kBM + r;
+    const float lam = (float)lambda;
+    const float err0 = 4.f * (float)M * 5.9604645e-08f;
+    const double pruned = -(base + 0.0);
+    const float4 qi = i < n ? __ldg(&q[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const uint64_t row_off = (uint64_t)i * (2 * (uint64_t)n - (uint64_t)i - 1) / 2;
+    for (int c0 = 0; c0 < kBN; c0 += 16) {
+        uint32_t a1[16], a2[16], a3[16];
+        const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;
+        tmem_ld16(tmem + lane_addr + 0 * kBN + c0, a1);
+        tmem_ld16(tmem + lane_addr + 1 * kBN + c0, a2);
+        tmem_ld16(tmem + lane_addr + 2 * kBN + c0, a3);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        uint32_t surv_mask = 0;
+        float gv[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int j = J * kBN + c0 + u;
+            gv[u] = 0.f;
+            if (i < n && j < n && i < j) {
+                const float4 qj = __ldg(&q[j]);
+                const float g = (float)(2 * (int)a1[u]) - (qj.x * (float)(int)a2[u] + qi.x * (float)(int)a3[u]);
+                const float err = (qi.y + qj.y) * 1.0001f + err0;
+                if (fabsf(g) <= lam - err) {
+                    out.dist[row_off + (uint64_t)(j - i - 1)] = pruned;
+                } else {
+                    surv_mask |= 1u << u;
+                    gv[u] = g;
+                }
+            }
+        }
+        // compact this thread's survivors (warp-aggregated reservation)
+        const int cnt = __popc(surv_mask);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int tot = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned long long at = 0;
+        if (lane == 31 && tot) at = atomicAdd(out.ns, (unsigned long long)tot);
+        at = __shfl_sync(0xffffffffu, at, 31) + (unsigned long long)(incl - cnt);
+        for (uint32_t m = surv_mask; m; m &= m - 1) {
+            const int u = __ffs(m) - 1;
+            if (at < out.cap) {
+                const float g = gv[u];
+                out.si[at] = i;
+                out.sj[at] = J * kBN + c0 + u;
+                out.sg[at] = g;
+                const float4 qj = __ldg(&q[J * kBN + c0 + u]);
+                const float err = (qi.y + qj.y) * 1.0001f + err0;
+                out.sf[at] = fabsf(g) < lam + err ? 1 : 0;
+            }
+            ++at;
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
+}
+
+// X8 (+-1 bytes), T8 rows and per-node {d, E} of the node list, contiguous
+__global__ void tc_gather_kernel(const int32_t* __restrict__ nodes, uint64_t n, const uint32_t* __restrict__ Xb,
+                                 const int8_t* __restrict__ T8, const float4* __restrict__ Q8, int Mw, int Mp,
+                                 int8_t* __restrict__ zx, int8_t* __restrict__ zt, float4* __restrict__ q) {
+    const uint64_t a = blockIdx.x;
+    if (a >= n) return;
+    const int v = nodes[a];
+    for (int m = threadIdx.x; m < Mp; m += blockDim.x) {
+        // padding samples: spin bit 0 -> -1 byte, but T8 = 0 there and the x.x product
+        // is corrected below by zeroing padding spins
+        const uint32_t w = Xb[(size_t)v * Mw + (m >> 5)];
+        zx[a * Mp + m] = (int8_t)(((w >> (m & 31)) & 1u) ? 1 : -1);
+        zt[a * Mp + m] = T8[(size_t)v * Mp + m];
+    }
+    if (threadIdx.x == 0) q[a] = Q8[v];
+}
+__global__ void tc_zero_pad_kernel(int8_t* __restrict__ zx, uint64_t n, int M, int Mp) {
+    const uint64_t a = blockIdx.x;
+    for (int m = M + threadIdx.x; m < Mp; m += blockDim.x) zx[a * Mp + m] = 0;
+}
+// survivors -> the refine kernel's worklist (node ids, triangle slot)
+__global__ void tc_worklist_kernel(const int32_t* __restrict__ nodes, uint64_t n, const int32_t* __restrict__ si,
+                                   const int32_t* __restrict__ sj, uint64_t ns, int32_t* __restrict__ es,
+                                   int32_t* __restrict__ ep, uint32_t* __restrict__ slot,
+                                   uint64_t* __restrict__ idx) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ns) return;
+    const uint64_t i = (uint64_t)si[t], j = (uint64_t)sj[t];
+    es[t] = nodes[i];
+    ep[t] = nodes[j];
+    slot[t] = (uint32_t)(i * (2 * n - i - 1) / 2 + (j - i - 1));
+    idx[t] = t;
+}
+// existing edges with both endpoints in the list: full fp64 routine in K2
+__global__ void tc_edges_kernel(HashView W, uint64_t wcap, const int32_t* __restrict__ loc, uint64_t n,
+                                int32_t* __restrict__ es, int32_t* __restrict__ ep, uint32_t* __restrict__ slot,
+                                uint64_t* __restrict__ idx, float* __restrict__ sg, uint8_t* __restrict__ sf,
+                                unsigned long long* __restrict__ ns, uint64_t cap) {
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= wcap) return;
+    const uint64_t k = W.keys[s];
+    if (k >= kTombKey) return;
+    const int u = (int)(k >> 32), v = (int)(k & 0xffffffffu);
+    const int lu = loc[u], lv = loc[v];
+    if (lu < 0 || lv < 0) return;
+    const uint64_t i = (uint64_t)min(lu, lv), j = (uint64_t)max(lu, lv);
+    const unsigned long long at = atomicAdd(ns, 1ull);
+    if (at >= cap) return;
+    es[at] = u;
+    ep[at] = v;
+    slot[at] = (uint32_t)(i * (2 * n - i - 1) / 2 + (j - i - 1));
+    idx[at] = at;
+    sg[at] = 0.f;
+    sf[at] = 2;
+}
+__global__ void tc_loc_kernel(const int32_t* __restrict__ nodes, uint64_t n, int32_t* __restrict__ loc) {
+    const uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (a < n) loc[nodes[a]] = (int32_t)a;
+}
+
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiled encoder() {
+    static EncodeTiled fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        NRG_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) fail(100, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiled>(p);
+    }
+    return fn;
+}
+
+static CUtensorMap tile_map(void* base, uint64_t rows, uint64_t row_bytes) {
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {row_bytes, rows};
+    const cuuint64_t strides[1] = {row_bytes};
+    const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBM};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, es,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(100, "cuTensorMapEncodeTiled failed");
+    return m;
+}
+
+}  // namespace tc
+
+// The tensor-core exhaustive screen for Ising exact distances of all pairs of `nodes`
+// (row-major upper triangle, as score_all_pairs).  Returns false (nothing written) when
+// the shape is outside what it handles, so the caller takes the CUDA-core path.
+bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* dist) {
+    using namespace tc;
+    if (c.kind != ISING || n < 2 || n > 65535 || getenv("NRG_NO_TC")) return false;
+    ensure_snapshot(c);
+    const double base = generation_base(c);
+    c.tic();
+    const int Mp = c.Mp;
+    DevBuf zxb, ztb, qb, sib, sjb, sgb, sfb, nsb, esb, epb, slb, idb, locb;
+    int8_t* zx = zxb.as<int8_t>(n * Mp);
+    int8_t* zt = ztb.as<int8_t>(n * Mp);
+    float4* q = qb.as<float4>(n);
+    tc_gather_kernel<<<(unsigned)n, 256, 0, c.stream>>>(nodes, n, c.dXb(), static_cast<int8_t*>(c.T8.p),
+                                                        static_cast<float4*>(c.Q8.p), c.Mw, Mp, zx, zt, q);
+    if (Mp > c.M) tc_zero_pad_kernel<<<(unsigned)n, 256, 0, c.stream>>>(zx, n, c.M, Mp);
+    NRG_LAUNCH_CHECK();
+    const uint64_t pairs = n * (n - 1) / 2;
+    const uint64_t cap = std::max<uint64_t>(1u << 20, pairs / 4);
+    TcOut out;
+    out.dist = dist;
+    out.si = sib.as<int32_t>(cap);
+    out.sj = sjb.as<int32_t>(cap);
+    out.sg = sgb.as<float>(cap + c.Wcap);
+    out.sf = sfb.as<uint8_t>(cap + c.Wcap);
+    out.ns = nsb.as<unsigned long long>(1);
+    out.cap = cap;
+    NRG_CUDA(cudaMemsetAsync(out.ns, 0, 8, c.stream));
+    const CUtensorMap mx = tile_map(zx, n, (uint64_t)Mp), mt = tile_map(zt, n, (uint64_t)Mp);
+    const int T = (int)((n + kBM - 1) / kBM);
+    const size_t smem = (size_t)kStages * kStageBytes + 1024;
+    static bool attr = false;
+    if (!attr) {
+        NRG_CUDA(cudaFuncSetAttribute(tc_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    tc_screen_kernel<<<(unsigned)(T * (T + 1) / 2), 128, smem, c.stream>>>(mx, mt, q, (int)n, c.M, Mp, c.lambda,
+                                                                          base, out);
+    NRG_LAUNCH_CHECK();
+    unsigned long long ns = 0;
+    NRG_CUDA(cudaMemcpyAsync(&ns, out.ns, 8, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (ns > cap) {
+        c.toc(P_SCORE);
+        return false;  // more survivors than reserved: the CUDA-core path scores them
+    }
+    // K2 worklist: survivors + existing edges inside the list
+    const uint64_t wl = ns + c.Wcap;
+    int32_t* es = esb.as<int32_t>(wl);
+    int32_t* ep = epb.as<int32_t>(wl);
+    uint32_t* slot = slb.as<uint32_t>(wl);
+    uint64_t* idx = idb.as<uint64_t>(wl);
+    if (ns) {
+        tc_worklist_kernel<<<(unsigned)ceil_div(ns, 256), 256, 0, c.stream>>>(nodes, n, out.si, out.sj, ns, es, ep,
+                                                                             slot, idx);
+        NRG_LAUNCH_CHECK();
+    }
+    int32_t* loc = locb.as<int32_t>(c.n);
+    NRG_CUDA(cudaMemsetAsync(loc, 0xff, (size_t)c.n * 4, c.stream));
+    tc_loc_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(nodes, n, loc);
+    NRG_CUDA(cudaMemcpyAsync(out.ns, &ns, 8, cudaMemcpyHostToDevice, c.stream));
+    tc_edges_kernel<<<(unsigned)ceil_div(c.Wcap, 256), 256, 0, c.stream>>>(c.Wview(), c.Wcap, loc, n, es, ep, slot,
+                                                                          idx, out.sg, out.sf, out.ns, wl);
+    NRG_LAUNCH_CHECK();
+    unsigned long long nw = 0;
+    NRG_CUDA(cudaMemcpyAsync(&nw, out.ns, 8, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    c.toc(P_SCORE);
+    if (nw) {
+        ScoreOut so;
+        so.cache_vals = dist;
+        so.slot = slot;
+        refine_survivors(c, es, ep, idx, out.sg, out.sf, nw, base, so);
+    }
+    c.tc_launches += 1;
+    c.tc_pairs += (double)pairs;
+    return true;
+}
+
+}  // namespace nrg

@@ -190,7 +190,10 @@ __global__ void __launch_bounds__(128) ising_refine_kernel(IsingSnap S, HashView
     const int a = s < p ? s : p, b = s < p ? p : s;
     const TSnap T64{S.T64, S.Mp};
     EdgeOptD r;
-    if (surv_flag[t] == 0) {
+    // a certain survivor was screened assuming w_cur = 0 (K1 checks W; the tensor-core
+    // exhaustive screen does not): existing edges take the full routine
+    const double wcur = hash_get(W, pair_key(a, b), 0.0);
+    if (surv_flag[t] == 0 && wcur == 0.0) {
         const float g = surv_g[t];
         const double dir = g > 0.f ? 1.0 : -1.0;
         const double phi0 = fabs((double)g) - lambda;
@@ -202,7 +205,6 @@ __global__ void __launch_bounds__(128) ising_refine_kernel(IsingSnap S, HashView
         const double u = ising_newton32(S, a, b, lambda, dir, u0, dot, &passes, &conv);
         r = ising_newton64_at(T64, S.Xb, S.Mw, S.M, a, b, 0.0, lambda, dir, u, conv ? 0.0 : u, passes, dot);
     } else {
-        const double wcur = hash_get(W, pair_key(a, b), 0.0);
         r = ising_optimize_edge64(T64, S.Xb, S.Mw, S.M, a, b, wcur, lambda);
     }
     if (lane == 0) {
@@ -297,6 +299,24 @@ static int num_sms(Context& c) {
     return sms;
 }
 
+// K2 over a survivor list (entries surv[t] of the worklist (s, p)), timed into k2_*
+void refine_survivors(Context& c, const int32_t* s, const int32_t* p, const uint64_t* surv, const float* surv_g,
+                      const uint8_t* surv_flag, uint64_t ns, double base, const ScoreOut& out) {
+    if (!ns) return;
+    NRG_CUDA(cudaEventRecord(c.kev0, c.stream));
+    const unsigned rb = (unsigned)ceil_div((int64_t)ns * 32, 128);
+    ising_refine_kernel<<<rb, 128, 0, c.stream>>>(c.isnap(), c.Wview(), s, p, surv, surv_g, surv_flag, ns, c.lambda,
+                                                  base, out, c.dcounters());
+    NRG_LAUNCH_CHECK();
+    NRG_CUDA(cudaEventRecord(c.kev1, c.stream));
+    NRG_CUDA(cudaEventSynchronize(c.kev1));
+    float ms = 0.f;
+    NRG_CUDA(cudaEventElapsedTime(&ms, c.kev0, c.kev1));
+    c.k2_ms += ms;
+    c.k2_launches += 1;
+    c.k2_pairs += (double)ns;
+}
+
 void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uint64_t n,
                    const ScoreOut& out) {
     if (n == 0) return;
@@ -355,20 +375,7 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
                         (unsigned long long)n, (unsigned long long)ns, ms);
         }
         c.last_survivors = ns;
-        if (ns) {
-            NRG_CUDA(cudaEventRecord(c.kev0, c.stream));
-            const unsigned rb = (unsigned)ceil_div((int64_t)ns * 32, 128);
-            ising_refine_kernel<<<rb, 128, 0, c.stream>>>(S, W, s, p, surv, surv_g, surv_flag, ns, c.lambda, base, out,
-                                                          c.dcounters());
-            NRG_LAUNCH_CHECK();
-            NRG_CUDA(cudaEventRecord(c.kev1, c.stream));
-            NRG_CUDA(cudaEventSynchronize(c.kev1));
-            float ms = 0.f;
-            NRG_CUDA(cudaEventElapsedTime(&ms, c.kev0, c.kev1));
-            c.k2_ms += ms;
-            c.k2_launches += 1;
-            c.k2_pairs += (double)ns;
-        }
+        if (ns) refine_survivors(c, s, p, surv, surv_g, surv_flag, ns, base, out);
     } else {
         const uint64_t blocks = std::min<uint64_t>((n + 7) / 8, (uint64_t)sms * 16);
         generic_score_kernel<<<(unsigned)blocks, 256, 0, c.stream>>>(
@@ -395,6 +402,10 @@ __global__ void fill_rows_kernel(const int32_t* __restrict__ nodes, uint64_t n, 
 void score_all_pairs(Context& c, int mode, const int32_t* nodes, uint64_t n, double* dist) {
     // row-major upper triangle (inc/find_best.hpp:72-86), chunked by rows
     if (n < 2) return;
+    if (mode == EXACT && score_all_pairs_tc(c, nodes, n, dist)) {
+        if (c.rank == 0) counters_add_host(c, C_MISSES, n * (n - 1) / 2);
+        return;
+    }
     std::vector<uint64_t> off(n + 1, 0);
     for (uint64_t a = 0; a < n; ++a) off[a + 1] = off[a] + (n - a - 1);
     uint64_t* doff = c.s_o.as<uint64_t>(n + 1);
