@@ -11,9 +11,10 @@
 // exactly as in K1 and kink decisions stay exact.  Per tile (upper triangle of tiles
 // only): TMA loads 128-byte-swizzled K-major tiles of X and T8 for both row blocks into a
 // 3-stage smem ring, one elected thread issues tcgen05.mma.kind::i8 (M=128, N=128, K=32)
-// and commits to mbarriers, and all four warps drain TMEM with tcgen05.ld: pruned pairs
-// get dist = -base exactly, the rest are compacted for K2 (ising_refine_kernel), which
-// also re-decides existing edges.  The result is bitwise the CUDA-core path's.
+// and commits to mbarriers, and all four warps drain TMEM with tcgen05.ld.  A fill kernel
+// first writes dist = -base (the exact kink tie value) to every pair; the tile epilogue
+// only compacts the pairs it cannot prune for K2 (ising_refine_kernel), which also
+// re-decides existing edges.  The result is bitwise the CUDA-core path's.
 #include <cuda.h>
 
 #include <cstdio>
@@ -117,6 +118,7 @@ __global__ void __launch_bounds__(128, 1)
                                                            ~(uintptr_t)1023);
     __shared__ __align__(8) uint64_t full[kStages], empty[kStages], done;
     __shared__ uint32_t tmem_base;
+    __shared__ float2 qcol[kBN];  // {d_j, E_j} of the column block
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // linear tile index -> (I, J), I <= J
     const int T = (n + kBM - 1) / kBM;
@@ -126,6 +128,11 @@ __global__ void __launch_bounds__(128, 1)
         ++I;
     }
     const int J = I + rem;
+    {
+        const int j = J * kBN + (int)threadIdx.x;
+        const float4 v = j < n ? __ldg(&q[j]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        qcol[threadIdx.x] = make_float2(v.x, v.y);
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
@@ -189,9 +196,7 @@ __global__ void __launch_bounds__(128, 1)
     const int i = I * kBM + r;
     const float lam = (float)lambda;
     const float err0 = 4.f * (float)M * 5.9604645e-08f;
-    const double pruned = -(base + 0.0);
     const float4 qi = i < n ? __ldg(&q[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const uint64_t row_off = (uint64_t)i * (2 * (uint64_t)n - (uint64_t)i - 1) / 2;
     for (int c0 = 0; c0 < kBN; c0 += 16) {
         uint32_t a1[16], a2[16], a3[16];
         const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;
@@ -206,12 +211,11 @@ __global__ void __launch_bounds__(128, 1)
             const int j = J * kBN + c0 + u;
             gv[u] = 0.f;
             if (i < n && j < n && i < j) {
-                const float4 qj = __ldg(&q[j]);
+                // pruned pairs keep the -base the fill kernel wrote
+                const float2 qj = qcol[c0 + u];
                 const float g = (float)(2 * (int)a1[u]) - (qj.x * (float)(int)a2[u] + qi.x * (float)(int)a3[u]);
                 const float err = (qi.y + qj.y) * 1.0001f + err0;
-                if (fabsf(g) <= lam - err) {
-                    out.dist[row_off + (uint64_t)(j - i - 1)] = pruned;
-                } else {
+                if (fabsf(g) > lam - err) {
                     surv_mask |= 1u << u;
                     gv[u] = g;
                 }
@@ -236,7 +240,7 @@ __global__ void __launch_bounds__(128, 1)
                 out.si[at] = i;
                 out.sj[at] = J * kBN + c0 + u;
                 out.sg[at] = g;
-                const float4 qj = __ldg(&q[J * kBN + c0 + u]);
+                const float2 qj = qcol[c0 + u];
                 const float err = (qi.y + qj.y) * 1.0001f + err0;
                 out.sf[at] = fabsf(g) < lam + err ? 1 : 0;
             }
@@ -247,6 +251,11 @@ __global__ void __launch_bounds__(128, 1)
     __syncthreads();
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
+}
+
+__global__ void tc_fill_kernel(double* __restrict__ dist, uint64_t n, double v) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) dist[t] = v;
 }
 
 // X8 (+-1 bytes), T8 rows and per-node {d, E} of the node list, contiguous
@@ -369,6 +378,10 @@ bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* di
     out.ns = nsb.as<unsigned long long>(1);
     out.cap = cap;
     NRG_CUDA(cudaMemsetAsync(out.ns, 0, 8, c.stream));
+    // every pair starts pruned (dist = -base exactly, the kink tie value); the tile
+    // kernel only lists the rest for K2, which overwrites their slots
+    tc_fill_kernel<<<(unsigned)std::min<uint64_t>(ceil_div(pairs, 256), 148 * 16), 256, 0, c.stream>>>(
+        dist, pairs, -(base + 0.0));
     const CUtensorMap mx = tile_map(zx, n, (uint64_t)Mp), mt = tile_map(zt, n, (uint64_t)Mp);
     const int T = (int)((n + kBM - 1) / kBM);
     const size_t smem = (size_t)kStages * kStageBytes + 1024;
