@@ -182,6 +182,11 @@ int nrg_gcd_iteration(nrg_ctx* ctx, const nrg_gcd_cfg* cfg, int32_t iter, nrg_it
 /* reconstruct_gcd (inc/reconstruct.hpp:148-181) */
 int nrg_reconstruct_gcd(nrg_ctx* ctx, const nrg_gcd_cfg* cfg, nrg_iter_record* recs,
                         int32_t rec_cap, int32_t* n_iters, int32_t* converged);
+/* reconstruct_cd (inc/reconstruct.hpp:185-207): every iteration updates all pairs
+ * i < j in row-major order (sequential semantics), then the theta pass; stops when
+ * delta < eps (eps <= 0: 1e-6 N).  n(n-1)/2 < 2^31.  threads is accepted and ignored. */
+int nrg_reconstruct_cd(nrg_ctx* ctx, double eps, int32_t max_iters, int32_t threads, nrg_iter_record* recs,
+                       int32_t rec_cap, int32_t* n_iters, int32_t* converged);
 
 /* counters: pairs scored (cache misses, inc/model.hpp:83-84), cache hits,
  * line-search passes and warnings (inc/model.hpp:270-271). */

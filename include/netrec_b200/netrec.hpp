@@ -710,6 +710,23 @@ inline ReconstructionResult reconstruct_gcd(PseudoLikelihood& model, const Recon
     return res;
 }
 
+/// reconstruct_cd (inc/reconstruct.hpp:185-207) on the device
+inline ReconstructionResult reconstruct_cd(PseudoLikelihood& model, double eps = -1.0, int max_iters = 1000,
+                                           int threads = 1) {
+    std::vector<nrg_iter_record> recs(static_cast<std::size_t>(std::max(max_iters, 1)));
+    int32_t ni = 0, cv = 0;
+    detail::check(nrg_reconstruct_cd(model.context(), eps, max_iters, threads, recs.data(),
+                                     static_cast<int32_t>(recs.size()), &ni, &cv));
+    model.pull_state();
+    ReconstructionResult res;
+    res.converged = cv != 0;
+    for (int t = 0; t < ni; ++t) {
+        const auto& r = recs[static_cast<std::size_t>(t)];
+        res.trace.iterations.push_back({r.iter, r.delta, r.seconds, static_cast<std::size_t>(r.candidates), r.objective});
+    }
+    return res;
+}
+
 }  // namespace netrec
 
 #endif

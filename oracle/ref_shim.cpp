@@ -342,6 +342,21 @@ int ref_reconstruct_gcd(void* p, double kappa, double eps, int max_iters, int mo
     })
 }
 
+// reconstruct_cd (inc/reconstruct.hpp:185-207), the reference itself
+int ref_reconstruct_cd(void* p, double eps, int max_iters, int threads, RefIterRecord* recs, int rec_cap,
+                       int* n_iters, int* converged) {
+    auto* h = static_cast<Handle*>(p);
+    GUARD({
+        const ReconstructionResult r = reconstruct_cd(*h->model, eps, max_iters, threads);
+        *converged = r.converged ? 1 : 0;
+        *n_iters = static_cast<int>(r.trace.iterations.size());
+        for (int t = 0; t < *n_iters && t < rec_cap; ++t) {
+            const auto& it = r.trace.iterations[static_cast<std::size_t>(t)];
+            recs[t] = {it.iter, 0, it.delta, it.seconds, it.candidates, it.objective};
+        }
+    })
+}
+
 int ref_counters(void* p, std::uint64_t* misses, std::uint64_t* hits, std::uint64_t* evals,
                  std::uint64_t* warnings) {
     auto* h = static_cast<Handle*>(p);

@@ -81,6 +81,7 @@ SIGNATURES = {
     "nrg_theta_pass": (C.c_int, [_P]),
     "nrg_gcd_iteration": (C.c_int, [_P, C.POINTER(GcdCfg), _i32, _ITP, _VP, _u64, C.POINTER(_u64)]),
     "nrg_reconstruct_gcd": (C.c_int, [_P, C.POINTER(GcdCfg), _ITP, _i32, C.POINTER(_i32), C.POINTER(_i32)]),
+    "nrg_reconstruct_cd": (C.c_int, [_P, _d, _i32, _i32, _ITP, _i32, C.POINTER(_i32), C.POINTER(_i32)]),
     "nrg_counters": (C.c_int, [_P, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)]),
     "nrg_reset_counters": (C.c_int, [_P]),
     "nrg_recall_curve": (C.c_int, [_u64, _PAIRP, _PAIRP, _F64P]),
@@ -302,6 +303,12 @@ class Model:
         recs = np.zeros(max(max_iters, 1), ITER_DT)
         ni, cv = _i32(), _i32()
         check(self.L.nrg_reconstruct_gcd(self.h, C.byref(cfg), recs, len(recs), C.byref(ni), C.byref(cv)))
+        return recs[: ni.value].copy(), bool(cv.value)
+
+    def reconstruct_cd(self, eps=-1.0, max_iters=1000, threads=1):
+        recs = np.zeros(max(max_iters, 1), ITER_DT)
+        ni, cv = _i32(), _i32()
+        check(self.L.nrg_reconstruct_cd(self.h, eps, max_iters, threads, recs, len(recs), C.byref(ni), C.byref(cv)))
         return recs[: ni.value].copy(), bool(cv.value)
 
     def counters(self):

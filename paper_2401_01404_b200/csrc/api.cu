@@ -353,6 +353,41 @@ int nrg_reconstruct_gcd(nrg_ctx* x, const nrg_gcd_cfg* cfg, nrg_iter_record* rec
     });
 }
 
+int nrg_reconstruct_cd(nrg_ctx* x, double eps, int32_t max_iters, int32_t threads, nrg_iter_record* recs,
+                       int32_t rec_cap, int32_t* n_iters, int32_t* converged) {
+    (void)threads;
+    return guardx(x, [&] {
+        need_samples(x);
+        nrg::Context& c = x->c;
+        const uint64_t n = (uint64_t)c.n;
+        const uint64_t np = n * (n - 1) / 2;
+        if (np >= (1ull << 31)) nrg::fail(22, "reconstruct_cd: too many pairs (n > 65535)");
+        const double eps_eff = eps > 0.0 ? eps : 1e-6 * (double)n;
+        nrg::DevBuf bi, bj, bd;
+        int32_t* ci = bi.as<int32_t>(np);
+        int32_t* cj = bj.as<int32_t>(np);
+        double* tie = bd.as<double>(np);
+        nrg::all_pairs_list(c, ci, cj, tie);
+        *converged = 0;
+        *n_iters = 0;
+        for (int iter = 1; iter <= max_iters; ++iter) {
+            const auto t0 = std::chrono::steady_clock::now();
+            // every pair of the row-major list ties: apply_updates resolves the list in
+            // parallel rounds once few couplings still move, in dependency order otherwise
+            const double delta = nrg::apply_updates(c, ci, cj, np, nullptr, tie);
+            nrg::theta_pass(c, nullptr);
+            const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            const double obj = nrg::log_posterior(c);
+            if (*n_iters < rec_cap) recs[*n_iters] = {iter, 0, delta, secs, np, obj};
+            ++*n_iters;
+            if (delta < eps_eff) {
+                *converged = 1;
+                break;
+            }
+        }
+    });
+}
+
 int nrg_counters(nrg_ctx* x, uint64_t* misses, uint64_t* hits, uint64_t* evals, uint64_t* warnings) {
     return guardx(x, [&] {
         uint64_t h[nrg::C_N];

@@ -100,6 +100,7 @@ struct UpdateArgs {
     const int32_t* cj;
     const double* assign;
     const int32_t* dep;
+    const uint32_t* order;  // ticket -> pair (dependency-level order) or nullptr (list order)
     uint64_t n;
     double lambda;
     int* done;
@@ -126,6 +127,7 @@ __global__ void __launch_bounds__(NT, 3) update_kernel(UpdateArgs A) {
     for (;;) {
         if (tid == 0) {
             unsigned long long p = atomicAdd(A.ticket, 1ull);
+            if (p < A.n && A.order) p = (unsigned long long)A.order[p];  // level-ordered tickets
             if (p < A.n) {
                 // wait for the predecessors on both endpoints
                 const int d0 = A.dep[2 * p], d1 = A.dep[2 * p + 1];
@@ -272,6 +274,33 @@ static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64
     NRG_CUDA(cudaMemsetAsync(done, 0, n * 4, c.stream));
     NRG_CUDA(cudaMemsetAsync(ticket, 0, 8, c.stream));
     NRG_LAUNCH_CHECK();
+    // Tickets in dependency-level order (longest predecessor chain, then list index):
+    // a pair's predecessors sit at strictly lower levels, so they hold earlier tickets
+    // (no deadlock) and a whole wavefront is in flight at once.  In list order the
+    // resident CTAs only ever see a window of consecutive pairs, which for lists like
+    // reconstruct_cd's row-major all-pairs share one node and run one at a time.
+    DevBuf ordb;
+    uint32_t* order = nullptr;
+    if (n >= 4096 && !getenv("NRG_LIST_ORDER_TICKETS")) {
+        std::vector<int32_t> hdep(2 * n);
+        NRG_CUDA(cudaMemcpyAsync(hdep.data(), dep, 8 * n, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        std::vector<uint32_t> lev(n), cnt(1, 0);
+        for (uint64_t p = 0; p < n; ++p) {
+            uint32_t l = 0;
+            if (hdep[2 * p] >= 0) l = std::max(l, lev[hdep[2 * p]] + 1);
+            if (hdep[2 * p + 1] >= 0) l = std::max(l, lev[hdep[2 * p + 1]] + 1);
+            lev[p] = l;
+            if (l >= cnt.size()) cnt.resize(l + 1, 0);
+            ++cnt[l];
+        }
+        std::vector<uint32_t> start(cnt.size(), 0), hord(n);
+        for (size_t l = 1; l < cnt.size(); ++l) start[l] = start[l - 1] + cnt[l - 1];
+        for (uint64_t p = 0; p < n; ++p) hord[start[lev[p]]++] = (uint32_t)p;
+        order = ordb.as<uint32_t>(n);
+        NRG_CUDA(cudaMemcpyAsync(order, hord.data(), 4 * n, cudaMemcpyHostToDevice, c.stream));
+        c.sync();
+    }
     UpdateArgs A;
     A.kind = c.kind;
     A.Xb = c.dXb();
@@ -287,6 +316,7 @@ static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64
     A.cj = cj;
     A.assign = assign;
     A.dep = dep;
+    A.order = order;
     A.n = n;
     A.lambda = c.lambda;
     A.done = done;
@@ -489,6 +519,24 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
     c.toc(P_UPDATE);
     c.state_version++;
     return h;
+}
+
+// all pairs i < j of 0..n-1 in row-major order (reconstruct_cd's list,
+// inc/reconstruct.hpp:190-192), with a constant tie distance
+__global__ void all_pairs_kernel(uint64_t n, int32_t* __restrict__ ci, int32_t* __restrict__ cj,
+                                 double* __restrict__ tie) {
+    const uint64_t i = blockIdx.x;
+    if (i >= n) return;
+    const uint64_t off = i * (2 * n - i - 1) / 2;
+    for (uint64_t j = i + 1 + threadIdx.x; j < n; j += blockDim.x) {
+        ci[off + j - i - 1] = (int32_t)i;
+        cj[off + j - i - 1] = (int32_t)j;
+        tie[off + j - i - 1] = 0.0;
+    }
+}
+void all_pairs_list(Context& c, int32_t* ci, int32_t* cj, double* tie) {
+    all_pairs_kernel<<<(unsigned)c.n, 256, 0, c.stream>>>((uint64_t)c.n, ci, cj, tie);
+    NRG_LAUNCH_CHECK();
 }
 
 // ---------------------------------------------------------------- theta pass

@@ -64,6 +64,7 @@ _SIGS = {
     "theta_pass": (_i, [_P, _i]),
     "reconstruct_gcd": (_i, [_P, _d, _d, _i, _i, _d, _u64, _i, _ITP, _i, C.POINTER(_i),
                              C.POINTER(_i), C.c_void_p, _u64, C.POINTER(_u64)]),
+    "reconstruct_cd": (_i, [_P, _d, _i, _i, _ITP, _i, C.POINTER(_i), C.POINTER(_i)]),
     "counters": (_i, [_P, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)]),
     "recall_curve": (_i, [_u64, _PAIRP, _PAIRP, _F64P]),
     "mix64": (_u64, [_u64, _u64]),
@@ -262,6 +263,13 @@ class CpuModel:
                                                     cand.ctypes.data if cand_cap else None,
                                                     cand_cap, C.byref(nc)))
         return recs[: ni.value].copy(), bool(cv.value), cand[: nc.value].copy()
+
+    def reconstruct_cd(self, eps=-1.0, max_iters=1000, threads=1):
+        recs = np.zeros(max(max_iters, 1), ITER_DT)
+        ni, cv = _i(), _i()
+        _chk(self.which, self._f("reconstruct_cd")(self.h, eps, max_iters, threads, recs, len(recs), C.byref(ni),
+                                                   C.byref(cv)))
+        return recs[: ni.value].copy(), bool(cv.value)
 
     def counters(self):
         v = [_u64() for _ in range(4)]
