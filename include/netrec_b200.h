@@ -222,6 +222,19 @@ int nrg_sample_scored_pairs(nrg_ctx* ctx, uint64_t cap, uint64_t seed, int32_t* 
  * out as int8 (X_out, N x M). */
 int nrg_generate_ising(nrg_ctx* ctx, double mean_deg, double w_sigma, double th_sigma,
                        int32_t burn_in, int32_t thin, uint64_t seed, int8_t* X_out);
+/* Config 5 truth: erased configuration model, degrees P(d) ~ d^-gamma for d >= dmin
+ * (capped at sqrt(N)); same Gibbs sampler and outputs as nrg_generate_ising. */
+int nrg_generate_ising_powerlaw(nrg_ctx* ctx, double gamma, int32_t dmin, double w_sigma, double th_sigma,
+                                int32_t burn_in, int32_t thin, uint64_t seed, int8_t* X_out);
+/* Gibbs samples of a caller-supplied Ising truth (distinct edges, theta[N]). */
+int nrg_generate_ising_graph(nrg_ctx* ctx, uint64_t n_edges, const int32_t* ei, const int32_t* ej,
+                             const double* w, const double* theta, int32_t burn_in, int32_t thin, uint64_t seed,
+                             int8_t* X_out);
+/* Config 3 (Gaussian context): random degree-regular precision matrix, off-diagonals
+ * U(-amp, amp), diagonal = row sum |K_ij| + 0.5; samples by graph-coloured Gibbs (the
+ * stationary law of a sparse-Cholesky draw); optionally copied out (X_out, N x M). */
+int nrg_generate_gaussian(nrg_ctx* ctx, int32_t degree, double amp, int32_t burn_in, int32_t thin, uint64_t seed,
+                          double* X_out);
 
 /* Multi-GPU: samples, sums, W and theta replicated (updates and theta
  * passes run identically on every rank); NNDescent nodes sharded by contiguous ranges;

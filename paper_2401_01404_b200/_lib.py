@@ -90,6 +90,9 @@ SIGNATURES = {
     "nrg_kernel_stats": (C.c_int, [_P, _F64P, _i32]),
     "nrg_sample_scored_pairs": (C.c_int, [_P, _u64, _u64, _I32P, _I32P, C.POINTER(_u64)]),
     "nrg_generate_ising": (C.c_int, [_P, _d, _d, _d, _i32, _i32, _u64, _VP]),
+    "nrg_generate_ising_powerlaw": (C.c_int, [_P, _d, _i32, _d, _d, _i32, _i32, _u64, _VP]),
+    "nrg_generate_ising_graph": (C.c_int, [_P, _u64, _I32P, _I32P, _F64P, _F64P, _i32, _i32, _u64, _VP]),
+    "nrg_generate_gaussian": (C.c_int, [_P, _i32, _d, _i32, _i32, _u64, _VP]),
     "nrg_comm_unique_id": (C.c_int, [C.c_char_p]),
     "nrg_comm_init": (C.c_int, [_P, C.c_char_p, _i32, _i32]),
     "nrg_loopback_create": (C.c_int, [_i32, C.POINTER(_VP)]),
@@ -180,6 +183,26 @@ class Model:
         out = np.zeros((self.n, self.M), np.int8) if want_samples else None
         check(self.L.nrg_generate_ising(self.h, mean_deg, w_sigma, th_sigma, burn_in, thin, seed,
                                         out.ctypes.data if out is not None else None))
+        return out
+
+    def generate_ising_powerlaw(self, gamma=2.5, dmin=2, w_sigma=0.2, th_sigma=0.1, burn_in=1000, thin=10, seed=0,
+                                want_samples=False):
+        out = np.zeros((self.n, self.M), np.int8) if want_samples else None
+        check(self.L.nrg_generate_ising_powerlaw(self.h, gamma, dmin, w_sigma, th_sigma, burn_in, thin, seed,
+                                                 out.ctypes.data if out is not None else None))
+        return out
+
+    def generate_ising_graph(self, ei, ej, w, theta, burn_in=1000, thin=10, seed=0, want_samples=False):
+        ei, ej, w, theta = _i32a(ei), _i32a(ej), _f64a(w), _f64a(theta)
+        out = np.zeros((self.n, self.M), np.int8) if want_samples else None
+        check(self.L.nrg_generate_ising_graph(self.h, len(ei), ei, ej, w, theta, burn_in, thin, seed,
+                                              out.ctypes.data if out is not None else None))
+        return out
+
+    def generate_gaussian(self, degree=4, amp=0.2, burn_in=1000, thin=10, seed=0, want_samples=False):
+        out = np.zeros((self.n, self.M)) if want_samples else None
+        check(self.L.nrg_generate_gaussian(self.h, degree, amp, burn_in, thin, seed,
+                                           out.ctypes.data if out is not None else None))
         return out
 
     def reset_state(self):

@@ -477,19 +477,53 @@ int nrg_recall_curve(uint64_t m, const nrg_pair* exact, const nrg_pair* approx, 
     });
 }
 
+namespace {
+// the bit-packed samples as int8 on the host
+void unpack_spins(nrg_ctx* x, int8_t* X_out) {
+    if (!X_out) return;
+    nrg::Context& c = x->c;
+    std::vector<uint32_t> bits((size_t)c.n * c.Mw);
+    NRG_CUDA(cudaMemcpyAsync(bits.data(), c.Xb.p, bits.size() * 4, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    for (int i = 0; i < c.n; ++i)
+        for (int m = 0; m < c.M; ++m)
+            X_out[(size_t)i * c.M + m] = ((bits[(size_t)i * c.Mw + (m >> 5)] >> (m & 31)) & 1u) ? 1 : -1;
+}
+}  // namespace
+
 int nrg_generate_ising(nrg_ctx* x, double mean_deg, double w_sigma, double th_sigma, int32_t burn_in, int32_t thin,
                        uint64_t seed, int8_t* X_out) {
     return guardx(x, [&] {
         nrg::generate_ising(x->c, mean_deg, w_sigma, th_sigma, burn_in, thin, seed);
+        unpack_spins(x, X_out);
+    });
+}
+
+int nrg_generate_ising_powerlaw(nrg_ctx* x, double gamma, int32_t dmin, double w_sigma, double th_sigma,
+                                int32_t burn_in, int32_t thin, uint64_t seed, int8_t* X_out) {
+    return guardx(x, [&] {
+        nrg::generate_ising_powerlaw(x->c, gamma, dmin, w_sigma, th_sigma, burn_in, thin, seed);
+        unpack_spins(x, X_out);
+    });
+}
+
+int nrg_generate_ising_graph(nrg_ctx* x, uint64_t n_edges, const int32_t* ei, const int32_t* ej, const double* w,
+                             const double* theta, int32_t burn_in, int32_t thin, uint64_t seed, int8_t* X_out) {
+    return guardx(x, [&] {
+        nrg::generate_ising_graph(x->c, n_edges, ei, ej, w, theta, burn_in, thin, seed);
+        unpack_spins(x, X_out);
+    });
+}
+
+int nrg_generate_gaussian(nrg_ctx* x, int32_t degree, double amp, int32_t burn_in, int32_t thin, uint64_t seed,
+                          double* X_out) {
+    return guardx(x, [&] {
+        nrg::generate_gaussian(x->c, degree, amp, burn_in, thin, seed);
         if (X_out) {
-            // unpack the bit-packed samples to int8 on the host
             nrg::Context& c = x->c;
-            std::vector<uint32_t> bits((size_t)c.n * c.Mw);
-            NRG_CUDA(cudaMemcpyAsync(bits.data(), c.Xb.p, bits.size() * 4, cudaMemcpyDeviceToHost, c.stream));
+            NRG_CUDA(cudaMemcpy2DAsync(X_out, (size_t)c.M * 8, c.Xd.p, (size_t)c.Mp * 8, (size_t)c.M * 8, c.n,
+                                       cudaMemcpyDeviceToHost, c.stream));
             c.sync();
-            for (int i = 0; i < c.n; ++i)
-                for (int m = 0; m < c.M; ++m)
-                    X_out[(size_t)i * c.M + m] = ((bits[(size_t)i * c.Mw + (m >> 5)] >> (m & 31)) & 1u) ? 1 : -1;
         }
     });
 }

@@ -328,5 +328,10 @@ void find_best(Context& c, int mode, uint64_t m, const int32_t* d_nodes, uint64_
 // ---- gen.cu
 void generate_ising(Context& c, double mean_deg, double w_sigma, double th_sigma, int burn_in,
                     int thin, uint64_t seed);
+void generate_ising_powerlaw(Context& c, double gamma, int dmin, double w_sigma, double th_sigma, int burn_in,
+                             int thin, uint64_t seed);
+void generate_ising_graph(Context& c, uint64_t ne, const int32_t* ei, const int32_t* ej, const double* w,
+                          const double* theta, int burn_in, int thin, uint64_t seed);
+void generate_gaussian(Context& c, int degree, double amp, int burn_in, int thin, uint64_t seed);
 
 }  // namespace nrg
