@@ -209,7 +209,7 @@ int nrg_timer(nrg_ctx* ctx, int32_t op, double* ms);
  * [0] screen (K1) device ms, [1] K1 launches, [2] pairs screened, [3] refine (K2) ms,
  * [4] K2 launches, [5] survivors refined, [6] kernel launches issued (all kernels),
  * [7] parallel rounds apply_updates spent on tie tails, [8] tensor-core all-pairs screens,
- * [9] pairs they screened. */
+ * [9] pairs they screened, [10] distance-cache flushes (a generation outgrew 2^31 slots). */
 int nrg_kernel_stats(nrg_ctx* ctx, double* out, int32_t cap);
 /* Uniform sample (up to cap) of the unique pairs scored in the current generation
  * (the distance cache's keys); returns the count in *n_out. */

@@ -351,10 +351,10 @@ class Model:
         return v.value
 
     def kernel_stats(self):
-        out = np.zeros(10)
-        check(self.L.nrg_kernel_stats(self.h, out, 10))
+        out = np.zeros(11)
+        check(self.L.nrg_kernel_stats(self.h, out, 11))
         keys = ["k1_ms", "k1_launches", "k1_pairs", "k2_ms", "k2_launches", "k2_pairs", "launches", "tail_rounds",
-                "tc_launches", "tc_pairs"]
+                "tc_launches", "tc_pairs", "cache_flushes"]
         return dict(zip(keys, out.tolist()))
 
     def sample_scored_pairs(self, cap, seed=0):

@@ -406,7 +406,7 @@ int nrg_reset_counters(nrg_ctx* x) {
         for (double& v : x->c.phase_ms) v = 0.0;
         x->c.k1_ms = x->c.k1_launches = x->c.k1_pairs = x->c.k2_ms = x->c.k2_launches = x->c.k2_pairs = 0;
         x->c.tail_rounds = 0;
-        x->c.tc_launches = x->c.tc_pairs = 0;
+        x->c.tc_launches = x->c.tc_pairs = x->c.cache_flushes = 0;
         x->c.launches0 = nrg::g_launches.load();
         x->c.sync();
     });
@@ -439,10 +439,10 @@ int nrg_timer(nrg_ctx* x, int32_t op, double* ms) {
 int nrg_kernel_stats(nrg_ctx* x, double* out, int32_t cap) {
     return guardx(x, [&] {
         const nrg::Context& c = x->c;
-        const double v[10] = {c.k1_ms, c.k1_launches, c.k1_pairs, c.k2_ms, c.k2_launches, c.k2_pairs,
+        const double v[11] = {c.k1_ms, c.k1_launches, c.k1_pairs, c.k2_ms, c.k2_launches, c.k2_pairs,
                               (double)(nrg::g_launches.load() - c.launches0), c.tail_rounds, c.tc_launches,
-                              c.tc_pairs};
-        for (int t = 0; t < 10 && t < cap; ++t) out[t] = v[t];
+                              c.tc_pairs, c.cache_flushes};
+        for (int t = 0; t < 11 && t < cap; ++t) out[t] = v[t];
     });
 }
 

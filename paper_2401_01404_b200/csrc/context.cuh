@@ -195,6 +195,7 @@ struct Context {
     double k1_ms = 0, k1_launches = 0, k1_pairs = 0, k2_ms = 0, k2_launches = 0, k2_pairs = 0;
     double tail_rounds = 0;  // apply_updates: parallel rounds spent on tie tails
     double tc_launches = 0, tc_pairs = 0;  // tensor-core exhaustive screen
+    double cache_flushes = 0;              // distance-cache flushes (generation exceeded 2^31 slots)
     uint64_t launches0 = 0;
     cudaEvent_t kev0 = nullptr, kev1 = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;

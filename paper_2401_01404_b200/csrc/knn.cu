@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(NT) knn_gather_kernel(const int32_t* __restric
                                                         uint64_t capn, int32_t* __restrict__ cand_id,
                                                         uint32_t* __restrict__ cand_slot,
                                                         int32_t* __restrict__ cand_cnt, uint64_t lo, int lw,
-                                                        const uint8_t* __restrict__ newf) {
+                                                        const uint8_t* __restrict__ newf, bool do_claim) {
     extern __shared__ int32_t tab[];
     __shared__ int ncand;
     const uint64_t li = lo + blockIdx.x;
@@ -443,6 +443,10 @@ __global__ void __launch_bounds__(NT) knn_gather_kernel(const int32_t* __restric
     }
     __syncthreads();
     const int cnt = ncand;
+    if (!do_claim) {  // cached metrics claim in claim_cands_kernel after the exact reservation
+        if (tid == 0) cand_cnt[li] = cnt;
+        return;
+    }
     // claim (pair_key(nodes[li], nodes[v])) in the per-generation distance cache
     const int32_t gs = nodes[li];
     for (int t0 = 0; t0 < cnt; t0 += NT) {
@@ -453,6 +457,34 @@ __global__ void __launch_bounds__(NT) knn_gather_kernel(const int32_t* __restric
         if (valid) cand_slot[li * capn + t] = sl;
     }
     if (tid == 0) cand_cnt[li] = cnt;
+}
+
+// claims of the gathered candidates, one warp per node (after cache_reserve sized the
+// table for exactly this sweep's candidates)
+__global__ void claim_cands_kernel(const int32_t* __restrict__ nodes, HashView h, ClaimSink sink, uint64_t own,
+                                   uint64_t lo, uint64_t capn, const int32_t* __restrict__ cand_id,
+                                   uint32_t* __restrict__ cand_slot, const int32_t* __restrict__ cand_cnt) {
+    const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= own) return;
+    const uint64_t li = lo + w;
+    const int cnt = cand_cnt[li];
+    const int32_t gs = nodes[li];
+    for (int t0 = 0; t0 < cnt; t0 += 32) {
+        const int t = t0 + lane;
+        const bool valid = t < cnt;
+        const int32_t v = valid ? cand_id[li * capn + t] : 0;
+        const uint32_t sl = claim_warp(h, sink, valid, gs, valid ? nodes[v] : 0, li * capn + t);
+        if (valid) cand_slot[li * capn + t] = sl;
+    }
+}
+
+__global__ void sum_counts_kernel(const int32_t* __restrict__ cnt, uint64_t n, unsigned long long* __restrict__ out) {
+    unsigned long long a = 0;
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x)
+        a += (unsigned long long)cnt[t];
+    for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if ((threadIdx.x & 31) == 0 && a) atomicAdd(out, a);
 }
 
 // ---------------------------------------------------------------- merge top-kw
@@ -946,7 +978,10 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         int P = 1;
         while (P < kw) P <<= 1;
         const size_t rs_smem = (size_t)P * 16;
-        if (rs_smem > 48 * 1024) fail(100, "find_knn: kw too large for the row sort");
+        if (rs_smem > 200 * 1024) fail(100, "find_knn: kw too large for the row sort");
+        if (rs_smem > 48 * 1024)
+            NRG_CUDA(cudaFuncSetAttribute(row_sort_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)rs_smem));
         if (own) {
             if (P <= 64)
                 row_sort_kernel<32><<<(unsigned)own, 32, rs_smem, c.stream>>>(gid + lo * kw, gd + lo * kw, d_nodes, own,
@@ -962,7 +997,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
 
     // ---- sweeps
     const uint64_t capn = std::min<uint64_t>((uint64_t)cap * cap, n - 1);
-    DevBuf adjb, alenb, adjpb, alenpb, newfb, cidb, cslb, ccntb, churnb, wsb, wpb, wslb;
+    DevBuf adjb, alenb, adjpb, alenpb, newfb, cidb, cslb, ccntb, churnb, churnb2, wsb, wpb, wslb;
     int32_t* adj = adjb.as<int32_t>(n * cap);
     int32_t* alen = alenb.as<int32_t>(n);
     int32_t* adjp = adjpb.as<int32_t>(n * cap);  // U of the previous sweep
@@ -1048,25 +1083,52 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                                                                          (sweep == 0 || !incremental) ? 1 : 0, newf);
         NRG_LAUNCH_CHECK();
         c.toc(P_KNN);
-        // gather + claim (own nodes; remote keys routed to their owner ranks)
-        if (cached) cache_reserve(c, wmax);
+        // gather (own nodes), then — for the cached metric — reserve the distance cache
+        // for exactly this sweep's candidates (job-wide: remote keys land on their owner)
+        // and claim them; uncached metrics claim flat slots inside the gather
+        // the worst case (every node gathers capn new pairs) normally fits the cache
+        // with room to spare: reserve it and claim inside the gather; otherwise gather,
+        // count, reserve exactly and claim in a second pass
+        const bool fused = !cached || (c.cache_live_host + wmax) * 10 <= (1ull << 31) * 6;
+        if (cached && fused) cache_reserve(c, wmax);
         c.tic();
         NRG_CUDA(cudaMemsetAsync(wcount, 0, 16, c.stream));
         NRG_CUDA(cudaMemsetAsync(churn, 0, 8, c.stream));
-        const HashView hv = cached ? c.Cview() : HashView{nullptr, nullptr, 0};
         const ClaimSink sk = sink_for(ws, wp, wsl, own * capn + 1);
         if (own) {
             int lw = 0;
             while ((1 << lw) < cap) ++lw;
+            const HashView hv0 = fused && cached ? c.Cview() : HashView{nullptr, nullptr, 0};
             if (big)
                 knn_gather_kernel<256><<<(unsigned)own, 256, tab_bytes, c.stream>>>(
-                    d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv, sk, capn, cand_id, cand_slot,
-                    cand_cnt, lo, lw, newf);
+                    d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv0, sk, capn, cand_id,
+                    cand_slot, cand_cnt, lo, lw, newf, fused);
             else
                 knn_gather_kernel<32><<<(unsigned)own, 32, tab_bytes, c.stream>>>(
-                    d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv, sk, capn, cand_id, cand_slot,
-                    cand_cnt, lo, lw, newf);
+                    d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv0, sk, capn, cand_id,
+                    cand_slot, cand_cnt, lo, lw, newf, fused);
             NRG_LAUNCH_CHECK();
+        }
+        if (cached && !fused) {
+            unsigned long long* tot = churnb2.as<unsigned long long>(1);
+            NRG_CUDA(cudaMemsetAsync(tot, 0, 8, c.stream));
+            if (own) {
+                sum_counts_kernel<<<(unsigned)std::min<uint64_t>(ceil_div(own, 256), 1184), 256, 0, c.stream>>>(
+                    cand_cnt + lo, own, tot);
+                NRG_LAUNCH_CHECK();
+            }
+            uint64_t total = 0;
+            NRG_CUDA(cudaMemcpyAsync(&total, tot, 8, cudaMemcpyDeviceToHost, c.stream));
+            c.sync();
+            if (c.world > 1) static_cast<Comm*>(c.comm)->allreduce_u64(&total, 1, false, c.stream);
+            c.toc(P_KNN);
+            cache_reserve(c, total);
+            c.tic();
+            if (own) {
+                claim_cands_kernel<<<(unsigned)ceil_div(own * 32, 256), 256, 0, c.stream>>>(
+                    d_nodes, c.Cview(), sk, own, lo, capn, cand_id, cand_slot, cand_cnt);
+                NRG_LAUNCH_CHECK();
+            }
         }
         unsigned long long nw = 0;
         NRG_CUDA(cudaMemcpyAsync(&nw, wcount, 8, cudaMemcpyDeviceToHost, c.stream));

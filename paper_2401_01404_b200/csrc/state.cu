@@ -595,9 +595,27 @@ void cache_reserve(Context& c, uint64_t extra) {
         c.sync();
     }
     c.cache_live_host = live;
-    if (c.Ccap && (live + extra) * 10 <= c.Ccap * 6) return;  // load factor <= 0.6
-    const uint64_t ncap = std::max<uint64_t>(1u << 20, next_pow2(2 * (live + extra)));
-    if (ncap > (1ull << 31)) fail(100, "distance cache would exceed 2^31 slots");
+    // load factor <= 0.6; slot indices are 31-bit (bit 31 flags remote slots), so at the
+    // 2^31-slot ceiling the table runs up to 0.85 full (longer probes, still exact)
+    const uint64_t kMax = 1ull << 31;
+    uint64_t need = live + extra;
+    if (c.Ccap && (need * 10 <= c.Ccap * 6 || (c.Ccap == kMax && need * 100 <= kMax * 85))) return;
+    if (need * 100 > kMax * 85 && c.Ccap && live) {
+        // the generation's pairs no longer fit 31-bit slots: flush the memo.  Callers
+        // reserve between sweeps, when no cache slot is referenced (rows, candidate
+        // lists and FindBest keys carry distances); within a generation distances are
+        // deterministic, so a flushed pair is re-scored to the same value.
+        NRG_CUDA(cudaMemsetAsync(c.Ckeys.p, 0xff, c.Ccap * 8, c.stream));
+        NRG_CUDA(cudaMemsetAsync(c.Ccount.p, 0, 8, c.stream));
+        c.sync();
+        c.cache_flushes += 1;
+        c.cache_live_host = live = 0;
+        need = extra;
+        if (need * 10 <= c.Ccap * 6 || (c.Ccap == kMax && need * 100 <= kMax * 85)) return;
+    }
+    const uint64_t ncap = std::max<uint64_t>(1u << 20, std::min<uint64_t>(next_pow2(2 * need), kMax));
+    if (need * 100 > ncap * 85) fail(100, "distance cache: one sweep needs more than 2^31 slots");
+    if (ncap == c.Ccap) return;
     DevBuf nk, nv;
     nk.ensure(ncap * 8);
     nv.ensure(ncap * 8);
