@@ -167,6 +167,131 @@ __global__ void __launch_bounds__(256, HW == 1 ? 4 : 3) ising_screen_kernel(Isin
     if (lane == 0 && counters) atomicAdd((unsigned long long*)&counters[C_EVALS], (unsigned long long)evals);
 }
 
+// K1 for short sample rows (Mw <= 16 words, e.g. M = 200 or 500): 32/G pairs per warp,
+// a group of G lanes per pair with one 32-sample word per lane, segmented butterfly
+// sums inside each group; otherwise the arithmetic, bound and outputs of
+// ising_screen_kernel.  Each warp takes 32 consecutive entries per chunk (indices
+// loaded lane-parallel) and scores them 32/G at a time.
+template <int G>
+__global__ void __launch_bounds__(256, 4) ising_screen_small_kernel(IsingSnap S, HashView W,
+                                                                    const int32_t* __restrict__ es,
+                                                                    const int32_t* __restrict__ ep, uint64_t n,
+                                                                    double lambda, double base, ScoreOut out,
+                                                                    uint64_t* __restrict__ surv,
+                                                                    float* __restrict__ surv_g,
+                                                                    uint8_t* __restrict__ surv_flag,
+                                                                    unsigned long long* __restrict__ nsurv,
+                                                                    uint64_t* counters) {
+    constexpr int P = 32 / G;  // pairs per step
+    const int lane = threadIdx.x & 31, grp = lane / G, r = lane % G;
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const bool word_ok = r < S.Mw;
+    uint32_t Ps[8], Xs[8], bs = 0;
+    int cur = -1;
+    float4 qs = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint64_t evals = 0;
+    const float err0 = 4.f * (float)S.M * 5.9604645e-08f;
+    const float lam = (float)lambda;
+    const double pruned_dist = -(base + 0.0);
+    for (uint64_t c0 = warp0 * 32; c0 < n; c0 += nwarps * 32) {
+        const int len = (int)min((uint64_t)32, n - c0);
+        const int li = lane < len ? lane : 0;
+        const int my_s = es[c0 + li], my_p = ep[c0 + li];
+        float my_g = 0.f;
+        int my_code = 0;
+        for (int k0 = 0; k0 < len; k0 += P) {
+            const int t = k0 + grp;  // this group's entry (offset in the chunk)
+            const bool live = t < len;
+            const int s = __shfl_sync(0xffffffffu, my_s, live ? t : 0);
+            const int p = __shfl_sync(0xffffffffu, my_p, live ? t : 0);
+            if (s != cur) {
+                if (word_ok) {
+                    const uint4* pp = reinterpret_cast<const uint4*>(S.P8 + ((size_t)s * S.Mw + r) * 8);
+                    const uint4 p0 = __ldg(pp), p1 = __ldg(pp + 1);
+                    Ps[0] = p0.x, Ps[1] = p0.y, Ps[2] = p0.z, Ps[3] = p0.w;
+                    Ps[4] = p1.x, Ps[5] = p1.y, Ps[6] = p1.z, Ps[7] = p1.w;
+                    bs = __ldg(&S.Xb[(size_t)s * S.Mw + r]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) Ps[j] = 0u;
+                    bs = 0u;
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) Xs[j] = pm1_bytes(bs >> (4 * j));
+                qs = __ldg(&S.Q8[s]);
+                cur = s;
+            }
+            uint4 t0 = make_uint4(0u, 0u, 0u, 0u), t1 = t0;
+            uint32_t bp = 0u;
+            if (word_ok) {
+                const uint4* tp = reinterpret_cast<const uint4*>(S.T8 + (size_t)p * S.Mp + 32 * r);
+                t0 = __ldg(tp);
+                t1 = __ldg(tp + 1);
+                bp = __ldg(&S.Xb[(size_t)p * S.Mw + r]);
+            }
+            const float4 qp = __ldg(&S.Q8[p]);
+            const double wcur = hash_get(W, pair_key(s, p), 0.0);
+            int l7 = 0;
+#pragma unroll
+            for (int j = 0; j < 7; ++j) l7 += __popc(Ps[j] & bp) << j;
+            const int a1 = l7 - (__popc(Ps[7] & bp) << 7);
+            const uint32_t tw[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+            int a2 = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a2 = __dp4a((int)tw[j], (int)Xs[j], a2);
+            int v = (a1 << 12) + __popc(bs ^ bp);
+#pragma unroll
+            for (int o = G / 2; o; o >>= 1) {
+                v += __shfl_xor_sync(0xffffffffu, v, o);
+                a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+            }
+            int code = 3;
+            float g = 0.f;
+            if (wcur == 0.0) {
+                const int dsum = v & 4095;
+                const int asum = (v - dsum) >> 12;
+                const float A = qs.x * (float)(2 * asum - __float_as_int(qs.z));
+                const float B = qp.x * (float)a2;
+                g = (float)(2 * (S.M - 2 * dsum)) - (A + B);
+                const float err = (qs.y + qp.y) * 1.0001f + err0;
+                code = fabsf(g) <= lam - err ? 0 : (fabsf(g) < lam + err ? 2 : 1);
+                if (live && r == 0) ++evals;
+            }
+            // hand each group's result to the lane that owns the entry
+            const int src = ((lane - k0) & (P - 1)) * G;
+            const float gg = __shfl_sync(0xffffffffu, g, src);
+            const int cc = __shfl_sync(0xffffffffu, code, src);
+            if (lane >= k0 && lane < k0 + P) {
+                my_g = gg;
+                my_code = cc;
+            }
+        }
+        const uint64_t e = c0 + lane;
+        if (lane < len && my_code == 0) {
+            if (out.cache_vals) out.cache_vals[out.slot[e]] = pruned_dist;
+            if (out.dist) out.dist[e] = pruned_dist;
+            if (out.w) out.w[e] = 0.0;
+            if (out.gain) out.gain[e] = 0.0;
+            if (out.warn) out.warn[e] = 0;
+        }
+        const unsigned sv = __ballot_sync(0xffffffffu, lane < len && my_code != 0);
+        if (sv) {
+            unsigned long long at = 0;
+            if (lane == 0) at = atomicAdd(nsurv, (unsigned long long)__popc(sv));
+            at = __shfl_sync(0xffffffffu, at, 0);
+            if ((sv >> lane) & 1u) {
+                const unsigned long long i = at + __popc(sv & ((1u << lane) - 1u));
+                surv[i] = e;
+                surv_g[i] = my_g;
+                surv_flag[i] = (uint8_t)(my_code == 1 ? 0 : (my_code == 2 ? 1 : 2));
+            }
+        }
+    }
+    evals = warp_sum((int)evals);
+    if (lane == 0 && counters && evals) atomicAdd((unsigned long long*)&counters[C_EVALS], (unsigned long long)evals);
+}
+
 // K2: survivors.  Certain survivors (w_cur = 0, |g0| > lambda + err) start Newton
 // from K1's fp32 g0 and the per-node sums Tsq = sum T^2 (second derivative at 0 is
 // -(2M - Tsq_a - Tsq_b)), so no pass is spent at w = 0; Newton then runs in fp32 on
@@ -353,10 +478,25 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
     ising_screen_kernel<Q><<<(unsigned)blocks, 256, 0, c.stream>>>(S, W, s, p, n, chunk, c.lambda, base, \
                                                                     out, surv, surv_g, surv_flag, nsurv,   \
                                                                     c.dcounters())
-        switch (HW) {
-            case 1: NRG_LAUNCH_MQ(1); break;
-            case 2: NRG_LAUNCH_MQ(2); break;
-            default: fail(100, "unsupported padded sample count");
+        const int G = c.Mw <= 4 ? 4 : (c.Mw <= 8 ? 8 : (c.Mw <= 16 ? 16 : 32));
+        if (G < 32 && !getenv("NRG_K1_WIDE")) {
+            const uint64_t sblocks = std::min<uint64_t>(ceil_div(n, 8 * 32), (uint64_t)sms * 16);
+#define NRG_LAUNCH_SMALL(GG)                                                                                 \
+    ising_screen_small_kernel<GG><<<(unsigned)sblocks, 256, 0, c.stream>>>(S, W, s, p, n, c.lambda, base, out, \
+                                                                         surv, surv_g, surv_flag, nsurv,     \
+                                                                         c.dcounters())
+            switch (G) {
+                case 4: NRG_LAUNCH_SMALL(4); break;
+                case 8: NRG_LAUNCH_SMALL(8); break;
+                default: NRG_LAUNCH_SMALL(16); break;
+            }
+#undef NRG_LAUNCH_SMALL
+        } else {
+            switch (HW) {
+                case 1: NRG_LAUNCH_MQ(1); break;
+                case 2: NRG_LAUNCH_MQ(2); break;
+                default: fail(100, "unsupported padded sample count");
+            }
         }
 #undef NRG_LAUNCH_MQ
         NRG_LAUNCH_CHECK();
