@@ -635,6 +635,20 @@ void cache_reserve(Context& c, uint64_t extra) {
 
 void begin_generation(Context& c) {
     if (c.Ccap) {
+        // size the (now empty) memo for the previous generation's pairs + 30%: growing
+        // here costs an allocation, growing mid-generation a rehash of every entry
+        uint64_t live = 0;
+        NRG_CUDA(cudaMemcpyAsync(&live, c.Ccount.p, 8, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        const uint64_t want = std::min<uint64_t>(live + live / 10 * 3, (1ull << 31) * 6 / 10);
+        if (want * 10 > c.Ccap * 6) {
+            const uint64_t ncap = std::min<uint64_t>(next_pow2(want * 10 / 6 + 1), 1ull << 31);
+            c.Ckeys = DevBuf();
+            c.Cvals = DevBuf();
+            c.Ckeys.ensure(ncap * 8);
+            c.Cvals.ensure(ncap * 8);
+            c.Ccap = ncap;
+        }
         NRG_CUDA(cudaMemsetAsync(c.Ckeys.p, 0xff, c.Ccap * 8, c.stream));
         NRG_CUDA(cudaMemsetAsync(c.Ccount.p, 0, 8, c.stream));
     }
