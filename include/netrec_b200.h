@@ -236,6 +236,24 @@ int nrg_generate_ising_graph(nrg_ctx* ctx, uint64_t n_edges, const int32_t* ei, 
 int nrg_generate_gaussian(nrg_ctx* ctx, int32_t degree, double amp, int32_t burn_in, int32_t thin, uint64_t seed,
                           double* X_out);
 
+/* Binary sample / state files (the fast replacement for the text
+ * formats of inc/io.hpp:36-115).  Samples: "NRGSMP01", u32 kind (0 Ising bit-packed,
+ * 1 Gaussian f64), u32 0, u64 n, u64 m, data.  State: "NRGSTA01", u64 n, u64 n_edges,
+ * theta[n] f64, n_edges x {i32 i, i32 j, f64 w}.  Host-only functions need no GPU;
+ * nrg_load_* / nrg_save_* move a file into / out of a context (load_state = empty state,
+ * theta, then the edges as set_edge calls). */
+int nrg_write_samples_file(const char* path, int32_t n, int32_t m, int32_t kind, const double* X);
+int nrg_read_samples_info(const char* path, int32_t* n, int32_t* m, int32_t* kind);
+int nrg_read_samples_file(const char* path, double* X);
+int nrg_load_samples_file(nrg_ctx* ctx, const char* path);
+int nrg_save_samples_file(nrg_ctx* ctx, const char* path);
+int nrg_write_state_file(const char* path, int32_t n, const double* theta, uint64_t n_edges, const int32_t* ei,
+                         const int32_t* ej, const double* w);
+int nrg_read_state_info(const char* path, int32_t* n, uint64_t* n_edges);
+int nrg_read_state_file(const char* path, double* theta, int32_t* ei, int32_t* ej, double* w);
+int nrg_load_state_file(nrg_ctx* ctx, const char* path);
+int nrg_save_state_file(nrg_ctx* ctx, const char* path);
+
 /* Multi-GPU: samples, sums, W and theta replicated (updates and theta
  * passes run identically on every rank); NNDescent nodes sharded by contiguous ranges;
  * the per-generation distance cache sharded by pair key, so each unique pair is scored

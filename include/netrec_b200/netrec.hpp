@@ -710,6 +710,47 @@ inline ReconstructionResult reconstruct_gcd(PseudoLikelihood& model, const Recon
     return res;
 }
 
+/// Binary sample / state files: the fast counterparts of the text
+/// formats in inc/io.hpp (samples_to_text / weights_to_text and their readers).
+inline void write_samples_binary(const std::string& path, const SampleMatrix& X, bool ising) {
+    detail::check(nrg_write_samples_file(path.c_str(), X.num_nodes(), X.num_samples(), ising ? 0 : 1, X.data()));
+}
+inline SampleMatrix read_samples_binary(const std::string& path) {
+    int32_t n = 0, m = 0, kind = 0;
+    detail::check(nrg_read_samples_info(path.c_str(), &n, &m, &kind));
+    std::vector<double> v(static_cast<std::size_t>(n) * static_cast<std::size_t>(m));
+    detail::check(nrg_read_samples_file(path.c_str(), v.data()));
+    SampleMatrix X(n, m);
+    for (NodeId i = 0; i < n; ++i)
+        for (int t = 0; t < m; ++t) X.set(i, t, v[static_cast<std::size_t>(i) * m + t]);
+    return X;
+}
+inline void write_weights_binary(const std::string& path, const SparseWeights& W) {
+    const NodeId n = W.num_nodes();
+    std::vector<double> th(static_cast<std::size_t>(n)), w;
+    std::vector<int32_t> ei, ej;
+    for (NodeId i = 0; i < n; ++i) th[static_cast<std::size_t>(i)] = W.theta(i);
+    W.for_each_edge([&](NodeId i, NodeId j, double v) {
+        ei.push_back(i);
+        ej.push_back(j);
+        w.push_back(v);
+    });
+    detail::check(nrg_write_state_file(path.c_str(), n, th.data(), ei.size(), ei.data(), ej.data(), w.data()));
+}
+/// rebuilds the sums against X (set_edge per stored coupling, inc/sparse_weights.hpp:54-85)
+inline SparseWeights read_weights_binary(const std::string& path, const SampleMatrix& X) {
+    int32_t n = 0;
+    uint64_t ne = 0;
+    detail::check(nrg_read_state_info(path.c_str(), &n, &ne));
+    std::vector<double> th(static_cast<std::size_t>(n)), w(ne + 1);
+    std::vector<int32_t> ei(ne + 1), ej(ne + 1);
+    detail::check(nrg_read_state_file(path.c_str(), th.data(), ei.data(), ej.data(), w.data()));
+    SparseWeights W(n, X.num_samples());
+    for (NodeId i = 0; i < n; ++i) W.set_theta(i, th[static_cast<std::size_t>(i)]);
+    for (uint64_t e = 0; e < ne; ++e) W.set_edge(ei[e], ej[e], w[e], X);
+    return W;
+}
+
 /// reconstruct_cd (inc/reconstruct.hpp:185-207) on the device
 inline ReconstructionResult reconstruct_cd(PseudoLikelihood& model, double eps = -1.0, int max_iters = 1000,
                                            int threads = 1) {

@@ -93,6 +93,16 @@ SIGNATURES = {
     "nrg_generate_ising_powerlaw": (C.c_int, [_P, _d, _i32, _d, _d, _i32, _i32, _u64, _VP]),
     "nrg_generate_ising_graph": (C.c_int, [_P, _u64, _I32P, _I32P, _F64P, _F64P, _i32, _i32, _u64, _VP]),
     "nrg_generate_gaussian": (C.c_int, [_P, _i32, _d, _i32, _i32, _u64, _VP]),
+    "nrg_write_samples_file": (C.c_int, [C.c_char_p, _i32, _i32, _i32, _F64P]),
+    "nrg_read_samples_info": (C.c_int, [C.c_char_p, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32)]),
+    "nrg_read_samples_file": (C.c_int, [C.c_char_p, _F64P]),
+    "nrg_load_samples_file": (C.c_int, [_P, C.c_char_p]),
+    "nrg_save_samples_file": (C.c_int, [_P, C.c_char_p]),
+    "nrg_write_state_file": (C.c_int, [C.c_char_p, _i32, _F64P, _u64, _I32P, _I32P, _F64P]),
+    "nrg_read_state_info": (C.c_int, [C.c_char_p, C.POINTER(_i32), C.POINTER(_u64)]),
+    "nrg_read_state_file": (C.c_int, [C.c_char_p, _F64P, _I32P, _I32P, _F64P]),
+    "nrg_load_state_file": (C.c_int, [_P, C.c_char_p]),
+    "nrg_save_state_file": (C.c_int, [_P, C.c_char_p]),
     "nrg_comm_unique_id": (C.c_int, [C.c_char_p]),
     "nrg_comm_init": (C.c_int, [_P, C.c_char_p, _i32, _i32]),
     "nrg_loopback_create": (C.c_int, [_i32, C.POINTER(_VP)]),
@@ -135,6 +145,35 @@ def _i32a(a):
 
 def _f64a(a):
     return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def write_samples_file(path, X, kind=0):
+    """Binary sample file (bit-packed +-1 for kind 0, f64 for kind 1)."""
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    check(load().nrg_write_samples_file(str(path).encode(), X.shape[0], X.shape[1], kind, X))
+
+
+def read_samples_file(path):
+    n, m, k = _i32(), _i32(), _i32()
+    check(load().nrg_read_samples_info(str(path).encode(), C.byref(n), C.byref(m), C.byref(k)))
+    X = np.zeros((n.value, m.value))
+    check(load().nrg_read_samples_file(str(path).encode(), X))
+    return X, k.value
+
+
+def write_state_file(path, theta, ei, ej, w):
+    theta, ei, ej, w = _f64a(theta), _i32a(ei), _i32a(ej), _f64a(w)
+    check(load().nrg_write_state_file(str(path).encode(), len(theta), theta, len(ei), ei, ej, w))
+
+
+def read_state_file(path):
+    n, ne = _i32(), _u64()
+    check(load().nrg_read_state_info(str(path).encode(), C.byref(n), C.byref(ne)))
+    th = np.zeros(n.value)
+    k = ne.value
+    ei, ej, w = np.zeros(max(k, 1), np.int32), np.zeros(max(k, 1), np.int32), np.zeros(max(k, 1))
+    check(load().nrg_read_state_file(str(path).encode(), th, ei, ej, w))
+    return th, ei[:k], ej[:k], w[:k]
 
 
 class Model:
@@ -204,6 +243,18 @@ class Model:
         check(self.L.nrg_generate_gaussian(self.h, degree, amp, burn_in, thin, seed,
                                            out.ctypes.data if out is not None else None))
         return out
+
+    def load_samples_file(self, path):
+        check(self.L.nrg_load_samples_file(self.h, str(path).encode()))
+
+    def save_samples_file(self, path):
+        check(self.L.nrg_save_samples_file(self.h, str(path).encode()))
+
+    def load_state_file(self, path):
+        check(self.L.nrg_load_state_file(self.h, str(path).encode()))
+
+    def save_state_file(self, path):
+        check(self.L.nrg_save_state_file(self.h, str(path).encode()))
 
     def reset_state(self):
         check(self.L.nrg_reset_state(self.h))

@@ -528,6 +528,81 @@ int nrg_generate_gaussian(nrg_ctx* x, int32_t degree, double amp, int32_t burn_i
     });
 }
 
+int nrg_write_samples_file(const char* path, int32_t n, int32_t m, int32_t kind, const double* X) {
+    return guard([&] {
+        if (n < 1 || m < 0) nrg::fail(22, "bad shape");
+        nrg::write_samples_file(path, (uint64_t)n, (uint64_t)m, kind, X);
+    });
+}
+int nrg_read_samples_info(const char* path, int32_t* n, int32_t* m, int32_t* kind) {
+    return guard([&] {
+        uint64_t nn = 0, mm = 0;
+        int k = 0;
+        nrg::read_samples_info(path, &nn, &mm, &k);
+        *n = (int32_t)nn;
+        *m = (int32_t)mm;
+        *kind = k;
+    });
+}
+int nrg_read_samples_file(const char* path, double* X) {
+    return guard([&] { nrg::read_samples_file(path, X); });
+}
+int nrg_load_samples_file(nrg_ctx* x, const char* path) {
+    return guardx(x, [&] { nrg::load_samples_file(x->c, path); });
+}
+int nrg_save_samples_file(nrg_ctx* x, const char* path) {
+    return guardx(x, [&] { nrg::save_samples_file(x->c, path); });
+}
+int nrg_write_state_file(const char* path, int32_t n, const double* theta, uint64_t n_edges, const int32_t* ei,
+                         const int32_t* ej, const double* w) {
+    return guard([&] {
+        if (n < 1) nrg::fail(22, "bad shape");
+        nrg::write_state_file(path, (uint64_t)n, theta, n_edges, ei, ej, w);
+    });
+}
+int nrg_read_state_info(const char* path, int32_t* n, uint64_t* n_edges) {
+    return guard([&] {
+        uint64_t nn = 0;
+        nrg::read_state_info(path, &nn, n_edges);
+        *n = (int32_t)nn;
+    });
+}
+int nrg_read_state_file(const char* path, double* theta, int32_t* ei, int32_t* ej, double* w) {
+    return guard([&] { nrg::read_state_file(path, theta, ei, ej, w); });
+}
+int nrg_load_state_file(nrg_ctx* x, const char* path) {
+    return guardx(x, [&] {
+        need_samples(x);
+        uint64_t n = 0, ne = 0;
+        nrg::read_state_info(path, &n, &ne);
+        if (n != (uint64_t)x->c.n) nrg::fail(22, "state file size does not match the context");
+        std::vector<double> th(n), w(ne);
+        std::vector<int32_t> ei(ne), ej(ne);
+        nrg::read_state_file(path, th.data(), ei.data(), ej.data(), w.data());
+        check_pairs(x, ne, ei.data(), ej.data());
+        nrg::reset_state_empty(x->c);
+        nrg::set_theta(x->c, th.data());
+        if (ne) {
+            int32_t* di = to_dev(x, x->q_i, ei.data(), ne);
+            int32_t* dj = to_dev(x, x->q_j, ej.data(), ne);
+            double* dw = to_dev(x, x->q_d, w.data(), ne);
+            nrg::apply_updates(x->c, di, dj, ne, dw);
+        }
+    });
+}
+int nrg_save_state_file(nrg_ctx* x, const char* path) {
+    return guardx(x, [&] {
+        nrg::Context& c = x->c;
+        std::vector<double> th(c.n);
+        uint64_t ne = 0;
+        nrg::get_state(c, th.data(), 0, nullptr, nullptr, nullptr, &ne);
+        std::vector<int32_t> ei(ne + 1), ej(ne + 1);
+        std::vector<double> w(ne + 1);
+        nrg::get_state(c, th.data(), ne, ei.data(), ej.data(), w.data(), &ne);
+        nrg::write_state_file(path, (uint64_t)c.n, th.data(), ne, ei.data(), ej.data(), w.data());
+    });
+}
+
 int nrg_comm_unique_id(uint8_t id[128]) {
     return guard([&] { nrg::nccl_unique_id(id); });
 }

@@ -250,6 +250,16 @@ void upload_samples_f64(Context& c, const double* X);
 void upload_spins_i8(Context& c, const int8_t* X);
 void set_theta(Context& c, const double* th);
 void reset_state_empty(Context& c);
+// ---- io.cu (binary sample / state files)
+void write_samples_file(const char* path, uint64_t n, uint64_t m, int kind, const double* X);
+void read_samples_info(const char* path, uint64_t* n, uint64_t* m, int* kind);
+void read_samples_file(const char* path, double* X);
+void load_samples_file(Context& c, const char* path);
+void save_samples_file(Context& c, const char* path);
+void write_state_file(const char* path, uint64_t n, const double* theta, uint64_t ne, const int32_t* ei,
+                      const int32_t* ej, const double* w);
+void read_state_info(const char* path, uint64_t* n, uint64_t* ne);
+void read_state_file(const char* path, double* theta, int32_t* ei, int32_t* ej, double* w);
 void w_reserve(Context& c, uint64_t extra);
 void get_state(Context& c, double* theta, uint64_t cap, int32_t* ei, int32_t* ej, double* w,
                uint64_t* n_edges);

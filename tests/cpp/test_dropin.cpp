@@ -135,6 +135,32 @@ int main() {
         std::printf("ok   reconstruct_gcd: %zu iterations, %zu edges, chain recall %.3f\n", res.trace.iterations.size(),
                     w.edge_count(), chain / double(n - 1));
     }
+    {  // binary sample / weight files and reconstruct_cd
+        const int n = 40, M = 64;
+        SampleMatrix x(n, M);
+        for (int i = 0; i < n; ++i)
+            for (int m = 0; m < M; ++m) x.set(i, m, ((i * 7 + m * 3 + i * m) % 5) < 2 ? 1.0 : -1.0);
+        SparseWeights w(n, M);
+        w.set_edge(1, 5, 0.25, x);
+        w.set_edge(7, 3, -0.5, x);
+        w.set_theta(2, 0.125);
+        const std::string sp = "/tmp/nrg_dropin_samples.bin", wp = "/tmp/nrg_dropin_weights.bin";
+        write_samples_binary(sp, x, true);
+        write_weights_binary(wp, w);
+        const SampleMatrix y = read_samples_binary(sp);
+        SparseWeights v = read_weights_binary(wp, y);
+        bool same = y.num_nodes() == n && y.num_samples() == M;
+        for (int i = 0; i < n && same; ++i)
+            for (int m = 0; m < M; ++m) same = same && y.row(i)[m] == x.row(i)[m];
+        CHECK(same);
+        CHECK(v.edge_count() == 2 && v.weight(1, 5) == 0.25 && v.weight(3, 7) == -0.5 && v.theta(2) == 0.125);
+        for (int i = 0; i < n; ++i)
+            for (int m = 0; m < M; ++m) CHECK(v.sums_row(i)[m] == w.sums_row(i)[m]);
+        PseudoLikelihood model(ModelKind::ising, 10.0, y, v);
+        const ReconstructionResult r = reconstruct_cd(model, -1.0, 5);
+        CHECK(!r.trace.iterations.empty() && r.trace.iterations[0].candidates == static_cast<std::size_t>(n * (n - 1) / 2));
+        std::printf("ok   binary sample/weight files round-trip; reconstruct_cd %zu sweeps\n", r.trace.iterations.size());
+    }
     {  // exception types (inc/model.hpp:115-123, inc/knn.hpp:153-155)
         SampleMatrix x(4, 3);
         SparseWeights w(4, 3);
