@@ -235,6 +235,12 @@ int nrg_generate_ising_graph(nrg_ctx* ctx, uint64_t n_edges, const int32_t* ei, 
  * stationary law of a sparse-Cholesky draw); optionally copied out (X_out, N x M). */
 int nrg_generate_gaussian(nrg_ctx* ctx, int32_t degree, double amp, int32_t burn_in, int32_t thin, uint64_t seed,
                           double* X_out);
+/* Gaussian samples for a caller-supplied precision matrix: off-diagonal entries kij on
+ * distinct edges (ei, ej), diagonal kdiag[N] > 0 (sample_gaussian, inc/synth.hpp:95-124,
+ * draws the same law by sparse Cholesky). */
+int nrg_generate_gaussian_graph(nrg_ctx* ctx, uint64_t n_edges, const int32_t* ei, const int32_t* ej,
+                                const double* kij, const double* kdiag, int32_t burn_in, int32_t thin, uint64_t seed,
+                                double* X_out);
 
 /* Binary sample / state files (the fast replacement for the text
  * formats of inc/io.hpp:36-115).  Samples: "NRGSMP01", u32 kind (0 Ising bit-packed,

@@ -93,6 +93,7 @@ SIGNATURES = {
     "nrg_generate_ising_powerlaw": (C.c_int, [_P, _d, _i32, _d, _d, _i32, _i32, _u64, _VP]),
     "nrg_generate_ising_graph": (C.c_int, [_P, _u64, _I32P, _I32P, _F64P, _F64P, _i32, _i32, _u64, _VP]),
     "nrg_generate_gaussian": (C.c_int, [_P, _i32, _d, _i32, _i32, _u64, _VP]),
+    "nrg_generate_gaussian_graph": (C.c_int, [_P, _u64, _I32P, _I32P, _F64P, _F64P, _i32, _i32, _u64, _VP]),
     "nrg_write_samples_file": (C.c_int, [C.c_char_p, _i32, _i32, _i32, _F64P]),
     "nrg_read_samples_info": (C.c_int, [C.c_char_p, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32)]),
     "nrg_read_samples_file": (C.c_int, [C.c_char_p, _F64P]),
@@ -236,6 +237,13 @@ class Model:
         out = np.zeros((self.n, self.M), np.int8) if want_samples else None
         check(self.L.nrg_generate_ising_graph(self.h, len(ei), ei, ej, w, theta, burn_in, thin, seed,
                                               out.ctypes.data if out is not None else None))
+        return out
+
+    def generate_gaussian_graph(self, ei, ej, kij, kdiag, burn_in=1000, thin=10, seed=0, want_samples=False):
+        ei, ej, kij, kdiag = _i32a(ei), _i32a(ej), _f64a(kij), _f64a(kdiag)
+        out = np.zeros((self.n, self.M)) if want_samples else None
+        check(self.L.nrg_generate_gaussian_graph(self.h, len(ei), ei, ej, kij, kdiag, burn_in, thin, seed,
+                                                 out.ctypes.data if out is not None else None))
         return out
 
     def generate_gaussian(self, degree=4, amp=0.2, burn_in=1000, thin=10, seed=0, want_samples=False):

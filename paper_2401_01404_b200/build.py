@@ -75,20 +75,21 @@ def build_lib(verbose: bool = False, jobs: int | None = None) -> Path:
 
 
 def build_cpp_tests(verbose: bool = False) -> Path:
-    """tests/cpp/test_dropin.cpp against include/netrec_b200/netrec.hpp + the library."""
-    src = ROOT / "tests" / "cpp" / "test_dropin.cpp"
-    out = PKG / "test_dropin"
-    deps = [src, LIB, ROOT / "include" / "netrec_b200" / "netrec.hpp", ROOT / "include" / "netrec_b200.h"]
-    if _stale(out, deps):
-        cmd = ["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", str(src), f"-L{PKG}", "-lnetrec_b200",
-               "-Wl,-rpath,$ORIGIN", "-o", str(out)]
-        if verbose:
-            print(" ".join(cmd), flush=True)
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError("C++ drop-in test build failed")
-    return out
+    """tests/cpp/*.cpp (the drop-in program and the harness program) against
+    include/netrec_b200/*.hpp + the library; returns the drop-in test binary."""
+    hdrs = sorted((ROOT / "include" / "netrec_b200").glob("*.hpp")) + [ROOT / "include" / "netrec_b200.h"]
+    for src in sorted((ROOT / "tests" / "cpp").glob("*.cpp")):
+        out = PKG / src.stem
+        if _stale(out, [src, LIB] + hdrs):
+            cmd = ["g++", "-std=c++20", "-O2", f"-I{ROOT / 'include'}", str(src), f"-L{PKG}", "-lnetrec_b200",
+                   "-Wl,-rpath,$ORIGIN", "-o", str(out)]
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            if r.returncode != 0:
+                sys.stderr.write(r.stdout + r.stderr)
+                raise RuntimeError(f"C++ test build failed: {src.name}")
+    return PKG / "test_dropin"
 
 
 def build_oracle(verbose: bool = False) -> None:

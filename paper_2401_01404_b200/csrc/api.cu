@@ -477,6 +477,19 @@ int nrg_recall_curve(uint64_t m, const nrg_pair* exact, const nrg_pair* approx, 
     });
 }
 
+int nrg_generate_gaussian_graph(nrg_ctx* x, uint64_t n_edges, const int32_t* ei, const int32_t* ej, const double* kij,
+                                const double* kdiag, int32_t burn_in, int32_t thin, uint64_t seed, double* X_out) {
+    return guardx(x, [&] {
+        nrg::generate_gaussian_graph(x->c, n_edges, ei, ej, kij, kdiag, burn_in, thin, seed);
+        if (X_out) {
+            nrg::Context& c = x->c;
+            NRG_CUDA(cudaMemcpy2DAsync(X_out, (size_t)c.M * 8, c.Xd.p, (size_t)c.Mp * 8, (size_t)c.M * 8, c.n,
+                                       cudaMemcpyDeviceToHost, c.stream));
+            c.sync();
+        }
+    });
+}
+
 namespace {
 // the bit-packed samples as int8 on the host
 void unpack_spins(nrg_ctx* x, int8_t* X_out) {

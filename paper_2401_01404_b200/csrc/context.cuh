@@ -344,5 +344,7 @@ void generate_ising_powerlaw(Context& c, double gamma, int dmin, double w_sigma,
 void generate_ising_graph(Context& c, uint64_t ne, const int32_t* ei, const int32_t* ej, const double* w,
                           const double* theta, int burn_in, int thin, uint64_t seed);
 void generate_gaussian(Context& c, int degree, double amp, int burn_in, int thin, uint64_t seed);
+void generate_gaussian_graph(Context& c, uint64_t ne, const int32_t* ei, const int32_t* ej, const double* kij,
+                             const double* kdiag, int burn_in, int thin, uint64_t seed);
 
 }  // namespace nrg

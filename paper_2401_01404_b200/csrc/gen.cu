@@ -351,6 +351,58 @@ void generate_ising_graph(Context& c, uint64_t ne, const int32_t* ei, const int3
     gibbs_ising(c, ea, eb, ew, th, burn_in, thin, seed);
 }
 
+// The coloured Gaussian chain on precision K (off-diagonals ew on edges ea-eb,
+// diagonal kd); samples into Xd, then the empty Gaussian state (theta = row RMS).
+static void gauss_chain(Context& c, const std::vector<int32_t>& ea, const std::vector<int32_t>& eb,
+                        const std::vector<double>& ew, const std::vector<double>& kd, int burn_in, int thin,
+                        uint64_t seed) {
+    const int n = c.n;
+    const ColoredGraph G = build_colored(n, ea, eb, ew);
+    DevGraph D(c, G, kd);
+    DevBuf dxs, dbar;
+    double* xs = dxs.as<double>(n);
+    NRG_CUDA(cudaMemsetAsync(xs, 0, (size_t)n * 8, c.stream));
+    c.Xd.ensure((size_t)n * c.Mp * 8);
+    NRG_CUDA(cudaMemsetAsync(c.Xd.p, 0, (size_t)n * c.Mp * 8, c.stream));
+    unsigned* bar = dbar.as<unsigned>(2);
+    NRG_CUDA(cudaMemsetAsync(bar, 0, 8, c.stream));
+    int per = 0, sms = 0;
+    NRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gauss_gibbs_kernel, 256, 0));
+    NRG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+    int grid = std::max(1, std::min(per * sms, (n + 255) / 256));
+    uint64_t key = mix64(seed, 2);
+    int64_t sweeps = (int64_t)burn_in + (int64_t)c.M * thin;
+    int ncol = G.ncol, M = c.M, Mp = c.Mp, nn = n;
+    double* xd = c.dXd();
+    void* args[] = {&D.d_mem, &D.d_cstart, &ncol, &D.d_off, &D.d_nbr, &D.d_nw, &D.d_th, &xs, &key, &sweeps,
+                    &burn_in, &thin, &M, &Mp, &nn, &xd, &bar};
+    NRG_CUDA(cudaLaunchCooperativeKernel((void*)gauss_gibbs_kernel, grid, 256, args, 0, c.stream));
+    NRG_LAUNCH_CHECK();
+    c.sync();
+    c.have_samples = true;
+    reset_state_empty(c);  // make_empty_state: theta = row RMS, W empty, sums 0
+}
+
+// Gaussian samples for a caller-supplied precision matrix (distinct off-diagonal edges,
+// positive diagonal) — SURVEY §8f row 2; sample_gaussian (inc/synth.hpp:95-124) draws
+// the same law by sparse Cholesky.
+void generate_gaussian_graph(Context& c, uint64_t ne, const int32_t* ei, const int32_t* ej, const double* kij,
+                             const double* kdiag, int burn_in, int thin, uint64_t seed) {
+    if (c.kind != GAUSSIAN) fail(22, "generate_gaussian_graph needs a gaussian context");
+    if (burn_in < 0 || thin < 1) fail(22, "generate_gaussian_graph: bad Gibbs params");
+    std::vector<int32_t> ea(ne), eb(ne);
+    std::vector<double> ew(kij, kij + ne), kd(kdiag, kdiag + c.n);
+    for (uint64_t e = 0; e < ne; ++e) {
+        if (ei[e] < 0 || ej[e] < 0 || ei[e] >= c.n || ej[e] >= c.n) fail(34, "generate_gaussian_graph: node id out of range");
+        if (ei[e] == ej[e]) fail(22, "generate_gaussian_graph: diagonal entries go in kdiag");
+        ea[e] = std::min(ei[e], ej[e]);
+        eb[e] = std::max(ei[e], ej[e]);
+    }
+    for (int i = 0; i < c.n; ++i)
+        if (!(kd[i] > 0.0)) fail(22, "generate_gaussian_graph: the diagonal must be positive");
+    gauss_chain(c, ea, eb, ew, kd, burn_in, thin, seed);
+}
+
 // Config 3: random d-regular graph (pairing model, resampled until simple), precision
 // off-diagonals K_ij ~ U(-amp, amp), diagonal K_ii = sum_j |K_ij| + 0.5 (diagonally
 // dominant), samples by the coloured Gibbs chain (the stationary law of the spec's sparse
@@ -391,30 +443,7 @@ void generate_gaussian(Context& c, int degree, double amp, int burn_in, int thin
         kd[ea.back()] += std::fabs(v);
         kd[eb.back()] += std::fabs(v);
     }
-    const ColoredGraph G = build_colored(n, ea, eb, ew);
-    DevGraph D(c, G, kd);
-    DevBuf dxs, dbar;
-    double* xs = dxs.as<double>(n);
-    NRG_CUDA(cudaMemsetAsync(xs, 0, (size_t)n * 8, c.stream));
-    c.Xd.ensure((size_t)n * c.Mp * 8);
-    NRG_CUDA(cudaMemsetAsync(c.Xd.p, 0, (size_t)n * c.Mp * 8, c.stream));
-    unsigned* bar = dbar.as<unsigned>(2);
-    NRG_CUDA(cudaMemsetAsync(bar, 0, 8, c.stream));
-    int per = 0, sms = 0;
-    NRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gauss_gibbs_kernel, 256, 0));
-    NRG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
-    int grid = std::max(1, std::min(per * sms, (n + 255) / 256));
-    uint64_t key = mix64(seed, 2);
-    int64_t sweeps = (int64_t)burn_in + (int64_t)c.M * thin;
-    int ncol = G.ncol, M = c.M, Mp = c.Mp, nn = n;
-    double* xd = c.dXd();
-    void* args[] = {&D.d_mem, &D.d_cstart, &ncol, &D.d_off, &D.d_nbr, &D.d_nw, &D.d_th, &xs, &key, &sweeps,
-                    &burn_in, &thin, &M, &Mp, &nn, &xd, &bar};
-    NRG_CUDA(cudaLaunchCooperativeKernel((void*)gauss_gibbs_kernel, grid, 256, args, 0, c.stream));
-    NRG_LAUNCH_CHECK();
-    c.sync();
-    c.have_samples = true;
-    reset_state_empty(c);  // make_empty_state: theta = row RMS, W empty, sums 0
+    gauss_chain(c, ea, eb, ew, kd, burn_in, thin, seed);
 }
 
 }  // namespace nrg

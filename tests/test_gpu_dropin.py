@@ -1,5 +1,6 @@
 """The drop-in C++ API (include/netrec_b200/netrec.hpp) exercised by a C++ program
-written like the reference's own tests (tests/cpp/test_dropin.cpp)."""
+written like the reference's own tests (tests/cpp/test_dropin.cpp), and the experiment
+harness (include/netrec_b200/bench.hpp, mirroring inc/bench.hpp) by tests/cpp/test_harness.cpp."""
 from __future__ import annotations
 
 import subprocess
@@ -17,6 +18,18 @@ def test_cpp_dropin_program():
         from paper_2401_01404_b200 import build
         build.build_cpp_tests()
     r = subprocess.run([str(BIN)], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "PASSED" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_harness_program():
+    exe = ROOT / "paper_2401_01404_b200" / "test_harness"
+    if not exe.exists():
+        from paper_2401_01404_b200 import build
+        build.build_cpp_tests()
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=900)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "PASSED" in r.stdout
