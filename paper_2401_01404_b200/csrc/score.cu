@@ -167,13 +167,14 @@ __global__ void __launch_bounds__(256, HW == 1 ? 4 : 3) ising_screen_kernel(Isin
     if (lane == 0 && counters) atomicAdd((unsigned long long*)&counters[C_EVALS], (unsigned long long)evals);
 }
 
-// K1 for short sample rows (Mw <= 16 words, e.g. M = 200 or 500): 32/G pairs per warp,
-// a group of G lanes per pair with one 32-sample word per lane, segmented butterfly
-// sums inside each group; otherwise the arithmetic, bound and outputs of
-// ising_screen_kernel.  Each warp takes 32 consecutive entries per chunk (indices
-// loaded lane-parallel) and scores them 32/G at a time.
-template <int G>
-__global__ void __launch_bounds__(256, 4) ising_screen_small_kernel(IsingSnap S, HashView W,
+// K1 with several pairs per warp: 32/G pairs at a time, a group of G lanes per pair with
+// WPL 32-sample words per lane (word r + G q), segmented butterfly sums inside each
+// group; otherwise the arithmetic, bound and outputs of ising_screen_kernel.  Short rows
+// (Mw <= 16) need it to keep every lane busy; longer rows use it to share the per-pair
+// overhead (indices, coupling probe, decision, outputs) between pairs.  Each warp takes
+// 32 consecutive entries per chunk (indices loaded lane-parallel).
+template <int G, int WPL>
+__global__ void __launch_bounds__(256, WPL == 1 ? 4 : 3) ising_screen_small_kernel(IsingSnap S, HashView W,
                                                                     const int32_t* __restrict__ es,
                                                                     const int32_t* __restrict__ ep, uint64_t n,
                                                                     double lambda, double base, ScoreOut out,
@@ -186,8 +187,7 @@ __global__ void __launch_bounds__(256, 4) ising_screen_small_kernel(IsingSnap S,
     const int lane = threadIdx.x & 31, grp = lane / G, r = lane % G;
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const bool word_ok = r < S.Mw;
-    uint32_t Ps[8], Xs[8], bs = 0;
+    uint32_t Ps[WPL][8], Xs[WPL][8], bs[WPL];
     int cur = -1;
     float4 qs = make_float4(0.f, 0.f, 0.f, 0.f);
     uint64_t evals = 0;
@@ -206,41 +206,55 @@ __global__ void __launch_bounds__(256, 4) ising_screen_small_kernel(IsingSnap S,
             const int s = __shfl_sync(0xffffffffu, my_s, live ? t : 0);
             const int p = __shfl_sync(0xffffffffu, my_p, live ? t : 0);
             if (s != cur) {
-                if (word_ok) {
-                    const uint4* pp = reinterpret_cast<const uint4*>(S.P8 + ((size_t)s * S.Mw + r) * 8);
-                    const uint4 p0 = __ldg(pp), p1 = __ldg(pp + 1);
-                    Ps[0] = p0.x, Ps[1] = p0.y, Ps[2] = p0.z, Ps[3] = p0.w;
-                    Ps[4] = p1.x, Ps[5] = p1.y, Ps[6] = p1.z, Ps[7] = p1.w;
-                    bs = __ldg(&S.Xb[(size_t)s * S.Mw + r]);
-                } else {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) Ps[j] = 0u;
-                    bs = 0u;
+                for (int q = 0; q < WPL; ++q) {
+                    const int w = r + G * q;  // word of this lane
+                    if (w < S.Mw) {
+                        const uint4* pp = reinterpret_cast<const uint4*>(S.P8 + ((size_t)s * S.Mw + w) * 8);
+                        const uint4 p0 = __ldg(pp), p1 = __ldg(pp + 1);
+                        Ps[q][0] = p0.x, Ps[q][1] = p0.y, Ps[q][2] = p0.z, Ps[q][3] = p0.w;
+                        Ps[q][4] = p1.x, Ps[q][5] = p1.y, Ps[q][6] = p1.z, Ps[q][7] = p1.w;
+                        bs[q] = __ldg(&S.Xb[(size_t)s * S.Mw + w]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) Ps[q][j] = 0u;
+                        bs[q] = 0u;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) Xs[q][j] = pm1_bytes(bs[q] >> (4 * j));
                 }
-#pragma unroll
-                for (int j = 0; j < 8; ++j) Xs[j] = pm1_bytes(bs >> (4 * j));
                 qs = __ldg(&S.Q8[s]);
                 cur = s;
             }
-            uint4 t0 = make_uint4(0u, 0u, 0u, 0u), t1 = t0;
-            uint32_t bp = 0u;
-            if (word_ok) {
-                const uint4* tp = reinterpret_cast<const uint4*>(S.T8 + (size_t)p * S.Mp + 32 * r);
-                t0 = __ldg(tp);
-                t1 = __ldg(tp + 1);
-                bp = __ldg(&S.Xb[(size_t)p * S.Mw + r]);
+            uint4 t0[WPL], t1[WPL];
+            uint32_t bp[WPL];
+#pragma unroll
+            for (int q = 0; q < WPL; ++q) {
+                const int w = r + G * q;
+                t0[q] = t1[q] = make_uint4(0u, 0u, 0u, 0u);
+                bp[q] = 0u;
+                if (w < S.Mw) {
+                    const uint4* tp = reinterpret_cast<const uint4*>(S.T8 + (size_t)p * S.Mp + 32 * w);
+                    t0[q] = __ldg(tp);
+                    t1[q] = __ldg(tp + 1);
+                    bp[q] = __ldg(&S.Xb[(size_t)p * S.Mw + w]);
+                }
             }
             const float4 qp = __ldg(&S.Q8[p]);
             const double wcur = hash_get(W, pair_key(s, p), 0.0);
-            int l7 = 0;
+            int a1 = 0, a2 = 0, diff = 0;
 #pragma unroll
-            for (int j = 0; j < 7; ++j) l7 += __popc(Ps[j] & bp) << j;
-            const int a1 = l7 - (__popc(Ps[7] & bp) << 7);
-            const uint32_t tw[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
-            int a2 = 0;
+            for (int q = 0; q < WPL; ++q) {
+                int l7 = 0;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) a2 = __dp4a((int)tw[j], (int)Xs[j], a2);
-            int v = (a1 << 12) + __popc(bs ^ bp);
+                for (int j = 0; j < 7; ++j) l7 += __popc(Ps[q][j] & bp[q]) << j;
+                a1 += l7 - (__popc(Ps[q][7] & bp[q]) << 7);
+                const uint32_t tw[8] = {t0[q].x, t0[q].y, t0[q].z, t0[q].w, t1[q].x, t1[q].y, t1[q].z, t1[q].w};
+#pragma unroll
+                for (int j = 0; j < 8; ++j) a2 = __dp4a((int)tw[j], (int)Xs[q][j], a2);
+                diff += __popc(bs[q] ^ bp[q]);
+            }
+            int v = (a1 << 12) + diff;
 #pragma unroll
             for (int o = G / 2; o; o >>= 1) {
                 v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -478,17 +492,22 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
     ising_screen_kernel<Q><<<(unsigned)blocks, 256, 0, c.stream>>>(S, W, s, p, n, chunk, c.lambda, base, \
                                                                     out, surv, surv_g, surv_flag, nsurv,   \
                                                                     c.dcounters())
-        const int G = c.Mw <= 4 ? 4 : (c.Mw <= 8 ? 8 : (c.Mw <= 16 ? 16 : 32));
-        if (G < 32 && !getenv("NRG_K1_WIDE")) {
+        const int G = c.Mw <= 4 ? 4 : (c.Mw <= 8 ? 8 : 16);
+        const int WPL = (c.Mw + G - 1) / G;  // 1, 2 (M <= 1024) or up to 4 (M <= 2048)
+        if (!getenv("NRG_K1_WIDE") && (WPL == 1 || (WPL == 2 && !getenv("NRG_K1_ONE_PAIR")))) {
             const uint64_t sblocks = std::min<uint64_t>(ceil_div(n, 8 * 32), (uint64_t)sms * 16);
-#define NRG_LAUNCH_SMALL(GG)                                                                                 \
-    ising_screen_small_kernel<GG><<<(unsigned)sblocks, 256, 0, c.stream>>>(S, W, s, p, n, c.lambda, base, out, \
-                                                                         surv, surv_g, surv_flag, nsurv,     \
-                                                                         c.dcounters())
-            switch (G) {
-                case 4: NRG_LAUNCH_SMALL(4); break;
-                case 8: NRG_LAUNCH_SMALL(8); break;
-                default: NRG_LAUNCH_SMALL(16); break;
+#define NRG_LAUNCH_SMALL(GG, WW)                                                                             \
+    ising_screen_small_kernel<GG, WW><<<(unsigned)sblocks, 256, 0, c.stream>>>(S, W, s, p, n, c.lambda, base, \
+                                                                             out, surv, surv_g, surv_flag,    \
+                                                                             nsurv, c.dcounters())
+            if (WPL == 2) {
+                NRG_LAUNCH_SMALL(16, 2);
+            } else {
+                switch (G) {
+                    case 4: NRG_LAUNCH_SMALL(4, 1); break;
+                    case 8: NRG_LAUNCH_SMALL(8, 1); break;
+                    default: NRG_LAUNCH_SMALL(16, 1); break;
+                }
             }
 #undef NRG_LAUNCH_SMALL
         } else {
