@@ -112,6 +112,11 @@ __device__ __forceinline__ double hash_get(const HashView h, uint64_t key, doubl
     }
 }
 
+// Bloom bit of node v in a partner mask: a clear bit proves (u, v) holds no coupling
+__host__ __device__ __forceinline__ unsigned long long bloom_bit(int v) {
+    return 1ull << (((uint32_t)v * 0x9E3779B1u) >> 26);
+}
+
 struct IsingSnap {
     const uint32_t* Xb;
     const float* T32;    // fp32 copy for the Newton iterations ahead of the final fp64 pass
@@ -119,6 +124,7 @@ struct IsingSnap {
     const int8_t* T8;    // int8 field T8 = round(T / d) for the screen (partner side)
     const uint32_t* P8;  // T8's 8 bit planes per 32-sample word (screen, register side)
     const float4* Q8;    // per node {d, E = sum |T - d T8| rounded up, sum T8 (int bits), 0}
+    const unsigned long long* BL;  // per node 64-bit Bloom mask of its coupling partners
     const double* Tsq;   // sum T64^2 per node (L''(0) = -(2M - Tsq_a - Tsq_b) for w_cur = 0)
     int M, Mp, Mw;
 };
@@ -173,7 +179,7 @@ struct Context {
     uint64_t state_version = 1;
 
     // snapshot
-    DevBuf T32, T64, T8, P8, Q8, Tsq, U, xx;
+    DevBuf T32, T64, T8, P8, Q8, BL, Tsq, U, xx;
     uint64_t snap_version = 0;
     bool base_valid = false;
     double base = 0.0;
@@ -226,7 +232,8 @@ struct Context {
     }
     IsingSnap isnap() {
         return {dXb(), static_cast<float*>(T32.p), static_cast<double*>(T64.p), static_cast<int8_t*>(T8.p),
-                static_cast<uint32_t*>(P8.p), static_cast<float4*>(Q8.p), static_cast<double*>(Tsq.p), M, Mp, Mw};
+                static_cast<uint32_t*>(P8.p), static_cast<float4*>(Q8.p),
+                static_cast<unsigned long long*>(BL.p), static_cast<double*>(Tsq.p), M, Mp, Mw};
     }
     GaussSnap gsnap() {
         return {dXd(), static_cast<double*>(U.p), static_cast<double*>(xx.p), dtheta(), M, Mp};

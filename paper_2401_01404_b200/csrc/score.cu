@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(256, HW == 1 ? 4 : 3) ising_screen_kernel(Isin
     Src8<HW> cs;
     int cur = -1;
     float4 qs = make_float4(0.f, 0.f, 0.f, 0.f);
+    unsigned long long bl_s = 0;
     uint64_t evals = 0;
     const float err0 = 4.f * (float)S.M * 5.9604645e-08f;  // fp32 rounding of the combination
     const float lam = (float)lambda;
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(256, HW == 1 ? 4 : 3) ising_screen_kernel(Isin
             if (s != cur) {
                 load_src8<HW>(cs, S, s, lane);
                 qs = __ldg(&S.Q8[s]);
+                bl_s = __ldg(&S.BL[s]);
                 cur = s;
             }
             // partner loads first (the W lookup and the per-node constants overlap them)
@@ -114,7 +116,7 @@ __global__ void __launch_bounds__(256, HW == 1 ? 4 : 3) ising_screen_kernel(Isin
                 }
             }
             const float4 qp = __ldg(&S.Q8[p]);
-            const double wcur = hash_get(W, pair_key(s, p), 0.0);
+            const double wcur = (bl_s & bloom_bit(p)) ? hash_get(W, pair_key(s, p), 0.0) : 0.0;
             bool pruned = false;
             float gk = 0.f;
             uint8_t flag = 2;  // 2: existing edge (full fp64), 1: kink inside the error band, 0: survivor
@@ -188,6 +190,7 @@ __global__ void __launch_bounds__(256, WPL == 1 ? 4 : 3) ising_screen_small_kern
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     uint32_t Ps[WPL][8], Xs[WPL][8], bs[WPL];
+    unsigned long long bl_s = 0;
     int cur = -1;
     float4 qs = make_float4(0.f, 0.f, 0.f, 0.f);
     uint64_t evals = 0;
@@ -224,6 +227,7 @@ __global__ void __launch_bounds__(256, WPL == 1 ? 4 : 3) ising_screen_small_kern
                     for (int j = 0; j < 8; ++j) Xs[q][j] = pm1_bytes(bs[q] >> (4 * j));
                 }
                 qs = __ldg(&S.Q8[s]);
+                bl_s = __ldg(&S.BL[s]);
                 cur = s;
             }
             uint4 t0[WPL], t1[WPL];
@@ -241,7 +245,7 @@ __global__ void __launch_bounds__(256, WPL == 1 ? 4 : 3) ising_screen_small_kern
                 }
             }
             const float4 qp = __ldg(&S.Q8[p]);
-            const double wcur = hash_get(W, pair_key(s, p), 0.0);
+            const double wcur = (bl_s & bloom_bit(p)) ? hash_get(W, pair_key(s, p), 0.0) : 0.0;
             int a1 = 0, a2 = 0, diff = 0;
 #pragma unroll
             for (int q = 0; q < WPL; ++q) {

@@ -413,6 +413,26 @@ __global__ void snapshot_gauss_kernel(const double* __restrict__ X, const double
     }
 }
 
+// partner Bloom masks from W (the screen skips the coupling probe on a clear bit)
+__global__ void bloom_kernel(const uint64_t* __restrict__ keys, uint64_t cap, unsigned long long* __restrict__ bl) {
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= cap) return;
+    const uint64_t k = keys[s];
+    if (k >= kTombKey) return;
+    const int u = (int)(k >> 32), v = (int)(k & 0xffffffffu);
+    atomicOr(&bl[u], bloom_bit(v));
+    atomicOr(&bl[v], bloom_bit(u));
+}
+static void build_bloom(Context& c) {
+    c.BL.ensure((size_t)c.n * 8);
+    NRG_CUDA(cudaMemsetAsync(c.BL.p, 0, (size_t)c.n * 8, c.stream));
+    if (c.Wcap) {
+        bloom_kernel<<<(unsigned)ceil_div(c.Wcap, 256), 256, 0, c.stream>>>(
+            static_cast<uint64_t*>(c.Wkeys.p), c.Wcap, static_cast<unsigned long long*>(c.BL.p));
+        NRG_LAUNCH_CHECK();
+    }
+}
+
 void ensure_snapshot(Context& c) {
     if (!c.have_samples) fail(22, "no samples uploaded");
     if (c.snap_version == c.state_version) return;
@@ -432,6 +452,7 @@ void ensure_snapshot(Context& c) {
                                                          static_cast<uint32_t*>(c.P8.p),
                                                          static_cast<float4*>(c.Q8.p),
                                                          static_cast<double*>(c.Tsq.p), nullptr);
+        build_bloom(c);
     } else {
         c.U.ensure(nm * 8);
         c.xx.ensure((size_t)c.n * 8);
@@ -452,12 +473,13 @@ void snapshot_rows(Context& c, const int32_t* rows, uint64_t nr) {
         return;
     }
     c.tic();
-    if (c.kind == ISING)
+    if (c.kind == ISING) {
         snapshot_ising_kernel<<<(unsigned)nr, 256, 0, c.stream>>>(
             c.dH(), c.dtheta(), c.M, c.Mp, static_cast<double*>(c.T64.p), static_cast<float*>(c.T32.p),
             static_cast<int8_t*>(c.T8.p), static_cast<uint32_t*>(c.P8.p), static_cast<float4*>(c.Q8.p),
             static_cast<double*>(c.Tsq.p), rows);
-    else
+        build_bloom(c);  // the rows' couplings changed too
+    } else
         snapshot_gauss_kernel<<<(unsigned)nr, 256, 0, c.stream>>>(c.dXd(), c.dH(), c.dtheta(), c.M, c.Mp,
                                                                    static_cast<double*>(c.U.p),
                                                                    static_cast<double*>(c.xx.p), rows);
