@@ -13,6 +13,8 @@
 #include <cuda/std/tuple>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "context.cuh"
@@ -203,7 +205,25 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
     kp.reverse = reverse;
     KnnResultD knn;
     DevBuf kid, kdist;
+    const bool dbg = getenv("NRG_DEBUG_LEVELS") != nullptr;
+    uint64_t m0 = 0;
+    double t0 = 0.0, s0 = 0.0, k20 = 0.0;
+    if (dbg) {
+        NRG_CUDA(cudaMemcpyAsync(&m0, c.dcounters() + C_MISSES, 8, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        t0 = c.phase_ms[P_KNN];
+        s0 = c.phase_ms[P_SCORE];
+        k20 = c.k2_pairs;
+    }
     find_knn(c, mode, k, S, n, kp, false, knn, kid, kdist);
+    if (dbg) {
+        uint64_t m1 = 0;
+        NRG_CUDA(cudaMemcpyAsync(&m1, c.dcounters() + C_MISSES, 8, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        fprintf(stderr, "level %d: n=%llu k=%d sweeps=%d knn_ms=%.2f score_ms=%.2f unique_pairs=%llu survivors=%.0f\n",
+                level, (unsigned long long)n, k, knn.sweeps, c.phase_ms[P_KNN] - t0, c.phase_ms[P_SCORE] - s0,
+                (unsigned long long)(m1 - m0), c.k2_pairs - k20);
+    }
     c.tic();
     const uint64_t nd = n * (uint64_t)knn.k;
     DevBuf dirb, dir2b, tmpb;

@@ -419,11 +419,13 @@ __global__ void __launch_bounds__(NT) knn_gather_kernel(const int32_t* __restric
     const int32_t* row_i = adj + li * cap;
     const int len_i = alen[li];
     int32_t* my_ids = cand_id + li * capn;
-    // 2-hop rows side by side: a group of 2^lw >= cap threads per row (or the whole CTA
-    // stepping through a row when cap > NT)
-    const int gw = 1 << lw;
-    const int rows = gw >= NT ? 1 : NT / gw;
-    const int r = gw >= NT ? 0 : tid >> lw, b0 = gw >= NT ? tid : tid & (gw - 1);
+    // 2-hop rows side by side: a group of 2^lw >= cap threads per row
+    // (rows wider than a warp: one warp per row, lanes striding it, so the CTA keeps
+    // NT/32 rows' dependent loads in flight instead of walking rows one at a time)
+    const int gl = lw < 5 ? lw : 5;
+    const int gw = 1 << gl;
+    const int rows = NT / gw;
+    const int r = tid >> gl, b0 = tid & (gw - 1);
     for (int a0 = 0; a0 < len_i; a0 += rows) {
         const int a = a0 + r;
         if (a < len_i) {
@@ -431,7 +433,7 @@ __global__ void __launch_bounds__(NT) knn_gather_kernel(const int32_t* __restric
             const int len_j = alen[lj];
             const int32_t* row_j = adj + (uint64_t)lj * cap;
             const bool old_a = !newf[li * cap + a];
-            for (int b = b0; b < len_j; b += (gw >= NT ? NT : gw)) {
+            for (int b = b0; b < len_j; b += gw) {
                 if (old_a && !newf[(uint64_t)lj * cap + b]) continue;  // old-old: lost last sweep
                 const int32_t v = row_j[b];
                 if (insert(v)) {
@@ -485,6 +487,111 @@ __global__ void sum_counts_kernel(const int32_t* __restrict__ cnt, uint64_t n, u
         a += (unsigned long long)cnt[t];
     for (int o = 16; o; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
     if ((threadIdx.x & 31) == 0 && a) atomicAdd(out, a);
+}
+
+// ---------------------------------------------------------------- gather, deep levels
+// For small levels with wide rows (n <= 16384 ids, cap >= 32) the 2-hop candidate set
+// is an OR of row bitsets: U(j) as a bitset over the level's ids, and new(U(j)) (the
+// entries that were not in U(j) last sweep).  cand(i) = OR over a in U(i) of
+// (a new in U(i) ? U(a) : new(U(a))) minus i's current row and i itself: the same set
+// the incremental join inserts one by one, without contended shared atomics.
+__global__ void u_bits_kernel(const int32_t* __restrict__ adj, const int32_t* __restrict__ alen,
+                              const uint8_t* __restrict__ newf, uint64_t n, int cap, int W, uint32_t* __restrict__ ub,
+                              uint32_t* __restrict__ nb) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n * (uint64_t)cap) return;
+    const uint64_t i = t / cap;
+    const int a = (int)(t - i * cap);
+    if (a >= alen[i]) return;
+    const int32_t j = adj[t];
+    const uint32_t bit = 1u << (j & 31);
+    atomicOr(&ub[i * W + (j >> 5)], bit);
+    if (newf[t]) atomicOr(&nb[i * W + (j >> 5)], bit);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __restrict__ nodes, uint64_t n,
+                                                             const int32_t* __restrict__ adj,
+                                                             const int32_t* __restrict__ alen, int cap,
+                                                             const int32_t* __restrict__ gid, int kw, int W,
+                                                             const uint32_t* __restrict__ ub,
+                                                             const uint32_t* __restrict__ nb,
+                                                             const uint8_t* __restrict__ newf, HashView h,
+                                                             ClaimSink sink, uint64_t capn,
+                                                             int32_t* __restrict__ cand_id,
+                                                             uint32_t* __restrict__ cand_slot,
+                                                             int32_t* __restrict__ cand_cnt, uint64_t lo, bool do_claim) {
+    extern __shared__ uint32_t bits_smem[];
+    uint32_t* acc = bits_smem;     // OR of the 2-hop rows
+    uint32_t* excl = acc + W;      // i's current row and i itself
+    typedef cub::BlockScan<int, NT> Scan;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ int s_total;
+    const uint64_t li = lo + blockIdx.x;
+    const int tid = threadIdx.x;
+    for (int w = tid; w < W; w += NT) acc[w] = excl[w] = 0u;
+    __syncthreads();
+    if (tid == 0) atomicOr(&excl[li >> 5], 1u << (li & 31));
+    for (int t = tid; t < kw; t += NT) {
+        const int32_t v = gid[li * kw + t];
+        atomicOr(&excl[v >> 5], 1u << (v & 31));
+    }
+    const int32_t* row_i = adj + li * cap;
+    const int len_i = alen[li];
+    if (W <= NT) {
+        // G threads per word, each ORs every G-th row into a register
+        const int G = NT / W;
+        const int w = tid % W, g = tid / W;
+        if (g < G) {
+            uint32_t r = 0u;
+            for (int a = g; a < len_i; a += G) {
+                const int32_t lj = row_i[a];
+                r |= (newf[li * cap + a] ? ub : nb)[(uint64_t)lj * W + w];
+            }
+            if (r) atomicOr(&acc[w], r);
+        }
+    } else {
+        for (int w = tid; w < W; w += NT) {
+            uint32_t r = 0u;
+            for (int a = 0; a < len_i; ++a) r |= (newf[li * cap + a] ? ub : nb)[(uint64_t)row_i[a] * W + w];
+            acc[w] = r;
+        }
+    }
+    __syncthreads();
+    // candidate ids in increasing order: popcounts of the thread's words, block scan
+    constexpr int kMaxWpt = 16384 / 32 / NT + 1;
+    int cnt = 0;
+    uint32_t cw[kMaxWpt];
+#pragma unroll
+    for (int q = 0; q < kMaxWpt; ++q) {
+        const int w = tid * kMaxWpt + q;
+        cw[q] = w < W ? (acc[w] & ~excl[w]) : 0u;
+        cnt += __popc(cw[q]);
+    }
+    int off = 0, total = 0;
+    Scan(scan_tmp).ExclusiveSum(cnt, off, total);
+    int32_t* my_ids = cand_id + li * capn;
+#pragma unroll
+    for (int q = 0; q < kMaxWpt; ++q) {
+        const int w = tid * kMaxWpt + q;
+        for (uint32_t m = cw[q]; m; m &= m - 1) my_ids[off++] = 32 * w + __ffs(m) - 1;
+    }
+    if (tid == 0) s_total = total;
+    __syncthreads();
+    const int ncand = s_total;
+    if (!do_claim) {
+        if (tid == 0) cand_cnt[li] = ncand;
+        return;
+    }
+    const int32_t gs = nodes[li];
+    for (int t0 = 0; t0 < ncand; t0 += NT) {
+        const int t = t0 + tid;
+        const bool valid = t < ncand;
+        const int32_t v = valid ? my_ids[t] : 0;
+        const uint32_t sl = claim_warp(h, sink, valid, gs, valid ? nodes[v] : 0, li * capn + t);
+        if (valid) cand_slot[li * capn + t] = sl;
+    }
+    if (tid == 0) cand_cnt[li] = ncand;
 }
 
 // ---------------------------------------------------------------- merge top-kw
@@ -997,7 +1104,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
 
     // ---- sweeps
     const uint64_t capn = std::min<uint64_t>((uint64_t)cap * cap, n - 1);
-    DevBuf adjb, alenb, adjpb, alenpb, newfb, cidb, cslb, ccntb, churnb, churnb2, wsb, wpb, wslb;
+    DevBuf adjb, alenb, adjpb, alenpb, newfb, cidb, cslb, ccntb, churnb, churnb2, wsb, wpb, wslb, ubitsb, nbitsb;
     int32_t* adj = adjb.as<int32_t>(n * cap);
     int32_t* alen = alenb.as<int32_t>(n);
     int32_t* adjp = adjpb.as<int32_t>(n * cap);  // U of the previous sweep
@@ -1099,7 +1206,18 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             int lw = 0;
             while ((1 << lw) < cap) ++lw;
             const HashView hv0 = fused && cached ? c.Cview() : HashView{nullptr, nullptr, 0};
-            if (big)
+            const int W = (int)((n + 31) / 32);
+            if (n <= 16384 && cap >= 32 && !getenv("NRG_KNN_HASH_GATHER")) {
+                uint32_t* ub = ubitsb.as<uint32_t>(n * (uint64_t)W);
+                uint32_t* nbits = nbitsb.as<uint32_t>(n * (uint64_t)W);
+                NRG_CUDA(cudaMemsetAsync(ub, 0, n * (uint64_t)W * 4, c.stream));
+                NRG_CUDA(cudaMemsetAsync(nbits, 0, n * (uint64_t)W * 4, c.stream));
+                u_bits_kernel<<<(unsigned)ceil_div(n * (uint64_t)cap, 256), 256, 0, c.stream>>>(adj, alen, newf, n, cap,
+                                                                                               W, ub, nbits);
+                knn_gather_bits_kernel<256><<<(unsigned)own, 256, 2 * W * 4, c.stream>>>(
+                    d_nodes, n, adj, alen, cap, gid, kw, W, ub, nbits, newf, hv0, sk, capn, cand_id, cand_slot, cand_cnt,
+                    lo, fused);
+            } else if (big)
                 knn_gather_kernel<256><<<(unsigned)own, 256, tab_bytes, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv0, sk, capn, cand_id,
                     cand_slot, cand_cnt, lo, lw, newf, fused);
