@@ -721,6 +721,105 @@ __global__ void __launch_bounds__(NT) knn_merge_kernel(const int32_t* __restrict
     if ((tid & 31) == 0 && ch) atomicAdd(churn, (unsigned long long)ch);
 }
 
+// Narrow rows (kw <= 64): one warp per node, 8 nodes per CTA, so many more merges are in
+// flight than with a 32-thread CTA per node (the resident-CTA limit).  Candidates are
+// consumed 64 at a time; those beating the current worst are ballot-compacted after the
+// row and the new row is selected by rank (as knn_merge_kernel).
+constexpr int kMergeWarps = 8;
+constexpr int kMergeBlk = 64;
+__global__ void __launch_bounds__(32 * kMergeWarps) knn_merge_warp_kernel(
+    const int32_t* __restrict__ nodes, uint64_t n, int32_t* __restrict__ gid, double* __restrict__ gd, int kw,
+    const int32_t* __restrict__ cand_id, const uint32_t* __restrict__ cand_slot,
+    const int32_t* __restrict__ cand_cnt, uint64_t capn, const double* __restrict__ cvals,
+    const double* __restrict__ rvals, unsigned long long* __restrict__ churn, uint64_t lo, uint64_t own) {
+    extern __shared__ unsigned char merge_warp_smem[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const uint64_t node = (uint64_t)blockIdx.x * kMergeWarps + wib;
+    if (node >= own) return;
+    const uint64_t li = lo + node;
+    const int cnt = cand_cnt[li];
+    if (cnt == 0) return;
+    const int cap = kw + kMergeBlk;
+    unsigned char* base = merge_warp_smem + (size_t)wib * ((size_t)cap + kw) * 20;
+    double* bd = reinterpret_cast<double*>(base);
+    double* od = bd + cap;
+    int32_t* bi = reinterpret_cast<int32_t*>(od + kw);
+    int32_t* bg = bi + cap;
+    int32_t* bo = bg + cap;
+    int32_t* oi = bo + cap;
+    int32_t* og = oi + kw;
+    int32_t* oo = og + kw;
+    int32_t* row_id = gid + li * kw;
+    double* row_d = gd + li * kw;
+    for (int t = lane; t < kw; t += 32) {
+        bd[t] = row_d[t];
+        bi[t] = row_id[t];
+        bg[t] = nodes[row_id[t]];
+        bo[t] = 0;
+    }
+    __syncwarp();
+    bool changed_any = false;
+    for (int blk = 0; blk < cnt; blk += kMergeBlk) {
+        const double wd = bd[kw - 1];
+        const int wg = bg[kw - 1];
+        int m = kw;
+        for (int t0 = blk; t0 < min(cnt, blk + kMergeBlk); t0 += 32) {
+            const int t = t0 + lane;
+            double d = 0.0;
+            int32_t v = 0, g = 0;
+            bool better = false;
+            if (t < cnt) {
+                v = cand_id[li * capn + t];
+                const uint32_t sl = cand_slot[li * capn + t];
+                d = (sl & kRemote) ? rvals[sl & ~kRemote] : cvals[sl];
+                g = nodes[v];
+                better = entry_less(d, g, wd, wg);
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, better);
+            if (better) {
+                const int at = m + __popc(bal & ((1u << lane) - 1u));
+                bd[at] = d;
+                bi[at] = v;
+                bg[at] = g;
+                bo[at] = 1;
+            }
+            m += __popc(bal);
+        }
+        __syncwarp();
+        if (m == kw) continue;  // nothing beats the worst
+        changed_any = true;
+        for (int t = lane; t < m; t += 32) {
+            const double d = bd[t];
+            const int g = bg[t];
+            int r = 0;
+            for (int j = 0; j < m; ++j) r += entry_less(bd[j], bg[j], d, g) ? 1 : 0;
+            if (r < kw) {
+                od[r] = d;
+                oi[r] = bi[t];
+                og[r] = g;
+                oo[r] = bo[t];
+            }
+        }
+        __syncwarp();
+        for (int t = lane; t < kw; t += 32) {
+            bd[t] = od[t];
+            bi[t] = oi[t];
+            bg[t] = og[t];
+            bo[t] = oo[t];
+        }
+        __syncwarp();
+    }
+    if (!changed_any) return;
+    int ch = 0;
+    for (int t = lane; t < kw; t += 32) {
+        row_d[t] = bd[t];
+        row_id[t] = bi[t];
+        ch += bo[t];
+    }
+    ch = warp_sum(ch);
+    if (lane == 0 && ch) atomicAdd(churn, (unsigned long long)ch);
+}
+
 // ---------------------------------------------------------------- exhaustive
 // rows of (id-sorted) candidates with distances from the triangular array
 __global__ void exh_fill2_kernel(const int32_t* __restrict__ sorted_loc, const int32_t* __restrict__ rank,
@@ -1267,6 +1366,10 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             if (kw > 64)
                 knn_merge_kernel<128><<<(unsigned)own, 128, merge_smem, c.stream>>>(
                     d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dvals, rvals, buf_cap, churn, lo);
+            else if (!getenv("NRG_MERGE_CTA"))
+                knn_merge_warp_kernel<<<(unsigned)ceil_div(own, kMergeWarps), 32 * kMergeWarps,
+                                        (size_t)kMergeWarps * (2 * kw + kMergeBlk) * 20, c.stream>>>(
+                    d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dvals, rvals, churn, lo, own);
             else
                 knn_merge_kernel<32><<<(unsigned)own, 32, merge_smem, c.stream>>>(
                     d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dvals, rvals, buf_cap, churn, lo);
