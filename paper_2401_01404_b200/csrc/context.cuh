@@ -190,6 +190,16 @@ struct Context {
     uint64_t cache_live_host = 0;
     uint64_t last_survivors = 0;
 
+    // dense FindBest level (find_best.cu): the exact distances of every pair of a deep
+    // level's node set S_D (row-major upper triangle over positions in S_D), computed once
+    // by the tensor-core screen; S_D and every deeper level (subsets of S_D) look their
+    // distances up here instead of claiming and scoring them one by one.  `dloc` maps a
+    // global id to its position in S_D (-1 outside), `dbits` marks the pairs probed so
+    // far (the generation's cache-miss count stays the reference's).
+    bool dense_active = false;
+    uint64_t dense_n = 0;
+    DevBuf dtri, dloc, dbits;
+
     // test metrics
     DevBuf table, line;
     uint64_t table_n = 0, line_n = 0;

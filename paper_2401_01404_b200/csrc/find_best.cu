@@ -13,6 +13,7 @@
 #include <cuda/std/tuple>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -140,6 +141,93 @@ __global__ void unpack_trikey_kernel(const TriKey* __restrict__ in, uint64_t n, 
     od[e] = dkey_inv(in[e].d);
 }
 
+// ---------------------------------------------------------------- dense levels
+// A deep level whose per-node candidate sets approach the level itself (cap^2 ~ |S|) probes
+// a large share of its |S|^2/2 pairs, each through a claim in the DRAM-resident distance
+// cache and a K1 screen.  There the exhaustive tensor-core screen of S (score_all_pairs_tc,
+// ~1e11 pairs/s) is cheaper than the probes: the level and every deeper one (subsets of S)
+// then look distances up in that triangle.  The NNDescent/FindBest semantics, the values
+// (the same deterministic scores) and the miss counting are unchanged.
+__global__ void dense_loc_kernel(const int32_t* __restrict__ nodes, uint64_t n, int32_t* __restrict__ loc) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) loc[nodes[t]] = (int32_t)t;
+}
+// base case below a dense root: the level's own triangle gathered from the root's
+__global__ void dense_subtri_kernel(const int32_t* __restrict__ nodes, uint64_t n, const int32_t* __restrict__ loc,
+                                    const double* __restrict__ tri, uint64_t dn, TriKey* __restrict__ out) {
+    const uint64_t a = blockIdx.x;
+    if (a >= n) return;
+    const uint64_t base = a * (2 * n - a - 1) / 2;
+    const int32_t x = nodes[a];
+    const uint64_t ra = (uint64_t)loc[x];
+    for (uint64_t c = a + 1 + threadIdx.x; c < n; c += blockDim.x) {
+        const int32_t y = nodes[c];
+        const uint64_t rb = (uint64_t)loc[y];
+        const uint64_t lo = ra < rb ? ra : rb, hi = ra < rb ? rb : ra;
+        TriKey k;
+        k.d = dkey(tri[lo * (2 * dn - lo - 1) / 2 + (hi - lo - 1)]);
+        k.a = (uint32_t)min(x, y);
+        k.b = (uint32_t)max(x, y);
+        out[base + (c - a - 1)] = k;
+    }
+}
+
+// Settles the dense root's probe counts (see dense_probe, knn.cu): every probe there was
+// counted as a hit; of the U distinct pairs probed (bits set), the ones no shallower level
+// had scored (absent from the distance cache: U - F) are the generation's misses.
+__global__ void dense_recount_kernel(HashView h, const int32_t* __restrict__ loc, const uint32_t* __restrict__ bits,
+                                     uint64_t nwords, uint64_t dn, uint64_t* __restrict__ counters) {
+    long long d = 0;
+    const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, st = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t w = t0; w < nwords; w += st) d += __popc(bits[w]);
+    if (h.keys) {
+        for (uint64_t s = t0; s <= h.mask; s += st) {
+            const uint64_t key = __ldcs(&h.keys[s]);
+            if (key >= kTombKey) continue;
+            const int32_t la = loc[(uint32_t)(key >> 32)], lb = loc[(uint32_t)(key & 0xffffffffu)];
+            if (la < 0 || lb < 0) continue;
+            const uint64_t a = (uint64_t)min(la, lb), b = (uint64_t)max(la, lb);
+            const uint64_t t = a * (2 * dn - a - 1) / 2 + (b - a - 1);
+            d -= (bits[t >> 5] >> (t & 31)) & 1u;
+        }
+    }
+    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    if ((threadIdx.x & 31) == 0 && d) {
+        atomicAdd((unsigned long long*)&counters[C_MISSES], (unsigned long long)d);
+        atomicAdd((unsigned long long*)&counters[C_HITS], (unsigned long long)(-d));
+    }
+}
+
+struct DenseGuard {  // the level that set up the dense root tears it down (also on throw)
+    Context& c;
+    bool owner = false;
+    explicit DenseGuard(Context& cc) : c(cc) {}
+    ~DenseGuard() {
+        if (owner) {
+            const uint64_t pairs = c.dense_n * (c.dense_n - 1) / 2;
+            const HashView h = (c.Ckeys.p && c.Ccap) ? c.Cview() : HashView{nullptr, nullptr, 0};
+            dense_recount_kernel<<<148 * 8, 256, 0, c.stream>>>(h, static_cast<const int32_t*>(c.dloc.p),
+                                                                static_cast<const uint32_t*>(c.dbits.p),
+                                                                (pairs + 31) / 32, c.dense_n, c.dcounters());
+            c.dense_active = false;
+            c.dense_n = 0;
+            c.dtri.release();
+            c.dbits.release();
+        }
+    }
+};
+
+static uint64_t dense_max_n() {
+    const char* e = getenv("NRG_DENSE_N");
+    return e ? (uint64_t)strtoull(e, nullptr, 10) : 16384;
+}
+// a level goes dense when its candidate sets (up to cap^2 per node) cover at least
+// 1/ratio of the level
+static uint64_t dense_ratio() {
+    const char* e = getenv("NRG_DENSE_RATIO");
+    return e ? (uint64_t)strtoull(e, nullptr, 10) : 4;
+}
+
 static inline unsigned g256(uint64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div(n, 256)); }
 
 // union of two candidate lists without duplicate pairs, then the (dist,i,j)-smallest
@@ -185,12 +273,22 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
     if (n * n <= 4 * m) {
         // base case: exhaustive scan (inc/find_best.hpp:98-104)
         DevBuf distb, keysb, tmpb;
-        double* dist = distb.as<double>(total);
-        score_all_pairs(c, mode, S, n, dist);
-        c.tic();
         TriKey* keys = keysb.as<TriKey>(total);
-        tri_from_pairs_kernel<<<(unsigned)n, 256, 0, c.stream>>>(S, n, dist, keys);
-        NRG_LAUNCH_CHECK();
+        if (mode == EXACT && c.dense_active && c.world == 1) {
+            c.tic();
+            dense_subtri_kernel<<<(unsigned)n, 256, 0, c.stream>>>(S, n, static_cast<const int32_t*>(c.dloc.p),
+                                                                  static_cast<const double*>(c.dtri.p), c.dense_n,
+                                                                  keys);
+            NRG_LAUNCH_CHECK();
+            // counted as score_all_pairs counts the base case: every pair a probe
+            counters_add_host(c, C_MISSES, total);
+        } else {
+            double* dist = distb.as<double>(total);
+            score_all_pairs(c, mode, S, n, dist);
+            c.tic();
+            tri_from_pairs_kernel<<<(unsigned)n, 256, 0, c.stream>>>(S, n, dist, keys);
+            NRG_LAUNCH_CHECK();
+        }
         TriKey* out = result.as<TriKey>(total);
         sort_trikeys(c, keys, out, total, tmpb);
         c.sync();
@@ -199,6 +297,38 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
         return want;
     }
     const int k = (int)((4 * m + n - 1) / n);
+    DenseGuard dg(c);
+    {
+        const uint64_t kw = (uint64_t)std::max(k, 4);
+        const uint64_t cap = reverse ? std::max<uint64_t>(2 * kw, 8) : std::max<uint64_t>(kw, 8);
+        if (!c.dense_active && mode == EXACT && c.kind == ISING && c.world == 1 && n <= dense_max_n() &&
+            dense_ratio() * cap * cap >= n) {
+            double* tri = c.dtri.as<double>(total);
+            const double ph0 = c.phase_ms[P_SCORE];
+            const auto w0 = std::chrono::steady_clock::now();
+            const bool ok = score_all_pairs_tc(c, S, n, tri);
+            if (getenv("NRG_DEBUG_LEVELS")) {
+                c.sync();
+                fprintf(stderr, "dense root level %d: n=%llu setup wall_ms=%.2f score_phase_ms=%.2f ok=%d\n", level,
+                        (unsigned long long)n,
+                        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count(),
+                        c.phase_ms[P_SCORE] - ph0, (int)ok);
+            }
+            if (ok) {
+                int32_t* loc = c.dloc.as<int32_t>(c.n);
+                NRG_CUDA(cudaMemsetAsync(loc, 0xff, (size_t)c.n * 4, c.stream));
+                dense_loc_kernel<<<g256(n), 256, 0, c.stream>>>(S, n, loc);
+                NRG_LAUNCH_CHECK();
+                uint32_t* bits = c.dbits.as<uint32_t>((total + 31) / 32);
+                NRG_CUDA(cudaMemsetAsync(bits, 0, (total + 31) / 32 * 4, c.stream));
+                c.dense_active = true;
+                c.dense_n = n;
+                dg.owner = true;
+            } else {
+                c.dtri.release();
+            }
+        }
+    }
     KnnParamsD kp;
     kp.eps = knn_eps;
     kp.seed = mix64(seed, (uint64_t)level);

@@ -176,7 +176,29 @@ struct ClaimSink {
     uint64_t* rkeys = nullptr;
     int32_t* rdest = nullptr;
     unsigned long long* rcount = nullptr;
+    // dense level (Context::dense_active): slots index the level's exhaustive distance
+    // triangle; nothing is claimed or scored, probes are only counted
+    const int32_t* dloc = nullptr;
+    uint32_t* dbits = nullptr;
+    uint64_t dn = 0;
 };
+
+// row-major upper-triangle index of positions a < b among n (inc/find_best.hpp:78-79)
+__device__ __forceinline__ uint64_t tri_index(uint64_t a, uint64_t b, uint64_t n) {
+    return a * (2 * n - a - 1) / 2 + (b - a - 1);
+}
+
+// Probe of pair (ra, rb) (positions in the dense root) at a dense level: its slot in the
+// triangle; the pair's bit is marked (fire-and-forget RED) and the probe counted as a hit.
+// dense_recount (find_best.cu) settles the counts once the root is done: of the U marked
+// pairs, those F the generation had not scored at a shallower level (absent from the
+// distance cache) move from the hits to the misses — the reference's DistanceCache
+// misses/hits (inc/model.hpp:54-70) without a round trip per probe.
+__device__ __forceinline__ uint32_t dense_probe(uint32_t* __restrict__ dbits, uint64_t dn, uint64_t ra, uint64_t rb) {
+    const uint64_t t = ra < rb ? tri_index(ra, rb, dn) : tri_index(rb, ra, dn);
+    atomicOr(&dbits[t >> 5], 1u << (t & 31));
+    return (uint32_t)t;
+}
 
 // warp-cooperative claim of one candidate per lane (active lanes given by `valid`).
 // Uncached metrics (h.keys == nullptr) claim every candidate into its flat slot.
@@ -186,6 +208,13 @@ __device__ __forceinline__ uint32_t claim_warp(HashView h, const ClaimSink& sink
     uint64_t sl = 0;
     int dest = 0;
     const uint64_t key = pair_key(gs, gp);
+    if (sink.dloc) {
+        if (valid) sl = dense_probe(sink.dbits, sink.dn, (uint64_t)sink.dloc[gs], (uint64_t)sink.dloc[gp]);
+        const unsigned hb = __ballot_sync(0xffffffffu, valid);
+        if ((threadIdx.x & 31) == 0 && hb)
+            atomicAdd((unsigned long long*)&sink.counters[C_HITS], (unsigned long long)__popc(hb));
+        return (uint32_t)sl;
+    }
     if (valid) {
         if (!h.keys) {
             sl = flat;
@@ -520,7 +549,8 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
                                                              ClaimSink sink, uint64_t capn,
                                                              int32_t* __restrict__ cand_id,
                                                              uint32_t* __restrict__ cand_slot,
-                                                             int32_t* __restrict__ cand_cnt, uint64_t lo, bool do_claim) {
+                                                             int32_t* __restrict__ cand_cnt, uint64_t lo, bool do_claim,
+                                                             const int32_t* __restrict__ rootpos) {
     extern __shared__ uint32_t bits_smem[];
     uint32_t* acc = bits_smem;     // OR of the 2-hop rows
     uint32_t* excl = acc + W;      // i's current row and i itself
@@ -571,6 +601,25 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
     int off = 0, total = 0;
     Scan(scan_tmp).ExclusiveSum(cnt, off, total);
     int32_t* my_ids = cand_id + li * capn;
+    if (rootpos) {
+        // dense level: slots in the root's distance triangle, probes marked and counted here
+        uint32_t* my_slot = cand_slot + li * capn;
+        const uint64_t ra = (uint64_t)rootpos[li];
+#pragma unroll
+        for (int q = 0; q < kMaxWpt; ++q) {
+            const int w = tid * kMaxWpt + q;
+            for (uint32_t m = cw[q]; m; m &= m - 1) {
+                const int v = 32 * w + __ffs(m) - 1;
+                my_ids[off] = v;
+                my_slot[off++] = dense_probe(sink.dbits, sink.dn, ra, (uint64_t)rootpos[v]);
+            }
+        }
+        const int probes = warp_sum(cnt);
+        if ((tid & 31) == 0 && probes)
+            atomicAdd((unsigned long long*)&sink.counters[C_HITS], (unsigned long long)probes);
+        if (tid == 0) cand_cnt[li] = total;
+        return;
+    }
 #pragma unroll
     for (int q = 0; q < kMaxWpt; ++q) {
         const int w = tid * kMaxWpt + q;
@@ -1103,6 +1152,17 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
     double* gd = gd_buf.as<double>(n * kw);
     unsigned long long* wcount = c.s_c.as<unsigned long long>(2);
     const bool cached = (mode == EXACT || mode == GRADIENT);
+    // dense level: distances come from the level's exhaustive triangle (find_best.cu)
+    const bool dense = mode == EXACT && c.dense_active && c.world == 1;
+    const double* dtri = dense ? static_cast<const double*>(c.dtri.p) : nullptr;
+    DevBuf rootposb;
+    int32_t* rootpos = nullptr;
+    if (dense) {
+        rootpos = rootposb.as<int32_t>(n);
+        gather_kernel<int32_t><<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(
+            static_cast<const int32_t*>(c.dloc.p), d_nodes, n, rootpos);
+        NRG_LAUNCH_CHECK();
+    }
     // node shard of this rank; the distance cache is sharded by key
     const int W = cached ? c.world : 1;
     uint64_t lo = 0, hi = n;
@@ -1119,6 +1179,11 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         s.live = static_cast<uint64_t*>(c.Ccount.p);
         s.rank = c.rank;
         s.world = W;
+        if (dense) {
+            s.dloc = static_cast<const int32_t*>(c.dloc.p);
+            s.dbits = static_cast<uint32_t*>(c.dbits.p);
+            s.dn = c.dense_n;
+        }
         if (W > 1) {
             s.rkeys = X.rkeys.as<uint64_t>(rcap);
             s.rdest = X.rdest.as<int32_t>(rcap);
@@ -1154,7 +1219,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         NRG_LAUNCH_CHECK();
         c.toc(P_KNN);
         if (cached) {
-            cache_reserve(c, n * (uint64_t)kw);
+            if (!dense) cache_reserve(c, n * (uint64_t)kw);
             uint32_t* slot = slb.as<uint32_t>(nq + 1);
             DevBuf wsb, wpb, wslb;
             int32_t* ws = wsb.as<int32_t>(nq + 1);
@@ -1169,10 +1234,10 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             unsigned long long nw = 0;
             NRG_CUDA(cudaMemcpyAsync(&nw, wcount, 8, cudaMemcpyDeviceToHost, c.stream));
             c.sync();
-            exchange_and_score(c, mode, sk, nw, X, 0);
+            if (!dense) exchange_and_score(c, mode, sk, nw, X, 0);
             if (nq) {
                 gather_vals_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, c.stream>>>(
-                    c.Cview().vals, static_cast<double*>(X.rvals.p), slot, nq, gd + lo * kw);
+                    dense ? dtri : c.Cview().vals, static_cast<double*>(X.rvals.p), slot, nq, gd + lo * kw);
                 NRG_LAUNCH_CHECK();
             }
         } else {
@@ -1295,8 +1360,8 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         // the worst case (every node gathers capn new pairs) normally fits the cache
         // with room to spare: reserve it and claim inside the gather; otherwise gather,
         // count, reserve exactly and claim in a second pass
-        const bool fused = !cached || (c.cache_live_host + wmax) * 10 <= (1ull << 31) * 6;
-        if (cached && fused) cache_reserve(c, wmax);
+        const bool fused = !cached || dense || (c.cache_live_host + wmax) * 10 <= (1ull << 31) * 6;
+        if (cached && fused && !dense) cache_reserve(c, wmax);
         c.tic();
         NRG_CUDA(cudaMemsetAsync(wcount, 0, 16, c.stream));
         NRG_CUDA(cudaMemsetAsync(churn, 0, 8, c.stream));
@@ -1315,7 +1380,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                                                                                                W, ub, nbits);
                 knn_gather_bits_kernel<256><<<(unsigned)own, 256, 2 * W * 4, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, W, ub, nbits, newf, hv0, sk, capn, cand_id, cand_slot, cand_cnt,
-                    lo, fused);
+                    lo, fused, rootpos);
             } else if (big)
                 knn_gather_kernel<256><<<(unsigned)own, 256, tab_bytes, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv0, sk, capn, cand_id,
@@ -1351,15 +1416,15 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         NRG_CUDA(cudaMemcpyAsync(&nw, wcount, 8, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
         c.toc(P_KNN);
-        if (cached) {
+        if (cached && !dense) {
             exchange_and_score(c, mode, sk, nw, X, 0);
-        } else if (nw) {
+        } else if (nw && !dense) {
             ScoreOut so;
             so.cache_vals = flat_d;
             so.slot = wsl;
             score_entries(c, mode, ws, wp, nw, so);
         }
-        const double* dvals = cached ? c.Cview().vals : flat_d;
+        const double* dvals = dense ? dtri : cached ? c.Cview().vals : flat_d;
         const double* rvals = static_cast<double*>(X.rvals.p);
         c.tic();
         if (own) {

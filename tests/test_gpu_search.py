@@ -265,3 +265,29 @@ def test_incremental_join_equals_full_join(gpu, monkeypatch):
     assert a[2] == b[2]
     np.testing.assert_array_equal(a[3], b[3])
     np.testing.assert_array_equal(a[4], b[4])
+
+
+@pytest.mark.parametrize("n,M,seed,kappa", [(1000, 500, 1, 2.0), (3000, 400, 2, 2.0), (2000, 300, 4, 6.0)])
+def test_dense_levels_equal_claim_path(gpu, monkeypatch, n, M, seed, kappa):
+    """Deep FindBest levels that read distances from the level's exhaustive tensor-core
+    triangle (find_best.cu, dense levels) give the identical pair list and trace as the
+    claim-and-score path, and count the same cache misses and hits (the unique pairs the
+    reference's DistanceCache would compute)."""
+    X, lam = _ising(n, M, seed)
+    nodes = np.arange(n, dtype=np.int32)
+    m_ = int(round(kappa * n))
+
+    def run(dense_n):
+        monkeypatch.setenv("NRG_DENSE_N", str(dense_n))
+        m = gpu.Model.from_samples(X.astype(np.int8), gpu.NRG_ISING, lam)
+        m.gcd_iteration(0, kappa=2.0, seed=9)  # a non-empty state (existing edges)
+        m.begin_generation()
+        m.reset_counters()
+        fb, tr, sc = m.find_best(gpu.NRG_EXACT, m_, nodes, seed=5)
+        c = m.counters()
+        return fb, tr, c["misses"], c["hits"], c["evals"]
+    a, b = run(0), run(1 << 20)
+    assert b[4] < a[4], "the dense path did not run (as many K1 screens as the claim path)"
+    np.testing.assert_array_equal(a[0], b[0])
+    assert list(map(tuple, a[1])) == list(map(tuple, b[1]))
+    assert (a[2], a[3]) == (b[2], b[3])
