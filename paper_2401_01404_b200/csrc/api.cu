@@ -402,6 +402,7 @@ int nrg_counters(nrg_ctx* x, uint64_t* misses, uint64_t* hits, uint64_t* evals, 
 
 int nrg_reset_counters(nrg_ctx* x) {
     return guardx(x, [&] {
+        x->c.flush_timing();
         NRG_CUDA(cudaMemsetAsync(x->c.counters.p, 0, nrg::C_N * 8, x->c.stream));
         for (double& v : x->c.phase_ms) v = 0.0;
         x->c.k1_ms = x->c.k1_launches = x->c.k1_pairs = x->c.k2_ms = x->c.k2_launches = x->c.k2_pairs = 0;
@@ -414,6 +415,7 @@ int nrg_reset_counters(nrg_ctx* x) {
 
 int nrg_phase_times(nrg_ctx* x, double* ms, int32_t cap) {
     return guardx(x, [&] {
+        x->c.flush_timing();
         for (int t = 0; t < nrg::P_N && t < cap; ++t) ms[t] = x->c.phase_ms[t];
     });
 }
@@ -438,6 +440,7 @@ int nrg_timer(nrg_ctx* x, int32_t op, double* ms) {
 
 int nrg_kernel_stats(nrg_ctx* x, double* out, int32_t cap) {
     return guardx(x, [&] {
+        x->c.flush_timing();
         const nrg::Context& c = x->c;
         const double v[11] = {c.k1_ms, c.k1_launches, c.k1_pairs, c.k2_ms, c.k2_launches, c.k2_pairs,
                               (double)(nrg::g_launches.load() - c.launches0), c.tail_rounds, c.tc_launches,

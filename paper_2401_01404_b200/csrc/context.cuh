@@ -150,6 +150,8 @@ struct ScoreOut {
 
 enum Counter { C_MISSES = 0, C_HITS = 1, C_EVALS = 2, C_WARN = 3, C_N = 4 };
 enum Phase { P_SCORE = 0, P_KNN = 1, P_SELECT = 2, P_UPDATE = 3, P_THETA = 4, P_LOGPOST = 5, P_SNAP = 6, P_N = 7 };
+// per-kernel timing tags beyond the phases (K1 screen, K2 refine)
+enum { T_K1 = P_N, T_K2 = P_N + 1 };
 
 struct StreamOwner {  // declared first in Context: destroyed after every DevBuf member
     cudaStream_t s = nullptr;
@@ -188,7 +190,7 @@ struct Context {
     DevBuf Ckeys, Cvals, Ccount;  // Ccount: u64 live
     uint64_t Ccap = 0;
     uint64_t cache_live_host = 0;
-    uint64_t last_survivors = 0;
+    uint64_t cache_live_bound = 0;  // host upper bound on the live count (claims <= reserved)
 
     // dense FindBest level (find_best.cu): the exact distances of every pair of a deep
     // level's node set S_D (row-major upper triangle over positions in S_D), computed once
@@ -213,8 +215,23 @@ struct Context {
     double tc_launches = 0, tc_pairs = 0;  // tensor-core exhaustive screen
     double cache_flushes = 0;              // distance-cache flushes (generation exceeded 2^31 slots)
     uint64_t launches0 = 0;
-    cudaEvent_t kev0 = nullptr, kev1 = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    // Deferred device timing: tic/toc record events on the stream and queue a span;
+    // spans are resolved (event elapsed times added to the phase / kernel totals) by
+    // flush_timing() at API boundaries, so the timers never stall the stream.  Pair
+    // counts known only on the device are copied (asynchronously) into pinned slots.
+    struct Span {
+        int tag;
+        cudaEvent_t a, b;
+        double pairs;
+        int pin;  // pinned count slot (-1: `pairs` is the count)
+    };
+    std::vector<cudaEvent_t> ev_free, ev_used, ev_hold;
+    std::vector<Span> spans;
+    cudaEvent_t ev_open = nullptr;
+    uint64_t* pin_counts = nullptr;  // pinned host slots
+    int pin_next = 0;
+    static constexpr int kPinSlots = 1 << 14;
 
     // scratch
     DevBuf s_a, s_b, s_c, s_d, s_e, s_f, s_g, s_h, s_i, s_j, s_k, s_l, s_m, s_n, s_o;
@@ -250,15 +267,56 @@ struct Context {
     }
     void sync() { NRG_CUDA(cudaStreamSynchronize(stream)); }
 
-    // phase timing (device events around a region on this stream)
-    void tic() { NRG_CUDA(cudaEventRecord(ev0, stream)); }
-    void toc(int phase) {
-        NRG_CUDA(cudaEventRecord(ev1, stream));
-        NRG_CUDA(cudaEventSynchronize(ev1));
-        float ms = 0.f;
-        NRG_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
-        phase_ms[phase] += ms;
+    // phase timing (device events around a region on this stream, resolved lazily)
+    cudaEvent_t take_event() {
+        cudaEvent_t e;
+        if (ev_free.empty()) {
+            NRG_CUDA(cudaEventCreate(&e));
+        } else {
+            e = ev_free.back();
+            ev_free.pop_back();
+        }
+        ev_used.push_back(e);
+        return e;
     }
+    void tic() {
+        ev_open = take_event();
+        NRG_CUDA(cudaEventRecord(ev_open, stream));
+    }
+    void toc(int tag) {
+        if (!ev_open) return;
+        cudaEvent_t b = take_event();
+        NRG_CUDA(cudaEventRecord(b, stream));
+        spans.push_back({tag, ev_open, b, 0.0, -1});
+        if (spans.size() >= 4096 || pin_next >= kPinSlots - 64) flush_timing();
+    }
+    // a kernel-level span: mark() before the launch, span() after (independent of tic/toc)
+    cudaEvent_t mark() {
+        cudaEvent_t a = take_event();
+        ev_hold.push_back(a);
+        NRG_CUDA(cudaEventRecord(a, stream));
+        return a;
+    }
+    void span(int tag, cudaEvent_t a, double pairs, int pin = -1) {
+        cudaEvent_t b = take_event();
+        NRG_CUDA(cudaEventRecord(b, stream));
+        for (size_t t = 0; t < ev_hold.size(); ++t)
+            if (ev_hold[t] == a) {
+                ev_hold[t] = ev_hold.back();
+                ev_hold.pop_back();
+                break;
+            }
+        spans.push_back({tag, a, b, pairs, pin});
+    }
+    // a device count into a pinned slot (stream-ordered, no synchronisation)
+    int pin_count(const void* dptr) {
+        if (!pin_counts) NRG_CUDA(cudaMallocHost(&pin_counts, kPinSlots * 8));
+        if (pin_next >= kPinSlots) flush_timing();
+        const int slot = pin_next++;
+        NRG_CUDA(cudaMemcpyAsync(pin_counts + slot, dptr, 8, cudaMemcpyDeviceToHost, stream));
+        return slot;
+    }
+    void flush_timing();
 };
 
 // ---- state.cu
@@ -293,14 +351,16 @@ void set_line(Context& c, uint64_t n, const double* pos);
 
 // ---- score.cu
 // score a worklist of pairs (s[e], p[e]) against the frozen snapshot
+// n_dev (optional): the worklist length lives on the device, n is then its capacity
 void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uint64_t n,
-                   const ScoreOut& out);
+                   const ScoreOut& out, const unsigned long long* n_dev = nullptr);
 // all pairs of `nodes` (device, n entries): dist[e] for e in the row-major upper triangle
 void score_all_pairs(Context& c, int mode, const int32_t* nodes, uint64_t n, double* dist);
 // tensor-core all-pairs screen (exhaustive_tc.cu); false = not applicable, nothing written
 bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* dist);
 void refine_survivors(Context& c, const int32_t* s, const int32_t* p, const uint64_t* surv, const float* surv_g,
-                      const uint8_t* surv_flag, uint64_t ns, double base, const ScoreOut& out);
+                      const uint8_t* surv_flag, uint64_t ns, double base, const ScoreOut& out,
+                      const unsigned long long* ns_dev = nullptr);
 // cached distance lookups for a batch (probe/claim/score/gather), device arrays
 void distance_batch(Context& c, int mode, const int32_t* i, const int32_t* j, uint64_t n,
                     double* dist);

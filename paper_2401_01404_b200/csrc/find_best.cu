@@ -37,12 +37,120 @@ __device__ __forceinline__ bool trikey_le(const TriKey& x, const TriKey& y) {
     return x.b <= y.b;
 }
 
+// Sorting (dist, a, b) keys takes 16 radix passes over 128 bits.  Node ids need only
+// ib = bits(N - 1) bits and a level's distances span few of the 64 dkey bits, so the
+// keys are packed as ((dkey - dmin) << 2 ib) | (a << ib) | b — the same total order —
+// into 64 or 128 bits and sorted over just the occupied bits (about 10 passes).
+struct Key128 {
+    uint64_t hi, lo;
+};
+struct Key128Decomposer {
+    __host__ __device__ cuda::std::tuple<uint64_t&, uint64_t&> operator()(Key128& k) const { return {k.hi, k.lo}; }
+};
+static int id_bits(const Context& c) {
+    int b = 1;
+    while (b < 32 && (1ull << b) < (uint64_t)c.n) ++b;
+    return b;
+}
+__global__ void dkey_range_kernel(const TriKey* __restrict__ in, uint64_t n, unsigned long long* __restrict__ mm) {
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long d = in[e].d;
+        lo = d < lo ? d : lo;
+        hi = d > hi ? d : hi;
+    }
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o), b = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = a < lo ? a : lo;
+        hi = b > hi ? b : hi;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(&mm[0], lo);
+        atomicMax(&mm[1], hi);
+    }
+}
+template <class K>
+__global__ void pack_trikey_kernel(const TriKey* __restrict__ in, uint64_t n, uint64_t dmin, int ib,
+                                   K* __restrict__ out) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    const TriKey t = in[e];
+    const uint64_t dd = t.d - dmin;
+    const uint64_t ids = ((uint64_t)t.a << ib) | t.b;
+    if constexpr (sizeof(K) == 8) {
+        out[e] = (K)((dd << (2 * ib)) | ids);
+    } else {
+        Key128 k;
+        k.lo = (dd << (2 * ib)) | ids;
+        k.hi = dd >> (64 - 2 * ib);
+        out[e] = k;
+    }
+}
+template <class K>
+__global__ void unpack_trikey_kernel2(const K* __restrict__ in, uint64_t n, uint64_t dmin, int ib,
+                                      TriKey* __restrict__ out) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    uint64_t lo, hi;
+    if constexpr (sizeof(K) == 8) {
+        lo = (uint64_t)in[e];
+        hi = 0;
+    } else {
+        lo = in[e].lo;
+        hi = in[e].hi;
+    }
+    const uint64_t m = (1ull << ib) - 1;
+    TriKey t;
+    t.b = (uint32_t)(lo & m);
+    t.a = (uint32_t)((lo >> ib) & m);
+    t.d = dmin + ((lo >> (2 * ib)) | (2 * ib ? hi << (64 - 2 * ib) : 0));
+    out[e] = t;
+}
+
 static void sort_trikeys(Context& c, TriKey* in, TriKey* out, uint64_t n, DevBuf& tmpb) {
     if (!n) return;
-    size_t bytes = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, bytes, in, out, (int64_t)n, TriKeyDecomposer{}, c.stream);
-    void* tmp = tmpb.ensure(bytes);
-    cub::DeviceRadixSort::SortKeys(tmp, bytes, in, out, (int64_t)n, TriKeyDecomposer{}, c.stream);
+    if (getenv("NRG_SORT_FULL")) {
+        size_t bytes = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, bytes, in, out, (int64_t)n, TriKeyDecomposer{}, c.stream);
+        void* tmp = tmpb.ensure(bytes);
+        cub::DeviceRadixSort::SortKeys(tmp, bytes, in, out, (int64_t)n, TriKeyDecomposer{}, c.stream);
+        NRG_LAUNCH_CHECK();
+        return;
+    }
+    DevBuf mmb, kb;
+    unsigned long long* mm = mmb.as<unsigned long long>(2);
+    const unsigned long long init[2] = {~0ull, 0ull};
+    NRG_CUDA(cudaMemcpyAsync(mm, init, 16, cudaMemcpyHostToDevice, c.stream));
+    dkey_range_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 148 * 4), 256, 0, c.stream>>>(in, n, mm);
+    NRG_LAUNCH_CHECK();
+    unsigned long long h[2];
+    NRG_CUDA(cudaMemcpyAsync(h, mm, 16, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    const int ib = id_bits(c);
+    const uint64_t span = h[1] - h[0];
+    int db = 0;
+    while (db < 64 && (span >> db)) ++db;
+    const int total = db + 2 * ib;
+    const unsigned g = (unsigned)ceil_div(n, 256);
+    if (total <= 64) {
+        uint64_t* k0 = kb.as<uint64_t>(2 * n);
+        uint64_t* k1 = k0 + n;
+        pack_trikey_kernel<uint64_t><<<g, 256, 0, c.stream>>>(in, n, h[0], ib, k0);
+        size_t bytes = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, bytes, k0, k1, (int64_t)n, 0, total, c.stream);
+        void* tmp = tmpb.ensure(bytes);
+        cub::DeviceRadixSort::SortKeys(tmp, bytes, k0, k1, (int64_t)n, 0, total, c.stream);
+        unpack_trikey_kernel2<uint64_t><<<g, 256, 0, c.stream>>>(k1, n, h[0], ib, out);
+    } else {
+        Key128* k0 = kb.as<Key128>(2 * n);
+        Key128* k1 = k0 + n;
+        pack_trikey_kernel<Key128><<<g, 256, 0, c.stream>>>(in, n, h[0], ib, k0);
+        size_t bytes = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, bytes, k0, k1, (int64_t)n, Key128Decomposer{}, 0, total, c.stream);
+        void* tmp = tmpb.ensure(bytes);
+        cub::DeviceRadixSort::SortKeys(tmp, bytes, k0, k1, (int64_t)n, Key128Decomposer{}, 0, total, c.stream);
+        unpack_trikey_kernel2<Key128><<<g, 256, 0, c.stream>>>(k1, n, h[0], ib, out);
+    }
     NRG_LAUNCH_CHECK();
 }
 
@@ -75,11 +183,13 @@ __global__ void directed_keys_kernel(const int32_t* __restrict__ nodes, const in
 }
 
 // canonical pair keys of D+ with an index back into the sorted directed list
-__global__ void dplus_pairkeys_kernel(const TriKey* __restrict__ dir, uint64_t m2, uint64_t* __restrict__ pk,
+// canonical pair (min << ib) | max: equal exactly for equal pairs, sorted over 2 ib bits
+__global__ void dplus_pairkeys_kernel(const TriKey* __restrict__ dir, uint64_t m2, int ib, uint64_t* __restrict__ pk,
                                       uint32_t* __restrict__ idx) {
     const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= m2) return;
-    pk[e] = pair_key((int32_t)dir[e].a, (int32_t)dir[e].b);
+    const uint64_t a = dir[e].a, b = dir[e].b;
+    pk[e] = a < b ? (a << ib) | b : (b << ib) | a;
     idx[e] = (uint32_t)e;
 }
 
@@ -118,11 +228,11 @@ __global__ void saturated_kernel(const int32_t* __restrict__ nodes, const int32_
     flag[li] = all ? 1 : 0;
 }
 
-__global__ void trikey_pk_kernel(const TriKey* __restrict__ in, uint64_t n, uint64_t* __restrict__ pk,
+__global__ void trikey_pk_kernel(const TriKey* __restrict__ in, uint64_t n, int ib, uint64_t* __restrict__ pk,
                                  uint32_t* __restrict__ idx) {
     const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= n) return;
-    pk[e] = ((uint64_t)in[e].a << 32) | in[e].b;
+    pk[e] = ((uint64_t)in[e].a << ib) | in[e].b;
     idx[e] = (uint32_t)e;
 }
 __global__ void gather_trikey_kernel(const TriKey* __restrict__ in, const uint32_t* __restrict__ idx,
@@ -210,22 +320,20 @@ struct DenseGuard {  // the level that set up the dense root tears it down (also
                                                                 static_cast<const uint32_t*>(c.dbits.p),
                                                                 (pairs + 31) / 32, c.dense_n, c.dcounters());
             c.dense_active = false;
-            c.dense_n = 0;
-            c.dtri.release();
-            c.dbits.release();
+            c.dense_n = 0;  // the buffers stay (grow-only): the next generation reuses them
         }
     }
 };
 
 static uint64_t dense_max_n() {
     const char* e = getenv("NRG_DENSE_N");
-    return e ? (uint64_t)strtoull(e, nullptr, 10) : 16384;
+    return e ? (uint64_t)strtoull(e, nullptr, 10) : 32768;
 }
 // a level goes dense when its candidate sets (up to cap^2 per node) cover at least
 // 1/ratio of the level
 static uint64_t dense_ratio() {
     const char* e = getenv("NRG_DENSE_RATIO");
-    return e ? (uint64_t)strtoull(e, nullptr, 10) : 4;
+    return e ? (uint64_t)strtoull(e, nullptr, 10) : 32;
 }
 
 static inline unsigned g256(uint64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div(n, 256)); }
@@ -242,11 +350,12 @@ static uint64_t merge_select(Context& c, TriKey* buf, uint64_t n, uint64_t want,
     TriKey* uniq = ub.as<TriKey>(n);
     unsigned long long* cnt = cntb.as<unsigned long long>(1);
     if (n) {
-        trikey_pk_kernel<<<g256(n), 256, 0, c.stream>>>(buf, n, pk, idx);
+        const int ib = id_bits(c);
+        trikey_pk_kernel<<<g256(n), 256, 0, c.stream>>>(buf, n, ib, pk, idx);
         size_t bytes = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, bytes, pk, pk2, idx, idx2, (int64_t)n, 0, 64, c.stream);
+        cub::DeviceRadixSort::SortPairs(nullptr, bytes, pk, pk2, idx, idx2, (int64_t)n, 0, 2 * ib, c.stream);
         void* tmp = tmpb.ensure(bytes);
-        cub::DeviceRadixSort::SortPairs(tmp, bytes, pk, pk2, idx, idx2, (int64_t)n, 0, 64, c.stream);
+        cub::DeviceRadixSort::SortPairs(tmp, bytes, pk, pk2, idx, idx2, (int64_t)n, 0, 2 * ib, c.stream);
         unique_flags_kernel<<<g256(n), 256, 0, c.stream>>>(pk2, n, flag);
         NRG_CUDA(cudaMemsetAsync(cnt, 0, 8, c.stream));
         gather_trikey_kernel<<<g256(n), 256, 0, c.stream>>>(buf, idx2, flag, n, uniq, cnt);
@@ -304,11 +413,12 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
         if (!c.dense_active && mode == EXACT && c.kind == ISING && c.world == 1 && n <= dense_max_n() &&
             dense_ratio() * cap * cap >= n) {
             double* tri = c.dtri.as<double>(total);
+            if (getenv("NRG_DEBUG_LEVELS")) c.flush_timing();
             const double ph0 = c.phase_ms[P_SCORE];
             const auto w0 = std::chrono::steady_clock::now();
             const bool ok = score_all_pairs_tc(c, S, n, tri);
             if (getenv("NRG_DEBUG_LEVELS")) {
-                c.sync();
+                c.flush_timing();
                 fprintf(stderr, "dense root level %d: n=%llu setup wall_ms=%.2f score_phase_ms=%.2f ok=%d\n", level,
                         (unsigned long long)n,
                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count(),
@@ -324,8 +434,6 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
                 c.dense_active = true;
                 c.dense_n = n;
                 dg.owner = true;
-            } else {
-                c.dtri.release();
             }
         }
     }
@@ -339,6 +447,7 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
     uint64_t m0 = 0;
     double t0 = 0.0, s0 = 0.0, k20 = 0.0;
     if (dbg) {
+        c.flush_timing();
         NRG_CUDA(cudaMemcpyAsync(&m0, c.dcounters() + C_MISSES, 8, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
         t0 = c.phase_ms[P_KNN];
@@ -348,6 +457,7 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
     find_knn(c, mode, k, S, n, kp, false, knn, kid, kdist);
     if (dbg) {
         uint64_t m1 = 0;
+        c.flush_timing();
         NRG_CUDA(cudaMemcpyAsync(&m1, c.dcounters() + C_MISSES, 8, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
         fprintf(stderr, "level %d: n=%llu k=%d sweeps=%d knn_ms=%.2f score_ms=%.2f unique_pairs=%llu survivors=%.0f\n",
@@ -371,12 +481,13 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
     uint32_t* idx2 = idx2b.as<uint32_t>(dplus);
     uint8_t* flag = flagb.as<uint8_t>(std::max<uint64_t>(dplus, n));
     unsigned long long* cnt = cntb.as<unsigned long long>(2);
-    dplus_pairkeys_kernel<<<g256(dplus), 256, 0, c.stream>>>(dirs, dplus, pk, idx);
+    const int ib = id_bits(c);
+    dplus_pairkeys_kernel<<<g256(dplus), 256, 0, c.stream>>>(dirs, dplus, ib, pk, idx);
     {
         size_t bytes = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, bytes, pk, pk2, idx, idx2, (int64_t)dplus, 0, 64, c.stream);
+        cub::DeviceRadixSort::SortPairs(nullptr, bytes, pk, pk2, idx, idx2, (int64_t)dplus, 0, 2 * ib, c.stream);
         void* tmp = tmpb.ensure(bytes);
-        cub::DeviceRadixSort::SortPairs(tmp, bytes, pk, pk2, idx, idx2, (int64_t)dplus, 0, 64, c.stream);
+        cub::DeviceRadixSort::SortPairs(tmp, bytes, pk, pk2, idx, idx2, (int64_t)dplus, 0, 2 * ib, c.stream);
     }
     unique_flags_kernel<<<g256(dplus), 256, 0, c.stream>>>(pk2, dplus, flag);
     DevBuf dpairsb;

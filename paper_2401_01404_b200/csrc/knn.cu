@@ -1231,10 +1231,19 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                 claim_list_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, c.stream>>>(c.Cview(), sk, qi, qj, nq, slot);
                 NRG_LAUNCH_CHECK();
             }
-            unsigned long long nw = 0;
-            NRG_CUDA(cudaMemcpyAsync(&nw, wcount, 8, cudaMemcpyDeviceToHost, c.stream));
-            c.sync();
-            if (!dense) exchange_and_score(c, mode, sk, nw, X, 0);
+            if (dense) {
+            } else if (c.world == 1) {
+                // claimed count stays on the device: the screen strides over it
+                ScoreOut so;
+                so.cache_vals = c.Cview().vals;
+                so.slot = wsl;
+                score_entries(c, mode, ws, wp, nq + 1, so, wcount);
+            } else {
+                unsigned long long nw = 0;
+                NRG_CUDA(cudaMemcpyAsync(&nw, wcount, 8, cudaMemcpyDeviceToHost, c.stream));
+                c.sync();
+                exchange_and_score(c, mode, sk, nw, X, 0);
+            }
             if (nq) {
                 gather_vals_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, c.stream>>>(
                     dense ? dtri : c.Cview().vals, static_cast<double*>(X.rvals.p), slot, nq, gd + lo * kw);
@@ -1412,13 +1421,21 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                 NRG_LAUNCH_CHECK();
             }
         }
-        unsigned long long nw = 0;
-        NRG_CUDA(cudaMemcpyAsync(&nw, wcount, 8, cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
         c.toc(P_KNN);
-        if (cached && !dense) {
+        unsigned long long nw = 0;
+        if (cached && !dense && c.world == 1) {
+            // claimed count stays on the device: the screen strides over it
+            ScoreOut so;
+            so.cache_vals = c.Cview().vals;
+            so.slot = wsl;
+            score_entries(c, mode, ws, wp, own * capn + 1, so, wcount);
+        } else if (!dense) {
+            NRG_CUDA(cudaMemcpyAsync(&nw, wcount, 8, cudaMemcpyDeviceToHost, c.stream));
+            c.sync();
+        }
+        if (cached && !dense && c.world > 1) {
             exchange_and_score(c, mode, sk, nw, X, 0);
-        } else if (nw && !dense) {
+        } else if (nw && !dense && !cached) {
             ScoreOut so;
             so.cache_vals = flat_d;
             so.slot = wsl;

@@ -77,7 +77,9 @@ __global__ void __launch_bounds__(256, HW == 1 ? 4 : 3) ising_screen_kernel(Isin
                                                               float* __restrict__ surv_g,
                                                               uint8_t* __restrict__ surv_flag,
                                                               unsigned long long* __restrict__ nsurv,
-                                                              uint64_t* counters) {
+                                                              uint64_t* counters,
+                                                              const unsigned long long* __restrict__ n_dev) {
+    if (n_dev) n = min(n, (uint64_t)*n_dev);
     const int lane = threadIdx.x & 31;
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -175,7 +177,8 @@ __global__ void __launch_bounds__(256, HW == 1 ? 4 : 3) ising_screen_kernel(Isin
 // (Mw <= 16) need it to keep every lane busy; longer rows use it to share the per-pair
 // overhead (indices, coupling probe, decision, outputs) between pairs.  Each warp takes
 // 32 consecutive entries per chunk (indices loaded lane-parallel).
-template <int G, int WPL>
+// FULL: Mw == G * WPL (every lane's words exist; sizes and offsets compile-time)
+template <int G, int WPL, bool FULL>
 __global__ void __launch_bounds__(256, WPL == 1 ? 4 : 3) ising_screen_small_kernel(IsingSnap S, HashView W,
                                                                     const int32_t* __restrict__ es,
                                                                     const int32_t* __restrict__ ep, uint64_t n,
@@ -184,15 +187,17 @@ __global__ void __launch_bounds__(256, WPL == 1 ? 4 : 3) ising_screen_small_kern
                                                                     float* __restrict__ surv_g,
                                                                     uint8_t* __restrict__ surv_flag,
                                                                     unsigned long long* __restrict__ nsurv,
-                                                                    uint64_t* counters) {
+                                                                    uint64_t* counters,
+                                                                    const unsigned long long* __restrict__ n_dev) {
+    if (n_dev) n = min(n, (uint64_t)*n_dev);
     constexpr int P = 32 / G;  // pairs per step
+    const uint32_t Mw = FULL ? (uint32_t)(G * WPL) : (uint32_t)S.Mw;
+    const uint32_t Mp = FULL ? (uint32_t)(32 * G * WPL) : (uint32_t)S.Mp;
     const int lane = threadIdx.x & 31, grp = lane / G, r = lane % G;
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     uint32_t Ps[WPL][8], Xs[WPL][8], bs[WPL];
-    unsigned long long bl_s = 0;
     int cur = -1;
-    float4 qs = make_float4(0.f, 0.f, 0.f, 0.f);
     uint64_t evals = 0;
     const float err0 = 4.f * (float)S.M * 5.9604645e-08f;
     const float lam = (float)lambda;
@@ -201,8 +206,10 @@ __global__ void __launch_bounds__(256, WPL == 1 ? 4 : 3) ising_screen_small_kern
         const int len = (int)min((uint64_t)32, n - c0);
         const int li = lane < len ? lane : 0;
         const int my_s = es[c0 + li], my_p = ep[c0 + li];
-        float my_g = 0.f;
-        int my_code = 0;
+        // per-entry operands of the decision, loaded ahead of the step loop
+        const float4 qs = __ldg(&S.Q8[my_s]), qp = __ldg(&S.Q8[my_p]);
+        const unsigned long long bl_s = __ldg(&S.BL[my_s]);
+        int my_v = 0, my_a2 = 0;
         for (int k0 = 0; k0 < len; k0 += P) {
             const int t = k0 + grp;  // this group's entry (offset in the chunk)
             const bool live = t < len;
@@ -211,13 +218,14 @@ __global__ void __launch_bounds__(256, WPL == 1 ? 4 : 3) ising_screen_small_kern
             if (s != cur) {
 #pragma unroll
                 for (int q = 0; q < WPL; ++q) {
-                    const int w = r + G * q;  // word of this lane
-                    if (w < S.Mw) {
-                        const uint4* pp = reinterpret_cast<const uint4*>(S.P8 + ((size_t)s * S.Mw + w) * 8);
+                    const uint32_t w = r + G * q;  // word of this lane
+                    if (FULL || w < Mw) {
+                        const uint64_t sw = (uint64_t)(uint32_t)s * Mw + w;
+                        const uint4* pp = reinterpret_cast<const uint4*>(S.P8 + sw * 8);
                         const uint4 p0 = __ldg(pp), p1 = __ldg(pp + 1);
                         Ps[q][0] = p0.x, Ps[q][1] = p0.y, Ps[q][2] = p0.z, Ps[q][3] = p0.w;
                         Ps[q][4] = p1.x, Ps[q][5] = p1.y, Ps[q][6] = p1.z, Ps[q][7] = p1.w;
-                        bs[q] = __ldg(&S.Xb[(size_t)s * S.Mw + w]);
+                        bs[q] = __ldg(&S.Xb[sw]);
                     } else {
 #pragma unroll
                         for (int j = 0; j < 8; ++j) Ps[q][j] = 0u;
@@ -226,26 +234,22 @@ __global__ void __launch_bounds__(256, WPL == 1 ? 4 : 3) ising_screen_small_kern
 #pragma unroll
                     for (int j = 0; j < 8; ++j) Xs[q][j] = pm1_bytes(bs[q] >> (4 * j));
                 }
-                qs = __ldg(&S.Q8[s]);
-                bl_s = __ldg(&S.BL[s]);
                 cur = s;
             }
             uint4 t0[WPL], t1[WPL];
             uint32_t bp[WPL];
 #pragma unroll
             for (int q = 0; q < WPL; ++q) {
-                const int w = r + G * q;
+                const uint32_t w = r + G * q;
                 t0[q] = t1[q] = make_uint4(0u, 0u, 0u, 0u);
                 bp[q] = 0u;
-                if (w < S.Mw) {
-                    const uint4* tp = reinterpret_cast<const uint4*>(S.T8 + (size_t)p * S.Mp + 32 * w);
+                if (FULL || w < Mw) {
+                    const uint4* tp = reinterpret_cast<const uint4*>(S.T8 + (uint64_t)(uint32_t)p * Mp + 32 * w);
                     t0[q] = __ldg(tp);
                     t1[q] = __ldg(tp + 1);
-                    bp[q] = __ldg(&S.Xb[(size_t)p * S.Mw + w]);
+                    bp[q] = __ldg(&S.Xb[(uint64_t)(uint32_t)p * Mw + w]);
                 }
             }
-            const float4 qp = __ldg(&S.Q8[p]);
-            const double wcur = (bl_s & bloom_bit(p)) ? hash_get(W, pair_key(s, p), 0.0) : 0.0;
             int a1 = 0, a2 = 0, diff = 0;
 #pragma unroll
             for (int q = 0; q < WPL; ++q) {
@@ -264,26 +268,28 @@ __global__ void __launch_bounds__(256, WPL == 1 ? 4 : 3) ising_screen_small_kern
                 v += __shfl_xor_sync(0xffffffffu, v, o);
                 a2 += __shfl_xor_sync(0xffffffffu, a2, o);
             }
-            int code = 3;
-            float g = 0.f;
-            if (wcur == 0.0) {
-                const int dsum = v & 4095;
-                const int asum = (v - dsum) >> 12;
-                const float A = qs.x * (float)(2 * asum - __float_as_int(qs.z));
-                const float B = qp.x * (float)a2;
-                g = (float)(2 * (S.M - 2 * dsum)) - (A + B);
-                const float err = (qs.y + qp.y) * 1.0001f + err0;
-                code = fabsf(g) <= lam - err ? 0 : (fabsf(g) < lam + err ? 2 : 1);
-                if (live && r == 0) ++evals;
-            }
-            // hand each group's result to the lane that owns the entry
+            // hand each group's sums to the lane that owns the entry
             const int src = ((lane - k0) & (P - 1)) * G;
-            const float gg = __shfl_sync(0xffffffffu, g, src);
-            const int cc = __shfl_sync(0xffffffffu, code, src);
+            const int vv = __shfl_sync(0xffffffffu, v, src);
+            const int aa = __shfl_sync(0xffffffffu, a2, src);
             if (lane >= k0 && lane < k0 + P) {
-                my_g = gg;
-                my_code = cc;
+                my_v = vv;
+                my_a2 = aa;
             }
+        }
+        // the decision, one entry per lane: couplings (Bloom-filtered probe), the bound
+        int my_code = 3;
+        float my_g = 0.f;
+        const double wcur = (lane < len && (bl_s & bloom_bit(my_p))) ? hash_get(W, pair_key(my_s, my_p), 0.0) : 0.0;
+        if (wcur == 0.0) {
+            const int dsum = my_v & 4095;
+            const int asum = (my_v - dsum) >> 12;
+            const float A = qs.x * (float)(2 * asum - __float_as_int(qs.z));
+            const float B = qp.x * (float)my_a2;
+            my_g = (float)(2 * (S.M - 2 * dsum)) - (A + B);
+            const float err = (qs.y + qp.y) * 1.0001f + err0;
+            my_code = fabsf(my_g) <= lam - err ? 0 : (fabsf(my_g) < lam + err ? 2 : 1);
+            if (lane < len) ++evals;
         }
         const uint64_t e = c0 + lane;
         if (lane < len && my_code == 0) {
@@ -324,10 +330,12 @@ __global__ void __launch_bounds__(128) ising_refine_kernel(IsingSnap S, HashView
                                                             const float* __restrict__ surv_g,
                                                             const uint8_t* __restrict__ surv_flag, uint64_t ns,
                                                             double lambda, double base, ScoreOut out,
-                                                            uint64_t* counters) {
+                                                            uint64_t* counters,
+                                                            const unsigned long long* __restrict__ ns_dev) {
+    if (ns_dev) ns = min(ns, (uint64_t)*ns_dev);
     const int lane = threadIdx.x & 31;
-    const uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (t >= ns) return;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ns; t += nwarps) {
     const uint64_t e = surv[t];
     const int s = es[e], p = ep[e];
     const int a = s < p ? s : p, b = s < p ? p : s;
@@ -361,6 +369,7 @@ __global__ void __launch_bounds__(128) ising_refine_kernel(IsingSnap S, HashView
             atomicAdd((unsigned long long*)&counters[C_EVALS], (unsigned long long)r.passes);
             if (r.warn) atomicAdd((unsigned long long*)&counters[C_WARN], 1ull);
         }
+    }
     }
 }
 
@@ -442,27 +451,36 @@ static int num_sms(Context& c) {
     return sms;
 }
 
-// K2 over a survivor list (entries surv[t] of the worklist (s, p)), timed into k2_*
+// K2 over a survivor list (entries surv[t] of the worklist (s, p)), timed into k2_*.
+// ns_dev: the survivor count lives on the device (ns is then the list's capacity); the
+// grid strides over it, so no host round trip sits between K1 and K2.
 void refine_survivors(Context& c, const int32_t* s, const int32_t* p, const uint64_t* surv, const float* surv_g,
-                      const uint8_t* surv_flag, uint64_t ns, double base, const ScoreOut& out) {
+                      const uint8_t* surv_flag, uint64_t ns, double base, const ScoreOut& out,
+                      const unsigned long long* ns_dev) {
     if (!ns) return;
-    NRG_CUDA(cudaEventRecord(c.kev0, c.stream));
-    const unsigned rb = (unsigned)ceil_div((int64_t)ns * 32, 128);
-    ising_refine_kernel<<<rb, 128, 0, c.stream>>>(c.isnap(), c.Wview(), s, p, surv, surv_g, surv_flag, ns, c.lambda,
-                                                  base, out, c.dcounters());
+    const cudaEvent_t a = c.mark();
+    const uint64_t rb = std::min<uint64_t>(ceil_div((int64_t)ns * 32, 128), (uint64_t)num_sms(c) * 16);
+    ising_refine_kernel<<<(unsigned)rb, 128, 0, c.stream>>>(c.isnap(), c.Wview(), s, p, surv, surv_g, surv_flag, ns,
+                                                            c.lambda, base, out, c.dcounters(), ns_dev);
     NRG_LAUNCH_CHECK();
-    NRG_CUDA(cudaEventRecord(c.kev1, c.stream));
-    NRG_CUDA(cudaEventSynchronize(c.kev1));
-    float ms = 0.f;
-    NRG_CUDA(cudaEventElapsedTime(&ms, c.kev0, c.kev1));
-    c.k2_ms += ms;
-    c.k2_launches += 1;
-    c.k2_pairs += (double)ns;
+    if (ns_dev)
+        c.span(T_K2, a, 0.0, c.pin_count(ns_dev));
+    else
+        c.span(T_K2, a, (double)ns);
 }
 
 void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uint64_t n,
-                   const ScoreOut& out) {
+                   const ScoreOut& out, const unsigned long long* n_dev) {
     if (n == 0) return;
+    if (n_dev && !(c.kind == ISING && mode == EXACT && (c.Mp + 1023) / 1024 <= 2)) {
+        // only the screen takes a device-side count: settle it here for the other paths
+        unsigned long long h = 0;
+        NRG_CUDA(cudaMemcpyAsync(&h, n_dev, 8, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        n = std::min<uint64_t>(n, h);
+        n_dev = nullptr;
+        if (n == 0) return;
+    }
     c.tic();
     if (mode == TABLE || mode == LINE) {
         if (mode == TABLE && !c.table_n) fail(22, "no distance table set");
@@ -491,26 +509,28 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
         uint8_t* surv_flag = c.sc_flag.as<uint8_t>(n);
         unsigned long long* nsurv = c.sc_n.as<unsigned long long>(1);
         NRG_CUDA(cudaMemsetAsync(nsurv, 0, 8, c.stream));
-        NRG_CUDA(cudaEventRecord(c.kev0, c.stream));
+        const cudaEvent_t k1a = c.mark();
 #define NRG_LAUNCH_MQ(Q)                                                                              \
     ising_screen_kernel<Q><<<(unsigned)blocks, 256, 0, c.stream>>>(S, W, s, p, n, chunk, c.lambda, base, \
                                                                     out, surv, surv_g, surv_flag, nsurv,   \
-                                                                    c.dcounters())
+                                                                    c.dcounters(), n_dev)
         const int G = c.Mw <= 4 ? 4 : (c.Mw <= 8 ? 8 : 16);
         const int WPL = (c.Mw + G - 1) / G;  // 1, 2 (M <= 1024) or up to 4 (M <= 2048)
         if (!getenv("NRG_K1_WIDE") && (WPL == 1 || (WPL == 2 && !getenv("NRG_K1_ONE_PAIR")))) {
             const uint64_t sblocks = std::min<uint64_t>(ceil_div(n, 8 * 32), (uint64_t)sms * 16);
-#define NRG_LAUNCH_SMALL(GG, WW)                                                                             \
-    ising_screen_small_kernel<GG, WW><<<(unsigned)sblocks, 256, 0, c.stream>>>(S, W, s, p, n, c.lambda, base, \
-                                                                             out, surv, surv_g, surv_flag,    \
-                                                                             nsurv, c.dcounters())
+#define NRG_LAUNCH_SMALL(GG, WW, FF)                                                                          \
+    ising_screen_small_kernel<GG, WW, FF><<<(unsigned)sblocks, 256, 0, c.stream>>>(S, W, s, p, n, c.lambda,   \
+                                                                                 base, out, surv, surv_g,      \
+                                                                                 surv_flag, nsurv,             \
+                                                                                 c.dcounters(), n_dev)
+            const bool full = c.Mw == G * WPL && !getenv("NRG_K1_NOFULL");
             if (WPL == 2) {
-                NRG_LAUNCH_SMALL(16, 2);
+                if (full) NRG_LAUNCH_SMALL(16, 2, true); else NRG_LAUNCH_SMALL(16, 2, false);
             } else {
                 switch (G) {
-                    case 4: NRG_LAUNCH_SMALL(4, 1); break;
-                    case 8: NRG_LAUNCH_SMALL(8, 1); break;
-                    default: NRG_LAUNCH_SMALL(16, 1); break;
+                    case 4: if (full) NRG_LAUNCH_SMALL(4, 1, true); else NRG_LAUNCH_SMALL(4, 1, false); break;
+                    case 8: if (full) NRG_LAUNCH_SMALL(8, 1, true); else NRG_LAUNCH_SMALL(8, 1, false); break;
+                    default: if (full) NRG_LAUNCH_SMALL(16, 1, true); else NRG_LAUNCH_SMALL(16, 1, false); break;
                 }
             }
 #undef NRG_LAUNCH_SMALL
@@ -523,22 +543,12 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
         }
 #undef NRG_LAUNCH_MQ
         NRG_LAUNCH_CHECK();
-        NRG_CUDA(cudaEventRecord(c.kev1, c.stream));
-        unsigned long long ns = 0;
-        NRG_CUDA(cudaMemcpyAsync(&ns, nsurv, 8, cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
-        {
-            float ms = 0.f;
-            NRG_CUDA(cudaEventElapsedTime(&ms, c.kev0, c.kev1));
-            c.k1_ms += ms;
-            c.k1_launches += 1;
-            c.k1_pairs += (double)n;
-            if (getenv("NRG_DEBUG_K1"))
-                fprintf(stderr, "K1 launch %d: %llu pairs, %llu survivors, %.3f ms\n", (int)c.k1_launches - 1,
-                        (unsigned long long)n, (unsigned long long)ns, ms);
-        }
-        c.last_survivors = ns;
-        if (ns) refine_survivors(c, s, p, surv, surv_g, surv_flag, ns, base, out);
+        if (n_dev)
+            c.span(T_K1, k1a, 0.0, c.pin_count(n_dev));
+        else
+            c.span(T_K1, k1a, (double)n);
+        // K2 strides over the device-side survivor count (no host round trip)
+        refine_survivors(c, s, p, surv, surv_g, surv_flag, n, base, out, nsurv);
     } else {
         const uint64_t blocks = std::min<uint64_t>((n + 7) / 8, (uint64_t)sms * 16);
         generic_score_kernel<<<(unsigned)blocks, 256, 0, c.stream>>>(

@@ -16,12 +16,40 @@ namespace nrg {
 Context::~Context() {
     if (device >= 0) cudaSetDevice(device);
     // DevBuf members release themselves; the device must be current for cudaFree
-    if (ev0) cudaEventDestroy(ev0);
-    if (ev1) cudaEventDestroy(ev1);
-    if (kev0) cudaEventDestroy(kev0);
-    if (kev1) cudaEventDestroy(kev1);
+    if (stream) cudaStreamSynchronize(stream);
+    for (cudaEvent_t e : ev_free) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_used) cudaEventDestroy(e);
+    if (pin_counts) cudaFreeHost(pin_counts);
     tl_stream = stream;  // members free in stream order; StreamOwner destroys the stream last
     delete static_cast<Comm*>(comm);
+}
+
+void Context::flush_timing() {
+    if (!spans.empty() || pin_next) NRG_CUDA(cudaStreamSynchronize(stream));
+    for (const Span& sp : spans) {
+        float ms = 0.f;
+        NRG_CUDA(cudaEventElapsedTime(&ms, sp.a, sp.b));
+        const double cnt = sp.pin >= 0 ? (double)pin_counts[sp.pin] : sp.pairs;
+        if (sp.tag < P_N) {
+            phase_ms[sp.tag] += ms;
+        } else if (sp.tag == T_K1) {
+            k1_ms += ms;
+            k1_launches += 1;
+            k1_pairs += cnt;
+        } else if (sp.tag == T_K2) {
+            k2_ms += ms;
+            k2_launches += 1;
+            k2_pairs += cnt;
+        }
+    }
+    spans.clear();
+    pin_next = 0;
+    // every event but the open one (a tic still waiting for its toc) is free again
+    std::vector<cudaEvent_t> keep(ev_hold);
+    if (ev_open) keep.push_back(ev_open);
+    for (cudaEvent_t e : ev_used)
+        if (std::find(keep.begin(), keep.end(), e) == keep.end()) ev_free.push_back(e);
+    ev_used = keep;
 }
 
 static uint64_t next_pow2(uint64_t v) {
@@ -49,10 +77,6 @@ void ctx_init(Context& c, int n, int m, int kind, double lambda, int device) {
         uint64_t thr = UINT64_MAX;
         NRG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     }
-    NRG_CUDA(cudaEventCreate(&c.ev0));
-    NRG_CUDA(cudaEventCreate(&c.ev1));
-    NRG_CUDA(cudaEventCreate(&c.kev0));
-    NRG_CUDA(cudaEventCreate(&c.kev1));
     // Mp = 256 * HQ: one 16-byte fp16 load per lane per 256 samples in the Ising screen
     // (score.cu instantiates HQ = 1..8, i.e. M <= 2048; larger M uses the fp64 path)
     c.Mp = 256 * (int)std::max<int64_t>(1, ceil_div(m, 256));
@@ -611,6 +635,16 @@ __global__ void cache_rehash_kernel(const uint64_t* __restrict__ ok, const doubl
 }
 
 void cache_reserve(Context& c, uint64_t extra) {
+    const uint64_t kMax = 1ull << 31;
+    // claims never exceed what was reserved: while the host bound fits, no readback
+    if (c.Ccap) {
+        const uint64_t b = c.cache_live_bound + extra;
+        if (b * 10 <= c.Ccap * 6 || (c.Ccap == kMax && b * 100 <= kMax * 85)) {
+            c.cache_live_bound = b;
+            c.cache_live_host = c.cache_live_bound - extra;
+            return;
+        }
+    }
     uint64_t live = 0;
     if (c.Ccap) {
         NRG_CUDA(cudaMemcpyAsync(&live, c.Ccount.p, 8, cudaMemcpyDeviceToHost, c.stream));
@@ -619,8 +653,8 @@ void cache_reserve(Context& c, uint64_t extra) {
     c.cache_live_host = live;
     // load factor <= 0.6; slot indices are 31-bit (bit 31 flags remote slots), so at the
     // 2^31-slot ceiling the table runs up to 0.85 full (longer probes, still exact)
-    const uint64_t kMax = 1ull << 31;
     uint64_t need = live + extra;
+    c.cache_live_bound = need;
     if (c.Ccap && (need * 10 <= c.Ccap * 6 || (c.Ccap == kMax && need * 100 <= kMax * 85))) return;
     if (need * 100 > kMax * 85 && c.Ccap && live) {
         // the generation's pairs no longer fit 31-bit slots: flush the memo.  Callers
@@ -633,6 +667,7 @@ void cache_reserve(Context& c, uint64_t extra) {
         c.cache_flushes += 1;
         c.cache_live_host = live = 0;
         need = extra;
+        c.cache_live_bound = need;
         if (need * 10 <= c.Ccap * 6 || (c.Ccap == kMax && need * 100 <= kMax * 85)) return;
     }
     const uint64_t ncap = std::max<uint64_t>(1u << 20, std::min<uint64_t>(next_pow2(2 * need), kMax));
@@ -675,17 +710,15 @@ void begin_generation(Context& c) {
         NRG_CUDA(cudaMemsetAsync(c.Ccount.p, 0, 8, c.stream));
     }
     c.cache_live_host = 0;
+    c.cache_live_bound = 0;
     c.base_valid = false;
 }
 
+__global__ void add_u64_kernel(unsigned long long* p, unsigned long long v) { *p += v; }
+
 void counters_add_host(Context& c, int which, uint64_t v) {
-    uint64_t h = 0;
-    uint64_t* d = c.dcounters() + which;
-    NRG_CUDA(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
-    h += v;
-    NRG_CUDA(cudaMemcpyAsync(d, &h, 8, cudaMemcpyHostToDevice, c.stream));
-    c.sync();
+    add_u64_kernel<<<1, 1, 0, c.stream>>>((unsigned long long*)(c.dcounters() + which), (unsigned long long)v);
+    NRG_LAUNCH_CHECK();
 }
 
 void set_table(Context& c, uint64_t n, const double* t) {

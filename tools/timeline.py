@@ -1,0 +1,51 @@
+"""GPU timeline of one steady-state config-4 sweep through torch.profiler (CUPTI): kernel
+busy time vs wall, and the largest idle gaps with the kernels either side of them."""
+import json, os, sys
+sys.path.insert(0, os.getcwd())
+import numpy as np
+import torch
+from torch.profiler import profile, ProfilerActivity
+import paper_2401_01404_b200 as P
+N, M = 100000, 1000
+lam = float(2 * np.sqrt(M * np.log(N)))
+m = P.Model(N, M, P.NRG_ISING, lam)
+m.generate_ising(mean_deg=5.0, seed=1)
+m.reset_state()
+for it in range(3):
+    m.gcd_iteration(it, kappa=2.0, seed=1)
+torch.cuda.synchronize()
+with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+    m.timer_start()
+    m.gcd_iteration(3, kappa=2.0, seed=1)
+    ms = m.timer_stop()
+out = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/timeline.json"
+prof.export_chrome_trace(out)
+ev = json.load(open(out))["traceEvents"]
+k = sorted([e for e in ev if e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")], key=lambda e: e["ts"])
+rt = [e for e in ev if e.get("cat") == "cuda_runtime"]
+busy = sum(e["dur"] for e in k)
+span = (k[-1]["ts"] + k[-1]["dur"] - k[0]["ts"]) if k else 0
+print(f"sweep ms (events) {ms:.2f}; kernels+copies {len(k)}; busy {busy/1e3:.2f} ms; span {span/1e3:.2f} ms")
+gaps = []
+for a, b in zip(k, k[1:]):
+    g = b["ts"] - (a["ts"] + a["dur"])
+    gaps.append((g, a["name"][:50], b["name"][:50]))
+gaps.sort(reverse=True)
+tot = sum(g for g, _, _ in gaps if g > 0)
+print(f"idle total {tot/1e3:.2f} ms over {sum(1 for g, _, _ in gaps if g > 5)} gaps > 5us")
+hist = {}
+for g, a, b in gaps:
+    key = (a.split('<')[0].split('(')[0], b.split('<')[0].split('(')[0])
+    hist.setdefault(key, [0, 0.0])
+    hist[key][0] += 1
+    hist[key][1] += max(g, 0)
+for key, (n_, t) in sorted(hist.items(), key=lambda x: -x[1][1])[:25]:
+    print(f"{t/1e3:8.2f} ms {n_:5d}x  {key[0]:40s} -> {key[1]}")
+rc = {}
+for e in rt:
+    rc.setdefault(e["name"], [0, 0.0])
+    rc[e["name"]][0] += 1
+    rc[e["name"]][1] += e["dur"]
+print("runtime API:")
+for name, (n_, t) in sorted(rc.items(), key=lambda x: -x[1][1])[:15]:
+    print(f"{t/1e3:8.2f} ms {n_:6d}x {name}")
