@@ -183,6 +183,8 @@ struct Context {
     // snapshot
     DevBuf T32, T64, T8, P8, Q8, BL, Tsq, U, xx;
     uint64_t snap_version = 0;
+    uint64_t lp_version = 0;  // log_posterior memo (state version it was computed at)
+    double lp_value = 0.0;
     bool base_valid = false;
     double base = 0.0;
 
@@ -201,6 +203,12 @@ struct Context {
     bool dense_active = false;
     uint64_t dense_n = 0;
     DevBuf dtri, dloc, dbits;
+    // Lazy K2 at the dense root: the screen's survivors (the pairs K2 must refine) sit in
+    // the triangle as NaN-boxed indices into this worklist and are refined only when a
+    // dense level first probes them (dense_resolve_*, exhaustive_tc.cu).
+    DevBuf dwl_es, dwl_ep, dwl_slot, dwl_sg, dwl_sf;
+    uint64_t dwl_n = 0;
+    DevBuf dres_idx, dres_g, dres_f, dres_cnt;
 
     // test metrics
     DevBuf table, line;
@@ -357,7 +365,44 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
 // all pairs of `nodes` (device, n entries): dist[e] for e in the row-major upper triangle
 void score_all_pairs(Context& c, int mode, const int32_t* nodes, uint64_t n, double* dist);
 // tensor-core all-pairs screen (exhaustive_tc.cu); false = not applicable, nothing written
-bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* dist);
+// use_cache: pairs already in this generation's distance cache take the cached value
+// lazy (dense root): survivors are left as markers for dense_resolve_* (worklist kept
+// in the Context) instead of being refined here
+bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* dist, bool use_cache = false,
+                        bool lazy = false);
+// Lazy K2 resolution: kernels that meet a triangle slot call dense_resolve_slot (claims a
+// marked pair for refinement); dense_resolve_end refines what was claimed.  Distances of
+// those slots are valid after dense_resolve_end.
+struct DenseResolve {
+    double* tri = nullptr;  // null: nothing marked (no lazy worklist)
+    const float* sg = nullptr;
+    const uint8_t* sf = nullptr;
+    uint64_t* idx = nullptr;
+    float* g = nullptr;
+    uint8_t* f = nullptr;
+    unsigned long long* cnt = nullptr;
+};
+constexpr unsigned long long kMarkTag = 0x7ff4ull << 48, kBusyTag = 0x7ff2ull << 48;
+__device__ __forceinline__ void dense_resolve_slot(const DenseResolve& R, uint32_t s) {
+    if (!R.tri) return;
+    unsigned long long* p = reinterpret_cast<unsigned long long*>(R.tri) + s;
+    const unsigned long long v = __ldcg(p);
+    if ((v & (0xffffull << 48)) != kMarkTag) return;
+    if (atomicCAS(p, v, (v & 0xffffffffffffull) | kBusyTag) != v) return;
+    const uint64_t t = v & 0xffffffffffffull;
+    const unsigned long long at = atomicAdd(R.cnt, 1ull);
+    R.idx[at] = t;
+    R.g[at] = R.sg[t];
+    R.f[at] = R.sf[t];
+}
+DenseResolve dense_resolve_begin(Context& c);
+void dense_resolve_end(Context& c);
+// the marked pairs among: a flat slot list / NNDescent candidate rows / every pair of a
+// subset of the root (the FindBest base case below a dense root)
+void dense_resolve_slots(Context& c, const uint32_t* slots, uint64_t n);
+void dense_resolve_rows(Context& c, const uint32_t* cand_slot, const int32_t* cand_cnt, uint64_t lo, uint64_t own,
+                        uint64_t capn);
+void dense_resolve_subtri(Context& c, const int32_t* nodes, uint64_t n);
 void refine_survivors(Context& c, const int32_t* s, const int32_t* p, const uint64_t* surv, const float* surv_g,
                       const uint8_t* surv_flag, uint64_t ns, double base, const ScoreOut& out,
                       const unsigned long long* ns_dev = nullptr);

@@ -313,6 +313,86 @@ __global__ void tc_edges_kernel(HashView W, uint64_t wcap, const int32_t* __rest
     sg[at] = 0.f;
     sf[at] = 2;
 }
+// pairs this generation already scored (distance cache hits) take the cached value; the
+// rest form the K2 worklist (values are deterministic: a re-score would give the same)
+__global__ void tc_cache_filter_kernel(HashView C, const int32_t* __restrict__ es, const int32_t* __restrict__ ep,
+                                       const uint32_t* __restrict__ slot, const float* __restrict__ sg,
+                                       const uint8_t* __restrict__ sf, uint64_t nw, double* __restrict__ dist,
+                                       uint64_t* __restrict__ idx2, float* __restrict__ sg2,
+                                       uint8_t* __restrict__ sf2, unsigned long long* __restrict__ cnt) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool keep = false;
+    if (t < nw) {
+        const uint64_t key = pair_key(es[t], ep[t]);
+        uint64_t s = slot_of(key, C.mask);
+        keep = true;
+        for (;;) {
+            const uint64_t k = C.keys[s];
+            if (k == key) {
+                dist[slot[t]] = C.vals[s];
+                keep = false;
+                break;
+            }
+            if (k == kEmptyKey) break;
+            s = (s + 1) & C.mask;
+        }
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, keep);
+    const int lane = threadIdx.x & 31;
+    unsigned long long at = 0;
+    if (lane == 0 && b) at = atomicAdd(cnt, (unsigned long long)__popc(b));
+    at = __shfl_sync(0xffffffffu, at, 0);
+    if (keep) {
+        const uint64_t o = at + __popc(b & ((1u << lane) - 1u));
+        idx2[o] = t;
+        sg2[o] = sg[t];
+        sf2[o] = sf[t];
+    }
+}
+// lazy mode: a survivor's slot holds its worklist index, NaN-boxed (or the cached value)
+__global__ void tc_mark_kernel(HashView C, const int32_t* __restrict__ es, const int32_t* __restrict__ ep,
+                               const uint32_t* __restrict__ slot, uint64_t nw, double* __restrict__ dist) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nw) return;
+    if (C.keys) {
+        const uint64_t key = pair_key(es[t], ep[t]);
+        uint64_t s = slot_of(key, C.mask);
+        for (;;) {
+            const uint64_t k = C.keys[s];
+            if (k == key) {
+                dist[slot[t]] = C.vals[s];
+                return;
+            }
+            if (k == kEmptyKey) break;
+            s = (s + 1) & C.mask;
+        }
+    }
+    reinterpret_cast<unsigned long long*>(dist)[slot[t]] = kMarkTag | t;
+}
+__global__ void resolve_slots_kernel(DenseResolve R, const uint32_t* __restrict__ slots, uint64_t n) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) dense_resolve_slot(R, slots[t]);
+}
+__global__ void resolve_rows_kernel(DenseResolve R, const uint32_t* __restrict__ cand_slot,
+                                    const int32_t* __restrict__ cand_cnt, uint64_t lo, uint64_t own, uint64_t capn) {
+    const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= own) return;
+    const uint64_t li = lo + w;
+    const int cnt = cand_cnt[li];
+    for (int t = lane; t < cnt; t += 32) dense_resolve_slot(R, cand_slot[li * capn + t]);
+}
+__global__ void resolve_subtri_kernel(DenseResolve R, const int32_t* __restrict__ nodes, uint64_t n,
+                                      const int32_t* __restrict__ loc, uint64_t dn) {
+    const uint64_t a = blockIdx.x;
+    if (a >= n) return;
+    const uint64_t ra = (uint64_t)loc[nodes[a]];
+    for (uint64_t b = a + 1 + threadIdx.x; b < n; b += blockDim.x) {
+        const uint64_t rb = (uint64_t)loc[nodes[b]];
+        const uint64_t lo = ra < rb ? ra : rb, hi = ra < rb ? rb : ra;
+        dense_resolve_slot(R, (uint32_t)(lo * (2 * dn - lo - 1) / 2 + (hi - lo - 1)));
+    }
+}
 __global__ void tc_loc_kernel(const int32_t* __restrict__ nodes, uint64_t n, int32_t* __restrict__ loc) {
     const uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (a < n) loc[nodes[a]] = (int32_t)a;
@@ -352,7 +432,7 @@ static CUtensorMap tile_map(void* base, uint64_t rows, uint64_t row_bytes) {
 // The tensor-core exhaustive screen for Ising exact distances of all pairs of `nodes`
 // (row-major upper triangle, as score_all_pairs).  Returns false (nothing written) when
 // the shape is outside what it handles, so the caller takes the CUDA-core path.
-bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* dist) {
+bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* dist, bool use_cache, bool lazy) {
     using namespace tc;
     if (c.kind != ISING || n < 2 || n > 65535 || getenv("NRG_NO_TC")) return false;
     ensure_snapshot(c);
@@ -422,15 +502,101 @@ bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* di
     NRG_CUDA(cudaMemcpyAsync(&nw, out.ns, 8, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
     c.toc(P_SCORE);
-    if (nw) {
+    if (lazy) {
+        // survivors stay in the triangle as markers; the worklist moves to the Context
+        if (nw) {
+            tc_mark_kernel<<<(unsigned)ceil_div(nw, 256), 256, 0, c.stream>>>(
+                (use_cache && c.Ckeys.p && c.Ccap) ? c.Cview() : HashView{nullptr, nullptr, 0}, es, ep, slot, nw,
+                dist);
+            NRG_LAUNCH_CHECK();
+        }
+        c.dwl_es = std::move(esb);
+        c.dwl_ep = std::move(epb);
+        c.dwl_slot = std::move(slb);
+        c.dwl_sg = std::move(sgb);
+        c.dwl_sf = std::move(sfb);
+        c.dwl_n = nw;
+        c.dres_idx.as<uint64_t>(nw + 1);
+        c.dres_g.as<float>(nw + 1);
+        c.dres_f.as<uint8_t>(nw + 1);
+        c.dres_cnt.as<unsigned long long>(1);
+    } else if (nw) {
         ScoreOut so;
         so.cache_vals = dist;
         so.slot = slot;
-        refine_survivors(c, es, ep, idx, out.sg, out.sf, nw, base, so);
+        if (use_cache && c.Ckeys.p && c.Ccap) {
+            DevBuf i2b, g2b, f2b, cb;
+            uint64_t* idx2 = i2b.as<uint64_t>(nw);
+            float* sg2 = g2b.as<float>(nw);
+            uint8_t* sf2 = f2b.as<uint8_t>(nw);
+            unsigned long long* cnt = cb.as<unsigned long long>(1);
+            NRG_CUDA(cudaMemsetAsync(cnt, 0, 8, c.stream));
+            tc_cache_filter_kernel<<<(unsigned)ceil_div(nw, 256), 256, 0, c.stream>>>(
+                c.Cview(), es, ep, slot, out.sg, out.sf, nw, dist, idx2, sg2, sf2, cnt);
+            NRG_LAUNCH_CHECK();
+            refine_survivors(c, es, ep, idx2, sg2, sf2, nw, base, so, cnt);
+        } else {
+            refine_survivors(c, es, ep, idx, out.sg, out.sf, nw, base, so);
+        }
     }
     c.tc_launches += 1;
     c.tc_pairs += (double)pairs;
     return true;
+}
+
+}  // namespace nrg
+
+namespace nrg {
+using namespace tc;
+
+DenseResolve dense_resolve_begin(Context& c) {
+    DenseResolve R;
+    if (!c.dwl_n) return R;
+    R.tri = static_cast<double*>(c.dtri.p);
+    R.sg = static_cast<const float*>(c.dwl_sg.p);
+    R.sf = static_cast<const uint8_t*>(c.dwl_sf.p);
+    R.idx = static_cast<uint64_t*>(c.dres_idx.p);
+    R.g = static_cast<float*>(c.dres_g.p);
+    R.f = static_cast<uint8_t*>(c.dres_f.p);
+    R.cnt = static_cast<unsigned long long*>(c.dres_cnt.p);
+    NRG_CUDA(cudaMemsetAsync(R.cnt, 0, 8, c.stream));
+    return R;
+}
+// K2 over the pairs the resolve calls claimed (count on the device)
+void dense_resolve_end(Context& c) {
+    if (!c.dwl_n) return;
+    ScoreOut so;
+    so.cache_vals = static_cast<double*>(c.dtri.p);
+    so.slot = static_cast<const uint32_t*>(c.dwl_slot.p);
+    refine_survivors(c, static_cast<const int32_t*>(c.dwl_es.p), static_cast<const int32_t*>(c.dwl_ep.p),
+                     static_cast<const uint64_t*>(c.dres_idx.p), static_cast<const float*>(c.dres_g.p),
+                     static_cast<const uint8_t*>(c.dres_f.p), c.dwl_n, generation_base(c), so,
+                     static_cast<const unsigned long long*>(c.dres_cnt.p));
+}
+
+void dense_resolve_slots(Context& c, const uint32_t* slots, uint64_t n) {
+    if (!c.dwl_n || !n) return;
+    const DenseResolve R = dense_resolve_begin(c);
+    resolve_slots_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(R, slots, n);
+    NRG_LAUNCH_CHECK();
+    dense_resolve_end(c);
+}
+void dense_resolve_rows(Context& c, const uint32_t* cand_slot, const int32_t* cand_cnt, uint64_t lo, uint64_t own,
+                        uint64_t capn) {
+    if (!c.dwl_n || !own) return;
+    const DenseResolve R = dense_resolve_begin(c);
+    resolve_rows_kernel<<<(unsigned)ceil_div(own * 32, 256), 256, 0, c.stream>>>(R, cand_slot, cand_cnt, lo, own,
+                                                                                capn);
+    NRG_LAUNCH_CHECK();
+    dense_resolve_end(c);
+}
+void dense_resolve_subtri(Context& c, const int32_t* nodes, uint64_t n) {
+    if (!c.dwl_n || n < 2) return;
+    const DenseResolve R = dense_resolve_begin(c);
+    resolve_subtri_kernel<<<(unsigned)n, 256, 0, c.stream>>>(R, nodes, n, static_cast<const int32_t*>(c.dloc.p),
+                                                            c.dense_n);
+    NRG_LAUNCH_CHECK();
+    dense_resolve_end(c);
 }
 
 }  // namespace nrg

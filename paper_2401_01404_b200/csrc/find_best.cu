@@ -321,6 +321,7 @@ struct DenseGuard {  // the level that set up the dense root tears it down (also
                                                                 (pairs + 31) / 32, c.dense_n, c.dcounters());
             c.dense_active = false;
             c.dense_n = 0;  // the buffers stay (grow-only): the next generation reuses them
+            c.dwl_n = 0;
         }
     }
 };
@@ -384,6 +385,7 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
         DevBuf distb, keysb, tmpb;
         TriKey* keys = keysb.as<TriKey>(total);
         if (mode == EXACT && c.dense_active && c.world == 1) {
+            dense_resolve_subtri(c, S, n);
             c.tic();
             dense_subtri_kernel<<<(unsigned)n, 256, 0, c.stream>>>(S, n, static_cast<const int32_t*>(c.dloc.p),
                                                                   static_cast<const double*>(c.dtri.p), c.dense_n,
@@ -416,7 +418,7 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
             if (getenv("NRG_DEBUG_LEVELS")) c.flush_timing();
             const double ph0 = c.phase_ms[P_SCORE];
             const auto w0 = std::chrono::steady_clock::now();
-            const bool ok = score_all_pairs_tc(c, S, n, tri);
+            const bool ok = score_all_pairs_tc(c, S, n, tri, true, !getenv("NRG_DENSE_EAGER"));
             if (getenv("NRG_DEBUG_LEVELS")) {
                 c.flush_timing();
                 fprintf(stderr, "dense root level %d: n=%llu setup wall_ms=%.2f score_phase_ms=%.2f ok=%d\n", level,

@@ -1244,6 +1244,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                 c.sync();
                 exchange_and_score(c, mode, sk, nw, X, 0);
             }
+            if (dense) dense_resolve_slots(c, slot, nq);  // refine the marked pairs first
             if (nq) {
                 gather_vals_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, c.stream>>>(
                     dense ? dtri : c.Cview().vals, static_cast<double*>(X.rvals.p), slot, nq, gd + lo * kw);
@@ -1441,6 +1442,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             so.slot = wsl;
             score_entries(c, mode, ws, wp, nw, so);
         }
+        if (dense) dense_resolve_rows(c, cand_slot, cand_cnt, lo, own, capn);  // refine the marked pairs first
         const double* dvals = dense ? dtri : cached ? c.Cview().vals : flat_d;
         const double* rvals = static_cast<double*>(X.rvals.p);
         c.tic();

@@ -3,6 +3,8 @@
 //
 // Reference: inc/sparse_weights.hpp (SparseWeights), inc/model.hpp:133-162
 // (log_posterior), :404-416 (make_empty_state), :36-97 (DistanceCache).
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -303,23 +305,60 @@ void w_reserve(Context& c, uint64_t extra) {
     c.Wcap = ncap;
 }
 
+// live couplings, compacted on the device with packed keys (i << ib) | j (ib = bits of N - 1)
+__global__ void w_live_kernel(const uint64_t* __restrict__ keys, const double* __restrict__ vals, uint64_t cap,
+                              int ib, uint64_t* __restrict__ okey, double* __restrict__ oval,
+                              unsigned long long* __restrict__ cnt) {
+    const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t k = s < cap ? keys[s] : kEmptyKey;
+    const bool live = k < kTombKey;
+    const unsigned b = __ballot_sync(0xffffffffu, live);
+    const int lane = threadIdx.x & 31;
+    unsigned long long at = 0;
+    if (lane == 0 && b) at = atomicAdd(cnt, (unsigned long long)__popc(b));
+    at = __shfl_sync(0xffffffffu, at, 0);
+    if (live) {
+        const uint64_t t = at + __popc(b & ((1u << lane) - 1u));
+        okey[t] = ((k >> 32) << ib) | (k & 0xffffffffu);
+        oval[t] = vals[s];
+    }
+}
+
 void get_state(Context& c, double* theta, uint64_t cap, int32_t* ei, int32_t* ej, double* w,
                uint64_t* n_edges) {
-    std::vector<uint64_t> keys(c.Wcap);
-    std::vector<double> vals(c.Wcap);
-    NRG_CUDA(cudaMemcpyAsync(keys.data(), c.Wkeys.p, c.Wcap * 8, cudaMemcpyDeviceToHost, c.stream));
-    NRG_CUDA(cudaMemcpyAsync(vals.data(), c.Wvals.p, c.Wcap * 8, cudaMemcpyDeviceToHost, c.stream));
     if (theta) NRG_CUDA(cudaMemcpyAsync(theta, c.theta.p, c.n * 8, cudaMemcpyDeviceToHost, c.stream));
+    int ib = 1;
+    while (ib < 31 && (1ll << ib) < (long long)c.n) ++ib;
+    DevBuf kb, vb, cb, tb;
+    uint64_t* k0 = kb.as<uint64_t>(2 * c.Wcap);
+    double* v0 = vb.as<double>(2 * c.Wcap);
+    unsigned long long* cnt = cb.as<unsigned long long>(1);
+    NRG_CUDA(cudaMemsetAsync(cnt, 0, 8, c.stream));
+    w_live_kernel<<<(unsigned)ceil_div(c.Wcap, 256), 256, 0, c.stream>>>(
+        static_cast<const uint64_t*>(c.Wkeys.p), static_cast<const double*>(c.Wvals.p), c.Wcap, ib, k0, v0, cnt);
+    NRG_LAUNCH_CHECK();
+    unsigned long long ne = 0;
+    NRG_CUDA(cudaMemcpyAsync(&ne, cnt, 8, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
-    std::vector<std::pair<uint64_t, double>> e;
-    for (uint64_t s = 0; s < c.Wcap; ++s)
-        if (keys[s] < kTombKey) e.emplace_back(keys[s], vals[s]);
-    std::sort(e.begin(), e.end());  // pair_key order == (i, j) order
-    *n_edges = e.size();
-    for (uint64_t t = 0; t < e.size() && t < cap; ++t) {
-        if (ei) ei[t] = (int32_t)(e[t].first >> 32);
-        if (ej) ej[t] = (int32_t)(e[t].first & 0xffffffffu);
-        if (w) w[t] = e[t].second;
+    *n_edges = ne;
+    const uint64_t take = std::min<uint64_t>(ne, cap);
+    if (!take || !(ei || ej || w)) return;
+    // (i, j) order == pair_key order (inc/sparse_weights.hpp rows are read back sorted)
+    uint64_t* k1 = k0 + c.Wcap;
+    double* v1 = v0 + c.Wcap;
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, k0, k1, v0, v1, (int64_t)ne, 0, 2 * ib, c.stream);
+    void* tmp = tb.ensure(bytes);
+    cub::DeviceRadixSort::SortPairs(tmp, bytes, k0, k1, v0, v1, (int64_t)ne, 0, 2 * ib, c.stream);
+    NRG_LAUNCH_CHECK();
+    std::vector<uint64_t> hk(take);
+    NRG_CUDA(cudaMemcpyAsync(hk.data(), k1, take * 8, cudaMemcpyDeviceToHost, c.stream));
+    if (w) NRG_CUDA(cudaMemcpyAsync(w, v1, take * 8, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    const uint64_t m = (1ull << ib) - 1;
+    for (uint64_t t = 0; t < take; ++t) {
+        if (ei) ei[t] = (int32_t)(hk[t] >> ib);
+        if (ej) ej[t] = (int32_t)(hk[t] & m);
     }
 }
 
@@ -582,6 +621,9 @@ __global__ void __launch_bounds__(256) w_abs_partial_kernel(const uint64_t* __re
 
 double log_posterior(Context& c) {
     if (!c.have_samples) fail(22, "no samples uploaded");
+    // memo per state version: the GCD loop's objective after a sweep is the next
+    // generation's base (inc/reconstruct.hpp:174-176, inc/model.hpp:73-81), same state
+    if (c.lp_version == c.state_version) return c.lp_value;
     c.tic();
     double* part = c.red.as<double>((size_t)c.n + 1024 + 8);
     double* res = part + c.n + 1024;
@@ -601,6 +643,8 @@ double log_posterior(Context& c) {
     c.toc(P_LOGPOST);
     const double acc = h[0] - c.lambda * h[1];
     if (!std::isfinite(acc)) fail(75, "log_posterior is not finite");
+    c.lp_version = c.state_version;
+    c.lp_value = acc;
     return acc;
 }
 
@@ -697,9 +741,11 @@ void begin_generation(Context& c) {
         uint64_t live = 0;
         NRG_CUDA(cudaMemcpyAsync(&live, c.Ccount.p, 8, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
+        // (shrinks too: clearing and scanning an oversized memo costs HBM time every sweep)
         const uint64_t want = std::min<uint64_t>(live + live / 10 * 3, (1ull << 31) * 6 / 10);
-        if (want * 10 > c.Ccap * 6) {
-            const uint64_t ncap = std::min<uint64_t>(next_pow2(want * 10 / 6 + 1), 1ull << 31);
+        const uint64_t ncap =
+            std::max<uint64_t>(1u << 20, std::min<uint64_t>(next_pow2(want * 10 / 6 + 1), 1ull << 31));
+        if (ncap != c.Ccap) {
             c.Ckeys = DevBuf();
             c.Cvals = DevBuf();
             c.Ckeys.ensure(ncap * 8);

@@ -572,30 +572,55 @@ __global__ void __launch_bounds__(256) theta_kernel(int kind, const uint32_t* __
             d2 = -gg;
             return sx - g;
         };
+        // Safeguarded Newton on the concave objective over [-20, 20] (the reference's
+        // golden_max bracket, inc/model.hpp:222-241), warm-started from the current theta:
+        // between sweeps theta moves little, so two or three passes reach the root.
+        // Near the bracket ends fp64 tanh saturates (f' can be exactly 0 on a flat
+        // stretch), so there the from-scratch procedure decides: boundary optima (f' of
+        // one sign over the whole bracket) are returned exactly, as golden_max does.
         double d2;
-        int passes = 2;
-        double res;
-        const double ghi = deriv(20.0, d2);
-        if (ghi >= 0.0) {
-            res = 20.0;
-        } else {
-            const double glo = deriv(-20.0, d2);
-            if (glo <= 0.0) {
-                res = -20.0;
-            } else {
-                double lo = -20.0, hi = 20.0, th = 0.0;
-                double g = deriv(th, d2);
-                for (int it = 0; it < 100; ++it) {
-                    ++passes;
-                    if (g > 0.0) lo = th; else hi = th;
-                    double tn = th - g / d2;
-                    if (!(tn > lo && tn < hi) || !isfinite(tn)) tn = 0.5 * (lo + hi);
-                    const bool done = fabs(tn - th) <= 1e-13 * fmax(1.0, fabs(tn)) || hi - lo <= 1e-14;
-                    th = tn;
-                    if (done) break;
-                    g = deriv(th, d2);
-                }
+        int passes = 0;
+        double res = 0.0;
+        {
+            double lo = -20.0, hi = 20.0;
+            double th = fmin(19.0, fmax(-19.0, theta_in[i]));
+            if (!isfinite(th)) th = 0.0;
+            for (int it = 0; it < 100; ++it) {
+                const double g = deriv(th, d2);
+                ++passes;
+                if (g > 0.0) lo = th; else if (g < 0.0) hi = th; else { res = th; break; }
+                double tn = th - g / d2;
+                if (!(tn > lo && tn < hi) || !isfinite(tn)) tn = 0.5 * (lo + hi);
+                const bool done = fabs(tn - th) <= 1e-13 * fmax(1.0, fabs(tn)) || hi - lo <= 1e-14;
+                th = tn;
                 res = th;
+                if (done || fabs(th) > 15.0) break;
+            }
+        }
+        if (fabs(res) > 15.0) {
+            const double ghi = deriv(20.0, d2);
+            passes += 2;
+            if (ghi >= 0.0) {
+                res = 20.0;
+            } else {
+                const double glo = deriv(-20.0, d2);
+                if (glo <= 0.0) {
+                    res = -20.0;
+                } else {
+                    double lo = -20.0, hi = 20.0, th = 0.0;
+                    double g = deriv(th, d2);
+                    for (int it = 0; it < 100; ++it) {
+                        ++passes;
+                        if (g > 0.0) lo = th; else hi = th;
+                        double tn = th - g / d2;
+                        if (!(tn > lo && tn < hi) || !isfinite(tn)) tn = 0.5 * (lo + hi);
+                        const bool done = fabs(tn - th) <= 1e-13 * fmax(1.0, fabs(tn)) || hi - lo <= 1e-14;
+                        th = tn;
+                        if (done) break;
+                        g = deriv(th, d2);
+                    }
+                    res = th;
+                }
             }
         }
         if (lane == 0) {
@@ -643,7 +668,6 @@ void theta_pass(Context& c, double* out_only) {
         NRG_CUDA(cudaMemcpyAsync(c.theta.p, out, (size_t)c.n * 8, cudaMemcpyDeviceToDevice, c.stream));
         c.state_version++;
     }
-    c.sync();
     c.toc(P_THETA);
 }
 

@@ -49,3 +49,16 @@ for e in rt:
 print("runtime API:")
 for name, (n_, t) in sorted(rc.items(), key=lambda x: -x[1][1])[:15]:
     print(f"{t/1e3:8.2f} ms {n_:6d}x {name}")
+agg = {}
+for e in k:
+    n = e["name"].replace("void ", "").replace("nrg::", "")
+    if "cub::" in n:
+        n = "cub::" + n.split("::")[-1].split("<")[0][:24] + ("<TriKey>" if "TriKey" in n or "Key128" in n else "")
+    else:
+        n = n.split("(")[0].split("<")[0]
+    agg.setdefault(n, [0, 0.0])
+    agg[n][0] += 1
+    agg[n][1] += e["dur"]
+print("kernels:")
+for n, (c_, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:30]:
+    print(f"{t/1e3:8.3f} ms {c_:5d} {n}")
