@@ -21,6 +21,10 @@
 
 #include "pairscore.cuh"
 
+#ifndef NRG_K1S_MINB
+#define NRG_K1S_MINB 3
+#endif
+
 namespace nrg {
 
 // Register side of the screen for one node: for each 32-sample word w = lane + 32 q
@@ -179,7 +183,7 @@ __global__ void __launch_bounds__(256, HW == 1 ? 4 : 3) ising_screen_kernel(Isin
 // 32 consecutive entries per chunk (indices loaded lane-parallel).
 // FULL: Mw == G * WPL (every lane's words exist; sizes and offsets compile-time)
 template <int G, int WPL, bool FULL>
-__global__ void __launch_bounds__(256, WPL == 1 ? 4 : 3) ising_screen_small_kernel(IsingSnap S, HashView W,
+__global__ void __launch_bounds__(256, WPL == 1 ? 4 : NRG_K1S_MINB) ising_screen_small_kernel(IsingSnap S, HashView W,
                                                                     const int32_t* __restrict__ es,
                                                                     const int32_t* __restrict__ ep, uint64_t n,
                                                                     double lambda, double base, ScoreOut out,
