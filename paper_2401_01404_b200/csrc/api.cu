@@ -166,7 +166,8 @@ int nrg_set_edges(nrg_ctx* x, uint64_t n, const int32_t* ei, const int32_t* ej, 
         int32_t* di = to_dev(x, x->q_i, ei, n);
         int32_t* dj = to_dev(x, x->q_j, ej, n);
         double* dw = to_dev(x, x->q_d, w, n);
-        nrg::apply_updates(x->c, di, dj, n, dw);
+        if (getenv("NRG_NO_BULK_SET") || !nrg::set_edges_bulk(x->c, di, dj, n, dw))
+            nrg::apply_updates(x->c, di, dj, n, dw);
     });
 }
 

@@ -421,6 +421,8 @@ uint64_t sample_scored_pairs(Context& c, uint64_t cap, uint64_t seed, int32_t* o
 double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n,
                      const double* assign, const double* dist = nullptr);
 void theta_pass(Context& c, double* out_only);
+// set_edges into an empty coupling table with distinct pairs (false: not applicable)
+bool set_edges_bulk(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n, const double* w);
 // reconstruct_cd's candidate list: all pairs i < j row-major, constant tie distance
 void all_pairs_list(Context& c, int32_t* ci, int32_t* cj, double* tie);
 

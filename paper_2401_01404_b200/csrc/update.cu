@@ -222,6 +222,118 @@ __global__ void __launch_bounds__(NT, 3) update_kernel(UpdateArgs A) {
     }
 }
 
+// ---------------------------------------------------------------- bulk set_edges
+// set_edges on an empty coupling table with distinct pairs (e.g. a state loaded into a
+// fresh context): the result of the reference's sequential set_edge calls
+// (inc/sparse_weights.hpp:54-85) is, per node i, H_i = sum over its incident pairs in list
+// order of w x_other — each H_i[m] sees exactly the sequential additions, in order — so
+// one pass per node over its incidence list reproduces it bitwise, without the
+// dependency-ordered kernel.
+__global__ void inc_keys_kernel(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj, uint64_t n, int ib,
+                                uint64_t* __restrict__ keys, uint64_t* __restrict__ canon) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    const uint64_t a = (uint64_t)ci[e], b = (uint64_t)cj[e];
+    keys[2 * e] = (a << 32) | e;
+    keys[2 * e + 1] = (b << 32) | e;
+    canon[e] = a < b ? (a << ib) | b : (b << ib) | a;
+}
+__global__ void dup_flag_kernel(const uint64_t* __restrict__ sorted, uint64_t n, int* __restrict__ dup) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e > 0 && e < n && sorted[e] == sorted[e - 1]) *dup = 1;
+}
+__global__ void inc_start_kernel(const uint64_t* __restrict__ sorted, uint64_t ne, uint64_t* __restrict__ start,
+                                 int nnodes) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ne) return;
+    const uint64_t node = sorted[t] >> 32;
+    const uint64_t prev = t ? (sorted[t - 1] >> 32) : (uint64_t)-1;
+    if (node != prev) start[node] = t;
+    if (t == ne - 1) start[nnodes] = ne;  // sentinel read only through the next-start search
+}
+__global__ void bulk_sums_kernel(int kind, const uint32_t* __restrict__ Xb, const double* __restrict__ Xd, int M,
+                                 int Mp, int Mw, const uint64_t* __restrict__ sorted, uint64_t ne,
+                                 const uint64_t* __restrict__ start, const int32_t* __restrict__ ci,
+                                 const int32_t* __restrict__ cj, const double* __restrict__ w,
+                                 double* __restrict__ H) {
+    const int i = blockIdx.x;
+    const uint64_t s0 = start[i];
+    if (s0 == ~0ull) return;  // no incident pair
+    double* Hi = H + (size_t)i * Mp;
+    for (int m = threadIdx.x; m < M; m += blockDim.x) {
+        double acc = Hi[m];
+        for (uint64_t t = s0; t < ne && (sorted[t] >> 32) == (uint64_t)i; ++t) {
+            const uint64_t e = sorted[t] & 0xffffffffu;
+            const int o = ci[e] == i ? cj[e] : ci[e];
+            const double x = kind == ISING ? xsign(Xb[(size_t)o * Mw + (m >> 5)], m & 31) : Xd[(size_t)o * Mp + m];
+            acc = kind == ISING ? acc + w[e] * x : __dadd_rn(acc, __dmul_rn(w[e], x));
+        }
+        Hi[m] = acc;
+    }
+}
+__global__ void bulk_insert_kernel(HashView W, const int32_t* __restrict__ ci, const int32_t* __restrict__ cj,
+                                   const double* __restrict__ w, uint64_t n, unsigned long long* __restrict__ cnt) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n || w[e] == 0.0) return;  // absent and zero: nothing stored
+    const uint64_t key = pair_key(ci[e], cj[e]);
+    uint64_t s = slot_of(key, W.mask);
+    for (;;) {
+        const unsigned long long prev =
+            atomicCAS((unsigned long long*)&W.keys[s], (unsigned long long)kEmptyKey, (unsigned long long)key);
+        if (prev == kEmptyKey) {
+            W.vals[s] = w[e];
+            atomicAdd(&cnt[0], 1ull);
+            atomicAdd(&cnt[1], 1ull);
+            return;
+        }
+        s = (s + 1) & W.mask;
+    }
+}
+
+bool set_edges_bulk(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n, const double* w) {
+    if (n == 0 || n >= (1ull << 31)) return false;
+    uint64_t cnt[2];
+    NRG_CUDA(cudaMemcpyAsync(cnt, c.Wcount.p, 16, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (cnt[1] != 0) return false;  // the table holds (or held) couplings: sequential path
+    int ib = 1;
+    while (ib < 31 && (1ll << ib) < (long long)c.n) ++ib;
+    DevBuf kb, k2b, cb, c2b, sb, db, tb;
+    const uint64_t ne = 2 * n;
+    uint64_t* keys = kb.as<uint64_t>(ne);
+    uint64_t* keys2 = k2b.as<uint64_t>(ne);
+    uint64_t* canon = cb.as<uint64_t>(n);
+    uint64_t* canon2 = c2b.as<uint64_t>(n);
+    int* dup = db.as<int>(1);
+    NRG_CUDA(cudaMemsetAsync(dup, 0, 4, c.stream));
+    inc_keys_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(ci, cj, n, ib, keys, canon);
+    size_t b1 = 0, b2 = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, b1, canon, canon2, (int64_t)n, 0, 2 * ib, c.stream);
+    cub::DeviceRadixSort::SortKeys(nullptr, b2, keys, keys2, (int64_t)ne, 0, 32 + ib, c.stream);
+    void* tmp = tb.ensure(std::max(b1, b2));
+    cub::DeviceRadixSort::SortKeys(tmp, b1, canon, canon2, (int64_t)n, 0, 2 * ib, c.stream);
+    dup_flag_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(canon2, n, dup);
+    NRG_LAUNCH_CHECK();
+    int hdup = 0;
+    NRG_CUDA(cudaMemcpyAsync(&hdup, dup, 4, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (hdup) return false;  // a pair listed twice: its second Delta depends on the first
+    c.tic();
+    w_reserve(c, n);
+    cub::DeviceRadixSort::SortKeys(tmp, b2, keys, keys2, (int64_t)ne, 0, 32 + ib, c.stream);
+    uint64_t* start = sb.as<uint64_t>((uint64_t)c.n + 1);
+    NRG_CUDA(cudaMemsetAsync(start, 0xff, ((uint64_t)c.n + 1) * 8, c.stream));
+    inc_start_kernel<<<(unsigned)ceil_div(ne, 256), 256, 0, c.stream>>>(keys2, ne, start, c.n);
+    bulk_sums_kernel<<<(unsigned)c.n, 256, 0, c.stream>>>(c.kind, c.dXb(), c.dXd(), c.M, c.Mp, c.Mw, keys2, ne, start,
+                                                         ci, cj, w, c.dH());
+    bulk_insert_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(
+        c.Wview(), ci, cj, w, n, static_cast<unsigned long long*>(c.Wcount.p));
+    NRG_LAUNCH_CHECK();
+    c.state_version++;
+    c.toc(P_UPDATE);
+    return true;
+}
+
 __global__ void __launch_bounds__(1024) sum_fixed_kernel(const double* __restrict__ v, uint64_t n,
                                                          double* __restrict__ out) {
     __shared__ double sh[32];

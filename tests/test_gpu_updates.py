@@ -85,6 +85,42 @@ def test_set_edges_sequential_semantics(gpu):
     np.testing.assert_allclose(dev.get_sums(), ref.get_sums(), rtol=0, atol=1e-15)
 
 
+@pytest.mark.parametrize("kind", ["ising", "gauss"])
+def test_bulk_set_edges_equals_sequential(gpu, monkeypatch, kind):
+    """set_edges into an empty table with distinct pairs takes the per-node incidence
+    pass (update.cu set_edges_bulk); its sums, couplings and objective are bitwise those
+    of the sequential set_edge path, and the reference's."""
+    rng = np.random.default_rng(3)
+    n, M = 400, 300
+    X = np.where(rng.random((n, M)) < 0.5, -1.0, 1.0) if kind == "ising" else rng.standard_normal((n, M))
+    K = gpu.NRG_ISING if kind == "ising" else gpu.NRG_GAUSSIAN
+    i = rng.integers(0, n, 5000)
+    j = rng.integers(0, n, 5000)
+    keep = i != j
+    key = np.minimum(i, j)[keep] * n + np.maximum(i, j)[keep]
+    _, first = np.unique(key, return_index=True)
+    first.sort()
+    ei, ej = i[keep][first].astype(np.int32), j[keep][first].astype(np.int32)
+    w = rng.normal(0, 0.2, len(ei))
+    w[::17] = 0.0
+    out = []
+    for bulk in (True, False):
+        if bulk:
+            monkeypatch.delenv("NRG_NO_BULK_SET", raising=False)
+        else:
+            monkeypatch.setenv("NRG_NO_BULK_SET", "1")
+        m = gpu.Model.from_samples(X, K, 1.0)
+        m.set_edges(ei, ej, w)
+        out.append((m.get_sums(), m.get_state(), m.log_posterior()))
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    for a, b in zip(out[0][1][1:], out[1][1][1:]):
+        np.testing.assert_array_equal(a, b)
+    assert out[0][2] == out[1][2]
+    ref = O.CpuModel("orc", X, 0 if kind == "ising" else 1, 1.0)
+    ref.set_edges(ei, ej, w)
+    np.testing.assert_array_equal(out[0][0], ref.get_sums())
+
+
 def test_device_generator_and_full_iteration(gpu):
     """Device Gibbs data (config-1 shape) + two GCD iterations run end to end; the
     objective increases and the edge count is plausible."""
