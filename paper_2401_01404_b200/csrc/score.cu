@@ -320,6 +320,172 @@ __global__ void __launch_bounds__(256, WPL == 1 ? 4 : NRG_K1S_MINB) ising_screen
     if (lane == 0 && counters && evals) atomicAdd((unsigned long long*)&counters[C_EVALS], (unsigned long long)evals);
 }
 
+// K1, software-pipelined (FULL rows only): the partner rows of the next step are copied
+// into shared memory with cp.async while the current step computes, so each warp keeps
+// two steps of partner loads in flight without holding them in registers (the small
+// kernel is bound by the latency of its partner loads at the occupancy its registers
+// allow).  Arithmetic, bound and outputs are those of ising_screen_small_kernel.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+template <int G, int WPL, int NS>
+__global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(IsingSnap S, HashView W,
+                                                                    const int32_t* __restrict__ es,
+                                                                    const int32_t* __restrict__ ep, uint64_t n,
+                                                                    double lambda, double base, ScoreOut out,
+                                                                    uint64_t* __restrict__ surv,
+                                                                    float* __restrict__ surv_g,
+                                                                    uint8_t* __restrict__ surv_flag,
+                                                                    unsigned long long* __restrict__ nsurv,
+                                                                    uint64_t* counters,
+                                                                    const unsigned long long* __restrict__ n_dev) {
+    if (n_dev) n = min(n, (uint64_t)*n_dev);
+    constexpr int P = 32 / G;                      // pairs per step
+    constexpr uint32_t Mw = G * WPL, Mp = 32 * Mw;  // words / bytes of a row
+    constexpr int RB = Mp + 4 * Mw;                 // staged row: int8 field + spin words
+    constexpr int CH = RB / 16;                     // 16-byte chunks per staged row
+    extern __shared__ __align__(16) unsigned char k1p_smem[];
+    const int lane = threadIdx.x & 31, grp = lane / G, r = lane % G;
+    unsigned char* wbuf = k1p_smem + (size_t)(threadIdx.x >> 5) * NS * P * RB;  // [stage][pair][row]
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint32_t Ps[WPL][8], Xs[WPL][8], bs[WPL];
+    int cur = -1;
+    uint64_t evals = 0;
+    const float err0 = 4.f * (float)S.M * 5.9604645e-08f;
+    const float lam = (float)lambda;
+    const double pruned_dist = -(base + 0.0);
+    // stage the partner row of this group's entry into ring buffer `st` (one commit group
+    // per step, empty past the chunk's end, so wait_group counts stay uniform)
+    auto stage = [&](int st, int p, bool any) {
+        unsigned char* dst = wbuf + (size_t)(st * P + grp) * RB;
+        if (!any) {
+            cp_async_commit();
+            return;
+        }
+        const unsigned char* t8 = reinterpret_cast<const unsigned char*>(S.T8) + (uint64_t)(uint32_t)p * Mp;
+        const unsigned char* xb = reinterpret_cast<const unsigned char*>(S.Xb) + (uint64_t)(uint32_t)p * Mw * 4;
+#pragma unroll
+        for (int c = r; c < CH; c += G) {
+            const unsigned char* src = c < (int)(Mp / 16) ? t8 + 16 * c : xb + 16 * (c - (int)(Mp / 16));
+            cp_async16(dst + 16 * c, src);
+        }
+        cp_async_commit();
+    };
+    for (uint64_t c0 = warp0 * 32; c0 < n; c0 += nwarps * 32) {
+        const int len = (int)min((uint64_t)32, n - c0);
+        const int li = lane < len ? lane : 0;
+        const int my_s = es[c0 + li], my_p = ep[c0 + li];
+        const float4 qs = __ldg(&S.Q8[my_s]), qp = __ldg(&S.Q8[my_p]);
+        const unsigned long long bl_s = __ldg(&S.BL[my_s]);
+        int my_v = 0, my_a2 = 0;
+#pragma unroll
+        for (int j = 0; j < NS - 1; ++j) {
+            const int tj = j * P + grp;
+            const int pj = __shfl_sync(0xffffffffu, my_p, tj < len ? tj : 0);
+            stage(j, pj, j * P < len);
+        }
+        for (int k0 = 0, st = 0; k0 < len; k0 += P, st = st + 1 == NS ? 0 : st + 1) {
+            const int t = k0 + grp;
+            const bool live = t < len;
+            const int s = __shfl_sync(0xffffffffu, my_s, live ? t : 0);
+            // the rows NS-1 steps ahead go in flight while this step computes
+            const int ka = k0 + (NS - 1) * P;
+            const int ta = ka + grp;
+            const int pa = __shfl_sync(0xffffffffu, my_p, ta < len ? ta : 0);
+            stage(st == 0 ? NS - 1 : st - 1, pa, ka < len);
+            if (s != cur) {
+#pragma unroll
+                for (int q = 0; q < WPL; ++q) {
+                    const uint32_t w = r + G * q;
+                    const uint64_t sw = (uint64_t)(uint32_t)s * Mw + w;
+                    const uint4* pp = reinterpret_cast<const uint4*>(S.P8 + sw * 8);
+                    const uint4 p0 = __ldg(pp), p1 = __ldg(pp + 1);
+                    Ps[q][0] = p0.x, Ps[q][1] = p0.y, Ps[q][2] = p0.z, Ps[q][3] = p0.w;
+                    Ps[q][4] = p1.x, Ps[q][5] = p1.y, Ps[q][6] = p1.z, Ps[q][7] = p1.w;
+                    bs[q] = __ldg(&S.Xb[sw]);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) Xs[q][j] = pm1_bytes(bs[q] >> (4 * j));
+                }
+                cur = s;
+            }
+            cp_async_wait<NS - 1>();
+            __syncwarp();
+            const unsigned char* row = wbuf + (size_t)(st * P + grp) * RB;
+            int a1 = 0, a2 = 0, diff = 0;
+#pragma unroll
+            for (int q = 0; q < WPL; ++q) {
+                const uint32_t w = r + G * q;
+                const uint4 t0 = *reinterpret_cast<const uint4*>(row + 32 * w);
+                const uint4 t1 = *reinterpret_cast<const uint4*>(row + 32 * w + 16);
+                const uint32_t bp = *reinterpret_cast<const uint32_t*>(row + Mp + 4 * w);
+                int l7 = 0;
+#pragma unroll
+                for (int j = 0; j < 7; ++j) l7 += __popc(Ps[q][j] & bp) << j;
+                a1 += l7 - (__popc(Ps[q][7] & bp) << 7);
+                const uint32_t tw[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+#pragma unroll
+                for (int j = 0; j < 8; ++j) a2 = __dp4a((int)tw[j], (int)Xs[q][j], a2);
+                diff += __popc(bs[q] ^ bp);
+            }
+            __syncwarp();  // the buffer is re-staged NS - 1 steps from now
+            int v = (a1 << 12) + diff;
+#pragma unroll
+            for (int o = G / 2; o; o >>= 1) {
+                v += __shfl_xor_sync(0xffffffffu, v, o);
+                a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+            }
+            const int src = ((lane - k0) & (P - 1)) * G;
+            const int vv = __shfl_sync(0xffffffffu, v, src);
+            const int aa = __shfl_sync(0xffffffffu, a2, src);
+            if (lane >= k0 && lane < k0 + P) {
+                my_v = vv;
+                my_a2 = aa;
+            }
+        }
+        int my_code = 3;
+        float my_g = 0.f;
+        const double wcur = (lane < len && (bl_s & bloom_bit(my_p))) ? hash_get(W, pair_key(my_s, my_p), 0.0) : 0.0;
+        if (wcur == 0.0) {
+            const int dsum = my_v & 4095;
+            const int asum = (my_v - dsum) >> 12;
+            const float A = qs.x * (float)(2 * asum - __float_as_int(qs.z));
+            const float B = qp.x * (float)my_a2;
+            my_g = (float)(2 * (S.M - 2 * dsum)) - (A + B);
+            const float err = (qs.y + qp.y) * 1.0001f + err0;
+            my_code = fabsf(my_g) <= lam - err ? 0 : (fabsf(my_g) < lam + err ? 2 : 1);
+            if (lane < len) ++evals;
+        }
+        const uint64_t e = c0 + lane;
+        if (lane < len && my_code == 0) {
+            if (out.cache_vals) out.cache_vals[out.slot[e]] = pruned_dist;
+            if (out.dist) out.dist[e] = pruned_dist;
+            if (out.w) out.w[e] = 0.0;
+            if (out.gain) out.gain[e] = 0.0;
+            if (out.warn) out.warn[e] = 0;
+        }
+        const unsigned sv = __ballot_sync(0xffffffffu, lane < len && my_code != 0);
+        if (sv) {
+            unsigned long long at = 0;
+            if (lane == 0) at = atomicAdd(nsurv, (unsigned long long)__popc(sv));
+            at = __shfl_sync(0xffffffffu, at, 0);
+            if ((sv >> lane) & 1u) {
+                const unsigned long long i = at + __popc(sv & ((1u << lane) - 1u));
+                surv[i] = e;
+                surv_g[i] = my_g;
+                surv_flag[i] = (uint8_t)(my_code == 1 ? 0 : (my_code == 2 ? 1 : 2));
+            }
+        }
+    }
+    evals = warp_sum((int)evals);
+    if (lane == 0 && counters && evals) atomicAdd((unsigned long long*)&counters[C_EVALS], (unsigned long long)evals);
+}
+
 // K2: survivors.  Certain survivors (w_cur = 0, |g0| > lambda + err) start Newton
 // from K1's fp32 g0 and the per-node sums Tsq = sum T^2 (second derivative at 0 is
 // -(2M - Tsq_a - Tsq_b)), so no pass is spent at w = 0; Newton then runs in fp32 on
@@ -528,7 +694,27 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
                                                                                  surv_flag, nsurv,             \
                                                                                  c.dcounters(), n_dev)
             const bool full = c.Mw == G * WPL && !getenv("NRG_K1_NOFULL");
-            if (WPL == 2) {
+            if (WPL == 2 && full && !getenv("NRG_K1_NOPIPE")) {
+                static const int ns = getenv("NRG_K1_STAGES") ? atoi(getenv("NRG_K1_STAGES")) : 2;
+#define NRG_LAUNCH_PIPE(NSV)                                                                                       \
+    {                                                                                                              \
+        constexpr size_t smem = (size_t)8 * (NSV) * 2 * (1024 + 128);                                             \
+        static bool attr = false;                                                                                  \
+        if (!attr) {                                                                                               \
+            NRG_CUDA(cudaFuncSetAttribute(ising_screen_pipe_kernel<16, 2, NSV>,                                    \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));                \
+            attr = true;                                                                                           \
+        }                                                                                                          \
+        ising_screen_pipe_kernel<16, 2, NSV><<<(unsigned)sblocks, 256, smem, c.stream>>>(                          \
+            S, W, s, p, n, c.lambda, base, out, surv, surv_g, surv_flag, nsurv, c.dcounters(), n_dev);            \
+    }
+                switch (ns) {
+                    case 2: NRG_LAUNCH_PIPE(2); break;
+                    case 3: NRG_LAUNCH_PIPE(3); break;
+                    default: NRG_LAUNCH_PIPE(4); break;
+                }
+#undef NRG_LAUNCH_PIPE
+            } else if (WPL == 2) {
                 if (full) NRG_LAUNCH_SMALL(16, 2, true); else NRG_LAUNCH_SMALL(16, 2, false);
             } else {
                 switch (G) {
