@@ -91,6 +91,44 @@ __global__ void knn_init_kernel(const int32_t* __restrict__ nodes, const int32_t
     }
 }
 
+// the same draws with the membership test on a per-warp bitmap of the picked ranks (small
+// levels with wide rows: O(kw) per node instead of O(kw^2 / 32))
+__global__ void knn_init_bits_kernel(const int32_t* __restrict__ nodes, const int32_t* __restrict__ sorted_ids,
+                                     const int32_t* __restrict__ rank, const int32_t* __restrict__ loc, uint64_t own,
+                                     uint64_t n, int kw, uint64_t seed, int32_t* __restrict__ gid,
+                                     int32_t* __restrict__ qi, int32_t* __restrict__ qj) {
+    extern __shared__ uint32_t init_bits[];
+    const int words = (int)((n + 31) / 32);
+    uint32_t* bm = init_bits + (size_t)(threadIdx.x >> 5) * words;
+    const uint64_t li = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (li >= own) return;
+    for (int w = lane; w < words; w += 32) bm[w] = 0u;
+    __syncwarp();
+    int32_t* picks = gid + li * kw;
+    if (lane == 0) {
+        const SplitRng root(seed);
+        SplitRng r = root.split((uint64_t)nodes[li] + 1);
+        int np = 0;
+        for (uint64_t t = n - 1 - (uint64_t)kw; t < n - 1; ++t) {
+            uint64_t v = r.below(t + 1);
+            if ((bm[v >> 5] >> (v & 31)) & 1u) v = t;
+            bm[v >> 5] |= 1u << (v & 31);
+            picks[np++] = (int32_t)v;
+        }
+    }
+    __syncwarp();
+    const uint64_t self = (uint64_t)rank[li];
+    for (int t = lane; t < kw; t += 32) {
+        uint64_t rk = (uint64_t)picks[t];
+        if (rk >= self) ++rk;
+        const int32_t g = sorted_ids[rk];
+        picks[t] = loc[g];
+        qi[li * kw + t] = nodes[li];
+        qj[li * kw + t] = g;
+    }
+}
+
 // sort each row (kw entries) by (dist, id): one CTA per row, bitonic in shared memory
 template <int NT>
 __global__ void __launch_bounds__(NT) row_sort_kernel(int32_t* __restrict__ gid, double* __restrict__ gd,
@@ -524,6 +562,29 @@ __global__ void sum_counts_kernel(const int32_t* __restrict__ cnt, uint64_t n, u
 // entries that were not in U(j) last sweep).  cand(i) = OR over a in U(i) of
 // (a new in U(i) ? U(a) : new(U(a))) minus i's current row and i itself: the same set
 // the incremental join inserts one by one, without contended shared atomics.
+// bit-set levels: U(i) as a bitset, then the new flags against last sweep's bitset (the
+// set semantics of u_new_kernel, O(1) per entry) and the bitset of new entries
+__global__ void u_set_kernel(const int32_t* __restrict__ adj, const int32_t* __restrict__ alen, uint64_t n, int cap,
+                             int W, uint32_t* __restrict__ ub) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n * (uint64_t)cap) return;
+    const uint64_t i = t / cap;
+    if ((int)(t - i * cap) >= alen[i]) return;
+    const int32_t j = adj[t];
+    atomicOr(&ub[i * W + (j >> 5)], 1u << (j & 31));
+}
+__global__ void u_new_bits_kernel(const int32_t* __restrict__ adj, const int32_t* __restrict__ alen, uint64_t n,
+                                  int cap, int W, const uint32_t* __restrict__ ubp, int first,
+                                  uint8_t* __restrict__ newf, uint32_t* __restrict__ nb) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n * (uint64_t)cap) return;
+    const uint64_t i = t / cap;
+    if ((int)(t - i * cap) >= alen[i]) return;
+    const int32_t j = adj[t];
+    const bool fresh = first || !((ubp[i * W + (j >> 5)] >> (j & 31)) & 1u);
+    newf[t] = fresh ? 1 : 0;
+    if (fresh) atomicOr(&nb[i * W + (j >> 5)], 1u << (j & 31));
+}
 __global__ void u_bits_kernel(const int32_t* __restrict__ adj, const int32_t* __restrict__ alen,
                               const uint8_t* __restrict__ newf, uint64_t n, int cap, int W, uint32_t* __restrict__ ub,
                               uint32_t* __restrict__ nb) {
@@ -1214,8 +1275,12 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         DevBuf qib, qjb, slb;
         int32_t* qi = qib.as<int32_t>(nq + 1);
         int32_t* qj = qjb.as<int32_t>(nq + 1);
-        knn_init_kernel<<<(unsigned)ceil_div(own * 32, 128), 128, 0, c.stream>>>(
-            d_nodes + lo, sorted_ids, rank + lo, loc, own, n, kw, p.seed, gid + lo * kw, qi, qj);
+        if (n <= 16384 && kw >= 64)
+            knn_init_bits_kernel<<<(unsigned)ceil_div(own * 32, 128), 128, 4 * ((n + 31) / 32) * 4, c.stream>>>(
+                d_nodes + lo, sorted_ids, rank + lo, loc, own, n, kw, p.seed, gid + lo * kw, qi, qj);
+        else
+            knn_init_kernel<<<(unsigned)ceil_div(own * 32, 128), 128, 0, c.stream>>>(
+                d_nodes + lo, sorted_ids, rank + lo, loc, own, n, kw, p.seed, gid + lo * kw, qi, qj);
         NRG_LAUNCH_CHECK();
         c.toc(P_KNN);
         if (cached) {
@@ -1278,7 +1343,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
 
     // ---- sweeps
     const uint64_t capn = std::min<uint64_t>((uint64_t)cap * cap, n - 1);
-    DevBuf adjb, alenb, adjpb, alenpb, newfb, cidb, cslb, ccntb, churnb, churnb2, wsb, wpb, wslb, ubitsb, nbitsb;
+    DevBuf adjb, alenb, adjpb, alenpb, newfb, cidb, cslb, ccntb, churnb, churnb2, wsb, wpb, wslb, ubitsb, ubitsb2, nbitsb;
     int32_t* adj = adjb.as<int32_t>(n * cap);
     int32_t* alen = alenb.as<int32_t>(n);
     int32_t* adjp = adjpb.as<int32_t>(n * cap);  // U of the previous sweep
@@ -1360,8 +1425,24 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                                                                            alen, seg);
             NRG_LAUNCH_CHECK();
         }
-        u_new_kernel<<<(unsigned)ceil_div(n * 32, 256), 256, 0, c.stream>>>(adj, alen, adjp, alenp, n, cap,
-                                                                         (sweep == 0 || !incremental) ? 1 : 0, newf);
+        const int Wb = (int)((n + 31) / 32);
+        const bool bitsmode = n <= 16384 && cap >= 32 && !getenv("NRG_KNN_HASH_GATHER");
+        if (bitsmode) {
+            // U bitsets ping-pong between sweeps: last sweep's set answers the new flags
+            uint32_t* ubc = (sweep & 1 ? ubitsb2 : ubitsb).as<uint32_t>(n * (uint64_t)Wb);
+            uint32_t* ubp = (sweep & 1 ? ubitsb : ubitsb2).as<uint32_t>(n * (uint64_t)Wb);
+            uint32_t* nbits = nbitsb.as<uint32_t>(n * (uint64_t)Wb);
+            NRG_CUDA(cudaMemsetAsync(ubc, 0, n * (uint64_t)Wb * 4, c.stream));
+            NRG_CUDA(cudaMemsetAsync(nbits, 0, n * (uint64_t)Wb * 4, c.stream));
+            const unsigned g = (unsigned)ceil_div(n * (uint64_t)cap, 256);
+            u_set_kernel<<<g, 256, 0, c.stream>>>(adj, alen, n, cap, Wb, ubc);
+            u_new_bits_kernel<<<g, 256, 0, c.stream>>>(adj, alen, n, cap, Wb, ubp,
+                                                      (sweep == 0 || !incremental) ? 1 : 0, newf, nbits);
+        } else {
+            u_new_kernel<<<(unsigned)ceil_div(n * 32, 256), 256, 0, c.stream>>>(adj, alen, adjp, alenp, n, cap,
+                                                                             (sweep == 0 || !incremental) ? 1 : 0,
+                                                                             newf);
+        }
         NRG_LAUNCH_CHECK();
         c.toc(P_KNN);
         // gather (own nodes), then — for the cached metric — reserve the distance cache
@@ -1380,14 +1461,10 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             int lw = 0;
             while ((1 << lw) < cap) ++lw;
             const HashView hv0 = fused && cached ? c.Cview() : HashView{nullptr, nullptr, 0};
-            const int W = (int)((n + 31) / 32);
-            if (n <= 16384 && cap >= 32 && !getenv("NRG_KNN_HASH_GATHER")) {
-                uint32_t* ub = ubitsb.as<uint32_t>(n * (uint64_t)W);
-                uint32_t* nbits = nbitsb.as<uint32_t>(n * (uint64_t)W);
-                NRG_CUDA(cudaMemsetAsync(ub, 0, n * (uint64_t)W * 4, c.stream));
-                NRG_CUDA(cudaMemsetAsync(nbits, 0, n * (uint64_t)W * 4, c.stream));
-                u_bits_kernel<<<(unsigned)ceil_div(n * (uint64_t)cap, 256), 256, 0, c.stream>>>(adj, alen, newf, n, cap,
-                                                                                               W, ub, nbits);
+            const int W = Wb;
+            if (bitsmode) {
+                uint32_t* ub = static_cast<uint32_t*>((sweep & 1 ? ubitsb2 : ubitsb).p);
+                uint32_t* nbits = static_cast<uint32_t*>(nbitsb.p);
                 knn_gather_bits_kernel<256><<<(unsigned)own, 256, 2 * W * 4, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, W, ub, nbits, newf, hv0, sk, capn, cand_id, cand_slot, cand_cnt,
                     lo, fused, rootpos);

@@ -72,7 +72,7 @@ def random_table(n, seed):
     return t
 
 
-@pytest.mark.parametrize("n,k,seed", [(120, 5, 1), (300, 8, 2), (500, 3, 3), (257, 12, 4)])
+@pytest.mark.parametrize("n,k,seed", [(120, 5, 1), (300, 8, 2), (500, 3, 3), (257, 12, 4), (700, 40, 5), (900, 96, 6)])
 def test_table_knn_vs_checker(gpu, n, k, seed):
     t = random_table(n, 100 + seed)
     nodes = np.arange(n, dtype=np.int32)
@@ -85,7 +85,7 @@ def test_table_knn_vs_checker(gpu, n, k, seed):
     np.testing.assert_array_equal(a[3], b[3])
 
 
-@pytest.mark.parametrize("n,m_,seed", [(150, 75, 77), (400, 100, 1), (200, 120, 4242), (90, 500, 5)])
+@pytest.mark.parametrize("n,m_,seed", [(150, 75, 77), (400, 100, 1), (200, 120, 4242), (90, 500, 5), (1200, 3000, 9)])
 def test_table_find_best_vs_checker(gpu, n, m_, seed):
     t = random_table(n, seed)
     nodes = np.arange(n, dtype=np.int32)
