@@ -441,9 +441,10 @@ struct KnnResultD {
     int32_t* ids = nullptr;
     double* dists = nullptr;
 };
+// sorted_valid: d_nodes is known strictly ascending and in range (skips sort + validation)
 void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n,
               const KnnParamsD& p, bool exhaustive, KnnResultD& out, DevBuf& ids_buf,
-              DevBuf& dist_buf);
+              DevBuf& dist_buf, bool sorted_valid = false);
 
 // ---- find_best.cu
 struct TraceLevelD {

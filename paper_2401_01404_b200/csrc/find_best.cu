@@ -337,6 +337,12 @@ static uint64_t dense_ratio() {
     return e ? (uint64_t)strtoull(e, nullptr, 10) : 32;
 }
 
+__global__ void ascending_check_kernel(const int32_t* __restrict__ v, uint64_t n, int n_total, int* __restrict__ bad) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    if (v[t] < 0 || v[t] >= n_total || (t > 0 && v[t] <= v[t - 1])) *bad = 1;
+}
+
 static inline unsigned g256(uint64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div(n, 256)); }
 
 // union of two candidate lists without duplicate pairs, then the (dist,i,j)-smallest
@@ -376,7 +382,7 @@ static uint64_t merge_select(Context& c, TriKey* buf, uint64_t n, uint64_t want,
 // result of a level: TriKey list (a<b canonical) sorted by (dist, a, b)
 static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* S, uint64_t n, double knn_eps,
                                uint64_t seed, bool reverse, int level, std::vector<TraceLevelD>& trace,
-                               DevBuf& result) {
+                               DevBuf& result, bool sorted) {
     if (n < 2) return 0;
     const uint64_t total = n * (n - 1) / 2;
     const uint64_t want = std::min(m, total);
@@ -456,7 +462,7 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
         s0 = c.phase_ms[P_SCORE];
         k20 = c.k2_pairs;
     }
-    find_knn(c, mode, k, S, n, kp, false, knn, kid, kdist);
+    find_knn(c, mode, k, S, n, kp, false, knn, kid, kdist, sorted);
     if (dbg) {
         uint64_t m1 = 0;
         c.flush_timing();
@@ -525,7 +531,9 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
     dirb.release();
 
     DevBuf rec;
-    const uint64_t nrec = find_best_impl(c, mode, m, sat, (uint64_t)hsat, knn_eps, seed, reverse, level + 1, trace, rec);
+    // S' keeps S's order (DeviceSelect), so a sorted S gives a sorted S'
+    const uint64_t nrec =
+        find_best_impl(c, mode, m, sat, (uint64_t)hsat, knn_eps, seed, reverse, level + 1, trace, rec, sorted);
     c.tic();
     // merge D with the recursive result (dropping duplicates) and select
     DevBuf allb;
@@ -563,7 +571,17 @@ void find_best(Context& c, int mode, uint64_t m, const int32_t* d_nodes, uint64_
         cnt = std::min(m, total);
         res.trace.push_back({0, 0, 1, 0, n, 0});
     } else {
-        cnt = find_best_impl(c, mode, m, d_nodes, n, knn_eps, seed, reverse, 0, res.trace, result);
+        // a strictly ascending, in-range node list (the GCD loop's 0..N-1) needs no per-level
+        // sort or validation; anything else takes find_knn's checked path
+        DevBuf okb;
+        int* ok = okb.as<int>(1);
+        NRG_CUDA(cudaMemsetAsync(ok, 0, 4, c.stream));
+        ascending_check_kernel<<<g256(n), 256, 0, c.stream>>>(d_nodes, n, c.n, ok);
+        NRG_LAUNCH_CHECK();
+        int hbad = 0;
+        NRG_CUDA(cudaMemcpyAsync(&hbad, ok, 4, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        cnt = find_best_impl(c, mode, m, d_nodes, n, knn_eps, seed, reverse, 0, res.trace, result, hbad == 0);
     }
     res.count = cnt;
     int32_t* oi = out_i.as<int32_t>(std::max<uint64_t>(cnt, 1));

@@ -45,10 +45,10 @@ __global__ void scatter_loc_kernel(const int32_t* __restrict__ nodes, uint64_t n
     if (t >= n) return;
     const int g = nodes[t];
     if (g < 0 || g >= n_total) {
-        atomicExch(bad, 1);
+        if (bad) atomicExch(bad, 1);
         return;
     }
-    if (atomicExch(&loc[g], (int32_t)t) != -1) atomicExch(bad, 2);  // duplicate node
+    if (atomicExch(&loc[g], (int32_t)t) != -1 && bad) atomicExch(bad, 2);  // duplicate node
 }
 __global__ void rank_kernel(const int32_t* __restrict__ perm, uint64_t n, int32_t* __restrict__ rank) {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1154,7 +1154,7 @@ static void score_claimed(Context& c, int mode, int32_t* ws, int32_t* wp, uint32
 }
 
 void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, const KnnParamsD& p,
-              bool exhaustive, KnnResultD& out, DevBuf& ids_buf, DevBuf& dist_buf) {
+              bool exhaustive, KnnResultD& out, DevBuf& ids_buf, DevBuf& dist_buf, bool sorted_valid) {
     if (n < 2) fail(22, exhaustive ? "find_knn_exhaustive: need two nodes" : "find_knn: need at least two nodes");
     if (!exhaustive) {
         if (k < 1) fail(22, "find_knn: k must be >= 1");
@@ -1167,33 +1167,47 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
     // collective in multi-rank jobs: every rank resolves the generation's base here
     if (mode == EXACT) generation_base(c);
 
-    // local index map, id-sorted node set and ranks
+    // local index map, id-sorted node set and ranks.  A node list already strictly
+    // ascending and in range (FindBest's levels: subsets of a sorted list, in order) is
+    // its own sorted order: no sort, no validation round trip.
     int32_t* loc = c.s_a.as<int32_t>(c.n);
-    int* bad = c.s_b.as<int>(1);
     NRG_CUDA(cudaMemsetAsync(loc, 0xff, (size_t)c.n * 4, c.stream));
-    NRG_CUDA(cudaMemsetAsync(bad, 0, 4, c.stream));
-    scatter_loc_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(d_nodes, n, loc, c.n, bad);
-    NRG_LAUNCH_CHECK();
     DevBuf sbuf_ids, sbuf_loc, sbuf_rank, stmp;
-    int32_t* sorted_ids = sbuf_ids.as<int32_t>(n);
-    int32_t* sorted_loc = sbuf_loc.as<int32_t>(n);
-    int32_t* rank = sbuf_rank.as<int32_t>(n);
-    {
-        int32_t* iota = rank;  // temporarily
-        iota_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(iota, n);
-        size_t tmp = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tmp, d_nodes, sorted_ids, iota, sorted_loc, (int)n, 0, 32,
-                                        c.stream);
-        void* dt = stmp.ensure(tmp);
-        cub::DeviceRadixSort::SortPairs(dt, tmp, d_nodes, sorted_ids, iota, sorted_loc, (int)n, 0, 32, c.stream);
-        rank_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(sorted_loc, n, rank);
+    const int32_t* sorted_ids = d_nodes;
+    int32_t* sorted_loc;
+    int32_t* rank;
+    if (sorted_valid) {
+        scatter_loc_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(d_nodes, n, loc, c.n, nullptr);
+        sorted_loc = sbuf_loc.as<int32_t>(n);
+        iota_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(sorted_loc, n);
+        rank = sorted_loc;  // identity
         NRG_LAUNCH_CHECK();
+    } else {
+        int* bad = c.s_b.as<int>(1);
+        NRG_CUDA(cudaMemsetAsync(bad, 0, 4, c.stream));
+        scatter_loc_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(d_nodes, n, loc, c.n, bad);
+        NRG_LAUNCH_CHECK();
+        int32_t* sids = sbuf_ids.as<int32_t>(n);
+        sorted_loc = sbuf_loc.as<int32_t>(n);
+        rank = sbuf_rank.as<int32_t>(n);
+        {
+            int32_t* iota = rank;  // temporarily
+            iota_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(iota, n);
+            size_t tmp = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tmp, d_nodes, sids, iota, sorted_loc, (int)n, 0, 32,
+                                            c.stream);
+            void* dt = stmp.ensure(tmp);
+            cub::DeviceRadixSort::SortPairs(dt, tmp, d_nodes, sids, iota, sorted_loc, (int)n, 0, 32, c.stream);
+            rank_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(sorted_loc, n, rank);
+            NRG_LAUNCH_CHECK();
+        }
+        sorted_ids = sids;
+        int hbad = 0;
+        NRG_CUDA(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        if (hbad == 1) fail(34, "node id out of range");
+        if (hbad == 2) fail(22, "find_knn: duplicate node ids");
     }
-    int hbad = 0;
-    NRG_CUDA(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
-    if (hbad == 1) fail(34, "node id out of range");
-    if (hbad == 2) fail(22, "find_knn: duplicate node ids");
 
     if (exhaustive || (uint64_t)k + 1 >= n) {
         knn_exhaustive(c, mode, (int)std::min<uint64_t>((uint64_t)k, n - 1), d_nodes, n, sorted_loc, rank, out,

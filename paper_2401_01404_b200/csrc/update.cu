@@ -520,6 +520,9 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
                      const double* dist) {
     if (n == 0) return 0.0;
     if (n >= (1ull << 31)) fail(22, "apply_updates: too many candidates");
+    // the snapshot describes the state on entry (FindBest just ran): a tie tail then
+    // needs only the rows the ordered part touches refreshed
+    const bool snap_fresh = c.snap_version == c.state_version;
     c.tic();
     w_reserve(c, n);
     DevBuf adb, sb, kb, wb, fb, ib, pib, pjb, ddb;
@@ -556,7 +559,18 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
                 break;
             }
             c.state_version++;  // the evaluation snapshot must include every update so far
-            if (round > 0) snapshot_rows(c, rows_dev, n_rows);  // only the last round's endpoints changed
+            if (round > 0) {
+                snapshot_rows(c, rows_dev, n_rows);  // only the last round's endpoints changed
+            } else if (snap_fresh && 2 * k < (uint64_t)c.n) {
+                // the ordered part changed only its candidates' endpoints (the generation's
+                // snapshot of every other row still holds; theta moves after the updates)
+                rows_dev = rowsb.as<int32_t>(2 * k + 1);
+                if (k) {
+                    NRG_CUDA(cudaMemcpyAsync(rows_dev, ci, k * 4, cudaMemcpyDeviceToDevice, c.stream));
+                    NRG_CUDA(cudaMemcpyAsync(rows_dev + k, cj, k * 4, cudaMemcpyDeviceToDevice, c.stream));
+                }
+                snapshot_rows(c, rows_dev, 2 * k);
+            }
             const uint64_t m = n - start;
             double* w = wb.as<double>(m);
             ScoreOut out;
