@@ -211,21 +211,18 @@ __global__ void d_pairs_kernel(const TriKey* __restrict__ dir, const uint32_t* _
     out[atomicAdd(cnt, 1ull)] = o;
 }
 
-// S': worst entry of node li (last of its (dist,id)-sorted row) <= threshold key
+// S': every out-entry of node li lies in D+ (inc/find_best.hpp:150-163).  Rows are sorted
+// by (dist, id) and (dist, li, id) orders them the same way, so the last entry decides.
 __global__ void saturated_kernel(const int32_t* __restrict__ nodes, const int32_t* __restrict__ ids,
                                  const double* __restrict__ dists, uint64_t n, int k, TriKey thr,
                                  uint8_t* __restrict__ flag) {
     const uint64_t li = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (li >= n) return;
-    bool all = true;
-    for (int t = 0; t < k && all; ++t) {
-        TriKey x;
-        x.d = dkey(dists[li * k + t]);
-        x.a = (uint32_t)nodes[li];
-        x.b = (uint32_t)ids[li * k + t];
-        all = trikey_le(x, thr);
-    }
-    flag[li] = all ? 1 : 0;
+    TriKey x;
+    x.d = dkey(dists[li * k + (k - 1)]);
+    x.a = (uint32_t)nodes[li];
+    x.b = (uint32_t)ids[li * k + (k - 1)];
+    flag[li] = trikey_le(x, thr) ? 1 : 0;
 }
 
 __global__ void trikey_pk_kernel(const TriKey* __restrict__ in, uint64_t n, int ib, uint64_t* __restrict__ pk,

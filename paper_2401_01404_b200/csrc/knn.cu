@@ -557,7 +557,7 @@ __global__ void sum_counts_kernel(const int32_t* __restrict__ cnt, uint64_t n, u
 }
 
 // ---------------------------------------------------------------- gather, deep levels
-// For small levels with wide rows (n <= 16384 ids, cap >= 32) the 2-hop candidate set
+// For small levels with wide rows (n <= kBitsMaxN ids, cap >= 32) the 2-hop candidate set
 // is an OR of row bitsets: U(j) as a bitset over the level's ids, and new(U(j)) (the
 // entries that were not in U(j) last sweep).  cand(i) = OR over a in U(i) of
 // (a new in U(i) ? U(a) : new(U(a))) minus i's current row and i itself: the same set
@@ -599,6 +599,7 @@ __global__ void u_bits_kernel(const int32_t* __restrict__ adj, const int32_t* __
     if (newf[t]) atomicOr(&nb[i * W + (j >> 5)], bit);
 }
 
+constexpr int kBitsMaxN = 32768;
 template <int NT>
 __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __restrict__ nodes, uint64_t n,
                                                              const int32_t* __restrict__ adj,
@@ -650,7 +651,7 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
     }
     __syncthreads();
     // candidate ids in increasing order: popcounts of the thread's words, block scan
-    constexpr int kMaxWpt = 16384 / 32 / NT + 1;
+    constexpr int kMaxWpt = kBitsMaxN / 32 / NT + 1;
     int cnt = 0;
     uint32_t cw[kMaxWpt];
 #pragma unroll
@@ -1440,7 +1441,10 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             NRG_LAUNCH_CHECK();
         }
         const int Wb = (int)((n + 31) / 32);
-        const bool bitsmode = n <= 16384 && cap >= 32 && !getenv("NRG_KNN_HASH_GATHER");
+        static const uint64_t bits_max_n =
+            getenv("NRG_BITS_MAXN") ? strtoull(getenv("NRG_BITS_MAXN"), nullptr, 10) : (uint64_t)kBitsMaxN;
+        const bool bitsmode = n <= std::min<uint64_t>(bits_max_n, kBitsMaxN) && cap >= 32 &&
+                              !getenv("NRG_KNN_HASH_GATHER");
         if (bitsmode) {
             // U bitsets ping-pong between sweeps: last sweep's set answers the new flags
             uint32_t* ubc = (sweep & 1 ? ubitsb2 : ubitsb).as<uint32_t>(n * (uint64_t)Wb);

@@ -334,6 +334,21 @@ bool set_edges_bulk(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n
     return true;
 }
 
+// distinct endpoints of pairs [0, k): first marker of a node appends it
+__global__ void endpoint_rows_kernel(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj, uint64_t k,
+                                     uint8_t* __restrict__ mark, int32_t* __restrict__ rows,
+                                     unsigned long long* __restrict__ cnt) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= k) return;
+    const int32_t e[2] = {ci[t], cj[t]};
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        unsigned int* w = reinterpret_cast<unsigned int*>(mark + (e[q] & ~3));
+        const unsigned int bit = 1u << (8 * (e[q] & 3));
+        if (!(atomicOr(w, bit) & bit)) rows[atomicAdd(cnt, 1ull)] = e[q];
+    }
+}
+
 __global__ void __launch_bounds__(1024) sum_fixed_kernel(const double* __restrict__ v, uint64_t n,
                                                          double* __restrict__ out) {
     __shared__ double sh[32];
@@ -409,6 +424,11 @@ static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64
         std::vector<uint32_t> start(cnt.size(), 0), hord(n);
         for (size_t l = 1; l < cnt.size(); ++l) start[l] = start[l - 1] + cnt[l - 1];
         for (uint64_t p = 0; p < n; ++p) hord[start[lev[p]]++] = (uint32_t)p;
+        if (getenv("NRG_DEBUG_UPD")) {
+            uint32_t mx = 0;
+            for (uint32_t v : cnt) mx = std::max(mx, v);
+            fprintf(stderr, "ordered_run: n=%llu levels=%zu widest=%u\n", (unsigned long long)n, cnt.size(), mx);
+        }
         order = ordb.as<uint32_t>(n);
         NRG_CUDA(cudaMemcpyAsync(order, hord.data(), 4 * n, cudaMemcpyHostToDevice, c.stream));
         c.sync();
@@ -565,11 +585,22 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
                 // the ordered part changed only its candidates' endpoints (the generation's
                 // snapshot of every other row still holds; theta moves after the updates)
                 rows_dev = rowsb.as<int32_t>(2 * k + 1);
+                uint64_t nr = 0;
                 if (k) {
-                    NRG_CUDA(cudaMemcpyAsync(rows_dev, ci, k * 4, cudaMemcpyDeviceToDevice, c.stream));
-                    NRG_CUDA(cudaMemcpyAsync(rows_dev + k, cj, k * 4, cudaMemcpyDeviceToDevice, c.stream));
+                    // distinct endpoints (a row re-snapshotted once)
+                    uint8_t* mark = fb.as<uint8_t>(std::max<uint64_t>((uint64_t)c.n, n));
+                    unsigned long long* cnt = kb.as<unsigned long long>(1);
+                    NRG_CUDA(cudaMemsetAsync(mark, 0, c.n, c.stream));
+                    NRG_CUDA(cudaMemsetAsync(cnt, 0, 8, c.stream));
+                    endpoint_rows_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, c.stream>>>(ci, cj, k, mark,
+                                                                                          rows_dev, cnt);
+                    NRG_LAUNCH_CHECK();
+                    unsigned long long h = 0;
+                    NRG_CUDA(cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, c.stream));
+                    c.sync();
+                    nr = h;
                 }
-                snapshot_rows(c, rows_dev, 2 * k);
+                snapshot_rows(c, rows_dev, nr);
             }
             const uint64_t m = n - start;
             double* w = wb.as<double>(m);
