@@ -237,7 +237,8 @@ struct Context {
     std::vector<cudaEvent_t> ev_free, ev_used, ev_hold;
     std::vector<Span> spans;
     cudaEvent_t ev_open = nullptr;
-    uint64_t* pin_counts = nullptr;  // pinned host slots
+    uint64_t* pin_counts = nullptr;  // pinned host copy of the count log
+    DevBuf count_log;
     int pin_next = 0;
     static constexpr int kPinSlots = 1 << 14;
 
@@ -316,13 +317,13 @@ struct Context {
             }
         spans.push_back({tag, a, b, pairs, pin});
     }
-    // a device count into a pinned slot (stream-ordered, no synchronisation)
-    int pin_count(const void* dptr) {
+    // a slot of the device count log: the kernel that knows a count writes it there
+    // (no copy in the stream); flush_timing reads the log back once
+    unsigned long long* log_slot(int* slot) {
         if (!pin_counts) NRG_CUDA(cudaMallocHost(&pin_counts, kPinSlots * 8));
         if (pin_next >= kPinSlots) flush_timing();
-        const int slot = pin_next++;
-        NRG_CUDA(cudaMemcpyAsync(pin_counts + slot, dptr, 8, cudaMemcpyDeviceToHost, stream));
-        return slot;
+        *slot = pin_next++;
+        return static_cast<unsigned long long*>(count_log.ensure(kPinSlots * 8)) + *slot;
     }
     void flush_timing();
 };

@@ -82,8 +82,10 @@ __global__ void __launch_bounds__(256, HW == 1 ? 4 : 3) ising_screen_kernel(Isin
                                                               uint8_t* __restrict__ surv_flag,
                                                               unsigned long long* __restrict__ nsurv,
                                                               uint64_t* counters,
-                                                              const unsigned long long* __restrict__ n_dev) {
+                                                              const unsigned long long* __restrict__ n_dev,
+                                                              unsigned long long* __restrict__ cnt_log) {
     if (n_dev) n = min(n, (uint64_t)*n_dev);
+    if (cnt_log && blockIdx.x == 0 && threadIdx.x == 0) *cnt_log = n;
     const int lane = threadIdx.x & 31;
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -192,8 +194,10 @@ __global__ void __launch_bounds__(256, WPL == 1 ? 4 : NRG_K1S_MINB) ising_screen
                                                                     uint8_t* __restrict__ surv_flag,
                                                                     unsigned long long* __restrict__ nsurv,
                                                                     uint64_t* counters,
-                                                                    const unsigned long long* __restrict__ n_dev) {
+                                                                    const unsigned long long* __restrict__ n_dev,
+                                                                    unsigned long long* __restrict__ cnt_log) {
     if (n_dev) n = min(n, (uint64_t)*n_dev);
+    if (cnt_log && blockIdx.x == 0 && threadIdx.x == 0) *cnt_log = n;
     constexpr int P = 32 / G;  // pairs per step
     const uint32_t Mw = FULL ? (uint32_t)(G * WPL) : (uint32_t)S.Mw;
     const uint32_t Mp = FULL ? (uint32_t)(32 * G * WPL) : (uint32_t)S.Mp;
@@ -343,8 +347,10 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
                                                                     uint8_t* __restrict__ surv_flag,
                                                                     unsigned long long* __restrict__ nsurv,
                                                                     uint64_t* counters,
-                                                                    const unsigned long long* __restrict__ n_dev) {
+                                                                    const unsigned long long* __restrict__ n_dev,
+                                                                    unsigned long long* __restrict__ cnt_log) {
     if (n_dev) n = min(n, (uint64_t)*n_dev);
+    if (cnt_log && blockIdx.x == 0 && threadIdx.x == 0) *cnt_log = n;
     constexpr int P = 32 / G;                      // pairs per step
     constexpr uint32_t Mw = G * WPL, Mp = 32 * Mw;  // words / bytes of a row
     constexpr int RB = Mp + 4 * Mw;                 // staged row: int8 field + spin words
@@ -501,8 +507,10 @@ __global__ void __launch_bounds__(128) ising_refine_kernel(IsingSnap S, HashView
                                                             const uint8_t* __restrict__ surv_flag, uint64_t ns,
                                                             double lambda, double base, ScoreOut out,
                                                             uint64_t* counters,
-                                                            const unsigned long long* __restrict__ ns_dev) {
+                                                            const unsigned long long* __restrict__ ns_dev,
+                                                            unsigned long long* __restrict__ cnt_log) {
     if (ns_dev) ns = min(ns, (uint64_t)*ns_dev);
+    if (cnt_log && blockIdx.x == 0 && threadIdx.x == 0) *cnt_log = ns;
     const int lane = threadIdx.x & 31;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t t = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ns; t += nwarps) {
@@ -630,13 +638,12 @@ void refine_survivors(Context& c, const int32_t* s, const int32_t* p, const uint
     if (!ns) return;
     const cudaEvent_t a = c.mark();
     const uint64_t rb = std::min<uint64_t>(ceil_div((int64_t)ns * 32, 128), (uint64_t)num_sms(c) * 16);
+    int slot = -1;
+    unsigned long long* lg = ns_dev ? c.log_slot(&slot) : nullptr;
     ising_refine_kernel<<<(unsigned)rb, 128, 0, c.stream>>>(c.isnap(), c.Wview(), s, p, surv, surv_g, surv_flag, ns,
-                                                            c.lambda, base, out, c.dcounters(), ns_dev);
+                                                            c.lambda, base, out, c.dcounters(), ns_dev, lg);
     NRG_LAUNCH_CHECK();
-    if (ns_dev)
-        c.span(T_K2, a, 0.0, c.pin_count(ns_dev));
-    else
-        c.span(T_K2, a, (double)ns);
+    c.span(T_K2, a, (double)ns, slot);
 }
 
 void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uint64_t n,
@@ -680,10 +687,12 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
         unsigned long long* nsurv = c.sc_n.as<unsigned long long>(1);
         NRG_CUDA(cudaMemsetAsync(nsurv, 0, 8, c.stream));
         const cudaEvent_t k1a = c.mark();
+        int k1slot = -1;
+        unsigned long long* k1log = n_dev ? c.log_slot(&k1slot) : nullptr;
 #define NRG_LAUNCH_MQ(Q)                                                                              \
     ising_screen_kernel<Q><<<(unsigned)blocks, 256, 0, c.stream>>>(S, W, s, p, n, chunk, c.lambda, base, \
                                                                     out, surv, surv_g, surv_flag, nsurv,   \
-                                                                    c.dcounters(), n_dev)
+                                                                    c.dcounters(), n_dev, k1log)
         const int G = c.Mw <= 4 ? 4 : (c.Mw <= 8 ? 8 : 16);
         const int WPL = (c.Mw + G - 1) / G;  // 1, 2 (M <= 1024) or up to 4 (M <= 2048)
         if (!getenv("NRG_K1_WIDE") && (WPL == 1 || (WPL == 2 && !getenv("NRG_K1_ONE_PAIR")))) {
@@ -692,7 +701,7 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
     ising_screen_small_kernel<GG, WW, FF><<<(unsigned)sblocks, 256, 0, c.stream>>>(S, W, s, p, n, c.lambda,   \
                                                                                  base, out, surv, surv_g,      \
                                                                                  surv_flag, nsurv,             \
-                                                                                 c.dcounters(), n_dev)
+                                                                                 c.dcounters(), n_dev, k1log)
             const bool full = c.Mw == G * WPL && !getenv("NRG_K1_NOFULL");
             if (WPL == 2 && full && !getenv("NRG_K1_NOPIPE")) {
                 static const int ns = getenv("NRG_K1_STAGES") ? atoi(getenv("NRG_K1_STAGES")) : 2;
@@ -706,7 +715,7 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
             attr = true;                                                                                           \
         }                                                                                                          \
         ising_screen_pipe_kernel<16, 2, NSV><<<(unsigned)sblocks, 256, smem, c.stream>>>(                          \
-            S, W, s, p, n, c.lambda, base, out, surv, surv_g, surv_flag, nsurv, c.dcounters(), n_dev);            \
+            S, W, s, p, n, c.lambda, base, out, surv, surv_g, surv_flag, nsurv, c.dcounters(), n_dev, k1log);            \
     }
                 switch (ns) {
                     case 2: NRG_LAUNCH_PIPE(2); break;
@@ -733,10 +742,7 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
         }
 #undef NRG_LAUNCH_MQ
         NRG_LAUNCH_CHECK();
-        if (n_dev)
-            c.span(T_K1, k1a, 0.0, c.pin_count(n_dev));
-        else
-            c.span(T_K1, k1a, (double)n);
+        c.span(T_K1, k1a, (double)n, k1slot);
         // K2 strides over the device-side survivor count (no host round trip)
         refine_survivors(c, s, p, surv, surv_g, surv_flag, n, base, out, nsurv);
     } else {

@@ -27,6 +27,8 @@ Context::~Context() {
 }
 
 void Context::flush_timing() {
+    if (pin_next)
+        NRG_CUDA(cudaMemcpyAsync(pin_counts, count_log.p, (size_t)pin_next * 8, cudaMemcpyDeviceToHost, stream));
     if (!spans.empty() || pin_next) NRG_CUDA(cudaStreamSynchronize(stream));
     for (const Span& sp : spans) {
         float ms = 0.f;
