@@ -579,6 +579,7 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
                 break;
             }
             c.state_version++;  // the evaluation snapshot must include every update so far
+            c.toc(P_UPDATE);    // snapshot refreshes time themselves (P_SNAP)
             if (round > 0) {
                 snapshot_rows(c, rows_dev, n_rows);  // only the last round's endpoints changed
             } else if (snap_fresh && 2 * k < (uint64_t)c.n) {
@@ -606,7 +607,6 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
             double* w = wb.as<double>(m);
             ScoreOut out;
             out.w = w;
-            c.toc(P_UPDATE);
             score_entries(c, EXACT, ci + start, cj + start, m, out);  // times itself as P_SCORE
             c.tic();
             uint8_t* ch = fb.as<uint8_t>(m);
