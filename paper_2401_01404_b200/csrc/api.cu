@@ -392,6 +392,7 @@ int nrg_reconstruct_cd(nrg_ctx* x, double eps, int32_t max_iters, int32_t thread
 int nrg_counters(nrg_ctx* x, uint64_t* misses, uint64_t* hits, uint64_t* evals, uint64_t* warnings) {
     return guardx(x, [&] {
         uint64_t h[nrg::C_N];
+        x->c.join_side();
         NRG_CUDA(cudaMemcpyAsync(h, x->c.counters.p, sizeof(h), cudaMemcpyDeviceToHost, x->c.stream));
         x->c.sync();
         if (misses) *misses = h[nrg::C_MISSES];

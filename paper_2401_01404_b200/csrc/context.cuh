@@ -276,6 +276,54 @@ struct Context {
     }
     void sync() { NRG_CUDA(cudaStreamSynchronize(stream)); }
 
+    // pinned host staging (grow-only) for the host-side planning steps' copies
+    struct PinBuf {
+        void* p = nullptr;
+        size_t bytes = 0;
+        ~PinBuf() {
+            if (p) cudaFreeHost(p);
+        }
+        template <class T>
+        T* as(size_t count) {
+            const size_t b = count * sizeof(T) + 16;
+            if (b > bytes) {
+                if (p) cudaFreeHost(p);
+                p = nullptr;
+                NRG_CUDA(cudaMallocHost(&p, b + b / 4));
+                bytes = b + b / 4;
+            }
+            return static_cast<T*>(p);
+        }
+    };
+    PinBuf hp_dep, hp_ord, hp_i, hp_j, hp_ch;
+
+    // side stream for work whose result is needed only later (the dense root's miss
+    // recount): fork() orders it after everything queued so far; join_side() makes the
+    // main stream wait for it (before the distance cache is cleared, resized or its
+    // counters read)
+    cudaStream_t side = nullptr;
+    cudaEvent_t side_fork = nullptr, side_done = nullptr;
+    bool side_pending = false;
+    cudaStream_t fork() {
+        if (!side) {
+            NRG_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+            NRG_CUDA(cudaEventCreateWithFlags(&side_fork, cudaEventDisableTiming));
+            NRG_CUDA(cudaEventCreateWithFlags(&side_done, cudaEventDisableTiming));
+        }
+        NRG_CUDA(cudaEventRecord(side_fork, stream));
+        NRG_CUDA(cudaStreamWaitEvent(side, side_fork, 0));
+        return side;
+    }
+    void fork_done() {
+        NRG_CUDA(cudaEventRecord(side_done, side));
+        side_pending = true;
+    }
+    void join_side() {
+        if (!side_pending) return;
+        NRG_CUDA(cudaStreamWaitEvent(stream, side_done, 0));
+        side_pending = false;
+    }
+
     // phase timing (device events around a region on this stream, resolved lazily)
     cudaEvent_t take_event() {
         cudaEvent_t e;

@@ -214,10 +214,11 @@ __global__ void d_pairs_kernel(const TriKey* __restrict__ dir, const uint32_t* _
 // S': every out-entry of node li lies in D+ (inc/find_best.hpp:150-163).  Rows are sorted
 // by (dist, id) and (dist, li, id) orders them the same way, so the last entry decides.
 __global__ void saturated_kernel(const int32_t* __restrict__ nodes, const int32_t* __restrict__ ids,
-                                 const double* __restrict__ dists, uint64_t n, int k, TriKey thr,
+                                 const double* __restrict__ dists, uint64_t n, int k, const TriKey* __restrict__ thrp,
                                  uint8_t* __restrict__ flag) {
     const uint64_t li = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (li >= n) return;
+    const TriKey thr = *thrp;
     TriKey x;
     x.d = dkey(dists[li * k + (k - 1)]);
     x.a = (uint32_t)nodes[li];
@@ -313,9 +314,13 @@ struct DenseGuard {  // the level that set up the dense root tears it down (also
         if (owner) {
             const uint64_t pairs = c.dense_n * (c.dense_n - 1) / 2;
             const HashView h = (c.Ckeys.p && c.Ccap) ? c.Cview() : HashView{nullptr, nullptr, 0};
-            dense_recount_kernel<<<148 * 8, 256, 0, c.stream>>>(h, static_cast<const int32_t*>(c.dloc.p),
-                                                                static_cast<const uint32_t*>(c.dbits.p),
-                                                                (pairs + 31) / 32, c.dense_n, c.dcounters());
+            // off the critical path: only the counters need it (and the cache must not
+            // change under it: join_side() before any clear, resize or counter read)
+            cudaStream_t ss = c.fork();
+            dense_recount_kernel<<<148 * 8, 256, 0, ss>>>(h, static_cast<const int32_t*>(c.dloc.p),
+                                                          static_cast<const uint32_t*>(c.dbits.p),
+                                                          (pairs + 31) / 32, c.dense_n, c.dcounters());
+            c.fork_done();
             c.dense_active = false;
             c.dense_n = 0;  // the buffers stay (grow-only): the next generation reuses them
             c.dwl_n = 0;
@@ -417,6 +422,7 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
         const uint64_t cap = reverse ? std::max<uint64_t>(2 * kw, 8) : std::max<uint64_t>(kw, 8);
         if (!c.dense_active && mode == EXACT && c.kind == ISING && c.world == 1 && n <= dense_max_n() &&
             dense_ratio() * cap * cap >= n) {
+            c.join_side();  // a previous root's recount still reads dloc / dbits
             double* tri = c.dtri.as<double>(total);
             if (getenv("NRG_DEBUG_LEVELS")) c.flush_timing();
             const double ph0 = c.phase_ms[P_SCORE];
@@ -500,14 +506,9 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
     NRG_CUDA(cudaMemsetAsync(cnt, 0, 16, c.stream));
     d_pairs_kernel<<<g256(dplus), 256, 0, c.stream>>>(dirs, idx2, flag, dplus, dpairs, cnt);
     NRG_LAUNCH_CHECK();
-    // threshold key = the dplus-th smallest directed entry
-    TriKey thr;
-    NRG_CUDA(cudaMemcpyAsync(&thr, dirs + (dplus - 1), sizeof(TriKey), cudaMemcpyDeviceToHost, c.stream));
-    unsigned long long nD = 0;
-    NRG_CUDA(cudaMemcpyAsync(&nD, cnt, 8, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
-    // S'
-    saturated_kernel<<<g256(n), 256, 0, c.stream>>>(S, knn.ids, knn.dists, n, knn.k, thr, flag);
+    // S': the threshold key (the dplus-th smallest directed entry) stays on the device;
+    // |D| and |S'| come back in one round trip
+    saturated_kernel<<<g256(n), 256, 0, c.stream>>>(S, knn.ids, knn.dists, n, knn.k, dirs + (dplus - 1), flag);
     NRG_LAUNCH_CHECK();
     DevBuf satb, nsatb;
     int32_t* sat = satb.as<int32_t>(n);
@@ -518,7 +519,9 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
         void* tmp = tmpb.ensure(bytes);
         cub::DeviceSelect::Flagged(tmp, bytes, S, flag, sat, nsat, (int64_t)n, c.stream);
     }
+    unsigned long long nD = 0;
     int hsat = 0;
+    NRG_CUDA(cudaMemcpyAsync(&nD, cnt, 8, cudaMemcpyDeviceToHost, c.stream));
     NRG_CUDA(cudaMemcpyAsync(&hsat, nsat, 4, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
     c.toc(P_SELECT);

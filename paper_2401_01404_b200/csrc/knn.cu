@@ -1577,8 +1577,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
     out.dists = dist_buf.as<double>(n * k);
     to_global_kernel<<<(unsigned)ceil_div(n * k, 256), 256, 0, c.stream>>>(gid, gd, d_nodes, n, kw, k, out.ids,
                                                                          out.dists);
-    NRG_LAUNCH_CHECK();
-    c.sync();
+    NRG_LAUNCH_CHECK();  // stream-ordered: callers read the lists on this stream
 }
 
 }  // namespace nrg

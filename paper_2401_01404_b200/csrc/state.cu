@@ -18,6 +18,12 @@ namespace nrg {
 Context::~Context() {
     if (device >= 0) cudaSetDevice(device);
     // DevBuf members release themselves; the device must be current for cudaFree
+    if (side) {
+        cudaStreamSynchronize(side);
+        cudaStreamDestroy(side);
+        cudaEventDestroy(side_fork);
+        cudaEventDestroy(side_done);
+    }
     if (stream) cudaStreamSynchronize(stream);
     for (cudaEvent_t e : ev_free) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_used) cudaEventDestroy(e);
@@ -27,6 +33,7 @@ Context::~Context() {
 }
 
 void Context::flush_timing() {
+    join_side();
     if (pin_next)
         NRG_CUDA(cudaMemcpyAsync(pin_counts, count_log.p, (size_t)pin_next * 8, cudaMemcpyDeviceToHost, stream));
     if (!spans.empty() || pin_next) NRG_CUDA(cudaStreamSynchronize(stream));
@@ -681,6 +688,7 @@ __global__ void cache_rehash_kernel(const uint64_t* __restrict__ ok, const doubl
 }
 
 void cache_reserve(Context& c, uint64_t extra) {
+    c.join_side();
     const uint64_t kMax = 1ull << 31;
     // claims never exceed what was reserved: while the host bound fits, no readback
     if (c.Ccap) {
@@ -737,6 +745,7 @@ void cache_reserve(Context& c, uint64_t extra) {
 }
 
 void begin_generation(Context& c) {
+    c.join_side();
     if (c.Ccap) {
         // size the (now empty) memo for the previous generation's pairs + 30%: growing
         // here costs an allocation, growing mid-generation a rehash of every entry

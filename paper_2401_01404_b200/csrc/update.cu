@@ -409,8 +409,8 @@ static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64
     DevBuf ordb;
     uint32_t* order = nullptr;
     if (n >= 4096 && !getenv("NRG_LIST_ORDER_TICKETS")) {
-        std::vector<int32_t> hdep(2 * n);
-        NRG_CUDA(cudaMemcpyAsync(hdep.data(), dep, 8 * n, cudaMemcpyDeviceToHost, c.stream));
+        int32_t* hdep = c.hp_dep.as<int32_t>(2 * n);
+        NRG_CUDA(cudaMemcpyAsync(hdep, dep, 8 * n, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
         std::vector<uint32_t> lev(n), cnt(1, 0);
         for (uint64_t p = 0; p < n; ++p) {
@@ -421,7 +421,8 @@ static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64
             if (l >= cnt.size()) cnt.resize(l + 1, 0);
             ++cnt[l];
         }
-        std::vector<uint32_t> start(cnt.size(), 0), hord(n);
+        std::vector<uint32_t> start(cnt.size(), 0);
+        uint32_t* hord = c.hp_ord.as<uint32_t>(n);
         for (size_t l = 1; l < cnt.size(); ++l) start[l] = start[l - 1] + cnt[l - 1];
         for (uint64_t p = 0; p < n; ++p) hord[start[lev[p]]++] = (uint32_t)p;
         if (getenv("NRG_DEBUG_UPD")) {
@@ -430,7 +431,7 @@ static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64
             fprintf(stderr, "ordered_run: n=%llu levels=%zu widest=%u\n", (unsigned long long)n, cnt.size(), mx);
         }
         order = ordb.as<uint32_t>(n);
-        NRG_CUDA(cudaMemcpyAsync(order, hord.data(), 4 * n, cudaMemcpyHostToDevice, c.stream));
+        NRG_CUDA(cudaMemcpyAsync(order, hord, 4 * n, cudaMemcpyHostToDevice, c.stream));
         c.sync();
     }
     UpdateArgs A;
@@ -563,10 +564,11 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
     uint64_t start = k;
     if (start < n) {
         const uint64_t nt = n - start;
-        std::vector<int32_t> hi(nt), hj(nt);
-        std::vector<uint8_t> hch(nt);
-        NRG_CUDA(cudaMemcpyAsync(hi.data(), ci + start, nt * 4, cudaMemcpyDeviceToHost, c.stream));
-        NRG_CUDA(cudaMemcpyAsync(hj.data(), cj + start, nt * 4, cudaMemcpyDeviceToHost, c.stream));
+        int32_t* hi = c.hp_i.as<int32_t>(nt);
+        int32_t* hj = c.hp_j.as<int32_t>(nt);
+        uint8_t* hch = c.hp_ch.as<uint8_t>(nt);
+        NRG_CUDA(cudaMemcpyAsync(hi, ci + start, nt * 4, cudaMemcpyDeviceToHost, c.stream));
+        NRG_CUDA(cudaMemcpyAsync(hj, cj + start, nt * 4, cudaMemcpyDeviceToHost, c.stream));
         std::vector<uint8_t> mod(c.n, 0);
         std::vector<int32_t> touched;
         std::vector<uint32_t> apply;
@@ -612,7 +614,7 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
             uint8_t* ch = fb.as<uint8_t>(m);
             change_flags_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, c.stream>>>(ci, cj, start, n, w, c.Wview(), ch);
             NRG_LAUNCH_CHECK();
-            NRG_CUDA(cudaMemcpyAsync(hch.data(), ch, m, cudaMemcpyDeviceToHost, c.stream));
+            NRG_CUDA(cudaMemcpyAsync(hch, ch, m, cudaMemcpyDeviceToHost, c.stream));
             c.sync();
             c.tail_rounds++;
             uint64_t nch = 0;
