@@ -431,8 +431,8 @@ static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64
             fprintf(stderr, "ordered_run: n=%llu levels=%zu widest=%u\n", (unsigned long long)n, cnt.size(), mx);
         }
         order = ordb.as<uint32_t>(n);
+        // pinned and stream-ordered: the next planning step syncs before hord is rewritten
         NRG_CUDA(cudaMemcpyAsync(order, hord, 4 * n, cudaMemcpyHostToDevice, c.stream));
-        c.sync();
     }
     UpdateArgs A;
     A.kind = c.kind;
@@ -617,8 +617,12 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
             NRG_CUDA(cudaMemcpyAsync(hch, ch, m, cudaMemcpyDeviceToHost, c.stream));
             c.sync();
             c.tail_rounds++;
-            uint64_t nch = 0;
-            for (uint64_t q = 0; q < m; ++q) nch += hch[q];
+            uint64_t nch = 0, first = m;
+            for (uint64_t q = 0; q < m; ++q)
+                if (hch[q]) {
+                    if (!nch) first = q;
+                    ++nch;
+                }
             if (nch > (uint64_t)(kTailRounds - round)) {
                 // more changes than rounds left (a tail still far from converged, e.g. the
                 // first sweep): the ordered kernel is the faster exact path
@@ -626,7 +630,9 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
                 break;
             }
             apply.clear();
-            uint64_t p = start;
+            // nothing is modified before the first changing pair: the scan starts there
+            // (no change at all: every remaining result stands, the tail is done)
+            uint64_t p = start + first;
             for (; p < n; ++p) {
                 const uint64_t q = p - k;
                 const int a = hi[q], b = hj[q];
