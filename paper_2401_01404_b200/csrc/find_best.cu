@@ -345,39 +345,90 @@ __global__ void ascending_check_kernel(const int32_t* __restrict__ v, uint64_t n
     if (v[t] < 0 || v[t] >= n_total || (t > 0 && v[t] <= v[t - 1])) *bad = 1;
 }
 
+// Unique undirected pairs of a TriKey list by hashing canonical pair keys into an
+// L2-resident table: duplicates of a pair carry the same distance (one value per pair and
+// generation), so any representative gives the same canonical (dist, min, max) entry and
+// the result is order-independent -- no sort needed.
+__global__ void pair_dedup_kernel(const TriKey* __restrict__ in, uint64_t n, int ib, uint64_t* __restrict__ table,
+                                  uint64_t mask, TriKey* __restrict__ out, unsigned long long* __restrict__ cnt) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool keep = false;
+    TriKey o;
+    if (e < n) {
+        const TriKey t = in[e];
+        o.d = t.d;
+        o.a = min(t.a, t.b);
+        o.b = max(t.a, t.b);
+        const uint64_t key = ((uint64_t)o.a << ib) | o.b;
+        uint64_t s = slot_of(key, mask);
+        for (;;) {
+            const unsigned long long prev =
+                atomicCAS((unsigned long long*)&table[s], (unsigned long long)kEmptyKey, (unsigned long long)key);
+            if (prev == kEmptyKey) {
+                keep = true;
+                break;
+            }
+            if (prev == key) break;
+            s = (s + 1) & mask;
+        }
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, keep);
+    const int lane = threadIdx.x & 31;
+    unsigned long long at = 0;
+    if (lane == 0 && b) at = atomicAdd(cnt, (unsigned long long)__popc(b));
+    at = __shfl_sync(0xffffffffu, at, 0);
+    if (keep) out[at + __popc(b & ((1u << lane) - 1u))] = o;
+}
+static void pair_dedup(Context& c, const TriKey* in, uint64_t n, TriKey* out, unsigned long long* cnt, DevBuf& tabb) {
+    uint64_t cap = 1024;
+    while (cap < 2 * n) cap <<= 1;
+    uint64_t* table = tabb.as<uint64_t>(cap);
+    NRG_CUDA(cudaMemsetAsync(table, 0xff, cap * 8, c.stream));
+    NRG_CUDA(cudaMemsetAsync(cnt, 0, 8, c.stream));
+    if (n) {
+        pair_dedup_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(in, n, id_bits(c), table, cap - 1, out,
+                                                                          cnt);
+        NRG_LAUNCH_CHECK();
+    }
+}
+
 static inline unsigned g256(uint64_t n) { return (unsigned)std::max<int64_t>(1, ceil_div(n, 256)); }
 
 // union of two candidate lists without duplicate pairs, then the (dist,i,j)-smallest
 // `want` (inc/find_best.hpp:171-174 + :62-70)
 static uint64_t merge_select(Context& c, TriKey* buf, uint64_t n, uint64_t want, DevBuf& outb) {
-    DevBuf pkb, idxb, pk2b, idx2b, flagb, tmpb, ub, cntb, sb;
-    uint64_t* pk = pkb.as<uint64_t>(n);
-    uint32_t* idx = idxb.as<uint32_t>(n);
-    uint64_t* pk2 = pk2b.as<uint64_t>(n);
-    uint32_t* idx2 = idx2b.as<uint32_t>(n);
-    uint8_t* flag = flagb.as<uint8_t>(n);
-    TriKey* uniq = ub.as<TriKey>(n);
+    DevBuf tmpb, ub, cntb, tabb;
+    TriKey* uniq = ub.as<TriKey>(std::max<uint64_t>(n, 1));
     unsigned long long* cnt = cntb.as<unsigned long long>(1);
-    if (n) {
-        const int ib = id_bits(c);
-        trikey_pk_kernel<<<g256(n), 256, 0, c.stream>>>(buf, n, ib, pk, idx);
-        size_t bytes = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, bytes, pk, pk2, idx, idx2, (int64_t)n, 0, 2 * ib, c.stream);
-        void* tmp = tmpb.ensure(bytes);
-        cub::DeviceRadixSort::SortPairs(tmp, bytes, pk, pk2, idx, idx2, (int64_t)n, 0, 2 * ib, c.stream);
-        unique_flags_kernel<<<g256(n), 256, 0, c.stream>>>(pk2, n, flag);
-        NRG_CUDA(cudaMemsetAsync(cnt, 0, 8, c.stream));
-        gather_trikey_kernel<<<g256(n), 256, 0, c.stream>>>(buf, idx2, flag, n, uniq, cnt);
-        NRG_LAUNCH_CHECK();
-    }
     unsigned long long nu = 0;
+    if (getenv("NRG_SORT_DEDUP")) {
+        DevBuf pkb, idxb, pk2b, idx2b, flagb;
+        uint64_t* pk = pkb.as<uint64_t>(n);
+        uint32_t* idx = idxb.as<uint32_t>(n);
+        uint64_t* pk2 = pk2b.as<uint64_t>(n);
+        uint32_t* idx2 = idx2b.as<uint32_t>(n);
+        uint8_t* flag = flagb.as<uint8_t>(n);
+        if (n) {
+            const int ib = id_bits(c);
+            trikey_pk_kernel<<<g256(n), 256, 0, c.stream>>>(buf, n, ib, pk, idx);
+            size_t bytes = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, bytes, pk, pk2, idx, idx2, (int64_t)n, 0, 2 * ib, c.stream);
+            void* tmp = tmpb.ensure(bytes);
+            cub::DeviceRadixSort::SortPairs(tmp, bytes, pk, pk2, idx, idx2, (int64_t)n, 0, 2 * ib, c.stream);
+            unique_flags_kernel<<<g256(n), 256, 0, c.stream>>>(pk2, n, flag);
+            NRG_CUDA(cudaMemsetAsync(cnt, 0, 8, c.stream));
+            gather_trikey_kernel<<<g256(n), 256, 0, c.stream>>>(buf, idx2, flag, n, uniq, cnt);
+            NRG_LAUNCH_CHECK();
+        }
+    } else {
+        pair_dedup(c, buf, n, uniq, cnt, tabb);
+    }
     if (n) {
         NRG_CUDA(cudaMemcpyAsync(&nu, cnt, 8, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
     }
     TriKey* sorted = outb.as<TriKey>(std::max<uint64_t>(nu, 1));
     sort_trikeys(c, uniq, sorted, nu, tmpb);
-    c.sync();
     return std::min<uint64_t>(nu, want);
 }
 
@@ -492,20 +543,25 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
     uint32_t* idx2 = idx2b.as<uint32_t>(dplus);
     uint8_t* flag = flagb.as<uint8_t>(std::max<uint64_t>(dplus, n));
     unsigned long long* cnt = cntb.as<unsigned long long>(2);
-    const int ib = id_bits(c);
-    dplus_pairkeys_kernel<<<g256(dplus), 256, 0, c.stream>>>(dirs, dplus, ib, pk, idx);
-    {
-        size_t bytes = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, bytes, pk, pk2, idx, idx2, (int64_t)dplus, 0, 2 * ib, c.stream);
-        void* tmp = tmpb.ensure(bytes);
-        cub::DeviceRadixSort::SortPairs(tmp, bytes, pk, pk2, idx, idx2, (int64_t)dplus, 0, 2 * ib, c.stream);
-    }
-    unique_flags_kernel<<<g256(dplus), 256, 0, c.stream>>>(pk2, dplus, flag);
-    DevBuf dpairsb;
+    DevBuf dpairsb, dtabb;
     TriKey* dpairs = dpairsb.as<TriKey>(dplus);
     NRG_CUDA(cudaMemsetAsync(cnt, 0, 16, c.stream));
-    d_pairs_kernel<<<g256(dplus), 256, 0, c.stream>>>(dirs, idx2, flag, dplus, dpairs, cnt);
-    NRG_LAUNCH_CHECK();
+    if (getenv("NRG_SORT_DEDUP")) {
+        const int ib = id_bits(c);
+        dplus_pairkeys_kernel<<<g256(dplus), 256, 0, c.stream>>>(dirs, dplus, ib, pk, idx);
+        {
+            size_t bytes = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, bytes, pk, pk2, idx, idx2, (int64_t)dplus, 0, 2 * ib, c.stream);
+            void* tmp = tmpb.ensure(bytes);
+            cub::DeviceRadixSort::SortPairs(tmp, bytes, pk, pk2, idx, idx2, (int64_t)dplus, 0, 2 * ib, c.stream);
+        }
+        unique_flags_kernel<<<g256(dplus), 256, 0, c.stream>>>(pk2, dplus, flag);
+        d_pairs_kernel<<<g256(dplus), 256, 0, c.stream>>>(dirs, idx2, flag, dplus, dpairs, cnt);
+        NRG_LAUNCH_CHECK();
+    } else {
+        // D: unique undirected pairs of D+ (inc/find_best.hpp:133-145)
+        pair_dedup(c, dirs, dplus, dpairs, cnt, dtabb);
+    }
     // S': the threshold key (the dplus-th smallest directed entry) stays on the device;
     // |D| and |S'| come back in one round trip
     saturated_kernel<<<g256(n), 256, 0, c.stream>>>(S, knn.ids, knn.dists, n, knn.k, dirs + (dplus - 1), flag);
