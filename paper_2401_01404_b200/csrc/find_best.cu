@@ -396,7 +396,11 @@ static inline unsigned g256(uint64_t n) { return (unsigned)std::max<int64_t>(1, 
 
 // union of two candidate lists without duplicate pairs, then the (dist,i,j)-smallest
 // `want` (inc/find_best.hpp:171-174 + :62-70)
-static uint64_t merge_select(Context& c, TriKey* buf, uint64_t n, uint64_t want, DevBuf& outb) {
+// sorted == false (inner levels): the whole unique set is returned, unsorted.  The parent
+// keeps the top `want` of (its D U this set), and an entry outside this level's top `want`
+// has `want` better entries here, so it can never enter the parent's top `want`: the
+// result is the same as with the truncated list, and only the root level sorts.
+static uint64_t merge_select(Context& c, TriKey* buf, uint64_t n, uint64_t want, DevBuf& outb, bool sorted) {
     DevBuf tmpb, ub, cntb, tabb;
     TriKey* uniq = ub.as<TriKey>(std::max<uint64_t>(n, 1));
     unsigned long long* cnt = cntb.as<unsigned long long>(1);
@@ -427,15 +431,19 @@ static uint64_t merge_select(Context& c, TriKey* buf, uint64_t n, uint64_t want,
         NRG_CUDA(cudaMemcpyAsync(&nu, cnt, 8, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
     }
-    TriKey* sorted = outb.as<TriKey>(std::max<uint64_t>(nu, 1));
-    sort_trikeys(c, uniq, sorted, nu, tmpb);
+    if (!sorted) {
+        outb = std::move(ub);
+        return nu;
+    }
+    TriKey* out = outb.as<TriKey>(std::max<uint64_t>(nu, 1));
+    sort_trikeys(c, uniq, out, nu, tmpb);
     return std::min<uint64_t>(nu, want);
 }
 
 // result of a level: TriKey list (a<b canonical) sorted by (dist, a, b)
 static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* S, uint64_t n, double knn_eps,
                                uint64_t seed, bool reverse, int level, std::vector<TraceLevelD>& trace,
-                               DevBuf& result, bool sorted) {
+                               DevBuf& result, bool sorted, bool root) {
     if (n < 2) return 0;
     const uint64_t total = n * (n - 1) / 2;
     const uint64_t want = std::min(m, total);
@@ -459,12 +467,17 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
             tri_from_pairs_kernel<<<(unsigned)n, 256, 0, c.stream>>>(S, n, dist, keys);
             NRG_LAUNCH_CHECK();
         }
-        TriKey* out = result.as<TriKey>(total);
-        sort_trikeys(c, keys, out, total, tmpb);
-        c.sync();
+        uint64_t ret = want;
+        if (root) {
+            TriKey* out = result.as<TriKey>(total);
+            sort_trikeys(c, keys, out, total, tmpb);
+        } else {
+            result = std::move(keysb);  // all pairs, unsorted (see merge_select)
+            ret = total;
+        }
         c.toc(P_SELECT);
         trace.push_back({level, 0, 1, 0, n, 0});
-        return want;
+        return ret;
     }
     const int k = (int)((4 * m + n - 1) / n);
     DenseGuard dg(c);
@@ -589,7 +602,7 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
     DevBuf rec;
     // S' keeps S's order (DeviceSelect), so a sorted S gives a sorted S'
     const uint64_t nrec =
-        find_best_impl(c, mode, m, sat, (uint64_t)hsat, knn_eps, seed, reverse, level + 1, trace, rec, sorted);
+        find_best_impl(c, mode, m, sat, (uint64_t)hsat, knn_eps, seed, reverse, level + 1, trace, rec, sorted, false);
     c.tic();
     // merge D with the recursive result (dropping duplicates) and select
     DevBuf allb;
@@ -597,7 +610,7 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
     if (nD) NRG_CUDA(cudaMemcpyAsync(all, dpairs, nD * sizeof(TriKey), cudaMemcpyDeviceToDevice, c.stream));
     if (nrec)
         NRG_CUDA(cudaMemcpyAsync(all + nD, rec.p, nrec * sizeof(TriKey), cudaMemcpyDeviceToDevice, c.stream));
-    const uint64_t cntres = merge_select(c, all, nD + nrec, want, result);
+    const uint64_t cntres = merge_select(c, all, nD + nrec, want, result, root);
     c.toc(P_SELECT);
     return cntres;
 }
@@ -637,7 +650,7 @@ void find_best(Context& c, int mode, uint64_t m, const int32_t* d_nodes, uint64_
         int hbad = 0;
         NRG_CUDA(cudaMemcpyAsync(&hbad, ok, 4, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
-        cnt = find_best_impl(c, mode, m, d_nodes, n, knn_eps, seed, reverse, 0, res.trace, result, hbad == 0);
+        cnt = find_best_impl(c, mode, m, d_nodes, n, knn_eps, seed, reverse, 0, res.trace, result, hbad == 0, true);
     }
     res.count = cnt;
     int32_t* oi = out_i.as<int32_t>(std::max<uint64_t>(cnt, 1));
