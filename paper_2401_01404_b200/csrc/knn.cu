@@ -575,7 +575,8 @@ __global__ void u_set_kernel(const int32_t* __restrict__ adj, const int32_t* __r
 }
 __global__ void u_new_bits_kernel(const int32_t* __restrict__ adj, const int32_t* __restrict__ alen, uint64_t n,
                                   int cap, int W, const uint32_t* __restrict__ ubp, int first,
-                                  uint8_t* __restrict__ newf, uint32_t* __restrict__ nb) {
+                                  uint8_t* __restrict__ newf, uint32_t* __restrict__ nb,
+                                  uint8_t* __restrict__ hasnew) {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n * (uint64_t)cap) return;
     const uint64_t i = t / cap;
@@ -583,7 +584,10 @@ __global__ void u_new_bits_kernel(const int32_t* __restrict__ adj, const int32_t
     const int32_t j = adj[t];
     const bool fresh = first || !((ubp[i * W + (j >> 5)] >> (j & 31)) & 1u);
     newf[t] = fresh ? 1 : 0;
-    if (fresh) atomicOr(&nb[i * W + (j >> 5)], 1u << (j & 31));
+    if (fresh) {
+        atomicOr(&nb[i * W + (j >> 5)], 1u << (j & 31));
+        hasnew[i] = 1;
+    }
 }
 __global__ void u_bits_kernel(const int32_t* __restrict__ adj, const int32_t* __restrict__ alen,
                               const uint8_t* __restrict__ newf, uint64_t n, int cap, int W, uint32_t* __restrict__ ub,
@@ -612,16 +616,20 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
                                                              int32_t* __restrict__ cand_id,
                                                              uint32_t* __restrict__ cand_slot,
                                                              int32_t* __restrict__ cand_cnt, uint64_t lo, bool do_claim,
-                                                             const int32_t* __restrict__ rootpos) {
+                                                             const int32_t* __restrict__ rootpos,
+                                                             const uint8_t* __restrict__ hasnew) {
     extern __shared__ uint32_t bits_smem[];
     uint32_t* acc = bits_smem;     // OR of the 2-hop rows
     uint32_t* excl = acc + W;      // i's current row and i itself
+    int32_t* srcs = reinterpret_cast<int32_t*>(excl + W);  // rows to OR: 2 lj + (row is new in U(i))
+    __shared__ int s_nsrc;
     typedef cub::BlockScan<int, NT> Scan;
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ int s_total;
     const uint64_t li = lo + blockIdx.x;
     const int tid = threadIdx.x;
     for (int w = tid; w < W; w += NT) acc[w] = excl[w] = 0u;
+    if (tid == 0) s_nsrc = 0;
     __syncthreads();
     if (tid == 0) atomicOr(&excl[li >> 5], 1u << (li & 31));
     for (int t = tid; t < kw; t += NT) {
@@ -630,22 +638,50 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
     }
     const int32_t* row_i = adj + li * cap;
     const int len_i = alen[li];
-    if (W <= NT) {
+    // the rows that contribute: U(a) for a new in U(i), new(U(a)) for an old a that has new
+    // entries (an old a without any contributes nothing: its new-bitset is empty)
+    for (int a = tid; a < len_i; a += NT) {
+        const int32_t lj = row_i[a];
+        const bool nw = newf[li * cap + a] != 0;
+        if (nw || hasnew[lj]) srcs[atomicAdd(&s_nsrc, 1)] = 2 * lj + (nw ? 1 : 0);
+    }
+    __syncthreads();
+    const int nsrc = s_nsrc;
+    if (2 * cap < W) {
+        // rows shorter than the bitsets: walk the source rows' entries (a warp per row,
+        // lanes over entries) into the shared bitmap instead of reading W words per row
+        const int lane = tid & 31, wid = tid >> 5;
+        for (int q = wid; q < nsrc; q += NT / 32) {
+            const int32_t e = srcs[q];
+            const uint64_t lj = (uint64_t)(e >> 1);
+            const int len_j = alen[lj];
+            const int32_t* row_j = adj + lj * cap;
+            const uint8_t* nf_j = newf + lj * cap;
+            for (int b = lane; b < len_j; b += 32) {
+                if (!(e & 1) && !nf_j[b]) continue;  // old hop: only its new entries
+                const int32_t v = row_j[b];
+                atomicOr(&acc[v >> 5], 1u << (v & 31));
+            }
+        }
+    } else if (W <= NT) {
         // G threads per word, each ORs every G-th row into a register
         const int G = NT / W;
         const int w = tid % W, g = tid / W;
         if (g < G) {
             uint32_t r = 0u;
-            for (int a = g; a < len_i; a += G) {
-                const int32_t lj = row_i[a];
-                r |= (newf[li * cap + a] ? ub : nb)[(uint64_t)lj * W + w];
+            for (int q = g; q < nsrc; q += G) {
+                const int32_t e = srcs[q];
+                r |= ((e & 1) ? ub : nb)[(uint64_t)(e >> 1) * W + w];
             }
             if (r) atomicOr(&acc[w], r);
         }
     } else {
         for (int w = tid; w < W; w += NT) {
             uint32_t r = 0u;
-            for (int a = 0; a < len_i; ++a) r |= (newf[li * cap + a] ? ub : nb)[(uint64_t)row_i[a] * W + w];
+            for (int q = 0; q < nsrc; ++q) {
+                const int32_t e = srcs[q];
+                r |= ((e & 1) ? ub : nb)[(uint64_t)(e >> 1) * W + w];
+            }
             acc[w] = r;
         }
     }
@@ -1358,7 +1394,8 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
 
     // ---- sweeps
     const uint64_t capn = std::min<uint64_t>((uint64_t)cap * cap, n - 1);
-    DevBuf adjb, alenb, adjpb, alenpb, newfb, cidb, cslb, ccntb, churnb, churnb2, wsb, wpb, wslb, ubitsb, ubitsb2, nbitsb;
+    DevBuf adjb, alenb, adjpb, alenpb, newfb, cidb, cslb, ccntb, churnb, churnb2, wsb, wpb, wslb, ubitsb, ubitsb2, nbitsb,
+        hasnewb;
     int32_t* adj = adjb.as<int32_t>(n * cap);
     int32_t* alen = alenb.as<int32_t>(n);
     int32_t* adjp = adjpb.as<int32_t>(n * cap);  // U of the previous sweep
@@ -1450,12 +1487,14 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             uint32_t* ubc = (sweep & 1 ? ubitsb2 : ubitsb).as<uint32_t>(n * (uint64_t)Wb);
             uint32_t* ubp = (sweep & 1 ? ubitsb : ubitsb2).as<uint32_t>(n * (uint64_t)Wb);
             uint32_t* nbits = nbitsb.as<uint32_t>(n * (uint64_t)Wb);
+            uint8_t* hasnew = hasnewb.as<uint8_t>(n);
             NRG_CUDA(cudaMemsetAsync(ubc, 0, n * (uint64_t)Wb * 4, c.stream));
             NRG_CUDA(cudaMemsetAsync(nbits, 0, n * (uint64_t)Wb * 4, c.stream));
+            NRG_CUDA(cudaMemsetAsync(hasnew, 0, n, c.stream));
             const unsigned g = (unsigned)ceil_div(n * (uint64_t)cap, 256);
             u_set_kernel<<<g, 256, 0, c.stream>>>(adj, alen, n, cap, Wb, ubc);
             u_new_bits_kernel<<<g, 256, 0, c.stream>>>(adj, alen, n, cap, Wb, ubp,
-                                                      (sweep == 0 || !incremental) ? 1 : 0, newf, nbits);
+                                                      (sweep == 0 || !incremental) ? 1 : 0, newf, nbits, hasnew);
         } else {
             u_new_kernel<<<(unsigned)ceil_div(n * 32, 256), 256, 0, c.stream>>>(adj, alen, adjp, alenp, n, cap,
                                                                              (sweep == 0 || !incremental) ? 1 : 0,
@@ -1483,9 +1522,9 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             if (bitsmode) {
                 uint32_t* ub = static_cast<uint32_t*>((sweep & 1 ? ubitsb2 : ubitsb).p);
                 uint32_t* nbits = static_cast<uint32_t*>(nbitsb.p);
-                knn_gather_bits_kernel<256><<<(unsigned)own, 256, 2 * W * 4, c.stream>>>(
+                knn_gather_bits_kernel<256><<<(unsigned)own, 256, 2 * W * 4 + 4 * cap, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, W, ub, nbits, newf, hv0, sk, capn, cand_id, cand_slot, cand_cnt,
-                    lo, fused, rootpos);
+                    lo, fused, rootpos, static_cast<const uint8_t*>(hasnewb.p));
             } else if (big)
                 knn_gather_kernel<256><<<(unsigned)own, 256, tab_bytes, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv0, sk, capn, cand_id,
