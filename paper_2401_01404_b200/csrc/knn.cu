@@ -1433,8 +1433,11 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
     }
     // merge buffer
     // merge buffer: a power of two >= kw + 64 (bitonic width), at least 256
+    // merge buffer: a power of two >= kw + 64; wide rows take big candidate blocks (fewer
+    // block sorts when a first sweep's candidates mostly beat the row)
+    static const int merge_buf_min = getenv("NRG_MERGE_BUF") ? atoi(getenv("NRG_MERGE_BUF")) : 256;
     const int buf_cap = [&] {
-        int b = 256;
+        int b = kw > 64 ? merge_buf_min : 256;
         while (b < kw + 64) b <<= 1;
         return b;
     }();
