@@ -219,7 +219,21 @@ struct ClaimSink {
     const int32_t* dloc = nullptr;
     uint32_t* dbits = nullptr;
     uint64_t dn = 0;
+    // fold: misses and the memo's live count are added once per claim phase from wcount
+    // (fold_claims_kernel) and hits once per warp at kernel end, instead of three hot
+    // global atomics per warp and chunk
+    bool fold = false;
 };
+
+__global__ void fold_claims_kernel(const unsigned long long* __restrict__ wcount, uint64_t* __restrict__ counters,
+                                   uint64_t* __restrict__ live) {
+    counters[C_MISSES] += *wcount;
+    *live += *wcount;
+}
+__device__ __forceinline__ void flush_hits(const ClaimSink& sink, unsigned long long hits) {
+    hits = __reduce_add_sync(0xffffffffu, (unsigned)hits);
+    if ((threadIdx.x & 31) == 0 && hits) atomicAdd((unsigned long long*)&sink.counters[C_HITS], hits);
+}
 
 // row-major upper-triangle index of positions a < b among n (inc/find_best.hpp:78-79)
 __device__ __forceinline__ uint64_t tri_index(uint64_t a, uint64_t b, uint64_t n) {
@@ -241,7 +255,7 @@ __device__ __forceinline__ uint32_t dense_probe(uint32_t* __restrict__ dbits, ui
 // warp-cooperative claim of one candidate per lane (active lanes given by `valid`).
 // Uncached metrics (h.keys == nullptr) claim every candidate into its flat slot.
 __device__ __forceinline__ uint32_t claim_warp(HashView h, const ClaimSink& sink, bool valid, int32_t gs,
-                                               int32_t gp, uint64_t flat = 0) {
+                                               int32_t gp, uint64_t flat = 0, unsigned* hit_acc = nullptr) {
     bool mine = false, remote = false;
     uint64_t sl = 0;
     int dest = 0;
@@ -288,11 +302,16 @@ __device__ __forceinline__ uint32_t claim_warp(HashView h, const ClaimSink& sink
         sink.wslot[at] = (uint32_t)sl;
     }
     if (lane == 0 && h.keys) {
-        if (ball) {
+        if (ball && !sink.fold) {
             atomicAdd((unsigned long long*)&sink.counters[C_MISSES], (unsigned long long)__popc(ball));
             atomicAdd((unsigned long long*)sink.live, (unsigned long long)__popc(ball));
         }
-        if (hits) atomicAdd((unsigned long long*)&sink.counters[C_HITS], (unsigned long long)__popc(hits));
+        if (hits) {
+            if (sink.fold && hit_acc)
+                *hit_acc += __popc(hits);
+            else
+                atomicAdd((unsigned long long*)&sink.counters[C_HITS], (unsigned long long)__popc(hits));
+        }
     }
     return (uint32_t)sl;
 }
@@ -302,8 +321,10 @@ __global__ void claim_list_kernel(HashView h, ClaimSink sink, const int32_t* __r
                                   const int32_t* __restrict__ qj, uint64_t n, uint32_t* __restrict__ slot) {
     const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool valid = e < n;
-    const uint32_t sl = claim_warp(h, sink, valid, valid ? qi[e] : 0, valid ? qj[e] : 0);
+    unsigned hit_acc = 0;
+    const uint32_t sl = claim_warp(h, sink, valid, valid ? qi[e] : 0, valid ? qj[e] : 0, 0, &hit_acc);
     if (valid) slot[e] = sl;
+    if (sink.fold) flush_hits(sink, hit_acc);
 }
 __global__ void gather_vals_kernel(const double* __restrict__ vals, const double* __restrict__ rvals,
                                    const uint32_t* __restrict__ slot, uint64_t n, double* __restrict__ out) {
@@ -518,13 +539,15 @@ __global__ void __launch_bounds__(NT) knn_gather_kernel(const int32_t* __restric
     }
     // claim (pair_key(nodes[li], nodes[v])) in the per-generation distance cache
     const int32_t gs = nodes[li];
+    unsigned hit_acc = 0;
     for (int t0 = 0; t0 < cnt; t0 += NT) {
         const int t = t0 + tid;
         const bool valid = t < cnt;
         const int32_t v = valid ? my_ids[t] : 0;
-        const uint32_t sl = claim_warp(h, sink, valid, gs, valid ? nodes[v] : 0, li * capn + t);
+        const uint32_t sl = claim_warp(h, sink, valid, gs, valid ? nodes[v] : 0, li * capn + t, &hit_acc);
         if (valid) cand_slot[li * capn + t] = sl;
     }
+    if (sink.fold) flush_hits(sink, hit_acc);
     if (tid == 0) cand_cnt[li] = cnt;
 }
 
@@ -1291,6 +1314,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         s.live = static_cast<uint64_t*>(c.Ccount.p);
         s.rank = c.rank;
         s.world = W;
+        s.fold = W == 1 && cached && !dense && !getenv("NRG_NO_FOLD");
         if (dense) {
             s.dloc = static_cast<const int32_t*>(c.dloc.p);
             s.dbits = static_cast<uint32_t*>(c.dbits.p);
@@ -1345,6 +1369,8 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             const ClaimSink sk = sink_for(ws, wp, wsl, nq + 1);
             if (nq) {
                 claim_list_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, c.stream>>>(c.Cview(), sk, qi, qj, nq, slot);
+                if (sk.fold)
+                    fold_claims_kernel<<<1, 1, 0, c.stream>>>(wcount, c.dcounters(), sk.live);
                 NRG_LAUNCH_CHECK();
             }
             if (dense) {
@@ -1558,6 +1584,10 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                     d_nodes, c.Cview(), sk, own, lo, capn, cand_id, cand_slot, cand_cnt);
                 NRG_LAUNCH_CHECK();
             }
+        }
+        if (sk.fold) {  // this sweep's claims into the miss count and the memo's live count
+            fold_claims_kernel<<<1, 1, 0, c.stream>>>(wcount, c.dcounters(), sk.live);
+            NRG_LAUNCH_CHECK();
         }
         c.toc(P_KNN);
         unsigned long long nw = 0;

@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out/r01zq
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -rf > gpurun_out/r01zq/pytest.log 2>&1; echo "rc=$?" >> gpurun_out/r01zq/pytest.log
+for v in "NRG_X=1" "NRG_UPD_CTA=1" "NRG_X=1" "NRG_UPD_CTA=1"; do env $v timeout 300 python tools/steady_sweep.py > gpurun_out/r01zq/steady_$v.$RANDOM.log 2>&1; done
+timeout 600 python tools/sweeps_trace.py 6 > gpurun_out/r01zq/trace.log 2>&1
