@@ -551,6 +551,87 @@ __global__ void __launch_bounds__(NT) knn_gather_kernel(const int32_t* __restric
     if (tid == 0) cand_cnt[li] = cnt;
 }
 
+// knn_gather_kernel for narrow levels: one warp per node, WPB nodes per CTA (a
+// 32-thread CTA per node caps residency at 32 warps per SM; the claims are bound by the
+// latency of DRAM-resident probes, so more warps in flight is what pays)
+template <int WPB>
+__global__ void __launch_bounds__(32 * WPB) knn_gather_warp_kernel(
+    const int32_t* __restrict__ nodes, uint64_t n, const int32_t* __restrict__ adj, const int32_t* __restrict__ alen,
+    int cap, const int32_t* __restrict__ gid, int kw, bool bitmap, int tsize, HashView h, ClaimSink sink,
+    uint64_t capn, int32_t* __restrict__ cand_id, uint32_t* __restrict__ cand_slot, int32_t* __restrict__ cand_cnt,
+    uint64_t lo, uint64_t own, int lw, const uint8_t* __restrict__ newf, bool do_claim) {
+    extern __shared__ int32_t tab_all[];
+    __shared__ int ncand_s[WPB];
+    const int wid = threadIdx.x >> 5, tid = threadIdx.x & 31;
+    const uint64_t node = (uint64_t)blockIdx.x * WPB + wid;
+    if (node >= own) return;  // whole warp: no block-wide barriers below
+    const uint64_t li = lo + node;
+    const int words = bitmap ? (int)((n + 31) / 32) : tsize;
+    int32_t* tab = tab_all + (size_t)wid * words;
+    int& ncand = ncand_s[wid];
+    for (int t = tid; t < words; t += 32) tab[t] = bitmap ? 0 : -1;
+    if (tid == 0) ncand = 0;
+    __syncwarp();
+    auto insert = [&](int32_t v) -> bool {
+        if (bitmap) {
+            const uint32_t bit = 1u << (v & 31);
+            return !(atomicOr((uint32_t*)&tab[v >> 5], bit) & bit);
+        }
+        const uint32_t mask = (uint32_t)tsize - 1;
+        uint32_t s = ((uint32_t)v * 2654435761u) & mask;
+        for (;;) {
+            const int32_t prev = atomicCAS(&tab[s], -1, v);
+            if (prev == -1) return true;
+            if (prev == v) return false;
+            s = (s + 1) & mask;
+        }
+    };
+    if (tid == 0) insert((int32_t)li);
+    for (int t = tid; t < kw; t += 32) insert(gid[li * kw + t]);
+    __syncwarp();
+    const int32_t* row_i = adj + li * cap;
+    const int len_i = alen[li];
+    int32_t* my_ids = cand_id + li * capn;
+    const int gl = lw < 5 ? lw : 5;
+    const int gw = 1 << gl;
+    const int rows = 32 / gw;
+    const int r = tid >> gl, b0 = tid & (gw - 1);
+    for (int a0 = 0; a0 < len_i; a0 += rows) {
+        const int a = a0 + r;
+        if (a < len_i) {
+            const int32_t lj = row_i[a];
+            const int len_j = alen[lj];
+            const int32_t* row_j = adj + (uint64_t)lj * cap;
+            const bool old_a = !newf[li * cap + a];
+            for (int b = b0; b < len_j; b += gw) {
+                if (old_a && !newf[(uint64_t)lj * cap + b]) continue;  // old-old: lost last sweep
+                const int32_t v = row_j[b];
+                if (insert(v)) {
+                    const int at = atomicAdd(&ncand, 1);
+                    my_ids[at] = v;
+                }
+            }
+        }
+    }
+    __syncwarp();
+    const int cnt = ncand;
+    if (!do_claim) {
+        if (tid == 0) cand_cnt[li] = cnt;
+        return;
+    }
+    const int32_t gs = nodes[li];
+    unsigned hit_acc = 0;
+    for (int t0 = 0; t0 < cnt; t0 += 32) {
+        const int t = t0 + tid;
+        const bool valid = t < cnt;
+        const int32_t v = valid ? my_ids[t] : 0;
+        const uint32_t sl = claim_warp(h, sink, valid, gs, valid ? nodes[v] : 0, li * capn + t, &hit_acc);
+        if (valid) cand_slot[li * capn + t] = sl;
+    }
+    if (sink.fold) flush_hits(sink, hit_acc);
+    if (tid == 0) cand_cnt[li] = cnt;
+}
+
 // claims of the gathered candidates, one warp per node (after cache_reserve sized the
 // table for exactly this sweep's candidates)
 __global__ void claim_cands_kernel(const int32_t* __restrict__ nodes, HashView h, ClaimSink sink, uint64_t own,
@@ -1558,6 +1639,10 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                 knn_gather_kernel<256><<<(unsigned)own, 256, tab_bytes, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv0, sk, capn, cand_id,
                     cand_slot, cand_cnt, lo, lw, newf, fused);
+            else if (!getenv("NRG_GATHER_CTA") && tab_bytes * 4 <= 48 * 1024)
+                knn_gather_warp_kernel<4><<<(unsigned)ceil_div(own, 4), 128, 4 * tab_bytes, c.stream>>>(
+                    d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv0, sk, capn, cand_id,
+                    cand_slot, cand_cnt, lo, own, lw, newf, fused);
             else
                 knn_gather_kernel<32><<<(unsigned)own, 32, tab_bytes, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv0, sk, capn, cand_id,
