@@ -228,3 +228,40 @@ def test_validation_errors(gpu):
     gm = gpu.Model.from_samples(X, gpu.NRG_GAUSSIAN, 1.0)
     with pytest.raises(ValueError):
         gm.set_theta(np.zeros(5))  # gaussian model requires theta > 0
+
+
+@pytest.mark.parametrize("M", [1000, 1024, 1500, 2048])
+def test_wide_rows_vs_checker(gpu, M):
+    """The screen variants by row width — M = 1000/1024 (the headline's shape: the
+    shared-memory-staged K1), 1500 (partial words), 2048 (two words per lane): scores,
+    couplings and gains vs the checker, at the empty state and after one checker GCD
+    iteration (existing edges, nonzero fields)."""
+    n = 200
+    X, _ = O.gen_ising(n, M, seed=M, burn_in=200, thin=3)
+    lam = O.ising_lambda(n, M)
+    ref = O.CpuModel("orc", X, 0, lam)
+    dev = gpu.Model.from_samples(X.astype(np.int8), gpu.NRG_ISING, lam)
+    rng = np.random.default_rng(M)
+    ri, rj = rng.integers(0, n, 4000), rng.integers(0, n, 4000)
+    keep = ri != rj
+    ri, rj = ri[keep], rj[keep]
+    d_ref = ref.distance(0, ri, rj)
+    d_dev = dev.distance(gpu.NRG_EXACT, ri, rj)
+    assert_rel(d_dev, d_ref, 1e-5, "dist (empty state)")
+    assert_gains(-(d_dev + dev.log_posterior()), np.maximum(-(d_ref + ref.log_posterior()), 0), M)
+    ref.reconstruct_gcd(kappa=2.0, max_iters=1, seed=4)
+    th, ei, ej, w = ref.get_state()
+    dev.set_theta(th)
+    dev.set_edges(ei, ej, w)
+    i = np.concatenate([ei, ri])
+    j = np.concatenate([ej, rj])
+    ref.begin_generation()
+    dev.begin_generation()
+    d_ref = ref.distance(0, i, j)
+    d_dev = dev.distance(gpu.NRG_EXACT, i, j)
+    assert_rel(d_dev, d_ref, 1e-5, "dist (after a GCD iteration)")
+    w_ref, g_ref, _ = ref.optimize_edge(i, j)
+    w_dev, g_dev, _ = dev.optimize_edge(i, j)
+    assert_w(w_dev, w_ref)
+    assert_gains(g_dev, g_ref, M)
+    assert_gains(-(d_dev + dev.log_posterior()), g_ref, M, "cached gain")

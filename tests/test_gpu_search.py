@@ -267,7 +267,7 @@ def test_incremental_join_equals_full_join(gpu, monkeypatch):
     np.testing.assert_array_equal(a[4], b[4])
 
 
-@pytest.mark.parametrize("n,M,seed,kappa", [(1000, 500, 1, 2.0), (3000, 400, 2, 2.0), (2000, 300, 4, 6.0)])
+@pytest.mark.parametrize("n,M,seed,kappa", [(1000, 500, 1, 2.0), (3000, 400, 2, 2.0), (2000, 300, 4, 6.0), (4000, 1000, 3, 2.0)])
 def test_dense_levels_equal_claim_path(gpu, monkeypatch, n, M, seed, kappa):
     """Deep FindBest levels that read distances from the level's exhaustive tensor-core
     triangle (find_best.cu, dense levels) give the identical pair list and trace as the
