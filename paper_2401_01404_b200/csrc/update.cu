@@ -114,7 +114,7 @@ struct UpdateArgs {
 // of levels at config 4), so per-update latency, not throughput, bounds the phase;
 // NT threads share each pass over the samples with block reductions.
 template <int NT>
-__global__ void __launch_bounds__(NT, 3) update_kernel(UpdateArgs A) {
+__global__ void __launch_bounds__(NT, 768 / NT) update_kernel(UpdateArgs A) {
     extern __shared__ double stage_smem[];
     __shared__ double red[4 * (NT / 32) + 4];
     __shared__ unsigned long long s_p;
@@ -367,8 +367,7 @@ __global__ void __launch_bounds__(1024) sum_fixed_kernel(const double* __restric
     }
 }
 
-constexpr int kUpdNT = 256;
-
+template <int kUpdNT>
 static int update_grid(Context& c, size_t smem) {
     int sms = 0, per = 0;
     NRG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
@@ -408,6 +407,7 @@ static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64
     // reconstruct_cd's row-major all-pairs share one node and run one at a time.
     DevBuf ordb;
     uint32_t* order = nullptr;
+    size_t nlevels = 0;
     if (n >= 4096 && !getenv("NRG_LIST_ORDER_TICKETS")) {
         int32_t* hdep = c.hp_dep.as<int32_t>(2 * n);
         NRG_CUDA(cudaMemcpyAsync(hdep, dep, 8 * n, cudaMemcpyDeviceToHost, c.stream));
@@ -421,6 +421,7 @@ static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64
             if (l >= cnt.size()) cnt.resize(l + 1, 0);
             ++cnt[l];
         }
+        nlevels = cnt.size();
         std::vector<uint32_t> start(cnt.size(), 0);
         uint32_t* hord = c.hp_ord.as<uint32_t>(n);
         for (size_t l = 1; l < cnt.size(); ++l) start[l] = start[l - 1] + cnt[l - 1];
@@ -459,10 +460,18 @@ static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64
     const size_t smem = (size_t)2 * c.Mp * sizeof(double);
     A.stage = (c.kind == ISING && smem <= 160 * 1024) ? 1 : 0;
     const size_t smem_use = A.stage ? smem : 0;
-    int grid = (int)std::min<uint64_t>(update_grid(c, smem_use), n);
+    // wide, shallow dependency structures (the steady-state lists: ~50k updates in ~60
+    // levels) are bound by how many updates are in flight: 128-thread CTAs (twice as
+    // many); deep chains (first sweeps, reconstruct_cd) by per-update latency: 256
+    static const int nt_env = getenv("NRG_UPD_NT") ? atoi(getenv("NRG_UPD_NT")) : 0;
+    const int nt = nt_env ? nt_env : (nlevels > 0 && n >= 256 * nlevels ? 128 : 256);
+    int grid = (int)std::min<uint64_t>(nt == 128 ? update_grid<128>(c, smem_use) : update_grid<256>(c, smem_use), n);
     const bool dbg = getenv("NRG_DEBUG_UPDATES") != nullptr;
     if (dbg && getenv("NRG_DEBUG_SERIAL")) grid = 1;
-    update_kernel<kUpdNT><<<grid, kUpdNT, smem_use, c.stream>>>(A);
+    if (nt == 128)
+        update_kernel<128><<<grid, 128, smem_use, c.stream>>>(A);
+    else
+        update_kernel<256><<<grid, 256, smem_use, c.stream>>>(A);
     NRG_LAUNCH_CHECK();
     if (dbg) {
         std::vector<int32_t> hd(2 * n), hi(n), hj(n);
