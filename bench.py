@@ -11,7 +11,7 @@ state: the `warmup` sweeps first, then the `steps` timed sweeps that continue it
 first sweep, from the empty state, is the most expensive one and is reported among the
 warm-up sweeps).  `value` = unique pair scores (distance-cache misses) of the timed
 sweeps / their device time, inputs resident in HBM.  `e2e` = the same through the C-ABI
-with host buffers: every step uploads the N x M int8 samples from pinned host memory
+with host buffers: every step uploads the N x M samples (bit-packed rows, the Ising sample-file layout) from pinned host memory
 and the state the timed sweeps started from, runs that sweep, and downloads the
 kappa*N candidate pairs and the new state.
 
@@ -273,7 +273,9 @@ def run_ours(args, rank, world, local, dist):
     Xh = model.generate_ising(mean_deg=md, w_sigma=0.3, th_sigma=0.1, burn_in=args.burn_in, thin=10,
                               seed=args.seed, want_samples=True)
     gen_s = time.perf_counter() - t0
-    pinned = torch.from_numpy(Xh).pin_memory()
+    # the e2e step's host input: the samples in the library's bit-packed row layout (the
+    # Ising sample-file format, 1 bit per spin) in pinned memory
+    pinned = torch.from_numpy(np.packbits(Xh > 0, axis=1, bitorder="little")).pin_memory()
     Xpin = pinned.numpy()
 
     # One reconstruction (inc/reconstruct.hpp:162-179 loop): `warmup` sweeps from the
@@ -312,7 +314,7 @@ def run_ours(args, rank, world, local, dist):
     h2d = d2h = 0
     model.timer_start()
     for s in range(args.steps):
-        model.upload_spins_i8(Xpin)
+        model.upload_spins_packed(Xpin)
         model.set_theta(th_w)
         model.set_edges(ei_w, ej_w, w_w)
         rec, cands = model.gcd_iteration(args.warmup, kappa=kappa, seed=args.seed, want_candidates=True)
@@ -381,7 +383,7 @@ def run_ours(args, rank, world, local, dist):
                              else None},
         "e2e": {"value": e2e_pairs / (e2e_ms / 1e3), "unit": "pairs/s", "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps, "ms_per_step": e2e_ms / args.steps,
-                "step": "upload samples + state S_W, sweep W, download candidates + state"},
+                "step": "upload bit-packed samples + state S_W, sweep W, download candidates + state"},
         "gpu_launches": int(kst["launches"]),
         "clocks": clk.summary(),
     }

@@ -113,6 +113,10 @@ int nrg_destroy(nrg_ctx* ctx);
 int nrg_upload_samples(nrg_ctx* ctx, const double* X);
 /* Ising fast path: N x M int8 spins (+1/-1). */
 int nrg_upload_spins_i8(nrg_ctx* ctx, const int8_t* X);
+/* Ising, bit-packed: N rows of row_bytes >= ceil(M/8) bytes, bit t (LSB first) of a row
+ * set = spin t is +1 -- the row layout of nrg_write_samples_file's Ising files, and
+ * 1/8 of the int8 upload.  Bits past M are ignored. */
+int nrg_upload_spins_packed(nrg_ctx* ctx, const uint8_t* bits, uint64_t row_bytes);
 
 /* make_empty_state (inc/model.hpp:404-416) on the uploaded samples: W = 0, sums 0,
  * theta 0 (Ising) / row RMS (Gaussian); clears the distance cache. */

@@ -60,6 +60,7 @@ SIGNATURES = {
     "nrg_destroy": (C.c_int, [_P]),
     "nrg_upload_samples": (C.c_int, [_P, _F64P]),
     "nrg_upload_spins_i8": (C.c_int, [_P, _I8P]),
+    "nrg_upload_spins_packed": (C.c_int, [_P, C.c_void_p, C.c_uint64]),
     "nrg_reset_state": (C.c_int, [_P]),
     "nrg_set_theta": (C.c_int, [_P, _F64P]),
     "nrg_set_edges": (C.c_int, [_P, _u64, _I32P, _I32P, _F64P]),
@@ -217,6 +218,11 @@ class Model:
 
     def upload_spins_i8(self, X):
         check(self.L.nrg_upload_spins_i8(self.h, np.ascontiguousarray(X, dtype=np.int8)))
+
+    def upload_spins_packed(self, bits):
+        """bits: uint8 [N][row_bytes], LSB-first (numpy.packbits(X > 0, axis=1, bitorder='little'))"""
+        bits = np.ascontiguousarray(bits, dtype=np.uint8)
+        check(self.L.nrg_upload_spins_packed(self.h, bits.ctypes.data, bits.shape[1]))
 
     def generate_ising(self, mean_deg=4.0, w_sigma=0.3, th_sigma=0.1, burn_in=1000, thin=10, seed=0,
                        want_samples=False):

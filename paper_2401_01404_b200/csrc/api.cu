@@ -144,6 +144,9 @@ int nrg_upload_samples(nrg_ctx* x, const double* X) {
 int nrg_upload_spins_i8(nrg_ctx* x, const int8_t* X) {
     return guardx(x, [&] { nrg::upload_spins_i8(x->c, X); });
 }
+int nrg_upload_spins_packed(nrg_ctx* x, const uint8_t* bits, uint64_t row_bytes) {
+    return guardx(x, [&] { nrg::upload_spins_packed(x->c, bits, row_bytes); });
+}
 
 int nrg_reset_state(nrg_ctx* x) {
     return guardx(x, [&] { nrg::reset_state_empty(x->c); });

@@ -380,6 +380,7 @@ struct Context {
 void ctx_init(Context& c, int n, int m, int kind, double lambda, int device);
 void upload_samples_f64(Context& c, const double* X);
 void upload_spins_i8(Context& c, const int8_t* X);
+void upload_spins_packed(Context& c, const uint8_t* bits, uint64_t row_bytes);
 void set_theta(Context& c, const double* th);
 void reset_state_empty(Context& c);
 // ---- io.cu (binary sample / state files)

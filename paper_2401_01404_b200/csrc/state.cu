@@ -147,6 +147,46 @@ __global__ void pack_spins_i8_kernel(const int8_t* __restrict__ X, int rows, int
     if (lane == 0) Xb[(size_t)r * Mw + w] = word;
 }
 
+// rows of LSB-first bit-packed spins (the sample-file layout: bit t of a row = spin t is
+// +1) into the device words: word w of row r = bytes 4w..4w+3 of the row, bits past M
+// cleared
+__global__ void repack_bits_kernel(const uint8_t* __restrict__ src, int rows, uint64_t row_bytes, int M, int Mw,
+                                   uint32_t* __restrict__ Xb) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (int64_t)rows * Mw) return;
+    const int r = (int)(t / Mw), w = (int)(t % Mw);
+    uint32_t v = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint64_t b = (uint64_t)4 * w + k;
+        if (b < row_bytes && (int)(8 * b) < M) v |= (uint32_t)src[(size_t)r * row_bytes + b] << (8 * k);
+    }
+    const int lo = 32 * w;
+    if (M - lo < 32) v &= (M - lo <= 0) ? 0u : ((1u << (M - lo)) - 1u);
+    Xb[(size_t)r * Mw + w] = v;
+}
+
+static void reset_state(Context& c);
+void upload_spins_packed(Context& c, const uint8_t* bits, uint64_t row_bytes) {
+    if (c.kind != ISING) fail(22, "packed spins are only valid for the ising model");
+    if (row_bytes * 8 < (uint64_t)c.M) fail(22, "packed spin rows shorter than M bits");
+    c.Xb.ensure((size_t)c.n * c.Mw * 4);
+    const int rows_per = std::max<int>(1, (int)std::min<int64_t>(c.n, (256ll << 20) / std::max<uint64_t>(1, row_bytes)));
+    uint8_t* d = c.s_a.as<uint8_t>((size_t)rows_per * row_bytes);
+    for (int r0 = 0; r0 < c.n; r0 += rows_per) {
+        const int rows = std::min(rows_per, c.n - r0);
+        NRG_CUDA(cudaMemcpyAsync(d, bits + (size_t)r0 * row_bytes, (size_t)rows * row_bytes, cudaMemcpyHostToDevice,
+                                 c.stream));
+        const int64_t words = (int64_t)rows * c.Mw;
+        repack_bits_kernel<<<(unsigned)ceil_div(words, 256), 256, 0, c.stream>>>(d, rows, row_bytes, c.M, c.Mw,
+                                                                              c.dXb() + (size_t)r0 * c.Mw);
+        NRG_LAUNCH_CHECK();
+    }
+    reset_state(c);
+    c.sync();
+    c.have_samples = true;
+}
+
 __global__ void gauss_theta_rms_kernel(const double* __restrict__ X, int M, int Mp,
                                        double* __restrict__ theta, int* __restrict__ bad) {
     // make_empty_state (inc/model.hpp:404-416): theta = max(rms, 1e-8); block per row

@@ -206,3 +206,28 @@ def test_reconstruct_cd_vs_reference(gpu, kind):
     assert_rel(ra["objective"], rb["objective"], 1e-7, "objective per CD sweep")
     assert_rel(ra["delta"], rb["delta"], 1e-5, "delta per CD sweep")
     assert_same_couplings(dev.get_state(), ref.get_state(), tol=1e-4)
+
+
+def test_packed_spin_upload_equals_int8(gpu):
+    """nrg_upload_spins_packed (LSB-first rows, the Ising sample-file layout, any row
+    stride >= ceil(M/8)) gives the same device samples as the int8 upload: identical
+    distances and GCD iteration."""
+    rng = np.random.default_rng(11)
+    n, M = 300, 203
+    X = np.where(rng.random((n, M)) < 0.45, -1, 1).astype(np.int8)
+    lam = O.ising_lambda(n, M)
+    a = gpu.Model.from_samples(X, gpu.NRG_ISING, lam)
+    b = gpu.Model(n, M, gpu.NRG_ISING, lam)
+    bits = np.packbits(X > 0, axis=1, bitorder="little")
+    padded = np.zeros((n, bits.shape[1] + 3), np.uint8)
+    padded[:, : bits.shape[1]] = bits
+    padded[:, bits.shape[1] - 1] |= 0xF0  # bits past M must be ignored
+    b.upload_spins_packed(padded)
+    i, j = rng.integers(0, n, 3000), rng.integers(0, n, 3000)
+    keep = i != j
+    np.testing.assert_array_equal(a.distance(gpu.NRG_EXACT, i[keep], j[keep]),
+                                  b.distance(gpu.NRG_EXACT, i[keep], j[keep]))
+    ra, ca = a.gcd_iteration(0, kappa=2.0, seed=3, want_candidates=True)
+    rb, cb = b.gcd_iteration(0, kappa=2.0, seed=3, want_candidates=True)
+    np.testing.assert_array_equal(ca, cb)
+    assert ra["objective"] == rb["objective"]
