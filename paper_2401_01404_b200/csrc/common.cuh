@@ -1,5 +1,6 @@
 // common.cuh — shared device helpers for libnetrec_b200 (sm_100a).
 #pragma once
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -123,5 +124,9 @@ __host__ __device__ __forceinline__ uint64_t slot_of(uint64_t key, uint64_t mask
 }
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// A/B and debug switches read once per call site (getenv scans the environment; several
+// sit on per-sweep paths).  Switches the tests toggle in-process keep plain getenv.
+#define NRG_ENV_ON(name) ([] { static const bool v_ = getenv(name) != nullptr; return v_; }())
 
 }  // namespace nrg

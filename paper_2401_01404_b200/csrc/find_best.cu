@@ -109,7 +109,7 @@ __global__ void unpack_trikey_kernel2(const K* __restrict__ in, uint64_t n, uint
 
 static void sort_trikeys(Context& c, TriKey* in, TriKey* out, uint64_t n, DevBuf& tmpb) {
     if (!n) return;
-    if (getenv("NRG_SORT_FULL")) {
+    if (NRG_ENV_ON("NRG_SORT_FULL")) {
         size_t bytes = 0;
         cub::DeviceRadixSort::SortKeys(nullptr, bytes, in, out, (int64_t)n, TriKeyDecomposer{}, c.stream);
         void* tmp = tmpb.ensure(bytes);
@@ -405,7 +405,7 @@ static uint64_t merge_select(Context& c, TriKey* buf, uint64_t n, uint64_t want,
     TriKey* uniq = ub.as<TriKey>(std::max<uint64_t>(n, 1));
     unsigned long long* cnt = cntb.as<unsigned long long>(1);
     unsigned long long nu = 0;
-    if (getenv("NRG_SORT_DEDUP")) {
+    if (NRG_ENV_ON("NRG_SORT_DEDUP")) {
         DevBuf pkb, idxb, pk2b, idx2b, flagb;
         uint64_t* pk = pkb.as<uint64_t>(n);
         uint32_t* idx = idxb.as<uint32_t>(n);
@@ -488,11 +488,11 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
             dense_ratio() * cap * cap >= n) {
             c.join_side();  // a previous root's recount still reads dloc / dbits
             double* tri = c.dtri.as<double>(total);
-            if (getenv("NRG_DEBUG_LEVELS")) c.flush_timing();
+            if (NRG_ENV_ON("NRG_DEBUG_LEVELS")) c.flush_timing();
             const double ph0 = c.phase_ms[P_SCORE];
             const auto w0 = std::chrono::steady_clock::now();
-            const bool ok = score_all_pairs_tc(c, S, n, tri, true, !getenv("NRG_DENSE_EAGER"));
-            if (getenv("NRG_DEBUG_LEVELS")) {
+            const bool ok = score_all_pairs_tc(c, S, n, tri, true, !NRG_ENV_ON("NRG_DENSE_EAGER"));
+            if (NRG_ENV_ON("NRG_DEBUG_LEVELS")) {
                 c.flush_timing();
                 fprintf(stderr, "dense root level %d: n=%llu setup wall_ms=%.2f score_phase_ms=%.2f ok=%d\n", level,
                         (unsigned long long)n,
@@ -518,7 +518,7 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
     kp.reverse = reverse;
     KnnResultD knn;
     DevBuf kid, kdist;
-    const bool dbg = getenv("NRG_DEBUG_LEVELS") != nullptr;
+    const bool dbg = NRG_ENV_ON("NRG_DEBUG_LEVELS");
     uint64_t m0 = 0;
     double t0 = 0.0, s0 = 0.0, k20 = 0.0;
     if (dbg) {
@@ -559,7 +559,7 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
     DevBuf dpairsb, dtabb;
     TriKey* dpairs = dpairsb.as<TriKey>(dplus);
     NRG_CUDA(cudaMemsetAsync(cnt, 0, 16, c.stream));
-    if (getenv("NRG_SORT_DEDUP")) {
+    if (NRG_ENV_ON("NRG_SORT_DEDUP")) {
         const int ib = id_bits(c);
         dplus_pairkeys_kernel<<<g256(dplus), 256, 0, c.stream>>>(dirs, dplus, ib, pk, idx);
         {

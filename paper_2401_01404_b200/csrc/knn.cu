@@ -1395,7 +1395,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         s.live = static_cast<uint64_t*>(c.Ccount.p);
         s.rank = c.rank;
         s.world = W;
-        s.fold = W == 1 && cached && !dense && !getenv("NRG_NO_FOLD");
+        s.fold = W == 1 && cached && !dense && !NRG_ENV_ON("NRG_NO_FOLD");
         if (dense) {
             s.dloc = static_cast<const int32_t*>(c.dloc.p);
             s.dbits = static_cast<uint32_t*>(c.dbits.p);
@@ -1591,7 +1591,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         static const uint64_t bits_max_n =
             getenv("NRG_BITS_MAXN") ? strtoull(getenv("NRG_BITS_MAXN"), nullptr, 10) : (uint64_t)kBitsMaxN;
         const bool bitsmode = n <= std::min<uint64_t>(bits_max_n, kBitsMaxN) && cap >= 32 &&
-                              !getenv("NRG_KNN_HASH_GATHER");
+                              !NRG_ENV_ON("NRG_KNN_HASH_GATHER");
         if (bitsmode) {
             // U bitsets ping-pong between sweeps: last sweep's set answers the new flags
             uint32_t* ubc = (sweep & 1 ? ubitsb2 : ubitsb).as<uint32_t>(n * (uint64_t)Wb);
@@ -1639,7 +1639,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                 knn_gather_kernel<256><<<(unsigned)own, 256, tab_bytes, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv0, sk, capn, cand_id,
                     cand_slot, cand_cnt, lo, lw, newf, fused);
-            else if (!getenv("NRG_GATHER_CTA") && tab_bytes * 4 <= 48 * 1024)
+            else if (!NRG_ENV_ON("NRG_GATHER_CTA") && tab_bytes * 4 <= 48 * 1024)
                 knn_gather_warp_kernel<4><<<(unsigned)ceil_div(own, 4), 128, 4 * tab_bytes, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv0, sk, capn, cand_id,
                     cand_slot, cand_cnt, lo, own, lw, newf, fused);
@@ -1702,7 +1702,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             if (kw > 64)
                 knn_merge_kernel<128><<<(unsigned)own, 128, merge_smem, c.stream>>>(
                     d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dvals, rvals, buf_cap, churn, lo);
-            else if (!getenv("NRG_MERGE_CTA"))
+            else if (!NRG_ENV_ON("NRG_MERGE_CTA"))
                 knn_merge_warp_kernel<<<(unsigned)ceil_div(own, kMergeWarps), 32 * kMergeWarps,
                                         (size_t)kMergeWarps * (2 * kw + kMergeBlk) * 20, c.stream>>>(
                     d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dvals, rvals, churn, lo, own);

@@ -695,15 +695,15 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
                                                                     c.dcounters(), n_dev, k1log)
         const int G = c.Mw <= 4 ? 4 : (c.Mw <= 8 ? 8 : 16);
         const int WPL = (c.Mw + G - 1) / G;  // 1, 2 (M <= 1024) or up to 4 (M <= 2048)
-        if (!getenv("NRG_K1_WIDE") && (WPL == 1 || (WPL == 2 && !getenv("NRG_K1_ONE_PAIR")))) {
+        if (!NRG_ENV_ON("NRG_K1_WIDE") && (WPL == 1 || (WPL == 2 && !NRG_ENV_ON("NRG_K1_ONE_PAIR")))) {
             const uint64_t sblocks = std::min<uint64_t>(ceil_div(n, 8 * 32), (uint64_t)sms * 16);
 #define NRG_LAUNCH_SMALL(GG, WW, FF)                                                                          \
     ising_screen_small_kernel<GG, WW, FF><<<(unsigned)sblocks, 256, 0, c.stream>>>(S, W, s, p, n, c.lambda,   \
                                                                                  base, out, surv, surv_g,      \
                                                                                  surv_flag, nsurv,             \
                                                                                  c.dcounters(), n_dev, k1log)
-            const bool full = c.Mw == G * WPL && !getenv("NRG_K1_NOFULL");
-            if (WPL == 2 && full && !getenv("NRG_K1_NOPIPE")) {
+            const bool full = c.Mw == G * WPL && !NRG_ENV_ON("NRG_K1_NOFULL");
+            if (WPL == 2 && full && !NRG_ENV_ON("NRG_K1_NOPIPE")) {
                 static const int ns = getenv("NRG_K1_STAGES") ? atoi(getenv("NRG_K1_STAGES")) : 2;
 #define NRG_LAUNCH_PIPE(NSV)                                                                                       \
     {                                                                                                              \

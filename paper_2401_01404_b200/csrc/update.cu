@@ -408,7 +408,7 @@ static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64
     DevBuf ordb;
     uint32_t* order = nullptr;
     size_t nlevels = 0;
-    if (n >= 4096 && !getenv("NRG_LIST_ORDER_TICKETS")) {
+    if (n >= 4096 && !NRG_ENV_ON("NRG_LIST_ORDER_TICKETS")) {
         int32_t* hdep = c.hp_dep.as<int32_t>(2 * n);
         NRG_CUDA(cudaMemcpyAsync(hdep, dep, 8 * n, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
@@ -426,7 +426,7 @@ static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64
         uint32_t* hord = c.hp_ord.as<uint32_t>(n);
         for (size_t l = 1; l < cnt.size(); ++l) start[l] = start[l - 1] + cnt[l - 1];
         for (uint64_t p = 0; p < n; ++p) hord[start[lev[p]]++] = (uint32_t)p;
-        if (getenv("NRG_DEBUG_UPD")) {
+        if (NRG_ENV_ON("NRG_DEBUG_UPD")) {
             uint32_t mx = 0;
             for (uint32_t v : cnt) mx = std::max(mx, v);
             fprintf(stderr, "ordered_run: n=%llu levels=%zu widest=%u\n", (unsigned long long)n, cnt.size(), mx);
@@ -466,8 +466,8 @@ static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64
     static const int nt_env = getenv("NRG_UPD_NT") ? atoi(getenv("NRG_UPD_NT")) : 0;
     const int nt = nt_env ? nt_env : (nlevels > 0 && n >= 256 * nlevels ? 128 : 256);
     int grid = (int)std::min<uint64_t>(nt == 128 ? update_grid<128>(c, smem_use) : update_grid<256>(c, smem_use), n);
-    const bool dbg = getenv("NRG_DEBUG_UPDATES") != nullptr;
-    if (dbg && getenv("NRG_DEBUG_SERIAL")) grid = 1;
+    const bool dbg = NRG_ENV_ON("NRG_DEBUG_UPDATES");
+    if (dbg && NRG_ENV_ON("NRG_DEBUG_SERIAL")) grid = 1;
     if (nt == 128)
         update_kernel<128><<<grid, 128, smem_use, c.stream>>>(A);
     else
@@ -653,7 +653,7 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
                     touched.push_back(b);
                 }
             }
-            if (getenv("NRG_DEBUG_TAIL")) {
+            if (NRG_ENV_ON("NRG_DEBUG_TAIL")) {
                 fprintf(stderr, "tail round %d: start=%llu m=%llu changed=%llu applied=%zu stop=%llu\n", round,
                         (unsigned long long)start, (unsigned long long)m, (unsigned long long)nch, apply.size(),
                         (unsigned long long)p);
