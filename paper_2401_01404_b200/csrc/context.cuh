@@ -209,6 +209,7 @@ struct Context {
     DevBuf dwl_es, dwl_ep, dwl_slot, dwl_sg, dwl_sf;
     uint64_t dwl_n = 0;
     DevBuf dres_idx, dres_g, dres_f, dres_cnt;
+    DevBuf dmark;  // one bit per triangle slot: still marked (L2-resident; the test a probe makes)
 
     // test metrics
     DevBuf table, line;
@@ -431,14 +432,18 @@ struct DenseResolve {
     float* g = nullptr;
     uint8_t* f = nullptr;
     unsigned long long* cnt = nullptr;
+    uint32_t* mark = nullptr;
 };
 constexpr unsigned long long kMarkTag = 0x7ff4ull << 48, kBusyTag = 0x7ff2ull << 48;
 __device__ __forceinline__ void dense_resolve_slot(const DenseResolve& R, uint32_t s) {
     if (!R.tri) return;
-    unsigned long long* p = reinterpret_cast<unsigned long long*>(R.tri) + s;
-    const unsigned long long v = __ldcg(p);
+    // the marked-slot bitmap (L2) answers for the unmarked majority; clearing the bit
+    // claims the pair, and only then is its triangle slot (the NaN-boxed index) read
+    const uint32_t bit = 1u << (s & 31);
+    if (!(__ldcg(&R.mark[s >> 5]) & bit)) return;
+    if (!(atomicAnd(&R.mark[s >> 5], ~bit) & bit)) return;
+    const unsigned long long v = __ldcg(reinterpret_cast<const unsigned long long*>(R.tri) + s);
     if ((v & (0xffffull << 48)) != kMarkTag) return;
-    if (atomicCAS(p, v, (v & 0xffffffffffffull) | kBusyTag) != v) return;
     const uint64_t t = v & 0xffffffffffffull;
     const unsigned long long at = atomicAdd(R.cnt, 1ull);
     R.idx[at] = t;

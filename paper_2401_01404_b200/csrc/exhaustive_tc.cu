@@ -351,7 +351,8 @@ __global__ void tc_cache_filter_kernel(HashView C, const int32_t* __restrict__ e
 }
 // lazy mode: a survivor's slot holds its worklist index, NaN-boxed (or the cached value)
 __global__ void tc_mark_kernel(HashView C, const int32_t* __restrict__ es, const int32_t* __restrict__ ep,
-                               const uint32_t* __restrict__ slot, uint64_t nw, double* __restrict__ dist) {
+                               const uint32_t* __restrict__ slot, uint64_t nw, double* __restrict__ dist,
+                               uint32_t* __restrict__ mark) {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nw) return;
     if (C.keys) {
@@ -368,6 +369,7 @@ __global__ void tc_mark_kernel(HashView C, const int32_t* __restrict__ es, const
         }
     }
     reinterpret_cast<unsigned long long*>(dist)[slot[t]] = kMarkTag | t;
+    atomicOr(&mark[slot[t] >> 5], 1u << (slot[t] & 31));
 }
 __global__ void resolve_slots_kernel(DenseResolve R, const uint32_t* __restrict__ slots, uint64_t n) {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -504,10 +506,12 @@ bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* di
     c.toc(P_SCORE);
     if (lazy) {
         // survivors stay in the triangle as markers; the worklist moves to the Context
+        uint32_t* mark = c.dmark.as<uint32_t>(pairs / 32 + 1);
+        NRG_CUDA(cudaMemsetAsync(mark, 0, (pairs / 32 + 1) * 4, c.stream));
         if (nw) {
             tc_mark_kernel<<<(unsigned)ceil_div(nw, 256), 256, 0, c.stream>>>(
                 (use_cache && c.Ckeys.p && c.Ccap) ? c.Cview() : HashView{nullptr, nullptr, 0}, es, ep, slot, nw,
-                dist);
+                dist, mark);
             NRG_LAUNCH_CHECK();
         }
         c.dwl_es = std::move(esb);
@@ -559,6 +563,7 @@ DenseResolve dense_resolve_begin(Context& c) {
     R.g = static_cast<float*>(c.dres_g.p);
     R.f = static_cast<uint8_t*>(c.dres_f.p);
     R.cnt = static_cast<unsigned long long*>(c.dres_cnt.p);
+    R.mark = static_cast<uint32_t*>(c.dmark.p);
     NRG_CUDA(cudaMemsetAsync(R.cnt, 0, 8, c.stream));
     return R;
 }
