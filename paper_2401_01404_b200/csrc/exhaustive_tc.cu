@@ -109,8 +109,11 @@ struct TcOut {
     uint64_t cap;
 };
 
-// one 128x128 tile (row block I <= column block J) per CTA, 4 warps
-__global__ void __launch_bounds__(128, 1)
+// one 128x128 tile (row block I <= column block J) per CTA, 8 warps: warp 0 lane 0
+// feeds TMA, warp 1 lane 0 issues the MMAs, and all 8 run the epilogue -- warps w and
+// w + 4 share TMEM lane quadrant w % 4 (rows) and split the tile's columns
+constexpr int kTcThreads = 256;
+__global__ void __launch_bounds__(kTcThreads, 1)
     tc_screen_kernel(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mt,
                      const float4* __restrict__ q, int n, int M, int Mp, double lambda, double base, TcOut out) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -128,7 +131,7 @@ __global__ void __launch_bounds__(128, 1)
         ++I;
     }
     const int J = I + rem;
-    {
+    if (threadIdx.x < kBN) {
         const int j = J * kBN + (int)threadIdx.x;
         const float4 v = j < n ? __ldg(&q[j]) : make_float4(0.f, 0.f, 0.f, 0.f);
         qcol[threadIdx.x] = make_float2(v.x, v.y);
@@ -191,15 +194,17 @@ __global__ void __launch_bounds__(128, 1)
     __syncwarp();
     mbar_wait(&done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // epilogue: thread = one row of the tile
-    const int r = warp * 32 + lane;
+    // epilogue: thread = one row of the tile, half of its columns
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const int cbeg = (warp >> 2) * (kBN / 2), cend = cbeg + kBN / 2;
     const int i = I * kBM + r;
     const float lam = (float)lambda;
     const float err0 = 4.f * (float)M * 5.9604645e-08f;
     const float4 qi = i < n ? __ldg(&q[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int c0 = 0; c0 < kBN; c0 += 16) {
+    for (int c0 = cbeg; c0 < cend; c0 += 16) {
         uint32_t a1[16], a2[16], a3[16];
-        const uint32_t lane_addr = (uint32_t)(warp * 32) << 16;
+        const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
         tmem_ld16(tmem + lane_addr + 0 * kBN + c0, a1);
         tmem_ld16(tmem + lane_addr + 1 * kBN + c0, a2);
         tmem_ld16(tmem + lane_addr + 2 * kBN + c0, a3);
@@ -472,7 +477,7 @@ bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* di
         NRG_CUDA(cudaFuncSetAttribute(tc_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    tc_screen_kernel<<<(unsigned)(T * (T + 1) / 2), 128, smem, c.stream>>>(mx, mt, q, (int)n, c.M, Mp, c.lambda,
+    tc_screen_kernel<<<(unsigned)(T * (T + 1) / 2), kTcThreads, smem, c.stream>>>(mx, mt, q, (int)n, c.M, Mp, c.lambda,
                                                                           base, out);
     NRG_LAUNCH_CHECK();
     unsigned long long ns = 0;
