@@ -135,6 +135,10 @@ struct GaussSnap {
     const double* xx;
     const double* theta;
     int M, Mp;
+    const float* U32;  // screen copies (fp32) and ||U|| per node
+    const float* X32;
+    const double* nu;
+    const unsigned long long* BL;
 };
 
 // outputs of a scoring pass: either scattered into the distance cache (slot-indexed)
@@ -182,6 +186,7 @@ struct Context {
 
     // snapshot
     DevBuf T32, T64, T8, P8, Q8, BL, Tsq, U, xx;
+    DevBuf U32, X32, nu;  // Gaussian screen: fp32 copies of U and X, ||U_i|| (fp64, rounded up)
     uint64_t snap_version = 0;
     uint64_t lp_version = 0;  // log_posterior memo (state version it was computed at)
     double lp_value = 0.0;
@@ -273,7 +278,9 @@ struct Context {
                 static_cast<unsigned long long*>(BL.p), static_cast<double*>(Tsq.p), M, Mp, Mw};
     }
     GaussSnap gsnap() {
-        return {dXd(), static_cast<double*>(U.p), static_cast<double*>(xx.p), dtheta(), M, Mp};
+        return {dXd(), static_cast<double*>(U.p), static_cast<double*>(xx.p), dtheta(), M, Mp,
+                static_cast<float*>(U32.p), static_cast<float*>(X32.p), static_cast<double*>(nu.p),
+                static_cast<unsigned long long*>(BL.p)};
     }
     void sync() { NRG_CUDA(cudaStreamSynchronize(stream)); }
 

@@ -551,18 +551,116 @@ __global__ void __launch_bounds__(128) ising_refine_kernel(IsingSnap S, HashView
     }
 }
 
+// Gaussian screen (exact mode): for w_cur = 0 the slice maximum is at the kink (w* = 0,
+// gain exactly 0, dist = -base) iff |P| <= lambda, P = <u_a, x_b> + <u_b, x_a>
+// (gauss_optimize).  P is formed in fp32 from fp32 copies of U and X with a rigorous
+// bound, |P32 - P64| <= (2 (M/32 + 8) 2^-24 + 1e-12)(||u_a|| ||x_b|| + ||u_b|| ||x_a||)
+// (input rounding, per-lane fp32 accumulation of M/16 products, a 5-level warp tree, and
+// the fp64 path's own rounding; Cauchy-Schwarz for sum |u x|); pairs it cannot settle,
+// and existing couplings, go to the fp64 kernel.  The stationary node's rows stay in
+// registers across a worklist run.  NF: float4 per lane per row (Mp = 128 NF).
+template <int NF>
+__global__ void __launch_bounds__(256) gauss_screen_kernel(GaussSnap G, HashView W, const int32_t* __restrict__ es,
+                                                           const int32_t* __restrict__ ep, uint64_t n,
+                                                           const unsigned long long* __restrict__ n_dev,
+                                                           double lambda, double base, ScoreOut out,
+                                                           uint64_t* __restrict__ surv,
+                                                           unsigned long long* __restrict__ nsurv,
+                                                           uint64_t* counters) {
+    if (n_dev) n = min(n, (uint64_t)*n_dev);
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const int Mp = 128 * NF;
+    float4 us[NF], xs[NF];
+    int cur = -1;
+    const double relerr = 2.0 * ((double)G.M / 32.0 + 8.0) * 5.9604644775390625e-08 + 1e-12;
+    const double pruned_dist = -(base + 0.0);
+    uint64_t evals = 0;
+    for (uint64_t c0 = warp0 * 32; c0 < n; c0 += nwarps * 32) {
+        const int len = (int)min((uint64_t)32, n - c0);
+        const int li = lane < len ? lane : 0;
+        const int my_s = es[c0 + li], my_p = ep[c0 + li];
+        float my_P = 0.f;
+        for (int k = 0; k < len; ++k) {
+            const int s = __shfl_sync(0xffffffffu, my_s, k);
+            const int p = __shfl_sync(0xffffffffu, my_p, k);
+            if (s != cur) {
+                const float4* u4 = reinterpret_cast<const float4*>(G.U32 + (size_t)s * Mp);
+                const float4* x4 = reinterpret_cast<const float4*>(G.X32 + (size_t)s * Mp);
+#pragma unroll
+                for (int q = 0; q < NF; ++q) {
+                    us[q] = __ldg(&u4[lane + 32 * q]);
+                    xs[q] = __ldg(&x4[lane + 32 * q]);
+                }
+                cur = s;
+            }
+            const float4* up = reinterpret_cast<const float4*>(G.U32 + (size_t)p * Mp);
+            const float4* xp = reinterpret_cast<const float4*>(G.X32 + (size_t)p * Mp);
+            float acc = 0.f;
+#pragma unroll
+            for (int q = 0; q < NF; ++q) {
+                const float4 a = __ldg(&xp[lane + 32 * q]), b = __ldg(&up[lane + 32 * q]);
+                acc = fmaf(us[q].x, a.x, acc);
+                acc = fmaf(us[q].y, a.y, acc);
+                acc = fmaf(us[q].z, a.z, acc);
+                acc = fmaf(us[q].w, a.w, acc);
+                acc = fmaf(b.x, xs[q].x, acc);
+                acc = fmaf(b.y, xs[q].y, acc);
+                acc = fmaf(b.z, xs[q].z, acc);
+                acc = fmaf(b.w, xs[q].w, acc);
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == k) my_P = acc;
+        }
+        const uint64_t e = c0 + lane;
+        bool settled = false;
+        if (lane < len) {
+            const int a = min(my_s, my_p), b = max(my_s, my_p);
+            const bool maybe_edge = (G.BL[a] & bloom_bit(b)) != 0ull;
+            const double wcur = maybe_edge ? hash_get(W, pair_key(a, b), 0.0) : 0.0;
+            if (wcur == 0.0) {
+                const double bound = relerr * (G.nu[a] * sqrt(G.xx[b]) + G.nu[b] * sqrt(G.xx[a])) * 1.01;
+                settled = fabs((double)my_P) <= lambda - bound;
+                ++evals;
+            }
+            if (settled) {
+                if (out.cache_vals) out.cache_vals[out.slot[e]] = pruned_dist;
+                if (out.dist) out.dist[e] = pruned_dist;
+                if (out.w) out.w[e] = 0.0;
+                if (out.gain) out.gain[e] = 0.0;
+                if (out.warn) out.warn[e] = 0;
+            }
+        }
+        const unsigned sv = __ballot_sync(0xffffffffu, lane < len && !settled);
+        if (sv) {
+            unsigned long long at = 0;
+            if (lane == 0) at = atomicAdd(nsurv, (unsigned long long)__popc(sv));
+            at = __shfl_sync(0xffffffffu, at, 0);
+            if ((sv >> lane) & 1u) surv[at + __popc(sv & ((1u << lane) - 1u))] = e;
+        }
+    }
+    evals = warp_sum((int)evals);
+    if (lane == 0 && counters && evals) atomicAdd((unsigned long long*)&counters[C_EVALS], (unsigned long long)evals);
+}
+
 // fp64 kernels for the remaining modes: Ising exact (M > 2048), Ising gradient,
 // Gaussian exact / gradient.  One warp per entry.
 __global__ void __launch_bounds__(256) generic_score_kernel(int kind, int mode, IsingSnap S, GaussSnap G,
                                                             HashView W, const int32_t* __restrict__ es,
                                                             const int32_t* __restrict__ ep, uint64_t n,
                                                             double lambda, double base, ScoreOut out,
-                                                            uint64_t* counters) {
+                                                            uint64_t* counters,
+                                                            const uint64_t* __restrict__ sel = nullptr,
+                                                            const unsigned long long* __restrict__ n_dev = nullptr) {
+    if (n_dev) n = min(n, (uint64_t)*n_dev);
     const int lane = threadIdx.x & 31;
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     uint64_t evals = 0, warns = 0;
-    for (uint64_t e = warp0; e < n; e += nwarps) {
+    for (uint64_t t = warp0; t < n; t += nwarps) {
+        const uint64_t e = sel ? sel[t] : t;
         const int s = es[e], p = ep[e];
         const int a = s < p ? s : p, b = s < p ? p : s;
         const double wcur = hash_get(W, pair_key(a, b), 0.0);
@@ -649,7 +747,8 @@ void refine_survivors(Context& c, const int32_t* s, const int32_t* p, const uint
 void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uint64_t n,
                    const ScoreOut& out, const unsigned long long* n_dev) {
     if (n == 0) return;
-    if (n_dev && !(c.kind == ISING && mode == EXACT && (c.Mp + 1023) / 1024 <= 2)) {
+    if (n_dev && !(mode == EXACT && ((c.kind == ISING && (c.Mp + 1023) / 1024 <= 2) ||
+                                     (c.kind == GAUSSIAN && c.Mp <= 1024 && !NRG_ENV_ON("NRG_NO_GAUSS_SCREEN"))))) {
         // only the screen takes a device-side count: settle it here for the other paths
         unsigned long long h = 0;
         NRG_CUDA(cudaMemcpyAsync(&h, n_dev, 8, cudaMemcpyDeviceToHost, c.stream));
@@ -745,6 +844,24 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
         c.span(T_K1, k1a, (double)n, k1slot);
         // K2 strides over the device-side survivor count (no host round trip)
         refine_survivors(c, s, p, surv, surv_g, surv_flag, n, base, out, nsurv);
+    } else if (c.kind == GAUSSIAN && mode == EXACT && c.Mp <= 1024 && !NRG_ENV_ON("NRG_NO_GAUSS_SCREEN")) {
+        // screen in fp32, the pairs it cannot settle (and existing couplings) in fp64
+        uint64_t* surv = c.sc_surv.as<uint64_t>(n);
+        unsigned long long* nsurv = c.sc_n.as<unsigned long long>(1);
+        NRG_CUDA(cudaMemsetAsync(nsurv, 0, 8, c.stream));
+        const uint64_t sblocks = std::min<uint64_t>(ceil_div(n, 8 * 32), (uint64_t)sms * 16);
+        const GaussSnap G = c.gsnap();
+        switch (c.Mp / 128) {
+            case 2: gauss_screen_kernel<2><<<(unsigned)sblocks, 256, 0, c.stream>>>(G, c.Wview(), s, p, n, n_dev, c.lambda, base, out, surv, nsurv, c.dcounters()); break;
+            case 4: gauss_screen_kernel<4><<<(unsigned)sblocks, 256, 0, c.stream>>>(G, c.Wview(), s, p, n, n_dev, c.lambda, base, out, surv, nsurv, c.dcounters()); break;
+            case 6: gauss_screen_kernel<6><<<(unsigned)sblocks, 256, 0, c.stream>>>(G, c.Wview(), s, p, n, n_dev, c.lambda, base, out, surv, nsurv, c.dcounters()); break;
+            default: gauss_screen_kernel<8><<<(unsigned)sblocks, 256, 0, c.stream>>>(G, c.Wview(), s, p, n, n_dev, c.lambda, base, out, surv, nsurv, c.dcounters()); break;
+        }
+        NRG_LAUNCH_CHECK();
+        const uint64_t blocks = std::min<uint64_t>((n + 7) / 8, (uint64_t)sms * 16);
+        generic_score_kernel<<<(unsigned)blocks, 256, 0, c.stream>>>(
+            c.kind, mode, c.isnap(), G, c.Wview(), s, p, n, c.lambda, base, out, c.dcounters(), surv, nsurv);
+        NRG_LAUNCH_CHECK();
     } else {
         const uint64_t blocks = std::min<uint64_t>((n + 7) / 8, (uint64_t)sms * 16);
         generic_score_kernel<<<(unsigned)blocks, 256, 0, c.stream>>>(

@@ -502,26 +502,44 @@ __global__ void __launch_bounds__(256) snapshot_ising_kernel(const double* __res
 }
 
 // Gaussian: U = X + theta^2 H (the current residual), xx = sum x^2
+// Gaussian snapshot: U = X + theta^2 H (fp64) and xx = sum x^2, plus the screen's fp32
+// copies of U and X and ||U|| (fp64 sum, the screen's error bound scales with it)
 __global__ void snapshot_gauss_kernel(const double* __restrict__ X, const double* __restrict__ H,
                                       const double* __restrict__ theta, int M, int Mp,
                                       double* __restrict__ U, double* __restrict__ xx,
-                                      const int32_t* __restrict__ rows) {
+                                      const int32_t* __restrict__ rows, float* __restrict__ U32,
+                                      float* __restrict__ X32, double* __restrict__ nu) {
     const int r = rows ? rows[blockIdx.x] : (int)blockIdx.x;
     const double t2 = theta[r] * theta[r];
-    double a = 0.0;
+    double a = 0.0, b = 0.0;
     for (int m = threadIdx.x; m < Mp; m += blockDim.x) {
         const double x = X[(size_t)r * Mp + m];
-        U[(size_t)r * Mp + m] = m < M ? x + t2 * H[(size_t)r * Mp + m] : 0.0;
+        const double u = m < M ? x + t2 * H[(size_t)r * Mp + m] : 0.0;
+        U[(size_t)r * Mp + m] = u;
+        if (U32) {
+            U32[(size_t)r * Mp + m] = (float)u;
+            X32[(size_t)r * Mp + m] = (float)x;
+        }
         a += x * x;
+        b += u * u;
     }
-    __shared__ double sh[32];
+    __shared__ double sh[32], sh2[32];
     a = warp_sum(a);
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = a;
+    b = warp_sum(b);
+    if ((threadIdx.x & 31) == 0) {
+        sh[threadIdx.x >> 5] = a;
+        sh2[threadIdx.x >> 5] = b;
+    }
     __syncthreads();
     if (threadIdx.x < 32) {
         double v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+        double w = threadIdx.x < (blockDim.x >> 5) ? sh2[threadIdx.x] : 0.0;
         v = warp_sum(v);
-        if (threadIdx.x == 0) xx[r] = v;
+        w = warp_sum(w);
+        if (threadIdx.x == 0) {
+            xx[r] = v;
+            if (nu) nu[r] = sqrt(w) * (1.0 + 1e-12);
+        }
     }
 }
 
@@ -568,9 +586,15 @@ void ensure_snapshot(Context& c) {
     } else {
         c.U.ensure(nm * 8);
         c.xx.ensure((size_t)c.n * 8);
+        c.U32.ensure(nm * 4);
+        c.X32.ensure(nm * 4);
+        c.nu.ensure((size_t)c.n * 8);
         snapshot_gauss_kernel<<<c.n, 256, 0, c.stream>>>(c.dXd(), c.dH(), c.dtheta(), c.M, c.Mp,
                                                          static_cast<double*>(c.U.p),
-                                                         static_cast<double*>(c.xx.p), nullptr);
+                                                         static_cast<double*>(c.xx.p), nullptr,
+                                                         static_cast<float*>(c.U32.p), static_cast<float*>(c.X32.p),
+                                                         static_cast<double*>(c.nu.p));
+        build_bloom(c);
     }
     NRG_LAUNCH_CHECK();
     c.toc(P_SNAP);
@@ -592,9 +616,15 @@ void snapshot_rows(Context& c, const int32_t* rows, uint64_t nr) {
             static_cast<double*>(c.Tsq.p), rows);
         build_bloom(c);  // the rows' couplings changed too
     } else
+    {
         snapshot_gauss_kernel<<<(unsigned)nr, 256, 0, c.stream>>>(c.dXd(), c.dH(), c.dtheta(), c.M, c.Mp,
                                                                    static_cast<double*>(c.U.p),
-                                                                   static_cast<double*>(c.xx.p), rows);
+                                                                   static_cast<double*>(c.xx.p), rows,
+                                                                   static_cast<float*>(c.U32.p),
+                                                                   static_cast<float*>(c.X32.p),
+                                                                   static_cast<double*>(c.nu.p));
+        build_bloom(c);
+    }
     NRG_LAUNCH_CHECK();
     c.toc(P_SNAP);
     c.snap_version = c.state_version;
