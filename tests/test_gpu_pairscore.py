@@ -265,3 +265,33 @@ def test_wide_rows_vs_checker(gpu, M):
     assert_w(w_dev, w_ref)
     assert_gains(g_dev, g_ref, M)
     assert_gains(-(d_dev + dev.log_posterior()), g_ref, M, "cached gain")
+
+
+@pytest.mark.parametrize("M", [120, 1000])
+def test_gaussian_screen_at_the_threshold(gpu, M):
+    """The fp32 Gaussian screen (gauss_screen_kernel) only settles pairs its bound proves
+    to be at the kink: with lambda at the median |P| (half the pairs within a hair of the
+    threshold) the kink set and the distances equal the checker's."""
+    rng = np.random.default_rng(M)
+    n = 300
+    X = rng.standard_normal((n, M)) + 0.3 * rng.standard_normal((1, M))
+    i, j = rng.integers(0, n, 6000), rng.integers(0, n, 6000)
+    keep = i != j
+    i, j = i[keep], j[keep]
+    th = np.sqrt((X * X).mean(axis=1))  # make_empty_state's theta (row RMS); sums are 0
+    U = X  # u = x + theta^2 s with s = 0
+    P = np.einsum("ij,ij->i", U[i], X[j]) + np.einsum("ij,ij->i", U[j], X[i])
+    lam = float(np.median(np.abs(P)))
+    ref = O.CpuModel("orc", X, 1, lam)
+    dev = gpu.Model.from_samples(X, gpu.NRG_GAUSSIAN, lam)
+    np.testing.assert_allclose(dev.get_state()[0], th, rtol=1e-12)
+    ref.begin_generation()
+    d_ref = ref.distance(0, i, j)
+    d_dev = dev.distance(gpu.NRG_EXACT, i, j)
+    base_ref = -ref.log_posterior()
+    base_dev = -dev.log_posterior()
+    kink_ref = d_ref == base_ref
+    kink_dev = d_dev == base_dev
+    assert 0.3 < kink_ref.mean() < 0.7
+    np.testing.assert_array_equal(kink_dev, kink_ref)
+    assert_rel(d_dev, d_ref, 1e-5, "gauss dist at the threshold")
