@@ -330,7 +330,7 @@ struct DenseGuard {  // the level that set up the dense root tears it down (also
 
 static uint64_t dense_max_n() {
     const char* e = getenv("NRG_DENSE_N");
-    return e ? (uint64_t)strtoull(e, nullptr, 10) : 32768;
+    return e ? (uint64_t)strtoull(e, nullptr, 10) : 65535;  // the tensor-core screen's limit
 }
 // a level goes dense when its candidate sets (up to cap^2 per node) cover at least
 // 1/ratio of the level

@@ -652,6 +652,23 @@ __global__ void claim_cands_kernel(const int32_t* __restrict__ nodes, HashView h
     }
 }
 
+// the same claims with every candidate in flight at once: blockIdx.y strides a node's
+// candidate row in blocks of 256 (wide rows at deep levels: a warp per node walks
+// thousands of dependent cache probes one chunk at a time)
+__global__ void claim_cands_flat_kernel(const int32_t* __restrict__ nodes, HashView h, ClaimSink sink, uint64_t own,
+                                        uint64_t lo, uint64_t capn, const int32_t* __restrict__ cand_id,
+                                        uint32_t* __restrict__ cand_slot, const int32_t* __restrict__ cand_cnt) {
+    const uint64_t li = lo + blockIdx.x;
+    const int cnt = cand_cnt[li];
+    const int t = (int)blockIdx.y * blockDim.x + threadIdx.x;
+    if ((int)blockIdx.y * (int)blockDim.x >= cnt) return;  // whole block past the row
+    const bool valid = t < cnt;
+    const int32_t gs = nodes[li];
+    const int32_t v = valid ? cand_id[li * capn + t] : 0;
+    const uint32_t sl = claim_warp(h, sink, valid, gs, valid ? nodes[v] : 0, li * capn + t);
+    if (valid) cand_slot[li * capn + t] = sl;
+}
+
 __global__ void sum_counts_kernel(const int32_t* __restrict__ cnt, uint64_t n, unsigned long long* __restrict__ out) {
     unsigned long long a = 0;
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x)
@@ -1665,8 +1682,12 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             cache_reserve(c, total);
             c.tic();
             if (own) {
-                claim_cands_kernel<<<(unsigned)ceil_div(own * 32, 256), 256, 0, c.stream>>>(
-                    d_nodes, c.Cview(), sk, own, lo, capn, cand_id, cand_slot, cand_cnt);
+                if (capn > 256)
+                    claim_cands_flat_kernel<<<dim3((unsigned)own, (unsigned)ceil_div(capn, 256)), 256, 0, c.stream>>>(
+                        d_nodes, c.Cview(), sk, own, lo, capn, cand_id, cand_slot, cand_cnt);
+                else
+                    claim_cands_kernel<<<(unsigned)ceil_div(own * 32, 256), 256, 0, c.stream>>>(
+                        d_nodes, c.Cview(), sk, own, lo, capn, cand_id, cand_slot, cand_cnt);
                 NRG_LAUNCH_CHECK();
             }
         }
