@@ -70,7 +70,15 @@ struct DevBuf {
     void* ensure(size_t b) {
         if (b > bytes) {
             release();
-            const size_t nb = b + b / 4 + 256;
+            // size classes (4 per octave): requests of similar size land on the same
+            // block size, so the stream-ordered pool reuses freed blocks exactly instead
+            // of mapping new memory for each slightly different size
+            size_t nb = b + b / 4 + 256;
+            if (nb > (1u << 20)) {
+                int lg = 63 - __builtin_clzll((unsigned long long)nb);
+                const size_t q = (size_t)1 << (lg - 2);
+                nb = (nb + q - 1) / q * q;
+            }
             s = tl_stream;
             if (sync_alloc())
                 NRG_CUDA(cudaMalloc(&p, nb));
