@@ -449,7 +449,7 @@ struct DenseResolve {
     unsigned long long* cnt = nullptr;
     uint32_t* mark = nullptr;
 };
-constexpr unsigned long long kMarkTag = 0x7ff4ull << 48, kBusyTag = 0x7ff2ull << 48;
+constexpr unsigned long long kMarkTag = 0x7ff4ull << 48;
 __device__ __forceinline__ void dense_resolve_slot(const DenseResolve& R, uint32_t s) {
     if (!R.tri) return;
     // the marked-slot bitmap (L2) answers for the unmarked majority; clearing the bit

@@ -710,20 +710,6 @@ __global__ void u_new_bits_kernel(const int32_t* __restrict__ adj, const int32_t
         hasnew[i] = 1;
     }
 }
-__global__ void u_bits_kernel(const int32_t* __restrict__ adj, const int32_t* __restrict__ alen,
-                              const uint8_t* __restrict__ newf, uint64_t n, int cap, int W, uint32_t* __restrict__ ub,
-                              uint32_t* __restrict__ nb) {
-    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n * (uint64_t)cap) return;
-    const uint64_t i = t / cap;
-    const int a = (int)(t - i * cap);
-    if (a >= alen[i]) return;
-    const int32_t j = adj[t];
-    const uint32_t bit = 1u << (j & 31);
-    atomicOr(&ub[i * W + (j >> 5)], bit);
-    if (newf[t]) atomicOr(&nb[i * W + (j >> 5)], bit);
-}
-
 constexpr int kBitsMaxN = 32768;
 template <int NT>
 __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __restrict__ nodes, uint64_t n,
