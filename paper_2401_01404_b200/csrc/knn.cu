@@ -1017,24 +1017,34 @@ __global__ void __launch_bounds__(32 * kMergeWarps) knn_merge_warp_kernel(
         const double wd = bd[kw - 1];
         const int wg = bg[kw - 1];
         int m = kw;
-        for (int t0 = blk; t0 < min(cnt, blk + kMergeBlk); t0 += 32) {
-            const int t = t0 + lane;
-            double d = 0.0;
-            int32_t v = 0, g = 0;
-            bool better = false;
+        // the block's candidates (kMergeBlk / 32 per lane) are all loaded before any is
+        // compared: their dependent loads (slot -> cached distance, id -> global id) are
+        // in flight together instead of one 32-wide step at a time
+        constexpr int kPer = kMergeBlk / 32;
+        double dv[kPer];
+        int32_t vv[kPer], gv[kPer];
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int t = blk + 32 * q + lane;
+            dv[q] = 0.0;
+            vv[q] = gv[q] = 0;
             if (t < cnt) {
-                v = cand_id[li * capn + t];
+                vv[q] = cand_id[li * capn + t];
                 const uint32_t sl = cand_slot[li * capn + t];
-                d = (sl & kRemote) ? rvals[sl & ~kRemote] : cvals[sl];
-                g = nodes[v];
-                better = entry_less(d, g, wd, wg);
+                dv[q] = (sl & kRemote) ? rvals[sl & ~kRemote] : cvals[sl];
+                gv[q] = nodes[vv[q]];
             }
+        }
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int t = blk + 32 * q + lane;
+            const bool better = t < cnt && entry_less(dv[q], gv[q], wd, wg);
             const unsigned bal = __ballot_sync(0xffffffffu, better);
             if (better) {
                 const int at = m + __popc(bal & ((1u << lane) - 1u));
-                bd[at] = d;
-                bi[at] = v;
-                bg[at] = g;
+                bd[at] = dv[q];
+                bi[at] = vv[q];
+                bg[at] = gv[q];
                 bo[at] = 1;
             }
             m += __popc(bal);
