@@ -135,6 +135,8 @@ struct IsingSnap {
     const unsigned long long* BL;  // per node 64-bit Bloom mask of its coupling partners
     const double* Tsq;   // sum T64^2 per node (L''(0) = -(2M - Tsq_a - Tsq_b) for w_cur = 0)
     int M, Mp, Mw;
+    const uint32_t* P4;  // 4 bit planes of T4 = round(T / d4) per 32-sample word (first-pass screen)
+    const float4* Q4;    // per node {d4, E4 = sum |T - d4 T4| rounded up, sum T4, 0}
 };
 
 struct GaussSnap {
@@ -194,6 +196,7 @@ struct Context {
 
     // snapshot
     DevBuf T32, T64, T8, P8, Q8, BL, Tsq, U, xx;
+    DevBuf P4, Q4;  // 4-bit field planes and {d4, E4, sum T4} for the first-pass screen
     DevBuf U32, X32, nu;  // Gaussian screen: fp32 copies of U and X, ||U_i|| (fp64, rounded up)
     uint64_t snap_version = 0;
     uint64_t lp_version = 0;  // log_posterior memo (state version it was computed at)
@@ -260,7 +263,7 @@ struct Context {
     DevBuf s_a, s_b, s_c, s_d, s_e, s_f, s_g, s_h, s_i, s_j, s_k, s_l, s_m, s_n, s_o;
     DevBuf red;  // reduction scratch
     // scorer-private scratch (score_entries only)
-    DevBuf sc_surv, sc_g, sc_flag, sc_w32, sc_n;
+    DevBuf sc_surv, sc_g, sc_flag, sc_w32, sc_n, sc_rchk, sc_rn;
     std::vector<char> host_scratch;
 
     // multi-GPU: node-sharded NNDescent + key-sharded distance cache (comm.cuh)
@@ -283,7 +286,8 @@ struct Context {
     IsingSnap isnap() {
         return {dXb(), static_cast<float*>(T32.p), static_cast<double*>(T64.p), static_cast<int8_t*>(T8.p),
                 static_cast<uint32_t*>(P8.p), static_cast<float4*>(Q8.p),
-                static_cast<unsigned long long*>(BL.p), static_cast<double*>(Tsq.p), M, Mp, Mw};
+                static_cast<unsigned long long*>(BL.p), static_cast<double*>(Tsq.p), M, Mp, Mw,
+                static_cast<uint32_t*>(P4.p), static_cast<float4*>(Q4.p)};
     }
     GaussSnap gsnap() {
         return {dXd(), static_cast<double*>(U.p), static_cast<double*>(xx.p), dtheta(), M, Mp,

@@ -337,7 +337,11 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-template <int G, int WPL, int NS>
+// FOUR: the first pass on the stationary node's 4-bit field (4 bit planes instead of 8,
+// error E4): pairs it proves pruned are finished; every other pair (and every existing
+// coupling) goes to the recheck list `surv`, which the 8-bit pass (FOUR = false, sel =
+// that list) screens exactly as before, so K2 sees the same survivors and inputs.
+template <int G, int WPL, int NS, bool FOUR>
 __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(IsingSnap S, HashView W,
                                                                     const int32_t* __restrict__ es,
                                                                     const int32_t* __restrict__ ep, uint64_t n,
@@ -348,7 +352,8 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
                                                                     unsigned long long* __restrict__ nsurv,
                                                                     uint64_t* counters,
                                                                     const unsigned long long* __restrict__ n_dev,
-                                                                    unsigned long long* __restrict__ cnt_log) {
+                                                                    unsigned long long* __restrict__ cnt_log,
+                                                                    const uint64_t* __restrict__ sel) {
     if (n_dev) n = min(n, (uint64_t)*n_dev);
     if (cnt_log && blockIdx.x == 0 && threadIdx.x == 0) *cnt_log = n;
     constexpr int P = 32 / G;                      // pairs per step
@@ -360,7 +365,8 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
     unsigned char* wbuf = k1p_smem + (size_t)(threadIdx.x >> 5) * NS * P * RB;  // [stage][pair][row]
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    uint32_t Ps[WPL][8], Xs[WPL][8], bs[WPL];
+    constexpr int NP = FOUR ? 4 : 8;  // bit planes of the stationary field
+    uint32_t Ps[WPL][NP], Xs[WPL][8], bs[WPL];
     int cur = -1;
     uint64_t evals = 0;
     const float err0 = 4.f * (float)S.M * 5.9604645e-08f;
@@ -386,8 +392,9 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
     for (uint64_t c0 = warp0 * 32; c0 < n; c0 += nwarps * 32) {
         const int len = (int)min((uint64_t)32, n - c0);
         const int li = lane < len ? lane : 0;
-        const int my_s = es[c0 + li], my_p = ep[c0 + li];
-        const float4 qs = __ldg(&S.Q8[my_s]), qp = __ldg(&S.Q8[my_p]);
+        const uint64_t my_e = sel ? sel[c0 + li] : c0 + li;
+        const int my_s = es[my_e], my_p = ep[my_e];
+        const float4 qs = __ldg(FOUR ? &S.Q4[my_s] : &S.Q8[my_s]), qp = __ldg(&S.Q8[my_p]);
         const unsigned long long bl_s = __ldg(&S.BL[my_s]);
         int my_v = 0, my_a2 = 0;
 #pragma unroll
@@ -410,10 +417,15 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
                 for (int q = 0; q < WPL; ++q) {
                     const uint32_t w = r + G * q;
                     const uint64_t sw = (uint64_t)(uint32_t)s * Mw + w;
-                    const uint4* pp = reinterpret_cast<const uint4*>(S.P8 + sw * 8);
-                    const uint4 p0 = __ldg(pp), p1 = __ldg(pp + 1);
-                    Ps[q][0] = p0.x, Ps[q][1] = p0.y, Ps[q][2] = p0.z, Ps[q][3] = p0.w;
-                    Ps[q][4] = p1.x, Ps[q][5] = p1.y, Ps[q][6] = p1.z, Ps[q][7] = p1.w;
+                    if constexpr (FOUR) {
+                        const uint4 p0 = __ldg(reinterpret_cast<const uint4*>(S.P4 + sw * 4));
+                        Ps[q][0] = p0.x, Ps[q][1] = p0.y, Ps[q][2] = p0.z, Ps[q][3] = p0.w;
+                    } else {
+                        const uint4* pp = reinterpret_cast<const uint4*>(S.P8 + sw * 8);
+                        const uint4 p0 = __ldg(pp), p1 = __ldg(pp + 1);
+                        Ps[q][0] = p0.x, Ps[q][1] = p0.y, Ps[q][2] = p0.z, Ps[q][3] = p0.w;
+                        Ps[q][4] = p1.x, Ps[q][5] = p1.y, Ps[q][6] = p1.z, Ps[q][7] = p1.w;
+                    }
                     bs[q] = __ldg(&S.Xb[sw]);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) Xs[q][j] = pm1_bytes(bs[q] >> (4 * j));
@@ -432,8 +444,8 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
                 const uint32_t bp = *reinterpret_cast<const uint32_t*>(row + Mp + 4 * w);
                 int l7 = 0;
 #pragma unroll
-                for (int j = 0; j < 7; ++j) l7 += __popc(Ps[q][j] & bp) << j;
-                a1 += l7 - (__popc(Ps[q][7] & bp) << 7);
+                for (int j = 0; j < NP - 1; ++j) l7 += __popc(Ps[q][j] & bp) << j;
+                a1 += l7 - (__popc(Ps[q][NP - 1] & bp) << (NP - 1));
                 const uint32_t tw[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
 #pragma unroll
                 for (int j = 0; j < 8; ++j) a2 = __dp4a((int)tw[j], (int)Xs[q][j], a2);
@@ -465,9 +477,9 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
             my_g = (float)(2 * (S.M - 2 * dsum)) - (A + B);
             const float err = (qs.y + qp.y) * 1.0001f + err0;
             my_code = fabsf(my_g) <= lam - err ? 0 : (fabsf(my_g) < lam + err ? 2 : 1);
-            if (lane < len) ++evals;
+            if (lane < len && (!FOUR || my_code == 0)) ++evals;  // rechecked pairs count in the 8-bit pass
         }
-        const uint64_t e = c0 + lane;
+        const uint64_t e = my_e;
         if (lane < len && my_code == 0) {
             if (out.cache_vals) out.cache_vals[out.slot[e]] = pruned_dist;
             if (out.dist) out.dist[e] = pruned_dist;
@@ -483,8 +495,10 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
             if ((sv >> lane) & 1u) {
                 const unsigned long long i = at + __popc(sv & ((1u << lane) - 1u));
                 surv[i] = e;
-                surv_g[i] = my_g;
-                surv_flag[i] = (uint8_t)(my_code == 1 ? 0 : (my_code == 2 ? 1 : 2));
+                if (!FOUR) {
+                    surv_g[i] = my_g;
+                    surv_flag[i] = (uint8_t)(my_code == 1 ? 0 : (my_code == 2 ? 1 : 2));
+                }
             }
         }
     }
@@ -804,17 +818,34 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
             const bool full = c.Mw == G * WPL && !NRG_ENV_ON("NRG_K1_NOFULL");
             if (WPL == 2 && full && !NRG_ENV_ON("NRG_K1_NOPIPE")) {
                 static const int ns = getenv("NRG_K1_STAGES") ? atoi(getenv("NRG_K1_STAGES")) : 2;
+                const bool four = S.P4 && !NRG_ENV_ON("NRG_K1_NO4");
+                // first pass (4-bit): prunes what it can, lists the rest for the exact 8-bit pass
+                uint64_t* rl = four ? c.sc_rchk.as<uint64_t>(n) : nullptr;
+                unsigned long long* rn = four ? c.sc_rn.as<unsigned long long>(1) : nullptr;
+                if (four) NRG_CUDA(cudaMemsetAsync(rn, 0, 8, c.stream));
 #define NRG_LAUNCH_PIPE(NSV)                                                                                       \
     {                                                                                                              \
         constexpr size_t smem = (size_t)8 * (NSV) * 2 * (1024 + 128);                                             \
         static bool attr = false;                                                                                  \
         if (!attr) {                                                                                               \
-            NRG_CUDA(cudaFuncSetAttribute(ising_screen_pipe_kernel<16, 2, NSV>,                                    \
+            NRG_CUDA(cudaFuncSetAttribute(ising_screen_pipe_kernel<16, 2, NSV, false>,                             \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));                \
+            NRG_CUDA(cudaFuncSetAttribute(ising_screen_pipe_kernel<16, 2, NSV, true>,                              \
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));                \
             attr = true;                                                                                           \
         }                                                                                                          \
-        ising_screen_pipe_kernel<16, 2, NSV><<<(unsigned)sblocks, 256, smem, c.stream>>>(                          \
-            S, W, s, p, n, c.lambda, base, out, surv, surv_g, surv_flag, nsurv, c.dcounters(), n_dev, k1log);            \
+        if (four) {                                                                                                \
+            ising_screen_pipe_kernel<16, 2, NSV, true><<<(unsigned)sblocks, 256, smem, c.stream>>>(                \
+                S, W, s, p, n, c.lambda, base, out, rl, nullptr, nullptr, rn, c.dcounters(), n_dev, k1log,          \
+                nullptr);                                                                                          \
+            ising_screen_pipe_kernel<16, 2, NSV, false><<<(unsigned)sblocks, 256, smem, c.stream>>>(               \
+                S, W, s, p, n, c.lambda, base, out, surv, surv_g, surv_flag, nsurv, c.dcounters(), rn, nullptr,    \
+                rl);                                                                                               \
+        } else {                                                                                                   \
+            ising_screen_pipe_kernel<16, 2, NSV, false><<<(unsigned)sblocks, 256, smem, c.stream>>>(               \
+                S, W, s, p, n, c.lambda, base, out, surv, surv_g, surv_flag, nsurv, c.dcounters(), n_dev, k1log,   \
+                nullptr);                                                                                          \
+        }                                                                                                          \
     }
                 switch (ns) {
                     case 2: NRG_LAUNCH_PIPE(2); break;

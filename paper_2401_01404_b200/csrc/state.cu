@@ -429,13 +429,14 @@ __global__ void __launch_bounds__(256) snapshot_ising_kernel(const double* __res
                                                              double* __restrict__ T64, float* __restrict__ T32,
                                                              int8_t* __restrict__ T8, uint32_t* __restrict__ P8,
                                                              float4* __restrict__ Q, double* __restrict__ Tsq,
-                                                             const int32_t* __restrict__ rows) {
+                                                             const int32_t* __restrict__ rows, uint32_t* __restrict__ P4,
+                                                             float4* __restrict__ Q4) {
     const int r = rows ? rows[blockIdx.x] : (int)blockIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const double th = theta[r];
-    __shared__ double sh[8], sq[8];
-    __shared__ int si[8];
-    __shared__ float s_d;
+    __shared__ double sh[8], sq[8], sh4[8];
+    __shared__ int si[8], si4[8];
+    __shared__ float s_d, s_d4;
     double mx = 0.0, q = 0.0;
     for (int m = threadIdx.x; m < Mp; m += blockDim.x) {
         double t = 0.0;
@@ -460,12 +461,13 @@ __global__ void __launch_bounds__(256) snapshot_ising_kernel(const double* __res
         }
         Tsq[r] = b;
         s_d = a > 0.0 ? __double2float_ru(a / 127.0) : 1.0f;
+        s_d4 = a > 0.0 ? __double2float_ru(a / 7.0) : 1.0f;
     }
     __syncthreads();
-    const double d = (double)s_d;
+    const double d = (double)s_d, d4 = (double)s_d4;
     const int Mw = Mp >> 5;
-    double e = 0.0;
-    int sum = 0;
+    double e = 0.0, e4 = 0.0;
+    int sum = 0, sum4 = 0;
     for (int w = wid; w < Mw; w += 8) {
         const int m = 32 * w + lane;
         const double t = T64[(size_t)r * Mp + m];  // 0 on padding
@@ -481,23 +483,46 @@ __global__ void __launch_bounds__(256) snapshot_ising_kernel(const double* __res
             if (lane == k) mine = pl;
         }
         if (lane < 8) P8[((size_t)r * Mw + w) * 8 + lane] = mine;
+        if (P4) {
+            // the 4-bit field of the first-pass screen: T4 = round(T / d4), |T4| <= 7
+            int v4 = (int)rint(t / d4);
+            v4 = max(-7, min(7, v4));
+            e4 += fabs(t - d4 * (double)v4);
+            sum4 += v4;
+            uint32_t mine4 = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t pl = __ballot_sync(0xffffffffu, ((uint32_t)v4 >> k) & 1u);
+                if (lane == k) mine4 = pl;
+            }
+            if (lane < 4) P4[((size_t)r * Mw + w) * 4 + lane] = mine4;
+        }
     }
     e = warp_sum(e);
-    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    e4 = warp_sum(e4);
+    for (int o = 16; o; o >>= 1) {
+        sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        sum4 += __shfl_xor_sync(0xffffffffu, sum4, o);
+    }
     __syncthreads();
     if (lane == 0) {
         sh[wid] = e;
         si[wid] = sum;
+        sh4[wid] = e4;
+        si4[wid] = sum4;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double a = 0.0;
-        int b = 0;
+        double a = 0.0, a4 = 0.0;
+        int b = 0, b4 = 0;
         for (int w = 0; w < 8; ++w) {
             a += sh[w];
             b += si[w];
+            a4 += sh4[w];
+            b4 += si4[w];
         }
         Q[r] = make_float4(s_d, __double2float_ru(a * (1.0 + 1e-12)), __int_as_float(b), 0.f);
+        if (Q4) Q4[r] = make_float4(s_d4, __double2float_ru(a4 * (1.0 + 1e-12)), __int_as_float(b4), 0.f);
     }
 }
 
@@ -575,13 +600,17 @@ void ensure_snapshot(Context& c) {
         c.P8.ensure(nm);
         c.Q8.ensure((size_t)c.n * 16);
         c.Tsq.ensure((size_t)c.n * 8);
+        c.P4.ensure(nm / 2);
+        c.Q4.ensure((size_t)c.n * 16);
         snapshot_ising_kernel<<<c.n, 256, 0, c.stream>>>(c.dH(), c.dtheta(), c.M, c.Mp,
                                                          static_cast<double*>(c.T64.p),
                                                          static_cast<float*>(c.T32.p),
                                                          static_cast<int8_t*>(c.T8.p),
                                                          static_cast<uint32_t*>(c.P8.p),
                                                          static_cast<float4*>(c.Q8.p),
-                                                         static_cast<double*>(c.Tsq.p), nullptr);
+                                                         static_cast<double*>(c.Tsq.p), nullptr,
+                                                         static_cast<uint32_t*>(c.P4.p),
+                                                         static_cast<float4*>(c.Q4.p));
         build_bloom(c);
     } else {
         c.U.ensure(nm * 8);
@@ -613,7 +642,7 @@ void snapshot_rows(Context& c, const int32_t* rows, uint64_t nr) {
         snapshot_ising_kernel<<<(unsigned)nr, 256, 0, c.stream>>>(
             c.dH(), c.dtheta(), c.M, c.Mp, static_cast<double*>(c.T64.p), static_cast<float*>(c.T32.p),
             static_cast<int8_t*>(c.T8.p), static_cast<uint32_t*>(c.P8.p), static_cast<float4*>(c.Q8.p),
-            static_cast<double*>(c.Tsq.p), rows);
+            static_cast<double*>(c.Tsq.p), rows, static_cast<uint32_t*>(c.P4.p), static_cast<float4*>(c.Q4.p));
         build_bloom(c);  // the rows' couplings changed too
     } else
     {
