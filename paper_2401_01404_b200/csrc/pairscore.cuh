@@ -28,6 +28,7 @@ __device__ __forceinline__ double xsign(uint32_t word, int bit) {
 // bound).  Element m of a row is owned by thread m % NT of the scope.
 struct WarpScope {
     static constexpr int NT = 32;
+    static constexpr int KU = 4;  // independent accumulator sets per thread (fp64 passes)
     __device__ __forceinline__ int tid() const { return threadIdx.x & 31; }
     __device__ __forceinline__ void sum4(double& a, double& b, double& c, double& d) const {
         a = warp_sum(a);
@@ -37,9 +38,10 @@ struct WarpScope {
     }
     __device__ __forceinline__ double sum(double a) const { return warp_sum(a); }
 };
-template <int NT_>
+template <int NT_, int KU_ = 1>
 struct BlockScope {
     static constexpr int NT = NT_;
+    static constexpr int KU = KU_;
     double* red;  // shared scratch: 4 * (NT/32) + 4 doubles
     __device__ __forceinline__ int tid() const { return threadIdx.x; }
     __device__ __forceinline__ void sum4(double& a, double& b, double& c, double& d) const {
@@ -142,7 +144,7 @@ __device__ __forceinline__ Pass64 ising_pass64(const TP& T, const uint32_t* __re
     // kU independent accumulator sets per thread for a warp scope: the fp64 add chains,
     // not the math, bound a single-set loop at the occupancy the scoring kernels run at
     // (a CTA scope has enough warps and only a few samples per thread)
-    constexpr int kU = SC::NT >= 128 ? 1 : 4;
+    constexpr int kU = SC::KU;
     const int tid = sc.tid();
     const double t = tanh(D);
     const double omt2 = 1.0 - t * t;
@@ -222,14 +224,24 @@ __device__ __forceinline__ float rcp32(float x) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
+// kStaged: the two fp32 rows sit in shared memory at sa / sb (T32 unused)
+template <class SC = WarpScope, bool kStaged = false>
 __device__ __forceinline__ Pass32 ising_pass32(const float* __restrict__ T32, int Mp, const uint32_t* __restrict__ Xb,
-                                               int Mw, int M, int a, int b, float t, int dot) {
-    const int lane = threadIdx.x & 31;
-    const float4* Ta = reinterpret_cast<const float4*>(T32 + (size_t)a * Mp);
-    const float4* Tb = reinterpret_cast<const float4*>(T32 + (size_t)b * Mp);
+                                               int Mw, int M, int a, int b, float t, int dot, const SC& sc = SC(),
+                                               const float* sa = nullptr, const float* sb = nullptr) {
+    const int lane = sc.tid();
+    const float4* Ta = reinterpret_cast<const float4*>(kStaged ? sa : T32 + (size_t)a * Mp);
+    const float4* Tb = reinterpret_cast<const float4*>(kStaged ? sb : T32 + (size_t)b * Mp);
     float Sq = 0.f, Lq = 0.f;
-    for (int m0 = 4 * lane; m0 < M; m0 += 128) {
-        const float4 va = __ldg(&Ta[m0 >> 2]), vb = __ldg(&Tb[m0 >> 2]);
+    for (int m0 = 4 * lane; m0 < M; m0 += 4 * SC::NT) {
+        float4 va, vb;
+        if constexpr (kStaged) {
+            va = Ta[m0 >> 2];
+            vb = Tb[m0 >> 2];
+        } else {
+            va = __ldg(&Ta[m0 >> 2]);
+            vb = __ldg(&Tb[m0 >> 2]);
+        }
         const uint32_t wa = __ldg(&Xb[(size_t)a * Mw + (m0 >> 5)]) >> (m0 & 31);
         const uint32_t wb = __ldg(&Xb[(size_t)b * Mw + (m0 >> 5)]) >> (m0 & 31);
         const float ta[4] = {va.x, va.y, va.z, va.w}, tb[4] = {vb.x, vb.y, vb.z, vb.w};
@@ -249,10 +261,17 @@ __device__ __forceinline__ Pass32 ising_pass32(const float* __restrict__ T32, in
         Sq += s;
         Lq += l;
     }
+    if constexpr (SC::NT == 32) {
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        Sq += __shfl_xor_sync(0xffffffffu, Sq, o);
-        Lq += __shfl_xor_sync(0xffffffffu, Lq, o);
+        for (int o = 16; o; o >>= 1) {
+            Sq += __shfl_xor_sync(0xffffffffu, Sq, o);
+            Lq += __shfl_xor_sync(0xffffffffu, Lq, o);
+        }
+    } else {
+        double x = Sq, y = Lq, z = 0.0, w = 0.0;
+        sc.sum4(x, y, z, w);
+        Sq = (float)x;
+        Lq = (float)y;
     }
     return {(float)(2 * dot) - Sq, -(1.f - t * t) * Lq};
 }
@@ -345,14 +364,16 @@ __device__ EdgeOptD ising_newton64(const TP& T, const uint32_t* __restrict__ Xb,
 // quadratic-model start u; returns the fp32-converged iterate (|error| ~ 1e-7 / M) for
 // the single fp64 objective pass, or the start when fp32 cannot be trusted (|u| large,
 // no descent).  Adds the passes spent to *passes.
+template <class SC = WarpScope, bool kStaged = false>
 __device__ __forceinline__ double ising_newton32(const IsingSnap& S, int a, int b, double lambda, double dir,
-                                                 double u0, int dot, int* passes, bool* conv) {
+                                                 double u0, int dot, int* passes, bool* conv, const SC& sc = SC(),
+                                                 const float* sa = nullptr, const float* sb = nullptr) {
     *conv = false;
     float u = (float)u0;
     const float lam = (float)lambda, fd = (float)dir;
     for (int it = 0; it < 12; ++it) {
         if (!(u > 0.f && u < 2.f)) return u0;
-        const Pass32 p = ising_pass32(S.T32, S.Mp, S.Xb, S.Mw, S.M, a, b, tanhf(fd * u), dot);
+        const Pass32 p = ising_pass32<SC, kStaged>(S.T32, S.Mp, S.Xb, S.Mw, S.M, a, b, tanhf(fd * u), dot, sc, sa, sb);
         ++*passes;
         const float phi = fd * p.Lp - lam;
         if (!(p.Lpp < 0.f)) return u0;

@@ -565,6 +565,88 @@ __global__ void __launch_bounds__(128) ising_refine_kernel(IsingSnap S, HashView
     }
 }
 
+// K2 with one CTA per survivor: the per-sample loops of a pass cover M in one or two
+// steps of NT * KU independent samples, so a pass costs about one memory latency plus a
+// block reduction instead of M / 128 dependent warp steps; a launch holds a few thousand
+// survivors at most, so per-survivor latency, not throughput, bounds K2.
+template <int NT, int KU>
+__global__ void __launch_bounds__(NT) ising_refine_cta_kernel(IsingSnap S, HashView W, const int32_t* __restrict__ es,
+                                                               const int32_t* __restrict__ ep,
+                                                               const uint64_t* __restrict__ surv,
+                                                               const float* __restrict__ surv_g,
+                                                               const uint8_t* __restrict__ surv_flag, uint64_t ns,
+                                                               double lambda, double base, ScoreOut out,
+                                                               uint64_t* counters,
+                                                               const unsigned long long* __restrict__ ns_dev,
+                                                               unsigned long long* __restrict__ cnt_log) {
+    __shared__ double red[4 * (NT / 32) + 4];
+    extern __shared__ double k2_rows[];  // T64 rows a, b (Mp each), then T32 rows a, b
+    const BlockScope<NT, KU> sc{red};
+    if (ns_dev) ns = min(ns, (uint64_t)*ns_dev);
+    if (cnt_log && blockIdx.x == 0 && threadIdx.x == 0) *cnt_log = ns;
+    const int Mp = S.Mp;
+    double* ta = k2_rows;
+    double* tb = k2_rows + Mp;
+    float* fa = reinterpret_cast<float*>(k2_rows + 2 * Mp);
+    float* fb = fa + Mp;
+    for (uint64_t t = blockIdx.x; t < ns; t += gridDim.x) {
+        const uint64_t e = surv[t];
+        const int s = es[e], p = ep[e];
+        const int a = s < p ? s : p, b = s < p ? p : s;
+        const double wcur = hash_get(W, pair_key(a, b), 0.0);
+        const bool certain = surv_flag[t] == 0 && wcur == 0.0;
+        // stage the rows once: every pass of this survivor reads them from shared memory
+        {
+            const double2* ga = reinterpret_cast<const double2*>(S.T64 + (size_t)a * Mp);
+            const double2* gb = reinterpret_cast<const double2*>(S.T64 + (size_t)b * Mp);
+            for (int k = threadIdx.x; k < Mp / 2; k += NT) {
+                reinterpret_cast<double2*>(ta)[k] = __ldg(&ga[k]);
+                reinterpret_cast<double2*>(tb)[k] = __ldg(&gb[k]);
+            }
+            if (certain) {
+                const float4* ha = reinterpret_cast<const float4*>(S.T32 + (size_t)a * Mp);
+                const float4* hb = reinterpret_cast<const float4*>(S.T32 + (size_t)b * Mp);
+                for (int k = threadIdx.x; k < Mp / 4; k += NT) {
+                    reinterpret_cast<float4*>(fa)[k] = __ldg(&ha[k]);
+                    reinterpret_cast<float4*>(fb)[k] = __ldg(&hb[k]);
+                }
+            }
+            __syncthreads();
+        }
+        const TStaged T64{ta, tb, a};
+        EdgeOptD r;
+        if (certain) {
+            const float g = surv_g[t];
+            const double dir = g > 0.f ? 1.0 : -1.0;
+            const double phi0 = fabs((double)g) - lambda;
+            const double phi1 = -(2.0 * S.M - S.Tsq[a] - S.Tsq[b]);
+            const int dot = spin_dot<BlockScope<NT, KU>>(S.Xb, S.Mw, S.M, a, b, sc);
+            const double u0 = phi0 / fmax(-phi1, 1e-300);
+            int passes = 0;
+            bool conv = false;
+            const double u = ising_newton32<BlockScope<NT, KU>, true>(S, a, b, lambda, dir, u0, dot, &passes, &conv,
+                                                                       sc, fa, fb);
+            r = ising_newton64_at<TStaged, BlockScope<NT, KU>>(T64, S.Xb, S.Mw, S.M, a, b, 0.0, lambda, dir, u,
+                                                                conv ? 0.0 : u, passes, dot, sc);
+        } else {
+            r = ising_optimize_edge64<TStaged, BlockScope<NT, KU>>(T64, S.Xb, S.Mw, S.M, a, b, wcur, lambda, sc);
+        }
+        __syncthreads();  // rows restaged for the next survivor
+        if (threadIdx.x == 0) {
+            const double dist = -(base + r.gain);
+            if (out.cache_vals) out.cache_vals[out.slot[e]] = dist;
+            if (out.dist) out.dist[e] = dist;
+            if (out.w) out.w[e] = r.w;
+            if (out.gain) out.gain[e] = r.gain;
+            if (out.warn) out.warn[e] = (uint8_t)r.warn;
+            if (counters) {
+                atomicAdd((unsigned long long*)&counters[C_EVALS], (unsigned long long)r.passes);
+                if (r.warn) atomicAdd((unsigned long long*)&counters[C_WARN], 1ull);
+            }
+        }
+    }
+}
+
 // Gaussian screen (exact mode): for w_cur = 0 the slice maximum is at the kink (w* = 0,
 // gain exactly 0, dist = -base) iff |P| <= lambda, P = <u_a, x_b> + <u_b, x_a>
 // (gauss_optimize).  P is formed in fp32 from fp32 copies of U and X with a rigorous
@@ -752,8 +834,23 @@ void refine_survivors(Context& c, const int32_t* s, const int32_t* p, const uint
     const uint64_t rb = std::min<uint64_t>(ceil_div((int64_t)ns * 32, 128), (uint64_t)num_sms(c) * 16);
     int slot = -1;
     unsigned long long* lg = ns_dev ? c.log_slot(&slot) : nullptr;
-    ising_refine_kernel<<<(unsigned)rb, 128, 0, c.stream>>>(c.isnap(), c.Wview(), s, p, surv, surv_g, surv_flag, ns,
-                                                            c.lambda, base, out, c.dcounters(), ns_dev, lg);
+    // CTA-per-survivor K2 (NT 128, 4 samples per thread per step); NRG_K2_WARP=1 keeps
+    // the warp-per-survivor kernel (A/B: profiles/r01_k2_cta/)
+    if (!NRG_ENV_ON("NRG_K2_WARP")) {
+        const uint64_t cb = std::min<uint64_t>(ns, (uint64_t)num_sms(c) * 32);
+        const size_t smem = (size_t)c.Mp * 24;
+        static size_t smem_set = 0;
+        if (smem > smem_set) {
+            NRG_CUDA(cudaFuncSetAttribute(ising_refine_cta_kernel<128, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+            smem_set = smem;
+        }
+        ising_refine_cta_kernel<128, 4><<<(unsigned)cb, 128, smem, c.stream>>>(
+            c.isnap(), c.Wview(), s, p, surv, surv_g, surv_flag, ns, c.lambda, base, out, c.dcounters(), ns_dev, lg);
+    } else {
+        ising_refine_kernel<<<(unsigned)rb, 128, 0, c.stream>>>(c.isnap(), c.Wview(), s, p, surv, surv_g, surv_flag,
+                                                                ns, c.lambda, base, out, c.dcounters(), ns_dev, lg);
+    }
     NRG_LAUNCH_CHECK();
     c.span(T_K2, a, (double)ns, slot);
 }
