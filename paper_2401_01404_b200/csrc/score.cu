@@ -358,7 +358,9 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
     if (cnt_log && blockIdx.x == 0 && threadIdx.x == 0) *cnt_log = n;
     constexpr int P = 32 / G;                      // pairs per step
     constexpr uint32_t Mw = G * WPL, Mp = 32 * Mw;  // words / bytes of a row
-    constexpr int RB = Mp + 4 * Mw;                 // staged row: int8 field + spin words
+    // staged partner row: int8 field (4-bit planes in the FOUR pass) + spin words
+    constexpr int FB = FOUR ? Mp / 2 : Mp;
+    constexpr int RB = FB + 4 * Mw;
     constexpr int CH = RB / 16;                     // 16-byte chunks per staged row
     extern __shared__ __align__(16) unsigned char k1p_smem[];
     const int lane = threadIdx.x & 31, grp = lane / G, r = lane % G;
@@ -380,11 +382,12 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
             cp_async_commit();
             return;
         }
-        const unsigned char* t8 = reinterpret_cast<const unsigned char*>(S.T8) + (uint64_t)(uint32_t)p * Mp;
+        const unsigned char* t8 = FOUR ? reinterpret_cast<const unsigned char*>(S.P4) + (uint64_t)(uint32_t)p * FB
+                                       : reinterpret_cast<const unsigned char*>(S.T8) + (uint64_t)(uint32_t)p * Mp;
         const unsigned char* xb = reinterpret_cast<const unsigned char*>(S.Xb) + (uint64_t)(uint32_t)p * Mw * 4;
 #pragma unroll
         for (int c = r; c < CH; c += G) {
-            const unsigned char* src = c < (int)(Mp / 16) ? t8 + 16 * c : xb + 16 * (c - (int)(Mp / 16));
+            const unsigned char* src = c < (int)(FB / 16) ? t8 + 16 * c : xb + 16 * (c - (int)(FB / 16));
             cp_async16(dst + 16 * c, src);
         }
         cp_async_commit();
@@ -394,7 +397,7 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
         const int li = lane < len ? lane : 0;
         const uint64_t my_e = sel ? sel[c0 + li] : c0 + li;
         const int my_s = es[my_e], my_p = ep[my_e];
-        const float4 qs = __ldg(FOUR ? &S.Q4[my_s] : &S.Q8[my_s]), qp = __ldg(&S.Q8[my_p]);
+        const float4 qs = __ldg(FOUR ? &S.Q4[my_s] : &S.Q8[my_s]), qp = __ldg(FOUR ? &S.Q4[my_p] : &S.Q8[my_p]);
         const unsigned long long bl_s = __ldg(&S.BL[my_s]);
         int my_v = 0, my_a2 = 0;
 #pragma unroll
@@ -427,8 +430,10 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
                         Ps[q][4] = p1.x, Ps[q][5] = p1.y, Ps[q][6] = p1.z, Ps[q][7] = p1.w;
                     }
                     bs[q] = __ldg(&S.Xb[sw]);
+                    if constexpr (!FOUR) {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) Xs[q][j] = pm1_bytes(bs[q] >> (4 * j));
+                        for (int j = 0; j < 8; ++j) Xs[q][j] = pm1_bytes(bs[q] >> (4 * j));
+                    }
                 }
                 cur = s;
             }
@@ -439,16 +444,24 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
 #pragma unroll
             for (int q = 0; q < WPL; ++q) {
                 const uint32_t w = r + G * q;
-                const uint4 t0 = *reinterpret_cast<const uint4*>(row + 32 * w);
-                const uint4 t1 = *reinterpret_cast<const uint4*>(row + 32 * w + 16);
-                const uint32_t bp = *reinterpret_cast<const uint32_t*>(row + Mp + 4 * w);
+                const uint32_t bp = *reinterpret_cast<const uint32_t*>(row + FB + 4 * w);
                 int l7 = 0;
 #pragma unroll
                 for (int j = 0; j < NP - 1; ++j) l7 += __popc(Ps[q][j] & bp) << j;
                 a1 += l7 - (__popc(Ps[q][NP - 1] & bp) << (NP - 1));
-                const uint32_t tw[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+                if constexpr (FOUR) {
+                    // partner's 4-bit planes against the stationary spins: sum of T4_p over
+                    // the samples with x_s = +1 (B = d_p (2 a2 - sum4_p) below)
+                    const uint4 pp = *reinterpret_cast<const uint4*>(row + 16 * w);
+                    a2 += __popc(pp.x & bs[q]) + (__popc(pp.y & bs[q]) << 1) + (__popc(pp.z & bs[q]) << 2) -
+                          (__popc(pp.w & bs[q]) << 3);
+                } else {
+                    const uint4 t0 = *reinterpret_cast<const uint4*>(row + 32 * w);
+                    const uint4 t1 = *reinterpret_cast<const uint4*>(row + 32 * w + 16);
+                    const uint32_t tw[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
 #pragma unroll
-                for (int j = 0; j < 8; ++j) a2 = __dp4a((int)tw[j], (int)Xs[q][j], a2);
+                    for (int j = 0; j < 8; ++j) a2 = __dp4a((int)tw[j], (int)Xs[q][j], a2);
+                }
                 diff += __popc(bs[q] ^ bp);
             }
             __syncwarp();  // the buffer is re-staged NS - 1 steps from now
@@ -473,7 +486,7 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
             const int dsum = my_v & 4095;
             const int asum = (my_v - dsum) >> 12;
             const float A = qs.x * (float)(2 * asum - __float_as_int(qs.z));
-            const float B = qp.x * (float)my_a2;
+            const float B = FOUR ? qp.x * (float)(2 * my_a2 - __float_as_int(qp.z)) : qp.x * (float)my_a2;
             my_g = (float)(2 * (S.M - 2 * dsum)) - (A + B);
             const float err = (qs.y + qp.y) * 1.0001f + err0;
             my_code = fabsf(my_g) <= lam - err ? 0 : (fabsf(my_g) < lam + err ? 2 : 1);
@@ -923,6 +936,7 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
 #define NRG_LAUNCH_PIPE(NSV)                                                                                       \
     {                                                                                                              \
         constexpr size_t smem = (size_t)8 * (NSV) * 2 * (1024 + 128);                                             \
+        constexpr size_t smem4 = (size_t)8 * (NSV) * 2 * (512 + 128);                                             \
         static bool attr = false;                                                                                  \
         if (!attr) {                                                                                               \
             NRG_CUDA(cudaFuncSetAttribute(ising_screen_pipe_kernel<16, 2, NSV, false>,                             \
@@ -932,7 +946,7 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
             attr = true;                                                                                           \
         }                                                                                                          \
         if (four) {                                                                                                \
-            ising_screen_pipe_kernel<16, 2, NSV, true><<<(unsigned)sblocks, 256, smem, c.stream>>>(                \
+            ising_screen_pipe_kernel<16, 2, NSV, true><<<(unsigned)sblocks, 256, smem4, c.stream>>>(               \
                 S, W, s, p, n, c.lambda, base, out, rl, nullptr, nullptr, rn, c.dcounters(), n_dev, k1log,          \
                 nullptr);                                                                                          \
             ising_screen_pipe_kernel<16, 2, NSV, false><<<(unsigned)sblocks, 256, smem, c.stream>>>(               \
