@@ -441,6 +441,35 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
             __syncwarp();
             const unsigned char* row = wbuf + (size_t)(st * P + grp) * RB;
             int a1 = 0, a2 = 0, diff = 0;
+            if constexpr (FOUR && WPL % 2 == 0) {
+                // carry-save form: offset-binary planes (T4 + 8: the sign plane inverted) of the
+                // lane's two words summed bit-sliced per weight (w1 half adder, w2/w4/w8 full
+                // adders), 5 popcounts per side instead of 8; the offset 8 npl comes off below
+                auto csa = [](uint32_t x0, uint32_t x1, uint32_t y0, uint32_t y1, uint32_t z0, uint32_t z1, uint32_t u0,
+                              uint32_t u1) {
+                    uint32_t s1 = x0 ^ x1, c = x0 & x1;
+                    const uint32_t s2 = y0 ^ y1 ^ c;
+                    c = (y0 & y1) | (c & (y0 ^ y1));
+                    const uint32_t s4 = z0 ^ z1 ^ c;
+                    c = (z0 & z1) | (c & (z0 ^ z1));
+                    const uint32_t s8 = u0 ^ u1 ^ c;
+                    c = (u0 & u1) | (c & (u0 ^ u1));
+                    return __popc(s1) + (__popc(s2) << 1) + (__popc(s4) << 2) + (__popc(s8) << 3) + (__popc(c) << 4);
+                };
+#pragma unroll
+                for (int q = 0; q < WPL; q += 2) {
+                    const uint32_t w0 = r + G * q, w1 = r + G * (q + 1);
+                    const uint32_t bp0 = *reinterpret_cast<const uint32_t*>(row + FB + 4 * w0);
+                    const uint32_t bp1 = *reinterpret_cast<const uint32_t*>(row + FB + 4 * w1);
+                    const uint4 q0 = *reinterpret_cast<const uint4*>(row + 16 * w0);
+                    const uint4 q1 = *reinterpret_cast<const uint4*>(row + 16 * w1);
+                    a1 += csa(Ps[q][0] & bp0, Ps[q + 1][0] & bp1, Ps[q][1] & bp0, Ps[q + 1][1] & bp1, Ps[q][2] & bp0,
+                              Ps[q + 1][2] & bp1, ~Ps[q][3] & bp0, ~Ps[q + 1][3] & bp1);
+                    a2 += csa(q0.x & bs[q], q1.x & bs[q + 1], q0.y & bs[q], q1.y & bs[q + 1], q0.z & bs[q],
+                              q1.z & bs[q + 1], ~q0.w & bs[q], ~q1.w & bs[q + 1]);
+                    diff += __popc(bs[q] ^ bp0) + __popc(bs[q + 1] ^ bp1);
+                }
+            } else
 #pragma unroll
             for (int q = 0; q < WPL; ++q) {
                 const uint32_t w = r + G * q;
@@ -484,9 +513,14 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
         const double wcur = (lane < len && (bl_s & bloom_bit(my_p))) ? hash_get(W, pair_key(my_s, my_p), 0.0) : 0.0;
         if (wcur == 0.0) {
             const int dsum = my_v & 4095;
-            const int asum = (my_v - dsum) >> 12;
+            int asum = (my_v - dsum) >> 12;
+            int bsum = my_a2;
+            if (FOUR && WPL % 2 == 0) {  // offset-binary sums: remove 8 per +1 sample
+                asum -= 8 * __float_as_int(qp.w);
+                bsum -= 8 * __float_as_int(qs.w);
+            }
             const float A = qs.x * (float)(2 * asum - __float_as_int(qs.z));
-            const float B = FOUR ? qp.x * (float)(2 * my_a2 - __float_as_int(qp.z)) : qp.x * (float)my_a2;
+            const float B = FOUR ? qp.x * (float)(2 * bsum - __float_as_int(qp.z)) : qp.x * (float)my_a2;
             my_g = (float)(2 * (S.M - 2 * dsum)) - (A + B);
             const float err = (qs.y + qp.y) * 1.0001f + err0;
             my_code = fabsf(my_g) <= lam - err ? 0 : (fabsf(my_g) < lam + err ? 2 : 1);
@@ -933,6 +967,7 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
                 uint64_t* rl = four ? c.sc_rchk.as<uint64_t>(n) : nullptr;
                 unsigned long long* rn = four ? c.sc_rn.as<unsigned long long>(1) : nullptr;
                 if (four) NRG_CUDA(cudaMemsetAsync(rn, 0, 8, c.stream));
+                static const int g4 = getenv("NRG_K1_G4") ? atoi(getenv("NRG_K1_G4")) : 8;  // lanes per pair (4-bit pass)
 #define NRG_LAUNCH_PIPE(NSV)                                                                                       \
     {                                                                                                              \
         constexpr size_t smem = (size_t)8 * (NSV) * 2 * (1024 + 128);                                             \
@@ -946,9 +981,32 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
             attr = true;                                                                                           \
         }                                                                                                          \
         if (four) {                                                                                                \
-            ising_screen_pipe_kernel<16, 2, NSV, true><<<(unsigned)sblocks, 256, smem4, c.stream>>>(               \
-                S, W, s, p, n, c.lambda, base, out, rl, nullptr, nullptr, rn, c.dcounters(), n_dev, k1log,          \
-                nullptr);                                                                                          \
+            if (g4 == 8) {                                                                                         \
+                constexpr size_t sm8 = (size_t)8 * (NSV) * 4 * (512 + 128);                                        \
+                static bool attr8 = false;                                                                         \
+                if (!attr8) {                                                                                      \
+                    NRG_CUDA(cudaFuncSetAttribute(ising_screen_pipe_kernel<8, 4, NSV, true>,                       \
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm8));         \
+                    attr8 = true;                                                                                  \
+                }                                                                                                  \
+                ising_screen_pipe_kernel<8, 4, NSV, true><<<(unsigned)sblocks, 256, sm8, c.stream>>>(              \
+                    S, W, s, p, n, c.lambda, base, out, rl, nullptr, nullptr, rn, c.dcounters(), n_dev, k1log,      \
+                    nullptr);                                                                                      \
+            } else if (g4 == 4) {                                                                                  \
+                constexpr size_t sm4 = (size_t)8 * (NSV) * 8 * (512 + 128);                                        \
+                static bool attr4 = false;                                                                         \
+                if (!attr4) {                                                                                      \
+                    NRG_CUDA(cudaFuncSetAttribute(ising_screen_pipe_kernel<4, 8, NSV, true>,                       \
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm4));         \
+                    attr4 = true;                                                                                  \
+                }                                                                                                  \
+                ising_screen_pipe_kernel<4, 8, NSV, true><<<(unsigned)sblocks, 256, sm4, c.stream>>>(              \
+                    S, W, s, p, n, c.lambda, base, out, rl, nullptr, nullptr, rn, c.dcounters(), n_dev, k1log,      \
+                    nullptr);                                                                                      \
+            } else                                                                                                 \
+                ising_screen_pipe_kernel<16, 2, NSV, true><<<(unsigned)sblocks, 256, smem4, c.stream>>>(           \
+                    S, W, s, p, n, c.lambda, base, out, rl, nullptr, nullptr, rn, c.dcounters(), n_dev, k1log,      \
+                    nullptr);                                                                                      \
             ising_screen_pipe_kernel<16, 2, NSV, false><<<(unsigned)sblocks, 256, smem, c.stream>>>(               \
                 S, W, s, p, n, c.lambda, base, out, surv, surv_g, surv_flag, nsurv, c.dcounters(), rn, nullptr,    \
                 rl);                                                                                               \

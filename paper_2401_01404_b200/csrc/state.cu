@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(256) snapshot_ising_kernel(const double* __res
                                                              int8_t* __restrict__ T8, uint32_t* __restrict__ P8,
                                                              float4* __restrict__ Q, double* __restrict__ Tsq,
                                                              const int32_t* __restrict__ rows, uint32_t* __restrict__ P4,
-                                                             float4* __restrict__ Q4) {
+                                                             float4* __restrict__ Q4, const uint32_t* __restrict__ Xb) {
     const int r = rows ? rows[blockIdx.x] : (int)blockIdx.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const double th = theta[r];
@@ -467,8 +467,9 @@ __global__ void __launch_bounds__(256) snapshot_ising_kernel(const double* __res
     const double d = (double)s_d, d4 = (double)s_d4;
     const int Mw = Mp >> 5;
     double e = 0.0, e4 = 0.0;
-    int sum = 0, sum4 = 0;
+    int sum = 0, sum4 = 0, npl = 0;  // npl: samples with x = +1 (the 4-bit screen's offset term)
     for (int w = wid; w < Mw; w += 8) {
+        if (lane == 0 && Xb) npl += __popc(Xb[(size_t)r * Mw + w]);
         const int m = 32 * w + lane;
         const double t = T64[(size_t)r * Mp + m];  // 0 on padding
         int v = (int)rint(t / d);
@@ -504,25 +505,28 @@ __global__ void __launch_bounds__(256) snapshot_ising_kernel(const double* __res
         sum += __shfl_xor_sync(0xffffffffu, sum, o);
         sum4 += __shfl_xor_sync(0xffffffffu, sum4, o);
     }
+    __shared__ int snpl[8];
     __syncthreads();
     if (lane == 0) {
         sh[wid] = e;
         si[wid] = sum;
         sh4[wid] = e4;
         si4[wid] = sum4;
+        snpl[wid] = npl;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         double a = 0.0, a4 = 0.0;
-        int b = 0, b4 = 0;
+        int b = 0, b4 = 0, np = 0;
         for (int w = 0; w < 8; ++w) {
             a += sh[w];
             b += si[w];
             a4 += sh4[w];
             b4 += si4[w];
+            np += snpl[w];
         }
         Q[r] = make_float4(s_d, __double2float_ru(a * (1.0 + 1e-12)), __int_as_float(b), 0.f);
-        if (Q4) Q4[r] = make_float4(s_d4, __double2float_ru(a4 * (1.0 + 1e-12)), __int_as_float(b4), 0.f);
+        if (Q4) Q4[r] = make_float4(s_d4, __double2float_ru(a4 * (1.0 + 1e-12)), __int_as_float(b4), __int_as_float(np));
     }
 }
 
@@ -610,7 +614,7 @@ void ensure_snapshot(Context& c) {
                                                          static_cast<float4*>(c.Q8.p),
                                                          static_cast<double*>(c.Tsq.p), nullptr,
                                                          static_cast<uint32_t*>(c.P4.p),
-                                                         static_cast<float4*>(c.Q4.p));
+                                                         static_cast<float4*>(c.Q4.p), c.dXb());
         build_bloom(c);
     } else {
         c.U.ensure(nm * 8);
@@ -642,7 +646,8 @@ void snapshot_rows(Context& c, const int32_t* rows, uint64_t nr) {
         snapshot_ising_kernel<<<(unsigned)nr, 256, 0, c.stream>>>(
             c.dH(), c.dtheta(), c.M, c.Mp, static_cast<double*>(c.T64.p), static_cast<float*>(c.T32.p),
             static_cast<int8_t*>(c.T8.p), static_cast<uint32_t*>(c.P8.p), static_cast<float4*>(c.Q8.p),
-            static_cast<double*>(c.Tsq.p), rows, static_cast<uint32_t*>(c.P4.p), static_cast<float4*>(c.Q4.p));
+            static_cast<double*>(c.Tsq.p), rows, static_cast<uint32_t*>(c.P4.p), static_cast<float4*>(c.Q4.p),
+            c.dXb());
         build_bloom(c);  // the rows' couplings changed too
     } else
     {

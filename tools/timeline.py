@@ -55,7 +55,8 @@ for e in k:
     if "cub::" in n:
         n = "cub::" + n.split("::")[-1].split("<")[0][:24] + ("<TriKey>" if "TriKey" in n or "Key128" in n else "")
     else:
-        n = n.split("(")[0].split("<")[0]
+        full = n.split("(")[0]
+        n = full.split("<")[0] + (("[4-bit]" if "true>" in full else "[8-bit]") if "screen_pipe" in full else "")
     agg.setdefault(n, [0, 0.0])
     agg[n][0] += 1
     agg[n][1] += e["dur"]
