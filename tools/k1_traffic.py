@@ -8,11 +8,11 @@ st = json.load(open(sys.argv[2]))
 agg = {}
 for r in rows:
     name = r[4]
-    tag = "4-bit" if ", true>" in name else "8-bit"
+    tag = "4-bit" if (", true>" in name or ", 1>(" in name) else "8-bit"
     a = agg.setdefault(tag, {"launches": set(), "read": 0.0, "write": 0.0, "ms": 0.0})
     a["launches"].add(r[0])
     unit, val = r[13], float(r[14].replace(",", ""))
-    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-3, "msecond": 1.0, "nsecond": 1e-6}[unit]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-3, "msecond": 1.0, "nsecond": 1e-6, "ns": 1e-6, "us": 1e-3, "ms": 1.0}[unit]
     if r[12] == "dram__bytes_read.sum": a["read"] += val * scale
     elif r[12] == "dram__bytes_write.sum": a["write"] += val * scale
     elif r[12] == "gpu__time_duration.sum": a["ms"] += val * scale
