@@ -239,6 +239,11 @@ struct Context {
     double tail_rounds = 0;  // apply_updates: parallel rounds spent on tie tails
     double tc_launches = 0, tc_pairs = 0;  // tensor-core exhaustive screen
     double cache_flushes = 0;              // distance-cache flushes (generation exceeded 2^31 slots)
+    double flushes_at_gen = 0;             // cache_flushes when the current generation began
+    // K2 launch shape: the largest survivor count of a K2 launch (device, reset per
+    // generation) and whether this generation may need the warp kernel (see refine_survivors)
+    DevBuf k2max;
+    bool k2_wide = true;
     uint64_t launches0 = 0;
 
     // Deferred device timing: tic/toc record events on the stream and queue a span;

@@ -569,8 +569,10 @@ __global__ void __launch_bounds__(128) ising_refine_kernel(IsingSnap S, HashView
                                                             double lambda, double base, ScoreOut out,
                                                             uint64_t* counters,
                                                             const unsigned long long* __restrict__ ns_dev,
-                                                            unsigned long long* __restrict__ cnt_log) {
+                                                            unsigned long long* __restrict__ cnt_log,
+                                                            uint64_t min_ns = 0) {
     if (ns_dev) ns = min(ns, (uint64_t)*ns_dev);
+    if (ns <= min_ns) return;  // few survivors: the CTA kernel launched before this one took them
     if (cnt_log && blockIdx.x == 0 && threadIdx.x == 0) *cnt_log = ns;
     const int lane = threadIdx.x & 31;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -625,12 +627,15 @@ __global__ void __launch_bounds__(NT) ising_refine_cta_kernel(IsingSnap S, HashV
                                                                double lambda, double base, ScoreOut out,
                                                                uint64_t* counters,
                                                                const unsigned long long* __restrict__ ns_dev,
-                                                               unsigned long long* __restrict__ cnt_log) {
+                                                               unsigned long long* __restrict__ cnt_log,
+                                                               uint64_t max_ns, unsigned long long* k2max) {
     __shared__ double red[4 * (NT / 32) + 4];
     extern __shared__ double k2_rows[];  // T64 rows a, b (Mp each), then T32 rows a, b
     const BlockScope<NT, KU> sc{red};
     if (ns_dev) ns = min(ns, (uint64_t)*ns_dev);
     if (cnt_log && blockIdx.x == 0 && threadIdx.x == 0) *cnt_log = ns;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && k2max) atomicMax(k2max, (unsigned long long)ns);
+    if (ns > max_ns) return;  // many survivors: the warp kernel launched after this one takes them
     const int Mp = S.Mp;
     double* ta = k2_rows;
     double* tb = k2_rows + Mp;
@@ -892,8 +897,22 @@ void refine_survivors(Context& c, const int32_t* s, const int32_t* p, const uint
                                           (int)smem));
             smem_set = smem;
         }
+        // The survivor count is on the device.  Up to 4 survivors per CTA the CTA kernel
+        // (latency-bound launches), beyond that the warp kernel (first sweeps: millions,
+        // throughput-bound); each exits at once when the count is the other's.  When the
+        // last generation's launches all fit CTA mode (the steady state) only the CTA
+        // kernel is launched and takes any count.
+        const uint64_t max_ns = c.k2_wide ? 4 * cb : ~0ull;
+        if (!c.k2max.p) NRG_CUDA(cudaMemsetAsync(c.k2max.as<unsigned long long>(1), 0, 8, c.stream));
+        unsigned long long* k2max = static_cast<unsigned long long*>(c.k2max.p);
         ising_refine_cta_kernel<128, 4><<<(unsigned)cb, 128, smem, c.stream>>>(
-            c.isnap(), c.Wview(), s, p, surv, surv_g, surv_flag, ns, c.lambda, base, out, c.dcounters(), ns_dev, lg);
+            c.isnap(), c.Wview(), s, p, surv, surv_g, surv_flag, ns, c.lambda, base, out, c.dcounters(), ns_dev, lg,
+            max_ns, k2max);
+        if (c.k2_wide && ns > max_ns)
+            ising_refine_kernel<<<(unsigned)rb, 128, 0, c.stream>>>(c.isnap(), c.Wview(), s, p, surv, surv_g,
+                                                                    surv_flag, ns, c.lambda, base, out, c.dcounters(),
+                                                                    ns_dev, lg, max_ns);
+
     } else {
         ising_refine_kernel<<<(unsigned)rb, 128, 0, c.stream>>>(c.isnap(), c.Wview(), s, p, surv, surv_g, surv_flag,
                                                                 ns, c.lambda, base, out, c.dcounters(), ns_dev, lg);

@@ -604,8 +604,11 @@ void ensure_snapshot(Context& c) {
         c.P8.ensure(nm);
         c.Q8.ensure((size_t)c.n * 16);
         c.Tsq.ensure((size_t)c.n * 8);
-        c.P4.ensure(nm / 2);
-        c.Q4.ensure((size_t)c.n * 16);
+        // the 4-bit first pass runs on the pipelined K1 only (M in (992, 1024])
+        if (c.Mw == 32) {
+            c.P4.ensure(nm / 2);
+            c.Q4.ensure((size_t)c.n * 16);
+        }
         snapshot_ising_kernel<<<c.n, 256, 0, c.stream>>>(c.dH(), c.dtheta(), c.M, c.Mp,
                                                          static_cast<double*>(c.T64.p),
                                                          static_cast<float*>(c.T32.p),
@@ -853,14 +856,22 @@ void begin_generation(Context& c) {
     if (c.Ccap) {
         // size the (now empty) memo for the previous generation's pairs + 30%: growing
         // here costs an allocation, growing mid-generation a rehash of every entry
-        uint64_t live = 0;
+        uint64_t live = 0, k2max = ~0ull;
         NRG_CUDA(cudaMemcpyAsync(&live, c.Ccount.p, 8, cudaMemcpyDeviceToHost, c.stream));
+        if (c.k2max.p) NRG_CUDA(cudaMemcpyAsync(&k2max, c.k2max.p, 8, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
+        // the next generation launches the warp kernel too only if this one needed it
+        // (3 x 148 x 32 x 4: CTA-mode capacity with room; a wrong guess costs time only)
+        c.k2_wide = k2max > 3ull * 148 * 32 * 4 / 2;
+        if (c.k2max.p) NRG_CUDA(cudaMemsetAsync(c.k2max.p, 0, 8, c.stream));
         // (shrinks too: clearing and scanning an oversized memo costs HBM time every sweep)
         const uint64_t want = std::min<uint64_t>(live + live / 10 * 3, (1ull << 31) * 6 / 10);
         const uint64_t ncap =
             std::max<uint64_t>(1u << 20, std::min<uint64_t>(next_pow2(want * 10 / 6 + 1), 1ull << 31));
-        if (ncap != c.Ccap) {
+        // a generation that flushed the memo counted only the pairs since its last flush:
+        // keep the size (config 5 would otherwise free and re-map tens of GB every sweep)
+        const bool flushed = c.cache_flushes != c.flushes_at_gen;
+        if (ncap != c.Ccap && !(flushed && ncap < c.Ccap)) {
             c.Ckeys = DevBuf();
             c.Cvals = DevBuf();
             c.Ckeys.ensure(ncap * 8);
@@ -873,6 +884,7 @@ void begin_generation(Context& c) {
     c.cache_live_host = 0;
     c.cache_live_bound = 0;
     c.base_valid = false;
+    c.flushes_at_gen = c.cache_flushes;
 }
 
 __global__ void add_u64_kernel(unsigned long long* p, unsigned long long v) { *p += v; }

@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+O=gpurun_out/r01t13
+mkdir -p $O
+for v in "NRG_X=1" "NRG_X=1"; do env $v timeout 300 python tools/steady_sweep.py > "$O/steady_${v// /_}.$RANDOM.log" 2>&1; done
+timeout 900 python tools/config_runs.py 5 5 > $O/cfg5.log 2>&1; echo "rc=$?" >> $O/cfg5.log
