@@ -16,6 +16,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
 #include <cstdlib>
 #include <vector>
@@ -80,10 +81,16 @@ struct DevBuf {
                 nb = (nb + q - 1) / q * q;
             }
             s = tl_stream;
+            static const bool dbg = getenv("NRG_DEBUG_ALLOC") != nullptr;
+            const auto t0 = dbg ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point();
             if (sync_alloc())
                 NRG_CUDA(cudaMalloc(&p, nb));
             else
                 NRG_CUDA(cudaMallocAsync(&p, nb, s));
+            if (dbg) {
+                const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+                if (ms > 1.0) fprintf(stderr, "alloc %.3f GB took %.1f ms\n", nb / 1e9, ms);
+            }
             bytes = nb;
         }
         return p;
@@ -219,6 +226,7 @@ struct Context {
     bool dense_active = false;
     uint64_t dense_n = 0;
     DevBuf dtri, dloc, dbits;
+    DevBuf kx_cid, kx_csl, kx_ws, kx_wp, kx_wsl;  // find_knn candidate / worklist scratch
     // Lazy K2 at the dense root: the screen's survivors (the pairs K2 must refine) sit in
     // the triangle as NaN-boxed indices into this worklist and are refined only when a
     // dense level first probes them (dense_resolve_*, exhaustive_tc.cu).

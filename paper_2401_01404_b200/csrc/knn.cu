@@ -1514,8 +1514,10 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
 
     // ---- sweeps
     const uint64_t capn = std::min<uint64_t>((uint64_t)cap * cap, n - 1);
-    DevBuf adjb, alenb, adjpb, alenpb, newfb, cidb, cslb, ccntb, churnb, churnb2, wsb, wpb, wslb, ubitsb, ubitsb2, nbitsb,
-        hasnewb;
+    DevBuf adjb, alenb, adjpb, alenpb, newfb, ccntb, churnb, churnb2, ubitsb, ubitsb2, nbitsb, hasnewb;
+    // the n x cap^2 candidate and worklist arrays (GBs at deep config-5 levels) persist in
+    // the context: re-mapping them per level and generation cost ~6 ms per GB
+    DevBuf &cidb = c.kx_cid, &cslb = c.kx_csl, &wsb = c.kx_ws, &wpb = c.kx_wp, &wslb = c.kx_wsl;
     int32_t* adj = adjb.as<int32_t>(n * cap);
     int32_t* alen = alenb.as<int32_t>(n);
     int32_t* adjp = adjpb.as<int32_t>(n * cap);  // U of the previous sweep

@@ -6,10 +6,14 @@ import numpy as np
 import torch
 from torch.profiler import profile, ProfilerActivity
 import paper_2401_01404_b200 as P
-N, M = 100000, 1000
+CFG5 = os.environ.get("TIMELINE_CFG") == "5"  # config 5 (N = 1e6, M = 200, power law) instead
+N, M = (1000000, 200) if CFG5 else (100000, 1000)
 lam = float(2 * np.sqrt(M * np.log(N)))
 m = P.Model(N, M, P.NRG_ISING, lam)
-m.generate_ising(mean_deg=5.0, seed=1)
+if CFG5:
+    m.generate_ising_powerlaw(gamma=2.5, dmin=2, w_sigma=0.2, th_sigma=0.1, burn_in=1000, thin=10, seed=5)
+else:
+    m.generate_ising(mean_deg=5.0, seed=1)
 m.reset_state()
 for it in range(3):
     m.gcd_iteration(it, kappa=2.0, seed=1)
@@ -41,6 +45,9 @@ for g, a, b in gaps:
     hist[key][1] += max(g, 0)
 for key, (n_, t) in sorted(hist.items(), key=lambda x: -x[1][1])[:25]:
     print(f"{t/1e3:8.2f} ms {n_:5d}x  {key[0]:40s} -> {key[1]}")
+print("largest single gaps:")
+for g, a, b in gaps[:10]:
+    print(f"    {g/1e3:8.2f} ms  {a:50s} -> {b}")
 rc = {}
 for e in rt:
     rc.setdefault(e["name"], [0, 0.0])
