@@ -438,13 +438,40 @@ __global__ void __launch_bounds__(256) snapshot_ising_kernel(const double* __res
     __shared__ int si[8], si4[8];
     __shared__ float s_d, s_d4;
     double mx = 0.0, q = 0.0;
-    for (int m = threadIdx.x; m < Mp; m += blockDim.x) {
-        double t = 0.0;
-        if (m < M) t = tanh(H[(size_t)r * Mp + m] + th);
-        T64[(size_t)r * Mp + m] = t;
-        T32[(size_t)r * Mp + m] = (float)t;
-        mx = fmax(mx, fabs(t));
-        q += t * t;
+    // rows of up to 2048 samples stay in registers between the two phases (thread
+    // threadIdx.x owns samples threadIdx.x + 256 k in both), their H loads issued together
+    constexpr int KMAX = 8;
+    const bool in_regs = Mp <= 256 * KMAX && blockDim.x == 256;
+    double tv[KMAX];
+    if (in_regs) {
+        double hv[KMAX];
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+            const int m = threadIdx.x + 256 * k;
+            hv[k] = m < M ? H[(size_t)r * Mp + m] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+            const int m = threadIdx.x + 256 * k;
+            tv[k] = 0.0;
+            if (m < Mp) {
+                const double t = m < M ? tanh(hv[k] + th) : 0.0;
+                tv[k] = t;
+                T64[(size_t)r * Mp + m] = t;
+                T32[(size_t)r * Mp + m] = (float)t;
+                mx = fmax(mx, fabs(t));
+                q += t * t;
+            }
+        }
+    } else {
+        for (int m = threadIdx.x; m < Mp; m += blockDim.x) {
+            double t = 0.0;
+            if (m < M) t = tanh(H[(size_t)r * Mp + m] + th);
+            T64[(size_t)r * Mp + m] = t;
+            T32[(size_t)r * Mp + m] = (float)t;
+            mx = fmax(mx, fabs(t));
+            q += t * t;
+        }
     }
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     q = warp_sum(q);
@@ -468,10 +495,9 @@ __global__ void __launch_bounds__(256) snapshot_ising_kernel(const double* __res
     const int Mw = Mp >> 5;
     double e = 0.0, e4 = 0.0;
     int sum = 0, sum4 = 0, npl = 0;  // npl: samples with x = +1 (the 4-bit screen's offset term)
-    for (int w = wid; w < Mw; w += 8) {
+    auto quant = [&](int w, double t) {
         if (lane == 0 && Xb) npl += __popc(Xb[(size_t)r * Mw + w]);
         const int m = 32 * w + lane;
-        const double t = T64[(size_t)r * Mp + m];  // 0 on padding
         int v = (int)rint(t / d);
         v = max(-127, min(127, v));
         e += fabs(t - d * (double)v);
@@ -498,6 +524,15 @@ __global__ void __launch_bounds__(256) snapshot_ising_kernel(const double* __res
             }
             if (lane < 4) P4[((size_t)r * Mw + w) * 4 + lane] = mine4;
         }
+    };
+    if (in_regs) {
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+            const int w = wid + 8 * k;  // sample 32 w + lane = threadIdx.x + 256 k
+            if (w < Mw) quant(w, tv[k]);
+        }
+    } else {
+        for (int w = wid; w < Mw; w += 8) quant(w, T64[(size_t)r * Mp + 32 * w + lane]);  // 0 on padding
     }
     e = warp_sum(e);
     e4 = warp_sum(e4);
