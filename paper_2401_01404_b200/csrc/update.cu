@@ -157,9 +157,23 @@ __global__ void __launch_bounds__(NT, 768 / NT) update_kernel(UpdateArgs A) {
             EdgeOptD r;
             if (A.stage) {
                 const double tha = __ldcg(&A.theta[a]), thb = __ldcg(&A.theta[b]);
-                for (int m = tid; m < A.M; m += NT) {
-                    ta[m] = tanh(__ldcg(&A.H[(size_t)a * A.Mp + m]) + tha);
-                    tb[m] = tanh(__ldcg(&A.H[(size_t)b * A.Mp + m]) + thb);
+                // four samples per row per thread in flight before their tanh
+                for (int m0 = tid; m0 < A.M; m0 += 4 * NT) {
+                    double ha[4], hb[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int m = m0 + u * NT;
+                        ha[u] = m < A.M ? __ldcg(&A.H[(size_t)a * A.Mp + m]) : 0.0;
+                        hb[u] = m < A.M ? __ldcg(&A.H[(size_t)b * A.Mp + m]) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int m = m0 + u * NT;
+                        if (m < A.M) {
+                            ta[m] = tanh(ha[u] + tha);
+                            tb[m] = tanh(hb[u] + thb);
+                        }
+                    }
                 }
                 __syncthreads();
                 r = ising_optimize_edge64<TStaged, BlockScope<NT>>(TStaged{ta, tb, a}, A.Xb, A.Mw, A.M, a, b, wcur,
