@@ -750,10 +750,18 @@ __global__ void __launch_bounds__(256) theta_kernel(int kind, const uint32_t* __
         sx = warp_sum(sx);
         auto deriv = [&](double th, double& d2) {
             double g = 0.0, gg = 0.0;
-            for (int m = lane; m < M; m += 32) {
-                const double t = tanh(h[m] + th);
-                g += t;
-                gg += 1.0 - t * t;
+            for (int m0 = lane; m0 < M; m0 += 128) {  // four loads in flight, same sum order
+                double hv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) hv[u] = m0 + 32 * u < M ? h[m0 + 32 * u] : 0.0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (m0 + 32 * u < M) {
+                        const double t = tanh(hv[u] + th);
+                        g += t;
+                        gg += 1.0 - t * t;
+                    }
+                }
             }
             g = warp_sum(g);
             gg = warp_sum(gg);
