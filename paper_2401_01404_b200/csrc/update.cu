@@ -207,11 +207,24 @@ __global__ void __launch_bounds__(NT, 768 / NT) update_kernel(UpdateArgs A) {
             double* Ha = A.H + (size_t)a * A.Mp;
             double* Hb = A.H + (size_t)b * A.Mp;
             if (A.kind == ISING) {
-                for (int m = tid; m < A.M; m += NT) {
-                    const uint32_t wa = A.Xb[(size_t)a * A.Mw + (m >> 5)], wb = A.Xb[(size_t)b * A.Mw + (m >> 5)];
-                    const double xa = xsign(wa, m & 31), xb = xsign(wb, m & 31);
-                    __stcg(&Ha[m], __ldcg(&Ha[m]) + delta * xb);
-                    __stcg(&Hb[m], __ldcg(&Hb[m]) + delta * xa);
+                for (int m0 = tid; m0 < A.M; m0 += 4 * NT) {  // four samples per row in flight
+                    double va[4], vb[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int m = m0 + u * NT;
+                        va[u] = m < A.M ? __ldcg(&Ha[m]) : 0.0;
+                        vb[u] = m < A.M ? __ldcg(&Hb[m]) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int m = m0 + u * NT;
+                        if (m < A.M) {
+                            const uint32_t wa = A.Xb[(size_t)a * A.Mw + (m >> 5)], wb = A.Xb[(size_t)b * A.Mw + (m >> 5)];
+                            const double xa = xsign(wa, m & 31), xb = xsign(wb, m & 31);
+                            __stcg(&Ha[m], va[u] + delta * xb);
+                            __stcg(&Hb[m], vb[u] + delta * xa);
+                        }
+                    }
                 }
             } else {
                 for (int m = tid; m < A.M; m += NT) {
