@@ -79,6 +79,17 @@ void need_samples(nrg_ctx* x) {
     if (!x->c.have_samples) nrg::fail(22, "no samples uploaded");
 }
 
+__global__ void iota_kernel(int32_t* __restrict__ v, uint64_t n) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) v[t] = (int32_t)t;
+}
+
+__global__ void pack_pairs_kernel(const int32_t* __restrict__ i, const int32_t* __restrict__ j,
+                                  const double* __restrict__ d, uint64_t k, nrg_pair* __restrict__ out) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < k) out[t] = {i[t], j[t], d[t]};
+}
+
 void gcd_iteration(nrg_ctx* x, const nrg_gcd_cfg* cfg, int iter, nrg_iter_record* rec, nrg_pair* cands, uint64_t cap,
                    uint64_t* n_cands) {
     nrg::Context& c = x->c;
@@ -89,21 +100,27 @@ void gcd_iteration(nrg_ctx* x, const nrg_gcd_cfg* cfg, int iter, nrg_iter_record
     const uint64_t m = (uint64_t)std::max(1.0, mm);
     const auto t0 = std::chrono::steady_clock::now();
     nrg::begin_generation(c);
-    std::vector<int32_t> all(n);
-    for (int t = 0; t < n; ++t) all[t] = t;
-    int32_t* dall = to_dev(x, x->q_i, all.data(), (uint64_t)n);
+    int32_t* dall = x->q_i.as<int32_t>((uint64_t)n);  // every node, 0..n-1
+    iota_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(dall, (uint64_t)n);
+    NRG_LAUNCH_CHECK();
     nrg::BestPairsD best;
     nrg::find_best(c, cfg->mode, m, dall, (uint64_t)n, cfg->knn_eps, nrg::mix64(cfg->seed, (uint64_t)iter),
                    cfg->reverse != 0, false, best, x->out_i, x->out_j, x->out_d);
     if (cands && cap) {
+        // packed on the device into the caller's record layout, one copy through pinned memory
         const uint64_t k = std::min(cap, best.count);
-        std::vector<int32_t> hi(k), hj(k);
-        std::vector<double> hd(k);
-        to_host(x, hi.data(), static_cast<int32_t*>(x->out_i.p), k);
-        to_host(x, hj.data(), static_cast<int32_t*>(x->out_j.p), k);
-        to_host(x, hd.data(), static_cast<double*>(x->out_d.p), k);
-        c.sync();
-        for (uint64_t t = 0; t < k; ++t) cands[t] = {hi[t], hj[t], hd[t]};
+        if (k) {
+            nrg::DevBuf packed;
+            nrg_pair* dp = packed.as<nrg_pair>(k);
+            pack_pairs_kernel<<<(unsigned)((k + 255) / 256), 256, 0, c.stream>>>(
+                static_cast<int32_t*>(x->out_i.p), static_cast<int32_t*>(x->out_j.p),
+                static_cast<double*>(x->out_d.p), k, dp);
+            NRG_LAUNCH_CHECK();
+            nrg_pair* hp = c.hp_pairs.as<nrg_pair>(k);
+            NRG_CUDA(cudaMemcpyAsync(hp, dp, k * sizeof(nrg_pair), cudaMemcpyDeviceToHost, c.stream));
+            c.sync();
+            std::memcpy(cands, hp, k * sizeof(nrg_pair));
+        }
     }
     if (n_cands) *n_cands = best.count;
     const double delta = nrg::apply_updates(c, static_cast<int32_t*>(x->out_i.p), static_cast<int32_t*>(x->out_j.p),

@@ -328,7 +328,7 @@ struct Context {
             return static_cast<T*>(p);
         }
     };
-    PinBuf hp_dep, hp_ord, hp_i, hp_j, hp_ch;
+    PinBuf hp_dep, hp_ord, hp_i, hp_j, hp_ch, hp_pairs;
 
     // side stream for work whose result is needed only later (the dense root's miss
     // recount): fork() orders it after everything queued so far; join_side() makes the
