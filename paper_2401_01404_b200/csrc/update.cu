@@ -408,7 +408,7 @@ static int update_grid(Context& c, size_t smem) {
 // The dependency-ordered kernel over candidates [0, n) of (ci, cj): |w - w_cur| per
 // pair into absdelta.
 static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n, const double* assign,
-                        double* absdelta) {
+                        double* absdelta, bool level_order = true) {
     if (n == 0) return;
     DevBuf kb, vb, k2b, v2b, depb, doneb, tb, tmpb;
     uint64_t* keys = kb.as<uint64_t>(2 * n);
@@ -435,7 +435,7 @@ static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64
     DevBuf ordb;
     uint32_t* order = nullptr;
     size_t nlevels = 0;
-    if (n >= 4096 && !NRG_ENV_ON("NRG_LIST_ORDER_TICKETS")) {
+    if (n >= 4096 && level_order && !NRG_ENV_ON("NRG_LIST_ORDER_TICKETS")) {
         int32_t* hdep = c.hp_dep.as<int32_t>(2 * n);
         NRG_CUDA(cudaMemcpyAsync(hdep, dep, 8 * n, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
@@ -491,7 +491,8 @@ static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64
     // levels) are bound by how many updates are in flight: 128-thread CTAs (twice as
     // many); deep chains (first sweeps, reconstruct_cd) by per-update latency: 256
     static const int nt_env = getenv("NRG_UPD_NT") ? atoi(getenv("NRG_UPD_NT")) : 0;
-    const int nt = nt_env ? nt_env : (nlevels > 0 && n >= 256 * nlevels ? 128 : 256);
+    const int nt = nt_env ? nt_env
+                          : ((nlevels > 0 && n >= 256 * nlevels) || (!level_order && n >= 4096) ? 128 : 256);
     int grid = (int)std::min<uint64_t>(nt == 128 ? update_grid<128>(c, smem_use) : update_grid<256>(c, smem_use), n);
     const bool dbg = NRG_ENV_ON("NRG_DEBUG_UPDATES");
     if (dbg && NRG_ENV_ON("NRG_DEBUG_SERIAL")) grid = 1;
@@ -596,7 +597,12 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
         c.sync();
         if (n - hk >= kTailMin) k = hk;
     }
-    ordered_run(c, ci, cj, k, assign, absdelta);
+    // a FindBest list (sorted by distance) is already a spread-out order: consecutive
+    // candidates rarely share a node, so list-order tickets keep the wavefront busy and the
+    // host-side level ordering (a round trip) costs more than it gains; other lists
+    // (reconstruct_cd's row-major all-pairs, user lists) take level order
+    static const bool fb_level = NRG_ENV_ON("NRG_FB_LEVEL_ORDER");
+    ordered_run(c, ci, cj, k, assign, absdelta, !dist || fb_level);
     uint64_t start = k;
     if (start < n) {
         const uint64_t nt = n - start;
