@@ -124,7 +124,8 @@ void gcd_iteration(nrg_ctx* x, const nrg_gcd_cfg* cfg, int iter, nrg_iter_record
     }
     if (n_cands) *n_cands = best.count;
     const double delta = nrg::apply_updates(c, static_cast<int32_t*>(x->out_i.p), static_cast<int32_t*>(x->out_j.p),
-                                            best.count, nullptr, static_cast<double*>(x->out_d.p));
+                                            best.count, nullptr, static_cast<double*>(x->out_d.p),
+                                            /*fb_sorted=*/true);
     nrg::theta_pass(c, nullptr);
     const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     const double obj = nrg::log_posterior(c);
@@ -618,6 +619,12 @@ int nrg_load_state_file(nrg_ctx* x, const char* path) {
         std::vector<int32_t> ei(ne), ej(ne);
         nrg::read_state_file(path, th.data(), ei.data(), ej.data(), w.data());
         check_pairs(x, ne, ei.data(), ej.data());
+        // everything validated before the current state is touched
+        for (uint64_t i = 0; i < n; ++i)
+            if (!std::isfinite(th[i]) || (x->c.kind == nrg::GAUSSIAN && !(th[i] > 0.0)))
+                nrg::fail(22, x->c.kind == nrg::GAUSSIAN ? "gaussian model requires theta > 0" : "non-finite theta");
+        for (uint64_t e = 0; e < ne; ++e)
+            if (!std::isfinite(w[e])) nrg::fail(22, "non-finite coupling in state file");
         nrg::reset_state_empty(x->c);
         nrg::set_theta(x->c, th.data());
         if (ne) {

@@ -65,6 +65,18 @@ void nccheck(ncclResult_t r, const char* what) {
 struct NcclComm final : Comm {
     ncclComm_t comm = nullptr;
     uint64_t* dscratch = nullptr;
+    size_t dscratch_n = 0;
+    // device staging for the host-scalar collectives, grown on demand (the routing
+    // matrix of exchange_and_score is world^2 counts)
+    uint64_t* scratch(size_t n) {
+        if (n > dscratch_n) {
+            if (dscratch) NRG_CUDA(cudaFree(dscratch));
+            dscratch = nullptr;
+            dscratch_n = std::max<size_t>(n, 64);
+            NRG_CUDA(cudaMalloc(&dscratch, dscratch_n * 8));
+        }
+        return dscratch;
+    }
     ~NcclComm() override {
         if (comm) nccl().commDestroy(comm);
         if (dscratch) cudaFree(dscratch);
@@ -102,15 +114,17 @@ struct NcclComm final : Comm {
         NRG_CUDA(cudaStreamSynchronize(s));
     }
     void allreduce_u64(uint64_t* v, int n, bool mx, cudaStream_t s) override {
-        NRG_CUDA(cudaMemcpyAsync(dscratch, v, n * 8, cudaMemcpyHostToDevice, s));
-        nccheck(nccl().allReduce(dscratch, dscratch, n, ncclUint64, mx ? ncclMax : ncclSum, comm, s), "allreduce");
-        NRG_CUDA(cudaMemcpyAsync(v, dscratch, n * 8, cudaMemcpyDeviceToHost, s));
+        uint64_t* d = scratch((size_t)n);
+        NRG_CUDA(cudaMemcpyAsync(d, v, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+        nccheck(nccl().allReduce(d, d, n, ncclUint64, mx ? ncclMax : ncclSum, comm, s), "allreduce");
+        NRG_CUDA(cudaMemcpyAsync(v, d, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
         NRG_CUDA(cudaStreamSynchronize(s));
     }
     void bcast_f64(double* v, int n, cudaStream_t s) override {
-        NRG_CUDA(cudaMemcpyAsync(dscratch, v, n * 8, cudaMemcpyHostToDevice, s));
-        nccheck(nccl().broadcast(dscratch, dscratch, n, ncclFloat64, 0, comm, s), "broadcast");
-        NRG_CUDA(cudaMemcpyAsync(v, dscratch, n * 8, cudaMemcpyDeviceToHost, s));
+        uint64_t* d = scratch((size_t)n);
+        NRG_CUDA(cudaMemcpyAsync(d, v, (size_t)n * 8, cudaMemcpyHostToDevice, s));
+        nccheck(nccl().broadcast(d, d, n, ncclFloat64, 0, comm, s), "broadcast");
+        NRG_CUDA(cudaMemcpyAsync(v, d, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
         NRG_CUDA(cudaStreamSynchronize(s));
     }
 };
@@ -133,7 +147,7 @@ Comm* make_nccl_comm(const uint8_t id[128], int rank, int world, int device) {
     std::memcpy(&u, id, 128);
     try {
         nccheck(nccl().commInitRank(&c->comm, world, u, rank), "comm init");
-        NRG_CUDA(cudaMalloc(&c->dscratch, 64 * 8));
+        c->scratch((size_t)world * world);
     } catch (...) {
         delete c;
         throw;

@@ -504,9 +504,11 @@ uint64_t sample_scored_pairs(Context& c, uint64_t cap, uint64_t seed, int32_t* o
 
 // ---- update.cu
 // candidates (device arrays, canonical i<j) in order; assign==nullptr -> optimize_edge;
-// dist (optional, device): the candidates' distances, used only to find a tie tail
+// dist (optional, device): the candidates' distances, used only to find a tie tail;
+// fb_sorted: the list is a FindBest result (sorted by distance), which takes list-order
+// tickets; any other list takes dependency-level order.  Results never depend on either.
 double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n,
-                     const double* assign, const double* dist = nullptr);
+                     const double* assign, const double* dist = nullptr, bool fb_sorted = false);
 void theta_pass(Context& c, double* out_only);
 // set_edges into an empty coupling table with distinct pairs (false: not applicable)
 bool set_edges_bulk(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n, const double* w);

@@ -9,6 +9,9 @@
 //
 // Host-side readers/writers work without a GPU; nrg_load_*/nrg_save_* move a file
 // straight into / out of a context.
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <cstdio>
 #include <cstring>
 #include <memory>
@@ -49,6 +52,48 @@ struct File {
     }
 };
 
+// Writer with the reference's atomic_write semantics (inc/io.hpp): the bytes go to
+// path + ".tmp", are flushed and fsync'ed, and only a complete file is renamed onto the
+// target, so a failed write (disk full, short write) never destroys the previous file.
+struct AtomicFile {
+    std::string path, tmp;
+    FILE* f = nullptr;
+    explicit AtomicFile(const char* p) : path(p ? p : "") {
+        if (!p) fail(22, "null path");
+        tmp = path + ".tmp";
+        f = std::fopen(tmp.c_str(), "wb");
+        if (!f) fail(5, "cannot open " + tmp);
+    }
+    ~AtomicFile() {  // not committed: drop the partial temporary
+        if (f) {
+            std::fclose(f);
+            std::remove(tmp.c_str());
+        }
+    }
+    void put(const void* d, size_t n) {
+        if (n && std::fwrite(d, 1, n, f) != n) fail(5, "write failed: " + tmp);
+    }
+    void commit() {
+        const bool ok = std::fflush(f) == 0 && fsync(fileno(f)) == 0;
+        const bool closed = std::fclose(f) == 0;
+        f = nullptr;
+        if (!ok || !closed) {
+            std::remove(tmp.c_str());
+            fail(5, "write failed: " + tmp);
+        }
+        if (std::rename(tmp.c_str(), path.c_str()) != 0) {
+            std::remove(tmp.c_str());
+            fail(5, "cannot rename " + tmp + " to " + path);
+        }
+    }
+};
+
+uint64_t file_size(File& f) {
+    struct stat st;
+    if (fstat(fileno(f.f), &st) != 0) fail(5, "cannot stat " + f.path);
+    return (uint64_t)st.st_size;
+}
+
 struct SampleHeader {
     uint32_t kind;
     uint64_t n, m;
@@ -65,6 +110,8 @@ SampleHeader read_sample_header(File& f) {
     f.get(&n, 8);
     f.get(&m, 8);
     if (kind > 1 || n == 0 || n > (1ull << 31) || m > (1ull << 31)) fail(22, "bad sample file header: " + f.path);
+    const uint64_t body = kind == 0 ? n * ((m + 7) / 8) : n * m * 8;
+    if (file_size(f) != 32 + body) fail(22, "sample file size does not match its header: " + f.path);
     return {kind, n, m};
 }
 
@@ -73,7 +120,10 @@ SampleHeader read_sample_header(File& f) {
 void write_samples_file(const char* path, uint64_t n, uint64_t m, int kind, const double* X) {
     if (kind != 0 && kind != 1) fail(22, "kind must be 0 (ising) or 1 (gaussian)");
     if (n == 0) fail(22, "no nodes");
-    File f(path, "wb");
+    if (kind == 0)  // validate before the target is touched
+        for (uint64_t e = 0; e < n * m; ++e)
+            if (X[e] != 1.0 && X[e] != -1.0) fail(22, "ising model requires +/-1 data");
+    AtomicFile f(path);
     f.put(kSampleMagic, 8);
     const uint32_t k = (uint32_t)kind, pad = 0;
     f.put(&k, 4);
@@ -86,16 +136,14 @@ void write_samples_file(const char* path, uint64_t n, uint64_t m, int kind, cons
         for (uint64_t i = 0; i < n; ++i) {
             std::fill(row.begin(), row.end(), 0);
             for (uint64_t t = 0; t < m; ++t) {
-                const double v = X[i * m + t];
-                if (v != 1.0 && v != -1.0) fail(22, "ising model requires +/-1 data");
-                if (v > 0.0) row[t >> 3] |= (uint8_t)(1u << (t & 7));
+                if (X[i * m + t] > 0.0) row[t >> 3] |= (uint8_t)(1u << (t & 7));
             }
             f.put(row.data(), rb);
         }
     } else {
         f.put(X, n * m * 8);
     }
-    f.close();
+    f.commit();
 }
 
 void read_samples_info(const char* path, uint64_t* n, uint64_t* m, int* kind) {
@@ -164,7 +212,7 @@ void save_samples_file(Context& c, const char* path) {
 
 void write_state_file(const char* path, uint64_t n, const double* theta, uint64_t ne, const int32_t* ei,
                       const int32_t* ej, const double* w) {
-    File f(path, "wb");
+    AtomicFile f(path);
     f.put(kStateMagic, 8);
     f.put(&n, 8);
     f.put(&ne, 8);
@@ -174,7 +222,7 @@ void write_state_file(const char* path, uint64_t n, const double* theta, uint64_
         f.put(&ej[e], 4);
         f.put(&w[e], 8);
     }
-    f.close();
+    f.commit();
 }
 
 static void read_state_header(File& f, uint64_t* n, uint64_t* ne) {
@@ -183,7 +231,9 @@ static void read_state_header(File& f, uint64_t* n, uint64_t* ne) {
     if (std::memcmp(magic, kStateMagic, 8) != 0) fail(22, "not a netrec state file: " + f.path);
     f.get(n, 8);
     f.get(ne, 8);
-    if (*n == 0 || *n > (1ull << 31)) fail(22, "bad state file header: " + f.path);
+    if (*n == 0 || *n > (1ull << 31) || *ne > (1ull << 40)) fail(22, "bad state file header: " + f.path);
+    // checked before anything is allocated for the body (a corrupt count cannot ask for GBs)
+    if (file_size(f) != 24 + 8 * *n + 16 * *ne) fail(22, "state file size does not match its header: " + f.path);
 }
 
 void read_state_info(const char* path, uint64_t* n, uint64_t* ne) {

@@ -574,8 +574,15 @@ constexpr int kTailRounds = 64;     // rounds before the rest of a tail is order
 // and starts the next.  The prefix before the tail, and a tail with more changes
 // than rounds left, go through the dependency-ordered kernel.  `dist` (device,
 // optional) only locates the tail; results never depend on it.
+// Precision note: a round decides "changes / does not change" with score_entries
+// (warp-scope reductions), while the applied pairs are re-optimised by update_kernel
+// (block-scope reductions).  Kink decisions (w_cur = 0 staying 0) are exact on both
+// paths (integer screen + error band), but for an existing coupling the two
+// reductions may disagree in the last ulp of w*, so the tail matches the sequential
+// loop to rounding (|dw| ~ 1e-15), not bitwise; tests/test_gpu_updates.py checks it
+// against the ordered path at 1e-9.
 double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n, const double* assign,
-                     const double* dist) {
+                     const double* dist, bool fb_sorted) {
     if (n == 0) return 0.0;
     if (n >= (1ull << 31)) fail(22, "apply_updates: too many candidates");
     // the snapshot describes the state on entry (FindBest just ran): a tie tail then
@@ -597,12 +604,13 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
         c.sync();
         if (n - hk >= kTailMin) k = hk;
     }
-    // a FindBest list (sorted by distance) is already a spread-out order: consecutive
-    // candidates rarely share a node, so list-order tickets keep the wavefront busy and the
-    // host-side level ordering (a round trip) costs more than it gains; other lists
-    // (reconstruct_cd's row-major all-pairs, user lists) take level order
+    // a FindBest list (sorted by distance, flagged by gcd_iteration) is already a
+    // spread-out order: consecutive candidates rarely share a node, so list-order tickets
+    // keep the wavefront busy and the host-side level ordering (a round trip) costs more
+    // than it gains; every other list (reconstruct_cd's row-major all-pairs, lists passed
+    // to nrg_apply_updates / edited by a candidate hook, set_edges) takes level order
     static const bool fb_level = NRG_ENV_ON("NRG_FB_LEVEL_ORDER");
-    ordered_run(c, ci, cj, k, assign, absdelta, !dist || fb_level);
+    ordered_run(c, ci, cj, k, assign, absdelta, !fb_sorted || fb_level);
     uint64_t start = k;
     if (start < n) {
         const uint64_t nt = n - start;

@@ -65,3 +65,39 @@ def test_context_load_save(gpu, tmp_path):
         np.testing.assert_array_equal(s_a, s_b)
         np.testing.assert_array_equal(s_a, s_c)
     assert abs(a.log_posterior() - c.log_posterior()) <= 1e-9 * abs(a.log_posterior())
+
+
+def test_failed_write_keeps_previous_file(tmp_path):
+    """Writes are atomic (the reference's atomic_write, inc/io.hpp): an invalid input is
+    rejected before the target is touched, and no temporary is left behind."""
+    rng = np.random.default_rng(1)
+    Xi = np.where(rng.random((5, 9)) < 0.5, -1.0, 1.0)
+    L.write_samples_file(tmp_path / "a.bin", Xi, kind=0)
+    before = (tmp_path / "a.bin").read_bytes()
+    bad = Xi.copy()
+    bad[4, 8] = 0.5  # the last value is invalid: nothing may be written
+    with pytest.raises(ValueError):
+        L.write_samples_file(tmp_path / "a.bin", bad, kind=0)
+    assert (tmp_path / "a.bin").read_bytes() == before
+    assert not (tmp_path / "a.bin.tmp").exists()
+    with pytest.raises(RuntimeError):  # unwritable directory: the error surfaces, nothing created
+        L.write_state_file(tmp_path / "no" / "dir" / "s.bin", np.zeros(3), [], [], [])
+
+
+def test_corrupt_headers_rejected_before_allocation(tmp_path):
+    """A state / sample header whose counts disagree with the file length is rejected
+    (no multi-GB allocation from a corrupt n_edges)."""
+    th = np.zeros(4)
+    L.write_state_file(tmp_path / "s.bin", th, np.array([0], np.int32), np.array([1], np.int32), np.array([0.5]))
+    raw = bytearray((tmp_path / "s.bin").read_bytes())
+    raw[16:24] = (1 << 36).to_bytes(8, "little")  # n_edges
+    (tmp_path / "bad.bin").write_bytes(bytes(raw))
+    with pytest.raises(ValueError):
+        L.read_state_file(tmp_path / "bad.bin")
+    (tmp_path / "short.bin").write_bytes((tmp_path / "s.bin").read_bytes()[:-3])
+    with pytest.raises(ValueError):
+        L.read_state_file(tmp_path / "short.bin")
+    L.write_samples_file(tmp_path / "x.bin", np.ones((3, 10)), kind=0)
+    (tmp_path / "x2.bin").write_bytes((tmp_path / "x.bin").read_bytes() + b"\0")
+    with pytest.raises(ValueError):
+        L.read_samples_file(tmp_path / "x2.bin")
