@@ -15,9 +15,19 @@ with host buffers: every step uploads the N x M samples (bit-packed rows, the Is
 and the state the timed sweeps started from, runs that sweep, and downloads the
 kappa*N candidate pairs and the new state.
 
+After the timed sweeps, rank 0 (N=1) times the reference's distance() on a sample of
+the pairs the last GPU sweep scored, at the same state (`cpu_baseline`), and diffs the
+device's distance / optimize_edge against the reference's on those pairs (`parity`;
+the run exits 3 if a north_star tolerance is broken).
+
 --impl reference: the reference's own CPU path (oracle/_ref = the netrec headers
 compiled unmodified) timing distance() (exact mode, parallel_for over all host threads)
-on a bounded sample of pairs, same metric and unit.
+on the device arm's data (the device Gibbs chain restated in C: identical samples) at
+the device arm's timed-sweep state, on a sample of the pairs a timed GPU sweep scored
+(bench_data/, written by --write-sample); same metric and unit.
+
+--gpus N: under torchrun (WORLD_SIZE set) one rank per GPU; without a launcher the
+script starts the N ranks itself.
 """
 from __future__ import annotations
 
@@ -129,6 +139,8 @@ def dist_setup():
         import torch.distributed as dist
         backend = "nccl" if torch.cuda.is_available() else "gloo"
         if backend == "nccl":
+            if local >= torch.cuda.device_count():
+                raise SystemExit(f"bench.py: rank {rank} needs GPU {local}, only {torch.cuda.device_count()} visible")
             torch.cuda.set_device(local)
         dist.init_process_group(backend)
     return rank, world, local, dist
@@ -164,56 +176,92 @@ def measured_peaks():
 
 
 # --------------------------------------------------------------------------- reference (CPU)
-def reference_pairs_per_sec(X_f64, lam, pairs_i, pairs_j, target_s, threads, state=None):
-    """The reference's distance() (exact mode) under its parallel_for over a pair sample,
-    via oracle/_ref (the netrec headers compiled unmodified).  Returns (pairs/s, n, kind)."""
-    sys.path.insert(0, str(ROOT / "tests"))
-    import oracle_lib as O
-    which = "ref" if O.available("ref") else "orc"
-    L = O.lib(which)
-    m = O.CpuModel(which, X_f64, 0, lam)
-    if state is not None:
-        th, ei, ej, w = state
-        m.set_theta(th)
-        m.set_edges(ei, ej, w)
-    if which == "ref":
-        f = getattr(L, "ref_distance_parallel")
-        f.restype = C.c_int
-        f.argtypes = [C.c_void_p, C.c_int, C.c_uint64, np.ctypeslib.ndpointer(np.int32, flags="C"),
-                      np.ctypeslib.ndpointer(np.int32, flags="C"), np.ctypeslib.ndpointer(np.float64, flags="C"),
-                      C.c_int]
+SAMPLE_DIR = ROOT / "bench_data"
 
-        def run(i, j):
-            out = np.zeros(len(i))
-            rc = f(m.h, 0, len(i), np.ascontiguousarray(i, np.int32), np.ascontiguousarray(j, np.int32), out,
-                   threads)
-            assert rc == 0
-            return out
-    else:
-        threads = 1
 
-        def run(i, j):
-            return m.distance(0, i, j)
-    # one generation: the first call computes the per-generation base (log_posterior,
-    # amortised over ~1e8 pairs in a real sweep); calibration and the timed run then
-    # use disjoint slices so no pair is a cache hit
-    m.begin_generation()
-    run(pairs_i[:1], pairs_j[:1])
-    n0 = min(len(pairs_i) // 4, max(2000, 500 * threads))
-    t = time.perf_counter()
-    run(pairs_i[1:1 + n0], pairs_j[1:1 + n0])
-    dt = time.perf_counter() - t
-    rate = n0 / max(dt, 1e-6)
-    rest_i, rest_j = pairs_i[1 + n0:], pairs_j[1 + n0:]
-    n = int(min(len(rest_i), max(n0, rate * target_s)))
-    t = time.perf_counter()
-    run(rest_i[:n], rest_j[:n])
-    dt = time.perf_counter() - t
-    m.close()
-    return n / dt, n, dt, which, threads
+def samples_digest(X) -> str:
+    """sha256 of the bit-packed +-1 samples (identifies the data set across the arms)"""
+    import hashlib
+    return hashlib.sha256(np.packbits(np.asarray(X) > 0, axis=1, bitorder="little").tobytes()).hexdigest()[:32]
+
+
+class RefScorer:
+    """The reference's own CPU path via oracle/_ref (the netrec headers compiled
+    unmodified): PseudoLikelihood + DistanceCache at a given state; distance() and
+    optimize_edge() under the reference's parallel_for over all host threads."""
+
+    def __init__(self, X_f64, lam, state=None, threads=None):
+        sys.path.insert(0, str(ROOT / "tests"))
+        import oracle_lib as O
+        self.which = "ref" if O.available("ref") else "orc"
+        self.L = O.lib(self.which)
+        self.threads = (threads or os.cpu_count() or 1) if self.which == "ref" else 1
+        self.m = O.CpuModel(self.which, X_f64, 0, lam)
+        if state is not None:
+            th, ei, ej, w = state
+            self.m.set_theta(th)
+            self.m.set_edges(ei, ej, w)
+        if self.which == "ref":
+            self._dp = self.L.ref_distance_parallel
+            self._dp.restype = C.c_int
+            self._dp.argtypes = [C.c_void_p, C.c_int, C.c_uint64, np.ctypeslib.ndpointer(np.int32, flags="C"),
+                                 np.ctypeslib.ndpointer(np.int32, flags="C"),
+                                 np.ctypeslib.ndpointer(np.float64, flags="C"), C.c_int]
+            self._op = self.L.ref_optimize_edge_parallel
+            self._op.restype = C.c_int
+            self._op.argtypes = [C.c_void_p, C.c_uint64, np.ctypeslib.ndpointer(np.int32, flags="C"),
+                                 np.ctypeslib.ndpointer(np.int32, flags="C"),
+                                 np.ctypeslib.ndpointer(np.float64, flags="C"),
+                                 np.ctypeslib.ndpointer(np.float64, flags="C"), C.c_void_p, C.c_int]
+
+    def distance(self, i, j):
+        i, j = np.ascontiguousarray(i, np.int32), np.ascontiguousarray(j, np.int32)
+        if self.which != "ref":
+            return self.m.distance(0, i, j)
+        out = np.zeros(len(i))
+        assert self._dp(self.m.h, 0, len(i), i, j, out, self.threads) == 0
+        return out
+
+    def optimize_edge(self, i, j):
+        i, j = np.ascontiguousarray(i, np.int32), np.ascontiguousarray(j, np.int32)
+        if self.which != "ref":
+            return self.m.optimize_edge(i, j)[:2]
+        w, g = np.zeros(len(i)), np.zeros(len(i))
+        assert self._op(self.m.h, len(i), i, j, w, g, None, self.threads) == 0
+        return w, g
+
+    def timed_distances(self, pi, pj, target_s):
+        """One generation (the first call computes the per-generation base, amortised over
+        ~1e8 pairs in a real sweep); a calibration slice, then about target_s seconds of
+        the rest -- disjoint slices, so no pair is a cache hit.  Returns
+        (pairs/s, n, seconds, index slice of the timed pairs, their distances)."""
+        self.m.begin_generation()
+        self.distance(pi[:1], pj[:1])
+        n0 = min(len(pi) // 4, max(2000, 500 * self.threads))
+        t = time.perf_counter()
+        self.distance(pi[1:1 + n0], pj[1:1 + n0])
+        rate = n0 / max(time.perf_counter() - t, 1e-6)
+        n = int(min(len(pi) - 1 - n0, max(n0, rate * target_s)))
+        sl = slice(1 + n0, 1 + n0 + n)
+        t = time.perf_counter()
+        d = self.distance(pi[sl], pj[sl])
+        dt = time.perf_counter() - t
+        return n / dt, n, dt, sl, d
+
+    def close(self):
+        self.m.close()
+
+
+def bench_sample_path(config, seed):
+    return SAMPLE_DIR / f"{config}_seed{seed}.npz"
 
 
 def run_reference(args, rank, world, dist):
+    """The reference arm: the reference's distance() under its parallel_for, on the
+    device arm's data (the coloured Gibbs chain restated in C, bit-identical to the
+    device sampler) at the device arm's timed-sweep state, on a sample of the pairs a
+    timed GPU sweep scored (bench_data/<config>_seed<seed>.npz, written by
+    `bench.py --write-sample`, checked against the data by digest)."""
     if rank != 0:
         return
     N, M, md = CONFIGS[args.config] if not args.n else (args.n, args.m, args.mean_deg)
@@ -221,20 +269,34 @@ def run_reference(args, rank, world, dist):
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_lib as O
     t0 = time.perf_counter()
-    X, _ = O.gen_ising(N, M, seed=args.seed, mean_deg=md, burn_in=args.burn_in, thin=10)
+    X, _ = O.gen_ising_colored(N, M, args.seed, mean_deg=md, w_sigma=0.3, th_sigma=0.1, burn_in=args.burn_in,
+                               thin=10)
     gen_s = time.perf_counter() - t0
-    rng = np.random.default_rng(args.seed)
-    pi = rng.integers(0, N, 4_000_000)
-    pj = rng.integers(0, N, 4_000_000)
-    keep = pi != pj
-    pi, pj = pi[keep].astype(np.int32), pj[keep].astype(np.int32)
-    threads = os.cpu_count() or 1
+    digest = samples_digest(X)
+    fx = bench_sample_path(args.config, args.seed)
+    state, sample_note = None, None
+    if fx.exists():
+        z = np.load(fx)
+        if str(z["digest"]) == digest:
+            state = (z["theta"], z["ei"], z["ej"], z["w"])
+            pi, pj = z["pi"].astype(np.int32), z["pj"].astype(np.int32)
+            sample_note = (f"{len(pi)} of the unique pairs GPU sweep {int(z['sweep'])} scored (uniform sample of its "
+                           f"distance cache), at that sweep's state ({len(z['ei'])} couplings)")
+    if state is None:  # no matching sample: the initial graph of NNDescent level 0 at the empty state
+        rng = np.random.default_rng(args.seed)
+        pi = rng.integers(0, N, 4_000_000)
+        pj = rng.integers(0, N, 4_000_000)
+        keep = pi != pj
+        pi, pj = pi[keep].astype(np.int32), pj[keep].astype(np.int32)
+        sample_note = "uniform random pairs at the empty state (no bench_data sample matching the data)"
+    R = RefScorer(X.astype(np.float64), lam, state)
+    del X
     vals = []
-    per_step = max(5.0, args.ref_seconds / max(1, args.steps))
+    per_step = max(4.0, args.ref_seconds / max(1, args.steps))
+    perm = np.random.default_rng(args.seed + 1)
     for s in range(args.warmup + args.steps):
-        off = (s * 997_331) % max(1, len(pi) - 1_000_000)
-        r, n, dt, which, thr = reference_pairs_per_sec(X, lam, pi[off:], pj[off:], per_step if s >= args.warmup else 2.0,
-                                                       threads)
+        o = perm.permutation(len(pi))  # a fresh generation and order per step (no memo carry-over)
+        r, n, dt, _, _ = R.timed_distances(pi[o], pj[o], per_step if s >= args.warmup else 1.0)
         if s >= args.warmup:
             vals.append((r, n, dt))
     value = float(np.median([v[0] for v in vals]))
@@ -243,15 +305,46 @@ def run_reference(args, rank, world, dist):
         "metric": "scored candidate pairs/sec and wall-time per GCD sweep (N=1e5, M=1e3)",
         "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": float(np.median([v[2] for v in vals]) * 1e3), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Gibbs, CPU checker)",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (the device arm's samples: coloured Gibbs chain restated in C, digest " + digest + ")",
         "config": {"workload": f"{args.config}: Ising N={N} M={M} mean_deg={md} lambda={lam:.1f} exact distance",
-                   "sample": "uniform random pairs on the same data (>97% pruned at the L1 kink, which favours the "
-                             "reference vs the FindBest mix)", "gen_seconds": round(gen_s, 1)},
-        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": vals and thr, "kind": "reference" if which == "ref"
-                         else "port", "sample": f"{vals[-1][1]} random pairs per step, distance() under parallel_for"},
+                   "sample": sample_note, "gen_seconds": round(gen_s, 1)},
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": R.threads,
+                         "kind": "reference" if R.which == "ref" else "port",
+                         "sample": f"{vals[-1][1]} pairs per step: {sample_note}; distance() under parallel_for"},
         "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    R.close()
     print(json.dumps(line), flush=True)
+
+
+def parity_block(model, R, si, sj, sl, d_ref, M, P):
+    """Config-4 parity at the identical state: the device's distance / optimize_edge vs
+    the reference's on the pairs the cpu_baseline leg scored (north_star tolerances:
+    dist 1e-5 relative, w* 1e-4, gain 1e-5 * max(|gain_ref|, 1e-8 M))."""
+    i, j = si[sl], sj[sl]
+    d_dev = model.distance(P.NRG_EXACT, i, j)
+    rel = np.abs(d_dev - d_ref) / np.abs(d_ref)
+    w_dev, g_dev, _ = model.optimize_edge(i, j)
+    # every pair the device does not prune, plus as many pruned ones, through the
+    # reference's optimize_edge (inc/model.hpp:201-217)
+    live = np.flatnonzero((w_dev != 0.0) | (g_dev > 0.0))
+    rng = np.random.default_rng(5)
+    live = live if len(live) <= 40000 else np.sort(rng.choice(live, 40000, replace=False))
+    dead = np.flatnonzero((w_dev == 0.0) & (g_dev == 0.0))
+    dead = dead if len(dead) <= max(20000, len(live)) else np.sort(rng.choice(dead, max(20000, len(live)),
+                                                                                 replace=False))
+    chk = np.concatenate([live, dead])
+    w_ref, g_ref = R.optimize_edge(i[chk], j[chk])
+    dw = np.abs(w_dev[chk] - w_ref)
+    gtol = 1e-5 * np.maximum(np.abs(g_ref), 1e-8 * M)
+    gbad = int((np.abs(g_dev[chk] - g_ref) > gtol).sum())
+    kink = int(((w_dev[chk] == 0.0) != (w_ref == 0.0)).sum())
+    ok = bool(rel.max() <= 1e-5 and dw.max() <= 1e-4 and gbad == 0)
+    return {"pairs_dist": int(len(i)), "max_rel_dist": float(rel.max()), "pairs_optimize_edge": int(len(chk)),
+            "unpruned_checked": int(len(live)), "max_dw": float(dw.max()), "gain_violations": gbad,
+            "kink_mismatches": kink, "max_abs_dgain": float(np.abs(g_dev[chk] - g_ref).max()),
+            "tolerances": "dist 1e-5 rel; w* 1e-4 abs; gain 1e-5*max(|g_ref|,1e-8*M)", "ok": ok}
 
 
 # --------------------------------------------------------------------------- ours
@@ -389,19 +482,49 @@ def run_ours(args, rank, world, local, dist):
         "gpu_launches": int(kst["launches"]),
         "clocks": clk.summary(),
     }
+    parity_ok = True
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         si, sj = model.sample_scored_pairs(2_000_000, seed=7)
         perm = np.random.default_rng(0).permutation(len(si))
         si, sj = si[perm], sj[perm]
-        rate, n, dt, which, thr = reference_pairs_per_sec(Xh.astype(np.float64), lam, si, sj, args.cpu_seconds,
-                                                         os.cpu_count() or 1, state=model.get_state())
-        line["cpu_baseline"] = {"value": rate, "unit": "pairs/s", "cores": thr,
-                                "kind": "reference" if which == "ref" else "port",
+        st = model.get_state()
+        R = RefScorer(Xh.astype(np.float64), lam, state=st)
+        rate, n, dt, sl, d_ref = R.timed_distances(si, sj, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": "pairs/s", "cores": R.threads,
+                                "kind": "reference" if R.which == "ref" else "port",
                                 "sample": f"{n} of the unique pairs the last timed GPU sweep scored (uniform sample "
                                           f"of the distance cache), reference distance() exact mode at the "
                                           f"reconstruction's current state, {dt:.1f} s"}
+        line["parity"] = parity_block(model, R, si, sj, sl, d_ref, M, P)
+        parity_ok = line["parity"]["ok"]
+        R.close()
+        if args.write_sample:
+            SAMPLE_DIR.mkdir(exist_ok=True)
+            k = min(len(si), args.write_sample)
+            np.savez_compressed(bench_sample_path(args.config, args.seed), digest=np.array(samples_digest(Xh)),
+                                sweep=np.array(args.warmup), theta=th_w, ei=ei_w, ej=ej_w, w=w_w,
+                                pi=si[:k].astype(np.int32), pj=sj[:k].astype(np.int32))
     if rank == 0:
         print(json.dumps(line), flush=True)
+    return parity_ok
+
+
+def self_launch(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: N ranks of this script, one per GPU
+    (RANK / LOCAL_RANK / WORLD_SIZE / MASTER_ADDR=127.0.0.1 / MASTER_PORT), the same
+    environment torchrun gives; rank 0 prints the line.  Returns the worst exit code."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, str(Path(__file__).resolve()), *sys.argv[1:]], env=env))
+    rcs = [p.wait() for p in procs]
+    return max(rcs, key=abs)
 
 
 def main():
@@ -419,16 +542,29 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-seconds", type=float, default=30.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--write-sample", type=int, default=0,
+                    help="also save S_W and this many scored pairs under bench_data/ (the reference arm's input)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: --warmup < 3 violates the timing contract", file=sys.stderr)
-    rank, world, local, dist = dist_setup()
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1:
+        sys.exit(self_launch(args.gpus))
+    if env_world is not None and int(env_world) != args.gpus:
+        print(f"bench.py: WORLD_SIZE={env_world} but --gpus {args.gpus}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
-        run_reference(args, rank, world, dist)
-    else:
-        run_ours(args, rank, world, local, dist)
+        # the reference is a CPU path: rank 0 alone runs it, the other ranks exit at once
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference(args, rank, int(env_world or 1), None)
+        sys.exit(0)
+    rank, world, local, dist = dist_setup()
+    ok = run_ours(args, rank, world, local, dist)
     if dist is not None:
         dist.destroy_process_group()
+    if not ok:
+        print("parity check failed (see the line's parity block)", file=sys.stderr)
+        sys.exit(3)
 
 
 if __name__ == "__main__":

@@ -222,6 +222,21 @@ int ref_optimize_edge(void* p, std::uint64_t n, const std::int32_t* i, const std
     });
 }
 
+// optimize_edge over a pair list under parallel_for (make_slice keeps its scratch
+// thread_local, inc/model.hpp:301) -- bench.py's config-4 parity block
+int ref_optimize_edge_parallel(void* p, std::uint64_t n, const std::int32_t* i, const std::int32_t* j,
+                               double* w, double* gain, std::uint8_t* warn, int threads) {
+    auto* h = static_cast<Handle*>(p);
+    GUARD(parallel_for(n, threads, [&](std::size_t b, std::size_t e) {
+        for (std::size_t t = b; t < e; ++t) {
+            const EdgeOpt r = h->model->optimize_edge(i[t], j[t]);
+            w[t] = r.w;
+            gain[t] = r.gain;
+            if (warn) warn[t] = r.warning ? 1 : 0;
+        }
+    }));
+}
+
 int ref_edge_gradient(void* p, std::uint64_t n, const std::int32_t* i, const std::int32_t* j,
                       double* g) {  // inc/model.hpp:175-195
     auto* h = static_cast<Handle*>(p);

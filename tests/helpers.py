@@ -75,3 +75,50 @@ def pairs_equal(a, b):
     return (len(a) == len(b) and (np.asarray(a["i"]) == np.asarray(b["i"])).all()
             and (np.asarray(a["j"]) == np.asarray(b["j"])).all()
             and (np.asarray(a["dist"]) == np.asarray(b["dist"])).all())
+
+
+def near_tie_tol(d_cut, base, M):
+    """Window around a cut distance inside which two implementations may order pairs
+    differently: the north_star gain tolerance at the cut's gain plus the rounding of
+    dist = -(base + gain) (a few ulps of base)."""
+    g_cut = -d_cut - base
+    return 1e-5 * max(abs(g_cut), 1e-8 * M) + 4 * float(np.spacing(abs(base)))
+
+
+def assert_rows_tie_aware(ids_a, d_a, ids_b, d_b, base, M, what="kNN rows"):
+    """Per-node kNN rows of two implementations: shared neighbours carry the same
+    distance (1e-9 relative), and every neighbour in one row but not the other is a
+    near-tie at that row's k-th distance.  Returns the number of rows that differ."""
+    diff_rows = 0
+    for r in range(len(ids_a)):
+        ra = {int(x): float(d) for x, d in zip(ids_a[r], d_a[r])}
+        rb = {int(x): float(d) for x, d in zip(ids_b[r], d_b[r])}
+        for k in ra.keys() & rb.keys():
+            assert abs(ra[k] - rb[k]) <= 1e-9 * abs(rb[k]), f"{what}: row {r} id {k}: {ra[k]!r} vs {rb[k]!r}"
+        only = [ra[k] for k in ra.keys() - rb.keys()] + [rb[k] for k in rb.keys() - ra.keys()]
+        if only:
+            diff_rows += 1
+            cut = max(max(ra.values()), max(rb.values()))
+            tol = near_tie_tol(cut, base, M)
+            worst = max(abs(d - cut) for d in only)
+            assert worst <= tol, (f"{what}: row {r} differs beyond a near-tie: "
+                                  f"{sorted(ra.items(), key=lambda t: t[1])} vs {sorted(rb.items(), key=lambda t: t[1])}")
+    return diff_rows
+
+
+def assert_lists_tie_aware(a, b, base, M, what="candidate lists"):
+    """Two FindBest pair lists (sorted by (dist, i, j)): same length, shared pairs with
+    the same distance (1e-9 relative), every pair in the symmetric difference a
+    near-tie at the cut.  Returns the size of the symmetric difference."""
+    assert len(a) == len(b), (len(a), len(b))
+    ka = {(int(x), int(y)): float(d) for x, y, d in zip(a["i"], a["j"], a["dist"])}
+    kb = {(int(x), int(y)): float(d) for x, y, d in zip(b["i"], b["j"], b["dist"])}
+    for k in ka.keys() & kb.keys():
+        assert abs(ka[k] - kb[k]) <= 1e-9 * abs(kb[k]), f"{what}: pair {k}: {ka[k]!r} vs {kb[k]!r}"
+    only = [(k, ka[k]) for k in ka.keys() - kb.keys()] + [(k, kb[k]) for k in kb.keys() - ka.keys()]
+    if only:
+        cut = max(float(a["dist"][-1]), float(b["dist"][-1]))
+        tol = near_tie_tol(cut, base, M)
+        bad = [(k, d) for k, d in only if abs(d - cut) > tol]
+        assert not bad, f"{what}: {len(bad)} of {len(only)} differing pairs are not near-ties at the cut: {bad[:6]}"
+    return len(only)

@@ -70,8 +70,12 @@ _SIGS = {
     "mix64": (_u64, [_u64, _u64]),
     "rng_stream": (None, [_u64, _u64, _i, _u64, _U64P]),
 }
-_OPTIONAL = {"gen_ising": (_i, [_i, _d, _d, _d, _i, _i, _i, _u64, _F64P, _F64P, _u64, _I32P, _I32P,
-                                _F64P, C.POINTER(_u64)])}
+_I8P = np.ctypeslib.ndpointer(np.int8, flags="C")
+_OPTIONAL = {"gen_ising": (_i, [_i, _d, _d, _d, _i, _i, _i, _u64, C.c_void_p, _F64P, _u64, _I32P, _I32P,
+                                _F64P, C.POINTER(_u64)]),
+             "gen_ising_colored": (_i, [_i, _d, _d, _d, _i, _i, _i, _u64, _i, _I8P, _F64P, _u64, _I32P, _I32P,
+                                        _F64P, C.POINTER(_u64)]),
+             "gibbs_colored": (_i, [_i, _u64, _I32P, _I32P, _F64P, _F64P, _i, _i, _i, _u64, _i, _I8P])}
 
 _LIBS: dict[str, C.CDLL] = {}
 
@@ -305,10 +309,38 @@ def gen_ising(n, M, seed, mean_deg=4.0, w_sigma=0.3, th_sigma=0.1, burn_in=1000,
     ej = np.zeros(cap, np.int32)
     w = np.zeros(cap)
     ne = _u64()
-    _chk("orc", L.orc_gen_ising(n, mean_deg, w_sigma, th_sigma, M, burn_in, thin, seed, X, th, cap,
+    _chk("orc", L.orc_gen_ising(n, mean_deg, w_sigma, th_sigma, M, burn_in, thin, seed, X.ctypes.data, th, cap,
                                 ei, ej, w, C.byref(ne)))
     k = ne.value
     return X, dict(theta=th, i=ei[:k].copy(), j=ej[:k].copy(), w=w[:k].copy())
+
+
+def gen_ising_colored(n, M, seed, mean_deg=4.0, w_sigma=0.3, th_sigma=0.1, burn_in=1000, thin=10, threads=None):
+    """The device data pipeline's chain (gen.cu generate_ising) restated in C: the same
+    truth as gen_ising and the coloured Gibbs chain, int8 samples [n][M]."""
+    L = lib("orc")
+    X = np.zeros((n, M), np.int8)
+    th = np.zeros(n)
+    cap = int(n * mean_deg * 1.5) + 1024
+    ei = np.zeros(cap, np.int32)
+    ej = np.zeros(cap, np.int32)
+    w = np.zeros(cap)
+    ne = _u64()
+    _chk("orc", L.orc_gen_ising_colored(n, mean_deg, w_sigma, th_sigma, M, burn_in, thin, seed,
+                                        int(threads or os.cpu_count() or 1), X, th, cap, ei, ej, w, C.byref(ne)))
+    k = ne.value
+    return X, dict(theta=th, i=ei[:k].copy(), j=ej[:k].copy(), w=w[:k].copy())
+
+
+def gibbs_colored(ei, ej, w, theta, M, seed, burn_in=1000, thin=10, threads=None):
+    """Coloured Gibbs samples of a given truth (gen.cu generate_ising_graph)."""
+    L = lib("orc")
+    n = len(theta)
+    lo, hi = np.minimum(ei, ej).astype(np.int32), np.maximum(ei, ej).astype(np.int32)
+    X = np.zeros((n, M), np.int8)
+    _chk("orc", L.orc_gibbs_colored(n, len(lo), lo, hi, _f64(w), _f64(theta), M, burn_in, thin, seed,
+                                    int(threads or os.cpu_count() or 1), X))
+    return X
 
 
 def ising_lambda(n: int, M: int) -> float:

@@ -26,6 +26,22 @@ def test_graph_sampler_reproduces_er_generator(gpu):
     np.testing.assert_array_equal(Xa, Xb)
 
 
+@pytest.mark.parametrize("n,M,deg,burn,thin,seed", [(1000, 500, 4.0, 1000, 10, 1), (20000, 200, 5.0, 300, 5, 4)])
+def test_device_chain_equals_checker_chain(gpu, n, M, deg, burn, thin, seed):
+    """The device Gibbs chain (gen.cu) and its C restatement (oracle orc_gen_ising_colored,
+    pthreads) give the identical samples and truth: config-1 shape at full burn-in and a
+    config-4-degree case.  This is what lets bench.py's reference arm score the device
+    arm's data."""
+    Xc, tc = O.gen_ising_colored(n, M, seed, mean_deg=deg, burn_in=burn, thin=thin)
+    m = gpu.Model(n, M, gpu.NRG_ISING, 1.0)
+    Xd = m.generate_ising(mean_deg=deg, burn_in=burn, thin=thin, seed=seed, want_samples=True)
+    np.testing.assert_array_equal(Xd, Xc)
+    Xg = m.generate_ising_graph(tc["i"], tc["j"], tc["w"], tc["theta"], burn_in=burn, thin=thin, seed=seed + 1,
+                                want_samples=True)
+    np.testing.assert_array_equal(Xg, O.gibbs_colored(tc["i"], tc["j"], tc["w"], tc["theta"], M, seed + 1,
+                                                      burn_in=burn, thin=thin))
+
+
 def test_graph_sampler_validation(gpu):
     m = gpu.Model(10, 32, gpu.NRG_ISING, 1.0)
     with pytest.raises(ValueError):
