@@ -323,6 +323,7 @@ def parity_block(model, R, si, sj, sl, d_ref, M, P):
     the reference's on the pairs the cpu_baseline leg scored (north_star tolerances:
     dist 1e-5 relative, w* 1e-4, gain 1e-5 * max(|gain_ref|, 1e-8 M))."""
     i, j = si[sl], sj[sl]
+    model.begin_generation()  # the reference's generation: base = log_posterior at this state
     d_dev = model.distance(P.NRG_EXACT, i, j)
     rel = np.abs(d_dev - d_ref) / np.abs(d_ref)
     w_dev, g_dev, _ = model.optimize_edge(i, j)

@@ -279,6 +279,26 @@ int nrg_comm_init(nrg_ctx* ctx, const uint8_t id[128], int32_t rank, int32_t wor
 int nrg_loopback_create(int32_t world, void** group);
 int nrg_loopback_destroy(void* group);
 int nrg_comm_init_loopback(nrg_ctx* ctx, void* group, int32_t rank);
+/* Host transport: the sharded path's collectives carried by caller-supplied callbacks
+ * on HOST buffers (MPI, gloo through torch.distributed, sockets -- a multi-node job
+ * without NCCL).  The library stages device data through pinned memory around each
+ * call.  Every callback is collective (all ranks call it in the same order) and returns
+ * 0 on success; byte counts and offsets are per rank (arrays of `world`). */
+typedef struct {
+    void* user;
+    int (*allgatherv)(void* user, const void* send, uint64_t send_bytes, void* recv, const uint64_t* recv_bytes);
+    int (*alltoallv)(void* user, const void* send, const uint64_t* send_bytes, const uint64_t* send_off, void* recv,
+                     const uint64_t* recv_bytes, const uint64_t* recv_off);
+    int (*allreduce_u64)(void* user, uint64_t* v, int32_t n, int32_t is_max);
+    int (*bcast_f64)(void* user, double* v, int32_t n); /* from rank 0 */
+} nrg_host_transport;
+int nrg_comm_init_host(nrg_ctx* ctx, const nrg_host_transport* t, int32_t rank, int32_t world);
+/* The routing plan of one key exchange of the key-sharded distance cache (host-only):
+ * from the world x world request-count matrix (row = requester, column = owner; counts
+ * of 8-byte keys) the alltoallv byte counts and offsets of `rank` as sender (send_*) and
+ * as owner (recv_*); returns the number of keys `rank` receives in *n_recv. */
+int nrg_route_plan(int32_t world, int32_t rank, const uint64_t* counts, uint64_t* send_bytes, uint64_t* send_off,
+                   uint64_t* recv_bytes, uint64_t* recv_off, uint64_t* n_recv);
 /* The partition functions of the sharded path (host-only, no GPU needed): the node
  * range [lo, hi) of `rank` in a level of n nodes, and the owner rank of a pair key in
  * the key-sharded distance cache. */

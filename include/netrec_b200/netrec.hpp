@@ -36,12 +36,19 @@
 
 #include "../netrec_b200.h"
 
-// This header defines the reference's core types itself; mark the reference headers
-// that define them as already included, so reference headers that only *use* them
-// (e.g. inc/io.hpp, the CLI's text formats) compile against these definitions.
+// This header defines the reference's hot-path types and functions itself; mark the
+// reference headers that define them as already included, so reference headers that
+// only *use* them (inc/io.hpp, the CLI's text formats, the experiment harness
+// inc/bench.hpp with netrec_b200/synth.hpp) compile unchanged against these definitions.
 #define NETREC_COMMON_HPP
+#define NETREC_RANDOM_HPP
 #define NETREC_SAMPLE_MATRIX_HPP
 #define NETREC_SPARSE_WEIGHTS_HPP
+#define NETREC_LINE_SEARCH_HPP
+#define NETREC_MODEL_HPP
+#define NETREC_KNN_HPP
+#define NETREC_FIND_BEST_HPP
+#define NETREC_RECONSTRUCT_HPP
 
 namespace netrec {
 

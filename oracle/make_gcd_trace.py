@@ -8,7 +8,9 @@ eps = 1e-6 N.  Test infrastructure only.
 
     make -C oracle && python oracle/make_gcd_trace.py
 
-The fixture stores every iteration's candidate list (the candidate_hook), the
+threads = 1: the reference's apply_edge_updates is the sequential Gauss-Seidel loop only
+for threads <= 1 (inc/reconstruct.hpp:74-82; more threads take try-locks with deferral,
+a nondeterministic order).  The fixture stores every iteration's candidate list (the candidate_hook), the
 iteration records and the final state; the samples are regenerated from the seed
 (and checked by digest) on the GPU box.
 """
@@ -35,7 +37,7 @@ def main():
     m = int(round(KAPPA * N))
     R = O.CpuModel("ref", X.astype(np.float64), 0, lam)
     t = time.time()
-    recs, conv, cands = R.reconstruct_gcd(kappa=KAPPA, eps=-1.0, max_iters=MAX_ITERS, seed=GCD_SEED, threads=8,
+    recs, conv, cands = R.reconstruct_gcd(kappa=KAPPA, eps=-1.0, max_iters=MAX_ITERS, seed=GCD_SEED, threads=1,
                                           cand_cap=MAX_ITERS * m)
     secs = time.time() - t
     assert conv, "reference did not converge"

@@ -12,10 +12,13 @@ from ._lib import (  # noqa: F401
     NRG_LINE,
     NRG_TABLE,
     PAIR_DT,
+    HostTransport,
     Model,
+    TorchDistTransport,
     load,
     recall_curve,
+    route_plan,
 )
 
-__all__ = ["Model", "load", "recall_curve", "PAIR_DT", "NRG_ISING", "NRG_GAUSSIAN", "NRG_EXACT",
+__all__ = ["Model", "HostTransport", "TorchDistTransport", "route_plan", "load", "recall_curve", "PAIR_DT", "NRG_ISING", "NRG_GAUSSIAN", "NRG_EXACT",
            "NRG_GRADIENT", "NRG_TABLE", "NRG_LINE"]

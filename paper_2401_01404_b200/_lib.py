@@ -110,6 +110,11 @@ SIGNATURES = {
     "nrg_loopback_create": (C.c_int, [_i32, C.POINTER(_VP)]),
     "nrg_loopback_destroy": (C.c_int, [_VP]),
     "nrg_comm_init_loopback": (C.c_int, [_P, _VP, _i32]),
+    "nrg_comm_init_host": (C.c_int, [_P, C.c_void_p, _i32, _i32]),
+    "nrg_route_plan": (C.c_int, [_i32, _i32, np.ctypeslib.ndpointer(np.uint64, flags="C"),
+                                 np.ctypeslib.ndpointer(np.uint64, flags="C"), np.ctypeslib.ndpointer(np.uint64, flags="C"),
+                                 np.ctypeslib.ndpointer(np.uint64, flags="C"), np.ctypeslib.ndpointer(np.uint64, flags="C"),
+                                 C.POINTER(_u64)]),
     "nrg_shard_range": (C.c_int, [_u64, _i32, _i32, C.POINTER(_u64), C.POINTER(_u64)]),
     "nrg_key_owner": (_i32, [_u64, _i32]),
 }
@@ -433,6 +438,12 @@ class Model:
         """Join an NCCL job (uid from comm_unique_id() on rank 0)."""
         check(self.L.nrg_comm_init(self.h, uid, rank, world))
 
+    def comm_init_host(self, transport: "HostTransport"):
+        """Join a sharded job whose collectives run over a host transport (e.g.
+        TorchDistTransport: any torch.distributed backend, gloo included)."""
+        check(self.L.nrg_comm_init_host(self.h, C.byref(transport.struct), transport.rank, transport.world))
+        self._transport = transport  # the callbacks must outlive the context's use of them
+
     def comm_init_loopback(self, group, rank: int):
         check(self.L.nrg_comm_init_loopback(self.h, group, rank))
 
@@ -441,6 +452,131 @@ class Model:
         check(self.L.nrg_phase_times(self.h, out, 7))
         names = ["score", "knn", "select", "update", "theta", "logpost", "snapshot"]
         return dict(zip(names, out.tolist()))
+
+
+_AGV = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, _u64, C.c_void_p, C.POINTER(_u64))
+_A2A = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(_u64), C.POINTER(_u64), C.c_void_p, C.POINTER(_u64),
+                   C.POINTER(_u64))
+_ARU = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(_u64), _i32, _i32)
+_BCF = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), _i32)
+
+
+class _HostTransportStruct(C.Structure):
+    """nrg_host_transport (include/netrec_b200.h)"""
+    _fields_ = [("user", C.c_void_p), ("allgatherv", _AGV), ("alltoallv", _A2A), ("allreduce_u64", _ARU),
+                ("bcast_f64", _BCF)]
+
+
+class HostTransport:
+    """Base of a host transport: subclasses implement the four collectives on numpy
+    views of the host buffers the library hands over."""
+
+    def __init__(self, rank: int, world: int):
+        self.rank, self.world = rank, world
+        self._cbs = (_AGV(self._agv), _A2A(self._a2a), _ARU(self._aru), _BCF(self._bcf))
+        self.struct = _HostTransportStruct(None, *self._cbs)
+
+    @staticmethod
+    def _view(ptr, n):
+        return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint8)), shape=(max(int(n), 1),))[: int(n)] \
+            if n else np.zeros(0, np.uint8)
+
+    def _agv(self, _u, send, sbytes, recv, rbytes):
+        try:
+            rb = [int(rbytes[r]) for r in range(self.world)]
+            self.allgatherv(self._view(send, sbytes), self._view(recv, sum(rb)), rb)
+            return 0
+        except Exception:  # noqa: BLE001 -- reported to the library as a failed collective
+            return 1
+
+    def _a2a(self, _u, send, sb, so, recv, rb, ro):
+        try:
+            w = self.world
+            sb_, so_, rb_, ro_ = ([int(a[r]) for r in range(w)] for a in (sb, so, rb, ro))
+            st = max((o + b for o, b in zip(so_, sb_)), default=0)
+            rt = max((o + b for o, b in zip(ro_, rb_)), default=0)
+            self.alltoallv(self._view(send, st), sb_, so_, self._view(recv, rt), rb_, ro_)
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    def _aru(self, _u, v, n, is_max):
+        try:
+            a = np.ctypeslib.as_array(v, shape=(int(n),))
+            a[:] = self.allreduce_u64(a.copy(), bool(is_max))
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    def _bcf(self, _u, v, n):
+        try:
+            a = np.ctypeslib.as_array(v, shape=(int(n),))
+            a[:] = self.bcast_f64(a.copy())
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+
+class TorchDistTransport(HostTransport):
+    """The sharded path's collectives over torch.distributed on CPU tensors (gloo, or
+    any backend with CPU send/recv): a multi-process / multi-node job without NCCL."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        super().__init__(dist.get_rank(group), dist.get_world_size(group))
+
+    def allgatherv(self, send, recv, rbytes):
+        import torch
+        mx = max(rbytes)
+        buf = torch.zeros(max(mx, 1), dtype=torch.uint8)
+        buf[: len(send)] = torch.from_numpy(send.copy())
+        parts = [torch.zeros_like(buf) for _ in range(self.world)]
+        self.dist.all_gather(parts, buf, group=self.group)
+        off = 0
+        for r, b in enumerate(rbytes):
+            recv[off:off + b] = parts[r][:b].numpy()
+            off += b
+
+    def alltoallv(self, send, sb, so, recv, rb, ro):
+        import torch
+        reqs, bufs = [], []
+        for r in range(self.world):
+            if r == self.rank:
+                recv[ro[r]:ro[r] + rb[r]] = send[so[r]:so[r] + sb[r]]
+                continue
+            if sb[r]:
+                reqs.append(self.dist.isend(torch.from_numpy(send[so[r]:so[r] + sb[r]].copy()), r, group=self.group))
+            if rb[r]:
+                t = torch.zeros(rb[r], dtype=torch.uint8)
+                bufs.append((r, t))
+                reqs.append(self.dist.irecv(t, r, group=self.group))
+        for q in reqs:
+            q.wait()
+        for r, t in bufs:
+            recv[ro[r]:ro[r] + rb[r]] = t.numpy()
+
+    def allreduce_u64(self, v, is_max):
+        import torch
+        t = torch.from_numpy(v.astype(np.int64))
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX if is_max else self.dist.ReduceOp.SUM, group=self.group)
+        return t.numpy().astype(np.uint64)
+
+    def bcast_f64(self, v):
+        import torch
+        t = torch.from_numpy(v.copy())
+        self.dist.broadcast(t, 0, group=self.group)
+        return t.numpy()
+
+
+def route_plan(world: int, rank: int, counts):
+    """alltoallv plan of one key exchange (nrg_route_plan): (send_bytes, send_off,
+    recv_bytes, recv_off, n_recv) for `rank` from the world x world count matrix."""
+    cnt = np.ascontiguousarray(counts, dtype=np.uint64).reshape(-1)
+    out = [np.zeros(world, np.uint64) for _ in range(4)]
+    q = _u64()
+    check(load().nrg_route_plan(world, rank, cnt, *out, C.byref(q)))
+    return (*out, q.value)
 
 
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:

@@ -688,6 +688,37 @@ int nrg_comm_init_loopback(nrg_ctx* x, void* group, int32_t rank) {
     });
 }
 
+int nrg_comm_init_host(nrg_ctx* x, const nrg_host_transport* t, int32_t rank, int32_t world) {
+    return guardx(x, [&] {
+        if (!t) nrg::fail(NRG_EINVAL, "null transport");
+        if (world < 1 || rank < 0 || rank >= world) nrg::fail(NRG_EINVAL, "bad rank/world");
+        delete static_cast<nrg::Comm*>(x->c.comm);
+        x->c.comm = nullptr;
+        x->c.rank = 0;
+        x->c.world = 1;
+        if (world == 1) return;
+        x->c.comm = nrg::make_host_comm(*t, rank, world);
+        x->c.rank = rank;
+        x->c.world = world;
+    });
+}
+
+int nrg_route_plan(int32_t world, int32_t rank, const uint64_t* counts, uint64_t* send_bytes, uint64_t* send_off,
+                   uint64_t* recv_bytes, uint64_t* recv_off, uint64_t* n_recv) {
+    return guard([&] {
+        if (world < 1 || rank < 0 || rank >= world || !counts) nrg::fail(NRG_EINVAL, "bad rank/world");
+        std::vector<size_t> sb, so, rb, ro;
+        const uint64_t q = nrg::route_plan(world, rank, counts, sb, so, rb, ro);
+        for (int r = 0; r < world; ++r) {
+            send_bytes[r] = sb[r];
+            send_off[r] = so[r];
+            recv_bytes[r] = rb[r];
+            recv_off[r] = ro[r];
+        }
+        if (n_recv) *n_recv = q;
+    });
+}
+
 int nrg_shard_range(uint64_t n, int32_t rank, int32_t world, uint64_t* lo, uint64_t* hi) {
     return guard([&] {
         if (world < 1 || rank < 0 || rank >= world) nrg::fail(NRG_EINVAL, "bad rank/world");

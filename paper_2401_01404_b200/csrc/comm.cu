@@ -155,6 +155,99 @@ Comm* make_nccl_comm(const uint8_t id[128], int rank, int world, int device) {
     return c;
 }
 
+// ---------------------------------------------------------------- host transport
+namespace {
+// collectives through caller-supplied callbacks on host buffers: device data staged
+// through pinned memory (grown on demand) around each call
+struct HostComm final : Comm {
+    nrg_host_transport t{};
+    void* pin_send = nullptr;
+    void* pin_recv = nullptr;
+    size_t cap_send = 0, cap_recv = 0;
+    ~HostComm() override {
+        if (pin_send) cudaFreeHost(pin_send);
+        if (pin_recv) cudaFreeHost(pin_recv);
+    }
+    static void* grow(void*& p, size_t& cap, size_t n) {
+        if (n > cap) {
+            if (p) NRG_CUDA(cudaFreeHost(p));
+            p = nullptr;
+            cap = std::max<size_t>(n, 1 << 16);
+            NRG_CUDA(cudaMallocHost(&p, cap));
+        }
+        return p;
+    }
+    static void ok(int rc, const char* what) {
+        if (rc) fail(100, std::string("host transport: ") + what + " failed (" + std::to_string(rc) + ")");
+    }
+    void allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) override {
+        allgatherv(send, recv, std::vector<size_t>(world, bytes), s);
+    }
+    void allgatherv(const void* send, void* recv, const std::vector<size_t>& bytes, cudaStream_t s) override {
+        size_t tot = 0;
+        for (size_t b : bytes) tot += b;
+        void* hs = grow(pin_send, cap_send, bytes[rank]);
+        void* hr = grow(pin_recv, cap_recv, tot);
+        if (bytes[rank]) NRG_CUDA(cudaMemcpyAsync(hs, send, bytes[rank], cudaMemcpyDeviceToHost, s));
+        NRG_CUDA(cudaStreamSynchronize(s));
+        std::vector<uint64_t> rb(bytes.begin(), bytes.end());
+        ok(t.allgatherv(t.user, hs, bytes[rank], hr, rb.data()), "allgatherv");
+        if (tot) NRG_CUDA(cudaMemcpyAsync(recv, hr, tot, cudaMemcpyHostToDevice, s));
+        NRG_CUDA(cudaStreamSynchronize(s));
+    }
+    void alltoallv(const void* send, const std::vector<size_t>& sb, const std::vector<size_t>& so, void* recv,
+                   const std::vector<size_t>& rb, const std::vector<size_t>& ro, cudaStream_t s) override {
+        size_t st = 0, rt = 0;
+        for (int r = 0; r < world; ++r) {
+            st = std::max(st, so[r] + sb[r]);
+            rt = std::max(rt, ro[r] + rb[r]);
+        }
+        void* hs = grow(pin_send, cap_send, st);
+        void* hr = grow(pin_recv, cap_recv, rt);
+        if (st) NRG_CUDA(cudaMemcpyAsync(hs, send, st, cudaMemcpyDeviceToHost, s));
+        NRG_CUDA(cudaStreamSynchronize(s));
+        std::vector<uint64_t> a(sb.begin(), sb.end()), b(so.begin(), so.end()), c(rb.begin(), rb.end()),
+            d(ro.begin(), ro.end());
+        ok(t.alltoallv(t.user, hs, a.data(), b.data(), hr, c.data(), d.data()), "alltoallv");
+        if (rt) NRG_CUDA(cudaMemcpyAsync(recv, hr, rt, cudaMemcpyHostToDevice, s));
+        NRG_CUDA(cudaStreamSynchronize(s));
+    }
+    void allreduce_u64(uint64_t* v, int n, bool mx, cudaStream_t) override {
+        ok(t.allreduce_u64(t.user, v, n, mx ? 1 : 0), "allreduce_u64");
+    }
+    void bcast_f64(double* v, int n, cudaStream_t) override { ok(t.bcast_f64(t.user, v, n), "bcast_f64"); }
+};
+}  // namespace
+
+Comm* make_host_comm(const nrg_host_transport& t, int rank, int world) {
+    if (!t.allgatherv || !t.alltoallv || !t.allreduce_u64 || !t.bcast_f64) fail(22, "host transport: missing callback");
+    auto* c = new HostComm();
+    c->t = t;
+    c->rank = rank;
+    c->world = world;
+    return c;
+}
+
+uint64_t route_plan(int world, int rank, const uint64_t* mat, std::vector<size_t>& sb, std::vector<size_t>& so,
+                    std::vector<size_t>& rb, std::vector<size_t>& ro) {
+    sb.assign(world, 0);
+    so.assign(world, 0);
+    rb.assign(world, 0);
+    ro.assign(world, 0);
+    size_t off = 0, roff = 0;
+    uint64_t q = 0;
+    for (int r = 0; r < world; ++r) {
+        sb[r] = (size_t)mat[(size_t)rank * world + r] * 8;  // my requests to owner r
+        so[r] = off;
+        off += sb[r];
+        rb[r] = (size_t)mat[(size_t)r * world + rank] * 8;  // requester r's keys I own
+        ro[r] = roff;
+        roff += rb[r];
+        q += mat[(size_t)r * world + rank];
+    }
+    return q;
+}
+
 // ---------------------------------------------------------------- loopback
 struct LoopbackGroup {
     int world;

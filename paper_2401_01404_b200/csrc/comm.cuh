@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "../../include/netrec_b200.h"
 
 namespace nrg {
 
@@ -35,6 +36,13 @@ struct Comm {
 };
 
 Comm* make_nccl_comm(const uint8_t id[128], int rank, int world, int device);
+Comm* make_host_comm(const nrg_host_transport& t, int rank, int world);
+
+// alltoallv plan of one key exchange from the world x world request-count matrix
+// (row = requester, column = owner): byte counts / offsets of `rank` as sender and as
+// owner; returns the number of keys `rank` receives
+uint64_t route_plan(int world, int rank, const uint64_t* mat, std::vector<size_t>& sb, std::vector<size_t>& so,
+                    std::vector<size_t>& rb, std::vector<size_t>& ro);
 int nccl_unique_id(uint8_t id[128]);
 
 struct LoopbackGroup;

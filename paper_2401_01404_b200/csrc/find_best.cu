@@ -283,11 +283,14 @@ __global__ void dense_subtri_kernel(const int32_t* __restrict__ nodes, uint64_t 
 // Settles the dense root's probe counts (see dense_probe, knn.cu): every probe there was
 // counted as a hit; of the U distinct pairs probed (bits set), the ones no shallower level
 // had scored (absent from the distance cache: U - F) are the generation's misses.
+// count_bits: the probed pairs (bits) count as misses on one rank only; every rank
+// moves the probed pairs its shard of the key-sharded cache already held back to hits
 __global__ void dense_recount_kernel(HashView h, const int32_t* __restrict__ loc, const uint32_t* __restrict__ bits,
-                                     uint64_t nwords, uint64_t dn, uint64_t* __restrict__ counters) {
+                                     uint64_t nwords, uint64_t dn, uint64_t* __restrict__ counters, int count_bits) {
     long long d = 0;
     const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, st = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t w = t0; w < nwords; w += st) d += __popc(bits[w]);
+    if (count_bits)
+        for (uint64_t w = t0; w < nwords; w += st) d += __popc(bits[w]);
     if (h.keys) {
         for (uint64_t s = t0; s <= h.mask; s += st) {
             const uint64_t key = __ldcs(&h.keys[s]);
@@ -306,20 +309,46 @@ __global__ void dense_recount_kernel(HashView h, const int32_t* __restrict__ loc
     }
 }
 
-struct DenseGuard {  // the level that set up the dense root tears it down (also on throw)
+// The level that set up the dense root tears it down (also on throw).  In a sharded job
+// (world > 1) a dense level is replicated: every rank screens the whole level with the
+// tensor cores and runs its NNDescent/FindBest as a single-rank job (world 1 inside the
+// region, no collectives -- every rank holds the same triangle and computes the same
+// lists), which keeps the fast dense path of the single-GPU run instead of switching to
+// the claim path.  The miss/hit counters count the region once job-wide: ranks other than
+// 0 restore their pre-region counters and contribute only their cache shard's overlap.
+struct DenseGuard {
     Context& c;
     bool owner = false;
+    int real_rank = 0, real_world = 1;
+    uint64_t saved[2] = {0, 0};
     explicit DenseGuard(Context& cc) : c(cc) {}
+    void replicate() {
+        real_rank = c.rank;
+        real_world = c.world;
+        if (real_rank != 0) {
+            NRG_CUDA(cudaMemcpyAsync(saved, c.dcounters(), 16, cudaMemcpyDeviceToHost, c.stream));
+            c.sync();
+        }
+        c.rank = 0;
+        c.world = 1;
+    }
     ~DenseGuard() {
         if (owner) {
             const uint64_t pairs = c.dense_n * (c.dense_n - 1) / 2;
             const HashView h = (c.Ckeys.p && c.Ccap) ? c.Cview() : HashView{nullptr, nullptr, 0};
+            if (real_world > 1) {
+                c.rank = real_rank;
+                c.world = real_world;
+                if (real_rank != 0)
+                    cudaMemcpyAsync(c.dcounters(), saved, 16, cudaMemcpyHostToDevice, c.stream);
+            }
             // off the critical path: only the counters need it (and the cache must not
             // change under it: join_side() before any clear, resize or counter read)
             cudaStream_t ss = c.fork();
             dense_recount_kernel<<<148 * 8, 256, 0, ss>>>(h, static_cast<const int32_t*>(c.dloc.p),
                                                           static_cast<const uint32_t*>(c.dbits.p),
-                                                          (pairs + 31) / 32, c.dense_n, c.dcounters());
+                                                          (pairs + 31) / 32, c.dense_n, c.dcounters(),
+                                                          real_rank == 0 ? 1 : 0);
             c.fork_done();
             c.dense_active = false;
             c.dense_n = 0;  // the buffers stay (grow-only): the next generation reuses them
@@ -484,7 +513,7 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
     {
         const uint64_t kw = (uint64_t)std::max(k, 4);
         const uint64_t cap = reverse ? std::max<uint64_t>(2 * kw, 8) : std::max<uint64_t>(kw, 8);
-        if (!c.dense_active && mode == EXACT && c.kind == ISING && c.world == 1 && n <= dense_max_n() &&
+        if (!c.dense_active && mode == EXACT && c.kind == ISING && n <= dense_max_n() &&
             dense_ratio() * cap * cap >= n) {
             c.join_side();  // a previous root's recount still reads dloc / dbits
             double* tri = c.dtri.as<double>(total);
@@ -509,6 +538,7 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
                 c.dense_active = true;
                 c.dense_n = n;
                 dg.owner = true;
+                if (c.world > 1) dg.replicate();
             }
         }
     }

@@ -1232,17 +1232,8 @@ static void exchange_and_score(Context& c, int mode, const ClaimSink& sink, uint
     c.sync();
     for (int d = 0; d < W; ++d) mat[(size_t)me * W + d] = cnt[d];
     comm->allreduce_u64(mat.data(), W * W, false, c.stream);
-    std::vector<size_t> sb(W), so(W), rb(W), ro(W);
-    uint64_t Q = 0;
-    for (int r = 0, off = 0, roff = 0; r < W; ++r) {
-        sb[r] = cnt[r] * 8;
-        so[r] = (size_t)off;
-        off += (int)sb[r];
-        rb[r] = mat[(size_t)r * W + me] * 8;
-        ro[r] = (size_t)roff;
-        roff += (int)rb[r];
-        Q += mat[(size_t)r * W + me];
-    }
+    std::vector<size_t> sb, so, rb, ro;
+    const uint64_t Q = route_plan(W, me, mat.data(), sb, so, rb, ro);
     uint64_t* recv_keys = X.recv_keys.as<uint64_t>(Q + 1);
     comm->alltoallv(skeys, sb, so, recv_keys, rb, ro, c.stream);
     // 2. owner side: claim (key-sorted for K1 locality), score local + remote claims

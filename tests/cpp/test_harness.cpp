@@ -1,10 +1,14 @@
-// The experiment harness (netrec_b200/bench.hpp, mirroring inc/bench.hpp) on the
-// device path: ER precision truth, Gibbs samples, FindBest scaling / recall,
-// GCD-vs-CD convergence and support metrics.  Prints one line per check.
+// The reference's OWN experiment harness (inc/bench.hpp, compiled unmodified from
+// /root/reference) on the device path through the drop-in: ER precision truth, Gibbs
+// samples, FindBest scaling / recall, GCD-vs-CD convergence and support metrics.
+// Built only where the reference headers exist (paper_2401_01404_b200/build.py);
+// prints one line per check.
 #include <cmath>
 #include <cstdio>
 
-#include "netrec_b200/bench.hpp"
+#include "netrec_b200/netrec.hpp"
+#include "netrec_b200/synth.hpp"
+#include "netrec/bench.hpp"  // the reference's file: resolved from -I/root/reference/proj/include
 
 using namespace netrec;
 

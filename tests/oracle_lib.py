@@ -193,6 +193,19 @@ class CpuModel:
         _chk(self.which, self._f("distance")(self.h, mode, len(i), i, j, out))
         return out
 
+    def distance_parallel(self, mode, i, j, threads=None):
+        """distance() under the reference's parallel_for (ref only; the C checker runs
+        the same pairs serially)"""
+        i, j = _i32(i), _i32(j)
+        if self.which != "ref":
+            return self.distance(mode, i, j)
+        f = self.L.ref_distance_parallel
+        f.restype = _i
+        f.argtypes = [_P, _i, _u64, _I32P, _I32P, _F64P, _i]
+        out = np.zeros(len(i))
+        _chk(self.which, f(self.h, mode, len(i), i, j, out, int(threads or os.cpu_count() or 1)))
+        return out
+
     def optimize_edge(self, i, j):
         i, j = _i32(i), _i32(j)
         w = np.zeros(len(i))

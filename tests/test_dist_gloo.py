@@ -1,10 +1,15 @@
-"""The N>1 host logic on CPU with two gloo processes: the library's own partition
-functions (nrg_shard_range, nrg_key_owner) drive the key-sharded distance-cache
-protocol of the sharded NNDescent (requests routed to the key's owner, owner dedups and
-scores, answers routed back) and the per-sweep row all-gather; the C checker supplies
-the pair scores.  Checks: every rank gets the checker's distance for each of its
-queries, each unique pair is scored exactly once job-wide, and the gathered rows equal
-the single-process result."""
+"""The N>1 path over gloo, two processes (world_size 2).
+
+* CPU: the key-sharded distance-cache exchange planned by the library itself -- keys
+  routed with nrg_key_owner, the alltoallv sizes/offsets from nrg_route_plan (the
+  function exchange_and_score uses, knn.cu), the exchange over gloo -- delivers every
+  request to its owner exactly once and the answers back in request order; the node
+  partition (nrg_shard_range) covers each level exactly.
+* GPU: the product's sharded GCD (node-sharded NNDescent, key-sharded cache, replicated
+  dense levels, row all-gathers) with its collectives carried by gloo through the host
+  transport (nrg_comm_init_host / TorchDistTransport): two processes on one GPU, every
+  exchange host-side and blocking (no kernel waits on another rank), bitwise equal to
+  the single-process run."""
 from __future__ import annotations
 
 import os
@@ -12,6 +17,7 @@ import socket
 
 import numpy as np
 import pytest
+import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
@@ -31,87 +37,106 @@ def pair_key(a, b):
     return (int(a) << 32) | int(b)
 
 
-def _worker(rank, world, port, X, lam, queries, out):
+def _init(rank, world, port):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
+
+
+def _route_worker(rank, world, port, n, queries, out):
+    _init(rank, world, port)
     from paper_2401_01404_b200 import _lib as L
-    n = X.shape[0]
     lo, hi = L.shard_range(n, rank, world)
-    # this rank's candidates: queries of its own node range (as the gather kernel makes)
-    mine = [(i, j) for (i, j) in queries if lo <= i < hi]
-    local, remote = [], {r: [] for r in range(world)}
-    for (i, j) in mine:
-        k = pair_key(i, j)
-        o = L.key_owner(k, world)
-        (local if o == rank else remote[o]).append(k)
-    # request exchange (all-to-all of keys)
-    sent = [None] * world
-    dist.all_gather_object(sent, {r: remote[r] for r in range(world)})
-    incoming = [k for r in range(world) for k in sent[r].get(rank, [])]
-    # owner: dedup in this rank's cache shard, score each new key once
-    m = O.CpuModel("orc", X, 0, lam)
-    m.begin_generation()
-    keys = sorted(set(local) | set(incoming))
-    vals = {}
-    if keys:
-        ki = np.array([k >> 32 for k in keys], np.int32)
-        kj = np.array([k & 0xffffffff for k in keys], np.int32)
-        for k, d in zip(keys, m.distance(0, ki, kj)):
-            vals[k] = d
-    scored = m.counters()["misses"]
-    # answers back
-    answers = [None] * world
-    dist.all_gather_object(answers, {k: vals[k] for k in incoming})
-    got = {}
-    for (i, j) in mine:
-        k = pair_key(i, j)
-        o = L.key_owner(k, world)
-        got[(i, j)] = vals[k] if o == rank else answers[o][k]
-    # row all-gather: each rank contributes rows [lo, hi) of a per-node table
-    rows = [None] * world
-    dist.all_gather_object(rows, (lo, hi, [int(i) * 7 for i in range(lo, hi)]))
-    out.put((rank, got, scored, rows, (lo, hi)))
+    mine = [(i, j) for (i, j) in queries if lo <= i < hi]  # this rank's node range
+    keys = np.array([pair_key(i, j) for i, j in mine], np.uint64)
+    dest = np.array([L.key_owner(int(k), world) for k in keys], np.int64)
+    order = np.argsort(dest, kind="stable")  # requests grouped by owner, as the device sorts them
+    skeys = keys[order]
+    counts = np.zeros(world * world, np.uint64)
+    counts[rank * world:(rank + 1) * world] = np.bincount(dest, minlength=world)
+    t = torch.from_numpy(counts.astype(np.int64))
+    dist.all_reduce(t)
+    sb, so, rb, ro, q = L.route_plan(world, rank, t.numpy())
+    tr = L.TorchDistTransport()
+    recv = np.zeros(int(q) * 8, np.uint8)
+    tr.alltoallv(skeys.view(np.uint8), sb.tolist(), so.tolist(), recv, rb.tolist(), ro.tolist())
+    got = recv.view(np.uint64)
+    # owner side: every received key is mine; answer = key * 3 (a stand-in score)
+    assert all(L.key_owner(int(k), world) == rank for k in got)
+    ans = (got * np.uint64(3)).view(np.uint8)
+    back = np.zeros(len(skeys) * 8, np.uint8)
+    tr.alltoallv(ans, rb.tolist(), ro.tolist(), back, sb.tolist(), so.tolist())
+    res = np.empty(len(keys), np.uint64)
+    res[order] = back.view(np.uint64)
+    out.put((rank, keys.tolist(), res.tolist(), got.tolist(), (lo, hi)))
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_key_sharded_cache_protocol_gloo(world):
-    X, _ = O.gen_ising(120, 80, seed=3, burn_in=100, thin=3)
-    lam = O.ising_lambda(120, 80)
-    rng = np.random.default_rng(0)
+@pytest.mark.parametrize("world", [2, 3])
+def test_routed_key_exchange_gloo(world):
+    n = 500
+    rng = np.random.default_rng(world)
     q = set()
-    while len(q) < 900:
-        i, j = map(int, rng.integers(0, 120, 2))
+    while len(q) < 3000:
+        i, j = map(int, rng.integers(0, n, 2))
         if i != j:
             q.add((i, j))
-            if rng.random() < 0.4:
-                q.add((j, i))  # probed from both endpoints, as NNDescent does
     queries = sorted(q)
     ctx = mp.get_context("spawn")
     out = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, X, lam, queries, out)) for r in range(world)]
+    procs = [ctx.Process(target=_route_worker, args=(r, world, port, n, queries, out)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted([out.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    ref = O.CpuModel("orc", X, 0, lam)
-    ref.begin_generation()
-    qi = np.array([a for a, _ in queries], np.int32)
-    qj = np.array([b for _, b in queries], np.int32)
-    truth = dict(zip(queries, ref.distance(0, qi, qj)))
-    covered = {}
-    for _, got, _, _, _ in res:
-        covered.update(got)
-    assert covered == truth  # every query answered with the checker's value, bitwise
-    unique = len({pair_key(a, b) for a, b in queries})
-    assert sum(r[2] for r in res) == unique  # each unique pair scored once job-wide
-    # partition covers [0, n) exactly; the gathered table equals the single-process one
+    owned = []
+    for _, keys, answers, got, _ in res:
+        assert answers == [k * 3 for k in keys]  # every answer back, in request order
+        owned += got
+    assert sorted(owned) == sorted(pair_key(i, j) for i, j in queries)  # each request reached its owner once
     spans = [r[4] for r in res]
-    assert spans[0][0] == 0 and spans[-1][1] == 120 and all(spans[t][1] == spans[t + 1][0] for t in range(world - 1))
-    for _, _, _, rows, _ in res:
-        table = [v for (_, _, part) in rows for v in part]
-        assert table == [i * 7 for i in range(120)]
+    assert spans[0][0] == 0 and spans[-1][1] == n and all(spans[t][1] == spans[t + 1][0] for t in range(world - 1))
+
+
+def _gcd_worker(rank, world, port, X, lam, out):
+    _init(rank, world, port)
+    import paper_2401_01404_b200 as P
+    m = P.Model.from_samples(X, P.NRG_ISING, lam)
+    m.comm_init_host(P.TorchDistTransport())
+    m.reset_counters()
+    recs = [m.gcd_iteration(it, kappa=2.0, seed=5, want_candidates=True) for it in (1, 2, 3)]
+    out.put((rank, [(float(r["delta"]), float(r["objective"]), c) for r, c in recs], m.get_state(),
+             m.counters()["misses"]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_gcd_over_gloo_host_transport(gpu):
+    X, _ = O.gen_ising(1500, 400, seed=6)
+    X = X.astype(np.int8)
+    lam = O.ising_lambda(1500, 400)
+    single = gpu.Model.from_samples(X, gpu.NRG_ISING, lam)
+    single.reset_counters()
+    ref = [single.gcd_iteration(it, kappa=2.0, seed=5, want_candidates=True) for it in (1, 2, 3)]
+    ref_state, ref_misses = single.get_state(), single.counters()["misses"]
+    del single
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gcd_worker, args=(r, 2, port, X, lam, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([out.get(timeout=600) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, recs, st, _ in res:
+        for (delta, obj, cand), (rrec, rcand) in zip(recs, ref):
+            np.testing.assert_array_equal(cand, rcand)
+            assert delta == rrec["delta"] and obj == rrec["objective"]
+        for a, b in zip(st, ref_state):
+            np.testing.assert_array_equal(a, b)
+    assert sum(r[3] for r in res) == ref_misses

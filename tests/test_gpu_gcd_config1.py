@@ -54,12 +54,18 @@ def test_gcd_config1_lockstep_vs_reference(gpu, golden):
     iters = len(g["rec_objective"])
     base = dev.log_posterior()
     assert_rel(base, -n * M * np.log(2.0), 1e-12, "empty-state objective")
-    n_diff = []
+    n_diff, beyond = [], []
     for it in range(1, iters + 1):
         dev.begin_generation()
         fb, _, _ = dev.find_best(gpu.NRG_EXACT, m, nodes, seed=O.mix64(int(g["gcd_seed"]), it))
         ref = _pairs(g["cand_i"][it - 1], g["cand_j"][it - 1], g["cand_dist"][it - 1])
-        n_diff.append(assert_lists_tie_aware(fb, ref, base, M, f"iteration {it}"))
+        try:
+            n_diff.append(assert_lists_tie_aware(fb, ref, base, M, f"iteration {it}"))
+        except AssertionError as e:
+            beyond.append((it, str(e)[:300]))
+            ka = set(zip(fb["i"].tolist(), fb["j"].tolist()))
+            kb = set(zip(ref["i"].tolist(), ref["j"].tolist()))
+            n_diff.append(len(ka ^ kb))
         delta = dev.apply_updates(ref)
         dev.theta_pass()
         base = dev.log_posterior()
@@ -70,7 +76,8 @@ def test_gcd_config1_lockstep_vs_reference(gpu, golden):
     assert_same_couplings(st, (None, g["final_i"], g["final_j"], g["final_w"]), tol=1e-4)
     np.testing.assert_allclose(st[0], g["final_theta"], rtol=0, atol=1e-4)
     print(f"config-1 lock-step: {iters} iterations, lists identical in {n_diff.count(0)}, "
-          f"differing candidates per iteration max {max(n_diff)}")
+          f"differing candidates per iteration {n_diff}; beyond near-ties: {beyond}")
+    assert not beyond
 
 
 def test_gcd_config1_free_running_converges_like_reference(gpu, golden):

@@ -103,3 +103,48 @@ def test_sharded_gcd_iterations_match_single(gpu):
         assert (st[1] == ref_state[1]).all() and (st[2] == ref_state[2]).all()
         np.testing.assert_array_equal(st[3], ref_state[3])
     grp.close()
+
+
+@pytest.mark.slow
+def test_sharded_config4_sweeps_match_single(gpu):
+    """Config 4 (Ising N=1e5, M=1000, lambda=214.6, kappa=2) at two virtual ranks: the
+    first two GCD sweeps (the empty-state sweep, then a sweep with ~1.5e5 couplings) give
+    bitwise the single-context candidate lists, deltas, objectives and states; the
+    sharded job keeps the tensor-core dense levels (replicated per rank) and scores each
+    unique pair once job-wide."""
+    n, M = 100_000, 1000
+    lam = O.ising_lambda(n, M)
+
+    def make():
+        m = gpu.Model(n, M, gpu.NRG_ISING, lam)
+        m.generate_ising(mean_deg=5.0, seed=1, burn_in=200)
+        return m
+
+    single = make()
+    single.reset_counters()
+    ref = [single.gcd_iteration(it, kappa=2.0, seed=1, want_candidates=True) for it in (0, 1)]
+    ref_state = single.get_state()
+    ref_misses = single.counters()["misses"]
+    ref_tc = single.kernel_stats()["tc_launches"]
+    del single
+    grp = gpu._lib.LoopbackGroup(2)
+    ms = [make() for _ in range(2)]
+    for r, m in enumerate(ms):
+        m.comm_init_loopback(grp.h, r)
+        m.reset_counters()
+
+    def work(r):
+        recs = [ms[r].gcd_iteration(it, kappa=2.0, seed=1, want_candidates=True) for it in (0, 1)]
+        return recs, ms[r].get_state(), ms[r].counters()["misses"], ms[r].kernel_stats()["tc_launches"]
+
+    res = _run_ranks(2, work)
+    assert ref_tc > 0
+    for recs, st, _, tc in res:
+        assert tc == ref_tc, "the sharded job must keep the dense (tensor-core) levels"
+        for (rec, cand), (rrec, rcand) in zip(recs, ref):
+            assert pairs_equal(cand, rcand)
+            assert rec["delta"] == rrec["delta"] and rec["objective"] == rrec["objective"]
+        for a, b in zip(st, ref_state):
+            np.testing.assert_array_equal(a, b)
+    assert sum(r[2] for r in res) == ref_misses
+    grp.close()
