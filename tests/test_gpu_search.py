@@ -263,7 +263,7 @@ def test_model_knn_and_find_best_vs_reference(gpu, seed):
     tab = table_model(gpu, t_ref)
     a = tab.find_knn(gpu.NRG_TABLE, 8, nodes, seed=11 + seed)
     assert row_sets(a[0]) == row_sets(b[0]) and a[2] == b[2]
-    np.testing.assert_array_equal(a[1], b[1])
+    np.testing.assert_array_equal(np.sort(a[1], axis=1), np.sort(b[1], axis=1))  # (reference rows: heap order)
     np.testing.assert_array_equal(a[3], b[3])
     fa, ta, sa = tab.find_best(gpu.NRG_TABLE, 2 * n, nodes, seed=12 + seed)
     assert pairs_equal(fa, fb) and (ta == tb).all() and sa == sb
