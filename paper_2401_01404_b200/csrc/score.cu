@@ -329,8 +329,9 @@ __global__ void __launch_bounds__(256, WPL == 1 ? 4 : NRG_K1S_MINB) ising_screen
 // two steps of partner loads in flight without holding them in registers (the small
 // kernel is bound by the latency of its partner loads at the occupancy its registers
 // allow).  Arithmetic, bound and outputs are those of ising_screen_small_kernel.
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+// smem: a shared-window address (computed once per thread: converting a generic
+// pointer inside the loop costs an S2R of the CTA's shared window per conversion)
+__device__ __forceinline__ void cp_async16(uint32_t sa, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
@@ -365,6 +366,7 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
     extern __shared__ __align__(16) unsigned char k1p_smem[];
     const int lane = threadIdx.x & 31, grp = lane / G, r = lane % G;
     unsigned char* wbuf = k1p_smem + (size_t)(threadIdx.x >> 5) * NS * P * RB;  // [stage][pair][row]
+    const uint32_t wbuf_sa = (uint32_t)__cvta_generic_to_shared(wbuf);
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     constexpr int NP = FOUR ? 4 : 8;  // bit planes of the stationary field
@@ -377,7 +379,7 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
     // stage the partner row of this group's entry into ring buffer `st` (one commit group
     // per step, empty past the chunk's end, so wait_group counts stay uniform)
     auto stage = [&](int st, int p, bool any) {
-        unsigned char* dst = wbuf + (size_t)(st * P + grp) * RB;
+        const uint32_t dst = wbuf_sa + (uint32_t)((st * P + grp) * RB);
         if (!any) {
             cp_async_commit();
             return;

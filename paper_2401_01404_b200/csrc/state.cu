@@ -726,9 +726,9 @@ __global__ void __launch_bounds__(256) logpost_node_kernel(int kind, const uint3
                                                            const double* __restrict__ Xd,
                                                            const double* __restrict__ H,
                                                            const double* __restrict__ theta, int M,
-                                                           int Mp, int Mw, double* __restrict__ out) {
+                                                           int Mp, int Mw, double* __restrict__ out, int r0 = 0) {
     __shared__ double sh[32];
-    const int r = blockIdx.x;
+    const int r = r0 + blockIdx.x;
     const double th = theta[r];
     double a = 0.0;
     if (kind == ISING) {
@@ -778,9 +778,23 @@ double log_posterior(Context& c) {
     c.tic();
     double* part = c.red.as<double>((size_t)c.n + 1024 + 8);
     double* res = part + c.n + 1024;
-    logpost_node_kernel<<<c.n, 256, 0, c.stream>>>(c.kind, c.dXb(), c.dXd(), c.dH(), c.dtheta(), c.M,
-                                                   c.Mp, c.Mw, part);
+    // per-node terms (a sharded job computes its node range and all-gathers the per-node
+    // values, so the fixed-order reduction below is bitwise the single-GPU one)
+    uint64_t lo = 0, hi = (uint64_t)c.n;
+    if (c.world > 1) shard_range((uint64_t)c.n, c.rank, c.world, lo, hi);
+    if (hi > lo)
+        logpost_node_kernel<<<(unsigned)(hi - lo), 256, 0, c.stream>>>(c.kind, c.dXb(), c.dXd(), c.dH(), c.dtheta(),
+                                                                     c.M, c.Mp, c.Mw, part, (int)lo);
     NRG_LAUNCH_CHECK();
+    if (c.world > 1) {
+        std::vector<size_t> bytes(c.world);
+        for (int r = 0; r < c.world; ++r) {
+            uint64_t l, h;
+            shard_range((uint64_t)c.n, r, c.world, l, h);
+            bytes[r] = (h - l) * 8;
+        }
+        static_cast<Comm*>(c.comm)->allgatherv(part + lo, part, bytes, c.stream);
+    }
     reduce_fixed_kernel<<<1, 1024, 0, c.stream>>>(part, c.n, res);
     NRG_LAUNCH_CHECK();
     const int nb = 592;

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "comm.cuh"
 #include "pairscore.cuh"
 
 namespace nrg {
@@ -758,10 +759,11 @@ void all_pairs_list(Context& c, int32_t* ci, int32_t* cj, double* tie) {
 __global__ void __launch_bounds__(256) theta_kernel(int kind, const uint32_t* __restrict__ Xb,
                                                     const double* __restrict__ Xd, const double* __restrict__ H,
                                                     const double* __restrict__ theta_in, int n, int M, int Mp,
-                                                    int Mw, double* __restrict__ theta_out, uint64_t* counters) {
+                                                    int Mw, double* __restrict__ theta_out, uint64_t* counters,
+                                                    int i0 = 0) {
     const int lane = threadIdx.x & 31;
-    const int i = (int)(((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-    if (i >= n) return;
+    const int i = i0 + (int)(((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (i >= n) return;  // n: the end of this launch's node range
     if (M == 0) {
         if (lane == 0) theta_out[i] = theta_in[i];
         return;
@@ -881,12 +883,27 @@ __global__ void __launch_bounds__(256) theta_kernel(int kind, const uint32_t* __
     }
 }
 
+// theta pass (inc/reconstruct.hpp:129-138).  In a sharded job every rank optimises the
+// fields of its node range and the ranges are all-gathered: each theta_i
+// is a function of node i's row only, so the result is bitwise the single-GPU pass.
 void theta_pass(Context& c, double* out_only) {
     c.tic();
     double* out = out_only ? out_only : c.s_n.as<double>(c.n);
-    theta_kernel<<<(unsigned)ceil_div((int64_t)c.n * 32, 256), 256, 0, c.stream>>>(
-        c.kind, c.dXb(), c.dXd(), c.dH(), c.dtheta(), c.n, c.M, c.Mp, c.Mw, out, c.dcounters());
+    uint64_t lo = 0, hi = (uint64_t)c.n;
+    if (c.world > 1) shard_range((uint64_t)c.n, c.rank, c.world, lo, hi);
+    if (hi > lo)
+        theta_kernel<<<(unsigned)ceil_div((int64_t)(hi - lo) * 32, 256), 256, 0, c.stream>>>(
+            c.kind, c.dXb(), c.dXd(), c.dH(), c.dtheta(), (int)hi, c.M, c.Mp, c.Mw, out, c.dcounters(), (int)lo);
     NRG_LAUNCH_CHECK();
+    if (c.world > 1) {
+        std::vector<size_t> bytes(c.world);
+        for (int r = 0; r < c.world; ++r) {
+            uint64_t l, h;
+            shard_range((uint64_t)c.n, r, c.world, l, h);
+            bytes[r] = (h - l) * 8;
+        }
+        static_cast<Comm*>(c.comm)->allgatherv(out + lo, out, bytes, c.stream);
+    }
     if (!out_only) {
         NRG_CUDA(cudaMemcpyAsync(c.theta.p, out, (size_t)c.n * 8, cudaMemcpyDeviceToDevice, c.stream));
         c.state_version++;
