@@ -226,6 +226,12 @@ int nrg_sample_scored_pairs(nrg_ctx* ctx, uint64_t cap, uint64_t seed, int32_t* 
  * out as int8 (X_out, N x M). */
 int nrg_generate_ising(nrg_ctx* ctx, double mean_deg, double w_sigma, double th_sigma,
                        int32_t burn_in, int32_t thin, uint64_t seed, int8_t* X_out);
+/* The truth behind the last nrg_generate_* call of this context: n_edges edges (i < j)
+ * with couplings w (Ising) or precision off-diagonals (Gaussian), and per node the
+ * field theta (Ising) or the precision diagonal (Gaussian).  Call with cap = 0 for the
+ * count; copies min(cap, n_edges) edges and, if node_out is non-null, N node values. */
+int nrg_generated_truth(nrg_ctx* ctx, uint64_t cap, int32_t* ei, int32_t* ej, double* w, double* node_out,
+                        uint64_t* n_edges);
 /* Config 5 truth: erased configuration model, degrees P(d) ~ d^-gamma for d >= dmin
  * (capped at sqrt(N)); same Gibbs sampler and outputs as nrg_generate_ising. */
 int nrg_generate_ising_powerlaw(nrg_ctx* ctx, double gamma, int32_t dmin, double w_sigma, double th_sigma,

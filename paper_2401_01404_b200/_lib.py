@@ -91,6 +91,7 @@ SIGNATURES = {
     "nrg_kernel_stats": (C.c_int, [_P, _F64P, _i32]),
     "nrg_sample_scored_pairs": (C.c_int, [_P, _u64, _u64, _I32P, _I32P, C.POINTER(_u64)]),
     "nrg_generate_ising": (C.c_int, [_P, _d, _d, _d, _i32, _i32, _u64, _VP]),
+    "nrg_generated_truth": (C.c_int, [_P, _u64, _VP, _VP, _VP, _VP, C.POINTER(_u64)]),
     "nrg_generate_ising_powerlaw": (C.c_int, [_P, _d, _i32, _d, _d, _i32, _i32, _u64, _VP]),
     "nrg_generate_ising_graph": (C.c_int, [_P, _u64, _I32P, _I32P, _F64P, _F64P, _i32, _i32, _u64, _VP]),
     "nrg_generate_gaussian": (C.c_int, [_P, _i32, _d, _i32, _i32, _u64, _VP]),
@@ -262,6 +263,18 @@ class Model:
         check(self.L.nrg_generate_gaussian(self.h, degree, amp, burn_in, thin, seed,
                                            out.ctypes.data if out is not None else None))
         return out
+
+    def generated_truth(self):
+        """(ei, ej, w, node) of the last generate_* call: couplings and fields (Ising) or
+        precision off-diagonals and diagonal (Gaussian)."""
+        ne = _u64()
+        check(self.L.nrg_generated_truth(self.h, 0, None, None, None, None, C.byref(ne)))
+        k = ne.value
+        ei, ej, w, node = np.zeros(max(k, 1), np.int32), np.zeros(max(k, 1), np.int32), np.zeros(max(k, 1)), \
+            np.zeros(self.n)
+        check(self.L.nrg_generated_truth(self.h, k, ei.ctypes.data, ej.ctypes.data, w.ctypes.data, node.ctypes.data,
+                                         C.byref(ne)))
+        return ei[:k], ej[:k], w[:k], node
 
     def load_samples_file(self, path):
         check(self.L.nrg_load_samples_file(self.h, str(path).encode()))

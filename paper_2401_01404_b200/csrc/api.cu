@@ -538,6 +538,22 @@ int nrg_generate_ising(nrg_ctx* x, double mean_deg, double w_sigma, double th_si
     });
 }
 
+int nrg_generated_truth(nrg_ctx* x, uint64_t cap, int32_t* ei, int32_t* ej, double* w, double* node_out,
+                        uint64_t* n_edges) {
+    return guardx(x, [&] {
+        const nrg::Context& c = x->c;
+        if (c.truth_node.empty()) nrg::fail(NRG_EINVAL, "no generated data in this context");
+        const uint64_t ne = c.truth_i.size();
+        if (n_edges) *n_edges = ne;
+        for (uint64_t e = 0; e < std::min(cap, ne); ++e) {
+            ei[e] = c.truth_i[e];
+            ej[e] = c.truth_j[e];
+            w[e] = c.truth_w[e];
+        }
+        if (node_out) std::copy(c.truth_node.begin(), c.truth_node.end(), node_out);
+    });
+}
+
 int nrg_generate_ising_powerlaw(nrg_ctx* x, double gamma, int32_t dmin, double w_sigma, double th_sigma,
                                 int32_t burn_in, int32_t thin, uint64_t seed, int8_t* X_out) {
     return guardx(x, [&] {

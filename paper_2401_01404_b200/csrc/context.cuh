@@ -278,6 +278,10 @@ struct Context {
     // scorer-private scratch (score_entries only)
     DevBuf sc_surv, sc_g, sc_flag, sc_w32, sc_n, sc_rchk, sc_rn;
     std::vector<char> host_scratch;
+    // truth of the last device generator call (edges i < j, couplings / precision
+    // off-diagonals, fields / precision diagonal), for evaluation against the truth
+    std::vector<int32_t> truth_i, truth_j;
+    std::vector<double> truth_w, truth_node;
 
     // multi-GPU: node-sharded NNDescent + key-sharded distance cache (comm.cuh)
     void* comm = nullptr;  // nrg::Comm*

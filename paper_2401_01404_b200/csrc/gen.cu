@@ -198,6 +198,10 @@ static void gibbs_ising(Context& c, const std::vector<int32_t>& ea, const std::v
                         const std::vector<double>& ew, const std::vector<double>& th, int burn_in, int thin,
                         uint64_t seed) {
     const int n = c.n;
+    c.truth_i = ea;
+    c.truth_j = eb;
+    c.truth_w = ew;
+    c.truth_node = th;
     const ColoredGraph G = build_colored(n, ea, eb, ew);
     DevGraph D(c, G, th);
     int ncol = G.ncol;
@@ -357,6 +361,10 @@ static void gauss_chain(Context& c, const std::vector<int32_t>& ea, const std::v
                         const std::vector<double>& ew, const std::vector<double>& kd, int burn_in, int thin,
                         uint64_t seed) {
     const int n = c.n;
+    c.truth_i = ea;
+    c.truth_j = eb;
+    c.truth_w = ew;
+    c.truth_node = kd;
     const ColoredGraph G = build_colored(n, ea, eb, ew);
     DevGraph D(c, G, kd);
     DevBuf dxs, dbar;

@@ -36,6 +36,9 @@ def test_device_chain_equals_checker_chain(gpu, n, M, deg, burn, thin, seed):
     m = gpu.Model(n, M, gpu.NRG_ISING, 1.0)
     Xd = m.generate_ising(mean_deg=deg, burn_in=burn, thin=thin, seed=seed, want_samples=True)
     np.testing.assert_array_equal(Xd, Xc)
+    ti, tj, tw, tth = m.generated_truth()
+    for a, b in ((ti, tc["i"]), (tj, tc["j"]), (tw, tc["w"]), (tth, tc["theta"])):
+        np.testing.assert_array_equal(a, b)
     Xg = m.generate_ising_graph(tc["i"], tc["j"], tc["w"], tc["theta"], burn_in=burn, thin=thin, seed=seed + 1,
                                 want_samples=True)
     np.testing.assert_array_equal(Xg, O.gibbs_colored(tc["i"], tc["j"], tc["w"], tc["theta"], M, seed + 1,
