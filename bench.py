@@ -420,29 +420,38 @@ def run_ours(args, rank, world, local, dist):
     e2e_pairs, = allreduce(dist, [e2e_pairs], "sum")
     e2e_ms, = allreduce(dist, [e2e_ms], "max")
 
-    # roofline of the dominant kernel (K1 screen): algorithmic bytes = the partner column
-    # per screened pair in the first (4-bit) pass, which every pair takes: 4-bit field
-    # planes M/2 + packed spins M/8 (the stationary column is held in registers across a
-    # worklist run).  The 8-bit recheck pass of the pairs the 4-bit bound cannot settle is
-    # inside the timed span but its bytes are not counted (conservative).
+    # Roofline of the dominant kernel (K1, the pair screen: a 4-bit pass over every pair,
+    # an 8-bit recheck of the pairs it cannot settle), timed live on the library's stream
+    # (kernel_stats: CUDA events around every K1 launch of the timed sweeps).  Three views:
+    #   * HBM (the contract's bound): MEASURED DRAM bytes per pair of the committed ncu
+    #     capture (dram__bytes_read.sum + dram__bytes_write.sum over every K1 launch of a
+    #     steady sweep / its pairs) x this run's pairs per launch / the launch time;
+    #   * bytes model (partner column per pair): void for this kernel -- the
+    #     4-bit planes are M/2 + M/8 = 625 B per pair and partner rows recur across
+    #     worklist runs (L1/L2 hits), so the "achieved" model bandwidth exceeds HBM;
+    #   * issue: executed warp instructions per pair (ncu smsp__inst_executed.sum over the
+    #     same launches / pairs) x pairs per launch / time, against 148 SMs x 4 schedulers
+    #     x 1 warp instruction per clock at the run's SM clock -- the binding resource.
     peak, peak_kind = measured_peaks()
-    bytes_per_pair = M / 2 + M / 8
     k1_ms_avg = kst["k1_ms"] / max(1.0, kst["k1_launches"])
     k1_pairs_avg = kst["k1_pairs"] / max(1.0, kst["k1_launches"])
-    achieved = (k1_pairs_avg * bytes_per_pair) / (k1_ms_avg / 1e3) / 1e9 if k1_ms_avg > 0 else 0.0
-
-    # DRAM traffic per K1 launch: the per-pair bytes of the committed ncu --set full
-    # capture (dram__bytes_read.sum + dram__bytes_write.sum of one launch / its pairs)
-    # times this run's pairs per launch
-    traffic = None
-    dram_per_pair = None
-    tf = ROOT / "profiles" / "r01_k1_traffic.json"
-    if tf.exists():
-        try:
-            dram_per_pair = json.loads(tf.read_text())["dram_bytes_per_pair"]
-            traffic = dram_per_pair * k1_pairs_avg
-        except Exception:
-            traffic = None
+    model_bytes = M / 2 + M / 8
+    model_gbs = (k1_pairs_avg * model_bytes) / (k1_ms_avg / 1e3) / 1e9 if k1_ms_avg > 0 else 0.0
+    cnt_file = ROOT / "profiles" / "r02" / "k1_counters.json"
+    kc = json.loads(cnt_file.read_text()) if cnt_file.exists() else {}
+    dram_per_pair = kc.get("dram_bytes_per_pair")
+    inst_per_pair = kc.get("inst_per_pair")
+    traffic = dram_per_pair * k1_pairs_avg if dram_per_pair else None
+    dram_gbs = traffic / (k1_ms_avg / 1e3) / 1e9 if traffic and k1_ms_avg > 0 else 0.0
+    clk = clk.summary() if hasattr(clk, "summary") else clk
+    sm_hz = (clk.get("sm_mhz") or 1965.0) * 1e6
+    issue = None
+    if inst_per_pair and k1_ms_avg > 0:
+        ach = inst_per_pair * k1_pairs_avg / (k1_ms_avg / 1e3)
+        pk = 148 * 4 * sm_hz
+        issue = {"inst_per_pair": inst_per_pair, "achieved_winst_per_s": ach, "peak_winst_per_s": pk,
+                 "frac": ach / pk, "peak": "148 SMs x 4 warp schedulers x 1 warp instruction/clk at the run's SM "
+                                           "clock", "source": kc.get("capture")}
     line = {
         "metric": "scored candidate pairs/sec and wall-time per GCD sweep (N=1e5, M=1e3)",
         "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -465,23 +474,22 @@ def run_ours(args, rank, world, local, dist):
                   "warmup_sweeps_ms": [round(x, 1) for x in warm_ms],
                   "edges_at_start": int(len(ei_w)), "objective": [float(r["objective"]) for r in recs],
                   "tail_rounds": kst.get("tail_rounds")},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "traffic_unit": "bytes per launch",
-                     "traffic_source": "profiles/r01_k1_traffic.json",
+        "roofline": {"bound": "hbm", "achieved": dram_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": dram_gbs / peak, "traffic": traffic, "traffic_unit": "bytes per launch",
+                     "traffic_source": kc.get("capture"),
                      "kernel": "ising_screen_pipe_kernel (K1, the pair screen: 4-bit pass + 8-bit recheck pass)",
-                     "bytes_per_unit": bytes_per_pair, "units_per_launch": k1_pairs_avg,
-                     "ms_per_launch": k1_ms_avg, "peak_kind": peak_kind,
-                     "dram_gbs": (traffic / (k1_ms_avg / 1e3) / 1e9) if traffic and k1_ms_avg > 0 else None,
-                     "note": "achieved counts the partner row each pair needs (M/2 + M/8 bytes); partner rows recur "
-                             "within and across worklist runs, so L1/L2 serve most of them (DRAM traffic per pair: "
-                             f"{dram_per_pair:.0f} B, profiles/r01_k1_traffic.json) and achieved can pass the HBM "
-                             "peak; the kernel is issue-bound (profiles/r01_kernels/k1_4bit.txt)" if dram_per_pair
-                             else None},
+                     "bytes_per_unit": dram_per_pair, "bytes_per_unit_kind": "measured DRAM bytes per scored pair",
+                     "units_per_launch": k1_pairs_avg, "ms_per_launch": k1_ms_avg, "peak_kind": peak_kind,
+                     "bytes_model": {"bytes_per_pair": model_bytes, "achieved_gbs": model_gbs,
+                                     "frac": model_gbs / peak,
+                                     "status": "void: 4-bit planes + L1/L2 reuse of partner rows (model bytes "
+                                               "exceed what HBM could stream)"},
+                     "issue": issue, "binding": "instruction issue" if issue else None},
         "e2e": {"value": e2e_pairs / (e2e_ms / 1e3), "unit": "pairs/s", "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps, "ms_per_step": e2e_ms / args.steps,
                 "step": "upload bit-packed samples + state S_W, sweep W, download candidates + state"},
         "gpu_launches": int(kst["launches"]),
-        "clocks": clk.summary(),
+        "clocks": clk,
     }
     parity_ok = True
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -332,7 +332,17 @@ struct Context {
             return static_cast<T*>(p);
         }
     };
-    PinBuf hp_dep, hp_ord, hp_i, hp_j, hp_ch, hp_pairs;
+    PinBuf hp_dep, hp_ord, hp_i, hp_j, hp_ch, hp_pairs, hp_small;
+
+    // one device scalar read back through pinned memory (a DMA straight into the
+    // host buffer; a pageable destination is staged by the driver)
+    template <class T>
+    T read_scalar(const T* d) {
+        T* h = hp_small.as<T>(1);
+        NRG_CUDA(cudaMemcpyAsync(h, d, sizeof(T), cudaMemcpyDeviceToHost, stream));
+        sync();
+        return *h;
+    }
 
     // side stream for work whose result is needed only later (the dense root's miss
     // recount): fork() orders it after everything queued so far; join_side() makes the

@@ -238,18 +238,22 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         unsigned long long at = 0;
         if (lane == 31 && tot) at = atomicAdd(out.ns, (unsigned long long)tot);
         at = __shfl_sync(0xffffffffu, at, 31) + (unsigned long long)(incl - cnt);
-        for (uint32_t m = surv_mask; m; m &= m - 1) {
-            const int u = __ffs(m) - 1;
-            if (at < out.cap) {
-                const float g = gv[u];
-                out.si[at] = i;
-                out.sj[at] = J * kBN + c0 + u;
-                out.sg[at] = g;
-                const float2 qj = qcol[c0 + u];
-                const float err = (qi.y + qj.y) * 1.0001f + err0;
-                out.sf[at] = fabsf(g) < lam + err ? 1 : 0;
+        // unrolled over the 16 columns with compile-time indices: gv stays in registers
+        // (a loop over the set bits indexed it dynamically and spilled it to local memory)
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            if ((surv_mask >> u) & 1u) {
+                if (at < out.cap) {
+                    const float g = gv[u];
+                    out.si[at] = i;
+                    out.sj[at] = J * kBN + c0 + u;
+                    out.sg[at] = g;
+                    const float2 qj = qcol[c0 + u];
+                    const float err = (qi.y + qj.y) * 1.0001f + err0;
+                    out.sf[at] = fabsf(g) < lam + err ? 1 : 0;
+                }
+                ++at;
             }
-            ++at;
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -481,8 +485,7 @@ bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* di
                                                                           base, out);
     NRG_LAUNCH_CHECK();
     unsigned long long ns = 0;
-    NRG_CUDA(cudaMemcpyAsync(&ns, out.ns, 8, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
+    ns = c.read_scalar(out.ns);
     if (ns > cap) {
         c.toc(P_SCORE);
         return false;  // more survivors than reserved: the CUDA-core path scores them
@@ -506,8 +509,7 @@ bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* di
                                                                           idx, out.sg, out.sf, out.ns, wl);
     NRG_LAUNCH_CHECK();
     unsigned long long nw = 0;
-    NRG_CUDA(cudaMemcpyAsync(&nw, out.ns, 8, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
+    nw = c.read_scalar(out.ns);
     c.toc(P_SCORE);
     if (lazy) {
         // survivors stay in the triangle as markers; the worklist moves to the Context

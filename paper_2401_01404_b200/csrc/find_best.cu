@@ -457,8 +457,7 @@ static uint64_t merge_select(Context& c, TriKey* buf, uint64_t n, uint64_t want,
         pair_dedup(c, buf, n, uniq, cnt, tabb);
     }
     if (n) {
-        NRG_CUDA(cudaMemcpyAsync(&nu, cnt, 8, cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
+        nu = c.read_scalar(cnt);
     }
     if (!sorted) {
         outb = std::move(ub);
@@ -553,8 +552,7 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
     double t0 = 0.0, s0 = 0.0, k20 = 0.0;
     if (dbg) {
         c.flush_timing();
-        NRG_CUDA(cudaMemcpyAsync(&m0, c.dcounters() + C_MISSES, 8, cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
+        m0 = c.read_scalar(c.dcounters() + C_MISSES);
         t0 = c.phase_ms[P_KNN];
         s0 = c.phase_ms[P_SCORE];
         k20 = c.k2_pairs;
@@ -563,8 +561,7 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
     if (dbg) {
         uint64_t m1 = 0;
         c.flush_timing();
-        NRG_CUDA(cudaMemcpyAsync(&m1, c.dcounters() + C_MISSES, 8, cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
+        m1 = c.read_scalar(c.dcounters() + C_MISSES);
         fprintf(stderr, "level %d: n=%llu k=%d sweeps=%d knn_ms=%.2f score_ms=%.2f unique_pairs=%llu survivors=%.0f\n",
                 level, (unsigned long long)n, k, knn.sweeps, c.phase_ms[P_KNN] - t0, c.phase_ms[P_SCORE] - s0,
                 (unsigned long long)(m1 - m0), c.k2_pairs - k20);
@@ -620,9 +617,8 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
     }
     unsigned long long nD = 0;
     int hsat = 0;
-    NRG_CUDA(cudaMemcpyAsync(&nD, cnt, 8, cudaMemcpyDeviceToHost, c.stream));
-    NRG_CUDA(cudaMemcpyAsync(&hsat, nsat, 4, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
+    nD = c.read_scalar(cnt);
+    hsat = c.read_scalar(nsat);
     c.toc(P_SELECT);
     trace.push_back({level, k, 0, knn.sweeps, n, (uint64_t)nD});
     kid.release();
@@ -678,8 +674,7 @@ void find_best(Context& c, int mode, uint64_t m, const int32_t* d_nodes, uint64_
         ascending_check_kernel<<<g256(n), 256, 0, c.stream>>>(d_nodes, n, c.n, ok);
         NRG_LAUNCH_CHECK();
         int hbad = 0;
-        NRG_CUDA(cudaMemcpyAsync(&hbad, ok, 4, cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
+        hbad = c.read_scalar(ok);
         cnt = find_best_impl(c, mode, m, d_nodes, n, knn_eps, seed, reverse, 0, res.trace, result, hbad == 0, true);
     }
     res.count = cnt;

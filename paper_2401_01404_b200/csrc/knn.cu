@@ -1202,8 +1202,7 @@ static void exchange_and_score(Context& c, int mode, const ClaimSink& sink, uint
     const int W = c.world, me = c.rank;
     unsigned long long R = 0;
     if (W > 1) {
-        NRG_CUDA(cudaMemcpyAsync(&R, sink.rcount, 8, cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
+        R = c.read_scalar(sink.rcount);
     }
     (void)reserve_hint;
     if (W == 1) {
@@ -1259,8 +1258,7 @@ static void exchange_and_score(Context& c, int mode, const ClaimSink& sink, uint
         NRG_CUDA(cudaMemsetAsync(s2.wcount, 0, 8, c.stream));
         claim_keys_kernel<<<(unsigned)ceil_div(Q, 256), 256, 0, c.stream>>>(c.Cview(), s2, sk, si, Q, slot_of);
         NRG_LAUNCH_CHECK_N(2);
-        NRG_CUDA(cudaMemcpyAsync(&nw2, s2.wcount, 8, cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
+        nw2 = c.read_scalar(s2.wcount);
     }
     score_claimed(c, mode, sink.ws, sink.wp, sink.wslot, nw_local);
     score_claimed(c, mode, ws2, wp2, wsl2, nw2);
@@ -1348,8 +1346,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         }
         sorted_ids = sids;
         int hbad = 0;
-        NRG_CUDA(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
+        hbad = c.read_scalar(bad);
         if (hbad == 1) fail(34, "node id out of range");
         if (hbad == 2) fail(22, "find_knn: duplicate node ids");
     }
@@ -1467,8 +1464,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                 score_entries(c, mode, ws, wp, nq + 1, so, wcount);
             } else {
                 unsigned long long nw = 0;
-                NRG_CUDA(cudaMemcpyAsync(&nw, wcount, 8, cudaMemcpyDeviceToHost, c.stream));
-                c.sync();
+                nw = c.read_scalar(wcount);
                 exchange_and_score(c, mode, sk, nw, X, 0);
             }
             if (dense) dense_resolve_slots(c, slot, nq);  // refine the marked pairs first
@@ -1664,8 +1660,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                 NRG_LAUNCH_CHECK();
             }
             uint64_t total = 0;
-            NRG_CUDA(cudaMemcpyAsync(&total, tot, 8, cudaMemcpyDeviceToHost, c.stream));
-            c.sync();
+            total = c.read_scalar(tot);
             if (c.world > 1) static_cast<Comm*>(c.comm)->allreduce_u64(&total, 1, false, c.stream);
             c.toc(P_KNN);
             cache_reserve(c, total);
@@ -1693,8 +1688,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             so.slot = wsl;
             score_entries(c, mode, ws, wp, own * capn + 1, so, wcount);
         } else if (!dense) {
-            NRG_CUDA(cudaMemcpyAsync(&nw, wcount, 8, cudaMemcpyDeviceToHost, c.stream));
-            c.sync();
+            nw = c.read_scalar(wcount);
         }
         if (cached && !dense && c.world > 1) {
             exchange_and_score(c, mode, sk, nw, X, 0);
@@ -1722,8 +1716,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             NRG_LAUNCH_CHECK();
         }
         unsigned long long changed = 0;
-        NRG_CUDA(cudaMemcpyAsync(&changed, churn, 8, cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
+        changed = c.read_scalar(churn);
         allgather_rows(gid, gd, kw);
         if (c.world > 1) {
             uint64_t ch = changed;

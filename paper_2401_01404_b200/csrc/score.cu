@@ -930,8 +930,7 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
                                      (c.kind == GAUSSIAN && c.Mp <= 1024 && !NRG_ENV_ON("NRG_NO_GAUSS_SCREEN"))))) {
         // only the screen takes a device-side count: settle it here for the other paths
         unsigned long long h = 0;
-        NRG_CUDA(cudaMemcpyAsync(&h, n_dev, 8, cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
+        h = c.read_scalar(n_dev);
         n = std::min<uint64_t>(n, h);
         n_dev = nullptr;
         if (n == 0) return;
@@ -1219,8 +1218,7 @@ void distance_batch(Context& c, int mode, const int32_t* qi, const int32_t* qj, 
         c.Cview(), qi, qj, n, slot, ws, wp, wslot, wcount, c.dcounters(), static_cast<uint64_t*>(c.Ccount.p));
     NRG_LAUNCH_CHECK();
     unsigned long long nw = 0;
-    NRG_CUDA(cudaMemcpyAsync(&nw, wcount, 8, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
+    nw = c.read_scalar(wcount);
     ScoreOut out;
     out.cache_vals = c.Cview().vals;
     out.slot = wslot;
@@ -1248,8 +1246,7 @@ __global__ void sample_keys_kernel(const uint64_t* __restrict__ keys, uint64_t c
 uint64_t sample_scored_pairs(Context& c, uint64_t cap, uint64_t seed, int32_t* oi, int32_t* oj) {
     if (!c.Ccap || !cap) return 0;
     uint64_t live = 0;
-    NRG_CUDA(cudaMemcpyAsync(&live, c.Ccount.p, 8, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
+    live = c.read_scalar(static_cast<const uint64_t*>(c.Ccount.p));
     const uint64_t stride = std::max<uint64_t>(1, live / cap);
     unsigned long long* cnt = c.s_g.as<unsigned long long>(1);
     NRG_CUDA(cudaMemsetAsync(cnt, 0, 8, c.stream));
@@ -1257,8 +1254,7 @@ uint64_t sample_scored_pairs(Context& c, uint64_t cap, uint64_t seed, int32_t* o
         static_cast<uint64_t*>(c.Ckeys.p), c.Ccap, stride, seed, cap, oi, oj, cnt);
     NRG_LAUNCH_CHECK();
     unsigned long long h = 0;
-    NRG_CUDA(cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
+    h = c.read_scalar(cnt);
     return std::min<uint64_t>(h, cap);
 }
 

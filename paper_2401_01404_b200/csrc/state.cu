@@ -252,8 +252,7 @@ void upload_samples_f64(Context& c, const double* X) {
         NRG_LAUNCH_CHECK();
     }
     int hbad = 0;
-    NRG_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
+    hbad = c.read_scalar(bad);
     if (hbad) {
         c.have_samples = false;
         fail(22, c.kind == ISING ? "ising model requires +/-1 data" : "gaussian samples must be finite");
@@ -279,8 +278,7 @@ void upload_spins_i8(Context& c, const int8_t* X) {
     }
     reset_state(c);
     int hbad = 0;
-    NRG_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
+    hbad = c.read_scalar(bad);
     if (hbad) {
         c.have_samples = false;
         fail(22, "ising model requires +/-1 data");
@@ -387,8 +385,7 @@ void get_state(Context& c, double* theta, uint64_t cap, int32_t* ei, int32_t* ej
         static_cast<const uint64_t*>(c.Wkeys.p), static_cast<const double*>(c.Wvals.p), c.Wcap, ib, k0, v0, cnt);
     NRG_LAUNCH_CHECK();
     unsigned long long ne = 0;
-    NRG_CUDA(cudaMemcpyAsync(&ne, cnt, 8, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
+    ne = c.read_scalar(cnt);
     *n_edges = ne;
     const uint64_t take = std::min<uint64_t>(ne, cap);
     if (!take || !(ei || ej || w)) return;
@@ -857,8 +854,7 @@ void cache_reserve(Context& c, uint64_t extra) {
     }
     uint64_t live = 0;
     if (c.Ccap) {
-        NRG_CUDA(cudaMemcpyAsync(&live, c.Ccount.p, 8, cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
+        live = c.read_scalar(static_cast<const uint64_t*>(c.Ccount.p));
     }
     c.cache_live_host = live;
     // load factor <= 0.6; slot indices are 31-bit (bit 31 flags remote slots), so at the
@@ -906,9 +902,8 @@ void begin_generation(Context& c) {
         // size the (now empty) memo for the previous generation's pairs + 30%: growing
         // here costs an allocation, growing mid-generation a rehash of every entry
         uint64_t live = 0, k2max = ~0ull;
-        NRG_CUDA(cudaMemcpyAsync(&live, c.Ccount.p, 8, cudaMemcpyDeviceToHost, c.stream));
-        if (c.k2max.p) NRG_CUDA(cudaMemcpyAsync(&k2max, c.k2max.p, 8, cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
+        live = c.read_scalar(static_cast<const uint64_t*>(c.Ccount.p));
+        if (c.k2max.p) k2max = c.read_scalar(static_cast<const uint64_t*>(c.k2max.p));
         // the next generation launches the warp kernel too only if this one needed it
         // (3 x 148 x 32 x 4: CTA-mode capacity with room; a wrong guess costs time only)
         c.k2_wide = k2max > 3ull * 148 * 32 * 4 / 2;

@@ -343,8 +343,7 @@ bool set_edges_bulk(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n
     dup_flag_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(canon2, n, dup);
     NRG_LAUNCH_CHECK();
     int hdup = 0;
-    NRG_CUDA(cudaMemcpyAsync(&hdup, dup, 4, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
+    hdup = c.read_scalar(dup);
     if (hdup) return false;  // a pair listed twice: its second Delta depends on the first
     c.tic();
     w_reserve(c, n);
@@ -601,8 +600,7 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
         tail_start_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(dist, n, dk);
         NRG_LAUNCH_CHECK();
         unsigned long long hk = 0;
-        NRG_CUDA(cudaMemcpyAsync(&hk, dk, 8, cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
+        hk = c.read_scalar(dk);
         if (n - hk >= kTailMin) k = hk;
     }
     // a FindBest list (sorted by distance, flagged by gcd_iteration) is already a
@@ -650,8 +648,7 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
                                                                                           rows_dev, cnt);
                     NRG_LAUNCH_CHECK();
                     unsigned long long h = 0;
-                    NRG_CUDA(cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, c.stream));
-                    c.sync();
+                    h = c.read_scalar(cnt);
                     nr = h;
                 }
                 snapshot_rows(c, rows_dev, nr);
@@ -730,8 +727,7 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
     sum_fixed_kernel<<<1, 1024, 0, c.stream>>>(absdelta, n, sum);
     NRG_LAUNCH_CHECK();
     double h = 0.0;
-    NRG_CUDA(cudaMemcpyAsync(&h, sum, 8, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
+    h = c.read_scalar(sum);
     c.toc(P_UPDATE);
     c.state_version++;
     return h;
