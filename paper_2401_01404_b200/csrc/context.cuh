@@ -226,7 +226,7 @@ struct Context {
     bool dense_active = false;
     uint64_t dense_n = 0;
     DevBuf dtri, dloc, dbits;
-    DevBuf kx_cid, kx_csl, kx_ws, kx_wp, kx_wsl;  // find_knn candidate / worklist scratch
+    DevBuf kx_cid, kx_csl, kx_ws, kx_wp, kx_wsl, kx_wd;  // find_knn candidate / worklist scratch
     // Lazy K2 at the dense root: the screen's survivors (the pairs K2 must refine) sit in
     // the triangle as NaN-boxed indices into this worklist and are refined only when a
     // dense level first probes them (dense_resolve_*, exhaustive_tc.cu).

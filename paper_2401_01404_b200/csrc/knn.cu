@@ -223,6 +223,10 @@ struct ClaimSink {
     // (fold_claims_kernel) and hits once per warp at kernel end, instead of three hot
     // global atomics per warp and chunk
     bool fold = false;
+    // wl_slots (single rank): a candidate this node claims gets slot kRemote | worklist
+    // index, so the merge reads its distance from the worklist-ordered array the screen
+    // writes alongside the memo (mostly contiguous), not from a random memo slot
+    bool wl_slots = false;
 };
 
 __global__ void fold_claims_kernel(const unsigned long long* __restrict__ wcount, uint64_t* __restrict__ counters,
@@ -300,6 +304,7 @@ __device__ __forceinline__ uint32_t claim_warp(HashView h, const ClaimSink& sink
         sink.ws[at] = gs;
         sink.wp[at] = gp;
         sink.wslot[at] = (uint32_t)sl;
+        if (sink.wl_slots) sl = kRemote | (uint32_t)at;
     }
     if (lane == 0 && h.keys) {
         if (ball && !sink.fold) {
@@ -1625,7 +1630,12 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         c.tic();
         NRG_CUDA(cudaMemsetAsync(wcount, 0, 16, c.stream));
         NRG_CUDA(cudaMemsetAsync(churn, 0, 8, c.stream));
-        const ClaimSink sk = sink_for(ws, wp, wsl, own * capn + 1);
+        ClaimSink sk = sink_for(ws, wp, wsl, own * capn + 1);
+        // own claims resolve through the worklist-ordered distances (single rank, a memo
+        // and worklist small enough for 31-bit indices)
+        const bool wl = W == 1 && cached && !dense && wmax < (uint64_t)kRemote && !NRG_ENV_ON("NRG_NO_WL_SLOTS");
+        double* wdist = wl ? c.kx_wd.as<double>(wmax) : nullptr;
+        sk.wl_slots = wl;
         if (own) {
             int lw = 0;
             while ((1 << lw) < cap) ++lw;
@@ -1686,6 +1696,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             ScoreOut so;
             so.cache_vals = c.Cview().vals;
             so.slot = wsl;
+            so.dist = wdist;  // the worklist-ordered copy the merge reads (wl slots)
             score_entries(c, mode, ws, wp, own * capn + 1, so, wcount);
         } else if (!dense) {
             nw = c.read_scalar(wcount);
@@ -1700,7 +1711,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         }
         if (dense) dense_resolve_rows(c, cand_slot, cand_cnt, lo, own, capn);  // refine the marked pairs first
         const double* dvals = dense ? dtri : cached ? c.Cview().vals : flat_d;
-        const double* rvals = static_cast<double*>(X.rvals.p);
+        const double* rvals = wl ? wdist : static_cast<double*>(X.rvals.p);
         c.tic();
         if (own) {
             if (kw > 64)
