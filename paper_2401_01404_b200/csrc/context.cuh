@@ -332,7 +332,7 @@ struct Context {
             return static_cast<T*>(p);
         }
     };
-    PinBuf hp_dep, hp_ord, hp_i, hp_j, hp_ch, hp_pairs, hp_small;
+    PinBuf hp_dep, hp_ord, hp_i, hp_j, hp_ch, hp_pairs, hp_small, hp_apply;
 
     // one device scalar read back through pinned memory (a DMA straight into the
     // host buffer; a pageable destination is staged by the driver)

@@ -815,36 +815,15 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
         // dense level: slots in the root's distance triangle, probes marked and counted here
         uint32_t* my_slot = cand_slot + li * capn;
         const uint64_t ra = (uint64_t)rootpos[li];
-        // candidates in batches of 4: their root-position loads are in flight together
-        // (one at a time, each probe waited a full memory latency on rootpos[v])
-        int pv[4], np = 0;
-        auto flush = [&](int cnt4) {
-            int rp[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) rp[k] = k < cnt4 ? __ldg(&rootpos[pv[k]]) : 0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (k < cnt4) {
-                    my_ids[off] = pv[k];
-                    my_slot[off++] = dense_probe(sink.dbits, sink.dn, ra, (uint64_t)rp[k]);
-                }
-        };
 #pragma unroll
         for (int q = 0; q < kMaxWpt; ++q) {
             const int w = tid * kMaxWpt + q;
             for (uint32_t m = cw[q]; m; m &= m - 1) {
                 const int v = 32 * w + __ffs(m) - 1;
-                if (np == 0) pv[0] = v;
-                else if (np == 1) pv[1] = v;
-                else if (np == 2) pv[2] = v;
-                else pv[3] = v;
-                if (++np == 4) {
-                    flush(4);
-                    np = 0;
-                }
+                my_ids[off] = v;
+                my_slot[off++] = dense_probe(sink.dbits, sink.dn, ra, (uint64_t)rootpos[v]);
             }
         }
-        if (np) flush(np);
         const int probes = warp_sum(cnt);
         if ((tid & 31) == 0 && probes)
             atomicAdd((unsigned long long*)&sink.counters[C_HITS], (unsigned long long)probes);

@@ -489,13 +489,17 @@ __global__ void __launch_bounds__(256) snapshot_ising_kernel(const double* __res
     }
     __syncthreads();
     const double d = (double)s_d, d4 = (double)s_d4;
+    // quantisation by the reciprocal (two fp64 divisions per sample were the kernel's
+    // longest dependency); the error sums below use the levels actually chosen, so the
+    // screen's bounds stay rigorous whichever way a boundary case rounds
+    const double rd = 1.0 / d, rd4 = 1.0 / d4;
     const int Mw = Mp >> 5;
     double e = 0.0, e4 = 0.0;
     int sum = 0, sum4 = 0, npl = 0;  // npl: samples with x = +1 (the 4-bit screen's offset term)
     auto quant = [&](int w, double t) {
         if (lane == 0 && Xb) npl += __popc(Xb[(size_t)r * Mw + w]);
         const int m = 32 * w + lane;
-        int v = (int)rint(t / d);
+        int v = (int)rint(t * rd);
         v = max(-127, min(127, v));
         e += fabs(t - d * (double)v);
         sum += v;
@@ -509,7 +513,7 @@ __global__ void __launch_bounds__(256) snapshot_ising_kernel(const double* __res
         if (lane < 8) P8[((size_t)r * Mw + w) * 8 + lane] = mine;
         if (P4) {
             // the 4-bit field of the first-pass screen: T4 = round(T / d4), |T4| <= 7
-            int v4 = (int)rint(t / d4);
+            int v4 = (int)rint(t * rd4);
             v4 = max(-7, min(7, v4));
             e4 += fabs(t - d4 * (double)v4);
             sum4 += v4;

@@ -705,7 +705,9 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
                 int32_t* pi = pib.as<int32_t>(na);
                 int32_t* pj = pjb.as<int32_t>(na);
                 double* dd = ddb.as<double>(na);
-                NRG_CUDA(cudaMemcpyAsync(di, apply.data(), na * 4, cudaMemcpyHostToDevice, c.stream));
+                uint32_t* hap = c.hp_apply.as<uint32_t>(na);  // pinned: the copy is a DMA, not a staged one
+                std::copy(apply.begin(), apply.end(), hap);
+                NRG_CUDA(cudaMemcpyAsync(di, hap, na * 4, cudaMemcpyHostToDevice, c.stream));
                 gather_pairs_kernel<<<ceil_div(na, 256), 256, 0, c.stream>>>(ci, cj, di, na, pi, pj);
                 NRG_LAUNCH_CHECK();
                 ordered_run(c, pi, pj, na, nullptr, dd);
