@@ -47,10 +47,12 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 CONFIGS = {
-    # name: (N, M, mean degree)
-    "config4": (100_000, 1000, 5.0),
-    "config2": (10_000, 1000, 4.0),
-    "config1": (1000, 500, 4.0),
+    # name: (N, M, mean degree / degree, generator) -- BASELINE.json configs
+    "config4": (100_000, 1000, 5.0, "er"),        # the headline (metric) configuration
+    "config2": (10_000, 1000, 4.0, "er"),
+    "config1": (1000, 500, 4.0, "er"),
+    "config3": (10_000, 1000, 4, "gauss"),         # Gaussian, 4-regular precision, U(-0.2, 0.2)
+    "config5": (1_000_000, 200, 2.5, "powerlaw"),  # power-law configuration model (gamma 2.5, dmin 2)
 }
 
 
@@ -190,13 +192,13 @@ class RefScorer:
     unmodified): PseudoLikelihood + DistanceCache at a given state; distance() and
     optimize_edge() under the reference's parallel_for over all host threads."""
 
-    def __init__(self, X_f64, lam, state=None, threads=None):
+    def __init__(self, X_f64, lam, state=None, threads=None, kind=0):
         sys.path.insert(0, str(ROOT / "tests"))
         import oracle_lib as O
         self.which = "ref" if O.available("ref") else "orc"
         self.L = O.lib(self.which)
         self.threads = (threads or os.cpu_count() or 1) if self.which == "ref" else 1
-        self.m = O.CpuModel(self.which, X_f64, 0, lam)
+        self.m = O.CpuModel(self.which, X_f64, kind, lam)
         if state is not None:
             th, ei, ej, w = state
             self.m.set_theta(th)
@@ -264,8 +266,13 @@ def run_reference(args, rank, world, dist):
     `bench.py --write-sample`, checked against the data by digest)."""
     if rank != 0:
         return
-    N, M, md = CONFIGS[args.config] if not args.n else (args.n, args.m, args.mean_deg)
+    N, M, md, gen = CONFIGS[args.config] if not args.n else (args.n, args.m, args.mean_deg, "er")
     lam = ising_lambda(N, M)
+    if gen != "er":
+        print(json.dumps({"impl": "reference", "unavailable": f"the reference arm regenerates the device data with "
+                          f"the C restatement of the ER chain; {args.config} ({gen}) is measured only through the "
+                          f"device arm's cpu_baseline"}), flush=True)
+        return
     sys.path.insert(0, str(ROOT / "tests"))
     import oracle_lib as O
     t0 = time.perf_counter()
@@ -353,24 +360,42 @@ def run_ours(args, rank, world, local, dist):
     import torch
     import paper_2401_01404_b200 as P
 
-    N, M, md = CONFIGS[args.config] if not args.n else (args.n, args.m, args.mean_deg)
-    lam = ising_lambda(N, M)
+    N, M, md, gen = CONFIGS[args.config] if not args.n else (args.n, args.m, args.mean_deg, "er")
+    gauss = gen == "gauss"
     kappa = 2.0
-    model = P.Model(N, M, P.NRG_ISING, lam, device=local)
+    t0 = time.perf_counter()
+    if gauss:
+        # config 3: lambda = 2 sqrt(M ln N) x the mean sample variance; the
+        # data come first (a lambda-free context), then the scoring context
+        g = P.Model(N, M, P.NRG_GAUSSIAN, 0.0, device=local)
+        Xh = g.generate_gaussian(degree=int(md), amp=0.2, burn_in=args.burn_in, thin=10, seed=args.seed,
+                                 want_samples=True)
+        g.close()
+        lam = ising_lambda(N, M) * float(Xh.var(axis=1).mean())
+        model = P.Model(N, M, P.NRG_GAUSSIAN, lam, device=local)
+        model.upload_samples(Xh)
+    else:
+        lam = ising_lambda(N, M)
+        model = P.Model(N, M, P.NRG_ISING, lam, device=local)
     if world > 1:
         # one sharded job over all ranks: NCCL communicator of the library, id via torch
         obj = [P._lib.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         model.comm_init(obj[0], rank, world)
-    t0 = time.perf_counter()
     # identical (replicated) samples on every rank: the path shards nodes, not data
-    Xh = model.generate_ising(mean_deg=md, w_sigma=0.3, th_sigma=0.1, burn_in=args.burn_in, thin=10,
-                              seed=args.seed, want_samples=True)
+    if gen == "er":
+        Xh = model.generate_ising(mean_deg=md, w_sigma=0.3, th_sigma=0.1, burn_in=args.burn_in, thin=10,
+                                  seed=args.seed, want_samples=True)
+    elif gen == "powerlaw":
+        Xh = model.generate_ising_powerlaw(gamma=md, dmin=2, w_sigma=0.2, th_sigma=0.1, burn_in=args.burn_in,
+                                           thin=10, seed=args.seed, want_samples=True)
     gen_s = time.perf_counter() - t0
-    # the e2e step's host input: the samples in the library's bit-packed row layout (the
-    # Ising sample-file format, 1 bit per spin) in pinned memory
-    pinned = torch.from_numpy(np.packbits(Xh > 0, axis=1, bitorder="little")).pin_memory()
-    Xpin = pinned.numpy()
+    # the e2e step's host input in pinned memory: Ising samples in the library's
+    # bit-packed row layout (the sample-file format, 1 bit per spin); Gaussian as f64
+    if gauss:
+        Xpin = torch.from_numpy(np.ascontiguousarray(Xh)).pin_memory().numpy()
+    else:
+        Xpin = torch.from_numpy(np.packbits(Xh > 0, axis=1, bitorder="little")).pin_memory().numpy()
 
     # One reconstruction (inc/reconstruct.hpp:162-179 loop): `warmup` sweeps from the
     # empty state, then `steps` timed consecutive sweeps of the same reconstruction.
@@ -408,7 +433,10 @@ def run_ours(args, rank, world, local, dist):
     h2d = d2h = 0
     model.timer_start()
     for s in range(args.steps):
-        model.upload_spins_packed(Xpin)
+        if gauss:
+            model.upload_samples(Xpin)
+        else:
+            model.upload_spins_packed(Xpin)
         model.set_theta(th_w)
         model.set_edges(ei_w, ej_w, w_w)
         rec, cands = model.gcd_iteration(args.warmup, kappa=kappa, seed=args.seed, want_candidates=True)
@@ -435,10 +463,14 @@ def run_ours(args, rank, world, local, dist):
     peak, peak_kind = measured_peaks()
     k1_ms_avg = kst["k1_ms"] / max(1.0, kst["k1_launches"])
     k1_pairs_avg = kst["k1_pairs"] / max(1.0, kst["k1_launches"])
-    model_bytes = M / 2 + M / 8
+    # the screen's streamed partner data per pair: Ising 4-bit planes + spin bits; Gaussian
+    # fp32 u and x rows (gauss_screen_kernel: 8 M bytes)
+    model_bytes = 8 * M if gauss else M / 2 + M / 8
+    desc = {"er": f"Ising ER mean_deg={md}", "powerlaw": f"Ising power-law gamma={md} dmin=2",
+            "gauss": f"Gaussian {int(md)}-regular precision U(-0.2,0.2)"}[gen]
     model_gbs = (k1_pairs_avg * model_bytes) / (k1_ms_avg / 1e3) / 1e9 if k1_ms_avg > 0 else 0.0
     cnt_file = ROOT / "profiles" / "r02" / "k1_counters.json"
-    kc = json.loads(cnt_file.read_text()) if cnt_file.exists() else {}
+    kc = json.loads(cnt_file.read_text()) if cnt_file.exists() and args.config == "config4" and not args.n else {}
     dram_per_pair = kc.get("dram_bytes_per_pair")
     inst_per_pair = kc.get("inst_per_pair")
     traffic = dram_per_pair * k1_pairs_avg if dram_per_pair else None
@@ -459,7 +491,7 @@ def run_ours(args, rank, world, local, dist):
         "scaling": "strong", "vs_baseline": None,
         "dtype": "int8/f32/f64 (exact-integer int8 screen with rigorous error bound, fp32 Newton, fp64 objective)",
         "data": "synthetic (device Gibbs sampler, seeded)",
-        "config": {"workload": f"{args.config}: Ising N={N} M={M} mean_deg={md} lambda={lam:.1f} kappa=2 "
+        "config": {"workload": f"{args.config}: {desc} N={N} M={M} lambda={lam:.1f} kappa=2 "
                                f"(NNDescent k=8) exact distance; a step = one GCD sweep, the timed steps are "
                                f"sweeps {args.warmup}..{args.warmup + args.steps - 1} of one reconstruction "
                                f"from the empty state",
@@ -474,11 +506,15 @@ def run_ours(args, rank, world, local, dist):
                   "warmup_sweeps_ms": [round(x, 1) for x in warm_ms],
                   "edges_at_start": int(len(ei_w)), "objective": [float(r["objective"]) for r in recs],
                   "tail_rounds": kst.get("tail_rounds")},
-        "roofline": {"bound": "hbm", "achieved": dram_gbs, "peak": peak, "unit": "GB/s",
-                     "frac": dram_gbs / peak, "traffic": traffic, "traffic_unit": "bytes per launch",
-                     "traffic_source": kc.get("capture"),
-                     "kernel": "ising_screen_pipe_kernel (K1, the pair screen: 4-bit pass + 8-bit recheck pass)",
-                     "bytes_per_unit": dram_per_pair, "bytes_per_unit_kind": "measured DRAM bytes per scored pair",
+        "roofline": {"bound": "hbm", "achieved": dram_gbs if traffic else model_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": (dram_gbs if traffic else model_gbs) / peak, "traffic": traffic,
+                     "traffic_unit": "bytes per launch", "traffic_source": kc.get("capture"),
+                     "kernel": ("gauss_screen_kernel (the fp32 pair screen)" if gauss else
+                                "ising_screen_pipe_kernel (K1, the pair screen: 4-bit pass + 8-bit recheck pass)"),
+                     "bytes_per_unit": dram_per_pair or model_bytes,
+                     "bytes_per_unit_kind": ("measured DRAM bytes per scored pair" if dram_per_pair else
+                                             "model bytes (the partner row each pair streams; no ncu capture "
+                                             "for this configuration)"),
                      "units_per_launch": k1_pairs_avg, "ms_per_launch": k1_ms_avg, "peak_kind": peak_kind,
                      "bytes_model": {"bytes_per_pair": model_bytes, "achieved_gbs": model_gbs,
                                      "frac": model_gbs / peak,
@@ -497,7 +533,7 @@ def run_ours(args, rank, world, local, dist):
         perm = np.random.default_rng(0).permutation(len(si))
         si, sj = si[perm], sj[perm]
         st = model.get_state()
-        R = RefScorer(Xh.astype(np.float64), lam, state=st)
+        R = RefScorer(Xh.astype(np.float64), lam, state=st, kind=1 if gauss else 0)
         rate, n, dt, sl, d_ref = R.timed_distances(si, sj, args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": "pairs/s", "cores": R.threads,
                                 "kind": "reference" if R.which == "ref" else "port",

@@ -716,8 +716,10 @@ __global__ void __launch_bounds__(256) gauss_screen_kernel(GaussSnap G, HashView
                                                            double lambda, double base, ScoreOut out,
                                                            uint64_t* __restrict__ surv,
                                                            unsigned long long* __restrict__ nsurv,
-                                                           uint64_t* counters) {
+                                                           uint64_t* counters,
+                                                           unsigned long long* __restrict__ cnt_log = nullptr) {
     if (n_dev) n = min(n, (uint64_t)*n_dev);
+    if (cnt_log && blockIdx.x == 0 && threadIdx.x == 0) *cnt_log = n;
     const int lane = threadIdx.x & 31;
     const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -1071,13 +1073,18 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
         NRG_CUDA(cudaMemsetAsync(nsurv, 0, 8, c.stream));
         const uint64_t sblocks = std::min<uint64_t>(ceil_div(n, 8 * 32), (uint64_t)sms * 16);
         const GaussSnap G = c.gsnap();
+        // timed like K1 (the screen every pair takes): kernel_stats' k1_* describe it
+        const cudaEvent_t k1a = c.mark();
+        int k1slot = -1;
+        unsigned long long* k1log = c.log_slot(&k1slot);
         switch (c.Mp / 128) {
-            case 2: gauss_screen_kernel<2><<<(unsigned)sblocks, 256, 0, c.stream>>>(G, c.Wview(), s, p, n, n_dev, c.lambda, base, out, surv, nsurv, c.dcounters()); break;
-            case 4: gauss_screen_kernel<4><<<(unsigned)sblocks, 256, 0, c.stream>>>(G, c.Wview(), s, p, n, n_dev, c.lambda, base, out, surv, nsurv, c.dcounters()); break;
-            case 6: gauss_screen_kernel<6><<<(unsigned)sblocks, 256, 0, c.stream>>>(G, c.Wview(), s, p, n, n_dev, c.lambda, base, out, surv, nsurv, c.dcounters()); break;
-            default: gauss_screen_kernel<8><<<(unsigned)sblocks, 256, 0, c.stream>>>(G, c.Wview(), s, p, n, n_dev, c.lambda, base, out, surv, nsurv, c.dcounters()); break;
+            case 2: gauss_screen_kernel<2><<<(unsigned)sblocks, 256, 0, c.stream>>>(G, c.Wview(), s, p, n, n_dev, c.lambda, base, out, surv, nsurv, c.dcounters(), k1log); break;
+            case 4: gauss_screen_kernel<4><<<(unsigned)sblocks, 256, 0, c.stream>>>(G, c.Wview(), s, p, n, n_dev, c.lambda, base, out, surv, nsurv, c.dcounters(), k1log); break;
+            case 6: gauss_screen_kernel<6><<<(unsigned)sblocks, 256, 0, c.stream>>>(G, c.Wview(), s, p, n, n_dev, c.lambda, base, out, surv, nsurv, c.dcounters(), k1log); break;
+            default: gauss_screen_kernel<8><<<(unsigned)sblocks, 256, 0, c.stream>>>(G, c.Wview(), s, p, n, n_dev, c.lambda, base, out, surv, nsurv, c.dcounters(), k1log); break;
         }
         NRG_LAUNCH_CHECK();
+        c.span(T_K1, k1a, (double)n, k1slot);
         const uint64_t blocks = std::min<uint64_t>((n + 7) / 8, (uint64_t)sms * 16);
         generic_score_kernel<<<(unsigned)blocks, 256, 0, c.stream>>>(
             c.kind, mode, c.isnap(), G, c.Wview(), s, p, n, c.lambda, base, out, c.dcounters(), surv, nsurv);
