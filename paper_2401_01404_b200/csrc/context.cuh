@@ -117,6 +117,27 @@ struct HashView {
     uint64_t mask;  // capacity - 1 (power of two)
 };
 
+// A dense level's distances, sparse: bit t of `bits` is set for the screen's survivors
+// (and existing couplings) among the triangle's pairs; their values sit in `vals` at
+// rank(t) = rank[t / 32] + popcount of the lower bits of word t / 32 (NaN-boxed worklist
+// entries until the lazy K2 resolves them); every other pair is pruned: -base exactly.
+struct DenseView {
+    const uint32_t* bits;
+    const uint32_t* rank;
+    double* vals;
+    double pruned;
+};
+__device__ __forceinline__ uint32_t dense_rank(const DenseView& D, uint64_t t) {
+    const uint32_t w = D.bits[t >> 5];
+    return D.rank[t >> 5] + __popc(w & ((1u << (t & 31)) - 1u));
+}
+__device__ __forceinline__ double dense_value(const DenseView& D, uint64_t t) {
+    const uint32_t w = __ldg(&D.bits[t >> 5]);
+    const uint32_t bit = 1u << (t & 31);
+    if (!(w & bit)) return D.pruned;
+    return D.vals[__ldg(&D.rank[t >> 5]) + __popc(w & (bit - 1u))];
+}
+
 __device__ __forceinline__ double hash_get(const HashView h, uint64_t key, double dflt) {
     uint64_t s = slot_of(key, h.mask);
     for (;;) {
@@ -219,13 +240,17 @@ struct Context {
 
     // dense FindBest level (find_best.cu): the exact distances of every pair of a deep
     // level's node set S_D (row-major upper triangle over positions in S_D), computed once
-    // by the tensor-core screen; S_D and every deeper level (subsets of S_D) look their
+    // by the tensor-core screen and held SPARSE (DenseView: a survivor bitmap over the
+    // triangle, per-word ranks, and the survivors' values; every other pair is pruned,
+    // dist = -base exactly) -- L2-sized instead of 8 bytes per pair; S_D and every deeper
+    // level (subsets of S_D) look their
     // distances up here instead of claiming and scoring them one by one.  `dloc` maps a
     // global id to its position in S_D (-1 outside), `dbits` marks the pairs probed so
     // far (the generation's cache-miss count stays the reference's).
     bool dense_active = false;
     uint64_t dense_n = 0;
-    DevBuf dtri, dloc, dbits;
+    DevBuf dsurv, drank, dval, dloc, dbits;
+    uint64_t dval_n = 0;
     DevBuf kx_cid, kx_csl, kx_ws, kx_wp, kx_wsl, kx_wd;  // find_knn candidate / worklist scratch
     // Lazy K2 at the dense root: the screen's survivors (the pairs K2 must refine) sit in
     // the triangle as NaN-boxed indices into this worklist and are refined only when a
@@ -299,6 +324,10 @@ struct Context {
     }
     HashView Cview() {
         return {static_cast<uint64_t*>(Ckeys.p), static_cast<double*>(Cvals.p), Ccap - 1};
+    }
+    DenseView dview() {
+        return {static_cast<const uint32_t*>(dsurv.p), static_cast<const uint32_t*>(drank.p),
+                static_cast<double*>(dval.p), -(base + 0.0)};
     }
     IsingSnap isnap() {
         return {dXb(), static_cast<float*>(T32.p), static_cast<double*>(T64.p), static_cast<int8_t*>(T8.p),
@@ -471,7 +500,7 @@ bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* di
 // marked pair for refinement); dense_resolve_end refines what was claimed.  Distances of
 // those slots are valid after dense_resolve_end.
 struct DenseResolve {
-    double* tri = nullptr;  // null: nothing marked (no lazy worklist)
+    DenseView D{nullptr, nullptr, nullptr, 0.0};  // D.bits null: nothing marked (no lazy worklist)
     const float* sg = nullptr;
     const uint8_t* sf = nullptr;
     uint64_t* idx = nullptr;
@@ -482,13 +511,13 @@ struct DenseResolve {
 };
 constexpr unsigned long long kMarkTag = 0x7ff4ull << 48;
 __device__ __forceinline__ void dense_resolve_slot(const DenseResolve& R, uint32_t s) {
-    if (!R.tri) return;
+    if (!R.D.bits) return;
     // the marked-slot bitmap (L2) answers for the unmarked majority; clearing the bit
     // claims the pair, and only then is its triangle slot (the NaN-boxed index) read
     const uint32_t bit = 1u << (s & 31);
     if (!(__ldcg(&R.mark[s >> 5]) & bit)) return;
     if (!(atomicAnd(&R.mark[s >> 5], ~bit) & bit)) return;
-    const unsigned long long v = __ldcg(reinterpret_cast<const unsigned long long*>(R.tri) + s);
+    const unsigned long long v = __ldcg(reinterpret_cast<const unsigned long long*>(R.D.vals) + dense_rank(R.D, s));
     if ((v & (0xffffull << 48)) != kMarkTag) return;
     const uint64_t t = v & 0xffffffffffffull;
     const unsigned long long at = atomicAdd(R.cnt, 1ull);

@@ -21,6 +21,8 @@
 #include <cstdlib>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "context.cuh"
 
 namespace nrg {
@@ -358,6 +360,43 @@ __global__ void tc_cache_filter_kernel(HashView C, const int32_t* __restrict__ e
         sf2[o] = sf[t];
     }
 }
+// sparse dense level: survivor bitmap over the triangle, then per-word ranks
+__global__ void tc_set_bits_kernel(const uint32_t* __restrict__ slot, uint64_t nw, uint32_t* __restrict__ bits) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < nw) atomicOr(&bits[slot[e] >> 5], 1u << (slot[e] & 31));
+}
+__global__ void tc_popc_kernel(const uint32_t* __restrict__ bits, uint64_t nwords, uint32_t* __restrict__ cnt) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords; w += stride)
+        cnt[w] = __popc(bits[w]);
+}
+// worklist slots -> value ranks; in lazy mode each survivor's value is its NaN-boxed
+// worklist index (or the cached value), marked for the lazy K2
+__global__ void tc_rank_mark_kernel(DenseView D, HashView C, const int32_t* __restrict__ es,
+                                    const int32_t* __restrict__ ep, uint32_t* __restrict__ slot, uint64_t nw,
+                                    uint32_t* __restrict__ mark) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nw) return;
+    const uint32_t t = slot[e];
+    const uint32_t r = dense_rank(D, t);
+    slot[e] = r;
+    if (!mark) return;  // eager mode: K2 writes every value
+    if (C.keys) {
+        const uint64_t key = pair_key(es[e], ep[e]);
+        uint64_t s = slot_of(key, C.mask);
+        for (;;) {
+            const uint64_t k = C.keys[s];
+            if (k == key) {
+                D.vals[r] = C.vals[s];
+                return;
+            }
+            if (k == kEmptyKey) break;
+            s = (s + 1) & C.mask;
+        }
+    }
+    reinterpret_cast<unsigned long long*>(D.vals)[r] = kMarkTag | e;
+    atomicOr(&mark[t >> 5], 1u << (t & 31));
+}
 // lazy mode: a survivor's slot holds its worklist index, NaN-boxed (or the cached value)
 __global__ void tc_mark_kernel(HashView C, const int32_t* __restrict__ es, const int32_t* __restrict__ ep,
                                const uint32_t* __restrict__ slot, uint64_t nw, double* __restrict__ dist,
@@ -469,10 +508,13 @@ bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* di
     out.ns = nsb.as<unsigned long long>(1);
     out.cap = cap;
     NRG_CUDA(cudaMemsetAsync(out.ns, 0, 8, c.stream));
-    // every pair starts pruned (dist = -base exactly, the kink tie value); the tile
-    // kernel only lists the rest for K2, which overwrites their slots
-    tc_fill_kernel<<<(unsigned)std::min<uint64_t>(ceil_div(pairs, 256), 148 * 16), 256, 0, c.stream>>>(
-        dist, pairs, -(base + 0.0));
+    // dist == nullptr: the dense-level (sparse) form -- pruned pairs are implicit, only
+    // the survivors get values (Context::dview); otherwise every pair starts pruned
+    // (dist = -base exactly, the kink tie value) and K2 overwrites the listed slots
+    const bool sparse = dist == nullptr;
+    if (!sparse)
+        tc_fill_kernel<<<(unsigned)std::min<uint64_t>(ceil_div(pairs, 256), 148 * 16), 256, 0, c.stream>>>(
+            dist, pairs, -(base + 0.0));
     const CUtensorMap mx = tile_map(zx, n, (uint64_t)Mp), mt = tile_map(zt, n, (uint64_t)Mp);
     const int T = (int)((n + kBM - 1) / kBM);
     const size_t smem = (size_t)kStages * kStageBytes + 1024;
@@ -511,15 +553,50 @@ bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* di
     unsigned long long nw = 0;
     nw = c.read_scalar(out.ns);
     c.toc(P_SCORE);
+    if (sparse) {
+        // survivor bitmap + ranks over the triangle, values at the survivors' ranks
+        const uint64_t nwords = pairs / 32 + 1;
+        uint32_t* bits = c.dsurv.as<uint32_t>(nwords);
+        uint32_t* rank = c.drank.as<uint32_t>(nwords);
+        NRG_CUDA(cudaMemsetAsync(bits, 0, nwords * 4, c.stream));
+        if (nw) {
+            tc_set_bits_kernel<<<(unsigned)ceil_div(nw, 256), 256, 0, c.stream>>>(slot, nw, bits);
+            NRG_LAUNCH_CHECK();
+        }
+        DevBuf cntb, tmpb;
+        uint32_t* cnt = cntb.as<uint32_t>(nwords);
+        tc_popc_kernel<<<148 * 8, 256, 0, c.stream>>>(bits, nwords, cnt);
+        NRG_LAUNCH_CHECK();
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, rank, (int64_t)nwords, c.stream);
+        void* tmp = tmpb.ensure(tb);
+        cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, rank, (int64_t)nwords, c.stream);
+        c.dval.as<double>(nw + 1);
+        c.dval_n = nw;
+        dist = static_cast<double*>(c.dval.p);  // K2 / cache hits write the values at the ranks
+        uint32_t* mark = nullptr;
+        if (lazy) {
+            mark = c.dmark.as<uint32_t>(pairs / 32 + 1);
+            NRG_CUDA(cudaMemsetAsync(mark, 0, (pairs / 32 + 1) * 4, c.stream));
+        }
+        if (nw) {
+            tc_rank_mark_kernel<<<(unsigned)ceil_div(nw, 256), 256, 0, c.stream>>>(
+                c.dview(), (lazy && use_cache && c.Ckeys.p && c.Ccap) ? c.Cview() : HashView{nullptr, nullptr, 0},
+                es, ep, slot, nw, mark);
+            NRG_LAUNCH_CHECK();
+        }
+    }
     if (lazy) {
         // survivors stay in the triangle as markers; the worklist moves to the Context
-        uint32_t* mark = c.dmark.as<uint32_t>(pairs / 32 + 1);
-        NRG_CUDA(cudaMemsetAsync(mark, 0, (pairs / 32 + 1) * 4, c.stream));
-        if (nw) {
-            tc_mark_kernel<<<(unsigned)ceil_div(nw, 256), 256, 0, c.stream>>>(
-                (use_cache && c.Ckeys.p && c.Ccap) ? c.Cview() : HashView{nullptr, nullptr, 0}, es, ep, slot, nw,
-                dist, mark);
-            NRG_LAUNCH_CHECK();
+        if (!sparse) {
+            uint32_t* mark = c.dmark.as<uint32_t>(pairs / 32 + 1);
+            NRG_CUDA(cudaMemsetAsync(mark, 0, (pairs / 32 + 1) * 4, c.stream));
+            if (nw) {
+                tc_mark_kernel<<<(unsigned)ceil_div(nw, 256), 256, 0, c.stream>>>(
+                    (use_cache && c.Ckeys.p && c.Ccap) ? c.Cview() : HashView{nullptr, nullptr, 0}, es, ep, slot, nw,
+                    dist, mark);
+                NRG_LAUNCH_CHECK();
+            }
         }
         c.dwl_es = std::move(esb);
         c.dwl_ep = std::move(epb);
@@ -563,7 +640,7 @@ using namespace tc;
 DenseResolve dense_resolve_begin(Context& c) {
     DenseResolve R;
     if (!c.dwl_n) return R;
-    R.tri = static_cast<double*>(c.dtri.p);
+    R.D = c.dview();
     R.sg = static_cast<const float*>(c.dwl_sg.p);
     R.sf = static_cast<const uint8_t*>(c.dwl_sf.p);
     R.idx = static_cast<uint64_t*>(c.dres_idx.p);
@@ -578,7 +655,7 @@ DenseResolve dense_resolve_begin(Context& c) {
 void dense_resolve_end(Context& c) {
     if (!c.dwl_n) return;
     ScoreOut so;
-    so.cache_vals = static_cast<double*>(c.dtri.p);
+    so.cache_vals = static_cast<double*>(c.dval.p);  // the worklist slots hold value ranks
     so.slot = static_cast<const uint32_t*>(c.dwl_slot.p);
     refine_survivors(c, static_cast<const int32_t*>(c.dwl_es.p), static_cast<const int32_t*>(c.dwl_ep.p),
                      static_cast<const uint64_t*>(c.dres_idx.p), static_cast<const float*>(c.dres_g.p),

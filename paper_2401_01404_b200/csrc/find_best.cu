@@ -262,7 +262,7 @@ __global__ void dense_loc_kernel(const int32_t* __restrict__ nodes, uint64_t n, 
 }
 // base case below a dense root: the level's own triangle gathered from the root's
 __global__ void dense_subtri_kernel(const int32_t* __restrict__ nodes, uint64_t n, const int32_t* __restrict__ loc,
-                                    const double* __restrict__ tri, uint64_t dn, TriKey* __restrict__ out) {
+                                    DenseView D, uint64_t dn, TriKey* __restrict__ out) {
     const uint64_t a = blockIdx.x;
     if (a >= n) return;
     const uint64_t base = a * (2 * n - a - 1) / 2;
@@ -273,7 +273,7 @@ __global__ void dense_subtri_kernel(const int32_t* __restrict__ nodes, uint64_t 
         const uint64_t rb = (uint64_t)loc[y];
         const uint64_t lo = ra < rb ? ra : rb, hi = ra < rb ? rb : ra;
         TriKey k;
-        k.d = dkey(tri[lo * (2 * dn - lo - 1) / 2 + (hi - lo - 1)]);
+        k.d = dkey(dense_value(D, lo * (2 * dn - lo - 1) / 2 + (hi - lo - 1)));
         k.a = (uint32_t)min(x, y);
         k.b = (uint32_t)max(x, y);
         out[base + (c - a - 1)] = k;
@@ -483,8 +483,7 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
             dense_resolve_subtri(c, S, n);
             c.tic();
             dense_subtri_kernel<<<(unsigned)n, 256, 0, c.stream>>>(S, n, static_cast<const int32_t*>(c.dloc.p),
-                                                                  static_cast<const double*>(c.dtri.p), c.dense_n,
-                                                                  keys);
+                                                                  c.dview(), c.dense_n, keys);
             NRG_LAUNCH_CHECK();
             // counted as score_all_pairs counts the base case: every pair a probe
             counters_add_host(c, C_MISSES, total);
@@ -515,11 +514,12 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
         if (!c.dense_active && mode == EXACT && c.kind == ISING && n <= dense_max_n() &&
             dense_ratio() * cap * cap >= n) {
             c.join_side();  // a previous root's recount still reads dloc / dbits
-            double* tri = c.dtri.as<double>(total);
+
             if (NRG_ENV_ON("NRG_DEBUG_LEVELS")) c.flush_timing();
             const double ph0 = c.phase_ms[P_SCORE];
             const auto w0 = std::chrono::steady_clock::now();
-            const bool ok = score_all_pairs_tc(c, S, n, tri, true, !NRG_ENV_ON("NRG_DENSE_EAGER"));
+            // the level's distances, sparse (Context::dview): survivors only
+            const bool ok = score_all_pairs_tc(c, S, n, nullptr, true, !NRG_ENV_ON("NRG_DENSE_EAGER"));
             if (NRG_ENV_ON("NRG_DEBUG_LEVELS")) {
                 c.flush_timing();
                 fprintf(stderr, "dense root level %d: n=%llu setup wall_ms=%.2f score_phase_ms=%.2f ok=%d\n", level,

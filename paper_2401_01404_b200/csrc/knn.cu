@@ -331,13 +331,17 @@ __global__ void claim_list_kernel(HashView h, ClaimSink sink, const int32_t* __r
     if (valid) slot[e] = sl;
     if (sink.fold) flush_hits(sink, hit_acc);
 }
-__global__ void gather_vals_kernel(const double* __restrict__ vals, const double* __restrict__ rvals,
+// the distance behind a candidate slot: a dense level's sparse triangle (D.bits set), a
+// worklist / remote answer (kRemote), or the distance memo
+__device__ __forceinline__ double slot_value(const DenseView& D, const double* __restrict__ vals,
+                                             const double* __restrict__ rvals, uint32_t sl) {
+    if (D.bits) return dense_value(D, sl);
+    return (sl & kRemote) ? rvals[sl & ~kRemote] : vals[sl];
+}
+__global__ void gather_vals_kernel(DenseView D, const double* __restrict__ vals, const double* __restrict__ rvals,
                                    const uint32_t* __restrict__ slot, uint64_t n, double* __restrict__ out) {
     const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < n) {
-        const uint32_t sl = slot[e];
-        out[e] = (sl & kRemote) ? rvals[sl & ~kRemote] : vals[sl];
-    }
+    if (e < n) out[e] = slot_value(D, vals, rvals, slot[e]);
 }
 
 // ---------------------------------------------------------------- key-sharded cache exchange
@@ -867,7 +871,7 @@ __global__ void __launch_bounds__(NT) knn_merge_kernel(const int32_t* __restrict
                                                        const int32_t* __restrict__ cand_id,
                                                        const uint32_t* __restrict__ cand_slot,
                                                        const int32_t* __restrict__ cand_cnt, uint64_t capn,
-                                                       const double* __restrict__ cvals,
+                                                       DenseView D, const double* __restrict__ cvals,
                                                        const double* __restrict__ rvals, int buf_cap,
                                                        unsigned long long* __restrict__ churn, uint64_t lo) {
     extern __shared__ unsigned char smem_raw[];
@@ -904,7 +908,7 @@ __global__ void __launch_bounds__(NT) knn_merge_kernel(const int32_t* __restrict
         for (int t = blk + tid; t < end; t += NT) {
             const int32_t v = cand_id[li * capn + t];
             const uint32_t sl = cand_slot[li * capn + t];
-            const double d = (sl & kRemote) ? rvals[sl & ~kRemote] : cvals[sl];
+            const double d = slot_value(D, cvals, rvals, sl);
             const int g = nodes[v];
             if (entry_less(d, g, wd, wg)) {
                 const int at = atomicAdd(&nb, 1);
@@ -989,7 +993,7 @@ constexpr int kMergeBlk = 64;
 __global__ void __launch_bounds__(32 * kMergeWarps) knn_merge_warp_kernel(
     const int32_t* __restrict__ nodes, uint64_t n, int32_t* __restrict__ gid, double* __restrict__ gd, int kw,
     const int32_t* __restrict__ cand_id, const uint32_t* __restrict__ cand_slot,
-    const int32_t* __restrict__ cand_cnt, uint64_t capn, const double* __restrict__ cvals,
+    const int32_t* __restrict__ cand_cnt, uint64_t capn, DenseView D, const double* __restrict__ cvals,
     const double* __restrict__ rvals, unsigned long long* __restrict__ churn, uint64_t lo, uint64_t own) {
     extern __shared__ unsigned char merge_warp_smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1036,7 +1040,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) knn_merge_warp_kernel(
             if (t < cnt) {
                 vv[q] = cand_id[li * capn + t];
                 const uint32_t sl = cand_slot[li * capn + t];
-                dv[q] = (sl & kRemote) ? rvals[sl & ~kRemote] : cvals[sl];
+                dv[q] = slot_value(D, cvals, rvals, sl);
                 gv[q] = nodes[vv[q]];
             }
         }
@@ -1376,7 +1380,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
     const bool cached = (mode == EXACT || mode == GRADIENT);
     // dense level: distances come from the level's exhaustive triangle (find_best.cu)
     const bool dense = mode == EXACT && c.dense_active && c.world == 1;
-    const double* dtri = dense ? static_cast<const double*>(c.dtri.p) : nullptr;
+    const DenseView dview = dense ? c.dview() : DenseView{nullptr, nullptr, nullptr, 0.0};
     DevBuf rootposb;
     int32_t* rootpos = nullptr;
     if (dense) {
@@ -1475,7 +1479,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             if (dense) dense_resolve_slots(c, slot, nq);  // refine the marked pairs first
             if (nq) {
                 gather_vals_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, c.stream>>>(
-                    dense ? dtri : c.Cview().vals, static_cast<double*>(X.rvals.p), slot, nq, gd + lo * kw);
+                    dview, dense ? nullptr : c.Cview().vals, static_cast<double*>(X.rvals.p), slot, nq, gd + lo * kw);
                 NRG_LAUNCH_CHECK();
             }
         } else {
@@ -1710,20 +1714,20 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             score_entries(c, mode, ws, wp, nw, so);
         }
         if (dense) dense_resolve_rows(c, cand_slot, cand_cnt, lo, own, capn);  // refine the marked pairs first
-        const double* dvals = dense ? dtri : cached ? c.Cview().vals : flat_d;
+        const double* dvals = dense ? nullptr : cached ? c.Cview().vals : flat_d;
         const double* rvals = wl ? wdist : static_cast<double*>(X.rvals.p);
         c.tic();
         if (own) {
             if (kw > 64)
                 knn_merge_kernel<128><<<(unsigned)own, 128, merge_smem, c.stream>>>(
-                    d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dvals, rvals, buf_cap, churn, lo);
+                    d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dview, dvals, rvals, buf_cap, churn, lo);
             else if (!NRG_ENV_ON("NRG_MERGE_CTA"))
                 knn_merge_warp_kernel<<<(unsigned)ceil_div(own, kMergeWarps), 32 * kMergeWarps,
                                         (size_t)kMergeWarps * (2 * kw + kMergeBlk) * 20, c.stream>>>(
-                    d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dvals, rvals, churn, lo, own);
+                    d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dview, dvals, rvals, churn, lo, own);
             else
                 knn_merge_kernel<32><<<(unsigned)own, 32, merge_smem, c.stream>>>(
-                    d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dvals, rvals, buf_cap, churn, lo);
+                    d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dview, dvals, rvals, buf_cap, churn, lo);
             NRG_LAUNCH_CHECK();
         }
         unsigned long long changed = 0;
