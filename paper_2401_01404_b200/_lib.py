@@ -10,7 +10,10 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libnetrec_b200.so"
+import os
+
+# NRG_LIB: another build of the same library (A/B timing of two builds on one box)
+LIB_PATH = Path(os.environ.get("NRG_LIB") or Path(__file__).resolve().parent / "libnetrec_b200.so")
 
 NRG_ISING, NRG_GAUSSIAN = 0, 1
 NRG_EXACT, NRG_GRADIENT, NRG_TABLE, NRG_LINE = 0, 1, 2, 3

@@ -259,6 +259,9 @@ struct Context {
     uint64_t dwl_n = 0;
     DevBuf dres_idx, dres_g, dres_f, dres_cnt;
     DevBuf dmark;  // one bit per triangle slot: still marked (L2-resident; the test a probe makes)
+    // tensor-core screen scratch (score_all_pairs_tc), grow-only
+    DevBuf tc_zx, tc_zt, tc_q, tc_si, tc_sj, tc_sg, tc_sf, tc_ns, tc_es, tc_ep, tc_slot, tc_idx, tc_loc, tc_cnt,
+        tc_tmp;
 
     // test metrics
     DevBuf table, line;

@@ -489,7 +489,11 @@ bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* di
     const double base = generation_base(c);
     c.tic();
     const int Mp = c.Mp;
-    DevBuf zxb, ztb, qb, sib, sjb, sgb, sfb, nsb, esb, epb, slb, idb, locb;
+    // scratch persists in the context (grow-only): re-mapping ~1 GB of pool blocks per
+    // dense root cost milliseconds whenever the pool could not hand a freed block back
+    DevBuf &zxb = c.tc_zx, &ztb = c.tc_zt, &qb = c.tc_q, &sib = c.tc_si, &sjb = c.tc_sj, &sgb = c.tc_sg,
+           &sfb = c.tc_sf, &nsb = c.tc_ns, &esb = c.tc_es, &epb = c.tc_ep, &slb = c.tc_slot, &idb = c.tc_idx,
+           &locb = c.tc_loc;
     int8_t* zx = zxb.as<int8_t>(n * Mp);
     int8_t* zt = ztb.as<int8_t>(n * Mp);
     float4* q = qb.as<float4>(n);
@@ -498,7 +502,9 @@ bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* di
     if (Mp > c.M) tc_zero_pad_kernel<<<(unsigned)n, 256, 0, c.stream>>>(zx, n, c.M, Mp);
     NRG_LAUNCH_CHECK();
     const uint64_t pairs = n * (n - 1) / 2;
-    const uint64_t cap = std::max<uint64_t>(1u << 20, pairs / 4);
+    // survivors are ~0.1% of the pairs at a steady state and a few % at the empty state;
+    // a screen that overflows this returns false and the level takes the claim path
+    const uint64_t cap = std::max<uint64_t>(1u << 22, pairs / 16);
     TcOut out;
     out.dist = dist;
     out.si = sib.as<int32_t>(cap);
@@ -563,7 +569,7 @@ bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* di
             tc_set_bits_kernel<<<(unsigned)ceil_div(nw, 256), 256, 0, c.stream>>>(slot, nw, bits);
             NRG_LAUNCH_CHECK();
         }
-        DevBuf cntb, tmpb;
+        DevBuf &cntb = c.tc_cnt, &tmpb = c.tc_tmp;
         uint32_t* cnt = cntb.as<uint32_t>(nwords);
         tc_popc_kernel<<<148 * 8, 256, 0, c.stream>>>(bits, nwords, cnt);
         NRG_LAUNCH_CHECK();
@@ -598,11 +604,13 @@ bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* di
                 NRG_LAUNCH_CHECK();
             }
         }
-        c.dwl_es = std::move(esb);
-        c.dwl_ep = std::move(epb);
-        c.dwl_slot = std::move(slb);
-        c.dwl_sg = std::move(sgb);
-        c.dwl_sf = std::move(sfb);
+        // the worklist moves to the Context (roles swapped: the previous worklist's
+        // buffers, no longer referenced, become the next screen's scratch)
+        std::swap(c.dwl_es, esb);
+        std::swap(c.dwl_ep, epb);
+        std::swap(c.dwl_slot, slb);
+        std::swap(c.dwl_sg, sgb);
+        std::swap(c.dwl_sf, sfb);
         c.dwl_n = nw;
         c.dres_idx.as<uint64_t>(nw + 1);
         c.dres_g.as<float>(nw + 1);
