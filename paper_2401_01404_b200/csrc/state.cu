@@ -87,6 +87,29 @@ void ctx_init(Context& c, int n, int m, int kind, double lambda, int device) {
         NRG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
         uint64_t thr = UINT64_MAX;
         NRG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        // Back the pool with physical memory once per device and process: a first large
+        // allocation, freed, stays in the pool (threshold above), so the sweeps' scratch
+        // is carved from mapped memory -- mapping fresh pool memory mid-sweep measured
+        // anywhere from 3 to 300 ms per few hundred MB.  NRG_POOL_RESERVE_GB overrides
+        // (0 disables); at most a quarter of the free memory.
+        static bool reserved[64] = {};
+        if (device >= 0 && device < 64 && !reserved[device]) {
+            reserved[device] = true;
+            const char* e = getenv("NRG_POOL_RESERVE_GB");
+            size_t want = (size_t)((e ? atof(e) : 16.0) * (1ull << 30));
+            size_t fr = 0, tot = 0;
+            NRG_CUDA(cudaMemGetInfo(&fr, &tot));
+            want = std::min(want, fr / 4);
+            if (want >= (64ull << 20)) {
+                void* p = nullptr;
+                if (cudaMallocAsync(&p, want, c.stream) == cudaSuccess) {
+                    NRG_CUDA(cudaFreeAsync(p, c.stream));
+                    NRG_CUDA(cudaStreamSynchronize(c.stream));
+                } else {
+                    cudaGetLastError();
+                }
+            }
+        }
     }
     // Mp = 256 * HQ: one 16-byte fp16 load per lane per 256 samples in the Ising screen
     // (score.cu instantiates HQ = 1..8, i.e. M <= 2048; larger M uses the fp64 path)

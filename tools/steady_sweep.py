@@ -13,6 +13,8 @@ m.reset_state()
 for it in range(3):
     m.gcd_iteration(it, kappa=2.0, seed=1)
 m.reset_counters()
+if os.environ.get("NRG_DEBUG_ALLOC"):
+    print("=== measured sweep", file=sys.stderr, flush=True)
 torch.cuda.cudart().cudaProfilerStart()
 m.timer_start()
 m.gcd_iteration(3, kappa=2.0, seed=1)
