@@ -127,6 +127,20 @@ struct DenseView {
     double* vals;
     double pruned;
 };
+// The distance memo's values: a pair the screen pruned is never written (its distance is
+// -base exactly: bit clear in the survivor bitmap, the L2-resident test every read makes);
+// the rest (K2 results) are written with their bit set.  Saves the K1 screen a scattered
+// 8-byte store into the multi-GB value array for every pruned pair.
+struct MemoView {
+    const uint32_t* bits;
+    const double* vals;
+    double pruned;
+};
+__device__ __forceinline__ double memo_value(const MemoView& C, uint64_t s) {
+    if (!C.bits) return C.vals[s];
+    return (__ldg(&C.bits[s >> 5]) >> (s & 31)) & 1u ? C.vals[s] : C.pruned;
+}
+
 __device__ __forceinline__ uint32_t dense_rank(const DenseView& D, uint64_t t) {
     const uint32_t w = D.bits[t >> 5];
     return D.rank[t >> 5] + __popc(w & ((1u << (t & 31)) - 1u));
@@ -184,6 +198,9 @@ struct GaussSnap {
 struct ScoreOut {
     double* cache_vals = nullptr;
     const uint32_t* slot = nullptr;
+    // cache_bits (the distance memo's survivor bitmap): pruned pairs are not written,
+    // refined ones are written and their bit set (MemoView)
+    uint32_t* cache_bits = nullptr;
     double* dist = nullptr;
     double* w = nullptr;
     double* gain = nullptr;
@@ -234,6 +251,7 @@ struct Context {
 
     // distance cache
     DevBuf Ckeys, Cvals, Ccount;  // Ccount: u64 live
+    DevBuf Csurv;                 // survivor bitmap over the memo's slots (MemoView)
     uint64_t Ccap = 0;
     uint64_t cache_live_host = 0;
     uint64_t cache_live_bound = 0;  // host upper bound on the live count (claims <= reserved)
@@ -328,6 +346,10 @@ struct Context {
     HashView Cview() {
         return {static_cast<uint64_t*>(Ckeys.p), static_cast<double*>(Cvals.p), Ccap - 1};
     }
+    MemoView mview() {
+        return {static_cast<const uint32_t*>(Csurv.p), static_cast<const double*>(Cvals.p), -(base + 0.0)};
+    }
+    uint32_t* dsurvbits() { return static_cast<uint32_t*>(Csurv.p); }
     DenseView dview() {
         return {static_cast<const uint32_t*>(dsurv.p), static_cast<const uint32_t*>(drank.p),
                 static_cast<double*>(dval.p), -(base + 0.0)};

@@ -326,7 +326,8 @@ __global__ void tc_edges_kernel(HashView W, uint64_t wcap, const int32_t* __rest
 }
 // pairs this generation already scored (distance cache hits) take the cached value; the
 // rest form the K2 worklist (values are deterministic: a re-score would give the same)
-__global__ void tc_cache_filter_kernel(HashView C, const int32_t* __restrict__ es, const int32_t* __restrict__ ep,
+__global__ void tc_cache_filter_kernel(HashView C, MemoView Cv, const int32_t* __restrict__ es,
+                                       const int32_t* __restrict__ ep,
                                        const uint32_t* __restrict__ slot, const float* __restrict__ sg,
                                        const uint8_t* __restrict__ sf, uint64_t nw, double* __restrict__ dist,
                                        uint64_t* __restrict__ idx2, float* __restrict__ sg2,
@@ -340,7 +341,7 @@ __global__ void tc_cache_filter_kernel(HashView C, const int32_t* __restrict__ e
         for (;;) {
             const uint64_t k = C.keys[s];
             if (k == key) {
-                dist[slot[t]] = C.vals[s];
+                dist[slot[t]] = memo_value(Cv, s);
                 keep = false;
                 break;
             }
@@ -372,7 +373,7 @@ __global__ void tc_popc_kernel(const uint32_t* __restrict__ bits, uint64_t nword
 }
 // worklist slots -> value ranks; in lazy mode each survivor's value is its NaN-boxed
 // worklist index (or the cached value), marked for the lazy K2
-__global__ void tc_rank_mark_kernel(DenseView D, HashView C, const int32_t* __restrict__ es,
+__global__ void tc_rank_mark_kernel(DenseView D, HashView C, MemoView Cv, const int32_t* __restrict__ es,
                                     const int32_t* __restrict__ ep, uint32_t* __restrict__ slot, uint64_t nw,
                                     uint32_t* __restrict__ mark) {
     const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -387,7 +388,7 @@ __global__ void tc_rank_mark_kernel(DenseView D, HashView C, const int32_t* __re
         for (;;) {
             const uint64_t k = C.keys[s];
             if (k == key) {
-                D.vals[r] = C.vals[s];
+                D.vals[r] = memo_value(Cv, s);
                 return;
             }
             if (k == kEmptyKey) break;
@@ -398,7 +399,7 @@ __global__ void tc_rank_mark_kernel(DenseView D, HashView C, const int32_t* __re
     atomicOr(&mark[t >> 5], 1u << (t & 31));
 }
 // lazy mode: a survivor's slot holds its worklist index, NaN-boxed (or the cached value)
-__global__ void tc_mark_kernel(HashView C, const int32_t* __restrict__ es, const int32_t* __restrict__ ep,
+__global__ void tc_mark_kernel(HashView C, MemoView Cv, const int32_t* __restrict__ es, const int32_t* __restrict__ ep,
                                const uint32_t* __restrict__ slot, uint64_t nw, double* __restrict__ dist,
                                uint32_t* __restrict__ mark) {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -409,7 +410,7 @@ __global__ void tc_mark_kernel(HashView C, const int32_t* __restrict__ es, const
         for (;;) {
             const uint64_t k = C.keys[s];
             if (k == key) {
-                dist[slot[t]] = C.vals[s];
+                dist[slot[t]] = memo_value(Cv, s);
                 return;
             }
             if (k == kEmptyKey) break;
@@ -588,7 +589,7 @@ bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* di
         if (nw) {
             tc_rank_mark_kernel<<<(unsigned)ceil_div(nw, 256), 256, 0, c.stream>>>(
                 c.dview(), (lazy && use_cache && c.Ckeys.p && c.Ccap) ? c.Cview() : HashView{nullptr, nullptr, 0},
-                es, ep, slot, nw, mark);
+                c.mview(), es, ep, slot, nw, mark);
             NRG_LAUNCH_CHECK();
         }
     }
@@ -599,8 +600,8 @@ bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* di
             NRG_CUDA(cudaMemsetAsync(mark, 0, (pairs / 32 + 1) * 4, c.stream));
             if (nw) {
                 tc_mark_kernel<<<(unsigned)ceil_div(nw, 256), 256, 0, c.stream>>>(
-                    (use_cache && c.Ckeys.p && c.Ccap) ? c.Cview() : HashView{nullptr, nullptr, 0}, es, ep, slot, nw,
-                    dist, mark);
+                    (use_cache && c.Ckeys.p && c.Ccap) ? c.Cview() : HashView{nullptr, nullptr, 0}, c.mview(), es, ep,
+                    slot, nw, dist, mark);
                 NRG_LAUNCH_CHECK();
             }
         }
@@ -628,7 +629,7 @@ bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* di
             unsigned long long* cnt = cb.as<unsigned long long>(1);
             NRG_CUDA(cudaMemsetAsync(cnt, 0, 8, c.stream));
             tc_cache_filter_kernel<<<(unsigned)ceil_div(nw, 256), 256, 0, c.stream>>>(
-                c.Cview(), es, ep, slot, out.sg, out.sf, nw, dist, idx2, sg2, sf2, cnt);
+                c.Cview(), c.mview(), es, ep, slot, out.sg, out.sf, nw, dist, idx2, sg2, sf2, cnt);
             NRG_LAUNCH_CHECK();
             refine_survivors(c, es, ep, idx2, sg2, sf2, nw, base, so, cnt);
         } else {

@@ -333,15 +333,15 @@ __global__ void claim_list_kernel(HashView h, ClaimSink sink, const int32_t* __r
 }
 // the distance behind a candidate slot: a dense level's sparse triangle (D.bits set), a
 // worklist / remote answer (kRemote), or the distance memo
-__device__ __forceinline__ double slot_value(const DenseView& D, const double* __restrict__ vals,
-                                             const double* __restrict__ rvals, uint32_t sl) {
+__device__ __forceinline__ double slot_value(const DenseView& D, const MemoView& V, const double* __restrict__ rvals,
+                                             uint32_t sl) {
     if (D.bits) return dense_value(D, sl);
-    return (sl & kRemote) ? rvals[sl & ~kRemote] : vals[sl];
+    return (sl & kRemote) ? rvals[sl & ~kRemote] : memo_value(V, sl);
 }
-__global__ void gather_vals_kernel(DenseView D, const double* __restrict__ vals, const double* __restrict__ rvals,
+__global__ void gather_vals_kernel(DenseView D, MemoView V, const double* __restrict__ rvals,
                                    const uint32_t* __restrict__ slot, uint64_t n, double* __restrict__ out) {
     const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < n) out[e] = slot_value(D, vals, rvals, slot[e]);
+    if (e < n) out[e] = slot_value(D, V, rvals, slot[e]);
 }
 
 // ---------------------------------------------------------------- key-sharded cache exchange
@@ -370,10 +370,10 @@ __global__ void claim_keys_kernel(HashView h, ClaimSink sink, const uint64_t* __
     const uint32_t sl = claim_warp(h, local, valid, (int32_t)(k >> 32), (int32_t)(k & 0xffffffffu));
     if (valid) slot_of[idx[e]] = sl;
 }
-__global__ void answer_kernel(const double* __restrict__ vals, const uint32_t* __restrict__ slot_of, uint64_t n,
+__global__ void answer_kernel(MemoView vals, const uint32_t* __restrict__ slot_of, uint64_t n,
                               double* __restrict__ out) {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < n) out[t] = vals[slot_of[t]];
+    if (t < n) out[t] = memo_value(vals, slot_of[t]);
 }
 
 // ---------------------------------------------------------------- U (capped undirected view)
@@ -871,7 +871,7 @@ __global__ void __launch_bounds__(NT) knn_merge_kernel(const int32_t* __restrict
                                                        const int32_t* __restrict__ cand_id,
                                                        const uint32_t* __restrict__ cand_slot,
                                                        const int32_t* __restrict__ cand_cnt, uint64_t capn,
-                                                       DenseView D, const double* __restrict__ cvals,
+                                                       DenseView D, MemoView cvals,
                                                        const double* __restrict__ rvals, int buf_cap,
                                                        unsigned long long* __restrict__ churn, uint64_t lo) {
     extern __shared__ unsigned char smem_raw[];
@@ -993,7 +993,7 @@ constexpr int kMergeBlk = 64;
 __global__ void __launch_bounds__(32 * kMergeWarps) knn_merge_warp_kernel(
     const int32_t* __restrict__ nodes, uint64_t n, int32_t* __restrict__ gid, double* __restrict__ gd, int kw,
     const int32_t* __restrict__ cand_id, const uint32_t* __restrict__ cand_slot,
-    const int32_t* __restrict__ cand_cnt, uint64_t capn, DenseView D, const double* __restrict__ cvals,
+    const int32_t* __restrict__ cand_cnt, uint64_t capn, DenseView D, MemoView cvals,
     const double* __restrict__ rvals, unsigned long long* __restrict__ churn, uint64_t lo, uint64_t own) {
     extern __shared__ unsigned char merge_warp_smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -1276,7 +1276,7 @@ static void exchange_and_score(Context& c, int mode, const ClaimSink& sink, uint
     double* resp = X.resp.as<double>(R + 1);
     double* rvals = X.rvals.as<double>(R + 1);
     if (Q) {
-        answer_kernel<<<(unsigned)ceil_div(Q, 256), 256, 0, c.stream>>>(c.Cview().vals, slot_of, Q, ans);
+        answer_kernel<<<(unsigned)ceil_div(Q, 256), 256, 0, c.stream>>>(c.mview(), slot_of, Q, ans);
         NRG_LAUNCH_CHECK();
     }
     comm->alltoallv(ans, rb, ro, resp, sb, so, c.stream);
@@ -1301,6 +1301,7 @@ static void score_claimed(Context& c, int mode, int32_t* ws, int32_t* wp, uint32
     if (!nw) return;
     ScoreOut so;
     so.cache_vals = c.Cview().vals;
+    so.cache_bits = c.dsurvbits();
     so.slot = wslot;
     score_entries(c, mode, ws, wp, nw, so);
 }
@@ -1469,6 +1470,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                 // claimed count stays on the device: the screen strides over it
                 ScoreOut so;
                 so.cache_vals = c.Cview().vals;
+                so.cache_bits = c.dsurvbits();
                 so.slot = wsl;
                 score_entries(c, mode, ws, wp, nq + 1, so, wcount);
             } else {
@@ -1479,7 +1481,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             if (dense) dense_resolve_slots(c, slot, nq);  // refine the marked pairs first
             if (nq) {
                 gather_vals_kernel<<<(unsigned)ceil_div(nq, 256), 256, 0, c.stream>>>(
-                    dview, dense ? nullptr : c.Cview().vals, static_cast<double*>(X.rvals.p), slot, nq, gd + lo * kw);
+                    dview, c.mview(), static_cast<double*>(X.rvals.p), slot, nq, gd + lo * kw);
                 NRG_LAUNCH_CHECK();
             }
         } else {
@@ -1699,6 +1701,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             // claimed count stays on the device: the screen strides over it
             ScoreOut so;
             so.cache_vals = c.Cview().vals;
+            so.cache_bits = c.dsurvbits();
             so.slot = wsl;
             so.dist = wdist;  // the worklist-ordered copy the merge reads (wl slots)
             score_entries(c, mode, ws, wp, own * capn + 1, so, wcount);
@@ -1714,7 +1717,9 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             score_entries(c, mode, ws, wp, nw, so);
         }
         if (dense) dense_resolve_rows(c, cand_slot, cand_cnt, lo, own, capn);  // refine the marked pairs first
-        const double* dvals = dense ? nullptr : cached ? c.Cview().vals : flat_d;
+        // distances behind the candidate slots: the memo (pruned pairs implicit), or the
+        // flat per-candidate array of an uncached metric
+        const MemoView dvals = cached ? c.mview() : MemoView{nullptr, flat_d, 0.0};
         const double* rvals = wl ? wdist : static_cast<double*>(X.rvals.p);
         c.tic();
         if (own) {

@@ -64,6 +64,13 @@ __device__ __forceinline__ void load_src8(Src8<HW>& c, const IsingSnap& S, int r
     }
 }
 
+// a refined distance into the memo (and its survivor bit) or a plain slot array
+__device__ __forceinline__ void memo_store(const ScoreOut& out, uint64_t e, double v) {
+    const uint32_t s = out.slot[e];
+    out.cache_vals[s] = v;
+    if (out.cache_bits) atomicOr(&out.cache_bits[s >> 5], 1u << (s & 31));
+}
+
 // K1: the bandwidth-bound screen on the int8 field.  Per pair (s stationary, p streamed)
 //   g0 = 2<x_s,x_p> - sum_m x_p T_s - sum_m x_s T_p
 //      ~ 2 (M - 2 popc(b_s ^ b_p)) - d_s (2 sum_{b_p=1} T8_s - sum T8_s) - d_p sum x_s T8_p
@@ -160,7 +167,7 @@ __global__ void __launch_bounds__(256, HW == 1 ? 4 : 3) ising_screen_kernel(Isin
             if (pruned) {
                 // L1 kink: w* = 0 and gain = 0 exactly (inc/model.hpp:205-209)
                 if (lane == 0) {
-                    if (out.cache_vals) out.cache_vals[out.slot[e]] = pruned_dist;
+                    if (out.cache_vals && !out.cache_bits) out.cache_vals[out.slot[e]] = pruned_dist;
                     if (out.dist) out.dist[e] = pruned_dist;
                     if (out.w) out.w[e] = 0.0;
                     if (out.gain) out.gain[e] = 0.0;
@@ -301,7 +308,7 @@ __global__ void __launch_bounds__(256, WPL == 1 ? 4 : NRG_K1S_MINB) ising_screen
         }
         const uint64_t e = c0 + lane;
         if (lane < len && my_code == 0) {
-            if (out.cache_vals) out.cache_vals[out.slot[e]] = pruned_dist;
+            if (out.cache_vals && !out.cache_bits) out.cache_vals[out.slot[e]] = pruned_dist;
             if (out.dist) out.dist[e] = pruned_dist;
             if (out.w) out.w[e] = 0.0;
             if (out.gain) out.gain[e] = 0.0;
@@ -530,7 +537,7 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
         }
         const uint64_t e = my_e;
         if (lane < len && my_code == 0) {
-            if (out.cache_vals) out.cache_vals[out.slot[e]] = pruned_dist;
+            if (out.cache_vals && !out.cache_bits) out.cache_vals[out.slot[e]] = pruned_dist;
             if (out.dist) out.dist[e] = pruned_dist;
             if (out.w) out.w[e] = 0.0;
             if (out.gain) out.gain[e] = 0.0;
@@ -603,7 +610,7 @@ __global__ void __launch_bounds__(128) ising_refine_kernel(IsingSnap S, HashView
     }
     if (lane == 0) {
         const double dist = -(base + r.gain);
-        if (out.cache_vals) out.cache_vals[out.slot[e]] = dist;
+        if (out.cache_vals) memo_store(out, e, dist);
         if (out.dist) out.dist[e] = dist;
         if (out.w) out.w[e] = r.w;
         if (out.gain) out.gain[e] = r.gain;
@@ -688,7 +695,7 @@ __global__ void __launch_bounds__(NT) ising_refine_cta_kernel(IsingSnap S, HashV
         __syncthreads();  // rows restaged for the next survivor
         if (threadIdx.x == 0) {
             const double dist = -(base + r.gain);
-            if (out.cache_vals) out.cache_vals[out.slot[e]] = dist;
+            if (out.cache_vals) memo_store(out, e, dist);
             if (out.dist) out.dist[e] = dist;
             if (out.w) out.w[e] = r.w;
             if (out.gain) out.gain[e] = r.gain;
@@ -778,7 +785,7 @@ __global__ void __launch_bounds__(256) gauss_screen_kernel(GaussSnap G, HashView
                 ++evals;
             }
             if (settled) {
-                if (out.cache_vals) out.cache_vals[out.slot[e]] = pruned_dist;
+                if (out.cache_vals && !out.cache_bits) out.cache_vals[out.slot[e]] = pruned_dist;
                 if (out.dist) out.dist[e] = pruned_dist;
                 if (out.w) out.w[e] = 0.0;
                 if (out.gain) out.gain[e] = 0.0;
@@ -847,7 +854,7 @@ __global__ void __launch_bounds__(256) generic_score_kernel(int kind, int mode, 
         evals += r.passes;
         warns += r.warn;
         if (lane == 0) {
-            if (out.cache_vals) out.cache_vals[out.slot[e]] = dist;
+            if (out.cache_vals) memo_store(out, e, dist);
             if (out.dist) out.dist[e] = dist;
             if (out.w) out.w[e] = r.w;
             if (out.gain) out.gain[e] = r.gain;
@@ -869,7 +876,7 @@ __global__ void metric_score_kernel(int mode, const double* __restrict__ table, 
     const int s = es[e], p = ep[e];
     const int a = s < p ? s : p, b = s < p ? p : s;
     const double d = mode == TABLE ? table[(uint64_t)a * tn + b] : fabs(pos[s] - pos[p]);
-    if (out.cache_vals) out.cache_vals[out.slot[e]] = d;
+    if (out.cache_vals) memo_store(out, e, d);
     if (out.dist) out.dist[e] = d;
 }
 
@@ -1200,10 +1207,10 @@ __global__ void probe_claim_kernel(HashView h, const int32_t* __restrict__ qi, c
     }
 }
 
-__global__ void gather_cache_kernel(const double* __restrict__ vals, const uint32_t* __restrict__ slot,
-                                    uint64_t n, double* __restrict__ out) {
+__global__ void gather_cache_kernel(MemoView C, const uint32_t* __restrict__ slot, uint64_t n,
+                                    double* __restrict__ out) {
     const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e < n) out[e] = vals[slot[e]];
+    if (e < n) out[e] = memo_value(C, slot[e]);
 }
 
 void distance_batch(Context& c, int mode, const int32_t* qi, const int32_t* qj, uint64_t n, double* dist) {
@@ -1228,9 +1235,10 @@ void distance_batch(Context& c, int mode, const int32_t* qi, const int32_t* qj, 
     nw = c.read_scalar(wcount);
     ScoreOut out;
     out.cache_vals = c.Cview().vals;
+    out.cache_bits = c.dsurvbits();
     out.slot = wslot;
     score_entries(c, mode, ws, wp, nw, out);
-    gather_cache_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(c.Cview().vals, slot, n, dist);
+    gather_cache_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(c.mview(), slot, n, dist);
     NRG_LAUNCH_CHECK();
 }
 

@@ -850,17 +850,22 @@ double generation_base(Context& c) {
 
 // ---------------------------------------------------------------- distance cache
 __global__ void cache_rehash_kernel(const uint64_t* __restrict__ ok, const double* __restrict__ ov,
-                                    uint64_t ocap, HashView nw) {
+                                    const uint32_t* __restrict__ obits, uint64_t ocap, HashView nw,
+                                    uint32_t* __restrict__ nbits) {
     const uint64_t s = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= ocap) return;
     const uint64_t k = ok[s];
     if (k == kEmptyKey) return;
+    const bool surv = (obits[s >> 5] >> (s & 31)) & 1u;  // pruned entries carry no value
     uint64_t t = slot_of(k, nw.mask);
     for (;;) {
         const unsigned long long prev =
             atomicCAS((unsigned long long*)&nw.keys[t], (unsigned long long)kEmptyKey, (unsigned long long)k);
         if (prev == kEmptyKey) {
-            nw.vals[t] = ov[s];
+            if (surv) {
+                nw.vals[t] = ov[s];
+                atomicOr(&nbits[t >> 5], 1u << (t & 31));
+            }
             return;
         }
         t = (t + 1) & nw.mask;
@@ -895,6 +900,7 @@ void cache_reserve(Context& c, uint64_t extra) {
         // lists and FindBest keys carry distances); within a generation distances are
         // deterministic, so a flushed pair is re-scored to the same value.
         NRG_CUDA(cudaMemsetAsync(c.Ckeys.p, 0xff, c.Ccap * 8, c.stream));
+        NRG_CUDA(cudaMemsetAsync(c.Csurv.p, 0, c.Ccap / 8, c.stream));
         NRG_CUDA(cudaMemsetAsync(c.Ccount.p, 0, 8, c.stream));
         c.sync();
         c.cache_flushes += 1;
@@ -906,20 +912,24 @@ void cache_reserve(Context& c, uint64_t extra) {
     const uint64_t ncap = std::max<uint64_t>(1u << 20, std::min<uint64_t>(next_pow2(2 * need), kMax));
     if (need * 100 > ncap * 85) fail(100, "distance cache: one sweep needs more than 2^31 slots");
     if (ncap == c.Ccap) return;
-    DevBuf nk, nv;
+    DevBuf nk, nv, nb;
     nk.ensure(ncap * 8);
     nv.ensure(ncap * 8);
+    nb.ensure(ncap / 8);
     NRG_CUDA(cudaMemsetAsync(nk.p, 0xff, ncap * 8, c.stream));
+    NRG_CUDA(cudaMemsetAsync(nb.p, 0, ncap / 8, c.stream));
     HashView nw{static_cast<uint64_t*>(nk.p), static_cast<double*>(nv.p), ncap - 1};
     if (c.Ccap && live) {
         cache_rehash_kernel<<<(unsigned)ceil_div(c.Ccap, 256), 256, 0, c.stream>>>(
-            static_cast<uint64_t*>(c.Ckeys.p), static_cast<double*>(c.Cvals.p), c.Ccap, nw);
+            static_cast<uint64_t*>(c.Ckeys.p), static_cast<double*>(c.Cvals.p), static_cast<uint32_t*>(c.Csurv.p),
+            c.Ccap, nw, static_cast<uint32_t*>(nb.p));
         NRG_LAUNCH_CHECK();
     }
     if (!c.Ccap) NRG_CUDA(cudaMemsetAsync(c.Ccount.p, 0, 8, c.stream));
     c.sync();
     c.Ckeys = std::move(nk);
     c.Cvals = std::move(nv);
+    c.Csurv = std::move(nb);
     c.Ccap = ncap;
 }
 
@@ -945,11 +955,14 @@ void begin_generation(Context& c) {
         if (ncap != c.Ccap && !(flushed && ncap < c.Ccap)) {
             c.Ckeys = DevBuf();
             c.Cvals = DevBuf();
+            c.Csurv = DevBuf();
             c.Ckeys.ensure(ncap * 8);
             c.Cvals.ensure(ncap * 8);
+            c.Csurv.ensure(ncap / 8);
             c.Ccap = ncap;
         }
         NRG_CUDA(cudaMemsetAsync(c.Ckeys.p, 0xff, c.Ccap * 8, c.stream));
+        NRG_CUDA(cudaMemsetAsync(c.Csurv.p, 0, c.Ccap / 8, c.stream));
         NRG_CUDA(cudaMemsetAsync(c.Ccount.p, 0, 8, c.stream));
     }
     c.cache_live_host = 0;
