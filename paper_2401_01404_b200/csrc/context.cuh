@@ -386,7 +386,10 @@ struct Context {
             return static_cast<T*>(p);
         }
     };
-    PinBuf hp_dep, hp_ord, hp_i, hp_j, hp_ch, hp_pairs, hp_small, hp_apply;
+    PinBuf hp_dep, hp_ord, hp_i, hp_j, hp_ch, hp_pairs, hp_small, hp_apply, hp_tail;
+    // device tie-tail walk (update.cu): per-node modification stamps, applied list, counts
+    DevBuf tail_mod, tail_apply, tail_cnt;
+    uint32_t tail_stamp = 0;
 
     // one device scalar read back through pinned memory (a DMA straight into the
     // host buffer; a pageable destination is staged by the driver)

@@ -533,14 +533,97 @@ __global__ void tail_start_kernel(const double* __restrict__ dist, uint64_t n, u
 }
 
 // changed[p - lo] = 1 when the re-evaluated coupling of pair p differs from the current one
+// tail[0] += changed entries, tail[1] = min(first changed, relative to lo) (set to the
+// tail length by the caller)
 __global__ void change_flags_kernel(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj, uint64_t lo,
                                     uint64_t n, const double* __restrict__ w, HashView W,
-                                    uint8_t* __restrict__ changed) {
+                                    uint8_t* __restrict__ changed, unsigned long long* __restrict__ tail) {
     const uint64_t p = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= n) return;
-    const int i = ci[p], j = cj[p];
-    const double wcur = hash_get(W, pair_key(min(i, j), max(i, j)), 0.0);
-    changed[p - lo] = w[p - lo] != wcur ? 1 : 0;
+    bool ch = false;
+    if (p < n) {
+        const int i = ci[p], j = cj[p];
+        const double wcur = hash_get(W, pair_key(min(i, j), max(i, j)), 0.0);
+        ch = w[p - lo] != wcur;
+        changed[p - lo] = ch ? 1 : 0;
+    }
+    if (!tail) return;
+    const unsigned b = __ballot_sync(0xffffffffu, ch);
+    if ((threadIdx.x & 31) == 0 && b) {
+        atomicAdd(&tail[0], (unsigned long long)__popc(b));
+        atomicMin(&tail[1], (unsigned long long)(p - lo + (__ffs(b) - 1)));
+    }
+}
+
+__global__ void tail_init_kernel(unsigned long long* tail, uint64_t m) {
+    tail[0] = 0;
+    tail[1] = m;
+    tail[2] = 0;
+    tail[3] = 0;
+}
+
+// One tie-tail round's walk (the sequential semantics of apply_updates, on the device):
+// from the first changing entry, every changing entry is applied until the first entry
+// (changing or not) that touches a node an applied entry modified; that entry starts the
+// next round.  One CTA, 1024 entries per step: conflicts with earlier steps through a
+// per-node stamp, within the step against the step's changing entries (at most the
+// round's change budget, kTailRounds).  tail[2] = applied count, tail[3] = stop (absolute).
+__global__ void __launch_bounds__(1024) tail_walk_kernel(const int32_t* __restrict__ ci,
+                                                          const int32_t* __restrict__ cj, uint64_t lo, uint64_t n,
+                                                          const uint8_t* __restrict__ changed,
+                                                          uint32_t* __restrict__ mod, uint32_t stamp,
+                                                          uint32_t* __restrict__ apply,
+                                                          unsigned long long* __restrict__ tail) {
+    __shared__ int s_a[1024], s_b[1024], s_pos[1024];
+    __shared__ int s_nch, s_stop;
+    const int tid = threadIdx.x;
+    uint64_t na = 0;
+    const uint64_t first = tail[1];
+    for (uint64_t base = lo + first; base < n; base += 1024) {
+        const uint64_t p = base + tid;
+        const bool valid = p < n;
+        const int a = valid ? ci[p] : -1, b = valid ? cj[p] : -1;
+        const bool ch = valid && changed[p - lo];
+        bool conf = valid && (mod[a] == stamp || mod[b] == stamp);
+        if (tid == 0) {
+            s_nch = 0;
+            s_stop = 1024;
+        }
+        __syncthreads();
+        if (ch) {
+            const int q = atomicAdd(&s_nch, 1);
+            s_a[q] = a;
+            s_b[q] = b;
+            s_pos[q] = tid;
+        }
+        __syncthreads();
+        const int nch = s_nch;
+        for (int q = 0; q < nch; ++q)
+            if (s_pos[q] < tid && (a == s_a[q] || a == s_b[q] || b == s_a[q] || b == s_b[q])) conf = true;
+        if (conf) atomicMin(&s_stop, tid);
+        __syncthreads();
+        const int stop = s_stop;
+        // applied: the changing entries before the stop, in list order
+        int before = 0;
+        for (int q = 0; q < nch; ++q) before += s_pos[q] < stop && s_pos[q] < tid ? 1 : 0;
+        if (ch && tid < stop) {
+            apply[na + before] = (uint32_t)p;
+            mod[a] = stamp;
+            mod[b] = stamp;
+        }
+        for (int q = 0; q < nch; ++q) na += s_pos[q] < stop ? 1 : 0;
+        __syncthreads();  // stamps visible to the next step
+        if (stop < 1024) {
+            if (tid == 0) {
+                tail[2] = na;
+                tail[3] = base + (uint64_t)stop;
+            }
+            return;
+        }
+    }
+    if (tid == 0) {
+        tail[2] = na;
+        tail[3] = n;
+    }
 }
 
 __global__ void gather_pairs_kernel(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj,
@@ -612,12 +695,29 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
     ordered_run(c, ci, cj, k, assign, absdelta, !fb_sorted || fb_level);
     uint64_t start = k;
     if (start < n) {
+        // the round's walk runs on the device (tail_walk_kernel: one readback per round);
+        // NRG_HOST_TAIL_WALK=1 walks the change flags on the host instead (A/B, same result)
+        static const bool host_walk = NRG_ENV_ON("NRG_HOST_TAIL_WALK");
         const uint64_t nt = n - start;
-        int32_t* hi = c.hp_i.as<int32_t>(nt);
-        int32_t* hj = c.hp_j.as<int32_t>(nt);
-        uint8_t* hch = c.hp_ch.as<uint8_t>(nt);
-        NRG_CUDA(cudaMemcpyAsync(hi, ci + start, nt * 4, cudaMemcpyDeviceToHost, c.stream));
-        NRG_CUDA(cudaMemcpyAsync(hj, cj + start, nt * 4, cudaMemcpyDeviceToHost, c.stream));
+        int32_t* hi = host_walk ? c.hp_i.as<int32_t>(nt) : nullptr;
+        int32_t* hj = host_walk ? c.hp_j.as<int32_t>(nt) : nullptr;
+        uint8_t* hch = host_walk ? c.hp_ch.as<uint8_t>(nt) : nullptr;
+        if (host_walk) {
+            NRG_CUDA(cudaMemcpyAsync(hi, ci + start, nt * 4, cudaMemcpyDeviceToHost, c.stream));
+            NRG_CUDA(cudaMemcpyAsync(hj, cj + start, nt * 4, cudaMemcpyDeviceToHost, c.stream));
+        }
+        unsigned long long* tail = c.tail_cnt.as<unsigned long long>(4);
+        unsigned long long* htail = c.hp_tail.as<unsigned long long>(4);
+        uint32_t* mod_dev = nullptr;
+        if (!host_walk) {
+            if (!c.tail_mod.p) {
+                mod_dev = c.tail_mod.as<uint32_t>((uint64_t)c.n);
+                NRG_CUDA(cudaMemsetAsync(mod_dev, 0, (size_t)c.n * 4, c.stream));
+                c.tail_stamp = 0;
+            }
+            mod_dev = static_cast<uint32_t*>(c.tail_mod.p);
+        }
+        uint32_t* apply_dev = host_walk ? nullptr : c.tail_apply.as<uint32_t>(nt);
         std::vector<uint8_t> mod(c.n, 0);
         std::vector<int32_t> touched;
         std::vector<uint32_t> apply;
@@ -660,7 +760,48 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
             score_entries(c, EXACT, ci + start, cj + start, m, out);  // times itself as P_SCORE
             c.tic();
             uint8_t* ch = fb.as<uint8_t>(m);
-            change_flags_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, c.stream>>>(ci, cj, start, n, w, c.Wview(), ch);
+            if (!host_walk) {
+                tail_init_kernel<<<1, 1, 0, c.stream>>>(tail, m);
+                change_flags_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, c.stream>>>(ci, cj, start, n, w, c.Wview(),
+                                                                                      ch, tail);
+                tail_walk_kernel<<<1, 1024, 0, c.stream>>>(ci, cj, start, n, ch, mod_dev, ++c.tail_stamp, apply_dev,
+                                                           tail);
+                NRG_LAUNCH_CHECK_N(3);
+                NRG_CUDA(cudaMemcpyAsync(htail, tail, 32, cudaMemcpyDeviceToHost, c.stream));
+                c.sync();
+                c.tail_rounds++;
+                const uint64_t nch = htail[0], na = htail[2], stop = htail[3];
+                if (NRG_ENV_ON("NRG_DEBUG_TAIL"))
+                    fprintf(stderr, "tail round %d: start=%llu m=%llu changed=%llu applied=%llu stop=%llu\n", round,
+                            (unsigned long long)start, (unsigned long long)m, (unsigned long long)nch,
+                            (unsigned long long)na, (unsigned long long)stop);
+                if (nch > (uint64_t)(kTailRounds - round)) {
+                    ordered_run(c, ci + start, cj + start, m, nullptr, absdelta + start);
+                    break;
+                }
+                if (na) {
+                    int32_t* pi = pib.as<int32_t>(na);
+                    int32_t* pj = pjb.as<int32_t>(na);
+                    double* dd = ddb.as<double>(na);
+                    gather_pairs_kernel<<<ceil_div(na, 256), 256, 0, c.stream>>>(ci, cj, apply_dev, (uint32_t)na, pi,
+                                                                                pj);
+                    NRG_LAUNCH_CHECK();
+                    ordered_run(c, pi, pj, na, nullptr, dd);
+                    scatter_delta_kernel<<<ceil_div(na, 256), 256, 0, c.stream>>>(dd, apply_dev, (uint32_t)na,
+                                                                                 absdelta);
+                    NRG_LAUNCH_CHECK();
+                    rows_dev = rowsb.as<int32_t>(2 * (size_t)na);
+                    NRG_CUDA(cudaMemcpyAsync(rows_dev, pi, na * 4, cudaMemcpyDeviceToDevice, c.stream));
+                    NRG_CUDA(cudaMemcpyAsync(rows_dev + na, pj, na * 4, cudaMemcpyDeviceToDevice, c.stream));
+                    n_rows = 2 * na;
+                } else {
+                    n_rows = 0;
+                }
+                start = stop;
+                continue;
+            }
+            change_flags_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, c.stream>>>(ci, cj, start, n, w, c.Wview(), ch,
+                                                                                  nullptr);
             NRG_LAUNCH_CHECK();
             NRG_CUDA(cudaMemcpyAsync(hch, ch, m, cudaMemcpyDeviceToHost, c.stream));
             c.sync();

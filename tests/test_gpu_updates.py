@@ -231,3 +231,23 @@ def test_packed_spin_upload_equals_int8(gpu):
     rb, cb = b.gcd_iteration(0, kappa=2.0, seed=3, want_candidates=True)
     np.testing.assert_array_equal(ca, cb)
     assert ra["objective"] == rb["objective"]
+
+
+def test_device_tail_walk_equals_host_walk(gpu, monkeypatch):
+    """The tie-tail round's walk on the device (tail_walk_kernel) applies exactly the pairs
+    the host walk applied (NRG_HOST_TAIL_WALK=1): identical reconstructions, bitwise."""
+    def run(host):
+        if host:
+            monkeypatch.setenv("NRG_HOST_TAIL_WALK", "1")
+        else:
+            monkeypatch.delenv("NRG_HOST_TAIL_WALK", raising=False)
+        m = gpu.Model(3000, 400, gpu.NRG_ISING, O.ising_lambda(3000, 400))
+        m.generate_ising(mean_deg=4.0, seed=7)
+        m.reset_counters()
+        recs = [m.gcd_iteration(it, kappa=2.0, seed=5)[0] for it in range(5)]
+        return m.get_state(), [(r["delta"], r["objective"]) for r in recs], m.kernel_stats()["tail_rounds"]
+    a, b = run(False), run(True)
+    assert a[2] > 0 and a[2] == b[2]
+    assert a[1] == b[1]
+    for x, y in zip(a[0], b[0]):
+        np.testing.assert_array_equal(x, y)

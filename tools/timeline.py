@@ -15,12 +15,13 @@ if CFG5:
 else:
     m.generate_ising(mean_deg=5.0, seed=1)
 m.reset_state()
-for it in range(3):
+PRE = int(os.environ.get("TIMELINE_SWEEP", "3"))  # sweeps before the profiled one
+for it in range(PRE):
     m.gcd_iteration(it, kappa=2.0, seed=1)
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
     m.timer_start()
-    m.gcd_iteration(3, kappa=2.0, seed=1)
+    m.gcd_iteration(PRE, kappa=2.0, seed=1)
     ms = m.timer_stop()
 out = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/timeline.json"
 prof.export_chrome_trace(out)
