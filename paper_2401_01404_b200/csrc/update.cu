@@ -407,23 +407,29 @@ static int update_grid(Context& c, size_t smem) {
 
 // The dependency-ordered kernel over candidates [0, n) of (ci, cj): |w - w_cur| per
 // pair into absdelta.
+// disjoint: the caller guarantees the pairs share no node (a tie-tail round's applied
+// set), so no pair waits on another: every dependency is empty without the sort
 static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n, const double* assign,
-                        double* absdelta, bool level_order = true) {
+                        double* absdelta, bool level_order = true, bool disjoint = false) {
     if (n == 0) return;
     DevBuf kb, vb, k2b, v2b, depb, doneb, tb, tmpb;
-    uint64_t* keys = kb.as<uint64_t>(2 * n);
-    uint32_t* vals = vb.as<uint32_t>(2 * n);
-    uint64_t* keys2 = k2b.as<uint64_t>(2 * n);
-    uint32_t* vals2 = v2b.as<uint32_t>(2 * n);
     int32_t* dep = depb.as<int32_t>(2 * n);
     int* done = doneb.as<int>(n);
     unsigned long long* ticket = tb.as<unsigned long long>(1);
-    dep_keys_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(ci, cj, n, keys, vals);
-    size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, keys2, vals, vals2, (int64_t)(2 * n), 0, 64, c.stream);
-    void* tmp = tmpb.ensure(bytes);
-    cub::DeviceRadixSort::SortPairs(tmp, bytes, keys, keys2, vals, vals2, (int64_t)(2 * n), 0, 64, c.stream);
-    dep_link_kernel<<<(unsigned)ceil_div(2 * n, 256), 256, 0, c.stream>>>(keys2, vals2, 2 * n, dep);
+    if (disjoint) {
+        NRG_CUDA(cudaMemsetAsync(dep, 0xff, 8 * n, c.stream));  // -1: no predecessor
+    } else {
+        uint64_t* keys = kb.as<uint64_t>(2 * n);
+        uint32_t* vals = vb.as<uint32_t>(2 * n);
+        uint64_t* keys2 = k2b.as<uint64_t>(2 * n);
+        uint32_t* vals2 = v2b.as<uint32_t>(2 * n);
+        dep_keys_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(ci, cj, n, keys, vals);
+        size_t bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, keys2, vals, vals2, (int64_t)(2 * n), 0, 64, c.stream);
+        void* tmp = tmpb.ensure(bytes);
+        cub::DeviceRadixSort::SortPairs(tmp, bytes, keys, keys2, vals, vals2, (int64_t)(2 * n), 0, 64, c.stream);
+        dep_link_kernel<<<(unsigned)ceil_div(2 * n, 256), 256, 0, c.stream>>>(keys2, vals2, 2 * n, dep);
+    }
     NRG_CUDA(cudaMemsetAsync(done, 0, n * 4, c.stream));
     NRG_CUDA(cudaMemsetAsync(ticket, 0, 8, c.stream));
     NRG_LAUNCH_CHECK();
@@ -435,7 +441,7 @@ static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64
     DevBuf ordb;
     uint32_t* order = nullptr;
     size_t nlevels = 0;
-    if (n >= 4096 && level_order && !NRG_ENV_ON("NRG_LIST_ORDER_TICKETS")) {
+    if (n >= 4096 && level_order && !disjoint && !NRG_ENV_ON("NRG_LIST_ORDER_TICKETS")) {
         int32_t* hdep = c.hp_dep.as<int32_t>(2 * n);
         NRG_CUDA(cudaMemcpyAsync(hdep, dep, 8 * n, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
@@ -786,7 +792,7 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
                     gather_pairs_kernel<<<ceil_div(na, 256), 256, 0, c.stream>>>(ci, cj, apply_dev, (uint32_t)na, pi,
                                                                                 pj);
                     NRG_LAUNCH_CHECK();
-                    ordered_run(c, pi, pj, na, nullptr, dd);
+                    ordered_run(c, pi, pj, na, nullptr, dd, true, /*disjoint=*/true);
                     scatter_delta_kernel<<<ceil_div(na, 256), 256, 0, c.stream>>>(dd, apply_dev, (uint32_t)na,
                                                                                  absdelta);
                     NRG_LAUNCH_CHECK();
