@@ -311,6 +311,8 @@ class Model:
         ej = np.zeros(max(k, 1), np.int32)
         w = np.zeros(max(k, 1))
         check(self.L.nrg_get_state(self.h, th, k, ei, ej, w, C.byref(ne)))
+        if ne.value != k:
+            raise RuntimeError(f"get_state: {ne.value} couplings, {k} counted")
         return th, ei[:k], ej[:k], w[:k]
 
     def get_sums(self):

@@ -394,9 +394,21 @@ __global__ void w_live_kernel(const uint64_t* __restrict__ keys, const double* _
     }
 }
 
+__global__ void split_keys_kernel(const uint64_t* __restrict__ k, uint64_t n, int ib, int32_t* __restrict__ oi,
+                                  int32_t* __restrict__ oj) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    oi[t] = (int32_t)(k[t] >> ib);
+    oj[t] = (int32_t)(k[t] & ((1ull << ib) - 1));
+}
+
 void get_state(Context& c, double* theta, uint64_t cap, int32_t* ei, int32_t* ej, double* w,
                uint64_t* n_edges) {
     if (theta) NRG_CUDA(cudaMemcpyAsync(theta, c.theta.p, c.n * 8, cudaMemcpyDeviceToHost, c.stream));
+    if (cap == 0) {  // count only: the table's live counter (no scan)
+        *n_edges = c.read_scalar(static_cast<const uint64_t*>(c.Wcount.p));
+        return;
+    }
     int ib = 1;
     while (ib < 31 && (1ll << ib) < (long long)c.n) ++ib;
     DevBuf kb, vb, cb, tb;
@@ -420,15 +432,15 @@ void get_state(Context& c, double* theta, uint64_t cap, int32_t* ei, int32_t* ej
     void* tmp = tb.ensure(bytes);
     cub::DeviceRadixSort::SortPairs(tmp, bytes, k0, k1, v0, v1, (int64_t)ne, 0, 2 * ib, c.stream);
     NRG_LAUNCH_CHECK();
-    std::vector<uint64_t> hk(take);
-    NRG_CUDA(cudaMemcpyAsync(hk.data(), k1, take * 8, cudaMemcpyDeviceToHost, c.stream));
+    // (i, j) split on the device (k0 is free again: it holds the int32 pairs now)
+    int32_t* di = reinterpret_cast<int32_t*>(k0);
+    int32_t* dj = di + take;
+    split_keys_kernel<<<(unsigned)ceil_div(take, 256), 256, 0, c.stream>>>(k1, take, ib, di, dj);
+    NRG_LAUNCH_CHECK();
+    if (ei) NRG_CUDA(cudaMemcpyAsync(ei, di, take * 4, cudaMemcpyDeviceToHost, c.stream));
+    if (ej) NRG_CUDA(cudaMemcpyAsync(ej, dj, take * 4, cudaMemcpyDeviceToHost, c.stream));
     if (w) NRG_CUDA(cudaMemcpyAsync(w, v1, take * 8, cudaMemcpyDeviceToHost, c.stream));
     c.sync();
-    const uint64_t m = (1ull << ib) - 1;
-    for (uint64_t t = 0; t < take; ++t) {
-        if (ei) ei[t] = (int32_t)(hk[t] >> ib);
-        if (ej) ej[t] = (int32_t)(hk[t] & m);
-    }
 }
 
 void get_sums(Context& c, double* out) {
