@@ -521,6 +521,10 @@ def run_ours(args, rank, world, local, dist):
                                      "status": "void: 4-bit planes + L1/L2 reuse of partner rows (model bytes "
                                                "exceed what HBM could stream)"},
                      "issue": issue, "binding": "instruction issue" if issue else None,
+                     "summary": (f"K1 moves {dram_per_pair:.0f} B of DRAM per pair (partner rows are L2-resident, "
+                                 f"pruned pairs write nothing): HBM is not its bound; it runs at "
+                                 f"{issue['frac']:.2f} of the SM instruction-issue peak" if issue and dram_per_pair
+                                 else None),
                      "note": (None if traffic else
                               "no ncu capture for this configuration: achieved counts the model bytes; above the "
                               "HBM peak they are served from L2 (the partner rows of N = 1e4 fit in it)"
