@@ -386,15 +386,7 @@ struct Context {
             return static_cast<T*>(p);
         }
     };
-    PinBuf hp_dep, hp_ord, hp_i, hp_j, hp_ch, hp_pairs, hp_small, hp_apply, hp_tail, hp_churn;
-    // two reusable events marking the end of speculative NNDescent sweeps (knn.cu)
-    cudaEvent_t sweep_ev_[2] = {nullptr, nullptr};
-    void sweep_events(cudaEvent_t* ev) {
-        for (int t = 0; t < 2; ++t) {
-            if (!sweep_ev_[t]) NRG_CUDA(cudaEventCreateWithFlags(&sweep_ev_[t], cudaEventDisableTiming));
-            ev[t] = sweep_ev_[t];
-        }
-    }
+    PinBuf hp_dep, hp_ord, hp_i, hp_j, hp_ch, hp_pairs, hp_small, hp_apply, hp_tail;
     // device tie-tail walk (update.cu): per-node modification stamps, applied list, counts
     DevBuf tail_mod, tail_apply, tail_cnt;
     uint32_t tail_stamp = 0;

@@ -379,9 +379,7 @@ __global__ void answer_kernel(MemoView vals, const uint32_t* __restrict__ slot_o
 // ---------------------------------------------------------------- U (capped undirected view)
 // out-part: rows of the (sorted) snapshot; in-part appended while rows have room
 __global__ void u_out_kernel(const int32_t* __restrict__ gid, uint64_t n, int kw, int cap,
-                             int32_t* __restrict__ adj, int32_t* __restrict__ alen,
-    const int* __restrict__ gate) {
-    if (gate && *gate) return;  // a speculative sweep after the churn test stopped the loop
+                             int32_t* __restrict__ adj, int32_t* __restrict__ alen) {
     const uint64_t li = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (li >= n) return;
     for (int t = 0; t < kw; ++t) adj[li * cap + t] = gid[li * kw + t];
@@ -461,9 +459,7 @@ __global__ void u_rev_kernel(const uint32_t* __restrict__ tgt_sorted, const int3
 // generation, so it cannot enter now and the gather skips it.  One warp per node.
 __global__ void u_new_kernel(const int32_t* __restrict__ adj, const int32_t* __restrict__ alen,
                              const int32_t* __restrict__ adjp, const int32_t* __restrict__ alenp, uint64_t n,
-                             int cap, int first, uint8_t* __restrict__ newf,
-    const int* __restrict__ gate) {
-    if (gate && *gate) return;  // a speculative sweep after the churn test stopped the loop
+                             int cap, int first, uint8_t* __restrict__ newf) {
     const uint64_t li = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (li >= n) return;
@@ -490,9 +486,7 @@ __global__ void __launch_bounds__(NT) knn_gather_kernel(const int32_t* __restric
                                                         uint64_t capn, int32_t* __restrict__ cand_id,
                                                         uint32_t* __restrict__ cand_slot,
                                                         int32_t* __restrict__ cand_cnt, uint64_t lo, int lw,
-                                                        const uint8_t* __restrict__ newf, bool do_claim,
-    const int* __restrict__ gate) {
-    if (gate && *gate) return;  // a speculative sweep after the churn test stopped the loop
+                                                        const uint8_t* __restrict__ newf, bool do_claim) {
     extern __shared__ int32_t tab[];
     __shared__ int ncand;
     const uint64_t li = lo + blockIdx.x;
@@ -574,9 +568,7 @@ __global__ void __launch_bounds__(32 * WPB) knn_gather_warp_kernel(
     const int32_t* __restrict__ nodes, uint64_t n, const int32_t* __restrict__ adj, const int32_t* __restrict__ alen,
     int cap, const int32_t* __restrict__ gid, int kw, bool bitmap, int tsize, HashView h, ClaimSink sink,
     uint64_t capn, int32_t* __restrict__ cand_id, uint32_t* __restrict__ cand_slot, int32_t* __restrict__ cand_cnt,
-    uint64_t lo, uint64_t own, int lw, const uint8_t* __restrict__ newf, bool do_claim,
-    const int* __restrict__ gate) {
-    if (gate && *gate) return;  // a speculative sweep after the churn test stopped the loop
+    uint64_t lo, uint64_t own, int lw, const uint8_t* __restrict__ newf, bool do_claim) {
     extern __shared__ int32_t tab_all[];
     __shared__ int ncand_s[WPB];
     const int wid = threadIdx.x >> 5, tid = threadIdx.x & 31;
@@ -653,9 +645,7 @@ __global__ void __launch_bounds__(32 * WPB) knn_gather_warp_kernel(
 // table for exactly this sweep's candidates)
 __global__ void claim_cands_kernel(const int32_t* __restrict__ nodes, HashView h, ClaimSink sink, uint64_t own,
                                    uint64_t lo, uint64_t capn, const int32_t* __restrict__ cand_id,
-                                   uint32_t* __restrict__ cand_slot, const int32_t* __restrict__ cand_cnt,
-    const int* __restrict__ gate) {
-    if (gate && *gate) return;  // a speculative sweep after the churn test stopped the loop
+                                   uint32_t* __restrict__ cand_slot, const int32_t* __restrict__ cand_cnt) {
     const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= own) return;
@@ -676,9 +666,7 @@ __global__ void claim_cands_kernel(const int32_t* __restrict__ nodes, HashView h
 // thousands of dependent cache probes one chunk at a time)
 __global__ void claim_cands_flat_kernel(const int32_t* __restrict__ nodes, HashView h, ClaimSink sink, uint64_t own,
                                         uint64_t lo, uint64_t capn, const int32_t* __restrict__ cand_id,
-                                        uint32_t* __restrict__ cand_slot, const int32_t* __restrict__ cand_cnt,
-    const int* __restrict__ gate) {
-    if (gate && *gate) return;  // a speculative sweep after the churn test stopped the loop
+                                        uint32_t* __restrict__ cand_slot, const int32_t* __restrict__ cand_cnt) {
     const uint64_t li = lo + blockIdx.x;
     const int cnt = cand_cnt[li];
     const int t = (int)blockIdx.y * blockDim.x + threadIdx.x;
@@ -707,9 +695,7 @@ __global__ void sum_counts_kernel(const int32_t* __restrict__ cnt, uint64_t n, u
 // bit-set levels: U(i) as a bitset, then the new flags against last sweep's bitset (the
 // set semantics of u_new_kernel, O(1) per entry) and the bitset of new entries
 __global__ void u_set_kernel(const int32_t* __restrict__ adj, const int32_t* __restrict__ alen, uint64_t n, int cap,
-                             int W, uint32_t* __restrict__ ub,
-    const int* __restrict__ gate) {
-    if (gate && *gate) return;  // a speculative sweep after the churn test stopped the loop
+                             int W, uint32_t* __restrict__ ub) {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n * (uint64_t)cap) return;
     const uint64_t i = t / cap;
@@ -720,9 +706,7 @@ __global__ void u_set_kernel(const int32_t* __restrict__ adj, const int32_t* __r
 __global__ void u_new_bits_kernel(const int32_t* __restrict__ adj, const int32_t* __restrict__ alen, uint64_t n,
                                   int cap, int W, const uint32_t* __restrict__ ubp, int first,
                                   uint8_t* __restrict__ newf, uint32_t* __restrict__ nb,
-                                  uint8_t* __restrict__ hasnew,
-    const int* __restrict__ gate) {
-    if (gate && *gate) return;  // a speculative sweep after the churn test stopped the loop
+                                  uint8_t* __restrict__ hasnew) {
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n * (uint64_t)cap) return;
     const uint64_t i = t / cap;
@@ -749,9 +733,7 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
                                                              uint32_t* __restrict__ cand_slot,
                                                              int32_t* __restrict__ cand_cnt, uint64_t lo, bool do_claim,
                                                              const int32_t* __restrict__ rootpos,
-                                                             const uint8_t* __restrict__ hasnew,
-    const int* __restrict__ gate) {
-    if (gate && *gate) return;  // a speculative sweep after the churn test stopped the loop
+                                                             const uint8_t* __restrict__ hasnew) {
     extern __shared__ uint32_t bits_smem[];
     uint32_t* acc = bits_smem;     // OR of the 2-hop rows
     uint32_t* excl = acc + W;      // i's current row and i itself
@@ -891,9 +873,7 @@ __global__ void __launch_bounds__(NT) knn_merge_kernel(const int32_t* __restrict
                                                        const int32_t* __restrict__ cand_cnt, uint64_t capn,
                                                        DenseView D, MemoView cvals,
                                                        const double* __restrict__ rvals, int buf_cap,
-                                                       unsigned long long* __restrict__ churn, uint64_t lo,
-    const int* __restrict__ gate) {
-    if (gate && *gate) return;  // a speculative sweep after the churn test stopped the loop
+                                                       unsigned long long* __restrict__ churn, uint64_t lo) {
     extern __shared__ unsigned char smem_raw[];
     double* bd = reinterpret_cast<double*>(smem_raw);
     double* od = bd + buf_cap;                               // selected row (kw)
@@ -1014,9 +994,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) knn_merge_warp_kernel(
     const int32_t* __restrict__ nodes, uint64_t n, int32_t* __restrict__ gid, double* __restrict__ gd, int kw,
     const int32_t* __restrict__ cand_id, const uint32_t* __restrict__ cand_slot,
     const int32_t* __restrict__ cand_cnt, uint64_t capn, DenseView D, MemoView cvals,
-    const double* __restrict__ rvals, unsigned long long* __restrict__ churn, uint64_t lo, uint64_t own,
-    const int* __restrict__ gate) {
-    if (gate && *gate) return;  // a speculative sweep after the churn test stopped the loop
+    const double* __restrict__ rvals, unsigned long long* __restrict__ churn, uint64_t lo, uint64_t own) {
     extern __shared__ unsigned char merge_warp_smem[];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const uint64_t node = (uint64_t)blockIdx.x * kMergeWarps + wib;
@@ -1328,16 +1306,6 @@ static void score_claimed(Context& c, int mode, int32_t* ws, int32_t* wp, uint32
     score_entries(c, mode, ws, wp, nw, so);
 }
 
-// the churn test of one NNDescent sweep on the device (the host's ratio < eps, same
-// arithmetic): records the sweep's churn and, if it stops the loop, gates the sweep the
-// host already queued behind it
-__global__ void churn_gate_kernel(const unsigned long long* __restrict__ churn, double denom, double eps,
-                                  int* __restrict__ gate, unsigned long long* __restrict__ hist) {
-    const unsigned long long ch = *churn;
-    *hist = ch;
-    if ((double)ch / denom < eps) *gate = 1;
-}
-
 void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, const KnnParamsD& p,
               bool exhaustive, KnnResultD& out, DevBuf& ids_buf, DevBuf& dist_buf, bool sorted_valid) {
     if (n < 2) fail(22, exhaustive ? "find_knn_exhaustive: need two nodes" : "find_knn: need at least two nodes");
@@ -1605,25 +1573,10 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
     out.sweeps = 0;
     out.churn.clear();
     DevBuf ktgt, kd, ksrc, vsrc, ktgt2, kd2, ksrc2, vsrc2, segb, sorttmp, permb, perm2b;
-    // Speculative sweeps (single rank): the host queues sweep s + 1 before it reads sweep
-    // s's churn, so the device never idles at a sweep boundary or while the host refills
-    // a drained queue; a one-thread kernel after each merge applies the churn test on the
-    // device and, when it stops the loop, gates the already-queued sweep's kernels into
-    // no-ops (its memsets touch scratch only).  Same sweeps, graphs and churn trace.
-    const bool spec = c.world == 1 && !NRG_ENV_ON("NRG_NO_SPEC_SWEEP");
-    DevBuf gateb, histb;
-    int* gate = gateb.as<int>(1);
-    unsigned long long* hist = histb.as<unsigned long long>((uint64_t)p.max_sweeps + 1);
-    NRG_CUDA(cudaMemsetAsync(gate, 0, 4, c.stream));
-    unsigned long long* hh = c.hp_churn.as<unsigned long long>((uint64_t)p.max_sweeps + 1);
-    cudaEvent_t sweep_ev[2];
-    if (spec) {
-        c.sweep_events(sweep_ev);
-    }
-    auto run_sweep = [&](int sweep) {
+    for (int sweep = 0; sweep < p.max_sweeps; ++sweep) {
         c.tic();
         // U
-        u_out_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, c.stream>>>(gid, n, kw, cap, adj, alen, gate);
+        u_out_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, c.stream>>>(gid, n, kw, cap, adj, alen);
         NRG_LAUNCH_CHECK();
         if (cap > kw) {
             const uint64_t ne = n * kw;
@@ -1662,13 +1615,13 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             NRG_CUDA(cudaMemsetAsync(nbits, 0, n * (uint64_t)Wb * 4, c.stream));
             NRG_CUDA(cudaMemsetAsync(hasnew, 0, n, c.stream));
             const unsigned g = (unsigned)ceil_div(n * (uint64_t)cap, 256);
-            u_set_kernel<<<g, 256, 0, c.stream>>>(adj, alen, n, cap, Wb, ubc, gate);
+            u_set_kernel<<<g, 256, 0, c.stream>>>(adj, alen, n, cap, Wb, ubc);
             u_new_bits_kernel<<<g, 256, 0, c.stream>>>(adj, alen, n, cap, Wb, ubp,
-                                                      (sweep == 0 || !incremental) ? 1 : 0, newf, nbits, hasnew, gate);
+                                                      (sweep == 0 || !incremental) ? 1 : 0, newf, nbits, hasnew);
         } else {
             u_new_kernel<<<(unsigned)ceil_div(n * 32, 256), 256, 0, c.stream>>>(adj, alen, adjp, alenp, n, cap,
                                                                              (sweep == 0 || !incremental) ? 1 : 0,
-                                                                             newf, gate);
+                                                                             newf);
         }
         NRG_LAUNCH_CHECK();
         c.toc(P_KNN);
@@ -1699,19 +1652,19 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                 uint32_t* nbits = static_cast<uint32_t*>(nbitsb.p);
                 knn_gather_bits_kernel<256><<<(unsigned)own, 256, 2 * W * 4 + 4 * cap, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, W, ub, nbits, newf, hv0, sk, capn, cand_id, cand_slot, cand_cnt,
-                    lo, fused, rootpos, static_cast<const uint8_t*>(hasnewb.p), gate);
+                    lo, fused, rootpos, static_cast<const uint8_t*>(hasnewb.p));
             } else if (big)
                 knn_gather_kernel<256><<<(unsigned)own, 256, tab_bytes, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv0, sk, capn, cand_id,
-                    cand_slot, cand_cnt, lo, lw, newf, fused, gate);
+                    cand_slot, cand_cnt, lo, lw, newf, fused);
             else if (!NRG_ENV_ON("NRG_GATHER_CTA") && tab_bytes * 4 <= 48 * 1024)
                 knn_gather_warp_kernel<4><<<(unsigned)ceil_div(own, 4), 128, 4 * tab_bytes, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv0, sk, capn, cand_id,
-                    cand_slot, cand_cnt, lo, own, lw, newf, fused, gate);
+                    cand_slot, cand_cnt, lo, own, lw, newf, fused);
             else
                 knn_gather_kernel<32><<<(unsigned)own, 32, tab_bytes, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv0, sk, capn, cand_id,
-                    cand_slot, cand_cnt, lo, lw, newf, fused, gate);
+                    cand_slot, cand_cnt, lo, lw, newf, fused);
             NRG_LAUNCH_CHECK();
         }
         if (cached && !fused) {
@@ -1731,10 +1684,10 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             if (own) {
                 if (capn > 256)
                     claim_cands_flat_kernel<<<dim3((unsigned)own, (unsigned)ceil_div(capn, 256)), 256, 0, c.stream>>>(
-                        d_nodes, c.Cview(), sk, own, lo, capn, cand_id, cand_slot, cand_cnt, gate);
+                        d_nodes, c.Cview(), sk, own, lo, capn, cand_id, cand_slot, cand_cnt);
                 else
                     claim_cands_kernel<<<(unsigned)ceil_div(own * 32, 256), 256, 0, c.stream>>>(
-                        d_nodes, c.Cview(), sk, own, lo, capn, cand_id, cand_slot, cand_cnt, gate);
+                        d_nodes, c.Cview(), sk, own, lo, capn, cand_id, cand_slot, cand_cnt);
                 NRG_LAUNCH_CHECK();
             }
         }
@@ -1772,54 +1725,31 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         if (own) {
             if (kw > 64)
                 knn_merge_kernel<128><<<(unsigned)own, 128, merge_smem, c.stream>>>(
-                    d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dview, dvals, rvals, buf_cap, churn, lo, gate);
+                    d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dview, dvals, rvals, buf_cap, churn, lo);
             else if (!NRG_ENV_ON("NRG_MERGE_CTA"))
                 knn_merge_warp_kernel<<<(unsigned)ceil_div(own, kMergeWarps), 32 * kMergeWarps,
                                         (size_t)kMergeWarps * (2 * kw + kMergeBlk) * 20, c.stream>>>(
-                    d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dview, dvals, rvals, churn, lo, own, gate);
+                    d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dview, dvals, rvals, churn, lo, own);
             else
                 knn_merge_kernel<32><<<(unsigned)own, 32, merge_smem, c.stream>>>(
-                    d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dview, dvals, rvals, buf_cap, churn, lo, gate);
+                    d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dview, dvals, rvals, buf_cap, churn, lo);
             NRG_LAUNCH_CHECK();
         }
-        if (spec) {
-            churn_gate_kernel<<<1, 1, 0, c.stream>>>(churn, (double)kw * (double)n, p.eps, gate, hist + sweep);
-            NRG_LAUNCH_CHECK();
-            NRG_CUDA(cudaMemcpyAsync(hh + sweep, hist + sweep, 8, cudaMemcpyDeviceToHost, c.stream));
-            NRG_CUDA(cudaEventRecord(sweep_ev[sweep & 1], c.stream));
+        unsigned long long changed = 0;
+        changed = c.read_scalar(churn);
+        allgather_rows(gid, gd, kw);
+        if (c.world > 1) {
+            uint64_t ch = changed;
+            static_cast<Comm*>(c.comm)->allreduce_u64(&ch, 1, false, c.stream);
+            changed = ch;
         }
         c.toc(P_KNN);
         std::swap(adj, adjp);  // this sweep's U is the next sweep's "previous"
         std::swap(alen, alenp);
-    };
-    if (spec) {
-        run_sweep(0);
-        for (int sweep = 0;; ++sweep) {
-            const bool ahead = sweep + 1 < p.max_sweeps;
-            if (ahead) run_sweep(sweep + 1);  // queued before this sweep's churn is known
-            NRG_CUDA(cudaEventSynchronize(sweep_ev[sweep & 1]));
-            ++out.sweeps;
-            const double ratio = (double)hh[sweep] / ((double)kw * (double)n);
-            out.churn.push_back(ratio);
-            if (ratio < p.eps || !ahead) break;
-        }
-    } else {
-        for (int sweep = 0; sweep < p.max_sweeps; ++sweep) {
-            run_sweep(sweep);
-            c.tic();
-            unsigned long long changed = c.read_scalar(churn);
-            allgather_rows(gid, gd, kw);
-            if (c.world > 1) {
-                uint64_t ch = changed;
-                static_cast<Comm*>(c.comm)->allreduce_u64(&ch, 1, false, c.stream);
-                changed = ch;
-            }
-            c.toc(P_KNN);
-            ++out.sweeps;
-            const double ratio = (double)changed / ((double)kw * (double)n);
-            out.churn.push_back(ratio);
-            if (ratio < p.eps) break;
-        }
+        ++out.sweeps;
+        const double ratio = (double)changed / ((double)kw * (double)n);
+        out.churn.push_back(ratio);
+        if (ratio < p.eps) break;
     }
     // trim to k / convert to global ids
     out.k = k;

@@ -25,8 +25,6 @@ Context::~Context() {
         cudaEventDestroy(side_done);
     }
     if (stream) cudaStreamSynchronize(stream);
-    for (cudaEvent_t e : sweep_ev_)
-        if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_free) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_used) cudaEventDestroy(e);
     if (pin_counts) cudaFreeHost(pin_counts);
