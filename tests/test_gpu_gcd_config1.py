@@ -31,8 +31,8 @@ from helpers import assert_lists_tie_aware, assert_rel, assert_same_couplings
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
-def _setup(gpu, golden):
-    g = golden("gcd_config1")
+def _setup(gpu, golden, name="gcd_config1"):
+    g = golden(name)
     n, M = int(g["n"]), int(g["M"])
     X, _ = O.gen_ising_colored(n, M, int(g["seed"]), mean_deg=4.0, w_sigma=0.3, th_sigma=0.1, burn_in=1000,
                                thin=10)
@@ -47,8 +47,11 @@ def _pairs(i, j, d):
     return out
 
 
-def test_gcd_config1_lockstep_vs_reference(gpu, golden):
-    g, n, M, dev = _setup(gpu, golden)
+@pytest.mark.parametrize("name", ["gcd_config1", "gcd_config2"])
+def test_gcd_lockstep_vs_reference(gpu, golden, name):
+    """config 1 to convergence (65 iterations); config 2 (N = 1e4, M = 1000, 20000
+    candidates per iteration) for its first three iterations (oracle/make_gcd_trace_c2.py)."""
+    g, n, M, dev = _setup(gpu, golden, name)
     m = int(round(float(g["kappa"]) * n))
     nodes = np.arange(n, dtype=np.int32)
     iters = len(g["rec_objective"])
@@ -80,7 +83,7 @@ def test_gcd_config1_lockstep_vs_reference(gpu, golden):
         obj_rel.append(abs(base - g["rec_objective"][it - 1]) / abs(g["rec_objective"][it - 1]))
         d_abs.append(abs(delta - g["rec_delta"][it - 1]))
     st = dev.get_state()
-    print(f"config-1 lock-step: {iters} iterations; objective max rel diff {max(obj_rel):.2e}; delta (sum |dw|) "
+    print(f"{name} lock-step: {iters} iterations; objective max rel diff {max(obj_rel):.2e}; delta (sum |dw|) "
           f"max abs diff {max(d_abs):.2e}; lists identical in {n_diff.count(0)} iterations, differing candidates "
           f"per iteration {n_diff}; beyond near-ties: {beyond}")
     # north_star: objective per iteration 1e-6 relative; couplings 1e-4 (delta is a sum
