@@ -29,13 +29,18 @@ namespace nrg {
 
 namespace tc {
 
+// 128 x 64 tiles: three 64-column accumulators fit a 256-column TMEM allocation and two
+// 2-stage smem rings (2 x 96 KB) fit one SM, so two CTAs share each SM and one's
+// epilogue / setup overlaps the other's MMAs (with 128 x 128 tiles the 384 accumulator
+// columns took a 512-column allocation: one CTA per SM, nothing overlapped)
 constexpr int kBM = 128;      // tile rows (TMEM lanes)
-constexpr int kBN = 128;      // tile columns (per accumulator)
+constexpr int kBN = 64;       // tile columns (per accumulator)
 constexpr int kBK = 128;      // K bytes per stage = one 128B swizzle atom
-constexpr int kStages = 3;
-constexpr int kTileBytes = kBM * kBK;  // 16 KB
-constexpr int kStageBytes = 4 * kTileBytes;
-constexpr int kTmemCols = 512;
+constexpr int kStages = 2;
+constexpr int kTileBytes = kBM * kBK;   // 16 KB: an A operand (rows of block I)
+constexpr int kTileBytesB = kBN * kBK;  // 8 KB: a B operand (rows of block J)
+constexpr int kStageBytes = 2 * kTileBytes + 2 * kTileBytesB;
+constexpr int kTmemCols = 256;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -115,8 +120,9 @@ struct TcOut {
 // feeds TMA, warp 1 lane 0 issues the MMAs, and all 8 run the epilogue -- warps w and
 // w + 4 share TMEM lane quadrant w % 4 (rows) and split the tile's columns
 constexpr int kTcThreads = 256;
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(kTcThreads, 2)
     tc_screen_kernel(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mt,
+                     const __grid_constant__ CUtensorMap mxb, const __grid_constant__ CUtensorMap mtb,
                      const float4* __restrict__ q, int n, int M, int Mp, double lambda, double base, TcOut out) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* ring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -126,13 +132,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     __shared__ float2 qcol[kBN];  // {d_j, E_j} of the column block
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // linear tile index -> (I, J), I <= J
-    const int T = (n + kBM - 1) / kBM;
+    // linear tile index -> (I, J): row block I (128 rows) pairs with the 64-column blocks
+    // J >= 2 I (the ones holding some j > i)
+    const int TB = (n + kBN - 1) / kBN;
     int I = 0, rem = (int)blockIdx.x;
-    while (rem >= T - I) {
-        rem -= T - I;
+    while (rem >= TB - 2 * I) {
+        rem -= TB - 2 * I;
         ++I;
     }
-    const int J = I + rem;
+    const int J = 2 * I + rem;
     if (threadIdx.x < kBN) {
         const int j = J * kBN + (int)threadIdx.x;
         const float4 v = j < n ? __ldg(&q[j]) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -167,8 +175,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mbar_expect_tx(&full[s], kStageBytes);
             tma_load_2d(st + 0 * kTileBytes, &mx, kb * kBK, I * kBM, &full[s]);
             tma_load_2d(st + 1 * kTileBytes, &mt, kb * kBK, I * kBM, &full[s]);
-            tma_load_2d(st + 2 * kTileBytes, &mx, kb * kBK, J * kBN, &full[s]);
-            tma_load_2d(st + 3 * kTileBytes, &mt, kb * kBK, J * kBN, &full[s]);
+            tma_load_2d(st + 2 * kTileBytes, &mxb, kb * kBK, J * kBN, &full[s]);
+            tma_load_2d(st + 2 * kTileBytes + kTileBytesB, &mtb, kb * kBK, J * kBN, &full[s]);
         }
     } else if (warp == 1 && lane == 0) {
         // MMA issuer: acc1 = X_I X_J^T, acc2 = X_I T8_J^T, acc3 = T8_I X_J^T
@@ -184,7 +192,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const uint64_t xi = smem_desc(st + 0 * kTileBytes, 32 * kk);
                 const uint64_t ti = smem_desc(st + 1 * kTileBytes, 32 * kk);
                 const uint64_t xj = smem_desc(st + 2 * kTileBytes, 32 * kk);
-                const uint64_t tj = smem_desc(st + 3 * kTileBytes, 32 * kk);
+                const uint64_t tj = smem_desc(st + 2 * kTileBytes + kTileBytesB, 32 * kk);
                 mma_i8(tmem + 0, xi, xj, acc);
                 mma_i8(tmem + kBN, xi, tj, acc);
                 mma_i8(tmem + 2 * kBN, ti, xj, acc);
@@ -465,11 +473,11 @@ static EncodeTiled encoder() {
     return fn;
 }
 
-static CUtensorMap tile_map(void* base, uint64_t rows, uint64_t row_bytes) {
+static CUtensorMap tile_map(void* base, uint64_t rows, uint64_t row_bytes, uint32_t box_rows = kBM) {
     CUtensorMap m;
     const cuuint64_t dims[2] = {row_bytes, rows};
     const cuuint64_t strides[1] = {row_bytes};
-    const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)kBM};
+    const cuuint32_t box[2] = {(cuuint32_t)kBK, (cuuint32_t)box_rows};
     const cuuint32_t es[2] = {1, 1};
     const CUresult r = encoder()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, es,
                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -523,15 +531,18 @@ bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* di
         tc_fill_kernel<<<(unsigned)std::min<uint64_t>(ceil_div(pairs, 256), 148 * 16), 256, 0, c.stream>>>(
             dist, pairs, -(base + 0.0));
     const CUtensorMap mx = tile_map(zx, n, (uint64_t)Mp), mt = tile_map(zt, n, (uint64_t)Mp);
-    const int T = (int)((n + kBM - 1) / kBM);
+    const CUtensorMap mxb = tile_map(zx, n, (uint64_t)Mp, kBN), mtb = tile_map(zt, n, (uint64_t)Mp, kBN);
+    const int T = (int)((n + kBM - 1) / kBM), TB = (int)((n + kBN - 1) / kBN);
+    int tiles = 0;
+    for (int I = 0; I < T; ++I) tiles += std::max(0, TB - 2 * I);
     const size_t smem = (size_t)kStages * kStageBytes + 1024;
     static bool attr = false;
     if (!attr) {
         NRG_CUDA(cudaFuncSetAttribute(tc_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    tc_screen_kernel<<<(unsigned)(T * (T + 1) / 2), kTcThreads, smem, c.stream>>>(mx, mt, q, (int)n, c.M, Mp, c.lambda,
-                                                                          base, out);
+    tc_screen_kernel<<<(unsigned)tiles, kTcThreads, smem, c.stream>>>(mx, mt, mxb, mtb, q, (int)n, c.M, Mp,
+                                                                   c.lambda, base, out);
     NRG_LAUNCH_CHECK();
     unsigned long long ns = 0;
     ns = c.read_scalar(out.ns);
