@@ -1286,6 +1286,15 @@ static void exchange_and_score(Context& c, int mode, const ClaimSink& sink, uint
     }
 }
 
+// nodes whose candidate count falls short of every other node outside the row
+__global__ void coverage_kernel(const int32_t* __restrict__ cand_cnt, uint64_t own, int full,
+                                unsigned long long* __restrict__ short_nodes) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool sh = t < own && cand_cnt[t] < full;
+    const unsigned b = __ballot_sync(0xffffffffu, sh);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(short_nodes, (unsigned long long)__popc(b));
+}
+
 // ---------------------------------------------------------------- driver
 __global__ void to_global_kernel(const int32_t* __restrict__ gid, const double* __restrict__ gd,
                                  const int32_t* __restrict__ nodes, uint64_t n, int kw, int k,
@@ -1525,7 +1534,9 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
     int32_t* cand_id = cidb.as<int32_t>(n * capn);
     uint32_t* cand_slot = cslb.as<uint32_t>(n * capn);
     int32_t* cand_cnt = ccntb.as<int32_t>(n);
-    unsigned long long* churn = churnb.as<unsigned long long>(1);
+    // churn[0]: entries this sweep changed; churn[1]: nodes whose candidate set missed
+    // some node (bit-set gathers of one rank; read back together)
+    unsigned long long* churn = churnb.as<unsigned long long>(2);
     const uint64_t wmax = n * capn;
     int32_t* ws = wsb.as<int32_t>(wmax);
     int32_t* wp = wpb.as<int32_t>(wmax);
@@ -1635,7 +1646,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         if (cached && fused && !dense) cache_reserve(c, wmax);
         c.tic();
         NRG_CUDA(cudaMemsetAsync(wcount, 0, 16, c.stream));
-        NRG_CUDA(cudaMemsetAsync(churn, 0, 8, c.stream));
+        NRG_CUDA(cudaMemsetAsync(churn, 0, 16, c.stream));
         ClaimSink sk = sink_for(ws, wp, wsl, own * capn + 1);
         // own claims resolve through the worklist-ordered distances (single rank, a memo
         // and worklist small enough for 31-bit indices)
@@ -1735,8 +1746,22 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                     d_nodes, n, gid, gd, kw, cand_id, cand_slot, cand_cnt, capn, dview, dvals, rvals, buf_cap, churn, lo);
             NRG_LAUNCH_CHECK();
         }
-        unsigned long long changed = 0;
-        changed = c.read_scalar(churn);
+        // Full coverage: when every node's candidate set (bit-set gathers: the 2-hop set minus
+        // the row and the node) was all the other nodes, each merged row is the exact top-kw
+        // of the level, so the next sweep cannot change an entry: its churn is 0 and the loop
+        // ends there.  That sweep is recorded (sweeps, churn trace) without being run -- it
+        // would only re-probe pairs this sweep already probed (hits, no misses).
+        const bool cov_check = bitsmode && c.world == 1 && !NRG_ENV_ON("NRG_NO_COVERAGE_SKIP");
+        if (cov_check && own) {
+            coverage_kernel<<<(unsigned)ceil_div(own, 256), 256, 0, c.stream>>>(cand_cnt + lo, own,
+                                                                             (int)(n - 1 - (uint64_t)kw), churn + 1);
+            NRG_LAUNCH_CHECK();
+        }
+        unsigned long long* hc = c.hp_small.as<unsigned long long>(2);
+        NRG_CUDA(cudaMemcpyAsync(hc, churn, 16, cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        unsigned long long changed = hc[0];
+        const bool covered = cov_check && hc[1] == 0;
         allgather_rows(gid, gd, kw);
         if (c.world > 1) {
             uint64_t ch = changed;
@@ -1750,6 +1775,11 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         const double ratio = (double)changed / ((double)kw * (double)n);
         out.churn.push_back(ratio);
         if (ratio < p.eps) break;
+        if (covered && sweep + 1 < p.max_sweeps) {
+            ++out.sweeps;  // the next sweep, settled in advance: churn 0 < eps
+            out.churn.push_back(0.0);
+            break;
+        }
     }
     // trim to k / convert to global ids
     out.k = k;
