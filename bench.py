@@ -377,11 +377,24 @@ def run_ours(args, rank, world, local, dist):
     else:
         lam = ising_lambda(N, M)
         model = P.Model(N, M, P.NRG_ISING, lam, device=local)
+    transport = "single GPU"
     if world > 1:
-        # one sharded job over all ranks: NCCL communicator of the library, id via torch
-        obj = [P._lib.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        model.comm_init(obj[0], rank, world)
+        # one sharded job over all ranks: NCCL communicator of the library, id via torch;
+        # if the library cannot bring NCCL up, its host transport over a gloo group
+        uid = None
+        if rank == 0:
+            try:
+                uid = P._lib.comm_unique_id()
+            except Exception as e:  # noqa: BLE001
+                print(f"bench.py: NCCL unavailable ({e}); host transport over gloo", file=sys.stderr)
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)  # every rank learns which transport it is
+        if obj[0] is not None:
+            model.comm_init(obj[0], rank, world)
+            transport = "NCCL"
+        else:
+            model.comm_init_host(P.TorchDistTransport(dist.new_group(backend="gloo")))
+            transport = "host transport (gloo)"
     # identical (replicated) samples on every rank: the path shards nodes, not data
     if gen == "er":
         Xh = model.generate_ising(mean_deg=md, w_sigma=0.3, th_sigma=0.1, burn_in=args.burn_in, thin=10,
@@ -497,8 +510,9 @@ def run_ours(args, rank, world, local, dist):
                                f"from the empty state",
                    "l2": "inputs > L2 (T32 {:.0f} MB + T64 {:.0f} MB per GPU)".format(N * 1024 * 4 / 1e6,
                                                                                       N * 1024 * 8 / 1e6),
-                   "parallelism": (f"node-sharded NNDescent + key-sharded distance cache over NCCL x{world}; "
-                                   "updates/theta replicated") if world > 1 else "single GPU",
+                   "parallelism": (f"node-sharded NNDescent + key-sharded distance cache over {transport} x{world}; "
+                                   "theta pass and objective sharded; dense levels, selection and updates "
+                                   "replicated") if world > 1 else "single GPU",
                    "gen_seconds": round(gen_s, 1)},
         "sweep": {"ms_per_sweep": ms_per_step, "pairs_per_sweep": tot_pairs / args.steps,
                   "hits_per_sweep": cnt["hits"] / args.steps, "survivors_per_sweep": kst["k2_pairs"] / args.steps,
