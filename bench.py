@@ -139,7 +139,12 @@ def dist_setup():
     if world > 1:
         import torch
         import torch.distributed as dist
-        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        # NRG_BENCH_ONE_DEVICE=1: every rank on GPU 0 with gloo and the library's host
+        # transport (exercises the N > 1 bench path on a one-GPU box; not a scaling number)
+        one = os.environ.get("NRG_BENCH_ONE_DEVICE") == "1"
+        backend = "nccl" if torch.cuda.is_available() and not one else "gloo"
+        if one:
+            local = 0
         if backend == "nccl":
             if local >= torch.cuda.device_count():
                 raise SystemExit(f"bench.py: rank {rank} needs GPU {local}, only {torch.cuda.device_count()} visible")
@@ -160,7 +165,7 @@ def allreduce(dist, vals, op="sum"):
     if dist is None:
         return vals
     import torch
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    dev = "cuda" if torch.cuda.is_available() and dist.get_backend() == "nccl" else "cpu"
     t = torch.tensor(vals, dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX)
     return t.cpu().tolist()
@@ -382,7 +387,7 @@ def run_ours(args, rank, world, local, dist):
         # one sharded job over all ranks: NCCL communicator of the library, id via torch;
         # if the library cannot bring NCCL up, its host transport over a gloo group
         uid = None
-        if rank == 0:
+        if rank == 0 and os.environ.get("NRG_BENCH_ONE_DEVICE") != "1":
             try:
                 uid = P._lib.comm_unique_id()
             except Exception as e:  # noqa: BLE001
