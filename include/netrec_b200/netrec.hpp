@@ -346,6 +346,11 @@ public:
         std::vector<std::int32_t> ei(ne), ej(ne);
         std::vector<double> w(ne);
         detail::check(nrg_get_state(ctx_.get(), th.data(), ne, ei.data(), ej.data(), w.data(), &ne));
+        if (ne < ei.size()) {  // the count call is an upper bound
+            ei.resize(ne);
+            ej.resize(ne);
+            w.resize(ne);
+        }
         std::vector<double> sums(static_cast<std::size_t>(n) * static_cast<std::size_t>(M));
         detail::check(nrg_get_sums(ctx_.get(), sums.data()));
         state_->assign_from_device(th, ei, ej, w, std::move(sums));

@@ -578,11 +578,12 @@ __global__ void __launch_bounds__(1024) tail_walk_kernel(const int32_t* __restri
                                                           const uint8_t* __restrict__ changed,
                                                           uint32_t* __restrict__ mod, uint32_t stamp,
                                                           uint32_t* __restrict__ apply,
-                                                          unsigned long long* __restrict__ tail) {
+                                                          unsigned long long* __restrict__ tail, uint64_t budget) {
     __shared__ int s_a[1024], s_b[1024], s_pos[1024];
     __shared__ int s_nch, s_stop;
     const int tid = threadIdx.x;
     uint64_t na = 0;
+    if (tail[0] > budget) return;  // more changes than rounds left: the host orders the rest
     const uint64_t first = tail[1];
     for (uint64_t base = lo + first; base < n; base += 1024) {
         const uint64_t p = base + tid;
@@ -771,7 +772,7 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
                 change_flags_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, c.stream>>>(ci, cj, start, n, w, c.Wview(),
                                                                                       ch, tail);
                 tail_walk_kernel<<<1, 1024, 0, c.stream>>>(ci, cj, start, n, ch, mod_dev, ++c.tail_stamp, apply_dev,
-                                                           tail);
+                                                           tail, (uint64_t)(kTailRounds - round));
                 NRG_LAUNCH_CHECK_N(3);
                 NRG_CUDA(cudaMemcpyAsync(htail, tail, 32, cudaMemcpyDeviceToHost, c.stream));
                 c.sync();
