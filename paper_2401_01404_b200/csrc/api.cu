@@ -106,26 +106,26 @@ void gcd_iteration(nrg_ctx* x, const nrg_gcd_cfg* cfg, int iter, nrg_iter_record
     nrg::BestPairsD best;
     nrg::find_best(c, cfg->mode, m, dall, (uint64_t)n, cfg->knn_eps, nrg::mix64(cfg->seed, (uint64_t)iter),
                    cfg->reverse != 0, false, best, x->out_i, x->out_j, x->out_d);
-    if (cands && cap) {
-        // packed on the device into the caller's record layout, one copy through pinned memory
-        const uint64_t k = std::min(cap, best.count);
-        if (k) {
-            nrg::DevBuf packed;
-            nrg_pair* dp = packed.as<nrg_pair>(k);
-            pack_pairs_kernel<<<(unsigned)((k + 255) / 256), 256, 0, c.stream>>>(
-                static_cast<int32_t*>(x->out_i.p), static_cast<int32_t*>(x->out_j.p),
-                static_cast<double*>(x->out_d.p), k, dp);
-            NRG_LAUNCH_CHECK();
-            nrg_pair* hp = c.hp_pairs.as<nrg_pair>(k);
-            NRG_CUDA(cudaMemcpyAsync(hp, dp, k * sizeof(nrg_pair), cudaMemcpyDeviceToHost, c.stream));
-            c.sync();
-            std::memcpy(cands, hp, k * sizeof(nrg_pair));
-        }
+    // the candidates, packed on the device into the caller's record layout, go down through
+    // pinned memory while the updates run; the host copy into `cands` waits until then
+    const uint64_t kc = (cands && cap) ? std::min(cap, best.count) : 0;
+    nrg::DevBuf packed;
+    nrg_pair* hp = nullptr;
+    if (kc) {
+        nrg_pair* dp = packed.as<nrg_pair>(kc);
+        pack_pairs_kernel<<<(unsigned)((kc + 255) / 256), 256, 0, c.stream>>>(
+            static_cast<int32_t*>(x->out_i.p), static_cast<int32_t*>(x->out_j.p),
+            static_cast<double*>(x->out_d.p), kc, dp);
+        NRG_LAUNCH_CHECK();
+        hp = c.hp_pairs.as<nrg_pair>(kc);
+        NRG_CUDA(cudaMemcpyAsync(hp, dp, kc * sizeof(nrg_pair), cudaMemcpyDeviceToHost, c.stream));
     }
     if (n_cands) *n_cands = best.count;
     const double delta = nrg::apply_updates(c, static_cast<int32_t*>(x->out_i.p), static_cast<int32_t*>(x->out_j.p),
                                             best.count, nullptr, static_cast<double*>(x->out_d.p),
                                             /*fb_sorted=*/true);
+    // apply_updates returned a host value: the stream (and the copy above) has completed
+    if (kc) std::memcpy(cands, hp, kc * sizeof(nrg_pair));
     nrg::theta_pass(c, nullptr);
     const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     const double obj = nrg::log_posterior(c);
