@@ -402,11 +402,11 @@ class Model:
         cfg = GcdCfg(kappa, eps, 1, mode, knn_eps, seed, 1, int(reverse))
         rec = np.zeros(1, ITER_DT)
         cap = int(max(1, round(kappa * self.n))) + 1 if want_candidates else 0
-        cand = np.zeros(max(cap, 1), PAIR_DT)
+        cand = np.empty(max(cap, 1), PAIR_DT)  # filled by the call (a fresh array: no copy on return)
         nc = _u64()
         check(self.L.nrg_gcd_iteration(self.h, C.byref(cfg), it, rec, cand.ctypes.data if cap else None, cap,
                                        C.byref(nc)))
-        return rec[0], (cand[: nc.value].copy() if cap else None)
+        return rec[0], (cand[: min(nc.value, cap)] if cap else None)
 
     def reconstruct_gcd(self, kappa=1.0, eps=-1.0, max_iters=1000, mode=NRG_EXACT, knn_eps=1e-3, seed=0,
                         reverse=False):

@@ -124,9 +124,11 @@ void gcd_iteration(nrg_ctx* x, const nrg_gcd_cfg* cfg, int iter, nrg_iter_record
     const double delta = nrg::apply_updates(c, static_cast<int32_t*>(x->out_i.p), static_cast<int32_t*>(x->out_j.p),
                                             best.count, nullptr, static_cast<double*>(x->out_d.p),
                                             /*fb_sorted=*/true);
-    // apply_updates returned a host value: the stream (and the copy above) has completed
-    if (kc) std::memcpy(cands, hp, kc * sizeof(nrg_pair));
     nrg::theta_pass(c, nullptr);
+    // apply_updates returned a host value, so the candidate copy above has completed; the
+    // host copy into the caller's buffer (first-touch pages) overlaps the theta pass
+    if (kc) std::memcpy(cands, hp, kc * sizeof(nrg_pair));
+    c.sync();  // IterationRecord.seconds covers FindBest + updates + theta pass (inc/reconstruct.hpp:163-173)
     const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     const double obj = nrg::log_posterior(c);
     if (rec) *rec = {iter, 0, delta, secs, best.count, obj};
