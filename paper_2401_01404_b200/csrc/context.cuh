@@ -20,6 +20,8 @@
 #include <cstdint>
 #include <cstdlib>
 #include <vector>
+#include <unordered_map>
+#include <mutex>
 
 #include <cuda_fp16.h>
 
@@ -43,6 +45,50 @@ struct StreamScope {
     explicit StreamScope(cudaStream_t s) : prev(tl_stream) { tl_stream = s; }
     ~StreamScope() { tl_stream = prev; }
 };
+
+// Freed blocks of a stream, by size class, kept on the host for that stream's next
+// allocation of the same class: a sweep allocates and frees ~600 scratch buffers, and the
+// pool calls (~1 us each) were host time the device spent starved between small kernels.
+// Stream-ordered like the pool: a block freed on stream s is reused only on s.  Dropped
+// (returned to the pool) when the stream's context goes (StreamOwner).
+struct BlockCache {
+    std::mutex mu;
+    std::unordered_map<cudaStream_t, std::unordered_map<size_t, std::vector<void*>>> free;
+    static BlockCache& get() {
+        static BlockCache* bc = new BlockCache();  // process lifetime (no static-destruction order issue)
+        return *bc;
+    }
+    void* take(cudaStream_t s, size_t bytes) {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = free.find(s);
+        if (it == free.end()) return nullptr;
+        auto jt = it->second.find(bytes);
+        if (jt == it->second.end() || jt->second.empty()) return nullptr;
+        void* p = jt->second.back();
+        jt->second.pop_back();
+        return p;
+    }
+    void put(cudaStream_t s, size_t bytes, void* p) {
+        std::lock_guard<std::mutex> lk(mu);
+        free[s][bytes].push_back(p);
+    }
+    void drop(cudaStream_t s) {
+        std::unordered_map<size_t, std::vector<void*>> blocks;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            auto it = free.find(s);
+            if (it == free.end()) return;
+            blocks.swap(it->second);
+            free.erase(it);
+        }
+        for (auto& kv : blocks)
+            for (void* p : kv.second) cudaFreeAsync(p, s);
+    }
+};
+inline bool block_cache_on() {
+    static const bool v = getenv("NRG_NO_BLOCK_CACHE") == nullptr;
+    return v;
+}
 
 // grow-only device buffer (RAII, move-only, stream-ordered)
 struct DevBuf {
@@ -85,7 +131,7 @@ struct DevBuf {
             const auto t0 = dbg ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point();
             if (sync_alloc())
                 NRG_CUDA(cudaMalloc(&p, nb));
-            else
+            else if (!(block_cache_on() && s && (p = BlockCache::get().take(s, nb))))
                 NRG_CUDA(cudaMallocAsync(&p, nb, s));
             if (dbg) {
                 const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -103,6 +149,8 @@ struct DevBuf {
         if (p) {
             if (sync_alloc())
                 cudaFree(p);
+            else if (block_cache_on() && s)
+                BlockCache::get().put(s, bytes, p);
             else
                 cudaFreeAsync(p, s);
         }
@@ -216,6 +264,7 @@ struct StreamOwner {  // declared first in Context: destroyed after every DevBuf
     cudaStream_t s = nullptr;
     ~StreamOwner() {
         if (s) {
+            BlockCache::get().drop(s);  // the stream's cached blocks back to the pool, in its order
             cudaStreamSynchronize(s);
             cudaStreamDestroy(s);
         }
