@@ -446,11 +446,7 @@ def run_ours(args, rank, world, local, dist):
     # e2e through the public API with host buffers: every step uploads the pinned int8
     # samples and the state S_W (theta + couplings), runs sweep W, and downloads the
     # candidate list and the new state
-    barrier(dist)
-    model.reset_counters()
-    h2d = d2h = 0
-    model.timer_start()
-    for s in range(args.steps):
+    def e2e_step():
         if gauss:
             model.upload_samples(Xpin)
         else:
@@ -458,7 +454,15 @@ def run_ours(args, rank, world, local, dist):
         model.set_theta(th_w)
         model.set_edges(ei_w, ej_w, w_w)
         rec, cands = model.gcd_iteration(args.warmup, kappa=kappa, seed=args.seed, want_candidates=True)
-        st = model.get_state()
+        return cands, model.get_state()
+
+    e2e_step()  # untimed warm-up of the host-buffer path (first touch of its host arrays)
+    barrier(dist)
+    model.reset_counters()
+    h2d = d2h = 0
+    model.timer_start()
+    for s in range(args.steps):
+        cands, st = e2e_step()
         h2d += Xpin.nbytes + th_w.nbytes + ei_w.nbytes + ej_w.nbytes + w_w.nbytes
         d2h += cands.nbytes + sum(a.nbytes for a in st)
     e2e_ms = model.timer_stop()
