@@ -384,20 +384,27 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
     const float lam = (float)lambda;
     const double pruned_dist = -(base + 0.0);
     // stage the partner row of this group's entry into ring buffer `st` (one commit group
-    // per step, empty past the chunk's end, so wait_group counts stay uniform)
+    // per step, empty past the chunk's end, so wait_group counts stay uniform).  Lane r of
+    // the group copies the 16-byte chunks r, r + G, ... of the field, then of the spin
+    // words: per-lane base addresses, the chunk offsets are immediates.
+    static_assert((FB / 16) % G == 0, "field chunks must split evenly over the group");
+    constexpr int KF = FB / 16 / G;               // field chunks per lane
+    constexpr int XC = 4 * Mw / 16;               // spin-word chunks of a row
+    constexpr int KX = (XC + G - 1) / G;
+    const uint32_t dst_lane = wbuf_sa + (uint32_t)(grp * RB + 16 * r);
+    const unsigned char* field = FOUR ? reinterpret_cast<const unsigned char*>(S.P4)
+                                      : reinterpret_cast<const unsigned char*>(S.T8);
+    const unsigned char* spins = reinterpret_cast<const unsigned char*>(S.Xb);
     auto stage = [&](int st, int p, bool any) {
-        const uint32_t dst = wbuf_sa + (uint32_t)((st * P + grp) * RB);
-        if (!any) {
-            cp_async_commit();
-            return;
-        }
-        const unsigned char* t8 = FOUR ? reinterpret_cast<const unsigned char*>(S.P4) + (uint64_t)(uint32_t)p * FB
-                                       : reinterpret_cast<const unsigned char*>(S.T8) + (uint64_t)(uint32_t)p * Mp;
-        const unsigned char* xb = reinterpret_cast<const unsigned char*>(S.Xb) + (uint64_t)(uint32_t)p * Mw * 4;
+        if (any) {
+            const uint32_t dst = dst_lane + (uint32_t)(st * P * RB);
+            const unsigned char* t8 = field + (uint64_t)(uint32_t)p * FB + 16 * r;
+            const unsigned char* xb = spins + (uint64_t)(uint32_t)p * (Mw * 4) + 16 * r;
 #pragma unroll
-        for (int c = r; c < CH; c += G) {
-            const unsigned char* src = c < (int)(FB / 16) ? t8 + 16 * c : xb + 16 * (c - (int)(FB / 16));
-            cp_async16(dst + 16 * c, src);
+            for (int k = 0; k < KF; ++k) cp_async16(dst + 16 * G * k, t8 + 16 * G * k);
+#pragma unroll
+            for (int k = 0; k < KX; ++k)
+                if (XC % G == 0 || r + G * k < XC) cp_async16(dst + FB + 16 * G * k, xb + 16 * G * k);
         }
         cp_async_commit();
     };
