@@ -154,6 +154,153 @@ static void sort_trikeys(Context& c, TriKey* in, TriKey* out, uint64_t n, DevBuf
     NRG_LAUNCH_CHECK();
 }
 
+// ---------------------------------------------------------------- radix select
+// The K smallest of n distinct (dist, a, b) keys, unsorted, and a threshold T such that
+// an input key is among the K smallest iff it is <= T (the reference's nth_element,
+// inc/find_best.hpp:114-131: D+ and the S' test need the set and its largest key, not
+// an order).  MSD radix select over the packed key (hi = dkey, lo = a << ib | b), 8-bit
+// digits, in ONE cooperative launch and without a host round trip: per pass every CTA
+// histograms the digit of the keys still matching the prefix, one grid barrier, then
+// every CTA reads the same 256 counts and extends the prefix identically.  Once the
+// remaining rank equals the size of the prefix group, the whole group is in and the
+// passes stop (T = prefix with the unresolved bits set: no input key lies between the
+// group's largest key and T).
+__device__ __forceinline__ void sel_grid_sync(unsigned* bar, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = bar + 1;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*gen == g) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+constexpr int kSelThreads = 512;
+__global__ void __launch_bounds__(kSelThreads) trikey_select_kernel(const TriKey* __restrict__ in, uint64_t n,
+                                                                    uint64_t K, int ib, unsigned* __restrict__ hist,
+                                                                    unsigned* bar, TriKey* __restrict__ out,
+                                                                    unsigned long long* __restrict__ cnt,
+                                                                    TriKey* __restrict__ thr) {
+    __shared__ unsigned sh[256];
+    __shared__ uint64_t s_p[2], s_m[2];  // prefix and mask over (hi, lo)
+    __shared__ unsigned long long s_krem;
+    __shared__ int s_done;
+    const int tid = threadIdx.x;
+    const int lob = 2 * ib;
+    const uint64_t lomask = lob >= 64 ? ~0ull : (1ull << lob) - 1;
+    if (tid == 0) {
+        s_p[0] = s_p[1] = s_m[0] = s_m[1] = 0;
+        s_krem = K;
+        s_done = 0;
+    }
+    __syncthreads();
+    const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + tid, st = (uint64_t)gridDim.x * blockDim.x;
+    const int npass = 8 + (lob + 7) / 8;
+    for (int pass = 0; pass < npass && !s_done; ++pass) {
+        int word, shift, width;
+        if (pass < 8) {
+            word = 0;
+            shift = 56 - 8 * pass;
+            width = 8;
+        } else {
+            word = 1;
+            shift = lob - 8 * (pass - 7);
+            width = 8;
+            if (shift < 0) {
+                width += shift;
+                shift = 0;
+            }
+        }
+        const uint64_t ph = s_p[0], pl = s_p[1], mh = s_m[0], ml = s_m[1];
+        for (int b = tid; b < 256; b += kSelThreads) sh[b] = 0u;
+        __syncthreads();
+        for (uint64_t e = t0; e < n; e += st) {
+            const TriKey k = in[e];
+            const uint64_t hi = k.d, lo = ((uint64_t)k.a << ib) | k.b;
+            if ((hi & mh) == ph && (lo & ml) == pl) {
+                const unsigned dg = (unsigned)(((word ? lo : hi) >> shift) & ((1u << width) - 1u));
+                atomicAdd(&sh[dg], 1u);
+            }
+        }
+        __syncthreads();
+        for (int b = tid; b < 256; b += kSelThreads)
+            if (sh[b]) atomicAdd(&hist[pass * 256 + b], sh[b]);
+        sel_grid_sync(bar, gridDim.x);
+        for (int b = tid; b < 256; b += kSelThreads) sh[b] = __ldcg(&hist[pass * 256 + b]);
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long below = 0, krem = s_krem;
+            int bin = 0;
+            for (; bin < (1 << width) - 1; ++bin) {
+                if (below + sh[bin] >= krem) break;
+                below += sh[bin];
+            }
+            const uint64_t wm = ((1ull << width) - 1) << shift;
+            s_p[word] |= (uint64_t)bin << shift;
+            s_m[word] |= wm;
+            s_krem = krem - below;
+            if (s_krem == sh[bin]) s_done = 1;  // the whole prefix group is in
+        }
+        __syncthreads();
+    }
+    const uint64_t th = s_p[0] | ~s_m[0], tl = s_p[1] | (~s_m[1] & lomask);
+    for (uint64_t e0 = (uint64_t)blockIdx.x * blockDim.x; e0 < n; e0 += st) {
+        const uint64_t e = e0 + tid;
+        bool keep = false;
+        TriKey k;
+        if (e < n) {
+            k = in[e];
+            const uint64_t hi = k.d, lo = ((uint64_t)k.a << ib) | k.b;
+            keep = hi < th || (hi == th && lo <= tl);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        const int lane = tid & 31;
+        unsigned long long at = 0;
+        if (lane == 0 && bal) at = atomicAdd(cnt, (unsigned long long)__popc(bal));
+        at = __shfl_sync(0xffffffffu, at, 0);
+        if (keep) out[at + __popc(bal & ((1u << lane) - 1u))] = k;
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        TriKey t;
+        t.d = th;
+        t.a = (uint32_t)(tl >> ib);
+        t.b = (uint32_t)(tl & ((1ull << ib) - 1));
+        *thr = t;
+    }
+}
+
+// out (K entries, any order) and *thr on the device; no host round trip
+static void select_trikeys(Context& c, const TriKey* in, uint64_t n, uint64_t K, TriKey* out, TriKey* thr,
+                           DevBuf& scratch) {
+    static int grid = 0;
+    if (!grid) {
+        int per = 0;
+        NRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, trikey_select_kernel, kSelThreads, 0));
+        int sms = 0;
+        NRG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+        grid = std::max(1, per) * sms;
+    }
+    const int ib = id_bits(c);
+    const int npass = 8 + (2 * ib + 7) / 8;
+    const size_t words = (size_t)npass * 256 + 2 + 2;  // hist, barrier, count (u64)
+    unsigned* hist = scratch.as<unsigned>(words);
+    unsigned* bar = hist + npass * 256;
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(bar + 2);
+    NRG_CUDA(cudaMemsetAsync(hist, 0, words * 4, c.stream));
+    const unsigned g = (unsigned)std::min<uint64_t>((uint64_t)grid, std::max<uint64_t>(1, ceil_div(n, kSelThreads)));
+    void* args[] = {(void*)&in, (void*)&n, (void*)&K, (void*)&ib, (void*)&hist, (void*)&bar, (void*)&out, (void*)&cnt,
+                    (void*)&thr};
+    NRG_CUDA(cudaLaunchCooperativeKernel((void*)trikey_select_kernel, g, kSelThreads, args, 0, c.stream));
+    NRG_LAUNCH_CHECK();
+}
+
 __global__ void tri_from_pairs_kernel(const int32_t* __restrict__ nodes, uint64_t n, const double* __restrict__ dist,
                                       TriKey* __restrict__ out) {
     // row-major upper triangle: candidate (min, max, dist) (inc/common.hpp:27-30)
@@ -463,8 +610,18 @@ static uint64_t merge_select(Context& c, TriKey* buf, uint64_t n, uint64_t want,
         outb = std::move(ub);
         return nu;
     }
+    // the root: select the `want` smallest (device radix select), then sort only those
+    uint64_t ns = nu;
+    const TriKey* src = uniq;
+    DevBuf selb, thrb, sscr;
+    if (nu > want && !NRG_ENV_ON("NRG_SORT_DPLUS")) {
+        TriKey* picked = selb.as<TriKey>(want);
+        select_trikeys(c, uniq, nu, want, picked, thrb.as<TriKey>(1), sscr);
+        src = picked;
+        ns = want;
+    }
     TriKey* out = outb.as<TriKey>(std::max<uint64_t>(nu, 1));
-    sort_trikeys(c, uniq, out, nu, tmpb);
+    sort_trikeys(c, const_cast<TriKey*>(src), out, ns, tmpb);
     return std::min<uint64_t>(nu, want);
 }
 
@@ -568,13 +725,21 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
     }
     c.tic();
     const uint64_t nd = n * (uint64_t)knn.k;
-    DevBuf dirb, dir2b, tmpb;
+    DevBuf dirb, dir2b, tmpb, thrb, selb;
     TriKey* dir = dirb.as<TriKey>(nd);
     TriKey* dirs = dir2b.as<TriKey>(nd);
     directed_keys_kernel<<<g256(nd), 256, 0, c.stream>>>(S, knn.ids, knn.dists, n, knn.k, dir);
     NRG_LAUNCH_CHECK();
-    sort_trikeys(c, dir, dirs, nd, tmpb);
     const uint64_t dplus = std::min<uint64_t>(2 * m, nd);
+    // D+ (the dplus smallest directed entries, any order) and its largest key: a device
+    // radix select (NRG_SORT_DPLUS=1: the full sort, D+ its sorted prefix)
+    TriKey* thr = thrb.as<TriKey>(1);
+    if (NRG_ENV_ON("NRG_SORT_DPLUS")) {
+        sort_trikeys(c, dir, dirs, nd, tmpb);
+        NRG_CUDA(cudaMemcpyAsync(thr, dirs + (dplus - 1), sizeof(TriKey), cudaMemcpyDeviceToDevice, c.stream));
+    } else {
+        select_trikeys(c, dir, nd, dplus, dirs, thr, selb);
+    }
     // D: unique undirected pairs of D+
     DevBuf pkb, idxb, pk2b, idx2b, flagb, cntb;
     uint64_t* pk = pkb.as<uint64_t>(dplus);
@@ -582,7 +747,7 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
     uint64_t* pk2 = pk2b.as<uint64_t>(dplus);
     uint32_t* idx2 = idx2b.as<uint32_t>(dplus);
     uint8_t* flag = flagb.as<uint8_t>(std::max<uint64_t>(dplus, n));
-    unsigned long long* cnt = cntb.as<unsigned long long>(2);
+    unsigned long long* cnt = cntb.as<unsigned long long>(2);  // |D|, |S'|
     DevBuf dpairsb, dtabb;
     TriKey* dpairs = dpairsb.as<TriKey>(dplus);
     NRG_CUDA(cudaMemsetAsync(cnt, 0, 16, c.stream));
@@ -604,21 +769,22 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
     }
     // S': the threshold key (the dplus-th smallest directed entry) stays on the device;
     // |D| and |S'| come back in one round trip
-    saturated_kernel<<<g256(n), 256, 0, c.stream>>>(S, knn.ids, knn.dists, n, knn.k, dirs + (dplus - 1), flag);
+    saturated_kernel<<<g256(n), 256, 0, c.stream>>>(S, knn.ids, knn.dists, n, knn.k, thr, flag);
     NRG_LAUNCH_CHECK();
-    DevBuf satb, nsatb;
+    DevBuf satb;
     int32_t* sat = satb.as<int32_t>(n);
-    int* nsat = nsatb.as<int>(1);
     {
         size_t bytes = 0;
-        cub::DeviceSelect::Flagged(nullptr, bytes, S, flag, sat, nsat, (int64_t)n, c.stream);
+        cub::DeviceSelect::Flagged(nullptr, bytes, S, flag, sat, cnt + 1, (int64_t)n, c.stream);
         void* tmp = tmpb.ensure(bytes);
-        cub::DeviceSelect::Flagged(tmp, bytes, S, flag, sat, nsat, (int64_t)n, c.stream);
+        cub::DeviceSelect::Flagged(tmp, bytes, S, flag, sat, cnt + 1, (int64_t)n, c.stream);
     }
-    unsigned long long nD = 0;
-    int hsat = 0;
-    nD = c.read_scalar(cnt);
-    hsat = c.read_scalar(nsat);
+    // |D| and |S'| in one round trip
+    unsigned long long* hc = c.hp_small.as<unsigned long long>(2);
+    NRG_CUDA(cudaMemcpyAsync(hc, cnt, 16, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    const unsigned long long nD = hc[0];
+    const int hsat = (int)hc[1];
     c.toc(P_SELECT);
     trace.push_back({level, k, 0, knn.sweeps, n, (uint64_t)nD});
     kid.release();
