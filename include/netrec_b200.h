@@ -299,6 +299,13 @@ typedef struct {
     int (*bcast_f64)(void* user, double* v, int32_t n); /* from rank 0 */
 } nrg_host_transport;
 int nrg_comm_init_host(nrg_ctx* ctx, const nrg_host_transport* t, int32_t rank, int32_t world);
+/* Self-test of the installed communicator (collective: every rank calls it): each
+ * collective the sharded path uses (all-gather, ragged all-gather, all-to-all with
+ * empty pairs, u64 sum/max all-reduce up to a world x world matrix, f64 broadcast) on
+ * seeded patterns, verified on every rank; NRG error 100 on a mismatch.  Without a
+ * communicator (single GPU) it runs them on a one-rank NCCL communicator created for
+ * the call, which checks that NCCL loads and starts on this device. */
+int nrg_comm_selftest(nrg_ctx* ctx);
 /* The routing plan of one key exchange of the key-sharded distance cache (host-only):
  * from the world x world request-count matrix (row = requester, column = owner; counts
  * of 8-byte keys) the alltoallv byte counts and offsets of `rank` as sender (send_*) and

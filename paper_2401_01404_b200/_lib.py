@@ -114,6 +114,7 @@ SIGNATURES = {
     "nrg_loopback_create": (C.c_int, [_i32, C.POINTER(_VP)]),
     "nrg_loopback_destroy": (C.c_int, [_VP]),
     "nrg_comm_init_loopback": (C.c_int, [_P, _VP, _i32]),
+    "nrg_comm_selftest": (C.c_int, [_P]),
     "nrg_comm_init_host": (C.c_int, [_P, C.c_void_p, _i32, _i32]),
     "nrg_route_plan": (C.c_int, [_i32, _i32, np.ctypeslib.ndpointer(np.uint64, flags="C"),
                                  np.ctypeslib.ndpointer(np.uint64, flags="C"), np.ctypeslib.ndpointer(np.uint64, flags="C"),
@@ -455,6 +456,11 @@ class Model:
     def comm_init(self, uid: bytes, rank: int, world: int):
         """Join an NCCL job (uid from comm_unique_id() on rank 0)."""
         check(self.L.nrg_comm_init(self.h, uid, rank, world))
+
+    def comm_selftest(self):
+        """Run every collective of the installed communicator on seeded patterns (all
+        ranks call it); on a single-GPU context, on a one-rank NCCL communicator."""
+        check(self.L.nrg_comm_selftest(self.h))
 
     def comm_init_host(self, transport: "HostTransport"):
         """Join a sharded job whose collectives run over a host transport (e.g.

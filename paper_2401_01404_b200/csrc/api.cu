@@ -12,6 +12,8 @@
 #include <vector>
 
 #include "../../include/netrec_b200.h"
+#include <memory>
+
 #include "comm.cuh"
 #include "context.cuh"
 
@@ -734,6 +736,19 @@ int nrg_comm_init_host(nrg_ctx* x, const nrg_host_transport* t, int32_t rank, in
         x->c.comm = nrg::make_host_comm(*t, rank, world);
         x->c.rank = rank;
         x->c.world = world;
+    });
+}
+
+int nrg_comm_selftest(nrg_ctx* x) {
+    return guardx(x, [&] {
+        if (x->c.comm) {
+            nrg::comm_selftest(*static_cast<nrg::Comm*>(x->c.comm), x->c.stream);
+            return;
+        }
+        uint8_t id[128];
+        nrg::nccl_unique_id(id);
+        std::unique_ptr<nrg::Comm> one(nrg::make_nccl_comm(id, 0, 1, x->c.device));
+        nrg::comm_selftest(*one, x->c.stream);
     });
 }
 

@@ -339,4 +339,97 @@ Comm* make_loopback_comm(LoopbackGroup* g, int rank) {
     return c;
 }
 
+// ---------------------------------------------------------------- self-test
+// Every collective of the interface on seeded patterns, checked on every rank (all ranks
+// call it together): the same code validates the NCCL, host-transport and loopback
+// backends, at any world size (world = 1 runs the NCCL calls against the rank itself).
+namespace {
+inline uint8_t pat(int from, int to, size_t i) { return (uint8_t)(mix64(((uint64_t)from << 40) ^ ((uint64_t)to << 20) ^ i) >> 56); }
+}  // namespace
+
+void comm_selftest(Comm& cm, cudaStream_t s) {
+    const int W = cm.world, R = cm.rank;
+    auto upload = [&](const std::vector<uint8_t>& h) {
+        uint8_t* d = nullptr;
+        NRG_CUDA(cudaMalloc(&d, std::max<size_t>(h.size(), 16)));
+        if (!h.empty()) NRG_CUDA(cudaMemcpyAsync(d, h.data(), h.size(), cudaMemcpyHostToDevice, s));
+        return d;
+    };
+    auto download = [&](const uint8_t* d, size_t n) {
+        std::vector<uint8_t> h(n);
+        if (n) NRG_CUDA(cudaMemcpyAsync(h.data(), d, n, cudaMemcpyDeviceToHost, s));
+        NRG_CUDA(cudaStreamSynchronize(s));
+        return h;
+    };
+    // allgather: 1000 bytes per rank
+    {
+        const size_t nb = 1000;
+        std::vector<uint8_t> h(nb);
+        for (size_t i = 0; i < nb; ++i) h[i] = pat(R, W, i);
+        uint8_t* ds = upload(h);
+        uint8_t* dr = upload(std::vector<uint8_t>(nb * W, 0xEE));
+        cm.allgather(ds, dr, nb, s);
+        const auto got = download(dr, nb * W);
+        for (int r = 0; r < W; ++r)
+            for (size_t i = 0; i < nb; ++i)
+                if (got[r * nb + i] != pat(r, W, i)) fail(100, "comm selftest: allgather mismatch");
+        cudaFree(ds), cudaFree(dr);
+    }
+    // allgatherv: ragged sizes, every third rank contributes nothing
+    {
+        std::vector<size_t> nb(W), off(W, 0);
+        for (int r = 0; r < W; ++r) nb[r] = r % 3 == 2 ? 0 : 100 * (size_t)(r + 1) + 7;
+        for (int r = 1; r < W; ++r) off[r] = off[r - 1] + nb[r - 1];
+        const size_t tot = off[W - 1] + nb[W - 1];
+        std::vector<uint8_t> h(nb[R]);
+        for (size_t i = 0; i < nb[R]; ++i) h[i] = pat(R, W + 1, i);
+        uint8_t* ds = upload(h);
+        uint8_t* dr = upload(std::vector<uint8_t>(tot, 0xEE));
+        cm.allgatherv(ds, dr, nb, s);
+        const auto got = download(dr, tot);
+        for (int r = 0; r < W; ++r)
+            for (size_t i = 0; i < nb[r]; ++i)
+                if (got[off[r] + i] != pat(r, W + 1, i)) fail(100, "comm selftest: allgatherv mismatch");
+        cudaFree(ds), cudaFree(dr);
+    }
+    // alltoallv: rank r sends sz(r, q) bytes to q (some pairs empty)
+    {
+        auto sz = [](int from, int to) { return (size_t)((from * 7 + to * 3) % 5) * 64 + ((from + to) % 4 == 3 ? 0 : 8); };
+        std::vector<size_t> sb(W), so(W, 0), rb(W), ro(W, 0);
+        for (int q = 0; q < W; ++q) sb[q] = sz(R, q), rb[q] = sz(q, R);
+        for (int q = 1; q < W; ++q) so[q] = so[q - 1] + sb[q - 1], ro[q] = ro[q - 1] + rb[q - 1];
+        std::vector<uint8_t> h(so[W - 1] + sb[W - 1]);
+        for (int q = 0; q < W; ++q)
+            for (size_t i = 0; i < sb[q]; ++i) h[so[q] + i] = pat(R, q, i);
+        const size_t tot = ro[W - 1] + rb[W - 1];
+        uint8_t* ds = upload(h);
+        uint8_t* dr = upload(std::vector<uint8_t>(tot, 0xEE));
+        cm.alltoallv(ds, sb, so, dr, rb, ro, s);
+        const auto got = download(dr, tot);
+        for (int q = 0; q < W; ++q)
+            for (size_t i = 0; i < rb[q]; ++i)
+                if (got[ro[q] + i] != pat(q, R, i)) fail(100, "comm selftest: alltoallv mismatch");
+        cudaFree(ds), cudaFree(dr);
+    }
+    // host-scalar collectives; the long vector is a world x world routing matrix and more
+    for (const int n : {3, W * W + 70}) {
+        std::vector<uint64_t> v(n), mx(n);
+        for (int t = 0; t < n; ++t) v[t] = (uint64_t)(R + 1) * (t + 1), mx[t] = mix64((uint64_t)R * 1000003 + t) >> 8;
+        cm.allreduce_u64(v.data(), n, false, s);
+        cm.allreduce_u64(mx.data(), n, true, s);
+        for (int t = 0; t < n; ++t) {
+            uint64_t want = 0;
+            for (int r = 0; r < W; ++r) want = std::max(want, mix64((uint64_t)r * 1000003 + t) >> 8);
+            if (v[t] != (uint64_t)W * (W + 1) / 2 * (t + 1) || mx[t] != want) fail(100, "comm selftest: allreduce mismatch");
+        }
+    }
+    {
+        double v[5];
+        for (int t = 0; t < 5; ++t) v[t] = R == 0 ? 0.1 * (t + 1) : -1.0;
+        cm.bcast_f64(v, 5, s);
+        for (int t = 0; t < 5; ++t)
+            if (v[t] != 0.1 * (t + 1)) fail(100, "comm selftest: broadcast mismatch");
+    }
+}
+
 }  // namespace nrg

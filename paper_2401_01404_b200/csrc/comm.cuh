@@ -44,6 +44,8 @@ Comm* make_host_comm(const nrg_host_transport& t, int rank, int world);
 uint64_t route_plan(int world, int rank, const uint64_t* mat, std::vector<size_t>& sb, std::vector<size_t>& so,
                     std::vector<size_t>& rb, std::vector<size_t>& ro);
 int nccl_unique_id(uint8_t id[128]);
+// every collective of `cm` on seeded patterns, verified on every rank (collective call)
+void comm_selftest(Comm& cm, cudaStream_t s);
 
 struct LoopbackGroup;
 LoopbackGroup* loopback_group_create(int world);

@@ -106,6 +106,7 @@ def _gcd_worker(rank, world, port, X, lam, out):
     import paper_2401_01404_b200 as P
     m = P.Model.from_samples(X, P.NRG_ISING, lam)
     m.comm_init_host(P.TorchDistTransport())
+    m.comm_selftest()  # every collective of the host transport on seeded patterns first
     m.reset_counters()
     recs = [m.gcd_iteration(it, kappa=2.0, seed=5, want_candidates=True) for it in (1, 2, 3)]
     out.put((rank, [(float(r["delta"]), float(r["objective"]), c) for r, c in recs], m.get_state(),

@@ -44,6 +44,25 @@ def _models(gpu, X, lam, world):
     return grp, ms
 
 
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_comm_selftest_loopback(gpu, world):
+    """Every collective of the interface on seeded patterns (ragged and empty
+    contributions, a world x world count matrix) through the loopback backend."""
+    X, _ = O.gen_ising(64, 64, seed=1)
+    grp, ms = _models(gpu, X, 10.0, world)
+    _run_ranks(world, lambda r: ms[r].comm_selftest())
+    del ms, grp
+
+
+def test_comm_selftest_nccl_one_rank(gpu):
+    """The NCCL backend on this GPU: libnccl loads, a one-rank communicator starts, and
+    its all-gather / all-reduce / broadcast calls return the expected data.  (Point-to-
+    point exchanges need a second GPU; the driver's multi-GPU bench runs them.)"""
+    X, _ = O.gen_ising(64, 64, seed=1)
+    m = gpu.Model.from_samples(X.astype(np.int8), gpu.NRG_ISING, 10.0)
+    m.comm_selftest()
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_knn_and_find_best_match_single(gpu, world):
     X, _ = O.gen_ising(700, 300, seed=4)
