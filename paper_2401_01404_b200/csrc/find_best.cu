@@ -158,13 +158,15 @@ static void sort_trikeys(Context& c, TriKey* in, TriKey* out, uint64_t n, DevBuf
 // The K smallest of n distinct (dist, a, b) keys, unsorted, and a threshold T such that
 // an input key is among the K smallest iff it is <= T (the reference's nth_element,
 // inc/find_best.hpp:114-131: D+ and the S' test need the set and its largest key, not
-// an order).  MSD radix select over the packed key (hi = dkey, lo = a << ib | b), 8-bit
-// digits, in ONE cooperative launch and without a host round trip: per pass every CTA
-// histograms the digit of the keys still matching the prefix, one grid barrier, then
-// every CTA reads the same 256 counts and extends the prefix identically.  Once the
-// remaining rank equals the size of the prefix group, the whole group is in and the
-// passes stop (T = prefix with the unresolved bits set: no input key lies between the
-// group's largest key and T).
+// an order).  MSD radix select in ONE cooperative launch, without a host round trip:
+// a first pass finds the range of the distance keys, so the select runs over the packed
+// key ((dkey - dmin) << 2 ib | a << ib | b -- the same order over only the occupied bits,
+// ~70 instead of 98 at config 4) in 12-bit digits: per pass every CTA histograms the
+// digit of the keys still matching the prefix (a warp whose keys share a digit -- the
+// tie block at -base -- adds once), one grid barrier, then every CTA scans the same 4096
+// counts and extends the prefix identically.  Once the remaining rank equals the size of
+// the prefix group, the whole group is in and the passes stop (T = prefix with the
+// unresolved bits set: no input key lies between the group's largest key and T).
 __device__ __forceinline__ void sel_grid_sync(unsigned* bar, unsigned nblocks) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -182,96 +184,181 @@ __device__ __forceinline__ void sel_grid_sync(unsigned* bar, unsigned nblocks) {
     }
     __syncthreads();
 }
-constexpr int kSelThreads = 512;
+constexpr int kSelThreads = 1024;
+constexpr int kSelBits = 12, kSelBins = 1 << kSelBits;
+constexpr int kSelMaxPass = (64 + 62 + kSelBits - 1) / kSelBits;
+// bits [shift, shift + width) of the 128-bit value (hi, lo), width <= 32
+__device__ __forceinline__ unsigned sel_digit(uint64_t hi, uint64_t lo, int shift, int width) {
+    uint64_t v;
+    if (shift >= 64)
+        v = hi >> (shift - 64);
+    else if (shift == 0)
+        v = lo;
+    else
+        v = (lo >> shift) | (hi << (64 - shift));
+    return (unsigned)v & ((1u << width) - 1u);
+}
 __global__ void __launch_bounds__(kSelThreads) trikey_select_kernel(const TriKey* __restrict__ in, uint64_t n,
                                                                     uint64_t K, int ib, unsigned* __restrict__ hist,
+                                                                    unsigned long long* __restrict__ mm,
                                                                     unsigned* bar, TriKey* __restrict__ out,
                                                                     unsigned long long* __restrict__ cnt,
                                                                     TriKey* __restrict__ thr) {
-    __shared__ unsigned sh[256];
-    __shared__ uint64_t s_p[2], s_m[2];  // prefix and mask over (hi, lo)
+    __shared__ unsigned sh[kSelBins];
+    __shared__ unsigned wsum[kSelThreads / 32];
+    __shared__ unsigned long long s_mm[2][kSelThreads / 32];
+    __shared__ uint64_t s_p[2], s_m[2];  // prefix and mask over the packed key (hi, lo)
     __shared__ unsigned long long s_krem;
     __shared__ int s_done;
-    const int tid = threadIdx.x;
-    const int lob = 2 * ib;
-    const uint64_t lomask = lob >= 64 ? ~0ull : (1ull << lob) - 1;
-    if (tid == 0) {
-        s_p[0] = s_p[1] = s_m[0] = s_m[1] = 0;
-        s_krem = K;
-        s_done = 0;
-    }
-    __syncthreads();
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int lob = 2 * ib;  // <= 62
     const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + tid, st = (uint64_t)gridDim.x * blockDim.x;
-    const int npass = 8 + (lob + 7) / 8;
-    for (int pass = 0; pass < npass && !s_done; ++pass) {
-        int word, shift, width;
-        if (pass < 8) {
-            word = 0;
-            shift = 56 - 8 * pass;
-            width = 8;
-        } else {
-            word = 1;
-            shift = lob - 8 * (pass - 7);
-            width = 8;
-            if (shift < 0) {
-                width += shift;
-                shift = 0;
-            }
-        }
-        const uint64_t ph = s_p[0], pl = s_p[1], mh = s_m[0], ml = s_m[1];
-        for (int b = tid; b < 256; b += kSelThreads) sh[b] = 0u;
-        __syncthreads();
+    // range of the distance keys (mm[0] = max of ~d, mm[1] = max of d; zero-initialised)
+    {
+        unsigned long long a = 0ull, b = 0ull;
         for (uint64_t e = t0; e < n; e += st) {
-            const TriKey k = in[e];
-            const uint64_t hi = k.d, lo = ((uint64_t)k.a << ib) | k.b;
-            if ((hi & mh) == ph && (lo & ml) == pl) {
-                const unsigned dg = (unsigned)(((word ? lo : hi) >> shift) & ((1u << width) - 1u));
-                atomicAdd(&sh[dg], 1u);
-            }
+            const unsigned long long d = in[e].d;
+            a = max(a, ~d);
+            b = max(b, d);
         }
-        __syncthreads();
-        for (int b = tid; b < 256; b += kSelThreads)
-            if (sh[b]) atomicAdd(&hist[pass * 256 + b], sh[b]);
-        sel_grid_sync(bar, gridDim.x);
-        for (int b = tid; b < 256; b += kSelThreads) sh[b] = __ldcg(&hist[pass * 256 + b]);
+        for (int o = 16; o; o >>= 1) {
+            a = max(a, __shfl_xor_sync(0xffffffffu, a, o));
+            b = max(b, __shfl_xor_sync(0xffffffffu, b, o));
+        }
+        if (lane == 0) {
+            s_mm[0][wid] = a;
+            s_mm[1][wid] = b;
+        }
         __syncthreads();
         if (tid == 0) {
-            unsigned long long below = 0, krem = s_krem;
-            int bin = 0;
-            for (; bin < (1 << width) - 1; ++bin) {
-                if (below + sh[bin] >= krem) break;
-                below += sh[bin];
+            for (int w = 1; w < kSelThreads / 32; ++w) {
+                a = max(a, s_mm[0][w]);
+                b = max(b, s_mm[1][w]);
             }
-            const uint64_t wm = ((1ull << width) - 1) << shift;
-            s_p[word] |= (uint64_t)bin << shift;
-            s_m[word] |= wm;
+            atomicMax(&mm[0], a);
+            atomicMax(&mm[1], b);
+            s_p[0] = s_p[1] = s_m[0] = s_m[1] = 0;
+            s_krem = K;
+            s_done = 0;
+        }
+        sel_grid_sync(bar, gridDim.x);
+    }
+    const uint64_t dmin = ~__ldcg(&mm[0]), dmax = __ldcg(&mm[1]);
+    const uint64_t span = dmax - dmin;
+    const int db = 64 - __clzll((long long)span);  // bits of d - dmin (0 when every d is equal)
+    const int T = db + lob;
+    const int npass = (T + kSelBits - 1) / kSelBits;
+    // packed key of an entry: lo = (dd << lob) | ids, hi = the bits of dd past lo
+    auto pack = [&](const TriKey& k, uint64_t& hi, uint64_t& lo) {
+        const uint64_t dd = k.d - dmin;
+        lo = (dd << lob) | ((uint64_t)k.a << ib) | k.b;
+        hi = dd >> (64 - lob);
+    };
+    for (int pass = 0; pass < npass && !s_done; ++pass) {
+        const int top = T - kSelBits * pass;          // this pass resolves bits [shift, top)
+        const int shift = max(0, top - kSelBits), width = top - shift;
+        const uint64_t ph = s_p[0], pl = s_p[1], mh = s_m[0], ml = s_m[1];
+        for (int b = tid; b < kSelBins; b += kSelThreads) sh[b] = 0u;
+        __syncthreads();
+        for (uint64_t e0 = (uint64_t)blockIdx.x * blockDim.x; e0 < n; e0 += st) {
+            const uint64_t e = e0 + tid;
+            bool hit = false;
+            unsigned dg = 0;
+            if (e < n) {
+                uint64_t hi, lo;
+                pack(in[e], hi, lo);
+                hit = (hi & mh) == ph && (lo & ml) == pl;
+                dg = sel_digit(hi, lo, shift, width);
+            }
+            const unsigned act = __ballot_sync(0xffffffffu, hit);
+            if (act) {
+                const int lead = __ffs(act) - 1;
+                const unsigned ldg = __shfl_sync(0xffffffffu, dg, lead);
+                const unsigned same = __ballot_sync(0xffffffffu, hit && dg == ldg);
+                if (lane == lead) atomicAdd(&sh[ldg], (unsigned)__popc(same));
+                if (hit && dg != ldg) atomicAdd(&sh[dg], 1u);
+            }
+        }
+        __syncthreads();
+        for (int b = tid; b < kSelBins; b += kSelThreads)
+            if (sh[b]) atomicAdd(&hist[pass * kSelBins + b], sh[b]);
+        sel_grid_sync(bar, gridDim.x);
+        // every CTA: the bin holding the krem-th key of the group (block scan of the counts;
+        // thread t owns bins [per t, per (t + 1)))
+        constexpr int per = kSelBins / kSelThreads;
+        unsigned c[per], mine = 0;
+#pragma unroll
+        for (int q = 0; q < per; ++q) {
+            c[q] = __ldcg(&hist[pass * kSelBins + tid * per + q]);
+            mine += c[q];
+        }
+        unsigned incl = mine;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        if (lane == 31) wsum[wid] = incl;
+        __syncthreads();
+        unsigned long long excl = incl - mine;
+        for (int w = 0; w < wid; ++w) excl += wsum[w];
+        const unsigned long long krem = s_krem;
+        __syncthreads();  // every thread has read s_krem
+        if (excl < krem && krem <= excl + mine) {
+            unsigned long long below = excl;
+            int q = 0;
+            for (; q < per - 1; ++q) {
+                if (below + c[q] >= krem) break;
+                below += c[q];
+            }
+            const unsigned bin = (unsigned)(tid * per + q);
+            // prefix and mask gain the bits [shift, shift + width) of the 128-bit key
+            const uint64_t wm = (width >= 64 ? ~0ull : (1ull << width) - 1);
+            if (shift >= 64) {
+                s_p[0] |= (uint64_t)bin << (shift - 64);
+                s_m[0] |= wm << (shift - 64);
+            } else {
+                s_p[1] |= (uint64_t)bin << shift;
+                s_m[1] |= wm << shift;
+                if (shift + width > 64) {
+                    s_p[0] |= (uint64_t)bin >> (64 - shift);
+                    s_m[0] |= wm >> (64 - shift);
+                }
+            }
             s_krem = krem - below;
-            if (s_krem == sh[bin]) s_done = 1;  // the whole prefix group is in
+            if (krem - below == c[q]) s_done = 1;  // the whole prefix group is in
         }
         __syncthreads();
     }
-    const uint64_t th = s_p[0] | ~s_m[0], tl = s_p[1] | (~s_m[1] & lomask);
+    // threshold in packed form: the prefix with every unresolved bit of the T-bit key set
+    const uint64_t full_lo = T >= 64 ? ~0ull : (1ull << T) - 1;
+    const uint64_t full_hi = T > 64 ? (1ull << (T - 64)) - 1 : 0ull;
+    const uint64_t th = s_p[0] | (~s_m[0] & full_hi), tl = s_p[1] | (~s_m[1] & full_lo);
     for (uint64_t e0 = (uint64_t)blockIdx.x * blockDim.x; e0 < n; e0 += st) {
         const uint64_t e = e0 + tid;
         bool keep = false;
         TriKey k;
         if (e < n) {
             k = in[e];
-            const uint64_t hi = k.d, lo = ((uint64_t)k.a << ib) | k.b;
+            uint64_t hi, lo;
+            pack(k, hi, lo);
             keep = hi < th || (hi == th && lo <= tl);
         }
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
-        const int lane = tid & 31;
         unsigned long long at = 0;
         if (lane == 0 && bal) at = atomicAdd(cnt, (unsigned long long)__popc(bal));
         at = __shfl_sync(0xffffffffu, at, 0);
         if (keep) out[at + __popc(bal & ((1u << lane) - 1u))] = k;
     }
     if (blockIdx.x == 0 && tid == 0) {
+        // back to (dist, a, b): dd = threshold >> lob; past the keys' span (unresolved
+        // distance bits) every key is in: T = (dmax, largest ids)
+        const uint64_t ddt = (tl >> lob) | (th << (64 - lob));
+        const bool over = (th >> lob) != 0 || ddt > span;
+        const uint64_t idm = (1ull << ib) - 1;
         TriKey t;
-        t.d = th;
-        t.a = (uint32_t)(tl >> ib);
-        t.b = (uint32_t)(tl & ((1ull << ib) - 1));
+        t.d = over ? dmax : dmin + ddt;
+        t.a = over ? (uint32_t)idm : (uint32_t)((tl >> ib) & idm);
+        t.b = over ? (uint32_t)idm : (uint32_t)(tl & idm);
         *thr = t;
     }
 }
@@ -285,18 +372,19 @@ static void select_trikeys(Context& c, const TriKey* in, uint64_t n, uint64_t K,
         NRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, trikey_select_kernel, kSelThreads, 0));
         int sms = 0;
         NRG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
-        grid = std::max(1, per) * sms;
+        grid = std::max(1, std::min(per, 1)) * sms;  // one CTA per SM: 4096 histogram adds per CTA and pass
     }
     const int ib = id_bits(c);
-    const int npass = 8 + (2 * ib + 7) / 8;
-    const size_t words = (size_t)npass * 256 + 2 + 2;  // hist, barrier, count (u64)
+    if (2 * ib > 62) fail(100, "select: node ids wider than 31 bits");
+    const size_t words = (size_t)kSelMaxPass * kSelBins + 4 + 2 + 2;  // hist, range (2 u64), barrier, count (u64)
     unsigned* hist = scratch.as<unsigned>(words);
-    unsigned* bar = hist + npass * 256;
+    unsigned long long* mm = reinterpret_cast<unsigned long long*>(hist + (size_t)kSelMaxPass * kSelBins);
+    unsigned* bar = reinterpret_cast<unsigned*>(mm + 2);
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(bar + 2);
     NRG_CUDA(cudaMemsetAsync(hist, 0, words * 4, c.stream));
     const unsigned g = (unsigned)std::min<uint64_t>((uint64_t)grid, std::max<uint64_t>(1, ceil_div(n, kSelThreads)));
-    void* args[] = {(void*)&in, (void*)&n, (void*)&K, (void*)&ib, (void*)&hist, (void*)&bar, (void*)&out, (void*)&cnt,
-                    (void*)&thr};
+    void* args[] = {(void*)&in, (void*)&n, (void*)&K, (void*)&ib, (void*)&hist, (void*)&mm, (void*)&bar, (void*)&out,
+                    (void*)&cnt, (void*)&thr};
     NRG_CUDA(cudaLaunchCooperativeKernel((void*)trikey_select_kernel, g, kSelThreads, args, 0, c.stream));
     NRG_LAUNCH_CHECK();
 }

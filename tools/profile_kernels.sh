@@ -9,6 +9,8 @@ while read -r name regex skip; do
   ncu --profile-from-start off --clock-control none --set full --import-source on \
       -k "regex:$regex" -s "$skip" -c 1 -f -o "$out/$name" python tools/steady_sweep.py > "$out/$name.json" 2> "$out/$name.err"
   python tools/ncu_sum.py "$out/$name.ncu-rep" > "$out/$name.txt" 2>&1
+  ncu -i "$out/$name.ncu-rep" --page details > "$out/$name.details.txt" 2>&1
+  [ -n "$KEEP_REP" ] || rm -f "$out/$name.ncu-rep"  # gpurun_out merges at most 64 MiB
 done <<'L'
 gather_bits knn_gather_bits_kernel 0
 gather256 knn_gather_kernel 1
