@@ -55,9 +55,14 @@ __global__ void rank_kernel(const int32_t* __restrict__ perm, uint64_t n, int32_
     if (t < n) rank[perm[t]] = (int32_t)t;
 }
 
-// initial out-neighbours: Floyd sampling (inc/knn.hpp:177-199).  One warp per node:
-// lane 0 draws the sequence, the warp tests membership in parallel.
+// initial out-neighbours: Floyd sampling (inc/knn.hpp:177-199).  One warp per node.  The
+// stream is counter-based (draw i = mix64 of key and i + 1, one draw per pick), so the
+// draws of a round of 32 picks are computed by the lanes in parallel; only the membership
+// rule (a draw already picked is replaced by t) runs in pick order, on registers.
 // (nodes, rank, gid, qi, qj point at this rank's first own row; `own` rows, n = level size)
+__device__ __forceinline__ uint64_t floyd_draw(const SplitRng& r, uint64_t i, uint64_t t) {
+    return __umul64hi(mix64(r.key + 0x9e3779b97f4a7c15ULL * (i + 1)), t + 1);  // SplitRng::below, draw i
+}
 __global__ void knn_init_kernel(const int32_t* __restrict__ nodes, const int32_t* __restrict__ sorted_ids,
                                 const int32_t* __restrict__ rank, const int32_t* __restrict__ loc, uint64_t own,
                                 uint64_t n, int kw, uint64_t seed, int32_t* __restrict__ gid,
@@ -66,20 +71,28 @@ __global__ void knn_init_kernel(const int32_t* __restrict__ nodes, const int32_t
     const int lane = threadIdx.x & 31;
     if (li >= own) return;
     const SplitRng root(seed);
-    SplitRng r = root.split((uint64_t)nodes[li] + 1);
+    const SplitRng r = root.split((uint64_t)nodes[li] + 1);
     const uint64_t self = (uint64_t)rank[li];
     int32_t* picks = gid + li * kw;  // ranks first, local ids after
-    int np = 0;
-    for (uint64_t t = n - 1 - (uint64_t)kw; t < n - 1; ++t) {
-        uint64_t v = 0;
-        if (lane == 0) v = r.below(t + 1);
-        v = __shfl_sync(0xffffffffu, v, 0);
+    const uint64_t tbase = n - 1 - (uint64_t)kw;
+    for (int base = 0; base < kw; base += 32) {
+        const int i = base + lane;
+        const uint64_t t = tbase + (uint64_t)i;
+        const uint64_t v = i < kw ? floyd_draw(r, (uint64_t)i, t) : 0;
+        // against the picks of earlier rounds
         bool hit = false;
-        for (int q = lane; q < np; q += 32) hit |= ((uint64_t)picks[q] == v);
-        if (__any_sync(0xffffffffu, hit)) v = t;
-        if (lane == 0) picks[np] = (int32_t)v;
+        for (int q = 0; q < base; ++q) hit |= ((uint64_t)picks[q] == v);
+        // within the round, in pick order
+        uint64_t mine = 0;
+        const int cnt = min(32, kw - base);
+        for (int s = 0; s < cnt; ++s) {
+            const uint64_t vs = __shfl_sync(0xffffffffu, v, s);
+            const bool hs = __shfl_sync(0xffffffffu, (int)hit, s) != 0;
+            const bool dup = __any_sync(0xffffffffu, lane < s && mine == vs);
+            if (lane == s) mine = (hs || dup) ? t : v;
+        }
+        if (i < kw) picks[i] = (int32_t)mine;
         __syncwarp();
-        ++np;
     }
     for (int t = lane; t < kw; t += 32) {
         uint64_t rk = (uint64_t)picks[t];
@@ -106,16 +119,27 @@ __global__ void knn_init_bits_kernel(const int32_t* __restrict__ nodes, const in
     for (int w = lane; w < words; w += 32) bm[w] = 0u;
     __syncwarp();
     int32_t* picks = gid + li * kw;
-    if (lane == 0) {
-        const SplitRng root(seed);
-        SplitRng r = root.split((uint64_t)nodes[li] + 1);
-        int np = 0;
-        for (uint64_t t = n - 1 - (uint64_t)kw; t < n - 1; ++t) {
-            uint64_t v = r.below(t + 1);
-            if ((bm[v >> 5] >> (v & 31)) & 1u) v = t;
-            bm[v >> 5] |= 1u << (v & 31);
-            picks[np++] = (int32_t)v;
+    const SplitRng root(seed);
+    const SplitRng r = root.split((uint64_t)nodes[li] + 1);
+    const uint64_t tbase = n - 1 - (uint64_t)kw;
+    for (int base = 0; base < kw; base += 32) {
+        const int i = base + lane;
+        const uint64_t t = tbase + (uint64_t)i;
+        const uint32_t v = i < kw ? (uint32_t)floyd_draw(r, (uint64_t)i, t) : 0u;
+        uint32_t mine = 0;
+        const int cnt = min(32, kw - base);
+        for (int s = 0; s < cnt; ++s) {
+            const uint32_t vs = __shfl_sync(0xffffffffu, v, s);
+            const bool dup = (bm[vs >> 5] >> (vs & 31)) & 1u;  // every lane reads the same word
+            const uint32_t pick = dup ? (uint32_t)(tbase + (uint64_t)(base + s)) : vs;
+            __syncwarp();
+            if (lane == s) {
+                mine = pick;
+                bm[pick >> 5] |= 1u << (pick & 31);
+            }
+            __syncwarp();
         }
+        if (i < kw) picks[i] = (int32_t)mine;
     }
     __syncwarp();
     const uint64_t self = (uint64_t)rank[li];

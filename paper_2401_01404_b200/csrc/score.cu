@@ -408,8 +408,16 @@ __global__ void __launch_bounds__(256, NRG_K1S_MINB) ising_screen_pipe_kernel(Is
         }
         cp_async_commit();
     };
-    for (uint64_t c0 = warp0 * 32; c0 < n; c0 += nwarps * 32) {
-        const int len = (int)min((uint64_t)32, n - c0);
+    // entries per warp chunk: 32, except on a recheck list (a device-side count that is
+    // usually a few hundred entries): spread over the resident warps, so no warp walks 16
+    // dependent steps while the others idle
+    int chunk = 32;
+    if (sel) {
+        const uint64_t per = (n + nwarps - 1) / nwarps;
+        chunk = (int)min((uint64_t)32, max((uint64_t)P, (per + P - 1) / P * P));
+    }
+    for (uint64_t c0 = warp0 * chunk; c0 < n; c0 += nwarps * chunk) {
+        const int len = (int)min((uint64_t)chunk, n - c0);
         const int li = lane < len ? lane : 0;
         const uint64_t my_e = sel ? sel[c0 + li] : c0 + li;
         const int my_s = es[my_e], my_p = ep[my_e];
@@ -1004,6 +1012,11 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
                 unsigned long long* rn = four ? c.sc_rn.as<unsigned long long>(1) : nullptr;
                 if (four) NRG_CUDA(cudaMemsetAsync(rn, 0, 8, c.stream));
                 static const int g4 = getenv("NRG_K1_G4") ? atoi(getenv("NRG_K1_G4")) : 8;  // lanes per pair (4-bit pass)
+                // the recheck pass strides over a device-side count that is a fraction of a percent of
+                // n in the steady state: one resident wave of CTAs (3 per SM) instead of a grid sized
+                // for n, whose empty CTAs cost ~20 us per launch
+                static const int rwaves = getenv("NRG_K1R_CTAS") ? atoi(getenv("NRG_K1R_CTAS")) : 3;
+                const uint64_t rblocks = std::min<uint64_t>(sblocks, (uint64_t)sms * rwaves);
 #define NRG_LAUNCH_PIPE(NSV)                                                                                       \
     {                                                                                                              \
         constexpr size_t smem = (size_t)8 * (NSV) * 2 * (1024 + 128);                                             \
@@ -1043,7 +1056,7 @@ void score_entries(Context& c, int mode, const int32_t* s, const int32_t* p, uin
                 ising_screen_pipe_kernel<16, 2, NSV, true><<<(unsigned)sblocks, 256, smem4, c.stream>>>(           \
                     S, W, s, p, n, c.lambda, base, out, rl, nullptr, nullptr, rn, c.dcounters(), n_dev, k1log,      \
                     nullptr);                                                                                      \
-            ising_screen_pipe_kernel<16, 2, NSV, false><<<(unsigned)sblocks, 256, smem, c.stream>>>(               \
+            ising_screen_pipe_kernel<16, 2, NSV, false><<<(unsigned)rblocks, 256, smem, c.stream>>>(               \
                 S, W, s, p, n, c.lambda, base, out, surv, surv_g, surv_flag, nsurv, c.dcounters(), rn, nullptr,    \
                 rl);                                                                                               \
         } else {                                                                                                   \
