@@ -198,6 +198,30 @@ __global__ void __launch_bounds__(NT) row_sort_kernel(int32_t* __restrict__ gid,
     }
 }
 
+// rows of up to 32 entries: one warp per row, an entry per lane; entries are distinct in
+// (dist, global id), so an entry's place is the number of entries ahead of it (kw rounds
+// of shuffles, no shared memory, no barriers)
+__global__ void __launch_bounds__(256) row_sort_warp_kernel(int32_t* __restrict__ gid, double* __restrict__ gd,
+                                                            const int32_t* __restrict__ nodes, uint64_t n, int kw) {
+    const uint64_t li = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (li >= n) return;
+    const bool have = lane < kw;
+    const double d = have ? gd[li * kw + lane] : 0.0;
+    const int32_t id = have ? gid[li * kw + lane] : 0;
+    const int32_t g = have ? nodes[id] : 0;
+    int ahead = 0;
+    for (int s = 0; s < kw; ++s) {
+        const double ds = __shfl_sync(0xffffffffu, d, s);
+        const int32_t gs = __shfl_sync(0xffffffffu, g, s);
+        ahead += (ds < d || (ds == d && gs < g)) ? 1 : 0;
+    }
+    if (have) {
+        gd[li * kw + ahead] = d;
+        gid[li * kw + ahead] = id;
+    }
+}
+
 // ---------------------------------------------------------------- cache claim
 __device__ __forceinline__ uint64_t cache_claim_k(HashView h, uint64_t key, bool& mine) {
     uint64_t s = slot_of(key, h.mask);
@@ -1531,7 +1555,10 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             NRG_CUDA(cudaFuncSetAttribute(row_sort_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)rs_smem));
         if (own) {
-            if (P <= 64)
+            if (kw <= 32)
+                row_sort_warp_kernel<<<(unsigned)ceil_div(own * 32, 256), 256, 0, c.stream>>>(gid + lo * kw, gd + lo * kw,
+                                                                                           d_nodes, own, kw);
+            else if (P <= 64)
                 row_sort_kernel<32><<<(unsigned)own, 32, rs_smem, c.stream>>>(gid + lo * kw, gd + lo * kw, d_nodes, own,
                                                                              kw, P);
             else
