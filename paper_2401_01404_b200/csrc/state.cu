@@ -90,13 +90,15 @@ void ctx_init(Context& c, int n, int m, int kind, double lambda, int device) {
         // Back the pool with physical memory once per device and process: a first large
         // allocation, freed, stays in the pool (threshold above), so the sweeps' scratch
         // is carved from mapped memory -- mapping fresh pool memory mid-sweep measured
-        // anywhere from 3 to 300 ms per few hundred MB.  NRG_POOL_RESERVE_GB overrides
-        // (0 disables); at most a quarter of the free memory.
+        // anywhere from 3 to 300 ms per few hundred MB.  40 GB: config 4 peaks near 20 GB while
+        // the distance memo is re-sized (with 16 GB, sweeps of 50-80 ms instead of 33 ms
+        // showed up every few generations).  NRG_POOL_RESERVE_GB overrides (0 disables); at
+        // most a quarter of the free memory.
         static bool reserved[64] = {};
         if (device >= 0 && device < 64 && !reserved[device]) {
             reserved[device] = true;
             const char* e = getenv("NRG_POOL_RESERVE_GB");
-            size_t want = (size_t)((e ? atof(e) : 16.0) * (1ull << 30));
+            size_t want = (size_t)((e ? atof(e) : 40.0) * (1ull << 30));
             size_t fr = 0, tot = 0;
             NRG_CUDA(cudaMemGetInfo(&fr, &tot));
             want = std::min(want, fr / 4);
@@ -964,7 +966,11 @@ void begin_generation(Context& c) {
         // a generation that flushed the memo counted only the pairs since its last flush:
         // keep the size (config 5 would otherwise free and re-map tens of GB every sweep)
         const bool flushed = c.cache_flushes != c.flushes_at_gen;
-        if (ncap != c.Ccap && !(flushed && ncap < c.Ccap)) {
+        // shrink only when the need plus another 30% fits half the table: a count that
+        // hovers at a power-of-two boundary (config 4: 161M * 10/6 vs 2^28) otherwise frees
+        // and re-maps 2 x 4 GB every few generations, a 20-80 ms stall each time
+        const bool shrink = ncap < c.Ccap && (want * 10 / 6) / 10 * 13 < c.Ccap / 2;
+        if ((ncap > c.Ccap || shrink) && !(flushed && ncap < c.Ccap)) {
             c.Ckeys = DevBuf();
             c.Cvals = DevBuf();
             c.Csurv = DevBuf();
