@@ -287,6 +287,29 @@ struct Context {
     uint64_t Wcap = 0;
     DevBuf Wcount;  // u64[2]: live, used (occupied incl. tombstones)
     uint64_t state_version = 1;
+    // Per-node staleness flags (u8[n]): bit 0 theta_i not yet re-optimised for the current
+    // row H_i, bit 1 the snapshot row, bit 2 the node's log-posterior term.  Set by the
+    // kernels that change H_i (the update kernel) or theta_i (the theta pass), cleared by
+    // the consumer that refreshes the row, so a sweep recomputes only the rows it touched
+    // (a third of the nodes early in a config-4 reconstruction, a tenth near convergence).
+    // flags_version is the state version the flags describe: a mutation that does not
+    // maintain them bumps state_version only, and the next consumer marks every row.
+    DevBuf row_flags, lp_node;
+    uint64_t flags_version = 0;
+    uint8_t* dflags() { return static_cast<uint8_t*>(row_flags.p); }
+    void sync_flags() {
+        static const bool off = getenv("NRG_NO_ROW_FLAGS") != nullptr;  // every row, every time
+        if (!off && flags_version == state_version && row_flags.p) return;
+        uint8_t* f = row_flags.as<uint8_t>((size_t)n);
+        NRG_CUDA(cudaMemsetAsync(f, 7, (size_t)n, stream));
+        flags_version = state_version;
+    }
+    // a state change whose kernels kept the flags exact
+    void bump_flagged() {
+        const bool ok = flags_version == state_version;
+        ++state_version;
+        if (ok) flags_version = state_version;
+    }
 
     // snapshot
     DevBuf T32, T64, T8, P8, Q8, BL, Tsq, U, xx;
@@ -551,7 +574,7 @@ void get_state(Context& c, double* theta, uint64_t cap, int32_t* ei, int32_t* ej
                uint64_t* n_edges);
 void get_sums(Context& c, double* out);
 void ensure_snapshot(Context& c);
-void snapshot_rows(Context& c, const int32_t* rows, uint64_t nr);  // refresh only these rows
+void snapshot_rows(Context& c, const int32_t* rows, uint64_t nr);  // only these rows are stale
 double log_posterior(Context& c);
 double generation_base(Context& c);
 void begin_generation(Context& c);

@@ -464,8 +464,15 @@ __global__ void __launch_bounds__(256) snapshot_ising_kernel(const double* __res
                                                              int8_t* __restrict__ T8, uint32_t* __restrict__ P8,
                                                              float4* __restrict__ Q, double* __restrict__ Tsq,
                                                              const int32_t* __restrict__ rows, uint32_t* __restrict__ P4,
-                                                             float4* __restrict__ Q4, const uint32_t* __restrict__ Xb) {
+                                                             float4* __restrict__ Q4, const uint32_t* __restrict__ Xb,
+                                                             uint8_t* __restrict__ flags) {
     const int r = rows ? rows[blockIdx.x] : (int)blockIdx.x;
+    // only the rows whose H_i or theta_i changed since their last snapshot (flag bit 1)
+    if (flags) {
+        if (!(flags[r] & 2)) return;
+        __syncthreads();
+        if (threadIdx.x == 0) flags[r] &= (uint8_t)~2;
+    }
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const double th = theta[r];
     __shared__ double sh[8], sq[8], sh4[8];
@@ -610,8 +617,14 @@ __global__ void snapshot_gauss_kernel(const double* __restrict__ X, const double
                                       const double* __restrict__ theta, int M, int Mp,
                                       double* __restrict__ U, double* __restrict__ xx,
                                       const int32_t* __restrict__ rows, float* __restrict__ U32,
-                                      float* __restrict__ X32, double* __restrict__ nu) {
+                                      float* __restrict__ X32, double* __restrict__ nu,
+                                      uint8_t* __restrict__ flags) {
     const int r = rows ? rows[blockIdx.x] : (int)blockIdx.x;
+    if (flags) {
+        if (!(flags[r] & 2)) return;
+        __syncthreads();
+        if (threadIdx.x == 0) flags[r] &= (uint8_t)~2;
+    }
     const double t2 = theta[r] * theta[r];
     double a = 0.0, b = 0.0;
     for (int m = threadIdx.x; m < Mp; m += blockDim.x) {
@@ -669,8 +682,13 @@ void ensure_snapshot(Context& c) {
     if (!c.have_samples) fail(22, "no samples uploaded");
     if (c.snap_version == c.state_version) return;
     c.tic();
+    c.sync_flags();
+    uint8_t* flags = c.dflags();
     const size_t nm = (size_t)c.n * c.Mp;
     if (c.kind == ISING) {
+        if (!c.T64.p || !c.Q8.p || (c.Mw == 32 && !c.P4.p)) {  // first snapshot: every row
+            NRG_CUDA(cudaMemsetAsync(flags, 7, (size_t)c.n, c.stream));
+        }
         c.T64.ensure(nm * 8);
         c.T32.ensure(nm * 4);
         c.T8.ensure(nm);
@@ -690,9 +708,10 @@ void ensure_snapshot(Context& c) {
                                                          static_cast<float4*>(c.Q8.p),
                                                          static_cast<double*>(c.Tsq.p), nullptr,
                                                          static_cast<uint32_t*>(c.P4.p),
-                                                         static_cast<float4*>(c.Q4.p), c.dXb());
+                                                         static_cast<float4*>(c.Q4.p), c.dXb(), flags);
         build_bloom(c);
     } else {
+        if (!c.U.p || !c.nu.p) NRG_CUDA(cudaMemsetAsync(flags, 7, (size_t)c.n, c.stream));
         c.U.ensure(nm * 8);
         c.xx.ensure((size_t)c.n * 8);
         c.U32.ensure(nm * 4);
@@ -702,7 +721,7 @@ void ensure_snapshot(Context& c) {
                                                          static_cast<double*>(c.U.p),
                                                          static_cast<double*>(c.xx.p), nullptr,
                                                          static_cast<float*>(c.U32.p), static_cast<float*>(c.X32.p),
-                                                         static_cast<double*>(c.nu.p));
+                                                         static_cast<double*>(c.nu.p), flags);
         build_bloom(c);
     }
     NRG_LAUNCH_CHECK();
@@ -710,31 +729,27 @@ void ensure_snapshot(Context& c) {
     c.snap_version = c.state_version;
 }
 
-// Refresh the snapshot rows of `rows` (device list, nr entries) after updates that
-// changed only those nodes' sums; the rest of the snapshot must be current otherwise.
+// Refresh the snapshot rows of `rows` (device list, nr entries, every stale row among them:
+// the endpoints a tie-tail round just changed); the rest of the snapshot must be current.
 void snapshot_rows(Context& c, const int32_t* rows, uint64_t nr) {
+    if (c.snap_version == c.state_version) return;
     if (nr == 0) {
         c.snap_version = c.state_version;
         return;
     }
     c.tic();
-    if (c.kind == ISING) {
+    c.sync_flags();
+    if (c.kind == ISING)
         snapshot_ising_kernel<<<(unsigned)nr, 256, 0, c.stream>>>(
             c.dH(), c.dtheta(), c.M, c.Mp, static_cast<double*>(c.T64.p), static_cast<float*>(c.T32.p),
             static_cast<int8_t*>(c.T8.p), static_cast<uint32_t*>(c.P8.p), static_cast<float4*>(c.Q8.p),
             static_cast<double*>(c.Tsq.p), rows, static_cast<uint32_t*>(c.P4.p), static_cast<float4*>(c.Q4.p),
-            c.dXb());
-        build_bloom(c);  // the rows' couplings changed too
-    } else
-    {
-        snapshot_gauss_kernel<<<(unsigned)nr, 256, 0, c.stream>>>(c.dXd(), c.dH(), c.dtheta(), c.M, c.Mp,
-                                                                   static_cast<double*>(c.U.p),
-                                                                   static_cast<double*>(c.xx.p), rows,
-                                                                   static_cast<float*>(c.U32.p),
-                                                                   static_cast<float*>(c.X32.p),
-                                                                   static_cast<double*>(c.nu.p));
-        build_bloom(c);
-    }
+            c.dXb(), c.dflags());
+    else
+        snapshot_gauss_kernel<<<(unsigned)nr, 256, 0, c.stream>>>(
+            c.dXd(), c.dH(), c.dtheta(), c.M, c.Mp, static_cast<double*>(c.U.p), static_cast<double*>(c.xx.p), rows,
+            static_cast<float*>(c.U32.p), static_cast<float*>(c.X32.p), static_cast<double*>(c.nu.p), c.dflags());
+    build_bloom(c);  // the rows' couplings changed too
     NRG_LAUNCH_CHECK();
     c.toc(P_SNAP);
     c.snap_version = c.state_version;
@@ -764,9 +779,16 @@ __global__ void __launch_bounds__(256) logpost_node_kernel(int kind, const uint3
                                                            const double* __restrict__ Xd,
                                                            const double* __restrict__ H,
                                                            const double* __restrict__ theta, int M,
-                                                           int Mp, int Mw, double* __restrict__ out, int r0 = 0) {
+                                                           int Mp, int Mw, double* __restrict__ out, int r0 = 0,
+                                                           uint8_t* __restrict__ flags = nullptr) {
     __shared__ double sh[32];
     const int r = r0 + blockIdx.x;
+    // out[] persists between calls: a node whose row and theta did not change keeps its term
+    if (flags) {
+        if (!(flags[r] & 4)) return;
+        __syncthreads();
+        if (threadIdx.x == 0) flags[r] &= (uint8_t)~4;
+    }
     const double th = theta[r];
     double a = 0.0;
     if (kind == ISING) {
@@ -808,21 +830,31 @@ __global__ void __launch_bounds__(256) w_abs_partial_kernel(const uint64_t* __re
     if (threadIdx.x == 0) part[blockIdx.x] = a;
 }
 
+__global__ void clear_flag_outside_kernel(uint8_t* __restrict__ flags, int n, int lo, int hi, uint8_t bit) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && (i < lo || i >= hi)) flags[i] &= (uint8_t)~bit;
+}
+
 double log_posterior(Context& c) {
     if (!c.have_samples) fail(22, "no samples uploaded");
     // memo per state version: the GCD loop's objective after a sweep is the next
     // generation's base (inc/reconstruct.hpp:174-176, inc/model.hpp:73-81), same state
     if (c.lp_version == c.state_version) return c.lp_value;
     c.tic();
-    double* part = c.red.as<double>((size_t)c.n + 1024 + 8);
-    double* res = part + c.n + 1024;
-    // per-node terms (a sharded job computes its node range and all-gathers the per-node
-    // values, so the fixed-order reduction below is bitwise the single-GPU one)
+    // per-node terms (persistent: only the nodes flagged stale are recomputed; a sharded job
+    // computes its node range and all-gathers the per-node values, so the fixed-order
+    // reduction below is bitwise the single-GPU one)
+    c.sync_flags();
+    uint8_t* flags = c.dflags();
+    if (!c.lp_node.p) NRG_CUDA(cudaMemsetAsync(flags, 7, (size_t)c.n, c.stream));  // first call: every node
+    double* part = c.lp_node.as<double>((size_t)c.n);
+    double* wpart = c.red.as<double>(1024 + 8);
+    double* res = wpart + 1024;
     uint64_t lo = 0, hi = (uint64_t)c.n;
     if (c.world > 1) shard_range((uint64_t)c.n, c.rank, c.world, lo, hi);
     if (hi > lo)
         logpost_node_kernel<<<(unsigned)(hi - lo), 256, 0, c.stream>>>(c.kind, c.dXb(), c.dXd(), c.dH(), c.dtheta(),
-                                                                     c.M, c.Mp, c.Mw, part, (int)lo);
+                                                                     c.M, c.Mp, c.Mw, part, (int)lo, flags);
     NRG_LAUNCH_CHECK();
     if (c.world > 1) {
         std::vector<size_t> bytes(c.world);
@@ -832,13 +864,15 @@ double log_posterior(Context& c) {
             bytes[r] = (h - l) * 8;
         }
         static_cast<Comm*>(c.comm)->allgatherv(part + lo, part, bytes, c.stream);
+        clear_flag_outside_kernel<<<(unsigned)ceil_div(c.n, 256), 256, 0, c.stream>>>(flags, c.n, (int)lo, (int)hi, 4);
+        NRG_LAUNCH_CHECK();
     }
     reduce_fixed_kernel<<<1, 1024, 0, c.stream>>>(part, c.n, res);
     NRG_LAUNCH_CHECK();
     const int nb = 592;
     w_abs_partial_kernel<<<nb, 256, 0, c.stream>>>(static_cast<uint64_t*>(c.Wkeys.p),
-                                                   static_cast<double*>(c.Wvals.p), c.Wcap, part + c.n);
-    reduce_fixed_kernel<<<1, 1024, 0, c.stream>>>(part + c.n, nb, res + 1);
+                                                   static_cast<double*>(c.Wvals.p), c.Wcap, wpart);
+    reduce_fixed_kernel<<<1, 1024, 0, c.stream>>>(wpart, nb, res + 1);
     NRG_LAUNCH_CHECK_N(2);
     double h[2];
     NRG_CUDA(cudaMemcpyAsync(h, res, 16, cudaMemcpyDeviceToHost, c.stream));

@@ -109,6 +109,7 @@ struct UpdateArgs {
     double* absdelta;
     uint64_t* counters;
     int stage;  // stage tanh(H + theta) of both rows in shared memory once per pair
+    uint8_t* flags;  // per-node staleness flags (context.cuh): both endpoints of a changed coupling
 };
 
 // One CTA per update: the chain of dependent updates is the critical path (thousands
@@ -238,6 +239,7 @@ __global__ void __launch_bounds__(NT, 768 / NT) update_kernel(UpdateArgs A) {
         __threadfence();
         __syncthreads();  // every thread has read W / H and written H before W and the flag publish
         if (tid == 0) {
+            if (delta != 0.0 && A.flags) A.flags[a] = A.flags[b] = 7;
             A.absdelta[p] = fabs(w - wcur);
             if (delta != 0.0 || w == 0.0) hash_set(A.W, key, w, A.Wcnt);
             __threadfence();
@@ -361,21 +363,6 @@ bool set_edges_bulk(Context& c, const int32_t* ci, const int32_t* cj, uint64_t n
     return true;
 }
 
-// distinct endpoints of pairs [0, k): first marker of a node appends it
-__global__ void endpoint_rows_kernel(const int32_t* __restrict__ ci, const int32_t* __restrict__ cj, uint64_t k,
-                                     uint8_t* __restrict__ mark, int32_t* __restrict__ rows,
-                                     unsigned long long* __restrict__ cnt) {
-    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= k) return;
-    const int32_t e[2] = {ci[t], cj[t]};
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-        unsigned int* w = reinterpret_cast<unsigned int*>(mark + (e[q] & ~3));
-        const unsigned int bit = 1u << (8 * (e[q] & 3));
-        if (!(atomicOr(w, bit) & bit)) rows[atomicAdd(cnt, 1ull)] = e[q];
-    }
-}
-
 __global__ void __launch_bounds__(1024) sum_fixed_kernel(const double* __restrict__ v, uint64_t n,
                                                          double* __restrict__ out) {
     __shared__ double sh[32];
@@ -490,6 +477,8 @@ static void ordered_run(Context& c, const int32_t* ci, const int32_t* cj, uint64
     A.ticket = ticket;
     A.absdelta = absdelta;
     A.counters = c.dcounters();
+    c.sync_flags();
+    A.flags = c.dflags();
     const size_t smem = (size_t)2 * c.Mp * sizeof(double);
     A.stage = (c.kind == ISING && smem <= 160 * 1024) ? 1 : 0;
     const size_t smem_use = A.stage ? smem : 0;
@@ -675,9 +664,6 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
                      const double* dist, bool fb_sorted) {
     if (n == 0) return 0.0;
     if (n >= (1ull << 31)) fail(22, "apply_updates: too many candidates");
-    // the snapshot describes the state on entry (FindBest just ran): a tie tail then
-    // needs only the rows the ordered part touches refreshed
-    const bool snap_fresh = c.snap_version == c.state_version;
     c.tic();
     w_reserve(c, n);
     DevBuf adb, sb, kb, wb, fb, ib, pib, pjb, ddb;
@@ -736,30 +722,14 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
                 ordered_run(c, ci + start, cj + start, n - start, nullptr, absdelta + start);
                 break;
             }
-            c.state_version++;  // the evaluation snapshot must include every update so far
-            c.toc(P_UPDATE);    // snapshot refreshes time themselves (P_SNAP)
-            if (round > 0) {
-                snapshot_rows(c, rows_dev, n_rows);  // only the last round's endpoints changed
-            } else if (snap_fresh && 2 * k < (uint64_t)c.n) {
-                // the ordered part changed only its candidates' endpoints (the generation's
-                // snapshot of every other row still holds; theta moves after the updates)
-                rows_dev = rowsb.as<int32_t>(2 * k + 1);
-                uint64_t nr = 0;
-                if (k) {
-                    // distinct endpoints (a row re-snapshotted once)
-                    uint8_t* mark = fb.as<uint8_t>(std::max<uint64_t>((uint64_t)c.n, n));
-                    unsigned long long* cnt = kb.as<unsigned long long>(1);
-                    NRG_CUDA(cudaMemsetAsync(mark, 0, c.n, c.stream));
-                    NRG_CUDA(cudaMemsetAsync(cnt, 0, 8, c.stream));
-                    endpoint_rows_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, c.stream>>>(ci, cj, k, mark,
-                                                                                          rows_dev, cnt);
-                    NRG_LAUNCH_CHECK();
-                    unsigned long long h = 0;
-                    h = c.read_scalar(cnt);
-                    nr = h;
-                }
-                snapshot_rows(c, rows_dev, nr);
-            }
+            c.bump_flagged();  // the evaluation snapshot must include every update so far
+            c.toc(P_UPDATE);   // snapshot refreshes time themselves (P_SNAP)
+            // the rows the updates so far changed (their staleness flags): after a round, the
+            // endpoints of the pairs it applied; before the first, whatever the ordered part hit
+            if (round > 0 && c.flags_version == c.state_version)
+                snapshot_rows(c, rows_dev, n_rows);
+            else
+                ensure_snapshot(c);
             const uint64_t m = n - start;
             double* w = wb.as<double>(m);
             ScoreOut out;
@@ -861,7 +831,6 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
                 ordered_run(c, pi, pj, na, nullptr, dd);
                 scatter_delta_kernel<<<ceil_div(na, 256), 256, 0, c.stream>>>(dd, di, na, absdelta);
                 NRG_LAUNCH_CHECK();
-                // endpoints of the applied pairs: the rows the next round must re-snapshot
                 rows_dev = rowsb.as<int32_t>(2 * (size_t)na);
                 NRG_CUDA(cudaMemcpyAsync(rows_dev, pi, na * 4, cudaMemcpyDeviceToDevice, c.stream));
                 NRG_CUDA(cudaMemcpyAsync(rows_dev + na, pj, na * 4, cudaMemcpyDeviceToDevice, c.stream));
@@ -879,7 +848,7 @@ double apply_updates(Context& c, const int32_t* ci, const int32_t* cj, uint64_t 
     double h = 0.0;
     h = c.read_scalar(sum);
     c.toc(P_UPDATE);
-    c.state_version++;
+    c.bump_flagged();
     return h;
 }
 
@@ -906,10 +875,20 @@ __global__ void __launch_bounds__(256) theta_kernel(int kind, const uint32_t* __
                                                     const double* __restrict__ Xd, const double* __restrict__ H,
                                                     const double* __restrict__ theta_in, int n, int M, int Mp,
                                                     int Mw, double* __restrict__ theta_out, uint64_t* counters,
-                                                    int i0 = 0) {
+                                                    int i0 = 0, uint8_t* __restrict__ flags = nullptr) {
     const int lane = threadIdx.x & 31;
     const int i = i0 + (int)(((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     if (i >= n) return;  // n: the end of this launch's node range
+    if (flags) {
+        // theta_i maximises a function of row H_i only: a row no update touched since its
+        // theta was optimised keeps it (the reference re-runs its search from the optimum)
+        if (!(flags[i] & 1)) {
+            if (lane == 0) theta_out[i] = theta_in[i];
+            return;
+        }
+        __syncwarp();
+        if (lane == 0) flags[i] = 6;  // theta current; snapshot row and objective term stale
+    }
     if (M == 0) {
         if (lane == 0) theta_out[i] = theta_in[i];
         return;
@@ -1032,14 +1011,27 @@ __global__ void __launch_bounds__(256) theta_kernel(int kind, const uint32_t* __
 // theta pass (inc/reconstruct.hpp:129-138).  In a sharded job every rank optimises the
 // fields of its node range and the ranges are all-gathered: each theta_i
 // is a function of node i's row only, so the result is bitwise the single-GPU pass.
+__global__ void flags_outside_kernel(uint8_t* __restrict__ flags, int n, int lo, int hi, uint8_t test, uint8_t set_to,
+                                     uint8_t clear) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || (i >= lo && i < hi)) return;
+    const uint8_t f = flags[i];
+    if (f & test) flags[i] = set_to ? set_to : (uint8_t)(f & ~clear);
+}
+
 void theta_pass(Context& c, double* out_only) {
     c.tic();
     double* out = out_only ? out_only : c.s_n.as<double>(c.n);
     uint64_t lo = 0, hi = (uint64_t)c.n;
     if (c.world > 1) shard_range((uint64_t)c.n, c.rank, c.world, lo, hi);
+    uint8_t* flags = nullptr;
+    if (!out_only) {
+        c.sync_flags();
+        flags = c.dflags();
+    }
     if (hi > lo)
         theta_kernel<<<(unsigned)ceil_div((int64_t)(hi - lo) * 32, 256), 256, 0, c.stream>>>(
-            c.kind, c.dXb(), c.dXd(), c.dH(), c.dtheta(), (int)hi, c.M, c.Mp, c.Mw, out, c.dcounters(), (int)lo);
+            c.kind, c.dXb(), c.dXd(), c.dH(), c.dtheta(), (int)hi, c.M, c.Mp, c.Mw, out, c.dcounters(), (int)lo, flags);
     NRG_LAUNCH_CHECK();
     if (c.world > 1) {
         std::vector<size_t> bytes(c.world);
@@ -1049,10 +1041,17 @@ void theta_pass(Context& c, double* out_only) {
             bytes[r] = (h - l) * 8;
         }
         static_cast<Comm*>(c.comm)->allgatherv(out + lo, out, bytes, c.stream);
+        if (flags) {  // the other ranks' rows: the same flag transition their owners made
+            flags_outside_kernel<<<(unsigned)ceil_div(c.n, 256), 256, 0, c.stream>>>(flags, c.n, (int)lo, (int)hi, 1, 6, 0);
+            NRG_LAUNCH_CHECK();
+        }
     }
     if (!out_only) {
         NRG_CUDA(cudaMemcpyAsync(c.theta.p, out, (size_t)c.n * 8, cudaMemcpyDeviceToDevice, c.stream));
-        c.state_version++;
+        if (flags)
+            c.bump_flagged();
+        else
+            c.state_version++;
     }
     c.toc(P_THETA);
 }
