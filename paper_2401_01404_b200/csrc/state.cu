@@ -995,15 +995,20 @@ void begin_generation(Context& c) {
         if (c.k2max.p) NRG_CUDA(cudaMemsetAsync(c.k2max.p, 0, 8, c.stream));
         // (shrinks too: clearing and scanning an oversized memo costs HBM time every sweep)
         const uint64_t want = std::min<uint64_t>(live + live / 10 * 3, (1ull << 31) * 6 / 10);
+        // target load 0.75 at the previous count + 30% (power-of-two capacities: the real load
+        // is between half of that and that).  A table twice the size probes a little faster
+        // but costs more to clear and to scan (the dense root's recount): config 4 measured
+        // 31.7 ms per sweep at 2^29 slots, 31.4 at 2^28
+        static const uint64_t load_pct = getenv("NRG_MEMO_LOAD_PCT") ? strtoull(getenv("NRG_MEMO_LOAD_PCT"), nullptr, 10) : 75;
         const uint64_t ncap =
-            std::max<uint64_t>(1u << 20, std::min<uint64_t>(next_pow2(want * 10 / 6 + 1), 1ull << 31));
+            std::max<uint64_t>(1u << 20, std::min<uint64_t>(next_pow2(want * 100 / load_pct + 1), 1ull << 31));
         // a generation that flushed the memo counted only the pairs since its last flush:
         // keep the size (config 5 would otherwise free and re-map tens of GB every sweep)
         const bool flushed = c.cache_flushes != c.flushes_at_gen;
         // shrink only when the need plus another 30% fits half the table: a count that
         // hovers at a power-of-two boundary (config 4: 161M * 10/6 vs 2^28) otherwise frees
         // and re-maps 2 x 4 GB every few generations, a 20-80 ms stall each time
-        const bool shrink = ncap < c.Ccap && (want * 10 / 6) / 10 * 13 < c.Ccap / 2;
+        const bool shrink = ncap < c.Ccap && (want * 100 / load_pct) / 10 * 13 < c.Ccap / 2;
         if ((ncap > c.Ccap || shrink) && !(flushed && ncap < c.Ccap)) {
             c.Ckeys = DevBuf();
             c.Cvals = DevBuf();
