@@ -21,6 +21,9 @@
 
 #include "pairscore.cuh"
 
+#ifndef NRG_K2_MINB
+#define NRG_K2_MINB 6  // CTAs per SM of the CTA-per-survivor K2 (85 registers, no spills; 4 at 128 registers)
+#endif
 #ifndef NRG_K1S_MINB
 #define NRG_K1S_MINB 3
 #endif
@@ -643,7 +646,7 @@ __global__ void __launch_bounds__(128) ising_refine_kernel(IsingSnap S, HashView
 // block reduction instead of M / 128 dependent warp steps; a launch holds a few thousand
 // survivors at most, so per-survivor latency, not throughput, bounds K2.
 template <int NT, int KU>
-__global__ void __launch_bounds__(NT) ising_refine_cta_kernel(IsingSnap S, HashView W, const int32_t* __restrict__ es,
+__global__ void __launch_bounds__(NT, NRG_K2_MINB) ising_refine_cta_kernel(IsingSnap S, HashView W, const int32_t* __restrict__ es,
                                                                const int32_t* __restrict__ ep,
                                                                const uint64_t* __restrict__ surv,
                                                                const float* __restrict__ surv_g,
