@@ -89,6 +89,11 @@ inline bool block_cache_on() {
     static const bool v = getenv("NRG_NO_BLOCK_CACHE") == nullptr;
     return v;
 }
+// Only small blocks are kept: a multi-GB buffer (the distance memo, config 5's candidate
+// arrays) goes straight back to the pool, where any later request can use its memory --
+// hoarded by exact size class it ran config 5 out of memory and left freed 2-4 GB memo
+// blocks idle while new ones were mapped.
+constexpr size_t kBlockCacheMax = (size_t)32 << 20;
 
 // grow-only device buffer (RAII, move-only, stream-ordered)
 struct DevBuf {
@@ -129,10 +134,19 @@ struct DevBuf {
             s = tl_stream;
             static const bool dbg = getenv("NRG_DEBUG_ALLOC") != nullptr;
             const auto t0 = dbg ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point();
-            if (sync_alloc())
+            if (sync_alloc()) {
                 NRG_CUDA(cudaMalloc(&p, nb));
-            else if (!(block_cache_on() && s && (p = BlockCache::get().take(s, nb))))
-                NRG_CUDA(cudaMallocAsync(&p, nb, s));
+            } else if (!(block_cache_on() && s && nb <= kBlockCacheMax && (p = BlockCache::get().take(s, nb)))) {
+                cudaError_t e = cudaMallocAsync(&p, nb, s);
+                if (e == cudaErrorMemoryAllocation) {
+                    // return every cached block to the pool, let queued frees land, retry once
+                    cudaGetLastError();
+                    BlockCache::get().drop(s);
+                    cudaStreamSynchronize(s);
+                    e = cudaMallocAsync(&p, nb, s);
+                }
+                NRG_CUDA(e);
+            }
             if (dbg) {
                 const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
                 if (ms > 1.0) fprintf(stderr, "alloc %.3f GB took %.1f ms\n", nb / 1e9, ms);
@@ -149,7 +163,7 @@ struct DevBuf {
         if (p) {
             if (sync_alloc())
                 cudaFree(p);
-            else if (block_cache_on() && s)
+            else if (block_cache_on() && s && bytes <= kBlockCacheMax)
                 BlockCache::get().put(s, bytes, p);
             else
                 cudaFreeAsync(p, s);
