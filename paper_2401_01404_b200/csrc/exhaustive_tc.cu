@@ -272,6 +272,203 @@ __global__ void __launch_bounds__(kTcThreads, 2)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols) : "memory");
 }
 
+// Persistent form of tc_screen_kernel: one CTA per SM walks the tile list.  Warp 0 feeds
+// TMA through a 4-stage ring that runs ahead across tile boundaries, warp 1 issues the MMAs
+// into one of TWO accumulator sets (2 x 192 of the 512 TMEM columns), warps 2-9 drain the
+// other set: a tile's epilogue, the TMEM allocation, the barrier setup and the first TMA
+// round trip no longer sit between two tiles' MMAs (the one-tile-per-CTA kernel kept the
+// tensor pipe 51% busy with two CTAs per SM covering for each other).  Same arithmetic,
+// same survivors (their order in the list differs; nothing reads it).
+constexpr int kStagesP = 4;
+constexpr int kTcThreadsP = 320;
+constexpr int kAccCols = 3 * kBN;  // columns of one accumulator set
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// linear tile index -> (I, J): row block I pairs with the 64-column blocks J >= 2 I; row I
+// starts at tile I TB - I (I - 1)
+__device__ __forceinline__ void tile_ij(int t, int TB, int& I, int& J) {
+    const float b = (float)(TB + 1);
+    int i = (int)((b - sqrtf(fmaxf(b * b - 4.f * (float)t, 0.f))) * 0.5f);
+    i = max(i, 0);
+    while (i > 0 && i * TB - i * (i - 1) > t) --i;
+    while ((i + 1) * TB - (i + 1) * i <= t) ++i;
+    I = i;
+    J = 2 * i + (t - (i * TB - i * (i - 1)));
+}
+__global__ void __launch_bounds__(kTcThreadsP, 1)
+    tc_screen_persistent_kernel(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mt,
+                                const __grid_constant__ CUtensorMap mxb, const __grid_constant__ CUtensorMap mtb,
+                                const float4* __restrict__ q, int n, int M, int Mp, double lambda, int tiles,
+                                TcOut out) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* ring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                                           ~(uintptr_t)1023);
+    __shared__ __align__(8) uint64_t full[kStagesP], empty[kStagesP], acc_full[2], acc_empty[2];
+    __shared__ uint32_t tmem_base;
+    __shared__ float2 qcol[2][kBN];  // {d_j, E_j} of the column block, per accumulator set
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int TB = (n + kBN - 1) / kBN;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStagesP; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 8);  // one arrival per epilogue warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                     "n"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tmem_base;
+    const int nkb = Mp / kBK;
+    if (warp == 0) {
+        if (lane == 0) {
+            uint32_t g = 0;
+            for (int t = (int)blockIdx.x; t < tiles; t += (int)gridDim.x) {
+                int I, J;
+                tile_ij(t, TB, I, J);
+                for (int kb = 0; kb < nkb; ++kb, ++g) {
+                    const int s = (int)(g % kStagesP);
+                    const uint32_t ph = (g / kStagesP) & 1u;
+                    mbar_wait(&empty[s], ph ^ 1u);
+                    unsigned char* st = ring + s * kStageBytes;
+                    mbar_expect_tx(&full[s], kStageBytes);
+                    tma_load_2d(st + 0 * kTileBytes, &mx, kb * kBK, I * kBM, &full[s]);
+                    tma_load_2d(st + 1 * kTileBytes, &mt, kb * kBK, I * kBM, &full[s]);
+                    tma_load_2d(st + 2 * kTileBytes, &mxb, kb * kBK, J * kBN, &full[s]);
+                    tma_load_2d(st + 2 * kTileBytes + kTileBytesB, &mtb, kb * kBK, J * kBN, &full[s]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            uint32_t g = 0, it = 0;
+            for (int t = (int)blockIdx.x; t < tiles; t += (int)gridDim.x, ++it) {
+                const uint32_t b = it & 1u, aph = (it >> 1) & 1u;
+                mbar_wait(&acc_empty[b], aph ^ 1u);  // the epilogue has drained this set
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t acc0 = tmem + b * kAccCols;
+                for (int kb = 0; kb < nkb; ++kb, ++g) {
+                    const int s = (int)(g % kStagesP);
+                    const uint32_t ph = (g / kStagesP) & 1u;
+                    mbar_wait(&full[s], ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const unsigned char* st = ring + s * kStageBytes;
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 32; ++kk) {
+                        const uint32_t acc = (kb | kk) ? 1u : 0u;
+                        const uint64_t xi = smem_desc(st + 0 * kTileBytes, 32 * kk);
+                        const uint64_t ti = smem_desc(st + 1 * kTileBytes, 32 * kk);
+                        const uint64_t xj = smem_desc(st + 2 * kTileBytes, 32 * kk);
+                        const uint64_t tj = smem_desc(st + 2 * kTileBytes + kTileBytesB, 32 * kk);
+                        mma_i8(acc0 + 0, xi, xj, acc);
+                        mma_i8(acc0 + kBN, xi, tj, acc);
+                        mma_i8(acc0 + 2 * kBN, ti, xj, acc);
+                    }
+                    mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+                }
+                mma_commit(&acc_full[b]);  // the tile's accumulators are complete
+            }
+        }
+    } else {
+        // epilogue warps 2..9: thread = one row of the tile, half of its columns
+        const int ew = warp - 2;                 // 0..7
+        const int quad = warp & 3;               // the TMEM lane quadrant this warp may read
+        const int et = threadIdx.x - 64;         // 0..255 within the epilogue group
+        const int r = quad * 32 + lane;
+        const int cbeg = (ew >> 2) * (kBN / 2), cend = cbeg + kBN / 2;
+        const float lam = (float)lambda;
+        const float err0 = 4.f * (float)M * 5.9604645e-08f;
+        uint32_t it = 0;
+        for (int t = (int)blockIdx.x; t < tiles; t += (int)gridDim.x, ++it) {
+            const uint32_t b = it & 1u, aph = (it >> 1) & 1u;
+            int I, J;
+            tile_ij(t, TB, I, J);
+            if (et < kBN) {
+                const int j = J * kBN + et;
+                const float4 v = j < n ? __ldg(&q[j]) : make_float4(0.f, 0.f, 0.f, 0.f);
+                qcol[b][et] = make_float2(v.x, v.y);
+            }
+            asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 epilogue warps
+            const int i = I * kBM + r;
+            const float4 qi = i < n ? __ldg(&q[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
+            mbar_wait(&acc_full[b], aph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t acc0 = tmem + b * kAccCols + ((uint32_t)(quad * 32) << 16);
+            for (int c0 = cbeg; c0 < cend; c0 += 16) {
+                uint32_t a1[16], a2[16], a3[16];
+                tmem_ld16(acc0 + 0 * kBN + c0, a1);
+                tmem_ld16(acc0 + 1 * kBN + c0, a2);
+                tmem_ld16(acc0 + 2 * kBN + c0, a3);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (c0 + 16 >= cend) {
+                    // last chunk read: hand the accumulator set back before the compaction
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&acc_empty[b]);
+                }
+                uint32_t surv_mask = 0;
+                float gv[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    const int j = J * kBN + c0 + u;
+                    gv[u] = 0.f;
+                    if (i < n && j < n && i < j) {
+                        const float2 qj = qcol[b][c0 + u];
+                        const float g = (float)(2 * (int)a1[u]) - (qj.x * (float)(int)a2[u] + qi.x * (float)(int)a3[u]);
+                        const float err = (qi.y + qj.y) * 1.0001f + err0;
+                        if (fabsf(g) > lam - err) {
+                            surv_mask |= 1u << u;
+                            gv[u] = g;
+                        }
+                    }
+                }
+                const int cnt = __popc(surv_mask);
+                int incl = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int tt = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += tt;
+                }
+                const int tot = __shfl_sync(0xffffffffu, incl, 31);
+                unsigned long long at = 0;
+                if (lane == 31 && tot) at = atomicAdd(out.ns, (unsigned long long)tot);
+                at = __shfl_sync(0xffffffffu, at, 31) + (unsigned long long)(incl - cnt);
+#pragma unroll
+                for (int u = 0; u < 16; ++u) {
+                    if ((surv_mask >> u) & 1u) {
+                        if (at < out.cap) {
+                            const float g = gv[u];
+                            out.si[at] = i;
+                            out.sj[at] = J * kBN + c0 + u;
+                            out.sg[at] = g;
+                            const float2 qj = qcol[b][c0 + u];
+                            const float err = (qi.y + qj.y) * 1.0001f + err0;
+                            out.sf[at] = fabsf(g) < lam + err ? 1 : 0;
+                        }
+                        ++at;
+                    }
+                }
+            }
+        }
+    }
+    __syncwarp();  // the producer's and the issuer's idle lanes wait for lane 0 here
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512) : "memory");
+}
+
 __global__ void tc_fill_kernel(double* __restrict__ dist, uint64_t n, double v) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) dist[t] = v;
@@ -541,8 +738,20 @@ bool score_all_pairs_tc(Context& c, const int32_t* nodes, uint64_t n, double* di
         NRG_CUDA(cudaFuncSetAttribute(tc_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    tc_screen_kernel<<<(unsigned)tiles, kTcThreads, smem, c.stream>>>(mx, mt, mxb, mtb, q, (int)n, c.M, Mp,
-                                                                   c.lambda, base, out);
+    if (NRG_ENV_ON("NRG_TC_ONE_TILE")) {
+        tc_screen_kernel<<<(unsigned)tiles, kTcThreads, smem, c.stream>>>(mx, mt, mxb, mtb, q, (int)n, c.M, Mp,
+                                                                       c.lambda, base, out);
+    } else {
+        const size_t smem_p = (size_t)kStagesP * kStageBytes + 1024;
+        static int sms = 0;
+        if (!sms) {
+            NRG_CUDA(cudaFuncSetAttribute(tc_screen_persistent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem_p));
+            NRG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+        }
+        tc_screen_persistent_kernel<<<(unsigned)std::min(tiles, sms), kTcThreadsP, smem_p, c.stream>>>(
+            mx, mt, mxb, mtb, q, (int)n, c.M, Mp, c.lambda, tiles, out);
+    }
     NRG_LAUNCH_CHECK();
     unsigned long long ns = 0;
     ns = c.read_scalar(out.ns);
