@@ -781,7 +781,8 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
                                                              uint32_t* __restrict__ cand_slot,
                                                              int32_t* __restrict__ cand_cnt, uint64_t lo, bool do_claim,
                                                              const int32_t* __restrict__ rootpos,
-                                                             const uint8_t* __restrict__ hasnew) {
+                                                             const uint8_t* __restrict__ hasnew,
+                                                             bool count_only = false) {
     extern __shared__ uint32_t bits_smem[];
     uint32_t* acc = bits_smem;     // OR of the 2-hop rows
     uint32_t* excl = acc + W;      // i's current row and i itself
@@ -862,6 +863,10 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
     }
     int off = 0, total = 0;
     Scan(scan_tmp).ExclusiveSum(cnt, off, total);
+    if (count_only) {  // the size of the candidate set only (the coverage test of a dense level)
+        if (tid == 0) cand_cnt[li] = total;
+        return;
+    }
     int32_t* my_ids = cand_id + li * capn;
     if (rootpos) {
         // dense level: slots in the root's distance triangle, probes marked and counted here
@@ -1343,6 +1348,154 @@ __global__ void coverage_kernel(const int32_t* __restrict__ cand_cnt, uint64_t o
     if ((threadIdx.x & 31) == 0 && b) atomicAdd(short_nodes, (unsigned long long)__popc(b));
 }
 
+// ---------------------------------------------------------------- covered dense levels
+// A dense FindBest level (distances from the level's exhaustive triangle) whose FIRST sweep
+// gives every node the whole level as candidates (deep levels: cap^2 >= n) ends with each row
+// the exact top-kw of the level, the next sweep settled (churn 0), every pair of the level
+// probed once from each side, and every survivor among the level's pairs refined.  All of
+// that follows from the coverage alone, so when the candidate-set SIZES (the OR of the
+// U-row bitsets, no candidate lists) show full coverage the level is finished directly:
+// probe marks by rows of the triangle, the survivors' refinement from the screen's
+// worklist, and the rows from each node's few survivors plus the smallest ids (every other
+// pair ties at -base).  Same rows, sweeps, churn, marks, hit and eval counts as the sweeps
+// (tests/test_gpu_search.py::test_dense_levels_equal_claim_path).
+__global__ void cover_members_kernel(const int32_t* __restrict__ rootpos, uint64_t n, uint32_t* __restrict__ M) {
+    const uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (a < n) atomicOr(&M[rootpos[a] >> 5], 1u << (rootpos[a] & 31));
+}
+// row ra of the root's triangle holds the pairs (ra, rb > ra) at consecutive slots: the
+// level's members among them are the member mask shifted into place, one RED per word
+__global__ void cover_mark_kernel(const int32_t* __restrict__ rootpos, uint64_t n, uint64_t dn,
+                                  const uint32_t* __restrict__ M, uint32_t* __restrict__ dbits) {
+    const uint64_t a = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (a >= n) return;
+    const uint64_t ra = (uint64_t)rootpos[a];
+    if (ra + 1 >= dn) return;
+    const uint64_t tbase = ra * (2 * dn - ra - 1) / 2, len = dn - ra - 1;
+    const uint64_t W0 = tbase >> 5, W1 = (tbase + len - 1) >> 5;
+    for (uint64_t W = W0 + lane; W <= W1; W += 32) {
+        const long long s = (long long)(32 * W) - (long long)tbase + (long long)ra + 1;  // member index of bit 0
+        uint32_t val;
+        if (s < 0) {
+            val = s > -32 ? M[0] << (unsigned)(-s) : 0u;
+        } else {
+            const uint64_t idx = (uint64_t)s >> 5;
+            const unsigned sh = (unsigned)s & 31u;
+            val = M[idx] >> sh;
+            if (sh) val |= M[idx + 1] << (32u - sh);
+        }
+        const long long cut = (long long)ra + 1 - s;  // bits below: positions <= ra
+        if (cut > 0) val &= cut >= 32 ? 0u : (~0u << (unsigned)cut);
+        if (val) atomicOr(&dbits[W], val);
+    }
+}
+// the screen's worklist entries with both endpoints in the level: claim the pair for the
+// lazy K2, and count / fill the two endpoints' survivor lists (a pair listed twice -- a
+// survivor that is also an existing coupling -- is taken once: `seen` over triangle slots)
+__global__ void cover_worklist_kernel(DenseResolve R, const int32_t* __restrict__ es, const int32_t* __restrict__ ep,
+                                      const uint32_t* __restrict__ wrank, uint64_t nw,
+                                      const int32_t* __restrict__ loc, const int32_t* __restrict__ dloc, uint64_t dn,
+                                      uint32_t* __restrict__ seen, uint8_t* __restrict__ keep,
+                                      unsigned long long* __restrict__ deg, const unsigned long long* __restrict__ off,
+                                      int32_t* __restrict__ adj_id, uint32_t* __restrict__ adj_rank, int pass) {
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nw) return;
+    const int32_t u = es[e], v = ep[e];
+    const int32_t a = loc[u], b = loc[v];
+    if (pass == 0) {
+        keep[e] = 0;
+        if (a < 0 || b < 0) return;
+        const uint64_t ra = (uint64_t)dloc[u], rb = (uint64_t)dloc[v];
+        const uint64_t t = ra < rb ? tri_index(ra, rb, dn) : tri_index(rb, ra, dn);
+        const uint32_t bit = 1u << (t & 31);
+        if (atomicOr(&seen[t >> 5], bit) & bit) return;
+        keep[e] = 1;
+        dense_resolve_slot(R, (uint32_t)t);
+        atomicAdd(&deg[a], 1ull);
+        atomicAdd(&deg[b], 1ull);
+    } else if (keep[e]) {
+        unsigned long long at = off[a] + atomicAdd(&deg[a], 1ull);
+        adj_id[at] = b;
+        adj_rank[at] = wrank[e];
+        at = off[b] + atomicAdd(&deg[b], 1ull);
+        adj_id[at] = a;
+        adj_rank[at] = wrank[e];
+    }
+}
+// one CTA per node: the survivors that beat the tie value, by (dist, global id), then the
+// smallest ids (local order = global order: the level's node list is ascending); churn =
+// entries that were not in the sweep-start (initial) row
+__global__ void __launch_bounds__(128) cover_rows_kernel(const int32_t* __restrict__ nodes, uint64_t n, int kw,
+                                                         const unsigned long long* __restrict__ off,
+                                                         const int32_t* __restrict__ adj_id,
+                                                         const uint32_t* __restrict__ adj_rank,
+                                                         const double* __restrict__ vals, double pruned,
+                                                         int32_t* __restrict__ gid, double* __restrict__ gd,
+                                                         unsigned long long* __restrict__ churn) {
+    extern __shared__ unsigned char cover_smem[];
+    double* od = reinterpret_cast<double*>(cover_smem);
+    int32_t* oi = reinterpret_cast<int32_t*>(od + kw);
+    int32_t* init = oi + kw;
+    int32_t* flag = init + kw;  // kw + 1 entries
+    __shared__ int s_nb, s_ch;
+    const uint64_t i = blockIdx.x;
+    const int tid = threadIdx.x;
+    const unsigned long long a0 = off[i];
+    const int s = (int)(off[i + 1] - a0);
+    for (int t = tid; t < kw; t += 128) init[t] = gid[i * kw + t];
+    if (tid == 0) s_nb = s_ch = 0;
+    __syncthreads();
+    int mine = 0;
+    for (int t = tid; t < s; t += 128) {
+        const double d = vals[adj_rank[a0 + t]];
+        if (!(d < pruned)) continue;
+        ++mine;
+        const int32_t v = adj_id[a0 + t];
+        const int g = nodes[v];
+        int r = 0;
+        for (int u = 0; u < s; ++u) {
+            const double du = vals[adj_rank[a0 + u]];
+            if (du < pruned) r += entry_less(du, nodes[adj_id[a0 + u]], d, g) ? 1 : 0;
+        }
+        if (r < kw) {
+            od[r] = d;
+            oi[r] = v;
+        }
+    }
+    if (mine) atomicAdd(&s_nb, mine);
+    __syncthreads();
+    const int sp = min(s_nb, kw);
+    // the first kw + 1 ids hold at least kw - sp nodes outside {i} and the sp chosen
+    for (int v = tid; v <= kw; v += 128) {
+        bool ok = (uint64_t)v != i && (uint64_t)v < n;
+        for (int u = 0; ok && u < sp; ++u) ok = oi[u] != v;
+        flag[v] = ok ? 1 : 0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int pos = sp;
+        for (int v = 0; v <= kw && pos < kw; ++v)
+            if (flag[v]) {
+                od[pos] = pruned;
+                oi[pos++] = v;
+            }
+    }
+    __syncthreads();
+    int ch = 0;
+    for (int t = tid; t < kw; t += 128) {
+        const int32_t v = oi[t];
+        bool in = false;
+        for (int u = 0; !in && u < kw; ++u) in = init[u] == v;
+        ch += in ? 0 : 1;
+        gid[i * kw + t] = v;
+        gd[i * kw + t] = od[t];
+    }
+    if (ch) atomicAdd(&s_ch, ch);
+    __syncthreads();
+    if (tid == 0 && s_ch) atomicAdd(churn, (unsigned long long)s_ch);
+}
+
 // ---------------------------------------------------------------- driver
 __global__ void to_global_kernel(const int32_t* __restrict__ gid, const double* __restrict__ gd,
                                  const int32_t* __restrict__ nodes, uint64_t n, int kw, int k,
@@ -1361,6 +1514,105 @@ static void score_claimed(Context& c, int mode, int32_t* ws, int32_t* wp, uint32
     so.cache_bits = c.dsurvbits();
     so.slot = wslot;
     score_entries(c, mode, ws, wp, nw, so);
+}
+
+// Finish a dense level whose first sweep covers every node (see "covered dense levels").
+// gid holds the initial rows (local ids, unsorted).  Returns false (nothing changed) when
+// some node's candidate set falls short; the sweeps then run as usual.
+static bool cover_level(Context& c, const int32_t* d_nodes, uint64_t n, int kw, int cap, const int32_t* loc,
+                        const int32_t* rootpos, int32_t* gid, double* gd, const KnnParamsD& p, KnnResultD& out) {
+    const int Wb = (int)((n + 31) / 32);
+    const uint64_t full = n - 1 - (uint64_t)kw;
+    DevBuf adjb, alenb, ubb, newfb, hnb, cntb, chb;
+    int32_t* adj = adjb.as<int32_t>(n * cap);
+    int32_t* alen = alenb.as<int32_t>(n);
+    uint32_t* ub = ubb.as<uint32_t>(n * (uint64_t)Wb);
+    uint8_t* newf = newfb.as<uint8_t>(n * cap);
+    uint8_t* hasnew = hnb.as<uint8_t>(n);
+    int32_t* cand_cnt = cntb.as<int32_t>(n);
+    unsigned long long* ch = chb.as<unsigned long long>(2);  // churn, nodes short of full coverage
+    c.tic();
+    u_out_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, c.stream>>>(gid, n, kw, cap, adj, alen);
+    NRG_CUDA(cudaMemsetAsync(ub, 0, n * (uint64_t)Wb * 4, c.stream));
+    NRG_CUDA(cudaMemsetAsync(newf, 1, n * cap, c.stream));  // first sweep: every entry is new
+    NRG_CUDA(cudaMemsetAsync(hasnew, 1, n, c.stream));
+    NRG_CUDA(cudaMemsetAsync(ch, 0, 16, c.stream));
+    u_set_kernel<<<(unsigned)ceil_div(n * (uint64_t)cap, 256), 256, 0, c.stream>>>(adj, alen, n, cap, Wb, ub);
+    ClaimSink sk{};
+    knn_gather_bits_kernel<256><<<(unsigned)n, 256, 2 * Wb * 4 + 4 * cap, c.stream>>>(
+        d_nodes, n, adj, alen, cap, gid, kw, Wb, ub, ub, newf, HashView{nullptr, nullptr, 0}, sk, 0, nullptr, nullptr,
+        cand_cnt, 0, false, rootpos, hasnew, /*count_only=*/true);
+    coverage_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(cand_cnt, n, (int)full, ch + 1);
+    NRG_LAUNCH_CHECK_N(4);
+    unsigned long long* hc = c.hp_small.as<unsigned long long>(2);
+    NRG_CUDA(cudaMemcpyAsync(hc, ch, 16, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (hc[1] != 0) {
+        c.toc(P_KNN);
+        return false;
+    }
+    // probes: the initial rows (n kw) and the sweep's candidates (n (n - 1 - kw)), all hits
+    // until the dense root's recount; marks: every pair of the level
+    counters_add_host(c, C_HITS, n * (n - 1));
+    const uint64_t dn = c.dense_n;
+    DevBuf mb, seenb, keepb, degb, offb, aidb, arkb, tmpb;
+    const uint64_t mwords = dn / 32 + 2;
+    uint32_t* M = mb.as<uint32_t>(mwords);
+    NRG_CUDA(cudaMemsetAsync(M, 0, mwords * 4, c.stream));
+    cover_members_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, c.stream>>>(rootpos, n, M);
+    cover_mark_kernel<<<(unsigned)ceil_div(n * 32, 256), 256, 0, c.stream>>>(rootpos, n, dn, M,
+                                                                           static_cast<uint32_t*>(c.dbits.p));
+    NRG_LAUNCH_CHECK_N(2);
+    // survivors of the level: claimed for K2, listed per node
+    const uint64_t nw = c.dwl_n;
+    unsigned long long* deg = degb.as<unsigned long long>(n + 1);
+    unsigned long long* off = offb.as<unsigned long long>(n + 1);
+    NRG_CUDA(cudaMemsetAsync(deg, 0, (n + 1) * 8, c.stream));
+    int32_t* adj_id = aidb.as<int32_t>(2 * nw + 1);
+    uint32_t* adj_rank = arkb.as<uint32_t>(2 * nw + 1);
+    if (nw) {
+        const uint64_t swords = dn * (dn - 1) / 2 / 32 + 1;
+        uint32_t* seen = seenb.as<uint32_t>(swords);
+        uint8_t* keep = keepb.as<uint8_t>(nw);
+        NRG_CUDA(cudaMemsetAsync(seen, 0, swords * 4, c.stream));
+        const DenseResolve R = dense_resolve_begin(c);
+        const int32_t* es = static_cast<const int32_t*>(c.dwl_es.p);
+        const int32_t* ep = static_cast<const int32_t*>(c.dwl_ep.p);
+        const uint32_t* wr = static_cast<const uint32_t*>(c.dwl_slot.p);
+        const int32_t* dloc = static_cast<const int32_t*>(c.dloc.p);
+        cover_worklist_kernel<<<(unsigned)ceil_div(nw, 256), 256, 0, c.stream>>>(R, es, ep, wr, nw, loc, dloc, dn, seen,
+                                                                                keep, deg, off, adj_id, adj_rank, 0);
+        NRG_LAUNCH_CHECK();
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, deg, off, (int64_t)(n + 1), c.stream);
+        void* tmp = tmpb.ensure(tb);
+        cub::DeviceScan::ExclusiveSum(tmp, tb, deg, off, (int64_t)(n + 1), c.stream);
+        NRG_CUDA(cudaMemsetAsync(deg, 0, (n + 1) * 8, c.stream));
+        cover_worklist_kernel<<<(unsigned)ceil_div(nw, 256), 256, 0, c.stream>>>(R, es, ep, wr, nw, loc, dloc, dn, seen,
+                                                                                keep, deg, off, adj_id, adj_rank, 1);
+        NRG_LAUNCH_CHECK();
+        c.toc(P_KNN);
+        dense_resolve_end(c);  // K2 on the claimed pairs (times itself)
+        c.tic();
+    } else {
+        NRG_CUDA(cudaMemsetAsync(off, 0, (n + 1) * 8, c.stream));
+    }
+    const DenseView D = c.dview();
+    cover_rows_kernel<<<(unsigned)n, 128, (size_t)kw * 16 + (size_t)(kw + 1) * 4 + 16, c.stream>>>(
+        d_nodes, n, kw, off, adj_id, adj_rank, D.vals, D.pruned, gid, gd, ch);
+    NRG_LAUNCH_CHECK();
+    NRG_CUDA(cudaMemcpyAsync(hc, ch, 16, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    c.toc(P_KNN);
+    out.sweeps = 1;
+    out.churn.clear();
+    const double ratio = (double)hc[0] / ((double)kw * (double)n);
+    out.churn.push_back(ratio);
+    if (!(ratio < p.eps) && p.max_sweeps > 1) {
+        ++out.sweeps;  // the next sweep, settled in advance: churn 0 < eps
+        out.churn.push_back(0.0);
+    }
+    return true;
 }
 
 void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, const KnnParamsD& p,
@@ -1507,6 +1759,19 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                 d_nodes + lo, sorted_ids, rank + lo, loc, own, n, kw, p.seed, gid + lo * kw, qi, qj);
         NRG_LAUNCH_CHECK();
         c.toc(P_KNN);
+        // a dense level the first sweep covers entirely is finished from the coverage alone
+        if (dense && sorted_valid && cap == kw && n <= (uint64_t)kBitsMaxN && cap >= 32 && p.max_sweeps >= 1 &&
+            (uint64_t)cap * cap >= n - 1 - (uint64_t)kw && !NRG_ENV_ON("NRG_NO_COVER_LEVEL") &&
+            !NRG_ENV_ON("NRG_NO_COVERAGE_SKIP") && !NRG_ENV_ON("NRG_KNN_HASH_GATHER") && !getenv("NRG_KNN_FULL_JOIN") &&
+            cover_level(c, d_nodes, n, kw, cap, loc, rootpos, gid, gd, p, out)) {
+            out.k = k;
+            out.ids = ids_buf.as<int32_t>(n * k);
+            out.dists = dist_buf.as<double>(n * k);
+            to_global_kernel<<<(unsigned)ceil_div(n * k, 256), 256, 0, c.stream>>>(gid, gd, d_nodes, n, kw, k, out.ids,
+                                                                                 out.dists);
+            NRG_LAUNCH_CHECK();
+            return;
+        }
         if (cached) {
             if (!dense) cache_reserve(c, n * (uint64_t)kw);
             uint32_t* slot = slb.as<uint32_t>(nq + 1);
