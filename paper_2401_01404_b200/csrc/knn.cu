@@ -782,7 +782,10 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
                                                              int32_t* __restrict__ cand_cnt, uint64_t lo, bool do_claim,
                                                              const int32_t* __restrict__ rootpos,
                                                              const uint8_t* __restrict__ hasnew,
-                                                             bool count_only = false) {
+                                                             bool count_only = false,
+                                                             const unsigned long long* __restrict__ sv_off = nullptr,
+                                                             const int32_t* __restrict__ sv_id = nullptr,
+                                                             int32_t* __restrict__ full_cnt = nullptr) {
     extern __shared__ uint32_t bits_smem[];
     uint32_t* acc = bits_smem;     // OR of the 2-hop rows
     uint32_t* excl = acc + W;      // i's current row and i itself
@@ -868,6 +871,68 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
         return;
     }
     int32_t* my_ids = cand_id + li * capn;
+    constexpr int kSvMax = 256;
+    if (rootpos && sv_off && (int)(sv_off[li + 1] - sv_off[li]) <= kSvMax &&
+        (uint64_t)(sv_off[li + 1] - sv_off[li]) + (uint64_t)kw <= capn) {
+        // Dense level, short list.  Every pair outside the screen's survivor list ties at
+        // -base, and among tied candidates only the kw smallest ids can enter a row; so the
+        // merge needs the node's survivors that are candidates plus the first kw other
+        // candidates -- a list of kw + a few entries instead of thousands (same merged row,
+        // same churn; the resolve and merge kernels read it unchanged).  Every candidate is
+        // still probed (marked and counted).
+        __shared__ int32_t s_sv[kSvMax];
+        __shared__ int s_n;
+        uint32_t* my_slot = cand_slot + li * capn;
+        const uint64_t ra = (uint64_t)rootpos[li];
+        const unsigned long long s0 = sv_off[li];
+        const int sdeg = (int)(sv_off[li + 1] - s0);
+        if (tid == 0) s_n = 0;
+        // the node's survivors that are candidates (the others do not take part)
+        for (int e = tid; e < kSvMax; e += NT) s_sv[e] = -1;
+        __syncthreads();
+        for (int e = tid; e < sdeg; e += NT) {
+            const int32_t v = sv_id[s0 + e];
+            if ((acc[v >> 5] & ~excl[v >> 5]) >> (v & 31) & 1u) {
+                s_sv[e] = v;
+                const int at = atomicAdd(&s_n, 1);
+                my_ids[at] = v;
+                const uint64_t rb = (uint64_t)rootpos[v];
+                my_slot[at] = (uint32_t)(ra < rb ? tri_index(ra, rb, sink.dn) : tri_index(rb, ra, sink.dn));
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < kMaxWpt; ++q) {
+            const int w = tid * kMaxWpt + q;
+            for (uint32_t m = cw[q]; m; m &= m - 1) {
+                const int v = 32 * w + __ffs(m) - 1;
+                const uint32_t t = dense_probe(sink.dbits, sink.dn, ra, (uint64_t)rootpos[v]);
+                if (off < kw + sdeg) {
+                    // rank among the candidates outside the survivor list, in id order
+                    int below = 0;
+                    bool is_sv = false;
+                    for (int e = 0; e < sdeg; ++e) {
+                        const int32_t u = s_sv[e];
+                        is_sv |= u == v;
+                        below += (u >= 0 && u < v) ? 1 : 0;
+                    }
+                    if (!is_sv && off - below < kw) {
+                        const int at = atomicAdd(&s_n, 1);
+                        my_ids[at] = v;
+                        my_slot[at] = t;
+                    }
+                }
+                ++off;
+            }
+        }
+        if (tid == 0 && total) atomicAdd((unsigned long long*)&sink.counters[C_HITS], (unsigned long long)total);
+        __syncthreads();
+        if (tid == 0) {
+            cand_cnt[li] = s_n;
+            full_cnt[li] = total;
+        }
+        return;
+    }
     if (rootpos) {
         // dense level: slots in the root's distance triangle, probes marked and counted here
         uint32_t* my_slot = cand_slot + li * capn;
@@ -884,7 +949,10 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
         const int probes = warp_sum(cnt);
         if ((tid & 31) == 0 && probes)
             atomicAdd((unsigned long long*)&sink.counters[C_HITS], (unsigned long long)probes);
-        if (tid == 0) cand_cnt[li] = total;
+        if (tid == 0) {
+            cand_cnt[li] = total;
+            if (full_cnt) full_cnt[li] = total;
+        }
         return;
     }
 #pragma unroll
@@ -1398,7 +1466,8 @@ __global__ void cover_worklist_kernel(DenseResolve R, const int32_t* __restrict_
                                       const int32_t* __restrict__ loc, const int32_t* __restrict__ dloc, uint64_t dn,
                                       uint32_t* __restrict__ seen, uint8_t* __restrict__ keep,
                                       unsigned long long* __restrict__ deg, const unsigned long long* __restrict__ off,
-                                      int32_t* __restrict__ adj_id, uint32_t* __restrict__ adj_rank, int pass) {
+                                      int32_t* __restrict__ adj_id, uint32_t* __restrict__ adj_rank, int pass,
+                                      bool claim) {
     const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= nw) return;
     const int32_t u = es[e], v = ep[e];
@@ -1411,7 +1480,7 @@ __global__ void cover_worklist_kernel(DenseResolve R, const int32_t* __restrict_
         const uint32_t bit = 1u << (t & 31);
         if (atomicOr(&seen[t >> 5], bit) & bit) return;
         keep[e] = 1;
-        dense_resolve_slot(R, (uint32_t)t);
+        if (claim) dense_resolve_slot(R, (uint32_t)t);
         atomicAdd(&deg[a], 1ull);
         atomicAdd(&deg[b], 1ull);
     } else if (keep[e]) {
@@ -1516,6 +1585,48 @@ static void score_claimed(Context& c, int mode, int32_t* ws, int32_t* wp, uint32
     score_entries(c, mode, ws, wp, nw, so);
 }
 
+// Per-node lists of the level's pairs on the dense root's survivor worklist (local ids),
+// for the short candidate lists of knn_gather_bits_kernel.  off: n + 1 offsets.
+struct LevelSurvivors {
+    DevBuf seenb, keepb, degb, offb, idb, rkb, tmpb;
+    const unsigned long long* off = nullptr;
+    const int32_t* id = nullptr;
+};
+static void level_survivors(Context& c, const int32_t* loc, uint64_t n, LevelSurvivors& L) {
+    const uint64_t nw = c.dwl_n, dn = c.dense_n;
+    unsigned long long* deg = L.degb.as<unsigned long long>(n + 1);
+    unsigned long long* off = L.offb.as<unsigned long long>(n + 1);
+    int32_t* adj_id = L.idb.as<int32_t>(2 * nw + 1);
+    uint32_t* adj_rank = L.rkb.as<uint32_t>(2 * nw + 1);
+    NRG_CUDA(cudaMemsetAsync(deg, 0, (n + 1) * 8, c.stream));
+    NRG_CUDA(cudaMemsetAsync(off, 0, (n + 1) * 8, c.stream));
+    if (nw) {
+        const uint64_t swords = dn * (dn - 1) / 2 / 32 + 1;
+        uint32_t* seen = L.seenb.as<uint32_t>(swords);
+        uint8_t* keep = L.keepb.as<uint8_t>(nw);
+        NRG_CUDA(cudaMemsetAsync(seen, 0, swords * 4, c.stream));
+        const DenseResolve R{};  // no claims here
+        const int32_t* es = static_cast<const int32_t*>(c.dwl_es.p);
+        const int32_t* ep = static_cast<const int32_t*>(c.dwl_ep.p);
+        const uint32_t* wr = static_cast<const uint32_t*>(c.dwl_slot.p);
+        const int32_t* dloc = static_cast<const int32_t*>(c.dloc.p);
+        cover_worklist_kernel<<<(unsigned)ceil_div(nw, 256), 256, 0, c.stream>>>(R, es, ep, wr, nw, loc, dloc, dn, seen,
+                                                                                keep, deg, off, adj_id, adj_rank, 0,
+                                                                                false);
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, deg, off, (int64_t)(n + 1), c.stream);
+        void* tmp = L.tmpb.ensure(tb);
+        cub::DeviceScan::ExclusiveSum(tmp, tb, deg, off, (int64_t)(n + 1), c.stream);
+        NRG_CUDA(cudaMemsetAsync(deg, 0, (n + 1) * 8, c.stream));
+        cover_worklist_kernel<<<(unsigned)ceil_div(nw, 256), 256, 0, c.stream>>>(R, es, ep, wr, nw, loc, dloc, dn, seen,
+                                                                                keep, deg, off, adj_id, adj_rank, 1,
+                                                                                false);
+        NRG_LAUNCH_CHECK_N(2);
+    }
+    L.off = off;
+    L.id = adj_id;
+}
+
 // Finish a dense level whose first sweep covers every node (see "covered dense levels").
 // gid holds the initial rows (local ids, unsorted).  Returns false (nothing changed) when
 // some node's candidate set falls short; the sweeps then run as usual.
@@ -1581,7 +1692,7 @@ static bool cover_level(Context& c, const int32_t* d_nodes, uint64_t n, int kw, 
         const uint32_t* wr = static_cast<const uint32_t*>(c.dwl_slot.p);
         const int32_t* dloc = static_cast<const int32_t*>(c.dloc.p);
         cover_worklist_kernel<<<(unsigned)ceil_div(nw, 256), 256, 0, c.stream>>>(R, es, ep, wr, nw, loc, dloc, dn, seen,
-                                                                                keep, deg, off, adj_id, adj_rank, 0);
+                                                                                keep, deg, off, adj_id, adj_rank, 0, true);
         NRG_LAUNCH_CHECK();
         size_t tb = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, tb, deg, off, (int64_t)(n + 1), c.stream);
@@ -1589,7 +1700,7 @@ static bool cover_level(Context& c, const int32_t* d_nodes, uint64_t n, int kw, 
         cub::DeviceScan::ExclusiveSum(tmp, tb, deg, off, (int64_t)(n + 1), c.stream);
         NRG_CUDA(cudaMemsetAsync(deg, 0, (n + 1) * 8, c.stream));
         cover_worklist_kernel<<<(unsigned)ceil_div(nw, 256), 256, 0, c.stream>>>(R, es, ep, wr, nw, loc, dloc, dn, seen,
-                                                                                keep, deg, off, adj_id, adj_rank, 1);
+                                                                                keep, deg, off, adj_id, adj_rank, 1, true);
         NRG_LAUNCH_CHECK();
         c.toc(P_KNN);
         dense_resolve_end(c);  // K2 on the claimed pairs (times itself)
@@ -1900,6 +2011,17 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
     out.sweeps = 0;
     out.churn.clear();
     DevBuf ktgt, kd, ksrc, vsrc, ktgt2, kd2, ksrc2, vsrc2, segb, sorttmp, permb, perm2b;
+    // dense bit-set levels: per-node survivor lists for the gathers' short candidate lists
+    LevelSurvivors LS;
+    DevBuf fullb;
+    int32_t* full_cnt = nullptr;
+    if (dense && n <= (uint64_t)kBitsMaxN && cap >= 32 && !NRG_ENV_ON("NRG_KNN_HASH_GATHER") &&
+        !NRG_ENV_ON("NRG_NO_SHORT_LISTS")) {
+        c.tic();
+        level_survivors(c, loc, n, LS);
+        full_cnt = fullb.as<int32_t>(n);
+        c.toc(P_KNN);
+    }
     for (int sweep = 0; sweep < p.max_sweeps; ++sweep) {
         c.tic();
         // U
@@ -1979,7 +2101,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                 uint32_t* nbits = static_cast<uint32_t*>(nbitsb.p);
                 knn_gather_bits_kernel<256><<<(unsigned)own, 256, 2 * W * 4 + 4 * cap, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, W, ub, nbits, newf, hv0, sk, capn, cand_id, cand_slot, cand_cnt,
-                    lo, fused, rootpos, static_cast<const uint8_t*>(hasnewb.p));
+                    lo, fused, rootpos, static_cast<const uint8_t*>(hasnewb.p), false, LS.off, LS.id, full_cnt);
             } else if (big)
                 knn_gather_kernel<256><<<(unsigned)own, 256, tab_bytes, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv0, sk, capn, cand_id,
@@ -2069,8 +2191,8 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         // would only re-probe pairs this sweep already probed (hits, no misses).
         const bool cov_check = bitsmode && c.world == 1 && !NRG_ENV_ON("NRG_NO_COVERAGE_SKIP");
         if (cov_check && own) {
-            coverage_kernel<<<(unsigned)ceil_div(own, 256), 256, 0, c.stream>>>(cand_cnt + lo, own,
-                                                                             (int)(n - 1 - (uint64_t)kw), churn + 1);
+            coverage_kernel<<<(unsigned)ceil_div(own, 256), 256, 0, c.stream>>>(
+                (full_cnt ? full_cnt : cand_cnt) + lo, own, (int)(n - 1 - (uint64_t)kw), churn + 1);
             NRG_LAUNCH_CHECK();
         }
         unsigned long long* hc = c.hp_small.as<unsigned long long>(2);
