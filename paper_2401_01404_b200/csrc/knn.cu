@@ -871,9 +871,9 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
         return;
     }
     int32_t* my_ids = cand_id + li * capn;
-    constexpr int kSvMax = 256;
+    constexpr int kSvMax = 256, kEarlyMax = 512;
     if (rootpos && sv_off && (int)(sv_off[li + 1] - sv_off[li]) <= kSvMax &&
-        (uint64_t)(sv_off[li + 1] - sv_off[li]) + (uint64_t)kw <= capn) {
+        (uint64_t)(sv_off[li + 1] - sv_off[li]) + (uint64_t)kw <= min((uint64_t)kEarlyMax, capn)) {
         // Dense level, short list.  Every pair outside the screen's survivor list ties at
         // -base, and among tied candidates only the kw smallest ids can enter a row; so the
         // merge needs the node's survivors that are candidates plus the first kw other
@@ -881,51 +881,57 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
         // same churn; the resolve and merge kernels read it unchanged).  Every candidate is
         // still probed (marked and counted).
         __shared__ int32_t s_sv[kSvMax];
+        __shared__ int32_t s_early[kEarlyMax];  // the first kw + sdeg candidates, in id order
         __shared__ int s_n;
         uint32_t* my_slot = cand_slot + li * capn;
         const uint64_t ra = (uint64_t)rootpos[li];
         const unsigned long long s0 = sv_off[li];
         const int sdeg = (int)(sv_off[li + 1] - s0);
+        const int need = kw + sdeg;
         if (tid == 0) s_n = 0;
-        // the node's survivors that are candidates (the others do not take part)
-        for (int e = tid; e < kSvMax; e += NT) s_sv[e] = -1;
         __syncthreads();
+        // the node's survivors that are candidates (the others do not take part)
         for (int e = tid; e < sdeg; e += NT) {
             const int32_t v = sv_id[s0 + e];
-            if ((acc[v >> 5] & ~excl[v >> 5]) >> (v & 31) & 1u) {
-                s_sv[e] = v;
+            const bool isc = (acc[v >> 5] & ~excl[v >> 5]) >> (v & 31) & 1u;
+            s_sv[e] = isc ? v : -1;
+            if (isc) {
                 const int at = atomicAdd(&s_n, 1);
                 my_ids[at] = v;
                 const uint64_t rb = (uint64_t)rootpos[v];
                 my_slot[at] = (uint32_t)(ra < rb ? tri_index(ra, rb, sink.dn) : tri_index(rb, ra, sink.dn));
             }
         }
-        __syncthreads();
 #pragma unroll
         for (int q = 0; q < kMaxWpt; ++q) {
             const int w = tid * kMaxWpt + q;
             for (uint32_t m = cw[q]; m; m &= m - 1) {
                 const int v = 32 * w + __ffs(m) - 1;
-                const uint32_t t = dense_probe(sink.dbits, sink.dn, ra, (uint64_t)rootpos[v]);
-                if (off < kw + sdeg) {
-                    // rank among the candidates outside the survivor list, in id order
-                    int below = 0;
-                    bool is_sv = false;
-                    for (int e = 0; e < sdeg; ++e) {
-                        const int32_t u = s_sv[e];
-                        is_sv |= u == v;
-                        below += (u >= 0 && u < v) ? 1 : 0;
-                    }
-                    if (!is_sv && off - below < kw) {
-                        const int at = atomicAdd(&s_n, 1);
-                        my_ids[at] = v;
-                        my_slot[at] = t;
-                    }
-                }
+                dense_probe(sink.dbits, sink.dn, ra, (uint64_t)rootpos[v]);
+                if (off < need) s_early[off] = v;
                 ++off;
             }
         }
         if (tid == 0 && total) atomicAdd((unsigned long long*)&sink.counters[C_HITS], (unsigned long long)total);
+        __syncthreads();
+        // rank of an early candidate among the candidates outside the survivor list
+        const int nearly = min(total, need);
+        for (int e = tid; e < nearly; e += NT) {
+            const int32_t v = s_early[e];
+            int below = 0;
+            bool is_sv = false;
+            for (int u = 0; u < sdeg; ++u) {
+                const int32_t x = s_sv[u];
+                is_sv |= x == v;
+                below += (x >= 0 && x < v) ? 1 : 0;
+            }
+            if (!is_sv && e - below < kw) {
+                const int at = atomicAdd(&s_n, 1);
+                my_ids[at] = v;
+                const uint64_t rb = (uint64_t)rootpos[v];
+                my_slot[at] = (uint32_t)(ra < rb ? tri_index(ra, rb, sink.dn) : tri_index(rb, ra, sink.dn));
+            }
+        }
         __syncthreads();
         if (tid == 0) {
             cand_cnt[li] = s_n;
