@@ -902,15 +902,35 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
                 my_slot[at] = (uint32_t)(ra < rb ? tri_index(ra, rb, sink.dn) : tri_index(rb, ra, sink.dn));
             }
         }
+        // at the dense root itself (local id = root position) the pairs (li, v > li) of a
+        // candidate word sit at consecutive triangle slots: one or two REDs mark them all
+        const bool ident = sink.dn == n;
+        const long long tbase = (long long)(ra * (2 * sink.dn - ra - 1) / 2);
 #pragma unroll
         for (int q = 0; q < kMaxWpt; ++q) {
             const int w = tid * kMaxWpt + q;
-            for (uint32_t m = cw[q]; m; m &= m - 1) {
-                const int v = 32 * w + __ffs(m) - 1;
-                dense_probe(sink.dbits, sink.dn, ra, (uint64_t)rootpos[v]);
-                if (off < need) s_early[off] = v;
-                ++off;
+            uint32_t m = cw[q];
+            if (!m) continue;
+            if (off < need) {
+                int o = off;
+                for (uint32_t mm = m; mm && o < need; mm &= mm - 1, ++o) s_early[o] = 32 * w + __ffs(mm) - 1;
             }
+            off += __popc(m);
+            if (ident) {
+                const int rel = (int)li - 32 * w;  // v > li <=> bit index > rel
+                const uint32_t mh = rel < 0 ? m : (rel >= 31 ? 0u : (m & (~0u << (rel + 1))));
+                if (mh) {
+                    const long long T0 = tbase + 32LL * w - (long long)li - 1;  // slot of bit 0
+                    const long long lw = T0 >> 5;
+                    const unsigned sh = (unsigned)(T0 & 31);
+                    const unsigned long long val = (unsigned long long)mh << sh;
+                    if ((uint32_t)val) atomicOr(&sink.dbits[lw], (uint32_t)val);
+                    if (val >> 32) atomicOr(&sink.dbits[lw + 1], (uint32_t)(val >> 32));
+                }
+                m &= ~mh;
+            }
+            for (; m; m &= m - 1)
+                dense_probe(sink.dbits, sink.dn, ra, (uint64_t)rootpos[32 * w + __ffs(m) - 1]);
         }
         if (tid == 0 && total) atomicAdd((unsigned long long*)&sink.counters[C_HITS], (unsigned long long)total);
         __syncthreads();
