@@ -520,25 +520,49 @@ __global__ void dense_subtri_kernel(const int32_t* __restrict__ nodes, uint64_t 
 // had scored (absent from the distance cache: U - F) are the generation's misses.
 // count_bits: the probed pairs (bits) count as misses on one rank only; every rank
 // moves the probed pairs its shard of the key-sharded cache already held back to hits
-__global__ void dense_recount_kernel(HashView h, const int32_t* __restrict__ loc, const uint32_t* __restrict__ bits,
-                                     uint64_t nwords, uint64_t dn, uint64_t* __restrict__ counters, int count_bits) {
+__global__ void dense_recount_kernel(HashView h, const int32_t* __restrict__ loc, const uint32_t* __restrict__ sq,
+                                     uint64_t dn, uint64_t* __restrict__ counters, int count_bits) {
     long long d = 0;
+    const uint64_t Wd = (dn + 31) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (count_bits) {
+        // distinct probed pairs: the square mark matrix OR its transpose, above the diagonal;
+        // one warp per 32 x 32 bit block (I <= J), lane r = row r of the block
+        const uint64_t warp0 = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+        for (uint64_t blk = warp0; blk < Wd * Wd; blk += nwarps) {
+            const uint64_t I = blk / Wd, J = blk % Wd;
+            if (J < I) continue;
+            const uint64_t ra = 32 * I + lane, rb = 32 * J + lane;
+            const uint32_t A = ra < dn ? sq[ra * Wd + J] : 0u;
+            const uint32_t B = rb < dn ? sq[rb * Wd + I] : 0u;
+            // transpose of B (bit c of lane r = bit r of B's lane c): five block-swap steps
+            uint32_t T = B;
+#pragma unroll
+            for (int j = 16; j; j >>= 1) {
+                const uint32_t hi = j == 16 ? 0xffff0000u : j == 8 ? 0xff00ff00u : j == 4 ? 0xf0f0f0f0u
+                                  : j == 2 ? 0xccccccccu : 0xaaaaaaaau;  // columns with bit j set
+                const uint32_t y = __shfl_xor_sync(0xffffffffu, T, j);
+                T = (lane & j) ? ((T & hi) | ((y >> j) & ~hi)) : ((T & ~hi) | ((y << j) & hi));
+            }
+            uint32_t X = A | T;
+            if (I == J) X &= lane == 31 ? 0u : (~0u << (lane + 1));  // columns past the diagonal
+            d += __popc(X);
+        }
+    }
     const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, st = (uint64_t)gridDim.x * blockDim.x;
-    if (count_bits)
-        for (uint64_t w = t0; w < nwords; w += st) d += __popc(bits[w]);
     if (h.keys) {
         for (uint64_t s = t0; s <= h.mask; s += st) {
             const uint64_t key = __ldcs(&h.keys[s]);
             if (key >= kTombKey) continue;
             const int32_t la = loc[(uint32_t)(key >> 32)], lb = loc[(uint32_t)(key & 0xffffffffu)];
             if (la < 0 || lb < 0) continue;
-            const uint64_t a = (uint64_t)min(la, lb), b = (uint64_t)max(la, lb);
-            const uint64_t t = a * (2 * dn - a - 1) / 2 + (b - a - 1);
-            d -= (bits[t >> 5] >> (t & 31)) & 1u;
+            const uint64_t a = (uint64_t)la, b = (uint64_t)lb;
+            d -= ((sq[a * Wd + (b >> 5)] >> (b & 31)) | (sq[b * Wd + (a >> 5)] >> (a & 31))) & 1u;
         }
     }
     for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-    if ((threadIdx.x & 31) == 0 && d) {
+    if (lane == 0 && d) {
         atomicAdd((unsigned long long*)&counters[C_MISSES], (unsigned long long)d);
         atomicAdd((unsigned long long*)&counters[C_HITS], (unsigned long long)(-d));
     }
@@ -581,9 +605,8 @@ struct DenseGuard {
             // change under it: join_side() before any clear, resize or counter read)
             cudaStream_t ss = c.fork();
             dense_recount_kernel<<<148 * 8, 256, 0, ss>>>(h, static_cast<const int32_t*>(c.dloc.p),
-                                                          static_cast<const uint32_t*>(c.dbits.p),
-                                                          (pairs + 31) / 32, c.dense_n, c.dcounters(),
-                                                          real_rank == 0 ? 1 : 0);
+                                                          static_cast<const uint32_t*>(c.dbits.p), c.dense_n,
+                                                          c.dcounters(), real_rank == 0 ? 1 : 0);
             c.fork_done();
             c.dense_active = false;
             c.dense_n = 0;  // the buffers stay (grow-only): the next generation reuses them
@@ -777,8 +800,10 @@ static uint64_t find_best_impl(Context& c, int mode, uint64_t m, const int32_t* 
                 NRG_CUDA(cudaMemsetAsync(loc, 0xff, (size_t)c.n * 4, c.stream));
                 dense_loc_kernel<<<g256(n), 256, 0, c.stream>>>(S, n, loc);
                 NRG_LAUNCH_CHECK();
-                uint32_t* bits = c.dbits.as<uint32_t>((total + 31) / 32);
-                NRG_CUDA(cudaMemsetAsync(bits, 0, (total + 31) / 32 * 4, c.stream));
+                // probe marks: square bit matrix over the root's positions (row = probing node)
+                const uint64_t mwords = n * ((n + 31) / 32);
+                uint32_t* bits = c.dbits.as<uint32_t>(mwords);
+                NRG_CUDA(cudaMemsetAsync(bits, 0, mwords * 4, c.stream));
                 c.dense_active = true;
                 c.dense_n = n;
                 dg.owner = true;

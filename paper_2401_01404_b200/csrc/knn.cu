@@ -300,7 +300,10 @@ __device__ __forceinline__ uint64_t tri_index(uint64_t a, uint64_t b, uint64_t n
 // misses/hits (inc/model.hpp:54-70) without a round trip per probe.
 __device__ __forceinline__ uint32_t dense_probe(uint32_t* __restrict__ dbits, uint64_t dn, uint64_t ra, uint64_t rb) {
     const uint64_t t = ra < rb ? tri_index(ra, rb, dn) : tri_index(rb, ra, dn);
-    atomicOr(&dbits[t >> 5], 1u << (t & 31));
+    // marks: a square bit matrix over root positions, row = the probing node (a node's marks
+    // of one sweep fall in one row: whole words of its candidate bitset at the root level);
+    // dense_recount symmetrises it
+    atomicOr(&dbits[ra * ((dn + 31) >> 5) + (rb >> 5)], 1u << (rb & 31));
     return (uint32_t)t;
 }
 
@@ -902,14 +905,17 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
                 my_slot[at] = (uint32_t)(ra < rb ? tri_index(ra, rb, sink.dn) : tri_index(rb, ra, sink.dn));
             }
         }
-        // at the dense root itself (local id = root position) the pairs (li, v > li) of a
-        // candidate word sit at consecutive triangle slots: one or two REDs mark them all
+        // marks go into row ra of the square matrix: at the dense root itself (local id = root
+        // position) a candidate word is a word of that row; deeper, consecutive candidates
+        // that share a word go out together
         const bool ident = sink.dn == n;
-        const long long tbase = (long long)(ra * (2 * sink.dn - ra - 1) / 2);
+        uint32_t* mrow = sink.dbits + ra * ((sink.dn + 31) >> 5);
+        uint64_t pw = ~0ull;
+        uint32_t pbits = 0u;
 #pragma unroll
         for (int q = 0; q < kMaxWpt; ++q) {
             const int w = tid * kMaxWpt + q;
-            uint32_t m = cw[q];
+            const uint32_t m = cw[q];
             if (!m) continue;
             if (off < need) {
                 int o = off;
@@ -917,21 +923,20 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
             }
             off += __popc(m);
             if (ident) {
-                const int rel = (int)li - 32 * w;  // v > li <=> bit index > rel
-                const uint32_t mh = rel < 0 ? m : (rel >= 31 ? 0u : (m & (~0u << (rel + 1))));
-                if (mh) {
-                    const long long T0 = tbase + 32LL * w - (long long)li - 1;  // slot of bit 0
-                    const long long lw = T0 >> 5;
-                    const unsigned sh = (unsigned)(T0 & 31);
-                    const unsigned long long val = (unsigned long long)mh << sh;
-                    if ((uint32_t)val) atomicOr(&sink.dbits[lw], (uint32_t)val);
-                    if (val >> 32) atomicOr(&sink.dbits[lw + 1], (uint32_t)(val >> 32));
+                atomicOr(&mrow[w], m);
+            } else {
+                for (uint32_t mm = m; mm; mm &= mm - 1) {
+                    const uint64_t rb = (uint64_t)rootpos[32 * w + __ffs(mm) - 1];
+                    if ((rb >> 5) != pw) {
+                        if (pbits) atomicOr(&mrow[pw], pbits);
+                        pw = rb >> 5;
+                        pbits = 0u;
+                    }
+                    pbits |= 1u << (rb & 31);
                 }
-                m &= ~mh;
             }
-            for (; m; m &= m - 1)
-                dense_probe(sink.dbits, sink.dn, ra, (uint64_t)rootpos[32 * w + __ffs(m) - 1]);
         }
+        if (pbits) atomicOr(&mrow[pw], pbits);
         if (tid == 0 && total) atomicAdd((unsigned long long*)&sink.counters[C_HITS], (unsigned long long)total);
         __syncthreads();
         // rank of an early candidate among the candidates outside the survivor list
@@ -1457,31 +1462,18 @@ __global__ void cover_members_kernel(const int32_t* __restrict__ rootpos, uint64
     const uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (a < n) atomicOr(&M[rootpos[a] >> 5], 1u << (rootpos[a] & 31));
 }
-// row ra of the root's triangle holds the pairs (ra, rb > ra) at consecutive slots: the
-// level's members among them are the member mask shifted into place, one RED per word
+// every pair of the level probed from both sides: row ra of the square mark matrix takes the
+// level's member mask (without ra itself)
 __global__ void cover_mark_kernel(const int32_t* __restrict__ rootpos, uint64_t n, uint64_t dn,
                                   const uint32_t* __restrict__ M, uint32_t* __restrict__ dbits) {
     const uint64_t a = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (a >= n) return;
-    const uint64_t ra = (uint64_t)rootpos[a];
-    if (ra + 1 >= dn) return;
-    const uint64_t tbase = ra * (2 * dn - ra - 1) / 2, len = dn - ra - 1;
-    const uint64_t W0 = tbase >> 5, W1 = (tbase + len - 1) >> 5;
-    for (uint64_t W = W0 + lane; W <= W1; W += 32) {
-        const long long s = (long long)(32 * W) - (long long)tbase + (long long)ra + 1;  // member index of bit 0
-        uint32_t val;
-        if (s < 0) {
-            val = s > -32 ? M[0] << (unsigned)(-s) : 0u;
-        } else {
-            const uint64_t idx = (uint64_t)s >> 5;
-            const unsigned sh = (unsigned)s & 31u;
-            val = M[idx] >> sh;
-            if (sh) val |= M[idx + 1] << (32u - sh);
-        }
-        const long long cut = (long long)ra + 1 - s;  // bits below: positions <= ra
-        if (cut > 0) val &= cut >= 32 ? 0u : (~0u << (unsigned)cut);
-        if (val) atomicOr(&dbits[W], val);
+    const uint64_t ra = (uint64_t)rootpos[a], Wd = (dn + 31) >> 5;
+    for (uint64_t w = lane; w < Wd; w += 32) {
+        uint32_t val = M[w];
+        if (w == (ra >> 5)) val &= ~(1u << (ra & 31));
+        if (val) atomicOr(&dbits[ra * Wd + w], val);
     }
 }
 // the screen's worklist entries with both endpoints in the level: claim the pair for the
