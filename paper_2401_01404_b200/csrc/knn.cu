@@ -1815,7 +1815,8 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
     DevBuf gid_buf, gd_buf;
     int32_t* gid = gid_buf.as<int32_t>(n * kw);
     double* gd = gd_buf.as<double>(n * kw);
-    unsigned long long* wcount = c.s_c.as<unsigned long long>(2);
+    // wcount[2] (claims) and churn[2] side by side: one clear and one readback per sweep
+    unsigned long long* wcount = c.s_c.as<unsigned long long>(4);
     const bool cached = (mode == EXACT || mode == GRADIENT);
     // dense level: distances come from the level's exhaustive triangle (find_best.cu)
     const bool dense = mode == EXACT && c.dense_active && c.world == 1;
@@ -1981,7 +1982,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
     int32_t* cand_cnt = ccntb.as<int32_t>(n);
     // churn[0]: entries this sweep changed; churn[1]: nodes whose candidate set missed
     // some node (bit-set gathers of one rank; read back together)
-    unsigned long long* churn = churnb.as<unsigned long long>(2);
+    unsigned long long* churn = wcount + 2;
     const uint64_t wmax = n * capn;
     int32_t* ws = wsb.as<int32_t>(wmax);
     int32_t* wp = wpb.as<int32_t>(wmax);
@@ -2101,8 +2102,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         const bool fused = !cached || dense || (c.cache_live_host + wmax) * 10 <= (1ull << 31) * 6;
         if (cached && fused && !dense) cache_reserve(c, wmax);
         c.tic();
-        NRG_CUDA(cudaMemsetAsync(wcount, 0, 16, c.stream));
-        NRG_CUDA(cudaMemsetAsync(churn, 0, 16, c.stream));
+        NRG_CUDA(cudaMemsetAsync(wcount, 0, 32, c.stream));  // and churn
         ClaimSink sk = sink_for(ws, wp, wsl, own * capn + 1);
         // own claims resolve through the worklist-ordered distances (single rank, a memo
         // and worklist small enough for 31-bit indices)
@@ -2213,11 +2213,14 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                 (full_cnt ? full_cnt : cand_cnt) + lo, own, (int)(n - 1 - (uint64_t)kw), churn + 1);
             NRG_LAUNCH_CHECK();
         }
-        unsigned long long* hc = c.hp_small.as<unsigned long long>(2);
-        NRG_CUDA(cudaMemcpyAsync(hc, churn, 16, cudaMemcpyDeviceToHost, c.stream));
+        unsigned long long* hc = c.hp_small.as<unsigned long long>(4);
+        NRG_CUDA(cudaMemcpyAsync(hc, wcount, 32, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
-        unsigned long long changed = hc[0];
-        const bool covered = cov_check && hc[1] == 0;
+        unsigned long long changed = hc[2];
+        const bool covered = cov_check && hc[3] == 0;
+        // the sweep's actual claims tighten the memo's host-side occupancy bound (reserved
+        // for the worst case, n x cap^2): fewer reserves fall back to reading the live count
+        if (sk.fold && fused) c.cache_live_bound = c.cache_live_host + hc[0];
         allgather_rows(gid, gd, kw);
         if (c.world > 1) {
             uint64_t ch = changed;
