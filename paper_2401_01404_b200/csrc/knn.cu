@@ -1892,6 +1892,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         // a dense level the first sweep covers entirely is finished from the coverage alone
         if (dense && sorted_valid && cap == kw && n <= (uint64_t)kBitsMaxN && cap >= 32 && p.max_sweeps >= 1 &&
             (uint64_t)cap * cap >= n - 1 - (uint64_t)kw && !NRG_ENV_ON("NRG_NO_COVER_LEVEL") &&
+            !NRG_ENV_ON("NRG_DENSE_EAGER") &&  // (the survivor lists come from the lazy root's worklist)
             !NRG_ENV_ON("NRG_NO_COVERAGE_SKIP") && !NRG_ENV_ON("NRG_KNN_HASH_GATHER") && !getenv("NRG_KNN_FULL_JOIN") &&
             cover_level(c, d_nodes, n, kw, cap, loc, rootpos, gid, gd, p, out)) {
             out.k = k;
@@ -2035,7 +2036,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
     DevBuf fullb;
     int32_t* full_cnt = nullptr;
     if (dense && n <= (uint64_t)kBitsMaxN && cap >= 32 && !NRG_ENV_ON("NRG_KNN_HASH_GATHER") &&
-        !NRG_ENV_ON("NRG_NO_SHORT_LISTS")) {
+        !NRG_ENV_ON("NRG_NO_SHORT_LISTS") && !NRG_ENV_ON("NRG_DENSE_EAGER")) {
         c.tic();
         level_survivors(c, loc, n, LS);
         full_cnt = fullb.as<int32_t>(n);

@@ -46,7 +46,7 @@ print("RESULT " + json.dumps(out))
 
 def _run(env_extra):
     env = dict(os.environ)
-    for k in ("NRG_TC_ONE_TILE", "NRG_NO_SHORT_LISTS", "NRG_NO_COVER_LEVEL", "NRG_NO_ROW_FLAGS"):
+    for k in ("NRG_TC_ONE_TILE", "NRG_NO_SHORT_LISTS", "NRG_NO_COVER_LEVEL", "NRG_NO_ROW_FLAGS", "NRG_DENSE_EAGER"):
         env.pop(k, None)
     env.update(env_extra)
     r = subprocess.run([sys.executable, "-c", SCRIPT], env=env, capture_output=True, text=True, timeout=600)
@@ -57,7 +57,7 @@ def _run(env_extra):
 
 def test_dense_fast_paths_equal_plain_paths():
     base = _run({})
-    for switch in ("NRG_TC_ONE_TILE", "NRG_NO_SHORT_LISTS", "NRG_NO_COVER_LEVEL"):
+    for switch in ("NRG_TC_ONE_TILE", "NRG_NO_SHORT_LISTS", "NRG_NO_COVER_LEVEL", "NRG_DENSE_EAGER"):
         assert _run({switch: "1"}) == base, switch
 
 
