@@ -659,11 +659,21 @@ __global__ void pair_dedup_kernel(const TriKey* __restrict__ in, uint64_t n, int
             s = (s + 1) & mask;
         }
     }
+    // one reservation per CTA (a returning atomic per warp on one address serialises in L2)
+    __shared__ unsigned s_w[8];
+    __shared__ unsigned long long s_base;
     const unsigned b = __ballot_sync(0xffffffffu, keep);
-    const int lane = threadIdx.x & 31;
-    unsigned long long at = 0;
-    if (lane == 0 && b) at = atomicAdd(cnt, (unsigned long long)__popc(b));
-    at = __shfl_sync(0xffffffffu, at, 0);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) s_w[wid] = (unsigned)__popc(b);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned tot = 0;
+        for (int w = 0; w < 8; ++w) tot += s_w[w];
+        s_base = tot ? atomicAdd(cnt, (unsigned long long)tot) : 0ull;
+    }
+    __syncthreads();
+    unsigned long long at = s_base;
+    for (int w = 0; w < wid; ++w) at += s_w[w];
     if (keep) out[at + __popc(b & ((1u << lane) - 1u))] = o;
 }
 static void pair_dedup(Context& c, const TriKey* in, uint64_t n, TriKey* out, unsigned long long* cnt, DevBuf& tabb) {
