@@ -343,11 +343,21 @@ __global__ void __launch_bounds__(kSelThreads) trikey_select_kernel(const TriKey
             pack(k, hi, lo);
             keep = hi < th || (hi == th && lo <= tl);
         }
+        // one reservation per CTA and step (a returning atomic per warp on one address
+        // serialises in L2: 50k of them at level 0)
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
-        unsigned long long at = 0;
-        if (lane == 0 && bal) at = atomicAdd(cnt, (unsigned long long)__popc(bal));
-        at = __shfl_sync(0xffffffffu, at, 0);
+        if (lane == 0) wsum[wid] = (unsigned)__popc(bal);
+        __syncthreads();
+        if (tid == 0) {
+            unsigned tot = 0;
+            for (int w = 0; w < kSelThreads / 32; ++w) tot += wsum[w];
+            s_krem = tot ? atomicAdd(cnt, (unsigned long long)tot) : 0ull;
+        }
+        __syncthreads();
+        unsigned long long at = s_krem;
+        for (int w = 0; w < wid; ++w) at += wsum[w];
         if (keep) out[at + __popc(bal & ((1u << lane) - 1u))] = k;
+        __syncthreads();  // wsum / s_krem are rewritten next step
     }
     if (blockIdx.x == 0 && tid == 0) {
         // back to (dist, a, b): dd = threshold >> lob; past the keys' span (unresolved
