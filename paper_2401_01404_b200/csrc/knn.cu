@@ -1891,7 +1891,9 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         c.toc(P_KNN);
         // a dense level the first sweep covers entirely is finished from the coverage alone
         if (dense && sorted_valid && cap == kw && n <= (uint64_t)kBitsMaxN && cap >= 32 && p.max_sweeps >= 1 &&
-            (uint64_t)cap * cap >= n - 1 - (uint64_t)kw && !NRG_ENV_ON("NRG_NO_COVER_LEVEL") &&
+            // (worth the size pass only where full coverage is likely: random initial rows give a
+            // node ~cap^2 two-hop paths; at cap^2 ~ 4 n some node still misses a few others)
+            (uint64_t)cap * cap >= 6 * (n - 1 - (uint64_t)kw) && !NRG_ENV_ON("NRG_NO_COVER_LEVEL") &&
             !NRG_ENV_ON("NRG_DENSE_EAGER") &&  // (the survivor lists come from the lazy root's worklist)
             !NRG_ENV_ON("NRG_NO_COVERAGE_SKIP") && !NRG_ENV_ON("NRG_KNN_HASH_GATHER") && !getenv("NRG_KNN_FULL_JOIN") &&
             cover_level(c, d_nodes, n, kw, cap, loc, rootpos, gid, gd, p, out)) {
