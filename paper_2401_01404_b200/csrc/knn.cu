@@ -770,6 +770,24 @@ __global__ void u_new_bits_kernel(const int32_t* __restrict__ adj, const int32_t
         hasnew[i] = 1;
     }
 }
+// u_set_kernel and u_new_bits_kernel in one pass over the U entries
+__global__ void u_bits_kernel(const int32_t* __restrict__ adj, const int32_t* __restrict__ alen, uint64_t n, int cap,
+                              int W, uint32_t* __restrict__ ub, const uint32_t* __restrict__ ubp, int first,
+                              uint8_t* __restrict__ newf, uint32_t* __restrict__ nb, uint8_t* __restrict__ hasnew) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n * (uint64_t)cap) return;
+    const uint64_t i = t / cap;
+    if ((int)(t - i * cap) >= alen[i]) return;
+    const int32_t j = adj[t];
+    const uint32_t bit = 1u << (j & 31);
+    atomicOr(&ub[i * W + (j >> 5)], bit);
+    const bool fresh = first || !(ubp[i * W + (j >> 5)] & bit);
+    newf[t] = fresh ? 1 : 0;
+    if (fresh) {
+        atomicOr(&nb[i * W + (j >> 5)], bit);
+        hasnew[i] = 1;
+    }
+}
 constexpr int kBitsMaxN = 32768;
 template <int NT>
 __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __restrict__ nodes, uint64_t n,
@@ -2080,15 +2098,14 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
             // U bitsets ping-pong between sweeps: last sweep's set answers the new flags
             uint32_t* ubc = (sweep & 1 ? ubitsb2 : ubitsb).as<uint32_t>(n * (uint64_t)Wb);
             uint32_t* ubp = (sweep & 1 ? ubitsb : ubitsb2).as<uint32_t>(n * (uint64_t)Wb);
-            uint32_t* nbits = nbitsb.as<uint32_t>(n * (uint64_t)Wb);
-            uint8_t* hasnew = hasnewb.as<uint8_t>(n);
+            // new-entry bitsets and the has-new flags share one buffer (one clear)
+            uint32_t* nbits = nbitsb.as<uint32_t>(n * (uint64_t)Wb + (n + 3) / 4);
+            uint8_t* hasnew = reinterpret_cast<uint8_t*>(nbits + n * (uint64_t)Wb);
             NRG_CUDA(cudaMemsetAsync(ubc, 0, n * (uint64_t)Wb * 4, c.stream));
-            NRG_CUDA(cudaMemsetAsync(nbits, 0, n * (uint64_t)Wb * 4, c.stream));
-            NRG_CUDA(cudaMemsetAsync(hasnew, 0, n, c.stream));
+            NRG_CUDA(cudaMemsetAsync(nbits, 0, n * (uint64_t)Wb * 4 + n, c.stream));
             const unsigned g = (unsigned)ceil_div(n * (uint64_t)cap, 256);
-            u_set_kernel<<<g, 256, 0, c.stream>>>(adj, alen, n, cap, Wb, ubc);
-            u_new_bits_kernel<<<g, 256, 0, c.stream>>>(adj, alen, n, cap, Wb, ubp,
-                                                      (sweep == 0 || !incremental) ? 1 : 0, newf, nbits, hasnew);
+            u_bits_kernel<<<g, 256, 0, c.stream>>>(adj, alen, n, cap, Wb, ubc, ubp,
+                                                  (sweep == 0 || !incremental) ? 1 : 0, newf, nbits, hasnew);
         } else {
             u_new_kernel<<<(unsigned)ceil_div(n * 32, 256), 256, 0, c.stream>>>(adj, alen, adjp, alenp, n, cap,
                                                                              (sweep == 0 || !incremental) ? 1 : 0,
@@ -2122,7 +2139,9 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                 uint32_t* nbits = static_cast<uint32_t*>(nbitsb.p);
                 knn_gather_bits_kernel<256><<<(unsigned)own, 256, 2 * W * 4 + 4 * cap, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, W, ub, nbits, newf, hv0, sk, capn, cand_id, cand_slot, cand_cnt,
-                    lo, fused, rootpos, static_cast<const uint8_t*>(hasnewb.p), false, LS.off, LS.id, full_cnt);
+                    lo, fused, rootpos,
+                    reinterpret_cast<const uint8_t*>(static_cast<const uint32_t*>(nbitsb.p) + n * (uint64_t)Wb), false,
+                    LS.off, LS.id, full_cnt);
             } else if (big)
                 knn_gather_kernel<256><<<(unsigned)own, 256, tab_bytes, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv0, sk, capn, cand_id,
