@@ -806,7 +806,9 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
                                                              bool count_only = false,
                                                              const unsigned long long* __restrict__ sv_off = nullptr,
                                                              const int32_t* __restrict__ sv_id = nullptr,
-                                                             int32_t* __restrict__ full_cnt = nullptr) {
+                                                             int32_t* __restrict__ full_cnt = nullptr,
+                                                             int cov_full = 0,
+                                                             unsigned long long* __restrict__ cov_short = nullptr) {
     extern __shared__ uint32_t bits_smem[];
     uint32_t* acc = bits_smem;     // OR of the 2-hop rows
     uint32_t* excl = acc + W;      // i's current row and i itself
@@ -979,6 +981,7 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
         if (tid == 0) {
             cand_cnt[li] = s_n;
             full_cnt[li] = total;
+            if (cov_short && total < cov_full) atomicAdd(cov_short, 1ull);  // a node short of full coverage
         }
         return;
     }
@@ -1001,6 +1004,7 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
         if (tid == 0) {
             cand_cnt[li] = total;
             if (full_cnt) full_cnt[li] = total;
+            if (cov_short && total < cov_full) atomicAdd(cov_short, 1ull);
         }
         return;
     }
@@ -1012,6 +1016,7 @@ __global__ void __launch_bounds__(NT) knn_gather_bits_kernel(const int32_t* __re
     if (tid == 0) s_total = total;
     __syncthreads();
     const int ncand = s_total;
+    if (tid == 0 && cov_short && ncand < cov_full) atomicAdd(cov_short, 1ull);
     if (!do_claim) {
         if (tid == 0) cand_cnt[li] = ncand;
         return;
@@ -2141,7 +2146,8 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
                     d_nodes, n, adj, alen, cap, gid, kw, W, ub, nbits, newf, hv0, sk, capn, cand_id, cand_slot, cand_cnt,
                     lo, fused, rootpos,
                     reinterpret_cast<const uint8_t*>(static_cast<const uint32_t*>(nbitsb.p) + n * (uint64_t)Wb), false,
-                    LS.off, LS.id, full_cnt);
+                    LS.off, LS.id, full_cnt, (int)(n - 1 - (uint64_t)kw),
+                    (c.world == 1 && !NRG_ENV_ON("NRG_NO_COVERAGE_SKIP")) ? churn + 1 : nullptr);
             } else if (big)
                 knn_gather_kernel<256><<<(unsigned)own, 256, tab_bytes, c.stream>>>(
                     d_nodes, n, adj, alen, cap, gid, kw, use_bitmap, (int)hash_slots, hv0, sk, capn, cand_id,
@@ -2230,11 +2236,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
         // ends there.  That sweep is recorded (sweeps, churn trace) without being run -- it
         // would only re-probe pairs this sweep already probed (hits, no misses).
         const bool cov_check = bitsmode && c.world == 1 && !NRG_ENV_ON("NRG_NO_COVERAGE_SKIP");
-        if (cov_check && own) {
-            coverage_kernel<<<(unsigned)ceil_div(own, 256), 256, 0, c.stream>>>(
-                (full_cnt ? full_cnt : cand_cnt) + lo, own, (int)(n - 1 - (uint64_t)kw), churn + 1);
-            NRG_LAUNCH_CHECK();
-        }
+        // (the bit-set gather counts the nodes short of full coverage into churn[1] itself)
         unsigned long long* hc = c.hp_small.as<unsigned long long>(4);
         NRG_CUDA(cudaMemcpyAsync(hc, wcount, 32, cudaMemcpyDeviceToHost, c.stream));
         c.sync();
