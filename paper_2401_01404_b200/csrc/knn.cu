@@ -431,10 +431,13 @@ __global__ void answer_kernel(MemoView vals, const uint32_t* __restrict__ slot_o
 // out-part: rows of the (sorted) snapshot; in-part appended while rows have room
 __global__ void u_out_kernel(const int32_t* __restrict__ gid, uint64_t n, int kw, int cap,
                              int32_t* __restrict__ adj, int32_t* __restrict__ alen) {
-    const uint64_t li = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (li >= n) return;
-    for (int t = 0; t < kw; ++t) adj[li * cap + t] = gid[li * kw + t];
-    alen[li] = kw;
+    // one thread per entry (coalesced over the rows)
+    const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * (uint64_t)kw) return;
+    const uint64_t li = e / kw;
+    const int t = (int)(e - li * kw);
+    adj[li * cap + t] = gid[e];
+    if (t == 0) alen[li] = kw;
 }
 __global__ void in_keys_kernel(const int32_t* __restrict__ gid, const double* __restrict__ gd,
                                const int32_t* __restrict__ nodes, uint64_t n, int kw,
@@ -1684,7 +1687,7 @@ static bool cover_level(Context& c, const int32_t* d_nodes, uint64_t n, int kw, 
     int32_t* cand_cnt = cntb.as<int32_t>(n);
     unsigned long long* ch = chb.as<unsigned long long>(2);  // churn, nodes short of full coverage
     c.tic();
-    u_out_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, c.stream>>>(gid, n, kw, cap, adj, alen);
+    u_out_kernel<<<(unsigned)ceil_div(n * (uint64_t)kw, 256), 256, 0, c.stream>>>(gid, n, kw, cap, adj, alen);
     NRG_CUDA(cudaMemsetAsync(ub, 0, n * (uint64_t)Wb * 4, c.stream));
     NRG_CUDA(cudaMemsetAsync(newf, 1, n * cap, c.stream));  // first sweep: every entry is new
     NRG_CUDA(cudaMemsetAsync(hasnew, 1, n, c.stream));
@@ -2070,7 +2073,7 @@ void find_knn(Context& c, int mode, int k, const int32_t* d_nodes, uint64_t n, c
     for (int sweep = 0; sweep < p.max_sweeps; ++sweep) {
         c.tic();
         // U
-        u_out_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, c.stream>>>(gid, n, kw, cap, adj, alen);
+        u_out_kernel<<<(unsigned)ceil_div(n * (uint64_t)kw, 256), 256, 0, c.stream>>>(gid, n, kw, cap, adj, alen);
         NRG_LAUNCH_CHECK();
         if (cap > kw) {
             const uint64_t ne = n * kw;
